@@ -1,0 +1,327 @@
+"""Benchmark: implicit-Euler heat steps (RHS + Jacobi-PCG to tol 1e-10) of the
+tensor B-spline heat problem at paper scale on B200.
+
+Metric (BASELINE.json): CG iteration DoF/s (GDoF/s) -- sum over the timed
+steps of (CG iterations x DoF) / device time, whole job.  One "step" is one
+implicit-Euler time step: b = M u + dt F (fused mass kernel) and the full
+Jacobi-PCG solve with x0 = u_prev.
+
+Default workload (N=1): C3, 930^3 coefficients (928^3 = 0.80 B nodes), p=3,
+lambda = dt/h^2 = 4, fp64, synthetic Gaussian IC/source.
+N>1: the same global grid split in z-slabs, one rank per GPU (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--ncoef 930] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_PASS_A = 24  # read r, p_old; write Ap              (per DoF)
+ALG_BYTES_PASS_B = 56  # read x, r, p_old, Ap; write x, r, p  (per DoF)
+ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port -- the reference is pure Python and
+# does not exist on the GPU box)
+
+
+def cpu_port_rate(ncoef=64, iters=20, repeats=3):
+    """Oracle port of the reference CG path (numpy/scipy Kronecker apply +
+    the reference pcg recurrence) on the C1 heat problem: CG DoF-it/s."""
+    from oracle import bspde_oracle as O
+
+    inp = O.heat_inputs(ncoef)
+    N, h, dt = inp["N"], inp["h"], inp["dt"]
+    A = O.KronOperator((N,) * 3, (h,) * 3, 3, dt, 1.0)
+    b = A.mass_apply(inp["u0"]) + dt * A.mass_apply(inp["q"])
+    O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=2, x0=inp["u0"])  # warm
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        _, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=iters, x0=inp["u0"])
+        times.append(time.perf_counter() - t0)
+    dofs = int(np.prod(A.cext))
+    t = float(np.median(times))
+    return dofs * rep["iterations"] / t, dict(dofs=dofs, iterations=rep["iterations"], seconds=t)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps, warm = max(args.steps, 1), max(args.warmup, 0)
+    vals = []
+    info = None
+    for i in range(warm + steps):
+        v, info = cpu_port_rate(64, iters=10, repeats=1)
+        if i >= warm:
+            vals.append(v)
+    val = float(np.median(vals)) / 1e9
+    sample = (f"C1 sample: 64^3 coefficients, p=3, lambda=4, {info['iterations']} Jacobi-PCG "
+              f"iterations per step (oracle port: scipy CSR 1-D factors, separable Kronecker "
+              f"apply, reference pcg recurrence); full config {args.ncoef}^3 infeasible on CPU")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GDoF/s", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": info["seconds"] * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(args, world),
+        "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "CG iteration DoF/s (GDoF/s) and % HBM roofline at 0.8B nodes, 1/2/4/8 B200"
+
+
+def config_of(args, world):
+    ncoef = args.ncoef
+    return {"workload": f"C3 heat: {ncoef}^3 coefficients ({ncoef - 2}^3 nodes), p=3, "
+                        f"implicit Euler lambda=4, Jacobi-PCG tol 1e-10, z-slabs x{world}",
+            "ncoef": ncoef, "degree": 3, "dofs": ncoef ** 3, "precision": "fp64",
+            "parallelism": f"zslab{world}", "l2": "inputs (6.4 GB/vector) >> 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1904_03057_b200 import SolveConfig, make_operator
+    from paper_1904_03057_b200.domain import Grid
+    from paper_1904_03057_b200.heat import HeatSolver
+    from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
+    from paper_1904_03057_b200.system import heat_system
+
+    if world > 1:
+        raise SystemExit("multi-GPU bench path: see paper_1904_03057_b200.distributed")
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    p = 3
+    N, h, dt = heat_c_inputs(args.ncoef, p)
+    g = Grid((N,) * 3, (h,) * 3)
+    data = heat_system(g, p, dt)
+    op = make_operator(data, "b200", device=local_rank)
+    lay = op.layout
+    u = lay.alloc(dev)
+    q = lay.alloc(dev)
+    gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, **IC)
+    gaussian_coeffs(N, h, p, device=dev, out=q, layout=lay, **SOURCE)
+    F = lay.alloc(dev)
+    op.mass_apply_device(q, F)
+    del q
+    u0 = u.clone()
+    cfg = SolveConfig(tol=1e-10, max_iter=5000, poll_every=args.poll)
+    hs = HeatSolver.from_device(op, dt, u, F, cfg)
+    dofs = int(np.prod(data.cext))
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        hs.step()
+    torch.cuda.synchronize()
+    plan = op.plan()
+    launches0 = plan.launches
+    clk = ClockSampler(local_rank)
+    clk.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    its = []
+    for _ in range(args.steps):
+        its.append(hs.step().iterations)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = plan.launches - launches0
+    total_its = int(sum(its))
+    value = total_its * dofs / (ms * 1e-3) / 1e9
+
+    # -- per-kernel durations (CUDA events on the launching stream) --
+    kt = kernel_times(op, hs, stream)
+    peak, peak_kind = measured_peaks()
+    a_gbs = ALG_BYTES_PASS_A * dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
+    b_gbs = ALG_BYTES_PASS_B * dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
+    dom = "pass_b" if kt["pass_b_ms"] >= kt["pass_a_ms"] else "pass_a"
+    ach = b_gbs if dom == "pass_b" else a_gbs
+    it_gbs = ALG_BYTES_ITER * dofs / ((kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3) / 1e9
+
+    # -- end to end through the host API: u from/to pinned host memory each step --
+    e2e = e2e_rate(hs, u0, lay, dofs, min(args.steps, 3), stream)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        rate, info = cpu_port_rate(64, iters=20, repeats=3)
+        cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
+               "sample": f"C1 64^3 p=3 heat system, {info['iterations']} Jacobi-PCG iterations, "
+                         "median of 3 (oracle port, scipy/numpy single thread)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(args, world),
+        "cg_iterations_per_step": its,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": None, "kernel": dom,
+                     "peak_source": peak_kind,
+                     "alg_bytes_per_dof": ALG_BYTES_PASS_B if dom == "pass_b" else ALG_BYTES_PASS_A,
+                     "pass_a_ms": kt["pass_a_ms"], "pass_b_ms": kt["pass_b_ms"],
+                     "pass_a_gbs": a_gbs, "pass_b_gbs": b_gbs,
+                     "cg_iteration_gbs": it_gbs, "cg_iteration_frac": it_gbs / peak},
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def kernel_times(op, hs, stream, reps=5):
+    """Average device duration of CG pass A and pass B (same stream, events)."""
+    import torch
+
+    from paper_1904_03057_b200.solver import _work
+
+    plan = op.plan()
+    w = _work(op, hs.config.max_iter)
+    hs.rhs()
+    plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
+    plan.cg_residual(hs.b, hs.u, w.r, w.scratch, 1)
+    ta, tb = [], []
+    for _ in range(reps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        plan.cg_pass_a(w.r, w.p, w.ap, w.scratch, 1)
+        e[1].record(stream)
+        plan.cg_pass_b(hs.u, w.r, w.p, w.ap, w.scratch, 1)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        ta.append(e[0].elapsed_time(e[1]))
+        tb.append(e[1].elapsed_time(e[2]))
+    return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:]))}
+
+
+def e2e_rate(hs, u0, lay, dofs, steps, stream):
+    import torch
+
+    host = torch.empty(lay.owned_shape, dtype=torch.float64).pin_memory()
+    host.copy_(lay.owned(u0).cpu())
+    own = lay.owned(hs.u)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    its = 0
+    for _ in range(steps):
+        own.copy_(host, non_blocking=True)
+        its += hs.step().iterations
+        host.copy_(own, non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    nbytes = dofs * 8
+    return {"value": its * dofs / (ms * 1e-3) / 1e9, "unit": "GDoF/s",
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "steps": steps, "api": "HeatSolver.step with u copied from/to pinned host memory"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--ncoef", type=int, default=930)
+    ap.add_argument("--poll", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

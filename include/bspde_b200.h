@@ -1,0 +1,158 @@
+/*
+ * bspde_b200.h -- C ABI of the B200 (sm_100a) tensor B-spline heat/elliptic
+ * solve path.  Plain pointers, sizes and a cudaStream_t passed as void*;
+ * no torch types.  Every entry point returns 0 on success and a nonzero
+ * BSPDE_ERR_* code on failure; bspde_last_error() returns the message of the
+ * calling thread's last failure.
+ *
+ * The reference (arxiv/paper_1904_03057, package `bspde`, pure Python) has
+ * no FFI; these entry points replace the numeric calls of its operator
+ * protocol and solver.  Each declaration names the reference interface it
+ * replaces (paths relative to /root/reference/pkg/src/bspde/).
+ *
+ * Device field layout ("ghosted slab"): a field of the local extended
+ * coefficient grid (nz owned z-planes, ny rows, nx columns; reference array
+ * axes (axis0, axis1, axis2) = (z, y, x), x contiguous) is stored as
+ *     double buf[nz + 2*ghost][ny][pitch_y]     (pitch_z = ny * pitch_y)
+ * with ghost == degree.  Owned plane k lives at buffer plane k + ghost.
+ * Ghost planes hold the neighbouring slab's planes (multi-GPU z-slabs) or
+ * zeros at a physical domain end; they are read, never written, by the
+ * kernels.  pitch_y is even (16-byte rows, a TMA requirement); columns
+ * nx..pitch_y-1 are ignored.  All pointers passed below are the buffer base
+ * (first ghost plane), 16-byte aligned, device memory.
+ */
+#ifndef BSPDE_B200_H
+#define BSPDE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSPDE_OK 0
+#define BSPDE_ERR_ARG 1      /* invalid argument (ValidationError) */
+#define BSPDE_ERR_CUDA 2     /* CUDA runtime / driver failure */
+#define BSPDE_ERR_STATE 3    /* API misuse */
+
+/* CG status codes (bspde_cg_report.status) */
+#define BSPDE_CG_RUNNING 0
+#define BSPDE_CG_CONVERGED 1
+#define BSPDE_CG_MAXITER 2
+#define BSPDE_CG_INDEFINITE 3 /* IndefiniteOperatorError, solver.py:88-92 */
+#define BSPDE_CG_DIVERGED 4   /* DivergenceError, solver.py:105-108 */
+#define BSPDE_CG_ZERO_RHS 5   /* early return, solver.py:63-67 */
+
+typedef struct bspde_plan bspde_plan; /* opaque */
+
+/*
+ * Operator description.  Replaces the data an OnTheFlyOperator reads from
+ * SystemData (assembly.py:342-389) for constant D / mu on a box domain with
+ * Neumann faces:
+ *   A = Mz(x)(My(x)(c_mass Mx + c_stiff[2] Kx) + c_stiff[1] Ky(x)Mx)
+ *       + c_stiff[0] Kz(x)My(x)Mx
+ * with c_mass = vol*mu and c_stiff[a] = vol*D/h_a^2 (assembly.py:426-433).
+ * Per axis a (0=z, 1=y, 2=x) the banded Gram factor is given in class form:
+ * table[c*(2p+1) + k+p] = G[i, i+k] for rows i of class c, classes
+ * 0..ew-1 = first rows, ew = interior (Toeplitz), ew+1..2ew = last rows.
+ * inv_diag_table[(cz*NCy + cy)*NCx + cx] (NCa = 2*ew[a]+1) is the Jacobi
+ * preconditioner 1/diag (1 where diag == 0, solver.py:69-73) per class triple.
+ */
+typedef struct {
+  int32_t device;       /* CUDA device ordinal the plan (and its launches) use */
+  int32_t degree;       /* p in 1..5 */
+  int32_t nz, ny, nx;   /* local extents: owned z planes, rows, columns */
+  int32_t nz_global;    /* global extended z extent */
+  int32_t z_offset;     /* global z index of owned plane 0 */
+  int32_t ew[3];        /* edge rows per axis end (z, y, x) */
+  int64_t pitch_y;      /* elements between rows (even, >= nx) */
+  const double* mass_table[3];  /* host, (2ew+1)*(2p+1) each */
+  const double* stiff_table[3]; /* host, same shape */
+  const double* inv_diag_table; /* host, NCz*NCy*NCx */
+  double c_mass;
+  double c_stiff[3];
+} bspde_plan_desc;
+
+typedef struct {
+  double tol;
+  int32_t max_iter;
+  int32_t record_history;
+  int32_t has_x0;       /* 0: x0 = None (x is zeroed), 1: x holds x0 */
+  int32_t poll_every;   /* iterations per CUDA-graph chunk between host polls (<=0: default 8) */
+} bspde_cg_config;
+
+typedef struct {
+  int32_t iterations;
+  int32_t status;       /* BSPDE_CG_* */
+  double relative_residual;
+  double residual;
+  double residual0;
+  double rhs_norm;
+  double last_pAp;      /* curvature at failure (indefinite) */
+} bspde_cg_report;
+
+/* ---- library ---------------------------------------------------------- */
+const char* bspde_last_error(void);
+int bspde_version(void);
+/* 1 if CUDA device `device` exists and has compute capability 10.x, else 0. */
+int bspde_device_ok(int device);
+
+/* ---- plan: replaces make_operator(data, strategy) (operator.py:407-414) */
+int bspde_plan_create(const bspde_plan_desc* desc, bspde_plan** out);
+int bspde_plan_destroy(bspde_plan* plan);
+/* Bytes of device scratch (CG scalar state, per-CTA partials, counters). */
+int64_t bspde_scratch_bytes(const bspde_plan* plan);
+/* Number of kernel launches issued by this plan since creation. */
+int64_t bspde_launch_count(const bspde_plan* plan);
+
+/* out = A c.  Replaces OnTheFlyOperator.apply (operator.py:217-229). */
+int bspde_apply(bspde_plan* plan, const double* c, double* out, void* stream);
+
+/* out = cm * (Mz(x)My(x)Mx) c + a * f   (f may be NULL).
+ * Replaces assembled_rhs(data, n_s=p, q) * (operator.py:417-441) for a box
+ * with Neumann faces (cm = vol), and the heat RHS  M u_prev + dt F. */
+int bspde_mass_apply(bspde_plan* plan, const double* c, const double* f,
+                     double cm, double a, double* out, void* stream);
+
+/* out = diag(A) on the owned region.
+ * Replaces _OperatorBase.jacobi_diagonal (operator.py:156-171). */
+int bspde_jacobi_diagonal(bspde_plan* plan, const double* diag_table,
+                          double* out, void* stream);
+
+/* Full Jacobi-PCG on one device.  Replaces pcg(operator, rhs, config, x0)
+ * (solver.py:51-117): identical recurrence, stopping rule (recursive
+ * ||r||/||b|| <= tol or max_iter), indefinite and divergence guards.
+ * b, x, r, p, ap are ghosted-slab fields; x holds x0 on entry when
+ * cfg->has_x0, the solution on exit.  scratch: bspde_scratch_bytes bytes.
+ * history: device array of max_iter+1 doubles or NULL. */
+int bspde_pcg_solve(bspde_plan* plan, const double* b, double* x, double* r,
+                    double* p, double* ap, void* scratch, double* history,
+                    const bspde_cg_config* cfg, bspde_cg_report* report,
+                    void* stream);
+
+/* ---- step-wise CG for the multi-GPU driver (z-slabs, one rank per GPU).
+ * fuse = 1: the kernel's last CTA reduces the per-CTA partials and runs the
+ * scalar update (single device).  fuse = 0: it only writes the local sums
+ * (4 doubles at the start of scratch); the caller all-reduces them and calls
+ * bspde_cg_finalize(kind). */
+int bspde_cg_setup(bspde_plan* plan, void* scratch, double* history,
+                   const bspde_cg_config* cfg, void* stream);
+/* r = b - A x (x = x0 or zero), sums = {<b,b>, <r,D^-1 r>, <r,r>}   kind 0 */
+int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
+                      double* r, void* scratch, int fuse, void* stream);
+/* p = D^-1 r + beta p_old on the fly; ap = A p; sums = {<p,Ap>}      kind 1 */
+int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p,
+                    double* ap, void* scratch, int fuse, void* stream);
+/* p = D^-1 r + beta p_old; x += alpha p; r -= alpha Ap;
+ * sums = {<r,D^-1 r>, <r,r>}                                          kind 2 */
+int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, double* p,
+                    const double* ap, void* scratch, int fuse, void* stream);
+int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
+/* Copy the scalar state to the host (synchronizes the stream). */
+int bspde_cg_read_report(bspde_plan* plan, const void* scratch,
+                         bspde_cg_report* report, int32_t* active, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSPDE_B200_H */

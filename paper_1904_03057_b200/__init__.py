@@ -1,0 +1,35 @@
+"""B200-native tensor B-spline heat / elliptic solve path.
+
+Drop-in for the solve path of the reference package ``bspde``
+(arxiv/paper_1904_03057): grid/degree setup, exact separable mass and
+stiffness Gram factors, the matrix-free operator apply, Jacobi-PCG and RHS
+assembly -- with the apply, the CG iteration and the RHS running as
+hand-written sm_100a CUDA kernels (``csrc/bspde_b200.cu``) behind a C ABI
+(``include/bspde_b200.h``).  Adds implicit-Euler heat stepping and z-slab
+multi-GPU sharding.  There is no CPU fallback.
+"""
+
+from .domain import BoxDomain, Grid
+from .errors import (ConditioningWarning, ConfigurationError, DegreeError, DeterminismError,
+                     DivergenceError, IndefiniteOperatorError, NativeLibraryError,
+                     ResourceError, ValidationError)
+from .gram import GramFactor, basis_extension, edge_width, gram_factor, min_axis_length
+from .heat import HeatProblem, HeatSolver, heat_solve
+from .operator import B200Operator, OpStats, assembled_rhs, make_operator
+from .solver import SolveConfig, SolveReport, pcg, pcg_device
+from .system import SystemData, build_system, heat_system, mass_system
+from .transform import direct_transform, sample_solution, transform_field
+
+__all__ = [
+    "BoxDomain", "Grid", "basis_extension", "edge_width", "gram_factor", "min_axis_length",
+    "GramFactor", "SystemData", "build_system", "heat_system", "mass_system",
+    "B200Operator", "OpStats", "make_operator", "assembled_rhs",
+    "SolveConfig", "SolveReport", "pcg", "pcg_device",
+    "HeatProblem", "HeatSolver", "heat_solve",
+    "direct_transform", "transform_field", "sample_solution",
+    "ConditioningWarning", "ConfigurationError", "DegreeError", "DeterminismError",
+    "DivergenceError", "IndefiniteOperatorError", "NativeLibraryError", "ResourceError",
+    "ValidationError",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,139 @@
+"""ctypes binding of the sm_100a C ABI (``include/bspde_b200.h``).
+
+This is the only door to the hot path.  There is no CPU fallback: if the
+library is missing or a call fails, :class:`NativeLibraryError` is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import NativeLibraryError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbspde_b200.so")
+
+BSPDE_CG_RUNNING = 0
+BSPDE_CG_CONVERGED = 1
+BSPDE_CG_MAXITER = 2
+BSPDE_CG_INDEFINITE = 3
+BSPDE_CG_DIVERGED = 4
+BSPDE_CG_ZERO_RHS = 5
+
+_dptr = C.POINTER(C.c_double)
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("degree", C.c_int32),
+        ("nz", C.c_int32), ("ny", C.c_int32), ("nx", C.c_int32),
+        ("nz_global", C.c_int32),
+        ("z_offset", C.c_int32),
+        ("ew", C.c_int32 * 3),
+        ("pitch_y", C.c_int64),
+        ("mass_table", _dptr * 3),
+        ("stiff_table", _dptr * 3),
+        ("inv_diag_table", _dptr),
+        ("c_mass", C.c_double),
+        ("c_stiff", C.c_double * 3),
+    ]
+
+
+class CgConfig(C.Structure):
+    _fields_ = [
+        ("tol", C.c_double),
+        ("max_iter", C.c_int32),
+        ("record_history", C.c_int32),
+        ("has_x0", C.c_int32),
+        ("poll_every", C.c_int32),
+    ]
+
+
+class CgReport(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32),
+        ("status", C.c_int32),
+        ("relative_residual", C.c_double),
+        ("residual", C.c_double),
+        ("residual0", C.c_double),
+        ("rhs_norm", C.c_double),
+        ("last_pAp", C.c_double),
+    ]
+
+
+# (name, restype, argtypes) -- must cover every function in include/bspde_b200.h
+_VP = C.c_void_p
+SIGNATURES = [
+    ("bspde_last_error", C.c_char_p, []),
+    ("bspde_version", C.c_int, []),
+    ("bspde_device_ok", C.c_int, [C.c_int]),
+    ("bspde_plan_create", C.c_int, [C.POINTER(PlanDesc), C.POINTER(_VP)]),
+    ("bspde_plan_destroy", C.c_int, [_VP]),
+    ("bspde_scratch_bytes", C.c_int64, [_VP]),
+    ("bspde_launch_count", C.c_int64, [_VP]),
+    ("bspde_apply", C.c_int, [_VP, _VP, _VP, _VP]),
+    ("bspde_mass_apply", C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP]),
+    ("bspde_jacobi_diagonal", C.c_int, [_VP, _dptr, _VP, _VP]),
+    ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                  C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
+    ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
+    ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_finalize", C.c_int, [_VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_read_report", C.c_int, [_VP, _VP, C.POINTER(CgReport),
+                                       C.POINTER(C.c_int32), _VP]),
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load the native library (once).  Raises NativeLibraryError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeLibraryError(
+                f"native library {path} not built; run "
+                "`python -m paper_1904_03057_b200.build` (no CPU fallback exists)")
+        try:
+            lib = C.CDLL(path)
+        except OSError as e:  # pragma: no cover - environment specific
+            raise NativeLibraryError(f"cannot load {path}: {e}") from e
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = load().bspde_last_error()
+        raise NativeLibraryError(
+            f"bspde native call failed (code {rc}): {msg.decode() if msg else ''}")
+
+
+def call(name, *args):
+    check(getattr(load(), name)(*args))
+
+
+def ptr(t) -> C.c_void_p:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return C.c_void_p(0)
+    return C.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream=None) -> C.c_void_p:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)

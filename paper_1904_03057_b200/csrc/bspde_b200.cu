@@ -1,0 +1,1316 @@
+// bspde_b200.cu -- sm_100a kernels and C ABI for the tensor B-spline
+// (M + dt K) apply, Jacobi-PCG and RHS assembly.  See include/bspde_b200.h
+// and DESIGN.md.
+//
+// Kernel family `sep_kernel<P, MODE>`: a persistent 2.5-D streaming apply of
+//   A = Mz(x)(My(x)(c_mass Mx + cx Kx) + cy Ky(x)Mx) + cz Kz(x)My(x)Mx
+// Work item = (32x32 x-y tile, z-chunk).  Per input z-plane:
+//   1. TMA (cp.async.bulk.tensor.3d) lands the haloed (32+2p)^2 plane tile in
+//      shared memory (out-of-bounds x/y -> zeros; z ghost planes are zeros or
+//      the neighbour slab's planes),
+//   2. [CG pass A] p = D^-1 r + beta p_old is formed in place on the tile,
+//   3. x-pass: u1 = Mx c, u2 = Kx c for all 32+2p rows -> shared memory,
+//   4. y-pass: wm = My u1, wa = My(c_mass u1 + cx u2) + cy Ky u1 in registers,
+//   5. z-pass: scatter wa, wm of this plane into a register ring of 2p+1
+//      partial outputs (the z-Gram factors are symmetric, so the scatter uses
+//      row z' of Mz/Kz); the output plane z'-p is complete and is emitted with
+//      the mode's epilogue (plain store / mass+axpy / residual / CG dot).
+// Edge rows (non-Toeplitz first/last ew rows of each axis) use per-class
+// tables in shared memory on warp/plane-uniform slow paths.
+//
+// Reference algorithm this replaces: stencil_block + _contract_block
+// (/root/reference/pkg/src/bspde/assembly.py:460-472, operator.py:77-89,
+// operator.py:217-229) and the pcg loop (solver.py:51-117).
+
+#include "../../include/bspde_b200.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// configuration
+
+constexpr int TX = 32;               // tile width (x), one lane per column
+constexpr int TY = 32;               // tile height (y)
+constexpr int NT = 256;              // threads per CTA
+constexpr int NW = NT / 32;          // warps
+constexpr int RPT = TY / NW;         // output rows per thread (4)
+constexpr int MAXP = 5;
+constexpr int MAXTAP = 2 * MAXP + 1;
+
+enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
+
+__host__ __device__ constexpr int edge_width_of(int p) {
+  return p == 1 ? 1 : (p <= 3 ? 3 : 5);
+}
+
+template <int P, int MODE>
+struct Cfg {
+  static constexpr int R = 2 * P + 1;
+  static constexpr int HX = TX + 2 * P;
+  static constexpr int HY = TY + 2 * P;
+  static constexpr int EW = edge_width_of(P);
+  static constexpr int NC = 2 * EW + 1;          // max classes per axis
+  static constexpr int NA = (MODE == M_CGA) ? 2 : 1;   // staged arrays per plane
+  static constexpr int NS = (MODE == M_CGA) ? (P <= 3 ? 3 : 2) : (P <= 3 ? 4 : 3);
+  static constexpr int NXB = (MODE == M_CGA) ? 1 : 2;  // X buffers
+  static constexpr bool STIFF = (MODE != M_MASS);
+  static constexpr bool INVD = (MODE == M_CGA || MODE == M_RESID);
+  static constexpr int ARR = HX * HY;                        // doubles
+  static constexpr int ARR_D = ((ARR * 8 + 127) / 128) * 16; // doubles, 128B-rounded
+  static constexpr int XARR = HY * TX;                       // doubles per X array
+  static constexpr int TAB = 6 * NC * R;                     // doubles
+  static constexpr int INV = INVD ? NC * NC * NC : 0;
+  static constexpr size_t smem_bytes() {
+    return (size_t)8 * (NS * NA * ARR_D + NXB * 2 * XARR + TAB + INV + NW * 4) + 8 * NS + 128;
+  }
+};
+
+struct CgState {
+  double sums[4];        // local partial sums (all-reduced across ranks for N>1)
+  double rz, alpha, beta, pAp;
+  double res, res0, scale, tol;
+  double rhs_norm, pad_d;
+  int it, max_iter, active, status;
+  int record_history, has_x0, pad_i0, pad_i1;
+  double* history;
+};
+
+struct SepParams {
+  int nx, ny, nz, nz_glob, z_off, ghost;
+  long long pitch_y, pitch_z;
+  int ew[3];
+  int tiles_x, tiles_y, nchunks, chunk_len, nitems;
+  double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
+  double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
+  const double* tab;             // device: [axis][kind][NC*R] (NC = class stride)
+  const double* invd;            // device: NCz*NCy*NCx
+  double* out;
+  const double* aux;
+  double aux_scale;
+  double* partials;
+  unsigned* counter;
+  CgState* state;
+  int fuse;
+};
+
+struct PassBParams {
+  int nx, ny, nz, nz_glob, z_off, ghost;
+  long long pitch_y, pitch_z;
+  int ew[3];
+  int rows_per_cta;
+  const double* invd;
+  double* x;
+  double* r;
+  double* p;
+  const double* ap;
+  double* partials;
+  unsigned* counter;
+  CgState* state;
+  int fuse;
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, phase)) {
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ int cls_of(int g, int n, int ew) {
+  return g < ew ? g : (g >= n - ew ? 2 * ew - (n - 1 - g) : ew);
+}
+
+// The CG search direction, bitwise identical in pass A and pass B.
+__device__ __forceinline__ double pdir(double r, double invd, double pold, double beta) {
+  return __fma_rn(beta, pold, __dmul_rn(invd, r));
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_vol(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
+
+// ---------------------------------------------------------------------------
+// scalar state machine (device).  Mirrors solver.py:63-108 step by step.
+
+__device__ void update_active(CgState* s) {
+  if (!(s->res / s->scale > s->tol)) {
+    s->status = BSPDE_CG_CONVERGED;
+    s->active = 0;
+  } else if (s->it >= s->max_iter) {
+    s->status = BSPDE_CG_MAXITER;
+    s->active = 0;
+  } else {
+    s->status = BSPDE_CG_RUNNING;
+    s->active = 1;
+  }
+}
+
+// kind 0: after r = b - A x0           (solver.py:63-83)
+// kind 1: after Ap, <p,Ap>              (solver.py:88-93)
+// kind 2: after x, r updates, <r,z>     (solver.py:96-108)
+__device__ void finalize_state(CgState* s, int kind) {
+  if (kind == 0) {
+    const double bb = s->sums[0], rz = s->sums[1], rr = s->sums[2];
+    s->rhs_norm = sqrt(bb);
+    s->it = 0;
+    s->beta = 0.0;
+    if (s->rhs_norm == 0.0 && !s->has_x0) {
+      s->status = BSPDE_CG_ZERO_RHS;
+      s->active = 0;
+      s->res = 0.0;
+      s->res0 = 0.0;
+      s->scale = 1.0;
+      s->rz = 0.0;
+      if (s->record_history) s->history[0] = 0.0;
+      return;
+    }
+    s->scale = s->rhs_norm > 0.0 ? s->rhs_norm : 1.0;
+    s->rz = rz;
+    s->res = sqrt(rr);
+    s->res0 = s->res;
+    if (s->record_history) s->history[0] = sqrt(fmax(rz, 0.0));
+    update_active(s);
+  } else if (kind == 1) {
+    const double pAp = s->sums[0];
+    s->pAp = pAp;
+    if (pAp <= 0.0) {
+      s->status = BSPDE_CG_INDEFINITE;
+      s->active = 0;
+      return;
+    }
+    s->alpha = s->rz / pAp;
+  } else {
+    const double rz_new = s->sums[0], rr = s->sums[1];
+    s->beta = rz_new / s->rz;
+    s->rz = rz_new;
+    s->res = sqrt(rr);
+    s->it += 1;
+    if (s->record_history) s->history[s->it] = sqrt(fmax(rz_new, 0.0));
+    if (s->res > 1e3 * s->res0) {
+      s->status = BSPDE_CG_DIVERGED;
+      s->active = 0;
+      return;
+    }
+    update_active(s);
+  }
+}
+
+__global__ void finalize_kernel(CgState* s, int kind) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (kind != 0 && !s->active) return;
+    finalize_state(s, kind);
+  }
+}
+
+// Deterministic block reduction of NV values, per-CTA partials, then the
+// last CTA to finish reduces the partials in fixed order (and optionally runs
+// the scalar update).  s_red must hold NWARP*4 doubles.
+template <int NV, int NWARP>
+__device__ void reduce_and_finalize(double (&v)[NV], double* s_red, double* partials,
+                                    unsigned* counter, CgState* st, int fuse, int kind) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s_red[warp * 4 + i] = v[i];
+  }
+  __syncthreads();
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double acc = 0.0;
+      for (int w = 0; w < NWARP; ++w) acc += s_red[w * 4 + i];
+      partials[blockIdx.x * 4 + i] = acc;
+    }
+    __threadfence();
+    const unsigned ticket = atomicAdd(counter, 1u);
+    s_last = (ticket == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last && warp == 0) {
+    __threadfence();
+    double tot[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tot[i] = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) tot[i] += ld_vol(&partials[b * 4 + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) tot[i] += __shfl_xor_sync(0xffffffffu, tot[i], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) st->sums[i] = tot[i];
+      if (fuse) finalize_state(st, kind);
+      *counter = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the separable streaming kernel
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
+    sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
+               const __grid_constant__ CUtensorMap tm1) {
+  using C = Cfg<P, MODE>;
+  constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
+  constexpr bool STIFF = C::STIFF;
+
+  if (MODE == M_CGA) {
+    if (!ld_vol(&prm.state->active)) return;
+  }
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* s_stage = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double* s_X = s_stage + NS * NA * C::ARR_D;
+  double* s_tab = s_X + C::NXB * 2 * C::XARR;
+  double* s_invd = s_tab + C::TAB;
+  double* s_red = s_invd + C::INV;
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nx = prm.nx, ny = prm.ny, nz = prm.nz;
+  const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1, ncz = 2 * ewz + 1;
+
+  for (int i = tid; i < C::TAB; i += NT) s_tab[i] = prm.tab[i];
+  if (C::INVD) {
+    const int n = ncz * ncy * ncx;
+    for (int i = tid; i < n; i += NT) s_invd[i] = prm.invd[i];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&s_bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // table accessors: axis a (0=z,1=y,2=x), kind 0=mass 1=stiff
+  auto tabv = [&](int a, int kind, int c, int k) -> double {
+    return s_tab[((a * 2 + kind) * NC + c) * R + k];
+  };
+
+  const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
+  const int G = gridDim.x;
+  const int tiles_xy = prm.tiles_x * prm.tiles_y;
+
+  // ---- producer cursor (thread 0 only) ----
+  int pf_item = blockIdx.x, pf_j = 0;
+  uint32_t pf_flat = 0;
+  auto item_geom = [&](int item, int& x0, int& y0, int& zc0, int& zc1) {
+    const int t = item % tiles_xy;
+    const int ch = item / tiles_xy;
+    x0 = (t % prm.tiles_x) * TX;
+    y0 = (t / prm.tiles_x) * TY;
+    zc0 = ch * prm.chunk_len;
+    zc1 = min(zc0 + prm.chunk_len, nz);
+  };
+  auto issue_next = [&]() {
+    if (pf_item >= prm.nitems) return;
+    int x0, y0, zc0, zc1;
+    item_geom(pf_item, x0, y0, zc0, zc1);
+    const int nin = zc1 - zc0 + 2 * P;
+    const int s = pf_flat % NS;
+    uint64_t* bar = &s_bar[s];
+    const int zb = zc0 - P + pf_j + prm.ghost;  // buffer plane
+    mbar_expect_tx(bar, NA * HX * HY * 8);
+    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, &tm0, x0 - P, y0 - P, zb, bar);
+    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, &tm1, x0 - P, y0 - P, zb, bar);
+    ++pf_flat;
+    if (++pf_j == nin) {
+      pf_j = 0;
+      pf_item += G;
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) issue_next();
+  }
+
+  double dsum[3] = {0.0, 0.0, 0.0};
+  uint32_t flat = 0;
+
+  for (int item = blockIdx.x; item < prm.nitems; item += G) {
+    int x0, y0, zc0, zc1;
+    item_geom(item, x0, y0, zc0, zc1);
+    const int nin = zc1 - zc0 + 2 * P;
+    // tile interior flags (uniform per item)
+    const bool fast_x_tile = (x0 - P >= ewx) && (x0 + TX + P - 1 < nx - ewx);
+    const bool fast_y_tile = (y0 - P >= ewy) && (y0 + TY + P - 1 < ny - ewy);
+    const int gy0 = y0 + warp * RPT;  // this warp's first output row
+    const bool fast_y_warp = (gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy);
+
+    double acc[R][RPT];
+    double pr[R][RPT];
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        acc[s][i] = 0.0;
+        pr[s][i] = 0.0;
+      }
+
+    for (int jb = 0; jb < nin; jb += R) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int j = jb + u;
+        if (j < nin) {
+          const int zl = zc0 - P + j;
+          const int zg = prm.z_off + zl;
+          const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
+          const int s = flat % NS;
+          mbar_wait(&s_bar[s], (flat / NS) & 1);
+          double* stC = s_stage + (s * NA + 0) * C::ARR_D;
+          double* stP = s_stage + (s * NA + (NA - 1)) * C::ARR_D;
+          double* X1 = s_X + (C::NXB == 2 ? (flat & 1) : 0) * 2 * C::XARR;
+          double* X2 = X1 + C::XARR;
+          const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
+
+          if (MODE == M_CGA) {
+            // ---- p = D^-1 r + beta p_old on the whole haloed tile ----
+            if (in_grid) {
+              const bool fast = fast_x_tile && fast_y_tile && (cz == ewz);
+              const double inv0 = s_invd[(cz * ncy + ewy) * ncx + ewx];
+              for (int e2 = tid; e2 < C::ARR / 2; e2 += NT) {
+                const int e = 2 * e2;
+                const double2 rv = *reinterpret_cast<const double2*>(stC + e);
+                const double2 qv = *reinterpret_cast<const double2*>(stP + e);
+                double i0 = inv0, i1 = inv0;
+                if (!fast) {
+                  const int row = e / HX, col = e - row * HX;
+                  const int gy = y0 - P + row, gx = x0 - P + col;
+                  const bool oky = (gy >= 0) && (gy < ny);
+                  if (oky) {
+                    const int cy = cls_of(gy, ny, ewy);
+                    const double* trow = s_invd + (cz * ncy + cy) * ncx;
+                    i0 = (gx >= 0 && gx < nx) ? trow[cls_of(gx, nx, ewx)] : 0.0;
+                    i1 = (gx + 1 >= 0 && gx + 1 < nx) ? trow[cls_of(gx + 1, nx, ewx)] : 0.0;
+                  } else {
+                    i0 = 0.0;
+                    i1 = 0.0;
+                  }
+                }
+                double2 pv;
+                pv.x = pdir(rv.x, i0, qv.x, beta);
+                pv.y = pdir(rv.y, i1, qv.y, beta);
+                *reinterpret_cast<double2*>(stP + e) = pv;
+              }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+              pr[u][i] = stP[(warp * RPT + i + P) * HX + lane + P];
+          }
+
+          // ---- x-pass: rows 0..HY-1, column pairs ----
+          if (in_grid) {
+            const double* src = stP;  // NA==1: stP == stC
+            for (int it = tid; it < HY * (TX / 2); it += NT) {
+              const int row = it >> 4;
+              const int q = it & 15;
+              const double* w = src + row * HX + 2 * q;
+              double win[2 * P + 2];
+#pragma unroll
+              for (int k = 0; k < P + 1; ++k) {
+                const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
+                win[2 * k] = t.x;
+                win[2 * k + 1] = t.y;
+              }
+              const int gx0 = x0 + 2 * q;
+              double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+              if (fast_x_tile || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
+#pragma unroll
+                for (int k = 0; k < 2 * P + 1; ++k) {
+                  m0 = fma(prm.txm[k], win[k], m0);
+                  m1 = fma(prm.txm[k], win[k + 1], m1);
+                  if (STIFF) {
+                    k0 = fma(prm.txk[k], win[k], k0);
+                    k1 = fma(prm.txk[k], win[k + 1], k1);
+                  }
+                }
+              } else {
+                const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
+                const int c1 = (gx0 + 1 < nx) ? cls_of(gx0 + 1, nx, ewx) : ewx;
+#pragma unroll
+                for (int k = 0; k < 2 * P + 1; ++k) {
+                  m0 = fma(tabv(2, 0, c0, k), win[k], m0);
+                  m1 = fma(tabv(2, 0, c1, k), win[k + 1], m1);
+                  if (STIFF) {
+                    k0 = fma(tabv(2, 1, c0, k), win[k], k0);
+                    k1 = fma(tabv(2, 1, c1, k), win[k + 1], k1);
+                  }
+                }
+              }
+              *reinterpret_cast<double2*>(X1 + row * TX + 2 * q) = make_double2(m0, m1);
+              if (STIFF) *reinterpret_cast<double2*>(X2 + row * TX + 2 * q) = make_double2(k0, k1);
+            }
+          }
+          __syncthreads();
+          if (tid == 0) {
+            fence_proxy_async();
+            issue_next();
+          }
+
+          if (in_grid) {
+            // ---- y-pass (register scatter over the 2p+RPT input rows) ----
+            double wm[RPT], wa[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              wm[i] = 0.0;
+              wa[i] = 0.0;
+            }
+            const double* x1c = X1 + (warp * RPT) * TX + lane;
+            const double* x2c = X2 + (warp * RPT) * TX + lane;
+            if (fast_y_warp) {
+#pragma unroll
+              for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+                const double a1 = x1c[rr * TX];
+                double t = 0.0;
+                if (STIFF) t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                  const int k = rr - i;
+                  if (k >= 0 && k <= 2 * P) {
+                    wm[i] = fma(prm.tym[k], a1, wm[i]);
+                    if (STIFF) {
+                      wa[i] = fma(prm.tym[k], t, wa[i]);
+                      wa[i] = fma(prm.tyk[k], a1, wa[i]);  // tyk pre-scaled by cy
+                    }
+                  }
+                }
+              }
+            } else {
+              int cyr[RPT];
+#pragma unroll
+              for (int i = 0; i < RPT; ++i) {
+                const int gy = gy0 + i;
+                cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
+              }
+#pragma unroll
+              for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+                const double a1 = x1c[rr * TX];
+                double t = 0.0;
+                if (STIFF) t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                  const int k = rr - i;
+                  if (k >= 0 && k <= 2 * P) {
+                    const double my = tabv(1, 0, cyr[i], k);
+                    wm[i] = fma(my, a1, wm[i]);
+                    if (STIFF) {
+                      wa[i] = fma(my, t, wa[i]);
+                      wa[i] = fma(prm.cy * tabv(1, 1, cyr[i], k), a1, wa[i]);
+                    }
+                  }
+                }
+              }
+            }
+
+            // ---- z-pass: scatter into the ring (row z' of symmetric Mz/Kz) ----
+            if (cz == ewz) {
+#pragma unroll
+              for (int k = 0; k < R; ++k) {
+                const int slot = (u + k) % R;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                  if (STIFF) {
+                    acc[slot][i] = fma(prm.tzm[k], wa[i], acc[slot][i]);
+                    acc[slot][i] = fma(prm.tzk[k], wm[i], acc[slot][i]);
+                  } else {
+                    acc[slot][i] = fma(prm.tzm[k], wm[i], acc[slot][i]);
+                  }
+                }
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < R; ++k) {
+                const int slot = (u + k) % R;
+                const double cm = tabv(0, 0, cz, k);
+                const double ck = prm.cz * tabv(0, 1, cz, k);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                  if (STIFF) {
+                    acc[slot][i] = fma(cm, wa[i], acc[slot][i]);
+                    acc[slot][i] = fma(ck, wm[i], acc[slot][i]);
+                  } else {
+                    acc[slot][i] = fma(cm, wm[i], acc[slot][i]);
+                  }
+                }
+              }
+            }
+          }
+
+          // ---- emit output plane zo = zl - P (complete) ----
+          if (j >= 2 * P) {
+            const int zo = zl - P;
+            const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z;
+            const int x = x0 + lane;
+            int czo = 0;
+            if (MODE == M_RESID) czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              const int y = gy0 + i;
+              const double v = acc[u][i];
+              if (y < ny && x < nx) {
+                const long long off = pbase + (long long)y * prm.pitch_y + x;
+                if (MODE == M_APPLY || MODE == M_CGA) {
+                  prm.out[off] = v;
+                  if (MODE == M_CGA) dsum[0] = fma(pr[(u + P + 1) % R][i], v, dsum[0]);
+                } else if (MODE == M_MASS) {
+                  double o = prm.c_mass * v;
+                  if (prm.aux) o = fma(prm.aux_scale, prm.aux[off], o);
+                  prm.out[off] = o;
+                } else {  // M_RESID
+                  const double b = prm.aux[off];
+                  const double r = b - v;
+                  prm.out[off] = r;
+                  const double inv =
+                      s_invd[(czo * ncy + cls_of(y, ny, ewy)) * ncx + cls_of(x, nx, ewx)];
+                  dsum[0] = fma(b, b, dsum[0]);
+                  dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
+                  dsum[2] = fma(r, r, dsum[2]);
+                }
+              }
+              acc[u][i] = 0.0;
+            }
+          }
+          ++flat;
+        }
+      }
+    }
+  }
+
+  if (MODE == M_CGA) {
+    double v[1] = {dsum[0]};
+    reduce_and_finalize<1, NW>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 1);
+  } else if (MODE == M_RESID) {
+    double v[3] = {dsum[0], dsum[1], dsum[2]};
+    reduce_and_finalize<3, NW>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CG pass B: streaming x/r/p update + <r, D^-1 r>, <r, r>
+
+constexpr int NTB = 256;
+
+__global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ PassBParams prm) {
+  if (!ld_vol(&prm.state->active)) return;
+  __shared__ double s_red[(NTB / 32) * 4];
+  extern __shared__ double s_inv[];
+  const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1, ncz = 2 * ewz + 1;
+  for (int i = threadIdx.x; i < ncz * ncy * ncx; i += NTB) s_inv[i] = prm.invd[i];
+  __syncthreads();
+  const double alpha = ld_vol(&prm.state->alpha);
+  const double beta = ld_vol(&prm.state->beta);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nx = prm.nx, ny = prm.ny;
+  const int nrows = prm.nz * ny;
+  const int r0 = blockIdx.x * prm.rows_per_cta;
+  const int r1 = min(r0 + prm.rows_per_cta, nrows);
+  double rz = 0.0, rr = 0.0;
+  const bool even = ((prm.pitch_y & 1) == 0);
+  for (int row = r0 + warp; row < r1; row += NTB / 32) {
+    const int zl = row / ny, y = row - zl * ny;
+    const int cz = cls_of(prm.z_off + zl, prm.nz_glob, ewz);
+    const int cy = cls_of(y, ny, ewy);
+    const double* trow = s_inv + (cz * ncy + cy) * ncx;
+    const double inv_int = trow[ewx];
+    const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
+    double* xr = prm.x + base;
+    double* rrw = prm.r + base;
+    double* pr = prm.p + base;
+    const double* apr = prm.ap + base;
+    if (even) {
+      const int npair = nx >> 1;
+      for (int q = lane; q < npair; q += 32) {
+        const int xx = 2 * q;
+        const double2 xv = *reinterpret_cast<const double2*>(xr + xx);
+        const double2 rv = *reinterpret_cast<const double2*>(rrw + xx);
+        const double2 pv = *reinterpret_cast<const double2*>(pr + xx);
+        const double2 av = *reinterpret_cast<const double2*>(apr + xx);
+        const double i0 = (xx >= ewx && xx < nx - ewx) ? inv_int : trow[cls_of(xx, nx, ewx)];
+        const double i1 =
+            (xx + 1 >= ewx && xx + 1 < nx - ewx) ? inv_int : trow[cls_of(xx + 1, nx, ewx)];
+        double2 pn, xn, rn;
+        pn.x = pdir(rv.x, i0, pv.x, beta);
+        pn.y = pdir(rv.y, i1, pv.y, beta);
+        xn.x = fma(alpha, pn.x, xv.x);
+        xn.y = fma(alpha, pn.y, xv.y);
+        rn.x = fma(-alpha, av.x, rv.x);
+        rn.y = fma(-alpha, av.y, rv.y);
+        rz = fma(rn.x, __dmul_rn(i0, rn.x), rz);
+        rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
+        rr = fma(rn.x, rn.x, rr);
+        rr = fma(rn.y, rn.y, rr);
+        *reinterpret_cast<double2*>(xr + xx) = xn;
+        *reinterpret_cast<double2*>(rrw + xx) = rn;
+        *reinterpret_cast<double2*>(pr + xx) = pn;
+      }
+      if ((nx & 1) && lane == 0) {
+        const int xx = nx - 1;
+        const double i0 = trow[cls_of(xx, nx, ewx)];
+        const double pn = pdir(rrw[xx], i0, pr[xx], beta);
+        const double rn = fma(-alpha, apr[xx], rrw[xx]);
+        xr[xx] = fma(alpha, pn, xr[xx]);
+        rrw[xx] = rn;
+        pr[xx] = pn;
+        rz = fma(rn, __dmul_rn(i0, rn), rz);
+        rr = fma(rn, rn, rr);
+      }
+    } else {
+      for (int xx = lane; xx < nx; xx += 32) {
+        const double i0 = trow[cls_of(xx, nx, ewx)];
+        const double pn = pdir(rrw[xx], i0, pr[xx], beta);
+        const double rn = fma(-alpha, apr[xx], rrw[xx]);
+        xr[xx] = fma(alpha, pn, xr[xx]);
+        rrw[xx] = rn;
+        pr[xx] = pn;
+        rz = fma(rn, __dmul_rn(i0, rn), rz);
+        rr = fma(rn, rn, rr);
+      }
+    }
+  }
+  double v[2] = {rz, rr};
+  reduce_and_finalize<2, NTB / 32>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 2);
+}
+
+// out = diag(A) expanded from the class table
+__global__ void diag_kernel(const double* __restrict__ tab, int nx, int ny, int nz, int nz_glob,
+                            int z_off, int ghost, long long pitch_y, long long pitch_z, int ewz,
+                            int ewy, int ewx, double* __restrict__ out) {
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
+  const long long total = (long long)nz * ny * nx;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx);
+    const long long t = i / nx;
+    const int y = (int)(t % ny);
+    const int zl = (int)(t / ny);
+    const int cz = cls_of(z_off + zl, nz_glob, ewz);
+    out[(long long)(zl + ghost) * pitch_z + (long long)y * pitch_y + x] =
+        tab[(cz * ncy + cls_of(y, ny, ewy)) * ncx + cls_of(x, nx, ewx)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(BSPDE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+struct KernelInfo {
+  const void* fn;
+  size_t smem;
+  int ctas_per_sm;
+};
+
+struct Launch {
+  int grid;
+  int nchunks, chunk_len, nitems;
+};
+
+}  // namespace
+
+struct bspde_plan {
+  bspde_plan_desc d;
+  int device = 0;
+  int p;
+  int NC;  // class stride of the device table (edge_width_of(p)*2+1)
+  int num_sms;
+  long long pitch_z;
+  double* d_tab = nullptr;   // [3][2][NC*R]
+  double* d_invd = nullptr;  // NCz*NCy*NCx
+  int64_t launches = 0;
+  // CUDA graph cache for the CG loop
+  struct GraphKey {
+    const void *x, *r, *p, *ap, *scratch;
+    int k;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(x, r, p, ap, scratch, k) < std::tie(o.x, o.r, o.p, o.ap, o.scratch, o.k);
+    }
+  };
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  void* host_state = nullptr;  // pinned CgState staging
+  std::vector<double> host_tab;  // [axis][kind][NC][R]
+};
+
+namespace {
+
+template <int P, int MODE>
+KernelInfo kernel_info() {
+  using C = Cfg<P, MODE>;
+  KernelInfo ki;
+  ki.fn = reinterpret_cast<const void*>(&sep_kernel<P, MODE>);
+  ki.smem = C::smem_bytes();
+  static int ctas = -1;
+  if (ctas < 0) {
+    cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ki.smem);
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ki.fn, NT, ki.smem);
+    ctas = std::max(n, 1);
+  }
+  ki.ctas_per_sm = ctas;
+  return ki;
+}
+
+template <int MODE>
+KernelInfo kernel_info_p(int p) {
+  switch (p) {
+    case 1: return kernel_info<1, MODE>();
+    case 2: return kernel_info<2, MODE>();
+    case 3: return kernel_info<3, MODE>();
+    case 4: return kernel_info<4, MODE>();
+    default: return kernel_info<5, MODE>();
+  }
+}
+
+KernelInfo kernel_for(int p, int mode) {
+  switch (mode) {
+    case M_APPLY: return kernel_info_p<M_APPLY>(p);
+    case M_MASS: return kernel_info_p<M_MASS>(p);
+    case M_RESID: return kernel_info_p<M_RESID>(p);
+    default: return kernel_info_p<M_CGA>(p);
+  }
+}
+
+// choose z-chunking so that items balance over the persistent grid
+Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
+  const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
+  const int tiles = tx * ty;
+  const int slots = std::max(1, pl->num_sms * ki.ctas_per_sm);
+  const int nz = pl->d.nz;
+  Launch best{1, 1, nz, tiles};
+  double best_cost = 1e300;
+  for (int nc = 1; nc <= nz; ++nc) {
+    const int len = (nz + nc - 1) / nc;
+    const int ncr = (nz + len - 1) / len;
+    const long long items = (long long)tiles * ncr;
+    const int grid = (int)std::min<long long>(items, slots);
+    const long long per = (items + grid - 1) / grid;
+    // time model: planes streamed by the busiest CTA (halo planes included)
+    const double cost = (double)per * (len + 2 * pl->p);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = Launch{grid, ncr, len, (int)items};
+    }
+    if (len <= 4 * pl->p) break;
+  }
+  return best;
+}
+
+int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int p = pl->p;
+  cuuint64_t dims[3] = {(cuuint64_t)pl->d.nx, (cuuint64_t)pl->d.ny,
+                        (cuuint64_t)(pl->d.nz + 2 * p)};
+  cuuint64_t strides[2] = {(cuuint64_t)(pl->d.pitch_y * 8), (cuuint64_t)(pl->pitch_z * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * p), (cuuint32_t)(TY + 2 * p), 1u};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" +
+                                                          std::to_string((int)rc) + ")");
+  return BSPDE_OK;
+}
+
+void fill_common(SepParams& sp, const bspde_plan* pl) {
+  const auto& d = pl->d;
+  const int p = pl->p, R = 2 * p + 1;
+  sp.nx = d.nx;
+  sp.ny = d.ny;
+  sp.nz = d.nz;
+  sp.nz_glob = d.nz_global;
+  sp.z_off = d.z_offset;
+  sp.ghost = p;
+  sp.pitch_y = d.pitch_y;
+  sp.pitch_z = pl->pitch_z;
+  for (int a = 0; a < 3; ++a) sp.ew[a] = d.ew[a];
+  sp.tiles_x = (d.nx + TX - 1) / TX;
+  sp.tiles_y = (d.ny + TY - 1) / TY;
+  for (int k = 0; k < MAXTAP; ++k) {
+    sp.tzm[k] = sp.tzk[k] = sp.tym[k] = sp.tyk[k] = sp.txm[k] = sp.txk[k] = 0.0;
+  }
+  for (int k = 0; k < R; ++k) {
+    sp.tzm[k] = d.mass_table[0][d.ew[0] * R + k];
+    sp.tzk[k] = d.c_stiff[0] * d.stiff_table[0][d.ew[0] * R + k];
+    sp.tym[k] = d.mass_table[1][d.ew[1] * R + k];
+    sp.tyk[k] = d.c_stiff[1] * d.stiff_table[1][d.ew[1] * R + k];
+    sp.txm[k] = d.mass_table[2][d.ew[2] * R + k];
+    sp.txk[k] = d.stiff_table[2][d.ew[2] * R + k];
+  }
+  sp.c_mass = d.c_mass;
+  sp.cx = d.c_stiff[2];
+  sp.cy = d.c_stiff[1];
+  sp.cz = d.c_stiff[0];
+  sp.tab = pl->d_tab;
+  sp.invd = pl->d_invd;
+  sp.out = nullptr;
+  sp.aux = nullptr;
+  sp.aux_scale = 0.0;
+  sp.partials = nullptr;
+  sp.counter = nullptr;
+  sp.state = nullptr;
+  sp.fuse = 1;
+}
+
+// scratch layout: CgState | partials[4*MAXGRID] | counter
+constexpr int MAXGRID = 4096;
+size_t scratch_size() { return sizeof(CgState) + sizeof(double) * 4 * MAXGRID + 64; }
+CgState* scratch_state(void* s) { return reinterpret_cast<CgState*>(s); }
+double* scratch_partials(void* s) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + sizeof(CgState));
+}
+unsigned* scratch_counter(void* s) {
+  return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(s) + sizeof(CgState) +
+                                     sizeof(double) * 4 * MAXGRID);
+}
+
+int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, double* out,
+               const double* aux, double aux_scale, double c_mass_override, bool use_override,
+               void* scratch, int fuse, cudaStream_t st) {
+  KernelInfo ki = kernel_for(pl->p, mode);
+  Launch ln = plan_launch(pl, ki);
+  SepParams sp;
+  fill_common(sp, pl);
+  sp.nchunks = ln.nchunks;
+  sp.chunk_len = ln.chunk_len;
+  sp.nitems = ln.nitems;
+  sp.out = out;
+  sp.aux = aux;
+  sp.aux_scale = aux_scale;
+  if (use_override) sp.c_mass = c_mass_override;
+  if (scratch) {
+    sp.state = scratch_state(scratch);
+    sp.partials = scratch_partials(scratch);
+    sp.counter = scratch_counter(scratch);
+  }
+  sp.fuse = fuse;
+  if (ln.grid > MAXGRID) return fail(BSPDE_ERR_STATE, "grid exceeds MAXGRID");
+  CUtensorMap m0, m1;
+  int rc = make_map(&m0, pl, in0);
+  if (rc) return rc;
+  if (in1) {
+    rc = make_map(&m1, pl, in1);
+    if (rc) return rc;
+  } else {
+    m1 = m0;
+  }
+  void* args[3] = {&sp, &m0, &m1};
+  CUDA_TRY(cudaLaunchKernel(ki.fn, dim3(ln.grid), dim3(NT), args, ki.smem, st));
+  pl->launches++;
+  return BSPDE_OK;
+}
+
+int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double* ap,
+                  void* scratch, int fuse, cudaStream_t st) {
+  PassBParams bp;
+  const auto& d = pl->d;
+  bp.nx = d.nx;
+  bp.ny = d.ny;
+  bp.nz = d.nz;
+  bp.nz_glob = d.nz_global;
+  bp.z_off = d.z_offset;
+  bp.ghost = pl->p;
+  bp.pitch_y = d.pitch_y;
+  bp.pitch_z = pl->pitch_z;
+  for (int a = 0; a < 3; ++a) bp.ew[a] = d.ew[a];
+  const int nrows = d.nz * d.ny;
+  int grid = std::min(std::max(1, pl->num_sms * 6), std::min(MAXGRID, (nrows + 7) / 8));
+  grid = std::max(grid, 1);
+  bp.rows_per_cta = (nrows + grid - 1) / grid;
+  grid = (nrows + bp.rows_per_cta - 1) / bp.rows_per_cta;
+  bp.invd = pl->d_invd;
+  bp.x = x;
+  bp.r = r;
+  bp.p = p;
+  bp.ap = ap;
+  bp.partials = scratch_partials(scratch);
+  bp.counter = scratch_counter(scratch);
+  bp.state = scratch_state(scratch);
+  bp.fuse = fuse;
+  const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
+  void* args[1] = {&bp};
+  CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&cg_pass_b_kernel), dim3(grid),
+                            dim3(NTB), args, sizeof(double) * ninv, st));
+  pl->launches++;
+  return BSPDE_OK;
+}
+
+int check_plan(const bspde_plan* pl) {
+  if (!pl) return fail(BSPDE_ERR_ARG, "null plan");
+  // the statically linked runtime keeps its own current-device state
+  cudaError_t e = cudaSetDevice(pl->device);
+  if (e != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return BSPDE_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+const char* bspde_last_error(void) { return g_err.c_str(); }
+
+int bspde_version(void) { return 1; }
+
+int bspde_device_ok(int device) {
+  int dev = device;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+  return prop.major == 10 ? 1 : 0;
+}
+
+int bspde_plan_create(const bspde_plan_desc* desc, bspde_plan** out) {
+  if (!desc || !out) return fail(BSPDE_ERR_ARG, "null argument");
+  const auto& d = *desc;
+  if (d.degree < 1 || d.degree > MAXP) return fail(BSPDE_ERR_ARG, "degree must be in 1..5");
+  if (d.nx < 1 || d.ny < 1 || d.nz < 1) return fail(BSPDE_ERR_ARG, "empty extents");
+  if (d.pitch_y < d.nx || (d.pitch_y & 1)) return fail(BSPDE_ERR_ARG, "pitch_y must be even and >= nx");
+  const int EW = edge_width_of(d.degree);
+  for (int a = 0; a < 3; ++a) {
+    if (d.ew[a] < 0 || d.ew[a] > EW) return fail(BSPDE_ERR_ARG, "edge width out of range");
+    if (!d.mass_table[a] || !d.stiff_table[a]) return fail(BSPDE_ERR_ARG, "missing tables");
+  }
+  if (!d.inv_diag_table) return fail(BSPDE_ERR_ARG, "missing inverse diagonal table");
+  if (d.z_offset < 0 || d.z_offset + d.nz > d.nz_global) return fail(BSPDE_ERR_ARG, "bad z slab");
+  if (d.device < 0) return fail(BSPDE_ERR_ARG, "bad device ordinal");
+  {
+    cudaError_t e = cudaSetDevice(d.device);
+    if (e != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  auto* pl = new bspde_plan();
+  pl->d = d;
+  pl->device = d.device;
+  pl->p = d.degree;
+  pl->NC = 2 * EW + 1;
+  pl->pitch_z = (long long)d.ny * d.pitch_y;
+  cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, d.device);
+  const int R = 2 * d.degree + 1;
+  // device tables: [axis][kind][NC][R], classes beyond 2*ew unused
+  std::vector<double> tab((size_t)6 * pl->NC * R, 0.0);
+  for (int a = 0; a < 3; ++a) {
+    const int nca = 2 * d.ew[a] + 1;
+    for (int c = 0; c < nca; ++c)
+      for (int k = 0; k < R; ++k) {
+        tab[((a * 2 + 0) * pl->NC + c) * R + k] = d.mass_table[a][c * R + k];
+        tab[((a * 2 + 1) * pl->NC + c) * R + k] = d.stiff_table[a][c * R + k];
+      }
+  }
+  const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
+  cudaError_t e1 = cudaMalloc(&pl->d_tab, tab.size() * sizeof(double));
+  cudaError_t e2 = cudaMalloc(&pl->d_invd, ninv * sizeof(double));
+  cudaError_t e3 = cudaMallocHost(&pl->host_state, sizeof(CgState));
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+    bspde_plan_destroy(pl);
+    return fail(BSPDE_ERR_CUDA, "plan allocation failed");
+  }
+  cudaMemcpy(pl->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(pl->d_invd, d.inv_diag_table, ninv * sizeof(double), cudaMemcpyHostToDevice);
+  // the plan keeps copies of the host tables it needs later
+  for (int a = 0; a < 3; ++a) {
+    pl->d.mass_table[a] = nullptr;
+    pl->d.stiff_table[a] = nullptr;
+  }
+  pl->d.inv_diag_table = nullptr;
+  pl->host_tab = tab;
+  for (int a = 0; a < 3; ++a) {
+    pl->d.mass_table[a] = pl->host_tab.data() + ((a * 2 + 0) * pl->NC) * R;
+    pl->d.stiff_table[a] = pl->host_tab.data() + ((a * 2 + 1) * pl->NC) * R;
+  }
+  // resolve kernel attributes before any stream capture
+  for (int mode = 0; mode < 4; ++mode) kernel_for(pl->p, mode);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    bspde_plan_destroy(pl);
+    return fail(BSPDE_ERR_CUDA, std::string("plan setup: ") + cudaGetErrorString(e));
+  }
+  *out = pl;
+  return BSPDE_OK;
+}
+
+int bspde_plan_destroy(bspde_plan* pl) {
+  if (!pl) return BSPDE_OK;
+  for (auto& kv : pl->graphs) cudaGraphExecDestroy(kv.second);
+  if (pl->d_tab) cudaFree(pl->d_tab);
+  if (pl->d_invd) cudaFree(pl->d_invd);
+  if (pl->host_state) cudaFreeHost(pl->host_state);
+  delete pl;
+  return BSPDE_OK;
+}
+
+int64_t bspde_scratch_bytes(const bspde_plan* pl) {
+  (void)pl;
+  return (int64_t)scratch_size();
+}
+
+int64_t bspde_launch_count(const bspde_plan* pl) { return pl ? pl->launches : 0; }
+
+int bspde_apply(bspde_plan* pl, const double* c, double* out, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!c || !out) return fail(BSPDE_ERR_ARG, "null field");
+  return launch_sep(pl, M_APPLY, c, nullptr, out, nullptr, 0.0, 0.0, false, nullptr, 1,
+                    (cudaStream_t)stream);
+}
+
+int bspde_mass_apply(bspde_plan* pl, const double* c, const double* f, double cm, double a,
+                     double* out, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!c || !out) return fail(BSPDE_ERR_ARG, "null field");
+  return launch_sep(pl, M_MASS, c, nullptr, out, f, a, cm, true, nullptr, 1,
+                    (cudaStream_t)stream);
+}
+
+int bspde_jacobi_diagonal(bspde_plan* pl, const double* diag_table, double* out, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  const auto& d = pl->d;
+  const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
+  double* dt = nullptr;
+  CUDA_TRY(cudaMalloc(&dt, ninv * sizeof(double)));
+  CUDA_TRY(cudaMemcpy(dt, diag_table, ninv * sizeof(double), cudaMemcpyHostToDevice));
+  const long long total = (long long)d.nz * d.ny * d.nx;
+  const int grid = (int)std::min<long long>((total + 255) / 256, pl->num_sms * 8);
+  diag_kernel<<<std::max(grid, 1), 256, 0, (cudaStream_t)stream>>>(
+      dt, d.nx, d.ny, d.nz, d.nz_global, d.z_offset, pl->p, d.pitch_y, pl->pitch_z, d.ew[0],
+      d.ew[1], d.ew[2], out);
+  pl->launches++;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  CUDA_TRY(cudaFree(dt));
+  return BSPDE_OK;
+}
+
+int bspde_cg_setup(bspde_plan* pl, void* scratch, double* history, const bspde_cg_config* cfg,
+                   void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!scratch || !cfg) return fail(BSPDE_ERR_ARG, "null argument");
+  if (!(cfg->tol > 0.0)) return fail(BSPDE_ERR_ARG, "tol must be positive");
+  if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
+  if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
+  CgState* hs = reinterpret_cast<CgState*>(pl->host_state);
+  cudaStream_t st = (cudaStream_t)stream;
+  // the pinned staging buffer may still be in use by a previous async copy
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::memset(hs, 0, sizeof(CgState));
+  hs->tol = cfg->tol;
+  hs->max_iter = cfg->max_iter;
+  hs->record_history = cfg->record_history ? 1 : 0;
+  hs->has_x0 = cfg->has_x0 ? 1 : 0;
+  hs->history = history;
+  hs->scale = 1.0;
+  CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(scratch_counter(scratch), 0, 64, st));
+  return BSPDE_OK;
+}
+
+int bspde_cg_residual(bspde_plan* pl, const double* b, const double* x, double* r,
+                      void* scratch, int fuse, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!b || !x || !r || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, fuse,
+                    (cudaStream_t)stream);
+}
+
+int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p, double* ap, void* scratch,
+                    int fuse, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!r || !p || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
+                    (cudaStream_t)stream);
+}
+
+int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double* ap,
+                    void* scratch, int fuse, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!x || !r || !p || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, x, r, p, ap, scratch, fuse, (cudaStream_t)stream);
+}
+
+int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  finalize_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(scratch_state(scratch), kind);
+  pl->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_cg_read_report(bspde_plan* pl, const void* scratch, bspde_cg_report* rep,
+                         int32_t* active, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CgState* hs = reinterpret_cast<CgState*>(pl->host_state);
+  CUDA_TRY(cudaMemcpyAsync(hs, scratch_state(const_cast<void*>(scratch)), sizeof(CgState),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (rep) {
+    rep->iterations = hs->it;
+    rep->status = hs->status;
+    rep->residual = hs->res;
+    rep->residual0 = hs->res0;
+    rep->rhs_norm = hs->rhs_norm;
+    rep->relative_residual = hs->res / hs->scale;
+    rep->last_pAp = hs->pAp;
+  }
+  if (active) *active = hs->active;
+  return BSPDE_OK;
+}
+
+int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* ap,
+                    void* scratch, double* history, const bspde_cg_config* cfg,
+                    bspde_cg_report* report, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!b || !x || !r || !p || !ap || !scratch || !cfg)
+    return fail(BSPDE_ERR_ARG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)(pl->d.nz + 2 * pl->p) * pl->pitch_z * sizeof(double);
+  int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
+  if (rc) return rc;
+  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
+  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
+  if (rc) return rc;
+  int32_t active = 0;
+  rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
+  if (rc) return rc;
+  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  while (active) {
+    bspde_plan::GraphKey key{x, r, p, ap, scratch, K};
+    auto itg = pl->graphs.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (itg == pl->graphs.end()) {
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      int crc = BSPDE_OK;
+      for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
+        crc = launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, 1, st);
+        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, ap, scratch, 1, st);
+      }
+      cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      if (crc) {
+        if (graph) cudaGraphDestroy(graph);
+        return crc;
+      }
+      if (ce != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
+      pl->graphs[key] = exec;
+      // launch counter for the captured kernels counts once per replay below
+      pl->launches -= 2 * K;
+    } else {
+      exec = itg->second;
+    }
+    CUDA_TRY(cudaGraphLaunch(exec, st));
+    pl->launches += 2 * K;
+    rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
+    if (rc) return rc;
+  }
+  return BSPDE_OK;
+}
+
+}  // extern "C"

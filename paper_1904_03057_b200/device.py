@@ -1,0 +1,208 @@
+"""Device-side plumbing: the ghosted-slab field layout and the native plan.
+
+Layout (``include/bspde_b200.h``): a field of the local extended grid is a
+torch float64 tensor ``buf[nz + 2*ghost, ny, pitch]`` on the GPU, owned plane
+``k`` at ``buf[k + ghost]``, ``pitch = nx`` rounded up to even (16-byte rows
+for TMA).  Ghost planes (``ghost = degree``) carry neighbour-slab planes in
+multi-GPU runs and zeros at physical domain ends.  At 930^3 a field is 6.4 GB;
+a CG solve keeps x, r, p, Ap (+ b) resident, 32 GB of 180 GB HBM3e.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import NativeLibraryError, ValidationError
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def require_cuda(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("the b200 strategy needs a CUDA device (no CPU fallback)")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    lib = N.load()
+    if not lib.bspde_device_ok(dev.index):
+        raise NativeLibraryError(f"device {dev} is not an sm_100 (B200-class) GPU")
+    return dev
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    nz: int          # owned z planes
+    ny: int
+    nx: int
+    ghost: int
+    z_offset: int = 0
+    nz_global: int = None
+
+    def __post_init__(self):
+        if self.nz_global is None:
+            object.__setattr__(self, "nz_global", self.nz)
+
+    @property
+    def pitch(self) -> int:
+        return self.nx + (self.nx & 1)
+
+    @property
+    def buf_shape(self):
+        return (self.nz + 2 * self.ghost, self.ny, self.pitch)
+
+    @property
+    def owned_shape(self):
+        return (self.nz, self.ny, self.nx)
+
+    @property
+    def bytes(self) -> int:
+        return int(np.prod(self.buf_shape)) * 8
+
+    def alloc(self, device):
+        torch = _torch()
+        return torch.zeros(self.buf_shape, dtype=torch.float64, device=device)
+
+    def owned(self, buf):
+        return buf[self.ghost:self.ghost + self.nz, :, :self.nx]
+
+    def upload(self, arr, device, buf=None):
+        """Host/torch array of the owned shape -> (new or given) device buffer."""
+        torch = _torch()
+        if buf is None:
+            buf = self.alloc(device)
+        src = arr if isinstance(arr, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(arr, dtype=np.float64))
+        src = src.reshape(self.owned_shape)
+        self.owned(buf).copy_(src, non_blocking=False)
+        return buf
+
+    def download(self, buf) -> np.ndarray:
+        return self.owned(buf).cpu().numpy().copy()
+
+
+class NativePlan:
+    """Owns one ``bspde_plan`` (operator tables on the device + launch setup)."""
+
+    def __init__(self, data, layout: SlabLayout, device, precond="jacobi"):
+        self.data = data
+        self.layout = layout
+        self.device = device
+        self.lib = N.load()
+        R = 2 * data.n_b + 1
+        self._keep = []
+
+        def arr(a):
+            a = np.ascontiguousarray(a, dtype=np.float64).ravel()
+            self._keep.append(a)
+            return a.ctypes.data_as(N._dptr)
+
+        d = N.PlanDesc()
+        d.device = int(device.index)
+        d.degree = int(data.n_b)
+        d.nz, d.ny, d.nx = layout.nz, layout.ny, layout.nx
+        d.nz_global = layout.nz_global
+        d.z_offset = layout.z_offset
+        for a in range(3):
+            d.ew[a] = data.mass[a].ew
+            d.mass_table[a] = arr(data.mass[a].table)
+            d.stiff_table[a] = arr(data.stiff[a].table)
+            assert data.mass[a].table.shape[1] == R
+        self.inv_table = data.inv_diag_table(precond)
+        d.inv_diag_table = arr(self.inv_table)
+        d.pitch_y = layout.pitch
+        d.c_mass = float(data.c_mass)
+        for a in range(3):
+            d.c_stiff[a] = float(data.c_stiff[a])
+        h = C.c_void_p()
+        N.check(self.lib.bspde_plan_create(C.byref(d), C.byref(h)))
+        self.handle = h
+        self.desc = d
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            self.lib.bspde_plan_destroy(self.handle)
+            self.handle = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.bspde_launch_count(self.handle))
+
+    def scratch(self):
+        torch = _torch()
+        n = int(self.lib.bspde_scratch_bytes(self.handle))
+        return torch.zeros(n, dtype=torch.uint8, device=self.device)
+
+    # thin wrappers ------------------------------------------------------
+    def apply(self, c, out, stream=None):
+        N.check(self.lib.bspde_apply(self.handle, N.ptr(c), N.ptr(out), N.stream_handle(stream)))
+
+    def mass_apply(self, c, f, cm, a, out, stream=None):
+        N.check(self.lib.bspde_mass_apply(self.handle, N.ptr(c), N.ptr(f), float(cm), float(a),
+                                          N.ptr(out), N.stream_handle(stream)))
+
+    def jacobi_diagonal(self, out, stream=None):
+        tab = np.ascontiguousarray(self.data.diag_table(), dtype=np.float64)
+        N.check(self.lib.bspde_jacobi_diagonal(self.handle, tab.ctypes.data_as(N._dptr),
+                                               N.ptr(out), N.stream_handle(stream)))
+
+    def pcg(self, b, x, r, p, ap, scratch, history, tol, max_iter, record_history, has_x0,
+            poll_every=8, stream=None):
+        cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
+                         int(bool(has_x0)), int(poll_every))
+        rep = N.CgReport()
+        N.check(self.lib.bspde_pcg_solve(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(p),
+                                         N.ptr(ap), N.ptr(scratch), N.ptr(history),
+                                         C.byref(cfg), C.byref(rep), N.stream_handle(stream)))
+        return rep
+
+    # step-wise CG (multi-GPU driver)
+    def cg_setup(self, scratch, history, tol, max_iter, record_history, has_x0, stream=None):
+        cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
+                         int(bool(has_x0)), 0)
+        N.check(self.lib.bspde_cg_setup(self.handle, N.ptr(scratch), N.ptr(history),
+                                        C.byref(cfg), N.stream_handle(stream)))
+
+    def cg_residual(self, b, x, r, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_residual(self.handle, N.ptr(b), N.ptr(x), N.ptr(r),
+                                           N.ptr(scratch), int(fuse), N.stream_handle(stream)))
+
+    def cg_pass_a(self, r, p, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_a(self.handle, N.ptr(r), N.ptr(p), N.ptr(ap),
+                                         N.ptr(scratch), int(fuse), N.stream_handle(stream)))
+
+    def cg_pass_b(self, x, r, p, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(p), N.ptr(ap),
+                                         N.ptr(scratch), int(fuse), N.stream_handle(stream)))
+
+    def cg_finalize(self, scratch, kind, stream=None):
+        N.check(self.lib.bspde_cg_finalize(self.handle, N.ptr(scratch), int(kind),
+                                           N.stream_handle(stream)))
+
+    def cg_read(self, scratch, stream=None):
+        rep = N.CgReport()
+        active = C.c_int32()
+        N.check(self.lib.bspde_cg_read_report(self.handle, N.ptr(scratch), C.byref(rep),
+                                              C.byref(active), N.stream_handle(stream)))
+        return rep, bool(active.value)
+
+
+def check_host_field(c, shape, what="input coefficients"):
+    c = np.asarray(c)
+    if c.shape != tuple(shape):
+        raise ValidationError(f"extents {c.shape} != operator grid {tuple(shape)}")
+    if not np.all(np.isfinite(c)):
+        raise ValidationError(f"{what} contain non-finite values")
+    return np.ascontiguousarray(c, dtype=np.float64)

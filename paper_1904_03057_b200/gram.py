@@ -1,0 +1,249 @@
+"""Exact 1-D B-spline Gram factors (host setup, computed once per grid).
+
+For constant diffusion ``D`` and absorption ``mu`` on a box domain without
+face terms, the reference operator (``OnTheFlyOperator`` over
+``build_system``, ``/root/reference/pkg/src/bspde/assembly.py:396-457``)
+is exactly the Kronecker sum
+
+    A = vol * [ mu * Mz(x)My(x)Mx
+                + D * ( Kz(x)My(x)Mx / hz^2 + Mz(x)Ky(x)Mx / hy^2 + Mz(x)My(x)Kx / hx^2 ) ]
+
+where ``Ma``/``Ka`` are the 1-D mass and stiffness Gram matrices of the
+degree-p centered B-splines on the *extended* coefficient axis (length
+``N + 2*ext``).  Each is banded (half-width p), symmetric, Toeplitz in the
+interior and position dependent in the first/last ``ew = ext + fc`` rows
+(``assembly.py:83-108``: ``trilinear_axis_band`` with ``edge_trilinear_table``
+for ``i < ew`` and the mirrored table for ``i >= n - ew``).
+
+The reference integrates the products with composite Gauss-Legendre
+quadrature (``kernels.py:65-93``).  Here every entry is computed in exact
+rational arithmetic (the B-spline pieces have rational coefficients and
+the integration limits are half-integers), then rounded once to fp64, so
+the factors are correctly rounded.  ``tests/test_gram.py`` pins them
+against the reference's tables (golden fixtures) at <= 1e-15.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+from functools import lru_cache
+
+import numpy as np
+
+from .errors import DegreeError, ValidationError
+
+MAX_DEGREE = 5
+
+
+# ---------------------------------------------------------------------------
+# exact polynomial helpers (coefficient lists, lowest power first)
+
+
+def _pmul(a, b):
+    out = [Fraction(0)] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        if x == 0:
+            continue
+        for j, y in enumerate(b):
+            out[i + j] += x * y
+    return out
+
+
+def _pshift(a, s):
+    """Coefficients of q(x) = a(x - s)."""
+    out = [Fraction(0)] * len(a)
+    for k, c in enumerate(a):
+        if c == 0:
+            continue
+        # (x - s)^k = sum_j C(k,j) x^j (-s)^(k-j)
+        for j in range(k + 1):
+            out[j] += c * math.comb(k, j) * (-s) ** (k - j)
+    return out
+
+
+def _pderiv(a):
+    return [a[k] * k for k in range(1, len(a))] or [Fraction(0)]
+
+
+def _pint(a, lo, hi):
+    tot = Fraction(0)
+    for k, c in enumerate(a):
+        if c != 0:
+            tot += c * (hi ** (k + 1) - lo ** (k + 1)) / (k + 1)
+    return tot
+
+
+@lru_cache(maxsize=None)
+def bspline_pieces(p: int, deriv: int = 0):
+    """Centered cardinal B-spline ``beta^p`` (or its derivative) as exact pieces.
+
+    Returns a tuple of ``(lo, hi, coeffs)`` on the knot intervals
+    ``[-(p+1)/2 + m, -(p+1)/2 + m + 1]``, using the truncated-power form
+    ``beta^p(x) = 1/p! sum_k (-1)^k C(p+1,k) (x - a_k)_+^p``.
+    """
+    if not 0 <= p <= 2 * MAX_DEGREE + 1:
+        raise DegreeError(f"degree {p} out of range")
+    if deriv > p:
+        raise ValidationError(f"order-{deriv} derivative of degree-{p} spline")
+    a0 = Fraction(-(p + 1), 2)
+    knots = [a0 + m for m in range(p + 2)]
+    pieces = []
+    for m in range(p + 1):
+        poly = [Fraction(0)] * (p + 1)
+        for k in range(m + 1):
+            term = _pshift([Fraction(0)] * p + [Fraction(1)], knots[k])  # (x - a_k)^p
+            coef = Fraction((-1) ** k * math.comb(p + 1, k), math.factorial(p))
+            for j, c in enumerate(term):
+                poly[j] += coef * c
+        for _ in range(deriv):
+            poly = _pderiv(poly)
+        pieces.append((knots[m], knots[m + 1], tuple(poly)))
+    return tuple(pieces)
+
+
+def product_integral(p, d1, s1, d2, s2, lo=None, hi=None) -> Fraction:
+    """Exact ``int_lo^hi D^d1 beta^p(x - s1) * D^d2 beta^p(x - s2) dx``."""
+    s1 = Fraction(s1)
+    s2 = Fraction(s2)
+    tot = Fraction(0)
+    for a1, b1, c1 in bspline_pieces(p, d1):
+        for a2, b2, c2 in bspline_pieces(p, d2):
+            a = max(a1 + s1, a2 + s2)
+            b = min(b1 + s1, b2 + s2)
+            if lo is not None:
+                a = max(a, Fraction(lo))
+            if hi is not None:
+                b = min(b, Fraction(hi))
+            if b <= a:
+                continue
+            prod = _pmul(_pshift(list(c1), s1), _pshift(list(c2), s2))
+            tot += _pint(prod, a, b)
+    return tot
+
+
+# ---------------------------------------------------------------------------
+# index conventions (reference: domain.py:222-224, assembly.py:37-44)
+
+
+def basis_extension(p: int) -> int:
+    """Extended-grid padding per side: ``ceil((p+1)/2) - 1``."""
+    return max(int(math.ceil((p + 1) / 2.0)) - 1, 0)
+
+
+def first_clean_position(p: int) -> int:
+    return int(math.ceil((p + 1) / 2.0 - 1e-12))
+
+
+def edge_width(p: int) -> int:
+    """Number of position-dependent rows per axis end (``ew = ext + fc``)."""
+    return basis_extension(p) + first_clean_position(p)
+
+
+def min_axis_length(p: int) -> int:
+    """Minimal number of cells per axis for non-interacting edge rows."""
+    return int(math.ceil(first_clean_position(p) - 1 + (p + 1) / 2.0))
+
+
+# ---------------------------------------------------------------------------
+# 1-D Gram factors
+
+
+@dataclass(frozen=True)
+class GramFactor:
+    """Banded symmetric 1-D Gram matrix in class form.
+
+    ``table[c, k + p]`` is the entry ``G[i, i + k]`` of any row ``i`` of class
+    ``c``; classes ``0..ew-1`` are the first rows, ``ew`` the interior
+    (Toeplitz) row, ``ew+1..2ew`` the last rows (``2ew`` = row ``n-1``).
+    """
+
+    degree: int
+    n: int  # extended axis length
+    ew: int
+    table: np.ndarray  # (2*ew + 1, 2*p + 1) float64
+
+    @property
+    def interior(self):
+        return self.table[self.ew]
+
+    def row_class(self, i):
+        i = np.asarray(i)
+        return np.where(i < self.ew, i,
+                        np.where(i >= self.n - self.ew, 2 * self.ew - (self.n - 1 - i), self.ew))
+
+    def dense(self) -> np.ndarray:
+        p = self.degree
+        G = np.zeros((self.n, self.n))
+        cls = self.row_class(np.arange(self.n))
+        for i in range(self.n):
+            for k in range(-p, p + 1):
+                j = i + k
+                if 0 <= j < self.n:
+                    G[i, j] = self.table[cls[i], k + p]
+        return G
+
+    def diagonal_by_class(self) -> np.ndarray:
+        return self.table[:, self.degree].copy()
+
+
+@lru_cache(maxsize=None)
+def _exact_rows(p: int, deriv: int):
+    """Interior taps and left edge rows (exact Fractions) for degree p."""
+    ext = basis_extension(p)
+    ew = edge_width(p)
+    interior = tuple(product_integral(p, deriv, k, deriv, 0) for k in range(-p, p + 1))
+    edge = []
+    for i in range(ew):
+        ci = i - ext
+        row = []
+        for k in range(-p, p + 1):
+            j = i + k
+            row.append(product_integral(p, deriv, j - ext, deriv, ci, lo=0)
+                       if j >= 0 else Fraction(0))
+        edge.append(tuple(row))
+    return interior, tuple(edge)
+
+
+def _check_degree(p):
+    if not isinstance(p, (int, np.integer)) or not 1 <= p <= MAX_DEGREE:
+        raise DegreeError(f"basis degree {p} not in 1..{MAX_DEGREE}")
+
+
+@lru_cache(maxsize=None)
+def gram_factor(p: int, num_nodes: int, kind: str) -> GramFactor:
+    """Mass (``kind='mass'``) or stiffness (``'stiff'``) factor for one axis.
+
+    ``num_nodes`` is the node count N of the axis; the factor acts on the
+    extended axis of length ``N + 2*ext``.  Entries are in unit-grid
+    coordinates (scale by h for mass, 1/h for stiffness).
+    """
+    _check_degree(p)
+    if kind not in ("mass", "stiff"):
+        raise ValidationError(f"unknown Gram kind {kind!r}")
+    if num_nodes - 1 < min_axis_length(p):
+        raise ValidationError(
+            f"axis with {num_nodes} nodes too short for degree {p} edge tables")
+    deriv = 1 if kind == "stiff" else 0
+    ext = basis_extension(p)
+    ew = edge_width(p)
+    n = num_nodes + 2 * ext
+    interior, edge = _exact_rows(p, deriv)
+    table = np.zeros((2 * ew + 1, 2 * p + 1))
+    for c in range(ew):
+        table[c] = [float(v) for v in edge[c]]
+        # right end mirrors the left one: G[n-1-i, n-1-i-k] = G[i, i+k]
+        table[2 * ew - c] = [float(v) for v in edge[c][::-1]]
+    table[ew] = [float(v) for v in interior]
+    table.setflags(write=False)
+    return GramFactor(degree=p, n=n, ew=ew, table=table)
+
+
+def degenerate_factor(p: int, kind: str) -> GramFactor:
+    """Unit factor for a padded (absent) axis: mass = identity, stiffness = 0."""
+    table = np.zeros((1, 2 * p + 1))
+    if kind == "mass":
+        table[0, p] = 1.0
+    table.setflags(write=False)
+    return GramFactor(degree=p, n=1, ew=0, table=table)

@@ -1,0 +1,133 @@
+"""Implicit-Euler heat stepping on the B200 (the loop the reference lacks).
+
+The reference solves steady problems only.  One implicit
+Euler step of ``u_t = kappa * Laplace(u) + f`` in the Galerkin B-spline space
+is exactly a reference system solve:
+
+    b = M u_prev + dt F                  M: mass system (D=0, mu=1)
+    (M + dt*kappa*K) u = b, x0 = u_prev  Jacobi-PCG
+
+with ``F = assembled_rhs(mass system, p, q)`` the Galerkin source.  Here both
+the RHS (``sep_kernel<P, M_MASS>``: fused mass apply + axpy) and the CG run
+on the GPU with every field resident in HBM between steps.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .domain import BoxDomain, Grid
+from .errors import ValidationError
+from .operator import B200Operator
+from .solver import SolveConfig, SolveReport, pcg_device
+from .system import heat_system
+from .transform import transform_field
+
+
+@dataclass
+class HeatProblem:
+    """Constant-conductivity heat problem on a box with natural (Neumann) faces.
+
+    ``initial`` and ``source`` accept a scalar, node samples or a callable of
+    the node coordinates (like the reference's ProblemSpec fields); pass
+    ``initial_coeffs`` / ``source_coeffs`` to give extended-grid coefficients
+    directly.
+    """
+
+    grid: Grid
+    degree: int
+    dt: float
+    conductivity: float = 1.0
+    initial: object = 0.0
+    source: object = 0.0
+    initial_coeffs: np.ndarray = None
+    source_coeffs: np.ndarray = None
+
+    def __post_init__(self):
+        if not self.dt > 0:
+            raise ValidationError(f"dt must be positive, got {self.dt}")
+
+
+@dataclass
+class HeatState:
+    """Device-resident state of a running heat solve."""
+
+    op: B200Operator
+    u: object          # ghosted-slab tensor (current coefficients)
+    F: object          # Galerkin source (or None)
+    b: object          # RHS work buffer
+    reports: list = field(default_factory=list)
+
+
+class HeatSolver:
+    """Holds the heat operator and resident fields; ``step()`` advances dt."""
+
+    def __init__(self, problem: HeatProblem, config: SolveConfig = None, device=None):
+        self.problem = problem
+        self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
+        data = heat_system(problem.grid, problem.degree, problem.dt, problem.conductivity)
+        self.data = data
+        self.dt = float(problem.dt)
+        self.op = B200Operator(data, device=device)
+        lay = self.op.layout
+        dev = self.op.device
+        u0 = problem.initial_coeffs
+        if u0 is None:
+            u0 = transform_field(problem.initial, problem.grid, problem.degree)
+        self.u = lay.upload(np.asarray(u0).reshape(lay.owned_shape), dev)
+        self.b = lay.alloc(dev)
+        q = problem.source_coeffs
+        if q is None and not (np.ndim(problem.source) == 0 and not callable(problem.source)
+                              and float(problem.source) == 0.0):
+            q = transform_field(problem.source, problem.grid, problem.degree)
+        self.F = None
+        if q is not None:
+            qb = lay.upload(np.asarray(q).reshape(lay.owned_shape), dev)
+            self.F = lay.alloc(dev)
+            self.op.mass_apply_device(qb, self.F)  # F = vol * (M(x)M(x)M) q
+            del qb
+        self.reports = []
+
+    @classmethod
+    def from_device(cls, op: B200Operator, dt, u_buf, F_buf=None, config=None):
+        """Wrap already-resident fields (bench / multi-step pipelines)."""
+        self = cls.__new__(cls)
+        self.problem = None
+        self.dt = float(dt)
+        self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
+        self.data = op.data
+        self.op = op
+        self.u = u_buf
+        self.F = F_buf
+        self.b = op.layout.alloc(op.device)
+        self.reports = []
+        return self
+
+    def rhs(self, stream=None):
+        """b = M u + dt F (one fused kernel)."""
+        self.op.mass_apply_device(self.u, self.b, self.F,
+                                  a=self.dt if self.F is not None else 0.0, stream=stream)
+        return self.b
+
+    def step(self, stream=None) -> SolveReport:
+        self.rhs(stream)
+        rep = pcg_device(self.op, self.b, self.u, self.config, has_x0=True, stream=stream)
+        self.reports.append(rep)
+        return rep
+
+    def run(self, steps: int):
+        for _ in range(int(steps)):
+            self.step()
+        return self.reports
+
+    def coefficients(self) -> np.ndarray:
+        return self.op.layout.download(self.u).reshape(self.data.cext)
+
+
+def heat_solve(problem: HeatProblem, steps: int, config: SolveConfig = None, device=None):
+    """Run ``steps`` implicit-Euler steps; returns (coefficients, [SolveReport])."""
+    hs = HeatSolver(problem, config, device)
+    hs.run(steps)
+    return hs.coefficients(), hs.reports

@@ -1,0 +1,172 @@
+"""System assembly for the B200 strategy (host setup, runs once).
+
+Mirrors the reference's ``build_system`` signature
+(``/root/reference/pkg/src/bspde/assembly.py:396-457``) for the operator the
+hot path realizes: constant diffusion ``D`` and absorption ``mu`` on a box
+domain with natural (Neumann) faces.  With constant fields the reference's
+per-node stencil collapses (partition of unity over the parameter splines)
+into the Kronecker sum documented in :mod:`.gram`; this module computes the
+1-D factors, the axis scales and the Jacobi diagonal by class, i.e. all the
+data the sm_100a kernels need.  Everything is O(p) host work.
+
+Reference dims ``d < 3`` are right-aligned onto the kernel's (z, y, x) axes;
+padded axes are degenerate (length 1, mass factor 1, no stiffness term).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .domain import BoxDomain, Grid
+from .errors import ConfigurationError, ValidationError
+from .gram import (GramFactor, basis_extension, degenerate_factor, edge_width,
+                   gram_factor, min_axis_length)
+
+
+def _constant_value(f, what):
+    arr = np.asarray(f, dtype=np.float64)
+    if arr.size == 0:
+        raise ValidationError(f"{what} field is empty")
+    if not np.all(np.isfinite(arr)):
+        raise ValidationError(f"{what} field contains non-finite values")
+    v = float(arr.flat[0])
+    if arr.size > 1 and not np.all(arr == v):
+        raise ConfigurationError(
+            f"the b200 strategy realizes constant {what}; variable-coefficient "
+            "operators are a later milestone (DESIGN.md 'next')")
+    return v
+
+
+@dataclass
+class SystemData:
+    """What the B200 operator, RHS and solver share (cf. reference SystemData)."""
+
+    domain: object
+    n_b: int
+    n_p: int
+    step: tuple
+    cext: tuple
+    ext: int
+    dtype: np.dtype
+    diffusion: float
+    absorption: float
+    faces: list = field(default_factory=list)
+    # kernel-space (z, y, x) data
+    dims3: tuple = None
+    mass: tuple = None
+    stiff: tuple = None
+    c_mass: float = 0.0
+    c_stiff: tuple = (0.0, 0.0, 0.0)
+    vol: float = 1.0
+
+    @property
+    def dim(self):
+        return len(self.cext)
+
+    @property
+    def a_flat_size(self):
+        return (2 * self.n_b + 1) ** self.dim
+
+    def num_unknowns(self):
+        return int(np.prod(self.cext))
+
+    @property
+    def ew3(self):
+        return tuple(f.ew for f in self.mass)
+
+    # -- Jacobi diagonal by class (operator.py:190-209 for constant fields) --
+    def diag_table(self) -> np.ndarray:
+        mz, my, mx = (f.diagonal_by_class() for f in self.mass)
+        kz, ky, kx = (f.diagonal_by_class() for f in self.stiff)
+        Z, Y, X = np.ix_(np.arange(len(mz)), np.arange(len(my)), np.arange(len(mx)))
+        cz, cy, cx = self.c_stiff
+        d = cz * kz[Z] * my[Y] * mx[X]
+        d = d + cy * mz[Z] * ky[Y] * mx[X]
+        d = d + cx * mz[Z] * my[Y] * kx[X]
+        d = d + self.c_mass * mz[Z] * my[Y] * mx[X]
+        return np.ascontiguousarray(d, dtype=np.float64)
+
+    def inv_diag_table(self, precond="jacobi") -> np.ndarray:
+        d = self.diag_table()
+        if precond == "none":
+            return np.ones_like(d)
+        with np.errstate(divide="ignore"):
+            return np.where(d != 0.0, 1.0 / d, 1.0)
+
+    def class_index(self, axis3, n=None) -> np.ndarray:
+        f = self.mass[axis3]
+        return f.row_class(np.arange(f.n if n is None else n))
+
+    def expand_table(self, table) -> np.ndarray:
+        """Class table (z,y,x) -> full array on the reference extents."""
+        cz, cy, cx = (self.class_index(a) for a in range(3))
+        full = table[np.ix_(cz, cy, cx)]
+        return full.reshape(self.cext)
+
+
+def _as3(seq, pad):
+    seq = tuple(seq)
+    return (pad,) * (3 - len(seq)) + seq
+
+
+def build_system(domain, n_b, n_p, dcoef_ext, mcoef_ext, face_specs=(), dtype=np.float64,
+                 block_bytes=4 << 20) -> SystemData:
+    """Reference-compatible constructor (assembly.py:396-457) for the b200 path.
+
+    ``dcoef_ext``/``mcoef_ext`` are the (constant) diffusion and absorption
+    coefficient fields on the extended parameter grid, or scalars.
+    ``face_specs`` must be empty: Robin / penalty faces are the next milestone.
+    """
+    if not isinstance(domain, BoxDomain):
+        raise ConfigurationError("the b200 strategy supports box domains (mask domains: out of scope)")
+    if face_specs:
+        raise ConfigurationError(
+            "the b200 strategy realizes natural (Neumann) faces; Robin / penalty "
+            "face terms are the next milestone")
+    if not 1 <= int(n_b) <= 5:
+        raise ValidationError(f"basis degree {n_b} not in 1..5")
+    grid = domain.grid
+    D = _constant_value(dcoef_ext, "diffusion")
+    mu = _constant_value(mcoef_ext, "absorption")
+    return _make(domain, int(n_b), int(n_p), D, mu, np.dtype(dtype))
+
+
+def _make(domain, p, n_p, D, mu, dtype) -> SystemData:
+    grid = domain.grid
+    ext = basis_extension(p)
+    for n in grid.extents:
+        if n - 1 < min_axis_length(p):
+            raise ValidationError(
+                f"axis with {n} nodes too short for degree {p} edge tables")
+    cext = tuple(n + 2 * ext for n in grid.extents)
+    vol = float(np.prod(grid.step))
+    mass = [gram_factor(p, n, "mass") for n in grid.extents]
+    stiff = [gram_factor(p, n, "stiff") for n in grid.extents]
+    cst = [vol * D / h ** 2 for h in grid.step]
+    pad = 3 - grid.dim
+    mass3 = tuple([degenerate_factor(p, "mass")] * pad + mass)
+    stiff3 = tuple([degenerate_factor(p, "stiff")] * pad + stiff)
+    c_stiff3 = tuple([0.0] * pad + cst)
+    return SystemData(
+        domain=domain, n_b=p, n_p=n_p, step=grid.step, cext=cext, ext=ext, dtype=dtype,
+        diffusion=D, absorption=mu, faces=[], dims3=_as3(cext, 1), mass=mass3,
+        stiff=stiff3, c_mass=vol * mu, c_stiff=c_stiff3, vol=vol)
+
+
+def heat_system(grid: Grid, degree: int, dt: float, conductivity: float = 1.0) -> SystemData:
+    """``A = M + dt*kappa*K`` of one implicit-Euler step (D = dt*kappa, mu = 1)."""
+    if not dt > 0:
+        raise ValidationError(f"dt must be positive, got {dt}")
+    return _make(BoxDomain(grid), int(degree), int(degree), float(dt) * float(conductivity),
+                 1.0, np.dtype(np.float64))
+
+
+def mass_system(grid: Grid, degree: int) -> SystemData:
+    """The mass operator ``M`` (D = 0, mu = 1)."""
+    return _make(BoxDomain(grid), int(degree), int(degree), 0.0, 1.0, np.dtype(np.float64))
+
+
+__all__ = ["SystemData", "build_system", "heat_system", "mass_system", "edge_width",
+           "GramFactor"]

@@ -1,0 +1,179 @@
+"""Generate golden fixtures from the REFERENCE implementation (build container only).
+
+Run from the repo root:  python tests/golden/make_golden.py
+Imports the reference read-only from /root/reference/pkg/src (it does not
+exist on the GPU box, so its outputs are committed here as small .npz
+fixtures).  Every fixture records the reference call that produced it.
+
+Fixtures:
+  gram.npz     -- 1-D mass/stiffness Gram matrices from the reference's
+                  build_system + assemble_sparse (1-D, unit fields), p=1..5
+  apply.npz    -- 3-D OnTheFlyOperator.apply / jacobi_diagonal for constant
+                  D, mu on small anisotropic boxes, p=1..5 (+ 2-D, 1-D cases)
+  rhs.npz      -- assembled_rhs(mass system, p, q) for random q, p=1..5
+  heat16.npz   -- 10 implicit-Euler heat steps at 16^3 coefficients, p=3,
+                  lambda=4, Jacobi-PCG tol 1e-10 (+ tol 1e-12 solution)
+  heat64.npz   -- C1: 64^3, p=3, lambda=4: 10-step CG counts at tol 1e-10,
+                  inputs, and the step-1 solution at tol 1e-12
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from bspde.assembly import basis_extension, build_system  # noqa: E402
+from bspde.bspline import BSplineBasis, direct_transform  # noqa: E402
+from bspde.domain import BoxDomain, Grid  # noqa: E402
+from bspde.operator import assembled_rhs, make_operator  # noqa: E402
+from bspde.solver import SolveConfig, pcg  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def system(extents, step, p, D, mu):
+    g = Grid(extents, step)
+    ext = basis_extension(p)
+    shp = tuple(n + 2 * ext for n in g.extents)
+    return build_system(BoxDomain(g), p, p, np.full(shp, D), np.full(shp, mu), [])
+
+
+def gram():
+    out = {}
+    for p in range(1, 6):
+        for N in (p + 6, 12):
+            ext = basis_extension(p)
+            n = N + 2 * ext
+            g = Grid((N,), (1.0,))
+            dm = build_system(BoxDomain(g), p, p, np.zeros(n), np.ones(n), [])
+            dk = build_system(BoxDomain(g), p, p, np.ones(n), np.zeros(n), [])
+            out[f"M_p{p}_N{N}"] = make_operator(dm, "sparse").matrix.toarray()
+            out[f"K_p{p}_N{N}"] = make_operator(dk, "sparse").matrix.toarray()
+    np.savez_compressed(os.path.join(OUT, "gram.npz"), **out)
+
+
+APPLY_CASES = [
+    # (tag, extents, step, p, D, mu)
+    ("p1", (9, 10, 11), (0.5, 1.0, 0.25), 1, 0.37, 1.3),
+    ("p2", (9, 10, 11), (0.5, 1.0, 0.25), 2, 0.37, 1.3),
+    ("p3", (9, 10, 11), (0.5, 1.0, 0.25), 3, 0.37, 1.3),
+    ("p4", (10, 11, 12), (0.5, 1.0, 0.25), 4, 0.37, 1.3),
+    ("p5", (10, 11, 12), (0.5, 1.0, 0.25), 5, 0.37, 1.3),
+    ("p3_heat", (12, 12, 12), (1 / 11, 1 / 11, 1 / 11), 3, 4.0 / 121, 1.0),
+    ("p3_min", (4, 5, 6), (1.0, 1.0, 1.0), 3, 1.0, 0.5),
+    ("p3_stiff", (8, 8, 8), (1.0, 1.0, 1.0), 3, 1.0, 0.0),
+    ("p2_2d", (13, 9), (0.5, 0.25), 2, 0.8, 0.2),
+    ("p1_1d", (12,), (1.0,), 1, 1.0, 0.0),
+    ("p3_1d", (15,), (0.3,), 3, 0.7, 1.1),
+]
+
+
+def apply_cases():
+    out = {}
+    rng = np.random.default_rng(1234)
+    for tag, ext_, step, p, D, mu in APPLY_CASES:
+        data = system(ext_, step, p, D, mu)
+        op = make_operator(data, "onthefly")
+        c = rng.normal(size=data.cext)
+        out[f"{tag}_c"] = c
+        out[f"{tag}_t"] = op.apply(c)
+        out[f"{tag}_diag"] = op.jacobi_diagonal()
+        out[f"{tag}_meta"] = np.array([p, D, mu] + list(step) + list(ext_), dtype=float)
+    np.savez_compressed(os.path.join(OUT, "apply.npz"), **out)
+
+
+def rhs_cases():
+    out = {}
+    rng = np.random.default_rng(99)
+    for p in range(1, 6):
+        ext_ = (9 + p, 8 + p, 10)
+        step = (0.5, 0.25, 1.0)
+        data = system(ext_, step, p, 0.0, 1.0)
+        q = rng.normal(size=data.cext)
+        out[f"p{p}_q"] = q
+        out[f"p{p}_t"] = assembled_rhs(data, p, q)
+        out[f"p{p}_meta"] = np.array([p] + list(step) + list(ext_), dtype=float)
+    np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
+
+
+def heat_inputs(ncoef, p=3, lam=4.0):
+    ext = basis_extension(p)
+    N = ncoef - 2 * ext
+    h = 1.0 / (N - 1)
+    dt = lam * h * h
+    g = Grid((N,) * 3, (h,) * 3)
+    X, Y, Z = np.meshgrid(*[g.node_coordinates(a) for a in range(3)], indexing="ij")
+
+    def coef(s):
+        return np.pad(direct_transform(s, BSplineBasis(p, g.step)), ext, mode="reflect")
+
+    u0 = coef(np.exp(-40 * ((X - .5) ** 2 + (Y - .4) ** 2 + (Z - .6) ** 2)))
+    q = coef(10 * np.exp(-60 * ((X - .3) ** 2 + (Y - .6) ** 2 + (Z - .5) ** 2)))
+    return g, N, h, dt, u0, q
+
+
+def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
+    p = 3
+    g, N, h, dt, u0, q = heat_inputs(ncoef, p)
+    t0 = time.time()
+    shp = u0.shape
+    Ad = build_system(BoxDomain(g), p, p, np.full(shp, dt), np.full(shp, 1.0), [])
+    Md = build_system(BoxDomain(g), p, p, np.full(shp, 0.0), np.full(shp, 1.0), [])
+    A = make_operator(Ad, strategy)
+    M = make_operator(Md, strategy)
+    F = assembled_rhs(Md, p, q)
+    out = dict(u0=u0, q=q, F=F, meta=np.array([p, N, h, dt, 4.0]))
+    u = u0.copy()
+    its, rels = [], []
+    sols = []
+    for step in range(steps):
+        u, rep = pcg(A, M.apply(u) + dt * F, SolveConfig(tol=1e-10, max_iter=5000), x0=u)
+        its.append(rep.iterations)
+        rels.append(rep.relative_residual)
+        if keep_all:
+            sols.append(u.copy())
+        print(fname, "step", step, rep.iterations, rep.relative_residual, f"{time.time()-t0:.1f}s",
+              flush=True)
+    out["iters_tol1e-10"] = np.array(its)
+    out["relres_tol1e-10"] = np.array(rels)
+    out["u_final_tol1e-10"] = u
+    if keep_all:
+        out["u_steps_tol1e-10"] = np.stack(sols)
+    # one step at tol 1e-12 for coefficient parity
+    b1 = M.apply(u0) + dt * F
+    out["b1"] = b1
+    u1, rep = pcg(A, b1, SolveConfig(tol=1e-12, max_iter=5000, record_history=True), x0=u0)
+    out["u1_tol1e-12"] = u1
+    out["iters1_tol1e-12"] = np.array([rep.iterations])
+    out["history1_tol1e-12"] = np.array(rep.history)
+    # the 1e-10 coefficient bar needs tol <= 1e-13 between two correct
+    # implementations (rounding drift ~ kappa*tol)
+    u13, rep13 = pcg(A, b1, SolveConfig(tol=1e-13, max_iter=5000), x0=u0)
+    out["u1_tol1e-13"] = u13
+    out["iters1_tol1e-13"] = np.array([rep13.iterations])
+    out["Au0"] = A.apply(u0)
+    out["diagA"] = A.jacobi_diagonal()
+    if not keep_all:
+        # C1 (64^3): keep the repo small -- inputs are regenerated by the oracle
+        # transform, which tests/test_oracle.py pins to the reference at 1e-14
+        for k in ("u0", "q", "F", "b1", "Au0", "diagA"):
+            out.pop(k)
+    np.savez_compressed(os.path.join(OUT, fname), **out)
+    print(fname, "done", its, f"{time.time()-t0:.1f}s")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "heat16", "heat64"]
+    if "gram" in which:
+        gram()
+    if "apply" in which:
+        apply_cases()
+    if "rhs" in which:
+        rhs_cases()
+    if "heat16" in which:
+        heat(16, 10, "heat16.npz")
+    if "heat64" in which:
+        heat(64, 10, "heat64.npz", keep_all=False)
