@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -58,7 +59,11 @@ __host__ __device__ constexpr int edge_width_of(int p) {
 template <int P, int MODE>
 struct Cfg {
   static constexpr int R = 2 * P + 1;
-  static constexpr int HX = TX + 2 * P;
+  // TMA needs the box's inner start (x0 - PX) * 8 bytes to be 16-byte aligned:
+  // the x halo is padded to an even width PX (odd p: one extra column per side)
+  static constexpr int PX = P + (P & 1);
+  static constexpr int DX = PX - P;  // 0 or 1: first used column of a window
+  static constexpr int HX = TX + 2 * PX;
   static constexpr int HY = TY + 2 * P;
   static constexpr int EW = edge_width_of(P);
   static constexpr int NC = 2 * EW + 1;          // max classes per axis
@@ -73,7 +78,7 @@ struct Cfg {
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
   static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + NXB * 2 * XARR + TAB + INV + NW * 4) + 8 * NS + 128;
+    return (size_t)8 * (NS * NA * ARR_D + NXB * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
   }
 };
 
@@ -178,9 +183,11 @@ __device__ __forceinline__ int cls_of(int g, int n, int ew) {
   return g < ew ? g : (g >= n - ew ? 2 * ew - (n - 1 - g) : ew);
 }
 
-// The CG search direction, bitwise identical in pass A and pass B.
+// The CG search direction p = z + beta*p_old with z = r*inv_diag, rounded in
+// the reference's order (solver.py:96-100: z = r*inv_diag; p = z + beta*p) and
+// bitwise identical in pass A and pass B.
 __device__ __forceinline__ double pdir(double r, double invd, double pold, double beta) {
-  return __fma_rn(beta, pold, __dmul_rn(invd, r));
+  return __dadd_rn(__dmul_rn(r, invd), __dmul_rn(beta, pold));
 }
 
 template <typename T>
@@ -265,8 +272,9 @@ __global__ void finalize_kernel(CgState* s, int kind) {
 // last CTA to finish reduces the partials in fixed order (and optionally runs
 // the scalar update).  s_red must hold NWARP*4 doubles.
 template <int NV, int NWARP>
-__device__ void reduce_and_finalize(double (&v)[NV], double* s_red, double* partials,
-                                    unsigned* counter, CgState* st, int fuse, int kind) {
+__device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_last_p,
+                                    double* partials, unsigned* counter, CgState* st, int fuse,
+                                    int kind) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -278,7 +286,7 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, double* part
     for (int i = 0; i < NV; ++i) s_red[warp * 4 + i] = v[i];
   }
   __syncthreads();
-  __shared__ unsigned s_last;
+  unsigned& s_last = *s_last_p;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -324,20 +332,23 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
                const __grid_constant__ CUtensorMap tm1) {
   using C = Cfg<P, MODE>;
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
+  constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
 
   if (MODE == M_CGA) {
     if (!ld_vol(&prm.state->active)) return;
   }
 
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* s_stage = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // no static shared memory in this kernel: the dynamic window starts at the
+  // (1 KB aligned) base, so every TMA destination below is 128-byte aligned
+  extern __shared__ __align__(1024) double smem[];
+  double* s_stage = smem;
   double* s_X = s_stage + NS * NA * C::ARR_D;
   double* s_tab = s_X + C::NXB * 2 * C::XARR;
   double* s_invd = s_tab + C::TAB;
   double* s_red = s_invd + C::INV;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4);
+  unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = prm.nx, ny = prm.ny, nz = prm.nz;
@@ -384,8 +395,8 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
     uint64_t* bar = &s_bar[s];
     const int zb = zc0 - P + pf_j + prm.ghost;  // buffer plane
     mbar_expect_tx(bar, NA * HX * HY * 8);
-    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, &tm0, x0 - P, y0 - P, zb, bar);
-    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, &tm1, x0 - P, y0 - P, zb, bar);
+    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, &tm0, x0 - PX, y0 - P, zb, bar);
+    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, &tm1, x0 - PX, y0 - P, zb, bar);
     ++pf_flat;
     if (++pf_j == nin) {
       pf_j = 0;
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
     item_geom(item, x0, y0, zc0, zc1);
     const int nin = zc1 - zc0 + 2 * P;
     // tile interior flags (uniform per item)
-    const bool fast_x_tile = (x0 - P >= ewx) && (x0 + TX + P - 1 < nx - ewx);
+    const bool fast_x_tile = (x0 - PX >= ewx) && (x0 + TX + PX - 1 < nx - ewx);
     const bool fast_y_tile = (y0 - P >= ewy) && (y0 + TY + P - 1 < ny - ewy);
     const int gy0 = y0 + warp * RPT;  // this warp's first output row
     const bool fast_y_warp = (gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy);
@@ -447,7 +458,7 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
                 double i0 = inv0, i1 = inv0;
                 if (!fast) {
                   const int row = e / HX, col = e - row * HX;
-                  const int gy = y0 - P + row, gx = x0 - P + col;
+                  const int gy = y0 - P + row, gx = x0 - PX + col;
                   const bool oky = (gy >= 0) && (gy < ny);
                   if (oky) {
                     const int cy = cls_of(gy, ny, ewy);
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
             __syncthreads();
 #pragma unroll
             for (int i = 0; i < RPT; ++i)
-              pr[u][i] = stP[(warp * RPT + i + P) * HX + lane + P];
+              pr[u][i] = stP[(warp * RPT + i + P) * HX + lane + PX];
           }
 
           // ---- x-pass: rows 0..HY-1, column pairs ----
@@ -478,13 +489,17 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
               const int row = it >> 4;
               const int q = it & 15;
               const double* w = src + row * HX + 2 * q;
+              // aligned double2 loads covering smem cols [2q, 2q + 2P + 1 + 2*DX]
+              double raw[2 * P + 2 + 2 * DX];
+#pragma unroll
+              for (int k = 0; k < P + 1 + DX; ++k) {
+                const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
+                raw[2 * k] = t.x;
+                raw[2 * k + 1] = t.y;
+              }
               double win[2 * P + 2];
 #pragma unroll
-              for (int k = 0; k < P + 1; ++k) {
-                const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
-                win[2 * k] = t.x;
-                win[2 * k + 1] = t.y;
-              }
+              for (int k = 0; k < 2 * P + 2; ++k) win[k] = raw[k + DX];
               const int gx0 = x0 + 2 * q;
               double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
               if (fast_x_tile || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
@@ -640,9 +655,12 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
                   dsum[2] = fma(r, r, dsum[2]);
                 }
               }
-              acc[u][i] = 0.0;
             }
           }
+          // the slot of the completed output is recycled for output zo + 2p + 1,
+          // also during the first 2p (warm-up) planes of a chunk
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) acc[u][i] = 0.0;
           ++flat;
         }
       }
@@ -651,10 +669,10 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
 
   if (MODE == M_CGA) {
     double v[1] = {dsum[0]};
-    reduce_and_finalize<1, NW>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 1);
+    reduce_and_finalize<1, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 1);
   } else if (MODE == M_RESID) {
     double v[3] = {dsum[0], dsum[1], dsum[2]};
-    reduce_and_finalize<3, NW>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 0);
+    reduce_and_finalize<3, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 0);
   }
 }
 
@@ -666,6 +684,7 @@ constexpr int NTB = 256;
 __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->active)) return;
   __shared__ double s_red[(NTB / 32) * 4];
+  __shared__ unsigned s_last;
   extern __shared__ double s_inv[];
   const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
   const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1, ncz = 2 * ewz + 1;
@@ -705,10 +724,10 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
         double2 pn, xn, rn;
         pn.x = pdir(rv.x, i0, pv.x, beta);
         pn.y = pdir(rv.y, i1, pv.y, beta);
-        xn.x = fma(alpha, pn.x, xv.x);
-        xn.y = fma(alpha, pn.y, xv.y);
-        rn.x = fma(-alpha, av.x, rv.x);
-        rn.y = fma(-alpha, av.y, rv.y);
+        xn.x = __dadd_rn(xv.x, __dmul_rn(alpha, pn.x));
+        xn.y = __dadd_rn(xv.y, __dmul_rn(alpha, pn.y));
+        rn.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
+        rn.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
         rz = fma(rn.x, __dmul_rn(i0, rn.x), rz);
         rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
         rr = fma(rn.x, rn.x, rr);
@@ -721,8 +740,8 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
         const int xx = nx - 1;
         const double i0 = trow[cls_of(xx, nx, ewx)];
         const double pn = pdir(rrw[xx], i0, pr[xx], beta);
-        const double rn = fma(-alpha, apr[xx], rrw[xx]);
-        xr[xx] = fma(alpha, pn, xr[xx]);
+        const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
+        xr[xx] = __dadd_rn(xr[xx], __dmul_rn(alpha, pn));
         rrw[xx] = rn;
         pr[xx] = pn;
         rz = fma(rn, __dmul_rn(i0, rn), rz);
@@ -732,8 +751,8 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       for (int xx = lane; xx < nx; xx += 32) {
         const double i0 = trow[cls_of(xx, nx, ewx)];
         const double pn = pdir(rrw[xx], i0, pr[xx], beta);
-        const double rn = fma(-alpha, apr[xx], rrw[xx]);
-        xr[xx] = fma(alpha, pn, xr[xx]);
+        const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
+        xr[xx] = __dadd_rn(xr[xx], __dmul_rn(alpha, pn));
         rrw[xx] = rn;
         pr[xx] = pn;
         rz = fma(rn, __dmul_rn(i0, rn), rz);
@@ -742,7 +761,8 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     }
   }
   double v[2] = {rz, rr};
-  reduce_and_finalize<2, NTB / 32>(v, s_red, prm.partials, prm.counter, prm.state, prm.fuse, 2);
+  reduce_and_finalize<2, NTB / 32>(v, s_red, &s_last, prm.partials, prm.counter, prm.state,
+                                   prm.fuse, 2);
 }
 
 // out = diag(A) expanded from the class table
@@ -832,6 +852,9 @@ struct bspde_plan {
   std::map<GraphKey, cudaGraphExec_t> graphs;
   void* host_state = nullptr;  // pinned CgState staging
   std::vector<double> host_tab;  // [axis][kind][NC][R]
+  cudaStream_t work = nullptr;    // private stream: CUDA graphs cannot be captured on
+  cudaEvent_t ev_in = nullptr;    // the legacy default stream the caller may use
+  cudaEvent_t ev_out = nullptr;
 };
 
 namespace {
@@ -881,6 +904,13 @@ Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
   const int nz = pl->d.nz;
   Launch best{1, 1, nz, tiles};
   double best_cost = 1e300;
+  if (const char* fc = getenv("BSPDE_FORCE_CHUNKS")) {  // debug / tuning override
+    const int nc = std::max(1, std::min(nz, atoi(fc)));
+    const int len = (nz + nc - 1) / nc;
+    const int ncr = (nz + len - 1) / len;
+    const long long items = (long long)tiles * ncr;
+    return Launch{(int)std::min<long long>(items, slots), ncr, len, (int)items};
+  }
   for (int nc = 1; nc <= nz; ++nc) {
     const int len = (nz + nc - 1) / nc;
     const int ncr = (nz + len - 1) / len;
@@ -905,7 +935,8 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
   cuuint64_t dims[3] = {(cuuint64_t)pl->d.nx, (cuuint64_t)pl->d.ny,
                         (cuuint64_t)(pl->d.nz + 2 * p)};
   cuuint64_t strides[2] = {(cuuint64_t)(pl->d.pitch_y * 8), (cuuint64_t)(pl->pitch_z * 8)};
-  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * p), (cuuint32_t)(TY + 2 * p), 1u};
+  const int px = p + (p & 1);
+  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(TY + 2 * p), 1u};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1048,6 +1079,66 @@ int check_plan(const bspde_plan* pl) {
 
 }  // namespace
 
+// forward declarations of ABI functions used by the solve helper
+extern "C" {
+int bspde_cg_setup(bspde_plan*, void*, double*, const bspde_cg_config*, void*);
+int bspde_cg_read_report(bspde_plan*, const void*, bspde_cg_report*, int32_t*, void*);
+}
+namespace {
+
+int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* ap,
+                 void* scratch, double* history, const bspde_cg_config* cfg,
+                 bspde_cg_report* report, cudaStream_t st) {
+  void* stream = (void*)st;
+  const size_t bytes = (size_t)(pl->d.nz + 2 * pl->p) * pl->pitch_z * sizeof(double);
+  int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
+  if (rc) return rc;
+  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
+  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
+  if (rc) return rc;
+  int32_t active = 0;
+  rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
+  if (rc) return rc;
+  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  while (active) {
+    bspde_plan::GraphKey key{x, r, p, ap, scratch, K};
+    auto itg = pl->graphs.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (itg == pl->graphs.end()) {
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      int crc = BSPDE_OK;
+      for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
+        crc = launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, 1, st);
+        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, ap, scratch, 1, st);
+      }
+      cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      if (crc) {
+        if (graph) cudaGraphDestroy(graph);
+        return crc;
+      }
+      if (ce != cudaSuccess)
+        return fail(BSPDE_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess)
+        return fail(BSPDE_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
+      pl->graphs[key] = exec;
+      pl->launches -= 2 * K;  // captured launches are counted per replay below
+    } else {
+      exec = itg->second;
+    }
+    CUDA_TRY(cudaGraphLaunch(exec, st));
+    pl->launches += 2 * K;
+    rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
+    if (rc) return rc;
+  }
+  return BSPDE_OK;
+}
+
+}  // namespace
+
 // ===========================================================================
 // C ABI
 
@@ -1106,7 +1197,11 @@ int bspde_plan_create(const bspde_plan_desc* desc, bspde_plan** out) {
   cudaError_t e1 = cudaMalloc(&pl->d_tab, tab.size() * sizeof(double));
   cudaError_t e2 = cudaMalloc(&pl->d_invd, ninv * sizeof(double));
   cudaError_t e3 = cudaMallocHost(&pl->host_state, sizeof(CgState));
-  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+  cudaError_t e4 = cudaStreamCreateWithFlags(&pl->work, cudaStreamNonBlocking);
+  cudaError_t e5 = cudaEventCreateWithFlags(&pl->ev_in, cudaEventDisableTiming);
+  cudaError_t e6 = cudaEventCreateWithFlags(&pl->ev_out, cudaEventDisableTiming);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
+      e5 != cudaSuccess || e6 != cudaSuccess) {
     bspde_plan_destroy(pl);
     return fail(BSPDE_ERR_CUDA, "plan allocation failed");
   }
@@ -1140,6 +1235,9 @@ int bspde_plan_destroy(bspde_plan* pl) {
   if (pl->d_tab) cudaFree(pl->d_tab);
   if (pl->d_invd) cudaFree(pl->d_invd);
   if (pl->host_state) cudaFreeHost(pl->host_state);
+  if (pl->work) cudaStreamDestroy(pl->work);
+  if (pl->ev_in) cudaEventDestroy(pl->ev_in);
+  if (pl->ev_out) cudaEventDestroy(pl->ev_out);
   delete pl;
   return BSPDE_OK;
 }
@@ -1266,51 +1364,16 @@ int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, doubl
   if (int rc = check_plan(pl)) return rc;
   if (!b || !x || !r || !p || !ap || !scratch || !cfg)
     return fail(BSPDE_ERR_ARG, "null argument");
-  cudaStream_t st = (cudaStream_t)stream;
-  const size_t bytes = (size_t)(pl->d.nz + 2 * pl->p) * pl->pitch_z * sizeof(double);
-  int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
-  if (rc) return rc;
-  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
-  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
-  rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
-  if (rc) return rc;
-  int32_t active = 0;
-  rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
-  if (rc) return rc;
-  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
-  while (active) {
-    bspde_plan::GraphKey key{x, r, p, ap, scratch, K};
-    auto itg = pl->graphs.find(key);
-    cudaGraphExec_t exec = nullptr;
-    if (itg == pl->graphs.end()) {
-      cudaGraph_t graph = nullptr;
-      CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      int crc = BSPDE_OK;
-      for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
-        crc = launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, 1, st);
-        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, ap, scratch, 1, st);
-      }
-      cudaError_t ce = cudaStreamEndCapture(st, &graph);
-      if (crc) {
-        if (graph) cudaGraphDestroy(graph);
-        return crc;
-      }
-      if (ce != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
-      ce = cudaGraphInstantiate(&exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
-      pl->graphs[key] = exec;
-      // launch counter for the captured kernels counts once per replay below
-      pl->launches -= 2 * K;
-    } else {
-      exec = itg->second;
-    }
-    CUDA_TRY(cudaGraphLaunch(exec, st));
-    pl->launches += 2 * K;
-    rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
-    if (rc) return rc;
-  }
-  return BSPDE_OK;
+  // everything runs on the plan's private stream, ordered after the caller's
+  // stream on entry and before it on exit
+  cudaStream_t caller = (cudaStream_t)stream;
+  cudaStream_t st = pl->work;
+  CUDA_TRY(cudaEventRecord(pl->ev_in, caller));
+  CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_in, 0));
+  int rc = pcg_solve_on(pl, b, x, r, p, ap, scratch, history, cfg, report, st);
+  cudaEventRecord(pl->ev_out, st);
+  cudaStreamWaitEvent(caller, pl->ev_out, 0);
+  return rc;
 }
 
 }  // extern "C"
