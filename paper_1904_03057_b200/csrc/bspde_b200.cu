@@ -23,6 +23,7 @@
 // operator.py:217-229) and the pcg loop (solver.py:51-117).
 
 #include "../../include/bspde_b200.h"
+#include "gram_taps.cuh"
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -35,6 +36,7 @@
 #include <map>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -42,11 +44,15 @@ namespace {
 // ---------------------------------------------------------------------------
 // configuration
 
-constexpr int TX = 32;               // tile width (x), one lane per column
-constexpr int TY = 32;               // tile height (y)
-constexpr int NT = 256;              // threads per CTA
+#ifndef BSPDE_NWY
+#define BSPDE_NWY 6
+#endif
+constexpr int NWY = BSPDE_NWY;       // warp row groups
+constexpr int RPT = 4;               // output rows per thread
+constexpr int TX = 64;               // tile width (x): two warps side by side
+constexpr int TY = NWY * RPT;        // tile height (y)
+constexpr int NT = 64 * NWY;         // threads per CTA (one CTA per SM)
 constexpr int NW = NT / 32;          // warps
-constexpr int RPT = TY / NW;         // output rows per thread (4)
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
 
@@ -69,7 +75,6 @@ struct Cfg {
   static constexpr int NC = 2 * EW + 1;          // max classes per axis
   static constexpr int NA = (MODE == M_CGA) ? 2 : 1;   // staged arrays per plane
   static constexpr int NS = (MODE == M_CGA) ? (P <= 3 ? 3 : 2) : (P <= 3 ? 4 : 3);
-  static constexpr int NXB = (MODE == M_CGA) ? 1 : 2;  // X buffers
   static constexpr bool STIFF = (MODE != M_MASS);
   static constexpr bool INVD = (MODE == M_CGA || MODE == M_RESID);
   static constexpr int ARR = HX * HY;                        // doubles
@@ -78,7 +83,7 @@ struct Cfg {
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
   static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + NXB * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
+    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
   }
 };
 
@@ -97,6 +102,7 @@ struct SepParams {
   long long pitch_y, pitch_z;
   int ew[3];
   int tiles_x, tiles_y, nchunks, chunk_len, nitems;
+  int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
   double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
   const double* tab;             // device: [axis][kind][NC*R] (NC = class stride)
@@ -325,146 +331,229 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
 
 // ---------------------------------------------------------------------------
 // the separable streaming kernel
+//
+// CTA = 512 threads, one per SM, persistent over work items (64x32 tile,
+// z-chunk).  Warp w: x-group g = w & 1 (tile columns 32g..32g+31, one per
+// lane) and row group rg = w >> 1 (tile rows 4rg..4rg+3).  For the x-pass (and
+// the CG p-formation) warp w owns whole haloed rows w, w+16, w+32, so those
+// two steps need only __syncwarp; one __syncthreads per plane separates the
+// x-pass from the y-pass (X is double-buffered).
 
-template <int P, int MODE>
-__global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
-    sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
-               const __grid_constant__ CUtensorMap tm1) {
+template <int U, int S>
+struct StaticFor {
+  template <typename F>
+  __device__ __forceinline__ static void run(F& f) {
+    f(std::integral_constant<int, U>{});
+    StaticFor<U + 1, S>::run(f);
+  }
+};
+template <int S>
+struct StaticFor<S, S> {
+  template <typename F>
+  __device__ __forceinline__ static void run(F&) {}
+};
+
+// Epilogue of one completed output point (plane zo, row gy0 + i, column gx).
+template <int MODE, bool INTERIOR>
+struct Emitter {
+  const SepParams& prm;
+  long long pbase;  // (zo + ghost) * pitch_z + gx
+  int gx, gy0, czo, ncy, ncx, ewy, ewx;
+  bool emit;
+  const double* s_invd;
+  const double* auxv;
+  double* dsum;
+  __device__ __forceinline__ void operator()(int i, double v, double pold) const {
+    if (!emit) return;
+    const int y = gy0 + i;
+    if (!(INTERIOR || (y < prm.ny && gx < prm.nx))) return;
+    const long long off = pbase + (long long)y * prm.pitch_y;
+    if (MODE == M_APPLY || MODE == M_CGA) {
+      __stcs(prm.out + off, v);
+      if (MODE == M_CGA) dsum[0] = fma(pold, v, dsum[0]);
+    } else if (MODE == M_MASS) {
+      double o = prm.c_mass * v;
+      if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
+      __stcs(prm.out + off, o);
+    } else {  // M_RESID
+      const double b = auxv[i];
+      const double r = b - v;
+      __stcs(prm.out + off, r);
+      const double inv = s_invd[(czo * ncy + (INTERIOR ? ewy : cls_of(y, prm.ny, ewy))) * ncx +
+                                (INTERIOR ? ewx : cls_of(gx, prm.nx, ewx))];
+      dsum[0] = fma(b, b, dsum[0]);
+      dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
+      dsum[2] = fma(r, r, dsum[2]);
+    }
+  }
+};
+
+// Static-slot z ring.  Output plane o lives in slot o mod 2P for its whole
+// accumulation; at item-local plane j the completing output (zl - P) is in
+// slot u = j mod 2P, which is extracted and reset through a warp-uniform
+// switch (two register moves per point), while every slot k receives the
+// coefficient of its offset d = (k - u) mod 2P from row z' of the symmetric
+// Mz / Kz (d = 0: the newly started output zl + P, i.e. tap 2P).  No slot is
+// ever renamed, so the plane loop needs neither unrolling nor register moves.
+template <int P, int K>
+__device__ __forceinline__ void ring_take(double (&acc)[2 * P][RPT], double (&out)[RPT]) {
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    out[i] = acc[K][i];
+    acc[K][i] = 0.0;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void ring_take_dispatch(int u, double (&acc)[2 * P][RPT],
+                                                   double (&out)[RPT]) {
+  switch (u) {
+#define BSPDE_TAKE(k) \
+  case k:             \
+    if constexpr (k < 2 * P) ring_take<P, k>(acc, out); \
+    break;
+    BSPDE_TAKE(0) BSPDE_TAKE(1) BSPDE_TAKE(2) BSPDE_TAKE(3) BSPDE_TAKE(4)
+    BSPDE_TAKE(5) BSPDE_TAKE(6) BSPDE_TAKE(7) BSPDE_TAKE(8) BSPDE_TAKE(9)
+#undef BSPDE_TAKE
+    default: break;
+  }
+}
+
+template <int P, int K>
+__device__ __forceinline__ void pring_swap(double (&pr)[P][RPT], double (&pold)[RPT],
+                                           const double* pnew, int stride) {
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    pold[i] = pr[K][i];
+    pr[K][i] = pnew[i * stride];
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void pring_dispatch(int s, double (&pr)[P][RPT], double (&pold)[RPT],
+                                               const double* pnew, int stride) {
+  switch (s) {
+#define BSPDE_PS(k) \
+  case k:           \
+    if constexpr (k < P) pring_swap<P, k>(pr, pold, pnew, stride); \
+    break;
+    BSPDE_PS(0) BSPDE_PS(1) BSPDE_PS(2) BSPDE_PS(3) BSPDE_PS(4)
+#undef BSPDE_PS
+    default: break;
+  }
+}
+
+// Per-item compute: INTERIOR = the haloed tile touches no edge row of x or y
+// and lies inside the grid (no class lookups, no bounds checks).
+template <int P, int MODE, bool INTERIOR>
+__device__ __forceinline__ void run_item(
+    const SepParams& prm, const CUtensorMap* tm0, const CUtensorMap* tm1, double* s_stage,
+    double* s_X, const double* s_tab, const double* s_invd, uint64_t* s_bar, int x0, int y0,
+    int zc0, int zc1, uint32_t& flat, double beta, double (&dsum)[3],
+    // producer state (thread 0)
+    int& pf_item, int& pf_j, uint32_t& pf_flat) {
   using C = Cfg<P, MODE>;
+  using T = GramTaps<P>;
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
-
-  if (MODE == M_CGA) {
-    if (!ld_vol(&prm.state->active)) return;
-  }
-
-  // no static shared memory in this kernel: the dynamic window starts at the
-  // (1 KB aligned) base, so every TMA destination below is 128-byte aligned
-  extern __shared__ __align__(1024) double smem[];
-  double* s_stage = smem;
-  double* s_X = s_stage + NS * NA * C::ARR_D;
-  double* s_tab = s_X + C::NXB * 2 * C::XARR;
-  double* s_invd = s_tab + C::TAB;
-  double* s_red = s_invd + C::INV;
-  unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nx = prm.nx, ny = prm.ny, nz = prm.nz;
+  const int g = warp & 1, rg = warp >> 1;
+  const int nx = prm.nx, ny = prm.ny;
   const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
-  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1, ncz = 2 * ewz + 1;
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
+  const int nin = zc1 - zc0 + 2 * P;
+  const int cxl = g * 32 + lane;          // this thread's output column in the tile
+  const int gx = x0 + cxl;                // global column
+  const int gy0 = y0 + rg * RPT;          // first global output row
+  const bool fast_y_warp = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
 
-  for (int i = tid; i < C::TAB; i += NT) s_tab[i] = prm.tab[i];
-  if (C::INVD) {
-    const int n = ncz * ncy * ncx;
-    for (int i = tid; i < n; i += NT) s_invd[i] = prm.invd[i];
-  }
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&s_bar[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  // table accessors: axis a (0=z,1=y,2=x), kind 0=mass 1=stiff
   auto tabv = [&](int a, int kind, int c, int k) -> double {
     return s_tab[((a * 2 + kind) * NC + c) * R + k];
   };
 
-  const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
-  const int G = gridDim.x;
-  const int tiles_xy = prm.tiles_x * prm.tiles_y;
-
-  // ---- producer cursor (thread 0 only) ----
-  int pf_item = blockIdx.x, pf_j = 0;
-  uint32_t pf_flat = 0;
-  auto item_geom = [&](int item, int& x0, int& y0, int& zc0, int& zc1) {
-    const int t = item % tiles_xy;
-    const int ch = item / tiles_xy;
-    x0 = (t % prm.tiles_x) * TX;
-    y0 = (t / prm.tiles_x) * TY;
-    zc0 = ch * prm.chunk_len;
-    zc1 = min(zc0 + prm.chunk_len, nz);
-  };
+  // producer: issue the next plane of this CTA's work list (thread 0)
   auto issue_next = [&]() {
     if (pf_item >= prm.nitems) return;
-    int x0, y0, zc0, zc1;
-    item_geom(pf_item, x0, y0, zc0, zc1);
-    const int nin = zc1 - zc0 + 2 * P;
+    const int tiles_xy = prm.tiles_x * prm.tiles_y;
+    const int t = pf_item % tiles_xy;
+    const int ch = pf_item / tiles_xy;
+    const int ix0 = (t % prm.tiles_x) * TX, iy0 = (t / prm.tiles_x) * TY;
+    const int izc0 = ch * prm.chunk_len;
+    const int izc1 = min(izc0 + prm.chunk_len, prm.nz);
+    const int inin = izc1 - izc0 + 2 * P;
     const int s = pf_flat % NS;
-    uint64_t* bar = &s_bar[s];
-    const int zb = zc0 - P + pf_j + prm.ghost;  // buffer plane
-    mbar_expect_tx(bar, NA * HX * HY * 8);
-    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, &tm0, x0 - PX, y0 - P, zb, bar);
-    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, &tm1, x0 - PX, y0 - P, zb, bar);
+    const int zb = izc0 - P + pf_j + prm.ghost;
+    mbar_expect_tx(&s_bar[s], NA * HX * HY * 8);
+    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, tm0, ix0 - PX, iy0 - P, zb, &s_bar[s]);
+    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, tm1, ix0 - PX, iy0 - P, zb, &s_bar[s]);
     ++pf_flat;
-    if (++pf_j == nin) {
+    if (++pf_j == inin) {
       pf_j = 0;
-      pf_item += G;
+      pf_item += gridDim.x;
     }
   };
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) issue_next();
-  }
 
-  double dsum[3] = {0.0, 0.0, 0.0};
-  uint32_t flat = 0;
-
-  for (int item = blockIdx.x; item < prm.nitems; item += G) {
-    int x0, y0, zc0, zc1;
-    item_geom(item, x0, y0, zc0, zc1);
-    const int nin = zc1 - zc0 + 2 * P;
-    // tile interior flags (uniform per item)
-    const bool fast_x_tile = (x0 - PX >= ewx) && (x0 + TX + PX - 1 < nx - ewx);
-    const bool fast_y_tile = (y0 - P >= ewy) && (y0 + TY + P - 1 < ny - ewy);
-    const int gy0 = y0 + warp * RPT;  // this warp's first output row
-    const bool fast_y_warp = (gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy);
-
-    double acc[R][RPT];
-    double pr[R][RPT];
+  // z ring (static slots, see zstep) and the CG own-p ring
+  double acc[2 * P][RPT];
+  double pr[P][RPT];
 #pragma unroll
-    for (int s = 0; s < R; ++s)
+  for (int k = 0; k < 2 * P; ++k)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[k][i] = 0.0;
+#pragma unroll
+  for (int k = 0; k < P; ++k)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) pr[k][i] = 0.0;
+
+  for (int j = 0; j < nin; ++j) {
+    const int zl = zc0 - P + j;
+    const int zg = prm.z_off + zl;
+    const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
+    const bool emit = (j >= 2 * P);
+    const int zo = zl - P;
+    const int s = flat % NS;
+    // epilogue operand prefetch (RESID: b, MASS: f) -- latency hidden by the passes
+    double auxv[RPT];
+    if ((MODE == M_RESID || MODE == M_MASS) && emit) {
+      const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        acc[s][i] = 0.0;
-        pr[s][i] = 0.0;
+        const int y = gy0 + i;
+        auxv[i] = 0.0;
+        if ((MODE == M_RESID || prm.aux != nullptr) && (INTERIOR || (y < ny && gx < nx)))
+          auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
       }
+    }
+    mbar_wait(&s_bar[s], (flat / NS) & 1);
+    double* stC = s_stage + (s * NA + 0) * C::ARR_D;
+    double* stP = s_stage + (s * NA + (NA - 1)) * C::ARR_D;
+    double* X1 = s_X + (flat & 1) * 2 * C::XARR;
+    double* X2 = X1 + C::XARR;
+    const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
 
-    for (int jb = 0; jb < nin; jb += R) {
+    if (in_grid) {
+      // ---- [CG] p = D^-1 r + beta p_old on this warp's haloed rows ----
+      if (MODE == M_CGA) {
+        const double inv0 = s_invd[(cz * ncy + ewy) * ncx + ewx];
 #pragma unroll
-      for (int u = 0; u < R; ++u) {
-        const int j = jb + u;
-        if (j < nin) {
-          const int zl = zc0 - P + j;
-          const int zg = prm.z_off + zl;
-          const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
-          const int s = flat % NS;
-          mbar_wait(&s_bar[s], (flat / NS) & 1);
-          double* stC = s_stage + (s * NA + 0) * C::ARR_D;
-          double* stP = s_stage + (s * NA + (NA - 1)) * C::ARR_D;
-          double* X1 = s_X + (C::NXB == 2 ? (flat & 1) : 0) * 2 * C::XARR;
-          double* X2 = X1 + C::XARR;
-          const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
-
-          if (MODE == M_CGA) {
-            // ---- p = D^-1 r + beta p_old on the whole haloed tile ----
-            if (in_grid) {
-              const bool fast = fast_x_tile && fast_y_tile && (cz == ewz);
-              const double inv0 = s_invd[(cz * ncy + ewy) * ncx + ewx];
-              for (int e2 = tid; e2 < C::ARR / 2; e2 += NT) {
-                const int e = 2 * e2;
+        for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
+          const int row = warp + NW * m;
+          if (row < HY) {
+#pragma unroll
+            for (int h = 0; h < (HX / 2 + 31) / 32; ++h) {
+              const int q = lane + 32 * h;
+              if (q < HX / 2) {
+                const int e = row * HX + 2 * q;
                 const double2 rv = *reinterpret_cast<const double2*>(stC + e);
                 const double2 qv = *reinterpret_cast<const double2*>(stP + e);
                 double i0 = inv0, i1 = inv0;
-                if (!fast) {
-                  const int row = e / HX, col = e - row * HX;
-                  const int gy = y0 - P + row, gx = x0 - PX + col;
-                  const bool oky = (gy >= 0) && (gy < ny);
-                  if (oky) {
-                    const int cy = cls_of(gy, ny, ewy);
-                    const double* trow = s_invd + (cz * ncy + cy) * ncx;
-                    i0 = (gx >= 0 && gx < nx) ? trow[cls_of(gx, nx, ewx)] : 0.0;
-                    i1 = (gx + 1 >= 0 && gx + 1 < nx) ? trow[cls_of(gx + 1, nx, ewx)] : 0.0;
+                if (!INTERIOR || cz != ewz) {
+                  const int gyy = y0 - P + row, gxx = x0 - PX + 2 * q;
+                  if (gyy >= 0 && gyy < ny) {
+                    const double* trow = s_invd + (cz * ncy + cls_of(gyy, ny, ewy)) * ncx;
+                    i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
+                    i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
                   } else {
                     i0 = 0.0;
                     i1 = 0.0;
@@ -476,195 +565,273 @@ __global__ void __launch_bounds__(NT, (P <= 3) ? 2 : 1)
                 *reinterpret_cast<double2*>(stP + e) = pv;
               }
             }
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < RPT; ++i)
-              pr[u][i] = stP[(warp * RPT + i + P) * HX + lane + PX];
           }
-
-          // ---- x-pass: rows 0..HY-1, column pairs ----
-          if (in_grid) {
-            const double* src = stP;  // NA==1: stP == stC
-            for (int it = tid; it < HY * (TX / 2); it += NT) {
-              const int row = it >> 4;
-              const int q = it & 15;
-              const double* w = src + row * HX + 2 * q;
-              // aligned double2 loads covering smem cols [2q, 2q + 2P + 1 + 2*DX]
-              double raw[2 * P + 2 + 2 * DX];
+        }
+        __syncwarp();
+      }
+      // ---- x-pass on this warp's rows: u1 = Mx c, u2 = Kx c ----
+      const double* src = stP;
 #pragma unroll
-              for (int k = 0; k < P + 1 + DX; ++k) {
-                const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
-                raw[2 * k] = t.x;
-                raw[2 * k + 1] = t.y;
-              }
-              double win[2 * P + 2];
+      for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
+        const int row = warp + NW * m;
+        if (row < HY) {
+          const double* w = src + row * HX + 2 * lane;
+          double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
-              for (int k = 0; k < 2 * P + 2; ++k) win[k] = raw[k + DX];
-              const int gx0 = x0 + 2 * q;
-              double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
-              if (fast_x_tile || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
-#pragma unroll
-                for (int k = 0; k < 2 * P + 1; ++k) {
-                  m0 = fma(prm.txm[k], win[k], m0);
-                  m1 = fma(prm.txm[k], win[k + 1], m1);
-                  if (STIFF) {
-                    k0 = fma(prm.txk[k], win[k], k0);
-                    k1 = fma(prm.txk[k], win[k + 1], k1);
-                  }
-                }
-              } else {
-                const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
-                const int c1 = (gx0 + 1 < nx) ? cls_of(gx0 + 1, nx, ewx) : ewx;
-#pragma unroll
-                for (int k = 0; k < 2 * P + 1; ++k) {
-                  m0 = fma(tabv(2, 0, c0, k), win[k], m0);
-                  m1 = fma(tabv(2, 0, c1, k), win[k + 1], m1);
-                  if (STIFF) {
-                    k0 = fma(tabv(2, 1, c0, k), win[k], k0);
-                    k1 = fma(tabv(2, 1, c1, k), win[k + 1], k1);
-                  }
-                }
-              }
-              *reinterpret_cast<double2*>(X1 + row * TX + 2 * q) = make_double2(m0, m1);
-              if (STIFF) *reinterpret_cast<double2*>(X2 + row * TX + 2 * q) = make_double2(k0, k1);
-            }
+          for (int k = 0; k < P + 1 + DX; ++k) {
+            const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
+            raw[2 * k] = t.x;
+            raw[2 * k + 1] = t.y;
           }
-          __syncthreads();
-          if (tid == 0) {
-            fence_proxy_async();
-            issue_next();
-          }
-
-          if (in_grid) {
-            // ---- y-pass (register scatter over the 2p+RPT input rows) ----
-            double wm[RPT], wa[RPT];
+          double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+          const int gx0 = x0 + 2 * lane;
+          if (INTERIOR || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
+            // symmetric taps: G[k] = G[2P-k]
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              wm[i] = 0.0;
-              wa[i] = 0.0;
-            }
-            const double* x1c = X1 + (warp * RPT) * TX + lane;
-            const double* x2c = X2 + (warp * RPT) * TX + lane;
-            if (fast_y_warp) {
-#pragma unroll
-              for (int rr = 0; rr < RPT + 2 * P; ++rr) {
-                const double a1 = x1c[rr * TX];
-                double t = 0.0;
-                if (STIFF) t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                  const int k = rr - i;
-                  if (k >= 0 && k <= 2 * P) {
-                    wm[i] = fma(prm.tym[k], a1, wm[i]);
-                    if (STIFF) {
-                      wa[i] = fma(prm.tym[k], t, wa[i]);
-                      wa[i] = fma(prm.tyk[k], a1, wa[i]);  // tyk pre-scaled by cy
-                    }
-                  }
-                }
-              }
-            } else {
-              int cyr[RPT];
-#pragma unroll
-              for (int i = 0; i < RPT; ++i) {
-                const int gy = gy0 + i;
-                cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
-              }
-#pragma unroll
-              for (int rr = 0; rr < RPT + 2 * P; ++rr) {
-                const double a1 = x1c[rr * TX];
-                double t = 0.0;
-                if (STIFF) t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                  const int k = rr - i;
-                  if (k >= 0 && k <= 2 * P) {
-                    const double my = tabv(1, 0, cyr[i], k);
-                    wm[i] = fma(my, a1, wm[i]);
-                    if (STIFF) {
-                      wa[i] = fma(my, t, wa[i]);
-                      wa[i] = fma(prm.cy * tabv(1, 1, cyr[i], k), a1, wa[i]);
-                    }
-                  }
-                }
+            for (int k = 0; k < P; ++k) {
+              const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
+              const double s1 = raw[DX + 1 + k] + raw[DX + 1 + 2 * P - k];
+              m0 = fma(T::M(k), s0, m0);
+              m1 = fma(T::M(k), s1, m1);
+              if (STIFF) {
+                k0 = fma(T::K(k), s0, k0);
+                k1 = fma(T::K(k), s1, k1);
               }
             }
-
-            // ---- z-pass: scatter into the ring (row z' of symmetric Mz/Kz) ----
-            if (cz == ewz) {
+            m0 = fma(T::M(P), raw[DX + P], m0);
+            m1 = fma(T::M(P), raw[DX + P + 1], m1);
+            if (STIFF) {
+              k0 = fma(T::K(P), raw[DX + P], k0);
+              k1 = fma(T::K(P), raw[DX + P + 1], k1);
+            }
+          } else {
+            const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
+            const int c1 = (gx0 + 1 < nx) ? cls_of(gx0 + 1, nx, ewx) : ewx;
 #pragma unroll
-              for (int k = 0; k < R; ++k) {
-                const int slot = (u + k) % R;
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                  if (STIFF) {
-                    acc[slot][i] = fma(prm.tzm[k], wa[i], acc[slot][i]);
-                    acc[slot][i] = fma(prm.tzk[k], wm[i], acc[slot][i]);
-                  } else {
-                    acc[slot][i] = fma(prm.tzm[k], wm[i], acc[slot][i]);
-                  }
-                }
-              }
-            } else {
-#pragma unroll
-              for (int k = 0; k < R; ++k) {
-                const int slot = (u + k) % R;
-                const double cm = tabv(0, 0, cz, k);
-                const double ck = prm.cz * tabv(0, 1, cz, k);
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                  if (STIFF) {
-                    acc[slot][i] = fma(cm, wa[i], acc[slot][i]);
-                    acc[slot][i] = fma(ck, wm[i], acc[slot][i]);
-                  } else {
-                    acc[slot][i] = fma(cm, wm[i], acc[slot][i]);
-                  }
-                }
+            for (int k = 0; k < 2 * P + 1; ++k) {
+              m0 = fma(tabv(2, 0, c0, k), raw[DX + k], m0);
+              m1 = fma(tabv(2, 0, c1, k), raw[DX + k + 1], m1);
+              if (STIFF) {
+                k0 = fma(tabv(2, 1, c0, k), raw[DX + k], k0);
+                k1 = fma(tabv(2, 1, c1, k), raw[DX + k + 1], k1);
               }
             }
           }
-
-          // ---- emit output plane zo = zl - P (complete) ----
-          if (j >= 2 * P) {
-            const int zo = zl - P;
-            const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z;
-            const int x = x0 + lane;
-            int czo = 0;
-            if (MODE == M_RESID) czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const int y = gy0 + i;
-              const double v = acc[u][i];
-              if (y < ny && x < nx) {
-                const long long off = pbase + (long long)y * prm.pitch_y + x;
-                if (MODE == M_APPLY || MODE == M_CGA) {
-                  prm.out[off] = v;
-                  if (MODE == M_CGA) dsum[0] = fma(pr[(u + P + 1) % R][i], v, dsum[0]);
-                } else if (MODE == M_MASS) {
-                  double o = prm.c_mass * v;
-                  if (prm.aux) o = fma(prm.aux_scale, prm.aux[off], o);
-                  prm.out[off] = o;
-                } else {  // M_RESID
-                  const double b = prm.aux[off];
-                  const double r = b - v;
-                  prm.out[off] = r;
-                  const double inv =
-                      s_invd[(czo * ncy + cls_of(y, ny, ewy)) * ncx + cls_of(x, nx, ewx)];
-                  dsum[0] = fma(b, b, dsum[0]);
-                  dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
-                  dsum[2] = fma(r, r, dsum[2]);
-                }
-              }
-            }
-          }
-          // the slot of the completed output is recycled for output zo + 2p + 1,
-          // also during the first 2p (warm-up) planes of a chunk
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) acc[u][i] = 0.0;
-          ++flat;
+          *reinterpret_cast<double2*>(X1 + row * TX + 2 * lane) = make_double2(m0, m1);
+          if (STIFF) *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(k0, k1);
         }
       }
     }
+    __syncthreads();
+    if (tid == 0) {
+      // the stage of the previous plane (CG: its own-p values were read after
+      // this plane's barrier was reached by everyone) or of this plane
+      if (MODE != M_CGA || flat > 0) {
+        fence_proxy_async();
+        issue_next();
+      }
+    }
+
+    double wm[RPT], wa[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      wm[i] = 0.0;
+      wa[i] = 0.0;
+    }
+    if (in_grid) {
+      // ---- y-pass: stream the 2P+RPT rows of this warp's column ----
+      const double* x1c = X1 + (rg * RPT) * TX + cxl;
+      const double* x2c = X2 + (rg * RPT) * TX + cxl;
+      if (fast_y_warp) {
+#pragma unroll
+        for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+          const double a1 = x1c[rr * TX];
+          double t = 0.0, u1c = 0.0;
+          if (STIFF) {
+            t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
+            u1c = prm.cy * a1;
+          }
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int k = rr - i;
+            if (k >= 0 && k <= 2 * P) {
+              wm[i] = fma(T::M(k), a1, wm[i]);
+              if (STIFF) {
+                wa[i] = fma(T::M(k), t, wa[i]);
+                wa[i] = fma(T::K(k), u1c, wa[i]);
+              }
+            }
+          }
+        }
+      } else {
+        int cyr[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int gy = gy0 + i;
+          cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
+        }
+#pragma unroll
+        for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+          const double a1 = x1c[rr * TX];
+          double t = 0.0, u1c = 0.0;
+          if (STIFF) {
+            t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
+            u1c = prm.cy * a1;
+          }
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int k = rr - i;
+            if (k >= 0 && k <= 2 * P) {
+              const double my = tabv(1, 0, cyr[i], k);
+              wm[i] = fma(my, a1, wm[i]);
+              if (STIFF) {
+                wa[i] = fma(my, t, wa[i]);
+                wa[i] = fma(tabv(1, 1, cyr[i], k), u1c, wa[i]);
+              }
+            }
+          }
+        }
+      }
+      if (STIFF) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) wm[i] *= prm.cz;
+      }
+    }
+    // ---- z-pass: scatter into the static ring (row z' of the symmetric Mz, Kz),
+    //      and the epilogue of the completed output plane zo = zl - P ----
+    {
+      // CG: own p of this plane (the stage stays intact until the next barrier)
+      const double* pnew = stP + (rg * RPT + P) * HX + cxl + PX;
+      Emitter<MODE, INTERIOR> emitter{prm,
+                                      (long long)(zo + prm.ghost) * prm.pitch_z + gx,
+                                      gx, gy0,
+                                      (MODE == M_RESID && emit) ? cls_of(prm.z_off + zo, prm.nz_glob, ewz) : 0,
+                                      ncy, ncx, ewy, ewx, emit, s_invd, auxv, dsum};
+      const bool zfast_plane = (cz == ewz) && prm.zfast;
+      const double* tzm = s_tab + ((0 * 2 + 0) * NC + cz) * R;
+      const double* tzk = s_tab + ((0 * 2 + 1) * NC + cz) * R;
+      constexpr int S = 2 * P;
+      const int u = j % S;
+      double out[RPT];
+      ring_take_dispatch<P>(u, acc, out);
+      if (in_grid) {
+        constexpr bool STIFF_ = (MODE != M_MASS);
+        // completing output: tap 0;  slot k: tap (k - u) mod S, 0 -> S
+        const double c0m = zfast_plane ? GramTaps<P>::M(0) : tzm[0];
+        const double c0k = zfast_plane ? GramTaps<P>::K(0) : tzk[0];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          out[i] = fma(c0m, STIFF_ ? wa[i] : wm[i], out[i]);
+          if (STIFF_) out[i] = fma(c0k, wm[i], out[i]);
+        }
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          int d = k - u;
+          d = (d < 0) ? d + S : d;
+          d = (d == 0) ? S : d;
+          const double cm = tzm[d];
+          const double ck = STIFF_ ? tzk[d] : 0.0;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            acc[k][i] = fma(cm, STIFF_ ? wa[i] : wm[i], acc[k][i]);
+            if (STIFF_) acc[k][i] = fma(ck, wm[i], acc[k][i]);
+          }
+        }
+      }
+      double pold[RPT];
+      if (MODE == M_CGA) pring_dispatch<P>(j % P, pr, pold, pnew, HX);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) emitter(i, out[i], MODE == M_CGA ? pold[i] : 0.0);
+
+    }
+
+    ++flat;
+  }
+}
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
+               const __grid_constant__ CUtensorMap tm1) {
+  using C = Cfg<P, MODE>;
+  constexpr int NS = C::NS;
+
+  if (MODE == M_CGA) {
+    if (!ld_vol(&prm.state->active)) return;
+  }
+
+  // no static shared memory in this kernel: the dynamic window starts at the
+  // (1 KB aligned) base, so every TMA destination below is 128-byte aligned
+  extern __shared__ __align__(1024) double smem[];
+  double* s_stage = smem;
+  double* s_X = s_stage + NS * C::NA * C::ARR_D;
+  double* s_tab = s_X + 2 * 2 * C::XARR;
+  double* s_invd = s_tab + C::TAB;
+  double* s_red = s_invd + C::INV;
+  unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
+
+  const int tid = threadIdx.x;
+  const int nx = prm.nx, ny = prm.ny;
+  const int ewy = prm.ew[1], ewx = prm.ew[2];
+
+  for (int i = tid; i < C::TAB; i += NT) s_tab[i] = prm.tab[i];
+  if (C::INVD) {
+    const int n = (2 * prm.ew[0] + 1) * (2 * ewy + 1) * (2 * ewx + 1);
+    for (int i = tid; i < n; i += NT) s_invd[i] = prm.invd[i];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&s_bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
+  const int G = gridDim.x;
+  const int tiles_xy = prm.tiles_x * prm.tiles_y;
+
+  int pf_item = blockIdx.x, pf_j = 0;
+  uint32_t pf_flat = 0;
+  // prologue: the first NS planes of the work list (issued by thread 0 via the
+  // same cursor logic as the steady state)
+  if (tid == 0) {
+    for (int s = 0; s < NS && pf_item < prm.nitems; ++s) {
+      const int t = pf_item % tiles_xy;
+      const int ch = pf_item / tiles_xy;
+      const int ix0 = (t % prm.tiles_x) * TX, iy0 = (t / prm.tiles_x) * TY;
+      const int izc0 = ch * prm.chunk_len;
+      const int izc1 = min(izc0 + prm.chunk_len, prm.nz);
+      const int inin = izc1 - izc0 + 2 * P;
+      const int st = pf_flat % NS;
+      const int zb = izc0 - P + pf_j + prm.ghost;
+      mbar_expect_tx(&s_bar[st], C::NA * C::HX * C::HY * 8);
+      tma_load_3d(s_stage + (st * C::NA + 0) * C::ARR_D, &tm0, ix0 - C::PX, iy0 - P, zb, &s_bar[st]);
+      if (C::NA == 2)
+        tma_load_3d(s_stage + (st * C::NA + 1) * C::ARR_D, &tm1, ix0 - C::PX, iy0 - P, zb, &s_bar[st]);
+      ++pf_flat;
+      if (++pf_j == inin) {
+        pf_j = 0;
+        pf_item += G;
+      }
+    }
+  }
+
+  double dsum[3] = {0.0, 0.0, 0.0};
+  uint32_t flat = 0;
+  for (int item = blockIdx.x; item < prm.nitems; item += G) {
+    const int t = item % tiles_xy;
+    const int ch = item / tiles_xy;
+    const int x0 = (t % prm.tiles_x) * TX, y0 = (t / prm.tiles_x) * TY;
+    const int zc0 = ch * prm.chunk_len;
+    const int zc1 = min(zc0 + prm.chunk_len, prm.nz);
+    const bool interior = (x0 - C::PX >= ewx) && (x0 + TX + C::PX <= nx - ewx) &&
+                          (y0 - P >= ewy) && (y0 + TY + P <= ny - ewy);
+    if (interior)
+      run_item<P, MODE, true>(prm, &tm0, &tm1, s_stage, s_X, s_tab, s_invd, s_bar, x0, y0, zc0,
+                              zc1, flat, beta, dsum, pf_item, pf_j, pf_flat);
+    else
+      run_item<P, MODE, false>(prm, &tm0, &tm1, s_stage, s_X, s_tab, s_invd, s_bar, x0, y0, zc0,
+                               zc1, flat, beta, dsum, pf_item, pf_j, pf_flat);
   }
 
   if (MODE == M_CGA) {
@@ -971,6 +1138,7 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
     sp.txm[k] = d.mass_table[2][d.ew[2] * R + k];
     sp.txk[k] = d.stiff_table[2][d.ew[2] * R + k];
   }
+  sp.zfast = (d.nz_global > 1 && d.ew[0] > 0) ? 1 : 0;
   sp.c_mass = d.c_mass;
   sp.cx = d.c_stiff[2];
   sp.cy = d.c_stiff[1];

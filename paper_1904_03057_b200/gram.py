@@ -247,3 +247,28 @@ def degenerate_factor(p: int, kind: str) -> GramFactor:
         table[0, p] = 1.0
     table.setflags(write=False)
     return GramFactor(degree=p, n=1, ew=0, table=table)
+
+
+def taps_header() -> str:
+    """C++ header with the exact interior taps (mass, stiffness) for p=1..5.
+
+    Generated into ``csrc/gram_taps.cuh``; the kernels use them as
+    compile-time constants (folded into the instruction stream / constant
+    bank).  ``tests/test_gram.py`` checks the committed header against
+    ``gram_factor`` so the two cannot drift.
+    """
+    def fn(name, vals):
+        body = " : ".join(f"k == {i} ? {repr(float(v))}" for i, v in enumerate(vals[:-1]))
+        return (f"  __host__ __device__ static constexpr double {name}(int k) {{\n"
+                f"    return {body} : {repr(float(vals[-1]))};\n  }}")
+
+    lines = ["// generated by paper_1904_03057_b200/gram.py:taps_header() -- do not edit",
+             "// exact interior taps G[i, i+k-p], k=0..2p, of the unit-step 1-D Gram",
+             "// factors (mass: int b(x)b(x-k); stiffness: int b'(x)b'(x-k)), p = 1..5",
+             "#pragma once", "", "template <int P> struct GramTaps;"]
+    for p in range(1, MAX_DEGREE + 1):
+        interior_m, _ = _exact_rows(p, 0)
+        interior_k, _ = _exact_rows(p, 1)
+        lines += [f"template <> struct GramTaps<{p}> {{", fn("M", interior_m), fn("K", interior_k),
+                  "};"]
+    return "\n".join(lines) + "\n"

@@ -72,3 +72,17 @@ def test_exact_integral_identities():
     assert product_integral(3, 0, 0, 0, 0) == Fraction(151, 315)
     # grad-grad Gram of linear splines: [-1, 2, -1]
     assert [product_integral(1, 1, k, 1, 0) for k in (-1, 0, 1)] == [-1, 2, -1]
+
+
+def test_taps_header_matches_factors():
+    import os
+
+    from paper_1904_03057_b200.gram import taps_header
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_1904_03057_b200", "csrc", "gram_taps.cuh")
+    assert open(path).read() == taps_header()
+    for p in range(1, 6):
+        assert f"struct GramTaps<{p}>" in taps_header()
+        interior = gram_factor(p, 20, "mass").interior
+        assert repr(float(interior[p])) in taps_header()
