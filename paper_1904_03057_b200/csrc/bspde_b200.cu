@@ -43,18 +43,27 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // configuration
-
-#ifndef BSPDE_NWY
-#define BSPDE_NWY 6
-#endif
-constexpr int NWY = BSPDE_NWY;       // warp row groups
-constexpr int RPT = 4;               // output rows per thread
-constexpr int TX = 64;               // tile width (x): two warps side by side
-constexpr int TY = NWY * RPT;        // tile height (y)
-constexpr int NT = 64 * NWY;         // threads per CTA (one CTA per SM)
-constexpr int NW = NT / 32;          // warps
+//
+// One persistent CTA of 512 threads per SM, warp-specialized:
+//   XY role: warps 0..7 (2 warpgroups) -- TMA consumer, CG p-formation,
+//            x-pass, y-pass; writes (wa, wm) of each plane into a 2-deep FIFO
+//   Z role:  warps 8..15 (2 warpgroups) -- owns the z ring of partial
+//            outputs, runs the epilogue (stores, dot products)
+constexpr int TX = 64;                       // tile width (x)
+constexpr int TY = 24;                       // tile height (y)
+constexpr int NXYW = 8;                      // XY warps
+constexpr int NZW = 8;                       // Z warps
+constexpr int NW = NXYW + NZW;
+constexpr int NT = 32 * NW;                  // 512 threads
+constexpr int NXYT = 32 * NXYW;              // 256 XY threads
+constexpr int RY = TY * TX / NXYT;           // 6 y-pass rows per XY thread (64 cols x 4 x 6)
+constexpr int RZ = TY * TX / (32 * NZW);     // 6 points (rows of one column) per Z thread
+constexpr int XY_REGS = 88;                  // setmaxnreg budgets: 256*88 + 256*168 = 64K
+constexpr int Z_REGS = 168;
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
+static_assert(NXYT == TX * (TY / RY), "XY y-pass mapping");
+static_assert(RZ * 32 * NZW == TX * TY, "Z mapping");
 
 enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
 
@@ -80,10 +89,12 @@ struct Cfg {
   static constexpr int ARR = HX * HY;                        // doubles
   static constexpr int ARR_D = ((ARR * 8 + 127) / 128) * 16; // doubles, 128B-rounded
   static constexpr int XARR = HY * TX;                       // doubles per X array
+  static constexpr int WARR = TY * TX;                       // doubles per W array
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
   static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
+    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + 2 * 2 * WARR + TAB + INV + NW * 4 + 2) +
+           8 * (NS + 4);
   }
 };
 
@@ -110,6 +121,8 @@ struct SepParams {
   double* out;
   const double* aux;
   double aux_scale;
+  const double* cg_r;  // CG pass A: r and p_old (the Z role recomputes p for <p, Ap>)
+  const double* cg_p;
   double* partials;
   unsigned* counter;
   CgState* state;
@@ -150,14 +163,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or the hint expires) instead of re-polling, so waiting
+// warps do not steal issue slots from the working role on the same SMSP.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(addr), "r"(phase)
+      : "r"(addr), "r"(phase), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
@@ -330,14 +346,15 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
 }
 
 // ---------------------------------------------------------------------------
-// the separable streaming kernel
-//
-// CTA = 512 threads, one per SM, persistent over work items (64x32 tile,
-// z-chunk).  Warp w: x-group g = w & 1 (tile columns 32g..32g+31, one per
-// lane) and row group rg = w >> 1 (tile rows 4rg..4rg+3).  For the x-pass (and
-// the CG p-formation) warp w owns whole haloed rows w, w+16, w+32, so those
-// two steps need only __syncwarp; one __syncthreads per plane separates the
-// x-pass from the y-pass (X is double-buffered).
+// the separable streaming kernel (warp-specialized)
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void xy_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NXYT) : "memory");
+}
 
 template <int U, int S>
 struct StaticFor {
@@ -353,182 +370,96 @@ struct StaticFor<S, S> {
   __device__ __forceinline__ static void run(F&) {}
 };
 
-// Epilogue of one completed output point (plane zo, row gy0 + i, column gx).
-template <int MODE, bool INTERIOR>
-struct Emitter {
-  const SepParams& prm;
-  long long pbase;  // (zo + ghost) * pitch_z + gx
-  int gx, gy0, czo, ncy, ncx, ewy, ewx;
-  bool emit;
-  const double* s_invd;
-  const double* auxv;
-  double* dsum;
-  __device__ __forceinline__ void operator()(int i, double v, double pold) const {
-    if (!emit) return;
-    const int y = gy0 + i;
-    if (!(INTERIOR || (y < prm.ny && gx < prm.nx))) return;
-    const long long off = pbase + (long long)y * prm.pitch_y;
-    if (MODE == M_APPLY || MODE == M_CGA) {
-      __stcs(prm.out + off, v);
-      if (MODE == M_CGA) dsum[0] = fma(pold, v, dsum[0]);
-    } else if (MODE == M_MASS) {
-      double o = prm.c_mass * v;
-      if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
-      __stcs(prm.out + off, o);
-    } else {  // M_RESID
-      const double b = auxv[i];
-      const double r = b - v;
-      __stcs(prm.out + off, r);
-      const double inv = s_invd[(czo * ncy + (INTERIOR ? ewy : cls_of(y, prm.ny, ewy))) * ncx +
-                                (INTERIOR ? ewx : cls_of(gx, prm.nx, ewx))];
-      dsum[0] = fma(b, b, dsum[0]);
-      dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
-      dsum[2] = fma(r, r, dsum[2]);
+struct ItemGeom {
+  int x0, y0, zc0, zc1;
+};
+
+__device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
+  const int tiles_xy = prm.tiles_x * prm.tiles_y;
+  const int t = item % tiles_xy;
+  const int ch = item / tiles_xy;
+  ItemGeom g;
+  g.x0 = (t % prm.tiles_x) * TX;
+  g.y0 = (t / prm.tiles_x) * TY;
+  g.zc0 = ch * prm.chunk_len;
+  g.zc1 = min(g.zc0 + prm.chunk_len, prm.nz);
+  return g;
+}
+
+template <int P, int MODE>
+__device__ __forceinline__ bool tile_interior(const SepParams& prm, const ItemGeom& g) {
+  using C = Cfg<P, MODE>;
+  return (g.x0 - C::PX >= prm.ew[2]) && (g.x0 + TX + C::PX <= prm.nx - prm.ew[2]) &&
+         (g.y0 - P >= prm.ew[1]) && (g.y0 + TY + P <= prm.ny - prm.ew[1]);
+}
+
+// TMA producer cursor (thread 0 only): issues the CTA's planes in work order
+template <int P, int MODE>
+struct Producer {
+  int item, j;
+  uint32_t flat;
+  __device__ __forceinline__ void issue(const SepParams& prm, const CUtensorMap* tm0,
+                                        const CUtensorMap* tm1, double* s_stage,
+                                        uint64_t* s_full) {
+    using C = Cfg<P, MODE>;
+    if (item >= prm.nitems) return;
+    const ItemGeom g = item_geom(prm, item);
+    const int nin = g.zc1 - g.zc0 + 2 * P;
+    const int s = flat % C::NS;
+    const int zb = g.zc0 - P + j + prm.ghost;
+    mbar_expect_tx(&s_full[s], C::NA * C::HX * C::HY * 8);
+    tma_load_3d(s_stage + (s * C::NA + 0) * C::ARR_D, tm0, g.x0 - C::PX, g.y0 - P, zb, &s_full[s]);
+    if (C::NA == 2)
+      tma_load_3d(s_stage + (s * C::NA + 1) * C::ARR_D, tm1, g.x0 - C::PX, g.y0 - P, zb,
+                  &s_full[s]);
+    ++flat;
+    if (++j == nin) {
+      j = 0;
+      item += gridDim.x;
     }
   }
 };
 
-// Static-slot z ring.  Output plane o lives in slot o mod 2P for its whole
-// accumulation; at item-local plane j the completing output (zl - P) is in
-// slot u = j mod 2P, which is extracted and reset through a warp-uniform
-// switch (two register moves per point), while every slot k receives the
-// coefficient of its offset d = (k - u) mod 2P from row z' of the symmetric
-// Mz / Kz (d = 0: the newly started output zl + P, i.e. tap 2P).  No slot is
-// ever renamed, so the plane loop needs neither unrolling nor register moves.
-template <int P, int K>
-__device__ __forceinline__ void ring_take(double (&acc)[2 * P][RPT], double (&out)[RPT]) {
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    out[i] = acc[K][i];
-    acc[K][i] = 0.0;
-  }
-}
-
-template <int P>
-__device__ __forceinline__ void ring_take_dispatch(int u, double (&acc)[2 * P][RPT],
-                                                   double (&out)[RPT]) {
-  switch (u) {
-#define BSPDE_TAKE(k) \
-  case k:             \
-    if constexpr (k < 2 * P) ring_take<P, k>(acc, out); \
-    break;
-    BSPDE_TAKE(0) BSPDE_TAKE(1) BSPDE_TAKE(2) BSPDE_TAKE(3) BSPDE_TAKE(4)
-    BSPDE_TAKE(5) BSPDE_TAKE(6) BSPDE_TAKE(7) BSPDE_TAKE(8) BSPDE_TAKE(9)
-#undef BSPDE_TAKE
-    default: break;
-  }
-}
-
-template <int P, int K>
-__device__ __forceinline__ void pring_swap(double (&pr)[P][RPT], double (&pold)[RPT],
-                                           const double* pnew, int stride) {
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    pold[i] = pr[K][i];
-    pr[K][i] = pnew[i * stride];
-  }
-}
-
-template <int P>
-__device__ __forceinline__ void pring_dispatch(int s, double (&pr)[P][RPT], double (&pold)[RPT],
-                                               const double* pnew, int stride) {
-  switch (s) {
-#define BSPDE_PS(k) \
-  case k:           \
-    if constexpr (k < P) pring_swap<P, k>(pr, pold, pnew, stride); \
-    break;
-    BSPDE_PS(0) BSPDE_PS(1) BSPDE_PS(2) BSPDE_PS(3) BSPDE_PS(4)
-#undef BSPDE_PS
-    default: break;
-  }
-}
-
-// Per-item compute: INTERIOR = the haloed tile touches no edge row of x or y
-// and lies inside the grid (no class lookups, no bounds checks).
+// ---- XY role: one work item -------------------------------------------------
 template <int P, int MODE, bool INTERIOR>
-__device__ __forceinline__ void run_item(
-    const SepParams& prm, const CUtensorMap* tm0, const CUtensorMap* tm1, double* s_stage,
-    double* s_X, const double* s_tab, const double* s_invd, uint64_t* s_bar, int x0, int y0,
-    int zc0, int zc1, uint32_t& flat, double beta, double (&dsum)[3],
-    // producer state (thread 0)
-    int& pf_item, int& pf_j, uint32_t& pf_flat) {
+__device__ __forceinline__ void xy_item(const SepParams& prm, const CUtensorMap* tm0,
+                                        const CUtensorMap* tm1, double* s_stage, double* s_X,
+                                        double* s_W, const double* s_tab, const double* s_invd,
+                                        uint64_t* s_full, uint64_t* s_wfull, uint64_t* s_wempty,
+                                        const ItemGeom& g, uint32_t& flat, double beta,
+                                        Producer<P, MODE>& prod) {
   using C = Cfg<P, MODE>;
   using T = GramTaps<P>;
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = warp & 1, rg = warp >> 1;
+  const int xt = threadIdx.x;  // 0..NXYT-1
+  const int lane = xt & 31, xw = xt >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
   const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
-  const int nin = zc1 - zc0 + 2 * P;
-  const int cxl = g * 32 + lane;          // this thread's output column in the tile
-  const int gx = x0 + cxl;                // global column
-  const int gy0 = y0 + rg * RPT;          // first global output row
-  const bool fast_y_warp = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
-
+  const int nin = g.zc1 - g.zc0 + 2 * P;
+  const int yc = xt & (TX - 1);       // y-pass column
+  const int yg = xt >> 6;             // y-pass row group (rows RY*yg ..)
+  const int gy0 = g.y0 + yg * RY;
+  const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RY - 1 < ny - ewy));
   auto tabv = [&](int a, int kind, int c, int k) -> double {
     return s_tab[((a * 2 + kind) * NC + c) * R + k];
   };
-
-  // producer: issue the next plane of this CTA's work list (thread 0)
-  auto issue_next = [&]() {
-    if (pf_item >= prm.nitems) return;
-    const int tiles_xy = prm.tiles_x * prm.tiles_y;
-    const int t = pf_item % tiles_xy;
-    const int ch = pf_item / tiles_xy;
-    const int ix0 = (t % prm.tiles_x) * TX, iy0 = (t / prm.tiles_x) * TY;
-    const int izc0 = ch * prm.chunk_len;
-    const int izc1 = min(izc0 + prm.chunk_len, prm.nz);
-    const int inin = izc1 - izc0 + 2 * P;
-    const int s = pf_flat % NS;
-    const int zb = izc0 - P + pf_j + prm.ghost;
-    mbar_expect_tx(&s_bar[s], NA * HX * HY * 8);
-    tma_load_3d(s_stage + (s * NA + 0) * C::ARR_D, tm0, ix0 - PX, iy0 - P, zb, &s_bar[s]);
-    if (NA == 2) tma_load_3d(s_stage + (s * NA + 1) * C::ARR_D, tm1, ix0 - PX, iy0 - P, zb, &s_bar[s]);
-    ++pf_flat;
-    if (++pf_j == inin) {
-      pf_j = 0;
-      pf_item += gridDim.x;
-    }
-  };
-
-  // z ring (static slots, see zstep) and the CG own-p ring
-  double acc[2 * P][RPT];
-  double pr[P][RPT];
+  double cyK[2 * P + 1];  // cy * Ky interior taps (registers)
 #pragma unroll
-  for (int k = 0; k < 2 * P; ++k)
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[k][i] = 0.0;
-#pragma unroll
-  for (int k = 0; k < P; ++k)
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) pr[k][i] = 0.0;
+  for (int k = 0; k <= 2 * P; ++k) cyK[k] = prm.cy * T::K(k);
 
   for (int j = 0; j < nin; ++j) {
-    const int zl = zc0 - P + j;
+    const int zl = g.zc0 - P + j;
     const int zg = prm.z_off + zl;
     const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
-    const bool emit = (j >= 2 * P);
-    const int zo = zl - P;
     const int s = flat % NS;
-    // epilogue operand prefetch (RESID: b, MASS: f) -- latency hidden by the passes
-    double auxv[RPT];
-    if ((MODE == M_RESID || MODE == M_MASS) && emit) {
-      const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int y = gy0 + i;
-        auxv[i] = 0.0;
-        if ((MODE == M_RESID || prm.aux != nullptr) && (INTERIOR || (y < ny && gx < nx)))
-          auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
-      }
-    }
-    mbar_wait(&s_bar[s], (flat / NS) & 1);
+    const int b = flat & 1;
+    mbar_wait(&s_full[s], (flat / NS) & 1);
     double* stC = s_stage + (s * NA + 0) * C::ARR_D;
     double* stP = s_stage + (s * NA + (NA - 1)) * C::ARR_D;
-    double* X1 = s_X + (flat & 1) * 2 * C::XARR;
+    double* X1 = s_X + b * 2 * C::XARR;
     double* X2 = X1 + C::XARR;
     const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
 
@@ -537,8 +468,8 @@ __device__ __forceinline__ void run_item(
       if (MODE == M_CGA) {
         const double inv0 = s_invd[(cz * ncy + ewy) * ncx + ewx];
 #pragma unroll
-        for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
-          const int row = warp + NW * m;
+        for (int m = 0; m < (HY + NXYW - 1) / NXYW; ++m) {
+          const int row = xw + NXYW * m;
           if (row < HY) {
 #pragma unroll
             for (int h = 0; h < (HX / 2 + 31) / 32; ++h) {
@@ -549,11 +480,17 @@ __device__ __forceinline__ void run_item(
                 const double2 qv = *reinterpret_cast<const double2*>(stP + e);
                 double i0 = inv0, i1 = inv0;
                 if (!INTERIOR || cz != ewz) {
-                  const int gyy = y0 - P + row, gxx = x0 - PX + 2 * q;
+                  // row class is warp-uniform; columns need lookups only near x ends
+                  const int gyy = g.y0 - P + row, gxx = g.x0 - PX + 2 * q;
                   if (gyy >= 0 && gyy < ny) {
                     const double* trow = s_invd + (cz * ncy + cls_of(gyy, ny, ewy)) * ncx;
-                    i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
-                    i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
+                    if (gxx >= ewx && gxx + 1 < nx - ewx) {
+                      i0 = trow[ewx];
+                      i1 = i0;
+                    } else {
+                      i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
+                      i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
+                    }
                   } else {
                     i0 = 0.0;
                     i1 = 0.0;
@@ -570,12 +507,11 @@ __device__ __forceinline__ void run_item(
         __syncwarp();
       }
       // ---- x-pass on this warp's rows: u1 = Mx c, u2 = Kx c ----
-      const double* src = stP;
 #pragma unroll
-      for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
-        const int row = warp + NW * m;
+      for (int m = 0; m < (HY + NXYW - 1) / NXYW; ++m) {
+        const int row = xw + NXYW * m;
         if (row < HY) {
-          const double* w = src + row * HX + 2 * lane;
+          const double* w = stP + row * HX + 2 * lane;
           double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
           for (int k = 0; k < P + 1 + DX; ++k) {
@@ -584,9 +520,8 @@ __device__ __forceinline__ void run_item(
             raw[2 * k + 1] = t.y;
           }
           double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
-          const int gx0 = x0 + 2 * lane;
+          const int gx0 = g.x0 + 2 * lane;
           if (INTERIOR || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
-            // symmetric taps: G[k] = G[2P-k]
 #pragma unroll
             for (int k = 0; k < P; ++k) {
               const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
@@ -618,135 +553,276 @@ __device__ __forceinline__ void run_item(
             }
           }
           *reinterpret_cast<double2*>(X1 + row * TX + 2 * lane) = make_double2(m0, m1);
-          if (STIFF) *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(k0, k1);
+          if (STIFF) {
+            // X2 holds t = c_mass*u1 + cx*u2, the input of the My filter for wa
+            const double t0 = fma(prm.cx, k0, prm.c_mass * m0);
+            const double t1 = fma(prm.cx, k1, prm.c_mass * m1);
+            *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(t0, t1);
+          }
         }
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      // the stage of the previous plane (CG: its own-p values were read after
-      // this plane's barrier was reached by everyone) or of this plane
-      if (MODE != M_CGA || flat > 0) {
-        fence_proxy_async();
-        issue_next();
-      }
+    xy_bar_sync();  // X of this plane complete; the stage is free
+    if (xt == 0) {
+      fence_proxy_async();
+      prod.issue(prm, tm0, tm1, s_stage, s_full);
     }
-
-    double wm[RPT], wa[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      wm[i] = 0.0;
-      wa[i] = 0.0;
-    }
+    // the Z role has drained W[b] (plane flat - 2)
+    mbar_wait(&s_wempty[b], ((flat >> 1) & 1) ^ 1);
+    double* Wa = s_W + b * 2 * C::WARR;
+    double* Wm = Wa + C::WARR;
     if (in_grid) {
-      // ---- y-pass: stream the 2P+RPT rows of this warp's column ----
-      const double* x1c = X1 + (rg * RPT) * TX + cxl;
-      const double* x2c = X2 + (rg * RPT) * TX + cxl;
-      if (fast_y_warp) {
+      // ---- y-pass: RY outputs of column yc, rows RY*yg .. ----
+      double wm[RY], wa[RY];
 #pragma unroll
-        for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+      for (int i = 0; i < RY; ++i) {
+        wm[i] = 0.0;
+        wa[i] = 0.0;
+      }
+      const double* x1c = X1 + (yg * RY) * TX + yc;
+      const double* x2c = X2 + (yg * RY) * TX + yc;
+      int cyr[RY];
+      if (!fast_y) {
+#pragma unroll
+        for (int i = 0; i < RY; ++i) {
+          const int gy = gy0 + i;
+          cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
+        }
+      }
+      if (fast_y) {
+#pragma unroll
+        for (int rr = 0; rr < RY + 2 * P; ++rr) {
           const double a1 = x1c[rr * TX];
-          double t = 0.0, u1c = 0.0;
-          if (STIFF) {
-            t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
-            u1c = prm.cy * a1;
-          }
+          const double t = STIFF ? x2c[rr * TX] : 0.0;
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
+          for (int i = 0; i < RY; ++i) {
             const int k = rr - i;
             if (k >= 0 && k <= 2 * P) {
               wm[i] = fma(T::M(k), a1, wm[i]);
               if (STIFF) {
                 wa[i] = fma(T::M(k), t, wa[i]);
-                wa[i] = fma(T::K(k), u1c, wa[i]);
+                wa[i] = fma(cyK[k], a1, wa[i]);
               }
             }
           }
         }
       } else {
-        int cyr[RPT];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const int gy = gy0 + i;
-          cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
-        }
-#pragma unroll
-        for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+        for (int rr = 0; rr < RY + 2 * P; ++rr) {
           const double a1 = x1c[rr * TX];
-          double t = 0.0, u1c = 0.0;
-          if (STIFF) {
-            t = fma(prm.cx, x2c[rr * TX], prm.c_mass * a1);
-            u1c = prm.cy * a1;
-          }
+          const double t = STIFF ? x2c[rr * TX] : 0.0;
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
+          for (int i = 0; i < RY; ++i) {
             const int k = rr - i;
             if (k >= 0 && k <= 2 * P) {
               const double my = tabv(1, 0, cyr[i], k);
               wm[i] = fma(my, a1, wm[i]);
               if (STIFF) {
                 wa[i] = fma(my, t, wa[i]);
-                wa[i] = fma(tabv(1, 1, cyr[i], k), u1c, wa[i]);
+                wa[i] = fma(prm.cy * tabv(1, 1, cyr[i], k), a1, wa[i]);
               }
             }
           }
         }
       }
-      if (STIFF) {
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) wm[i] *= prm.cz;
-      }
-    }
-    // ---- z-pass: scatter into the static ring (row z' of the symmetric Mz, Kz),
-    //      and the epilogue of the completed output plane zo = zl - P ----
-    {
-      // CG: own p of this plane (the stage stays intact until the next barrier)
-      const double* pnew = stP + (rg * RPT + P) * HX + cxl + PX;
-      Emitter<MODE, INTERIOR> emitter{prm,
-                                      (long long)(zo + prm.ghost) * prm.pitch_z + gx,
-                                      gx, gy0,
-                                      (MODE == M_RESID && emit) ? cls_of(prm.z_off + zo, prm.nz_glob, ewz) : 0,
-                                      ncy, ncx, ewy, ewx, emit, s_invd, auxv, dsum};
-      const bool zfast_plane = (cz == ewz) && prm.zfast;
-      const double* tzm = s_tab + ((0 * 2 + 0) * NC + cz) * R;
-      const double* tzk = s_tab + ((0 * 2 + 1) * NC + cz) * R;
-      constexpr int S = 2 * P;
-      const int u = j % S;
-      double out[RPT];
-      ring_take_dispatch<P>(u, acc, out);
-      if (in_grid) {
-        constexpr bool STIFF_ = (MODE != M_MASS);
-        // completing output: tap 0;  slot k: tap (k - u) mod S, 0 -> S
-        const double c0m = zfast_plane ? GramTaps<P>::M(0) : tzm[0];
-        const double c0k = zfast_plane ? GramTaps<P>::K(0) : tzk[0];
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          out[i] = fma(c0m, STIFF_ ? wa[i] : wm[i], out[i]);
-          if (STIFF_) out[i] = fma(c0k, wm[i], out[i]);
-        }
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-          int d = k - u;
-          d = (d < 0) ? d + S : d;
-          d = (d == 0) ? S : d;
-          const double cm = tzm[d];
-          const double ck = STIFF_ ? tzk[d] : 0.0;
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            acc[k][i] = fma(cm, STIFF_ ? wa[i] : wm[i], acc[k][i]);
-            if (STIFF_) acc[k][i] = fma(ck, wm[i], acc[k][i]);
-          }
+      for (int i = 0; i < RY; ++i) {
+        const int o = (yg * RY + i) * TX + yc;
+        if (STIFF) {
+          Wa[o] = wa[i];
+          Wm[o] = wm[i];
+        } else {
+          Wm[o] = wm[i];
         }
       }
-      double pold[RPT];
-      if (MODE == M_CGA) pring_dispatch<P>(j % P, pr, pold, pnew, HX);
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) emitter(i, out[i], MODE == M_CGA ? pold[i] : 0.0);
-
     }
-
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_wfull[b]);
     ++flat;
   }
+}
+
+// ---- Z role: one work item --------------------------------------------------
+// Output plane o lives in ring slot o mod 2P for its whole accumulation; at
+// item-local plane j (U = j mod 2P, compile-time: the plane loop is unrolled by
+// 2P through template recursion) the completing output zl-P is in slot U and
+// the new output zl+P takes it over.  Each slot gets tap (k - U) mod 2P of row
+// z' of the symmetric Mz / Kz (tap 2P for slot U).  No slot is ever renamed,
+// so the ring costs no register moves.
+struct ZCtx {
+  const SepParams* prm;
+  const double* s_W;
+  const double* s_tab;
+  const double* s_invd;
+  uint64_t* s_wfull;
+  uint64_t* s_wempty;
+  int x0, y0, zc0, nin, gx, gyb, zc, zrb, lane;
+  double beta;
+  double czK[2 * MAXP + 1];  // cz * Kz interior taps
+};
+
+template <int P, int MODE, bool INTERIOR, int U>
+__device__ __forceinline__ void z_plane(const ZCtx& c, double (&acc)[2 * P][RZ], int jb,
+                                        uint32_t& flat, double (&dsum)[3]) {
+  using C = Cfg<P, MODE>;
+  using T = GramTaps<P>;
+  constexpr int R = C::R, NC = C::NC, S = 2 * P;
+  constexpr bool STIFF = C::STIFF;
+  const int j = jb + U;
+  if (j >= c.nin) return;
+  const SepParams& prm = *c.prm;
+  const int nx = prm.nx, ny = prm.ny;
+  const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
+  const bool xok = INTERIOR || c.gx < nx;
+  const int zl = c.zc0 - P + j;
+  const int zg = prm.z_off + zl;
+  const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
+  const bool emit = (j >= 2 * P);
+  const int zo = zl - P;
+  const int b = flat & 1;
+  const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z + c.gx;
+  // epilogue operands of plane zo, in flight during the wait and the ring math
+  double a0[RZ], a1[RZ];
+#pragma unroll
+  for (int i = 0; i < RZ; ++i) {
+    a0[i] = 0.0;
+    a1[i] = 0.0;
+  }
+  if (emit && (MODE == M_RESID || MODE == M_CGA || (MODE == M_MASS && prm.aux != nullptr))) {
+    const double* src0 = (MODE == M_CGA) ? prm.cg_r : prm.aux;
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) {
+      const int y = c.gyb + i;
+      if (xok && (INTERIOR || y < ny)) {
+        const long long off = pbase + (long long)y * prm.pitch_y;
+        a0[i] = __ldcs(src0 + off);
+        if (MODE == M_CGA) a1[i] = __ldcs(prm.cg_p + off);
+      }
+    }
+  }
+  mbar_wait(&c.s_wfull[b], (flat >> 1) & 1);
+  const double* Wa = c.s_W + b * 2 * C::WARR + (c.zrb * RZ) * TX + c.zc;
+  const double* Wm = Wa + C::WARR;
+  const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
+  const bool zfast = (cz == ewz) && prm.zfast;
+  const double* tzm = c.s_tab + ((0 * 2 + 0) * NC + cz) * R;
+  const double* tzk = c.s_tab + ((0 * 2 + 1) * NC + cz) * R;
+  const double czs = prm.cz;
+  double out[RZ];
+  if (in_grid) {
+    double wa[RZ], wm[RZ];
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) {
+      wm[i] = Wm[i * TX];
+      wa[i] = STIFF ? Wa[i * TX] : wm[i];
+    }
+#pragma unroll
+    for (int k = 0; k <= S; ++k) {
+      const double cm = zfast ? T::M(k) : tzm[k];
+      const double ck = STIFF ? (zfast ? c.czK[k] : czs * tzk[k]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < RZ; ++i) {
+        if (k == 0) {
+          double o = fma(cm, wa[i], acc[U][i]);
+          if (STIFF) o = fma(ck, wm[i], o);
+          out[i] = o;
+        } else if (k == S) {
+          double n = cm * wa[i];
+          if (STIFF) n = fma(ck, wm[i], n);
+          acc[U][i] = n;
+        } else {
+          double v = fma(cm, wa[i], acc[(U + k) % S][i]);
+          if (STIFF) v = fma(ck, wm[i], v);
+          acc[(U + k) % S][i] = v;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) {
+      out[i] = acc[U][i];
+      acc[U][i] = 0.0;
+    }
+  }
+  __syncwarp();
+  if (c.lane == 0) mbar_arrive(&c.s_wempty[b]);
+  // ---- epilogue: output plane zo ----
+  if (emit) {
+    const int czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
+    const double inv_int = (C::INVD) ? c.s_invd[(czo * ncy + ewy) * ncx + ewx] : 0.0;
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) {
+      const int y = c.gyb + i;
+      if (xok && (INTERIOR || y < ny)) {
+        const long long off = pbase + (long long)y * prm.pitch_y;
+        const double v = out[i];
+        double inv = inv_int;
+        if (C::INVD && !INTERIOR)
+          inv = c.s_invd[(czo * ncy + cls_of(y, ny, ewy)) * ncx + cls_of(c.gx, nx, ewx)];
+        if (MODE == M_APPLY) {
+          __stcs(prm.out + off, v);
+        } else if (MODE == M_CGA) {
+          __stcs(prm.out + off, v);
+          dsum[0] = fma(pdir(a0[i], inv, a1[i], c.beta), v, dsum[0]);
+        } else if (MODE == M_MASS) {
+          double o = prm.c_mass * v;
+          if (prm.aux) o = fma(prm.aux_scale, a0[i], o);
+          __stcs(prm.out + off, o);
+        } else {  // M_RESID
+          const double bb = a0[i];
+          const double r = bb - v;
+          __stcs(prm.out + off, r);
+          dsum[0] = fma(bb, bb, dsum[0]);
+          dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
+          dsum[2] = fma(r, r, dsum[2]);
+        }
+      }
+    }
+  }
+  ++flat;
+}
+
+template <int P, int MODE, bool INTERIOR, int U>
+__device__ __forceinline__ void z_planes(const ZCtx& c, double (&acc)[2 * P][RZ], int jb,
+                                         uint32_t& flat, double (&dsum)[3]) {
+  if constexpr (U < 2 * P) {
+    z_plane<P, MODE, INTERIOR, U>(c, acc, jb, flat, dsum);
+    z_planes<P, MODE, INTERIOR, U + 1>(c, acc, jb, flat, dsum);
+  }
+}
+
+template <int P, int MODE, bool INTERIOR>
+__device__ __forceinline__ void z_item(const SepParams& prm, const double* s_W,
+                                       const double* s_tab, const double* s_invd,
+                                       uint64_t* s_wfull, uint64_t* s_wempty, const ItemGeom& g,
+                                       uint32_t& flat, double beta, double (&dsum)[3]) {
+  const int zt = threadIdx.x - NXYT;
+  ZCtx c;
+  c.prm = &prm;
+  c.s_W = s_W;
+  c.s_tab = s_tab;
+  c.s_invd = s_invd;
+  c.s_wfull = s_wfull;
+  c.s_wempty = s_wempty;
+  c.x0 = g.x0;
+  c.y0 = g.y0;
+  c.zc0 = g.zc0;
+  c.nin = g.zc1 - g.zc0 + 2 * P;
+  c.zc = zt & (TX - 1);
+  c.zrb = zt >> 6;
+  c.gx = g.x0 + c.zc;
+  c.gyb = g.y0 + c.zrb * RZ;
+  c.lane = zt & 31;
+  c.beta = beta;
+#pragma unroll
+  for (int k = 0; k <= 2 * P; ++k) c.czK[k] = prm.cz * GramTaps<P>::K(k);
+  double acc[2 * P][RZ];
+#pragma unroll
+  for (int k = 0; k < 2 * P; ++k)
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) acc[k][i] = 0.0;
+  for (int jb = 0; jb < c.nin; jb += 2 * P) z_planes<P, MODE, INTERIOR, 0>(c, acc, jb, flat, dsum);
 }
 
 template <int P, int MODE>
@@ -765,73 +841,58 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) double smem[];
   double* s_stage = smem;
   double* s_X = s_stage + NS * C::NA * C::ARR_D;
-  double* s_tab = s_X + 2 * 2 * C::XARR;
+  double* s_W = s_X + 2 * 2 * C::XARR;
+  double* s_tab = s_W + 2 * 2 * C::WARR;
   double* s_invd = s_tab + C::TAB;
   double* s_red = s_invd + C::INV;
   unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
+  uint64_t* s_wfull = s_full + NS;
+  uint64_t* s_wempty = s_wfull + 2;
 
   const int tid = threadIdx.x;
-  const int nx = prm.nx, ny = prm.ny;
-  const int ewy = prm.ew[1], ewx = prm.ew[2];
-
   for (int i = tid; i < C::TAB; i += NT) s_tab[i] = prm.tab[i];
   if (C::INVD) {
-    const int n = (2 * prm.ew[0] + 1) * (2 * ewy + 1) * (2 * ewx + 1);
+    const int n = (2 * prm.ew[0] + 1) * (2 * prm.ew[1] + 1) * (2 * prm.ew[2] + 1);
     for (int i = tid; i < n; i += NT) s_invd[i] = prm.invd[i];
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&s_bar[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&s_full[s], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_wfull[b], NXYW);
+      mbar_init(&s_wempty[b], NZW);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
   const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
-  const int G = gridDim.x;
-  const int tiles_xy = prm.tiles_x * prm.tiles_y;
-
-  int pf_item = blockIdx.x, pf_j = 0;
-  uint32_t pf_flat = 0;
-  // prologue: the first NS planes of the work list (issued by thread 0 via the
-  // same cursor logic as the steady state)
-  if (tid == 0) {
-    for (int s = 0; s < NS && pf_item < prm.nitems; ++s) {
-      const int t = pf_item % tiles_xy;
-      const int ch = pf_item / tiles_xy;
-      const int ix0 = (t % prm.tiles_x) * TX, iy0 = (t / prm.tiles_x) * TY;
-      const int izc0 = ch * prm.chunk_len;
-      const int izc1 = min(izc0 + prm.chunk_len, prm.nz);
-      const int inin = izc1 - izc0 + 2 * P;
-      const int st = pf_flat % NS;
-      const int zb = izc0 - P + pf_j + prm.ghost;
-      mbar_expect_tx(&s_bar[st], C::NA * C::HX * C::HY * 8);
-      tma_load_3d(s_stage + (st * C::NA + 0) * C::ARR_D, &tm0, ix0 - C::PX, iy0 - P, zb, &s_bar[st]);
-      if (C::NA == 2)
-        tma_load_3d(s_stage + (st * C::NA + 1) * C::ARR_D, &tm1, ix0 - C::PX, iy0 - P, zb, &s_bar[st]);
-      ++pf_flat;
-      if (++pf_j == inin) {
-        pf_j = 0;
-        pf_item += G;
-      }
-    }
-  }
-
   double dsum[3] = {0.0, 0.0, 0.0};
+  const int warp = tid >> 5;
   uint32_t flat = 0;
-  for (int item = blockIdx.x; item < prm.nitems; item += G) {
-    const int t = item % tiles_xy;
-    const int ch = item / tiles_xy;
-    const int x0 = (t % prm.tiles_x) * TX, y0 = (t / prm.tiles_x) * TY;
-    const int zc0 = ch * prm.chunk_len;
-    const int zc1 = min(zc0 + prm.chunk_len, prm.nz);
-    const bool interior = (x0 - C::PX >= ewx) && (x0 + TX + C::PX <= nx - ewx) &&
-                          (y0 - P >= ewy) && (y0 + TY + P <= ny - ewy);
-    if (interior)
-      run_item<P, MODE, true>(prm, &tm0, &tm1, s_stage, s_X, s_tab, s_invd, s_bar, x0, y0, zc0,
-                              zc1, flat, beta, dsum, pf_item, pf_j, pf_flat);
-    else
-      run_item<P, MODE, false>(prm, &tm0, &tm1, s_stage, s_X, s_tab, s_invd, s_bar, x0, y0, zc0,
-                               zc1, flat, beta, dsum, pf_item, pf_j, pf_flat);
+  if (warp < NXYW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(XY_REGS));
+    Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
+    if (tid == 0) {
+      for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, s_stage, s_full);
+    }
+    for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
+      const ItemGeom g = item_geom(prm, item);
+      if (tile_interior<P, MODE>(prm, g))
+        xy_item<P, MODE, true>(prm, &tm0, &tm1, s_stage, s_X, s_W, s_tab, s_invd, s_full,
+                               s_wfull, s_wempty, g, flat, beta, prod);
+      else
+        xy_item<P, MODE, false>(prm, &tm0, &tm1, s_stage, s_X, s_W, s_tab, s_invd, s_full,
+                                s_wfull, s_wempty, g, flat, beta, prod);
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(128));
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Z_REGS));
+    for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
+      const ItemGeom g = item_geom(prm, item);
+      z_item<P, MODE, false>(prm, s_W, s_tab, s_invd, s_wfull, s_wempty, g, flat, beta, dsum);
+    }
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(128));
   }
 
   if (MODE == M_CGA) {
@@ -1148,6 +1209,8 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
   sp.out = nullptr;
   sp.aux = nullptr;
   sp.aux_scale = 0.0;
+  sp.cg_r = nullptr;
+  sp.cg_p = nullptr;
   sp.partials = nullptr;
   sp.counter = nullptr;
   sp.state = nullptr;
@@ -1179,6 +1242,8 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.out = out;
   sp.aux = aux;
   sp.aux_scale = aux_scale;
+  sp.cg_r = (mode == M_CGA) ? in0 : nullptr;
+  sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
   if (use_override) sp.c_mass = c_mass_override;
   if (scratch) {
     sp.state = scratch_state(scratch);
