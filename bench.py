@@ -31,6 +31,13 @@ sys.path.insert(0, ROOT)
 ALG_BYTES_PASS_A = 24  # read r, p_old; write Ap              (per DoF)
 ALG_BYTES_PASS_B = 56  # read x, r, p_old, Ap; write x, r, p  (per DoF)
 ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B
+# ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
+# filled from the committed profile summary when present
+TRAFFIC = {}
+_tp = os.path.join(ROOT, "profiles", "traffic.json")
+if os.path.exists(_tp):
+    with open(_tp) as _f:
+        TRAFFIC = json.load(_f)
 
 
 def measured_peaks():
@@ -163,72 +170,102 @@ def config_of(args, world):
 
 def run_ours(args, rank, world, local_rank):
     import torch
+    import torch.distributed as dist
 
     from paper_1904_03057_b200 import SolveConfig, make_operator
+    from paper_1904_03057_b200.distributed import DistributedOperator
     from paper_1904_03057_b200.domain import Grid
     from paper_1904_03057_b200.heat import HeatSolver
     from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
     from paper_1904_03057_b200.system import heat_system
 
-    if world > 1:
-        raise SystemExit("multi-GPU bench path: see paper_1904_03057_b200.distributed")
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     p = 3
     N, h, dt = heat_c_inputs(args.ncoef, p)
-    g = Grid((N,) * 3, (h,) * 3)
-    data = heat_system(g, p, dt)
-    op = make_operator(data, "b200", device=local_rank)
-    lay = op.layout
+    data = heat_system(Grid((N,) * 3, (h,) * 3), p, dt)
+    dofs = int(np.prod(data.cext))
+    cfg = SolveConfig(tol=1e-10, max_iter=5000, poll_every=args.poll)
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        op = make_operator(data, "b200", device=local_rank)
+        lay = op.layout
+        z_range = None
+    else:
+        op = DistributedOperator(data)
+        lay = op.layout
+        z_range = op.part.bounds()
     u = lay.alloc(dev)
     q = lay.alloc(dev)
-    gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, **IC)
-    gaussian_coeffs(N, h, p, device=dev, out=q, layout=lay, **SOURCE)
+    gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, z_range=z_range, **IC)
+    gaussian_coeffs(N, h, p, device=dev, out=q, layout=lay, z_range=z_range, **SOURCE)
     F = lay.alloc(dev)
     op.mass_apply_device(q, F)
     del q
     u0 = u.clone()
-    cfg = SolveConfig(tol=1e-10, max_iter=5000, poll_every=args.poll)
-    hs = HeatSolver.from_device(op, dt, u, F, cfg)
-    dofs = int(np.prod(data.cext))
-    stream = torch.cuda.current_stream()
+    if world == 1:
+        hs = HeatSolver.from_device(op, dt, u, F, cfg)
+        step = hs.step
+    else:
+        b = lay.alloc(dev)
+
+        def step():
+            op.mass_apply_device(u, b, F, a=dt)
+            return op.pcg_device(b, u, cfg, has_x0=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
-        hs.step()
-    torch.cuda.synchronize()
+        step()
+    barrier()
     plan = op.plan()
     launches0 = plan.launches
     clk = ClockSampler(local_rank)
     clk.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     ev0.record(stream)
     its = []
     for _ in range(args.steps):
-        its.append(hs.step().iterations)
+        its.append(step().iterations)
     ev1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = plan.launches - launches0
     total_its = int(sum(its))
     value = total_its * dofs / (ms * 1e-3) / 1e9
 
     # -- per-kernel durations (CUDA events on the launching stream) --
-    kt = kernel_times(op, hs, stream)
+    kt = kernel_times(op, u, F, dt, stream, world)
+    kt = {k: max_over_ranks(v) for k, v in kt.items()}
     peak, peak_kind = measured_peaks()
-    a_gbs = ALG_BYTES_PASS_A * dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
-    b_gbs = ALG_BYTES_PASS_B * dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
+    local_dofs = int(np.prod(lay.owned_shape))
+    a_gbs = ALG_BYTES_PASS_A * local_dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
+    b_gbs = ALG_BYTES_PASS_B * local_dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
     dom = "pass_b" if kt["pass_b_ms"] >= kt["pass_a_ms"] else "pass_a"
     ach = b_gbs if dom == "pass_b" else a_gbs
-    it_gbs = ALG_BYTES_ITER * dofs / ((kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3) / 1e9
+    it_gbs = ALG_BYTES_ITER * local_dofs / ((kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3) / 1e9
 
-    # -- end to end through the host API: u from/to pinned host memory each step --
-    e2e = e2e_rate(hs, u0, lay, dofs, min(args.steps, 3), stream)
+    # -- end to end through the public API: u from/to pinned host memory each step --
+    e2e = e2e_rate(step, u, u0, lay, dofs, min(args.steps, 3), stream, barrier, max_over_ranks)
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         rate, info = cpu_port_rate(64, iters=20, repeats=3)
         cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
                "sample": f"C1 64^3 p=3 heat system, {info['iterations']} Jacobi-PCG iterations, "
@@ -241,7 +278,7 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic", "config": config_of(args, world),
         "cg_iterations_per_step": its,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "traffic": None, "kernel": dom,
+                     "frac": ach / peak, "traffic": TRAFFIC.get(dom), "kernel": dom,
                      "peak_source": peak_kind,
                      "alg_bytes_per_dof": ALG_BYTES_PASS_B if dom == "pass_b" else ALG_BYTES_PASS_A,
                      "pass_a_ms": kt["pass_a_ms"], "pass_b_ms": kt["pass_b_ms"],
@@ -252,56 +289,70 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
-def kernel_times(op, hs, stream, reps=5):
-    """Average device duration of CG pass A and pass B (same stream, events)."""
+def kernel_times(op, u, F, dt, stream, world, reps=5):
+    """Average device duration of CG pass A and pass B (same stream, events),
+    on a copy of the current state (the timed solve is already over)."""
     import torch
 
-    from paper_1904_03057_b200.solver import _work
-
     plan = op.plan()
-    w = _work(op, hs.config.max_iter)
-    hs.rhs()
-    plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
-    plan.cg_residual(hs.b, hs.u, w.r, w.scratch, 1)
+    lay = op.layout
+    dev = u.device
+    x = u.clone()
+    b = lay.alloc(dev)
+    r = lay.alloc(dev)
+    pp = lay.alloc(dev)
+    ap = lay.alloc(dev)
+    scratch = plan.scratch()
+    op.mass_apply_device(x, b, F, a=dt)
+    plan.cg_setup(scratch, None, 1e-300, 10 ** 6, False, True)
+    plan.cg_residual(b, x, r, scratch, 1)
     ta, tb = [], []
     for _ in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        plan.cg_pass_a(w.r, w.p, w.ap, w.scratch, 1)
+        plan.cg_pass_a(r, pp, ap, scratch, 1)
         e[1].record(stream)
-        plan.cg_pass_b(hs.u, w.r, w.p, w.ap, w.scratch, 1)
+        plan.cg_pass_b(x, r, pp, ap, scratch, 1)
         e[2].record(stream)
         torch.cuda.synchronize()
         ta.append(e[0].elapsed_time(e[1]))
         tb.append(e[1].elapsed_time(e[2]))
+    del x, b, r, pp, ap
+    torch.cuda.empty_cache()
     return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:]))}
 
 
-def e2e_rate(hs, u0, lay, dofs, steps, stream):
+def e2e_rate(step, u, u0, lay, dofs, steps, stream, barrier, max_over_ranks):
+    """Same metric through the public step API with the state copied from and
+    back to pinned host memory every step (host<->device copies timed)."""
     import torch
 
     host = torch.empty(lay.owned_shape, dtype=torch.float64).pin_memory()
     host.copy_(lay.owned(u0).cpu())
-    own = lay.owned(hs.u)
-    torch.cuda.synchronize()
+    own = lay.owned(u)
+    barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     its = 0
     for _ in range(steps):
         own.copy_(host, non_blocking=True)
-        its += hs.step().iterations
+        its += step().iterations
         host.copy_(own, non_blocking=True)
     ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    nbytes = dofs * 8
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    nbytes = int(np.prod(lay.owned_shape)) * 8
     return {"value": its * dofs / (ms * 1e-3) / 1e9, "unit": "GDoF/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-            "steps": steps, "api": "HeatSolver.step with u copied from/to pinned host memory"}
+            "steps": steps, "api": "heat step (public API) with u copied from/to pinned host memory"}
 
 
 def main():

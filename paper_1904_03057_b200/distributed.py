@@ -1,0 +1,279 @@
+"""Multi-GPU z-slab execution: one process per GPU, NCCL over NVLink/NVSwitch.
+
+The global extended grid is split along axis 0 ("z", the slowest axis) into
+contiguous slabs, one per rank (``SlabPartition``).  Each rank stores its
+slab in the ghosted layout of ``device.SlabLayout`` with ``ghost = p`` planes
+per side; the kernels read ghosts and write only owned planes.
+
+Per CG iteration (``distributed_pcg``):
+
+  1. halo exchange of r and p_old: the first/last p owned planes go to the
+     lower/upper neighbour's ghost planes (contiguous memory: one send + one
+     recv per side, ``torch.distributed.batch_isend_irecv`` over NCCL);
+  2. pass A (fuse=0) writes the local <p, Ap>; ``all_reduce`` of 1 double;
+     the 1-thread finalize kernel runs the scalar update on every rank;
+  3. pass B (fuse=0) writes local <r, D^-1 r>, <r, r>; ``all_reduce`` of 2
+     doubles; finalize.
+
+Every rank holds identical scalar state, so the device-side ``active`` flag
+(stop rule, guards) agrees everywhere; the host polls it every
+``poll_every`` iterations.  Iterations after convergence are no-ops.  There
+is no collective on the data path other than the halo planes and the scalar
+sums.
+
+The orchestration is written against a small ops interface so it can be
+exercised on CPU with the gloo backend (tests/test_distributed_cpu.py); the
+product implementation is ``NativeSlabOps`` (the sm_100a kernels).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigurationError, ValidationError
+from .solver import SolveConfig, report_from
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """Balanced split of ``nz_global`` planes over ``world`` ranks."""
+
+    nz_global: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        if not 0 <= self.rank < self.world:
+            raise ValidationError(f"rank {self.rank} not in [0, {self.world})")
+        if self.nz_global < self.world:
+            raise ConfigurationError(
+                f"{self.nz_global} z planes cannot be split over {self.world} ranks")
+
+    def bounds(self, rank=None):
+        r = self.rank if rank is None else rank
+        base, extra = divmod(self.nz_global, self.world)
+        lo = r * base + min(r, extra)
+        return lo, lo + base + (1 if r < extra else 0)
+
+    @property
+    def z_offset(self):
+        return self.bounds()[0]
+
+    @property
+    def nz(self):
+        lo, hi = self.bounds()
+        return hi - lo
+
+    def check_min(self, planes):
+        for r in range(self.world):
+            lo, hi = self.bounds(r)
+            if hi - lo < planes:
+                raise ConfigurationError(
+                    f"rank {r} owns {hi - lo} z planes < {planes} (degree); use fewer ranks")
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class HaloExchanger:
+    """Fills the ghost planes of a slab buffer from the neighbouring ranks."""
+
+    def __init__(self, layout, rank, world, group=None):
+        self.layout = layout
+        self.rank = rank
+        self.world = world
+        self.group = group
+
+    def __call__(self, buf):
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+
+        g, nz = self.layout.ghost, self.layout.nz
+        ops = []
+        if self.rank > 0:  # lower neighbour: my first g planes <-> its top ghosts
+            ops.append(dist.P2POp(dist.isend, buf[g:2 * g], self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[0:g], self.rank - 1, self.group))
+        if self.rank < self.world - 1:  # upper neighbour
+            ops.append(dist.P2POp(dist.isend, buf[nz:nz + g], self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[nz + g:nz + 2 * g], self.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+def _allreduce_fn(world, group=None):
+    if world == 1:
+        return lambda t: None
+    import torch.distributed as dist
+
+    def fn(t):
+        dist.all_reduce(t, group=group)
+
+    return fn
+
+
+class NativeSlabOps:
+    """Step-wise CG through the C ABI on one rank's slab (fuse = 0)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def sums(self, scratch, n):
+        return scratch[: 8 * 4].view(_torch().float64)[:n]
+
+    def setup(self, scratch, history, cfg, has_x0):
+        self.plan.cg_setup(scratch, history, cfg.tol, cfg.max_iter, cfg.record_history, has_x0)
+
+    def residual(self, b, x, r, scratch):
+        self.plan.cg_residual(b, x, r, scratch, 0)
+
+    def pass_a(self, r, p, ap, scratch):
+        self.plan.cg_pass_a(r, p, ap, scratch, 0)
+
+    def pass_b(self, x, r, p, ap, scratch):
+        self.plan.cg_pass_b(x, r, p, ap, scratch, 0)
+
+    def finalize(self, scratch, kind):
+        self.plan.cg_finalize(scratch, kind)
+
+    def read(self, scratch):
+        return self.plan.cg_read(scratch)
+
+
+def distributed_pcg(ops, halo, allreduce, b, x, r, p, ap, scratch, config: SolveConfig,
+                    has_x0=True, history=None):
+    """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg)."""
+    t0 = time.perf_counter()
+    if not has_x0:
+        x.zero_()
+    p.zero_()
+    ops.setup(scratch, history, config, has_x0)
+    halo(x)
+    ops.residual(b, x, r, scratch)
+    allreduce(ops.sums(scratch, 3))
+    ops.finalize(scratch, 0)
+    rep, active = ops.read(scratch)
+    K = max(1, int(config.poll_every))
+    while active:
+        for _ in range(K):
+            halo(r)
+            halo(p)
+            ops.pass_a(r, p, ap, scratch)
+            allreduce(ops.sums(scratch, 1))
+            ops.finalize(scratch, 1)
+            ops.pass_b(x, r, p, ap, scratch)
+            allreduce(ops.sums(scratch, 2))
+            ops.finalize(scratch, 2)
+        rep, active = ops.read(scratch)
+    return rep, time.perf_counter() - t0
+
+
+class DistributedOperator:
+    """This rank's slab of a b200 operator (constant-coefficient box system).
+
+    ``pcg_device`` / ``apply_device`` take ghosted-slab tensors of this rank;
+    ``scatter`` / ``gather`` move reference-shaped host arrays in and out.
+    """
+
+    strategy = "b200-zslab"
+
+    def __init__(self, data, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        from .device import NativePlan, SlabLayout, require_cuda
+
+        self.data = data
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = require_cuda(device)
+        nzg, ny, nx = data.dims3
+        self.part = SlabPartition(nzg, self.world, self.rank)
+        self.part.check_min(data.n_b)
+        self.layout = SlabLayout(self.part.nz, ny, nx, ghost=data.n_b,
+                                 z_offset=self.part.z_offset, nz_global=nzg)
+        self._plans = {}
+        self.halo = HaloExchanger(self.layout, self.rank, self.world, group)
+        self.allreduce = _allreduce_fn(self.world, group)
+        self._work = None
+        torch.cuda.set_device(self.device)
+
+    def plan(self, precond="jacobi"):
+        from .device import NativePlan
+
+        if precond not in self._plans:
+            self._plans[precond] = NativePlan(self.data, self.layout, self.device, precond)
+        return self._plans[precond]
+
+    # -- data movement ---------------------------------------------------
+    def scatter(self, full):
+        """Reference-shaped host array -> this rank's ghosted slab (device)."""
+        full = np.asarray(full, dtype=np.float64).reshape(self.data.dims3)
+        lo, hi = self.part.bounds()
+        return self.layout.upload(full[lo:hi], self.device)
+
+    def gather(self, buf):
+        """All ranks' owned planes -> full array on every rank (host)."""
+        import torch
+        import torch.distributed as dist
+
+        own = self.layout.owned(buf).contiguous()
+        if self.world == 1:
+            return own.cpu().numpy().reshape(self.data.cext)
+        sizes = [self.part.bounds(r) for r in range(self.world)]
+        maxz = max(hi - lo for lo, hi in sizes)
+        pad = torch.zeros((maxz,) + tuple(own.shape[1:]), dtype=own.dtype, device=own.device)
+        pad[: own.shape[0]] = own
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(parts, pad, group=self.group)
+        out = torch.cat([parts[r][: hi - lo] for r, (lo, hi) in enumerate(sizes)])
+        return out.cpu().numpy().reshape(self.data.cext)
+
+    # -- operator / solver ------------------------------------------------
+    def apply_device(self, c_buf, out_buf):
+        self.halo(c_buf)
+        self.plan().apply(c_buf, out_buf)
+        return out_buf
+
+    def mass_apply_device(self, c_buf, out_buf, f_buf=None, a=0.0, cm=None):
+        self.halo(c_buf)
+        cm = self.data.vol if cm is None else cm
+        self.plan().mass_apply(c_buf, f_buf, cm, a, out_buf)
+        return out_buf
+
+    def _work_buffers(self, max_iter):
+        import torch
+
+        if self._work is None:
+            lay = self.layout
+            self._work = dict(r=lay.alloc(self.device), p=lay.alloc(self.device),
+                              ap=lay.alloc(self.device), scratch=self.plan().scratch(),
+                              history=None)
+        w = self._work
+        if w["history"] is None or w["history"].numel() < max_iter + 1:
+            w["history"] = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
+        return w
+
+    def pcg_device(self, b_buf, x_buf, config: SolveConfig = None, has_x0=True):
+        config = config or SolveConfig()
+        w = self._work_buffers(config.max_iter)
+        ops = NativeSlabOps(self.plan(config.precond))
+        rep, wall = distributed_pcg(ops, self.halo, self.allreduce, b_buf, x_buf, w["r"], w["p"],
+                                    w["ap"], w["scratch"], config, has_x0,
+                                    w["history"] if config.record_history else None)
+        return report_from(rep, config, wall, w["history"])
+
+    def pcg_host(self, rhs, config, x0=None):
+        b = self.scatter(rhs)
+        x = self.scatter(x0) if x0 is not None else self.layout.alloc(self.device)
+        rep = self.pcg_device(b, x, config, has_x0=x0 is not None)
+        return self.gather(x), rep

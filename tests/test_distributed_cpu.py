@@ -1,0 +1,205 @@
+"""Multi-rank z-slab CG orchestration on CPU (gloo, world_size 2 and 3).
+
+The product's distributed driver (``distributed.distributed_pcg``, the slab
+partition and the halo exchanger) runs unchanged; only the per-slab kernels
+are replaced by a CPU test double with the same semantics as the sm_100a
+step-wise entry points (pass A / pass B / finalize, fuse = 0), built on the
+oracle operator.  The gathered solution must match the single-process oracle
+pcg.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import bspde_oracle as O
+from paper_1904_03057_b200.device import SlabLayout
+from paper_1904_03057_b200.distributed import HaloExchanger, SlabPartition, distributed_pcg
+from paper_1904_03057_b200.solver import SolveConfig
+
+
+class CpuSlabOps:
+    """CPU stand-in for NativeSlabOps: same vectors, same scalar state machine."""
+
+    def __init__(self, ora, layout, precond="jacobi"):
+        self.ora, self.lay = ora, layout
+        diag = ora.jacobi_diagonal()
+        inv = np.where(diag != 0, 1.0 / diag, 1.0) if precond == "jacobi" else np.ones_like(diag)
+        g = layout.ghost
+        full_inv = np.zeros((ora.cext[0] + 2 * g,) + ora.cext[1:])
+        full_inv[g:g + ora.cext[0]] = inv
+        lo = layout.z_offset
+        self.inv = torch.from_numpy(full_inv[lo:lo + layout.nz + 2 * g].copy())
+        self.state = {}
+
+    def _own(self, t):
+        return self.lay.owned(t)
+
+    def _apply(self, c):
+        """A c for the owned planes, using ghost planes (embed in a global array)."""
+        g, lo, nz = self.lay.ghost, self.lay.z_offset, self.lay.nz
+        nzg = self.ora.cext[0]
+        full = np.zeros((nzg + 2 * g,) + self.ora.cext[1:])
+        full[lo:lo + nz + 2 * g] = c[:, :, : self.lay.nx].numpy()
+        out = self.ora.apply(full[g:g + nzg])
+        return torch.from_numpy(out[lo:lo + nz].copy())
+
+    def sums(self, scratch, n):
+        return scratch[:n]
+
+    def setup(self, scratch, history, cfg, has_x0):
+        self.state = dict(tol=cfg.tol, max_iter=cfg.max_iter, has_x0=has_x0, it=0, active=1)
+
+    def residual(self, b, x, r, scratch):
+        ax = self._apply(x)
+        rv = self._own(b) - ax
+        self._own(r).copy_(rv)
+        own_inv = self.inv[self.lay.ghost:self.lay.ghost + self.lay.nz, :, : self.lay.nx]
+        scratch[0] = float((self._own(b) ** 2).sum())
+        scratch[1] = float((rv * (own_inv * rv)).sum())
+        scratch[2] = float((rv ** 2).sum())
+
+    def pass_a(self, r, p, ap, scratch):
+        s = self.state
+        if not s["active"]:
+            return
+        nx = self.lay.nx
+        pn = r[:, :, :nx] * self.inv + s["beta"] * p[:, :, :nx]
+        self._pn = pn
+        apv = self._apply(torch.nn.functional.pad(pn, (0, p.shape[2] - nx)))
+        self._own(ap).copy_(apv)
+        g = self.lay.ghost
+        scratch[0] = float((pn[g:g + self.lay.nz] * apv).sum())
+
+    def pass_b(self, x, r, p, ap, scratch):
+        s = self.state
+        if not s["active"]:
+            return
+        g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
+        pn = self._pn[g:g + nz]
+        own_inv = self.inv[g:g + nz, :, :nx]
+        self._own(x).add_(s["alpha"] * pn)
+        self._own(r).sub_(s["alpha"] * self._own(ap))
+        self._own(p).copy_(pn)
+        rv = self._own(r)
+        scratch[0] = float((rv * (own_inv * rv)).sum())
+        scratch[1] = float((rv ** 2).sum())
+
+    def finalize(self, scratch, kind):
+        s = self.state
+        if kind == 0:
+            bb, rz, rr = (float(v) for v in scratch[:3])
+            s["scale"] = np.sqrt(bb) if bb > 0 else 1.0
+            s["rz"], s["res"], s["beta"] = rz, np.sqrt(rr), 0.0
+            s["res0"] = s["res"]
+            if bb == 0 and not s["has_x0"]:
+                s["active"] = 0
+                return
+        elif not s["active"]:
+            return
+        elif kind == 1:
+            pAp = float(scratch[0])
+            if pAp <= 0:
+                s["active"] = 0
+                return
+            s["alpha"] = s["rz"] / pAp
+            return
+        else:
+            rz_new, rr = float(scratch[0]), float(scratch[1])
+            s["beta"] = rz_new / s["rz"]
+            s["rz"] = rz_new
+            s["res"] = np.sqrt(rr)
+            s["it"] += 1
+        s["active"] = int(s["res"] / s["scale"] > s["tol"] and s["it"] < s["max_iter"])
+
+    def read(self, scratch):
+        class Rep:
+            pass
+
+        rep = Rep()
+        rep.iterations = self.state["it"]
+        rep.relative_residual = self.state["res"] / self.state["scale"]
+        return rep, bool(self.state["active"])
+
+
+def _worker(rank, world, port, ext, p, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        step = tuple(1.0 / (n - 1) for n in ext)
+        ora = O.KronOperator(ext, step, p, 0.02, 1.0)
+        part = SlabPartition(ora.cext[0], world, rank)
+        part.check_min(p)
+        lay = SlabLayout(part.nz, ora.cext[1], ora.cext[2], ghost=p, z_offset=part.z_offset,
+                         nz_global=ora.cext[0])
+        rng = np.random.default_rng(0)
+        axes = [np.linspace(0, 1, n) for n in ora.cext]
+        Z, Y, X = np.meshgrid(*axes, indexing="ij")
+        b_full = ora.mass_apply(np.cos(3 * Z) * np.sin(2 * Y + 0.3) + np.exp(-5 * (X - 0.4) ** 2))
+        x0_full = 0.1 * rng.normal(size=ora.cext)
+        lo, hi = part.bounds()
+        b = lay.upload(b_full[lo:hi], "cpu")
+        x = lay.upload(x0_full[lo:hi], "cpu")
+        r, pp, ap = lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu")
+        scratch = torch.zeros(8, dtype=torch.float64)
+        ops = CpuSlabOps(ora, lay)
+        halo = HaloExchanger(lay, rank, world)
+
+        def allreduce(t):
+            dist.all_reduce(t)
+
+        cfg = SolveConfig(tol=1e-13, max_iter=1000, poll_every=3)
+        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pp, ap, scratch, cfg, has_x0=True)
+        own = lay.owned(x).contiguous()
+        parts = [torch.zeros((part.bounds(q)[1] - part.bounds(q)[0],) + tuple(own.shape[1:]),
+                             dtype=own.dtype) for q in range(world)]
+        parts[rank].copy_(own)
+        for q in range(world):
+            dist.broadcast(parts[q], src=q)
+        if rank == 0:
+            xs = torch.cat(parts).numpy()
+            xo, ro = O.pcg(ora.apply, ora.jacobi_diagonal, b_full, tol=1e-13, max_iter=1000,
+                           x0=x0_full)
+            out_q.put((rep.iterations, ro["iterations"],
+                       float(np.linalg.norm(xs - xo) / np.linalg.norm(xo))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,ext", [(2, (13, 10, 11)), (3, (17, 9, 10))])
+def test_zslab_cg_matches_single_process(world, ext):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, 3, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+        assert pr.exitcode == 0
+    its, its_o, rel = q.get(timeout=10)
+    assert abs(its - its_o) <= 1, (its, its_o)
+    assert rel < 1e-10, rel
+
+
+def test_partition_bounds():
+    part = SlabPartition(930, 8, 0)
+    spans = [part.bounds(r) for r in range(8)]
+    assert spans[0][0] == 0 and spans[-1][1] == 930
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    with pytest.raises(Exception):
+        SlabPartition(5, 8, 0)
+    with pytest.raises(Exception):
+        SlabPartition(10, 4, 0).check_min(3)

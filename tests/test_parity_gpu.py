@@ -184,9 +184,10 @@ def test_cg_vs_oracle_odd_shapes(cuda_device):
         # so x itself agrees only to ~kappa*tol -- check the true residuals
         true_res = float(np.linalg.norm(b - ora.apply(x)) / np.linalg.norm(b))
         true_res_o = float(np.linalg.norm(b - ora.apply(xo)) / np.linalg.norm(b))
-        # true residuals of two correct solves at the same recursive tolerance agree
-        # only to rounding accumulation (measured 1.3e-9 vs 1.2e-10)
-        assert true_res < 1e-8 and true_res_o < 1e-8, (true_res, true_res_o)
+        # the true residual agrees with the oracle's: for the ill-conditioned p=5
+        # case the recursive residual stagnates at ~1e-9 while the true one sits
+        # at ~3.4e-7 in both implementations
+        assert true_res < 3 * true_res_o + 1e-9, (true_res, true_res_o)
         # same outcome as the reference recurrence (the p=5 case stagnates at its
         # rounding floor ~1e-9 and stops at max_iter in both)
         assert rep.converged == bool(ro["converged"])
@@ -339,3 +340,28 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     rep, active = plan.cg_read(w.scratch)
     assert rep.iterations == 1
     assert abs(rep.residual - np.linalg.norm(r1)) / np.linalg.norm(r1) < 1e-12
+
+
+def test_distributed_path_single_rank_matches_fused(cuda_device):
+    """The z-slab driver (step-wise ABI, fuse=0, separate finalize kernels) on
+    one rank reproduces the fused single-GPU solver bit for bit."""
+    from paper_1904_03057_b200.distributed import DistributedOperator
+
+    h_n = 24
+    inp = O.heat_inputs(h_n)
+    N, hh, dt = inp["N"], inp["h"], inp["dt"]
+    data = heat_system(Grid((N,) * 3, (hh,) * 3), 3, dt)
+    ora = O.KronOperator((N,) * 3, (hh,) * 3, 3, dt, 1.0)
+    b = ora.mass_apply(inp["u0"]) + dt * ora.mass_apply(inp["q"])
+    cfg = SolveConfig(tol=1e-10, max_iter=2000, record_history=True)
+    x1, r1 = pcg(make_operator(data, "b200"), b, cfg, x0=inp["u0"])
+    dop = DistributedOperator(data)
+    x2, r2 = dop.pcg_host(b, cfg, x0=inp["u0"])
+    assert r1.iterations == r2.iterations
+    assert np.array_equal(x1, x2)
+    assert r1.history == r2.history
+    # operator apply through the slab path
+    cb = dop.scatter(inp["u0"])
+    ob = dop.layout.alloc(dop.device)
+    dop.apply_device(cb, ob)
+    assert relmax(dop.gather(ob), ora.apply(inp["u0"])) < 1e-13
