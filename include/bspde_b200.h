@@ -144,9 +144,18 @@ int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
 int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p,
                     double* ap, void* scratch, int fuse, void* stream);
 /* p = D^-1 r + beta p_old; x += alpha p; r -= alpha Ap;
- * sums = {<r,D^-1 r>, <r,r>}                                          kind 2 */
+ * sums = {<r,D^-1 r>, <r,r>}                                          kind 2
+ * (solver.py:94-101).  The x update is applied every other call, both
+ * updates in the reference's rounding order; call bspde_cg_flush_x before
+ * reading x. */
 int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, double* p,
                     const double* ap, void* scratch, int fuse, void* stream);
+/* Apply a pending x update (x += alpha_k p_k), if any.  bspde_pcg_solve does
+ * this itself; step-wise drivers call it once after their loop. */
+int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p, void* scratch,
+                     void* stream);
+/* kind 0/1/2: scalar update after residual / pass A / pass B (skipped when
+ * inactive); kind 3 is used internally by bspde_cg_flush_x. */
 int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
 /* Copy the scalar state to the host (synchronizes the stream). */
 int bspde_cg_read_report(bspde_plan* plan, const void* scratch,

@@ -13,7 +13,9 @@ import threading
 from .errors import NativeLibraryError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbspde_b200.so")
+# BSPDE_LIB selects a tuning variant built by build.py --out=... (development
+# only; the variant is the same source with different -D constants).
+LIB_PATH = os.environ.get("BSPDE_LIB") or os.path.join(HERE, "libbspde_b200.so")
 
 BSPDE_CG_RUNNING = 0
 BSPDE_CG_CONVERGED = 1
@@ -83,6 +85,7 @@ SIGNATURES = [
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_cg_finalize", C.c_int, [_VP, _VP, C.c_int, _VP]),
     ("bspde_cg_read_report", C.c_int, [_VP, _VP, C.POINTER(CgReport),
                                        C.POINTER(C.c_int32), _VP]),

@@ -34,22 +34,28 @@ def needs_rebuild():
     return any(os.path.getmtime(d) > mt for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_rebuild():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile the library; ``out``/``defines`` build tuning variants
+    (e.g. ``defines=["BSPDE_RPT=4"]``) next to the product library."""
+    out = out or LIB
+    if out == LIB and not defines and not force and not needs_rebuild():
         return LIB
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", SRC]
+           *[f"-D{d}" for d in defines],
+           "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libbspde_b200.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a[6:] for a in args if a.startswith("--out=")]
+    print(build(force=True, verbose="-v" in args, out=outs[0] if outs else None, defines=defs))

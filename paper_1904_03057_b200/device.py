@@ -187,6 +187,10 @@ class NativePlan:
         N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(p), N.ptr(ap),
                                          N.ptr(scratch), int(fuse), N.stream_handle(stream)))
 
+    def cg_flush_x(self, x, p, scratch, stream=None):
+        N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(p), N.ptr(scratch),
+                                          N.stream_handle(stream)))
+
     def cg_finalize(self, scratch, kind, stream=None):
         N.check(self.lib.bspde_cg_finalize(self.handle, N.ptr(scratch), int(kind),
                                            N.stream_handle(stream)))

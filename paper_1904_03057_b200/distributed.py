@@ -144,6 +144,9 @@ class NativeSlabOps:
     def finalize(self, scratch, kind):
         self.plan.cg_finalize(scratch, kind)
 
+    def flush_x(self, x, p, scratch):
+        self.plan.cg_flush_x(x, p, scratch)
+
     def read(self, scratch):
         return self.plan.cg_read(scratch)
 
@@ -173,6 +176,7 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, p, ap, scratch, config: Solve
             allreduce(ops.sums(scratch, 2))
             ops.finalize(scratch, 2)
         rep, active = ops.read(scratch)
+    ops.flush_x(x, p, scratch)  # pass B moves x every other iteration
     return rep, time.perf_counter() - t0
 
 

@@ -252,9 +252,11 @@ def degenerate_factor(p: int, kind: str) -> GramFactor:
 def taps_header() -> str:
     """C++ header with the exact interior taps (mass, stiffness) for p=1..5.
 
-    Generated into ``csrc/gram_taps.cuh``; the kernels use them as
-    compile-time constants (folded into the instruction stream / constant
-    bank).  ``tests/test_gram.py`` checks the committed header against
+    Generated into ``csrc/gram_taps.cuh``.  Two equivalent forms: constexpr
+    functions (immediates folded by ptxas) and, with ``BSPDE_CONST_TAPS``,
+    ``__constant__`` tables read with compile-time indices (constant-bank
+    operands).  Which one is faster depends on register pressure; the build
+    picks one.  ``tests/test_gram.py`` checks the committed header against
     ``gram_factor`` so the two cannot drift.
     """
     def fn(name, vals):
@@ -262,13 +264,27 @@ def taps_header() -> str:
         return (f"  __host__ __device__ static constexpr double {name}(int k) {{\n"
                 f"    return {body} : {repr(float(vals[-1]))};\n  }}")
 
+    rows_m, rows_k, spec = [], [], []
+    for p in range(1, MAX_DEGREE + 1):
+        im, _ = _exact_rows(p, 0)
+        ik, _ = _exact_rows(p, 1)
+        pad = [0.0] * (2 * MAX_DEGREE + 1 - len(im))
+        rows_m.append(", ".join(repr(float(v)) for v in list(im) + pad))
+        rows_k.append(", ".join(repr(float(v)) for v in list(ik) + pad))
+        spec += [f"template <> struct GramTaps<{p}> {{", fn("M", im), fn("K", ik), "};"]
     lines = ["// generated by paper_1904_03057_b200/gram.py:taps_header() -- do not edit",
              "// exact interior taps G[i, i+k-p], k=0..2p, of the unit-step 1-D Gram",
              "// factors (mass: int b(x)b(x-k); stiffness: int b'(x)b'(x-k)), p = 1..5",
-             "#pragma once", "", "template <int P> struct GramTaps;"]
-    for p in range(1, MAX_DEGREE + 1):
-        interior_m, _ = _exact_rows(p, 0)
-        interior_k, _ = _exact_rows(p, 1)
-        lines += [f"template <> struct GramTaps<{p}> {{", fn("M", interior_m), fn("K", interior_k),
-                  "};"]
+             "#pragma once", "", "#ifdef BSPDE_CONST_TAPS",
+             f"__constant__ double kGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
+    lines += [f"    {{{r}}}," for r in rows_m]
+    lines += ["};", f"__constant__ double kGramK[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
+    lines += [f"    {{{r}}}," for r in rows_k]
+    lines += ["};", "",
+              "template <int P>",
+              "struct GramTaps {",
+              "  __device__ __forceinline__ static double M(int k) { return kGramM[P - 1][k]; }",
+              "  __device__ __forceinline__ static double K(int k) { return kGramK[P - 1][k]; }",
+              "};", "#else", "template <int P> struct GramTaps;"]
+    lines += spec + ["#endif"]
     return "\n".join(lines) + "\n"

@@ -83,7 +83,8 @@ class CpuSlabOps:
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         pn = self._pn[g:g + nz]
         own_inv = self.inv[g:g + nz, :, :nx]
-        self._own(x).add_(s["alpha"] * pn)
+        if s.get("x_pending"):  # deferred update, same order as cg_pass_b_kernel
+            self._own(x).add_(s["alpha_pend"] * self._own(p)).add_(s["alpha"] * pn)
         self._own(r).sub_(s["alpha"] * self._own(ap))
         self._own(p).copy_(pn)
         rv = self._own(r)
@@ -111,11 +112,20 @@ class CpuSlabOps:
             return
         else:
             rz_new, rr = float(scratch[0]), float(scratch[1])
+            if s.get("x_pending"):
+                s["x_pending"] = 0
+            else:
+                s["x_pending"], s["alpha_pend"] = 1, s["alpha"]
             s["beta"] = rz_new / s["rz"]
             s["rz"] = rz_new
             s["res"] = np.sqrt(rr)
             s["it"] += 1
         s["active"] = int(s["res"] / s["scale"] > s["tol"] and s["it"] < s["max_iter"])
+
+    def flush_x(self, x, p, scratch):
+        if self.state.get("x_pending"):
+            self._own(x).add_(self.state["alpha_pend"] * self._own(p))
+            self.state["x_pending"] = 0
 
     def read(self, scratch):
         class Rep:

@@ -334,12 +334,51 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     torch.cuda.synchronize()
     x1 = x0 + alpha * p0
     r1 = r0 - alpha * Ap
-    assert relmax(lay.download(xb), x1) < 1e-13
+    # the x update of an odd pass B is deferred until the next one / a flush
+    assert np.array_equal(lay.download(xb), x0)
     assert relmax(lay.download(w.r), r1) < 1e-12
     assert float(relmax(lay.download(w.p), p0)) < 1e-13
     rep, active = plan.cg_read(w.scratch)
     assert rep.iterations == 1
     assert abs(rep.residual - np.linalg.norm(r1)) / np.linalg.norm(r1) < 1e-12
+    xe = xb.clone()
+    plan.cg_flush_x(xe, w.p, w.scratch)
+    torch.cuda.synchronize()
+    assert relmax(lay.download(xe), x1) < 1e-13
+    plan.cg_flush_x(xe, w.p, w.scratch)  # idempotent: nothing pending any more
+    assert relmax(lay.download(xe), x1) < 1e-13
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5])
+def test_deferred_x_update_is_bitwise_eager(cuda_device, iters):
+    """Pass B moves x every other iteration; the result after a flush must be
+    bit-identical to updating x after every iteration (two stored roundings)."""
+    import torch
+
+    ext, p = (13, 12, 11), 3
+    step = tuple(1.0 / (n - 1) for n in ext)
+    data = build_system(BoxDomain(Grid(ext, step)), p, p, 0.01, 1.0, [])
+    rng = np.random.default_rng(11)
+    b = rng.normal(size=data.cext)
+    x0 = rng.normal(size=data.cext)
+    outs = []
+    for eager in (False, True):
+        op = make_operator(data, "b200")
+        lay, plan = op.layout, op.plan()
+        bb, xb = lay.upload(b, op.device), lay.upload(x0, op.device)
+        r, pp, ap = lay.alloc(op.device), lay.alloc(op.device), lay.alloc(op.device)
+        scratch = plan.scratch()
+        plan.cg_setup(scratch, None, 1e-300, 100, False, True)
+        plan.cg_residual(bb, xb, r, scratch, 1)
+        for _ in range(iters):
+            plan.cg_pass_a(r, pp, ap, scratch, 1)
+            plan.cg_pass_b(xb, r, pp, ap, scratch, 1)
+            if eager:
+                plan.cg_flush_x(xb, pp, scratch)
+        plan.cg_flush_x(xb, pp, scratch)
+        torch.cuda.synchronize()
+        outs.append(lay.download(xb))
+    assert np.array_equal(outs[0], outs[1])
 
 
 def test_distributed_path_single_rank_matches_fused(cuda_device):
