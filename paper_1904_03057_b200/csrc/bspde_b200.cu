@@ -109,6 +109,7 @@ struct SepParams {
   int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
   double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
+  double gm[MAXTAP], gk[MAXTAP];  // unit interior taps (BSPDE_TAP_SRC == 1)
   const double* tab;             // device: [axis][kind][NC*R] (NC = class stride)
   const double* invd;            // device: NCz*NCy*NCx
   double* out;
@@ -120,6 +121,30 @@ struct SepParams {
   unsigned* counter;
   CgState* state;
   int fuse;
+};
+
+// Interior taps for the fast paths: compile-time immediates (0) or kernel
+// parameters, i.e. constant-bank operands of the FMAs (1).
+#ifndef BSPDE_UNROLL_PLANES
+#define BSPDE_UNROLL_PLANES 1
+#endif
+#ifndef BSPDE_SPLIT_WA
+#define BSPDE_SPLIT_WA 0
+#endif
+#ifndef BSPDE_TAP_SRC
+#define BSPDE_TAP_SRC 0
+#endif
+template <int P>
+struct TapSrc {
+  const SepParams& prm;
+  __device__ __forceinline__ double M(int k) const {
+    if constexpr (BSPDE_TAP_SRC == 1) return prm.gm[k];
+    else return GramTaps<P>::M(k);
+  }
+  __device__ __forceinline__ double K(int k) const {
+    if constexpr (BSPDE_TAP_SRC == 1) return prm.gk[k];
+    else return GramTaps<P>::K(k);
+  }
 };
 
 struct PassBParams {
@@ -425,7 +450,7 @@ template <int P, int MODE, bool INTERIOR>
 __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm,
                                             const ItemGeom& g, int jj, uint32_t f, double beta) {
   using C = Cfg<P, MODE>;
-  using T = GramTaps<P>;
+  const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
@@ -443,39 +468,47 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
   const int cz = cls_of(zg, prm.nz_glob, ewz);
 
   if (MODE == M_CGA) {
+    // p = D^-1 r + beta p_old over this warp's rows of the haloed tile, in
+    // place in the p_old stage.  The warp's rows (warp, warp+NW, ...) are
+    // walked as one flat list of double2 pairs so all lanes stay busy.
+    constexpr int PPR = HX / 2;                       // pairs per row
+    constexpr int NROW = (HY + NW - 1) / NW;          // rows of warps 0.. (HY % NW) - 1
+    const int nrow = (warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1;
+    const int npair = nrow * PPR;
     const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
-    const double inv0 = sm.invd[(cz * ncy + ewy) * ncx + ewx];
+    if (INTERIOR && cz == ewz) {
+      const double inv0 = sm.invd[(cz * ncy + ewy) * ncx + ewx];
 #pragma unroll
-    for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
-      const int row = warp + NW * m;
-      if (row < HY) {
+      for (int h = 0; h < (NROW * PPR + 31) / 32; ++h) {
+        const int t = lane + 32 * h;
+        if (t < npair) {
+          const int m = t / PPR, q = t - m * PPR;
+          const int e = (warp + NW * m) * HX + 2 * q;
+          const double2 rv = *reinterpret_cast<const double2*>(stC + e);
+          const double2 qv = *reinterpret_cast<const double2*>(stP + e);
+          double2 pv;
+          pv.x = pdir(rv.x, inv0, qv.x, beta);
+          pv.y = pdir(rv.y, inv0, qv.y, beta);
+          *reinterpret_cast<double2*>(stP + e) = pv;
+        }
+      }
+    } else {
+      for (int t = lane; t < npair; t += 32) {
+        const int m = t / PPR, q = t - m * PPR;
+        const int row = warp + NW * m;
+        const int e = row * HX + 2 * q;
         const int gyy = g.y0 - P + row;
+        const int gxx = g.x0 - PX + 2 * q;
         const bool rok = (gyy >= 0 && gyy < ny);
         const double* trow = sm.invd + (cz * ncy + (rok ? cls_of(gyy, ny, ewy) : ewy)) * ncx;
-        const double inv_row = rok ? trow[ewx] : 0.0;
-#pragma unroll
-        for (int h = 0; h < (HX / 2 + 31) / 32; ++h) {
-          const int q = lane + 32 * h;
-          if (q < HX / 2) {
-            const int e = row * HX + 2 * q;
-            const double2 rv = *reinterpret_cast<const double2*>(stC + e);
-            const double2 qv = *reinterpret_cast<const double2*>(stP + e);
-            double i0 = inv0, i1 = inv0;
-            if (!INTERIOR || cz != ewz) {
-              const int gxx = g.x0 - PX + 2 * q;
-              i0 = inv_row;
-              i1 = inv_row;
-              if (rok && !(gxx >= ewx && gxx + 1 < nx - ewx)) {
-                i0 = (gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
-                i1 = (gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
-              }
-            }
-            double2 pv;
-            pv.x = pdir(rv.x, i0, qv.x, beta);
-            pv.y = pdir(rv.y, i1, qv.y, beta);
-            *reinterpret_cast<double2*>(stP + e) = pv;
-          }
-        }
+        const double i0 = (rok && gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
+        const double i1 = (rok && gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
+        const double2 rv = *reinterpret_cast<const double2*>(stC + e);
+        const double2 qv = *reinterpret_cast<const double2*>(stP + e);
+        double2 pv;
+        pv.x = pdir(rv.x, i0, qv.x, beta);
+        pv.y = pdir(rv.y, i1, qv.y, beta);
+        *reinterpret_cast<double2*>(stP + e) = pv;
       }
     }
     __syncwarp();
@@ -500,18 +533,18 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
         for (int k = 0; k < P; ++k) {
           const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
           const double s1 = raw[DX + 1 + k] + raw[DX + 1 + 2 * P - k];
-          m0 = fma(T::M(k), s0, m0);
-          m1 = fma(T::M(k), s1, m1);
+          m0 = fma(T.M(k), s0, m0);
+          m1 = fma(T.M(k), s1, m1);
           if (STIFF) {
-            k0 = fma(T::K(k), s0, k0);
-            k1 = fma(T::K(k), s1, k1);
+            k0 = fma(T.K(k), s0, k0);
+            k1 = fma(T.K(k), s1, k1);
           }
         }
-        m0 = fma(T::M(P), raw[DX + P], m0);
-        m1 = fma(T::M(P), raw[DX + P + 1], m1);
+        m0 = fma(T.M(P), raw[DX + P], m0);
+        m1 = fma(T.M(P), raw[DX + P + 1], m1);
         if (STIFF) {
-          k0 = fma(T::K(P), raw[DX + P], k0);
-          k1 = fma(T::K(P), raw[DX + P + 1], k1);
+          k0 = fma(T.K(P), raw[DX + P], k0);
+          k1 = fma(T.K(P), raw[DX + P + 1], k1);
         }
       } else {
         const int c0 = (gx0 < nx) ? cls_of(gx0, nx, ewx) : ewx;
@@ -547,7 +580,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
                                            double (&pr)[P][RPT], const double (&auxv)[RPT],
                                            double (&dsum)[3], double beta) {
   using C = Cfg<P, MODE>;
-  using T = GramTaps<P>;
+  const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, NA = C::NA, NS = C::NS, NC = C::NC, S = 2 * P;
   constexpr int PX = C::PX;
   constexpr bool STIFF = C::STIFF;
@@ -567,11 +600,12 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   double out[RPT];
   if (in_grid) {
     // ---- y-pass: wm = My u1, wa = My t + cy Ky u1 for rows gy0 .. gy0+3 ----
-    double wm[RPT], wa[RPT];
+    double wm[RPT], wa[RPT], wb[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       wm[i] = 0.0;
       wa[i] = 0.0;
+      wb[i] = 0.0;
     }
     const double* x1c = X1 + (rg * RPT) * TX + cxl;
     const double* x2c = X2 + (rg * RPT) * TX + cxl;
@@ -586,13 +620,18 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         for (int i = 0; i < RPT; ++i) {
           const int k = rr - i;
           if (k >= 0 && k <= 2 * P) {
-            wm[i] = fma(T::M(k), a1, wm[i]);
+            wm[i] = fma(T.M(k), a1, wm[i]);
             if (STIFF) {
-              wa[i] = fma(T::M(k), t, wa[i]);
-              wa[i] = fma(T::K(k), u1c, wa[i]);
+              wa[i] = fma(T.M(k), t, wa[i]);
+              if (BSPDE_SPLIT_WA) wb[i] = fma(T.K(k), u1c, wb[i]);
+              else wa[i] = fma(T.K(k), u1c, wa[i]);
             }
           }
         }
+      }
+      if (BSPDE_SPLIT_WA && STIFF) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) wa[i] += wb[i];
       }
     } else {
       int cyr[RPT];
@@ -627,17 +666,17 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
       for (int i = 0; i < RPT; ++i) {
         const double a = STIFF ? wa[i] : wm[i];
         const double w2 = STIFF ? wm[i] * prm.cz : 0.0;
-        double o = fma(T::M(0), a, acc[0][i]);
-        if (STIFF) o = fma(T::K(0), w2, o);
+        double o = fma(T.M(0), a, acc[0][i]);
+        if (STIFF) o = fma(T.K(0), w2, o);
         out[i] = o;
 #pragma unroll
         for (int k = 0; k < S - 1; ++k) {
-          double v = fma(T::M(k + 1), a, acc[k + 1][i]);
-          if (STIFF) v = fma(T::K(k + 1), w2, v);
+          double v = fma(T.M(k + 1), a, acc[k + 1][i]);
+          if (STIFF) v = fma(T.K(k + 1), w2, v);
           acc[k][i] = v;
         }
-        double v = T::M(S) * a;
-        if (STIFF) v = fma(T::K(S), w2, v);
+        double v = T.M(S) * a;
+        if (STIFF) v = fma(T.K(S), w2, v);
         acc[S - 1][i] = v;
       }
     } else {
@@ -741,6 +780,9 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 
   plane_front<P, MODE, INTERIOR>(prm, sm, g, 0, flat, beta);
   __syncthreads();
+#if BSPDE_UNROLL_PLANES > 1
+#pragma unroll 2
+#endif
   for (int j = 0; j < nin; ++j) {
     // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
     double auxv[RPT];
@@ -1150,6 +1192,8 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
     sp.tyk[k] = d.c_stiff[1] * d.stiff_table[1][d.ew[1] * R + k];
     sp.txm[k] = d.mass_table[2][d.ew[2] * R + k];
     sp.txk[k] = d.stiff_table[2][d.ew[2] * R + k];
+    sp.gm[k] = k < R ? kHostGramM[pl->p - 1][k] : 0.0;
+    sp.gk[k] = k < R ? kHostGramK[pl->p - 1][k] : 0.0;
   }
   sp.zfast = (d.nz_global > 1 && d.ew[0] > 0) ? 1 : 0;
   sp.c_mass = d.c_mass;

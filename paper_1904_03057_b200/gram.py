@@ -275,8 +275,14 @@ def taps_header() -> str:
     lines = ["// generated by paper_1904_03057_b200/gram.py:taps_header() -- do not edit",
              "// exact interior taps G[i, i+k-p], k=0..2p, of the unit-step 1-D Gram",
              "// factors (mass: int b(x)b(x-k); stiffness: int b'(x)b'(x-k)), p = 1..5",
-             "#pragma once", "", "#ifdef BSPDE_CONST_TAPS",
-             f"__constant__ double kGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
+             "#pragma once", "",
+             "// host copy (kernel-parameter taps are filled from it)",
+             f"static const double kHostGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
+    lines += [f"    {{{r}}}," for r in rows_m]
+    lines += ["};", f"static const double kHostGramK[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
+    lines += [f"    {{{r}}}," for r in rows_k]
+    lines += ["};", "", "#ifdef BSPDE_CONST_TAPS",
+              f"__constant__ double kGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
     lines += [f"    {{{r}}}," for r in rows_m]
     lines += ["};", f"__constant__ double kGramK[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
     lines += [f"    {{{r}}}," for r in rows_k]
