@@ -106,6 +106,7 @@ struct SepParams {
   long long pitch_y, pitch_z;
   int ew[3];
   int tiles_x, tiles_y, nchunks, chunk_len, nitems;
+  int main_items, tail_split, sub_len;  // items >= main_items: tail chunks split tail_split ways
   int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
   double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
@@ -390,15 +391,28 @@ struct ItemGeom {
   int x0, y0, zc0, zc1;
 };
 
+// Items: (tile, z-chunk) in tile-fastest order, dealt round-robin so all
+// CTAs stream neighbouring tiles at the same z in lockstep (x/y halo planes
+// are then L2 hits).  The first main_items form whole waves; each remaining
+// chunk (the ragged last wave) is split tail_split ways so it is spread over
+// all SMs instead of extending the makespan by a full chunk.
 __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
   const int tiles_xy = prm.tiles_x * prm.tiles_y;
-  const int t = item % tiles_xy;
-  const int ch = item / tiles_xy;
+  // branch-free: for main items jt < 0 maps to (it = item, sub = 0) via max()
+  const int jt = max(item - prm.main_items, 0);
+  const int it = min(item, prm.main_items + jt / prm.tail_split);
+  const int sub = jt - (it - min(item, prm.main_items)) * prm.tail_split;
+  const int t = it % tiles_xy;
+  const int ch = it / tiles_xy;
+  const int len = prm.sub_len;  // == chunk_len when tail_split == 1
   ItemGeom g;
   g.x0 = (t % prm.tiles_x) * TX;
   g.y0 = (t / prm.tiles_x) * TY;
-  g.zc0 = ch * prm.chunk_len;
-  g.zc1 = min(g.zc0 + prm.chunk_len, prm.nz);
+  const int c0 = ch * prm.chunk_len;
+  const int c1 = min(c0 + prm.chunk_len, prm.nz);
+  const bool tail = item >= prm.main_items;
+  g.zc0 = tail ? min(c0 + sub * len, c1) : c0;   // an empty sub-chunk streams only its
+  g.zc1 = tail ? min(g.zc0 + len, c1) : c1;      // 2p warm-up planes
   return g;
 }
 
@@ -1049,6 +1063,7 @@ struct KernelInfo {
 struct Launch {
   int grid;
   int nchunks, chunk_len, nitems;
+  int main_items = 0, tail_split = 1;
 };
 
 }  // namespace
@@ -1077,6 +1092,7 @@ struct bspde_plan {
   cudaStream_t work = nullptr;    // private stream: CUDA graphs cannot be captured on
   cudaEvent_t ev_in = nullptr;    // the legacy default stream the caller may use
   cudaEvent_t ev_out = nullptr;
+  std::map<int, Launch> launch_cache;  // per kernel mode (plan_launch is a simulation)
 };
 
 namespace {
@@ -1118,34 +1134,84 @@ KernelInfo kernel_for(int p, int mode) {
   }
 }
 
-// choose z-chunking so that items balance over the persistent grid
+// Choose the z-chunking.  Items are dealt round-robin (item i -> CTA
+// i % grid, see item_geom), so the kernel time is the largest per-CTA sum of
+// streamed planes (chunk + 2p warm-up), with edge tiles weighted by their
+// measured extra cost.  Candidates: chunk counts nc (chunk length capped so
+// CTAs stay close in z and share halo planes through L2), each with and
+// without splitting the ragged last wave.  The plan is simulated exactly.
+constexpr double kEdgeTileWeight = 1.35;  // edge-tile plane cost / interior (B200, p=3)
+
 Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
   const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
   const int tiles = tx * ty;
   const int slots = std::max(1, pl->num_sms * ki.ctas_per_sm);
   const int nz = pl->d.nz;
-  Launch best{1, 1, nz, tiles};
-  double best_cost = 1e300;
+  const int p = pl->p, px = p + (p & 1);
   if (const char* fc = getenv("BSPDE_FORCE_CHUNKS")) {  // debug / tuning override
     const int nc = std::max(1, std::min(nz, atoi(fc)));
     const int len = (nz + nc - 1) / nc;
     const int ncr = (nz + len - 1) / len;
     const long long items = (long long)tiles * ncr;
-    return Launch{(int)std::min<long long>(items, slots), ncr, len, (int)items};
+    Launch f{(int)std::min<long long>(items, slots), ncr, len, (int)items};
+    f.main_items = (int)items;
+    return f;
   }
+  std::vector<double> w(tiles);
+  for (int t = 0; t < tiles; ++t) {
+    const int x0 = (t % tx) * TX, y0 = (t / tx) * TY;
+    const bool in = (x0 - px >= pl->d.ew[2]) && (x0 + TX + px <= pl->d.nx - pl->d.ew[2]) &&
+                    (y0 - p >= pl->d.ew[1]) && (y0 + TY + p <= pl->d.ny - pl->d.ew[1]);
+    w[t] = in ? 1.0 : kEdgeTileWeight;
+  }
+  const char* ml = getenv("BSPDE_MAX_LEN");
+  const int max_len = ml ? std::max(1, atoi(ml)) : 200;
+  Launch best{1, 1, nz, tiles};
+  best.main_items = tiles;
+  double best_cost = 1e300;
+  std::vector<double> load;
   for (int nc = 1; nc <= nz; ++nc) {
     const int len = (nz + nc - 1) / nc;
     const int ncr = (nz + len - 1) / len;
+    if (len > max_len && nc < nz) continue;
     const long long items = (long long)tiles * ncr;
-    const int grid = (int)std::min<long long>(items, slots);
-    const long long per = (items + grid - 1) / grid;
-    // time model: planes streamed by the busiest CTA (halo planes included)
-    const double cost = (double)per * (len + 2 * pl->p);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = Launch{grid, ncr, len, (int)items};
+    if (items > (1 << 22)) break;
+    const long long waves = items / slots;
+    const long long rem = items - waves * slots;
+    const int split_opt = rem > 0 ? (int)std::max<long long>(1, slots / rem) : 1;
+    for (int split : {1, split_opt}) {
+      const long long main_items = split > 1 ? waves * slots : items;
+      const long long nitems = main_items + (items - main_items) * split;
+      const int grid = (int)std::min<long long>(nitems, slots);
+      const int sub = (len + split - 1) / split;
+      load.assign(grid, 0.0);
+      for (long long i = 0; i < nitems; ++i) {
+        long long it = i;
+        int zl;
+        if (i < main_items) {
+          const int ch = (int)(it / tiles);
+          zl = std::min(len, nz - ch * len);
+        } else {
+          const long long jt = i - main_items;
+          it = main_items + jt / split;
+          const int sb = (int)(jt % split);
+          const int ch = (int)(it / tiles);
+          const int c1 = std::min(ch * len + len, nz);
+          const int z0 = std::min(ch * len + sb * sub, c1);
+          zl = std::min(z0 + sub, c1) - z0;
+        }
+        load[i % grid] += (zl + 2 * p) * w[it % tiles];
+      }
+      const double cost = *std::max_element(load.begin(), load.end());
+      if (cost < best_cost * (1.0 - 1e-9)) {
+        best_cost = cost;
+        best = Launch{grid, ncr, len, (int)nitems};
+        best.main_items = (int)main_items;
+        best.tail_split = split;
+      }
+      if (split_opt == 1) break;
     }
-    if (len <= 4 * pl->p) break;
+    if (len <= 4 * p) break;
   }
   return best;
 }
@@ -1229,12 +1295,23 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
                const double* aux, double aux_scale, double c_mass_override, bool use_override,
                void* scratch, int fuse, cudaStream_t st) {
   KernelInfo ki = kernel_for(pl->p, mode);
-  Launch ln = plan_launch(pl, ki);
+  auto lit = pl->launch_cache.find(mode);
+  if (lit == pl->launch_cache.end()) {
+    lit = pl->launch_cache.emplace(mode, plan_launch(pl, ki)).first;
+    if (getenv("BSPDE_PLAN_DEBUG"))
+      fprintf(stderr, "bspde plan: mode %d grid %d chunks %d len %d items %d main %d split %d\n", mode,
+              lit->second.grid, lit->second.nchunks, lit->second.chunk_len, lit->second.nitems,
+              lit->second.main_items, lit->second.tail_split);
+  }
+  const Launch ln = lit->second;
   SepParams sp;
   fill_common(sp, pl);
   sp.nchunks = ln.nchunks;
   sp.chunk_len = ln.chunk_len;
   sp.nitems = ln.nitems;
+  sp.main_items = ln.main_items;
+  sp.tail_split = ln.tail_split;
+  sp.sub_len = (ln.chunk_len + ln.tail_split - 1) / ln.tail_split;
   sp.out = out;
   sp.aux = aux;
   sp.aux_scale = aux_scale;
