@@ -129,6 +129,9 @@ struct SepParams {
 #ifndef BSPDE_UNROLL_PLANES
 #define BSPDE_UNROLL_PLANES 1
 #endif
+#ifndef BSPDE_ALL_EDGE
+#define BSPDE_ALL_EDGE 0
+#endif
 #ifndef BSPDE_SPLIT_WA
 #define BSPDE_SPLIT_WA 0
 #endif
@@ -419,6 +422,7 @@ __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
 template <int P, int MODE>
 __device__ __forceinline__ bool tile_interior(const SepParams& prm, const ItemGeom& g) {
   using C = Cfg<P, MODE>;
+  if (BSPDE_ALL_EDGE) return false;  // tuning: measure the edge-tile path everywhere
   return (g.x0 - C::PX >= prm.ew[2]) && (g.x0 + TX + C::PX <= prm.nx - prm.ew[2]) &&
          (g.y0 - P >= prm.ew[1]) && (g.y0 + TY + P <= prm.ny - prm.ew[1]);
 }
@@ -507,16 +511,22 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
         }
       }
     } else {
+      // edge tile or edge z plane: elements inside the x/y interior band use
+      // the plane's interior entry; only the boundary band looks up classes
+      const double inv_c = sm.invd[(cz * ncy + ewy) * ncx + ewx];
       for (int t = lane; t < npair; t += 32) {
         const int m = t / PPR, q = t - m * PPR;
         const int row = warp + NW * m;
         const int e = row * HX + 2 * q;
         const int gyy = g.y0 - P + row;
         const int gxx = g.x0 - PX + 2 * q;
-        const bool rok = (gyy >= 0 && gyy < ny);
-        const double* trow = sm.invd + (cz * ncy + (rok ? cls_of(gyy, ny, ewy) : ewy)) * ncx;
-        const double i0 = (rok && gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
-        const double i1 = (rok && gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
+        double i0 = inv_c, i1 = inv_c;
+        if (!(gyy >= ewy && gyy < ny - ewy && gxx >= ewx && gxx + 1 < nx - ewx)) {
+          const bool rok = (gyy >= 0 && gyy < ny);
+          const double* trow = sm.invd + (cz * ncy + (rok ? cls_of(gyy, ny, ewy) : ewy)) * ncx;
+          i0 = (rok && gxx >= 0 && gxx < nx) ? trow[cls_of(gxx, nx, ewx)] : 0.0;
+          i1 = (rok && gxx + 1 >= 0 && gxx + 1 < nx) ? trow[cls_of(gxx + 1, nx, ewx)] : 0.0;
+        }
         const double2 rv = *reinterpret_cast<const double2*>(stC + e);
         const double2 qv = *reinterpret_cast<const double2*>(stP + e);
         double2 pv;
@@ -1140,7 +1150,7 @@ KernelInfo kernel_for(int p, int mode) {
 // measured extra cost.  Candidates: chunk counts nc (chunk length capped so
 // CTAs stay close in z and share halo planes through L2), each with and
 // without splitting the ragged last wave.  The plan is simulated exactly.
-constexpr double kEdgeTileWeight = 1.35;  // edge-tile plane cost / interior (B200, p=3)
+constexpr double kEdgeTileWeight = 1.08;  // edge-tile plane cost / interior (B200, p=3, measured)
 
 Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
   const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
