@@ -129,6 +129,9 @@ struct SepParams {
 #ifndef BSPDE_UNROLL_PLANES
 #define BSPDE_UNROLL_PLANES 1
 #endif
+#ifndef BSPDE_YSKIP
+#define BSPDE_YSKIP 1
+#endif
 #ifndef BSPDE_ALL_EDGE
 #define BSPDE_ALL_EDGE 0
 #endif
@@ -390,9 +393,20 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
 // therefore interleaves two independent instruction streams, and the x-pass
 // row imbalance is diluted by the balanced back half.
 
+// tile kinds (compile-time variants of the plane loop): interior tiles use
+// the Toeplitz taps everywhere; edge tiles check classes per row/column;
+// ragged tiles (last tile row, fewer than TY valid rows) also skip the rows
+// below the grid
+constexpr int TILE_EDGE = 0, TILE_INTERIOR = 1, TILE_RAGGED = 2;
+
 struct ItemGeom {
   int x0, y0, zc0, zc1;
 };
+
+// valid output rows of a tile (< TY only in a ragged last tile row)
+__device__ __forceinline__ int tile_rows(const SepParams& prm, const ItemGeom& g) {
+  return min(TY, prm.ny - g.y0);
+}
 
 // Items: (tile, z-chunk) in tile-fastest order, dealt round-robin so all
 // CTAs stream neighbouring tiles at the same z in lockstep (x/y halo planes
@@ -464,9 +478,10 @@ struct Smem {
 
 // front half of plane jj (flat index f): wait for its stage, form p (CG),
 // x-pass of this warp's rows into X[f & 1]
-template <int P, int MODE, bool INTERIOR>
+template <int P, int MODE, int TK>
 __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm,
                                             const ItemGeom& g, int jj, uint32_t f, double beta) {
+  constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
@@ -491,7 +506,10 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
     // walked as one flat list of double2 pairs so all lanes stay busy.
     constexpr int PPR = HX / 2;                       // pairs per row
     constexpr int NROW = (HY + NW - 1) / NW;          // rows of warps 0.. (HY % NW) - 1
-    const int nrow = (warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1;
+    // a ragged last tile row only needs its valid rows + 2p halo rows
+    const int nrow = !RAGGED
+                         ? ((warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1)
+                         : max(0, (tile_rows(prm, g) + 2 * P - warp + NW - 1) / NW);
     const int npair = nrow * PPR;
     const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
     if (INTERIOR && cz == ewz) {
@@ -541,7 +559,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
 #pragma unroll
   for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
     const int row = warp + NW * m;
-    if (row < HY) {
+    if (row < HY && (!RAGGED || row < tile_rows(prm, g) + 2 * P)) {
       const double* w = stP + row * HX + 2 * lane;
       double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
@@ -598,11 +616,12 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
 }
 
 // back half of plane j (flat index f): y-pass, z-ring shift update, epilogue
-template <int P, int MODE, bool INTERIOR>
+template <int P, int MODE, int TK>
 __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm, const ItemGeom& g,
                                            int j, uint32_t f, double (&acc)[2 * P][RPT],
                                            double (&pr)[P][RPT], const double (&auxv)[RPT],
                                            double (&dsum)[3], double beta) {
+  constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, NA = C::NA, NS = C::NS, NC = C::NC, S = 2 * P;
@@ -634,7 +653,9 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     const double* x1c = X1 + (rg * RPT) * TX + cxl;
     const double* x2c = X2 + (rg * RPT) * TX + cxl;
     const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
-    if (fast_y) {
+    if (BSPDE_YSKIP && RAGGED && gy0 >= ny) {
+      // row group below the grid (ragged last tile row): nothing to filter
+    } else if (fast_y) {
 #pragma unroll
       for (int rr = 0; rr < RPT + 2 * P; ++rr) {
         const double a1 = x1c[rr * TX];
@@ -781,11 +802,12 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   }
 }
 
-template <int P, int MODE, bool INTERIOR>
+template <int P, int MODE, int TK>
 __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
                                          const CUtensorMap* tm1, const Smem& sm,
                                          const ItemGeom& g, uint32_t& flat, double beta,
                                          double (&dsum)[3], Producer<P, MODE>& prod) {
+  constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   constexpr int S = 2 * P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gx = g.x0 + (warp & 1) * 32 + lane;
@@ -802,7 +824,7 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 #pragma unroll
     for (int i = 0; i < RPT; ++i) pr[k][i] = 0.0;
 
-  plane_front<P, MODE, INTERIOR>(prm, sm, g, 0, flat, beta);
+  plane_front<P, MODE, TK>(prm, sm, g, 0, flat, beta);
   __syncthreads();
 #if BSPDE_UNROLL_PLANES > 1
 #pragma unroll 2
@@ -822,8 +844,8 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
           auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
       }
     }
-    if (j + 1 < nin) plane_front<P, MODE, INTERIOR>(prm, sm, g, j + 1, flat + 1, beta);
-    plane_back<P, MODE, INTERIOR>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
+    if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
+    plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
     __syncthreads();
     if (threadIdx.x == 0) {
       // the stage of plane j is consumed (x-pass one iteration ago, own p now)
@@ -879,9 +901,11 @@ __global__ void __launch_bounds__(NT, 1)
   for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
     const ItemGeom g = item_geom(prm, item);
     if (tile_interior<P, MODE>(prm, g))
-      run_item<P, MODE, true>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+      run_item<P, MODE, TILE_INTERIOR>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+    else if (tile_rows(prm, g) == TY)
+      run_item<P, MODE, TILE_EDGE>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
     else
-      run_item<P, MODE, false>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+      run_item<P, MODE, TILE_RAGGED>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
   }
 
   if (MODE == M_CGA) {
