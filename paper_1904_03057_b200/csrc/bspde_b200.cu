@@ -44,21 +44,30 @@ namespace {
 // ---------------------------------------------------------------------------
 // configuration
 //
-// One persistent CTA of 512 threads (16 warps) per SM.  Warp w owns output
-// columns 32*(w&1) .. +31 (one per lane) and output rows 4*(w>>1) .. +3 of the
-// 64x32 tile (the z ring of those 4 points lives in its registers); for the
-// x-pass and the CG p-formation it owns whole haloed rows w, w+16, w+32.
-#ifndef BSPDE_RPT
-#define BSPDE_RPT 4
-#endif
+// One persistent CTA per SM.  Warp w owns output columns 32*(w&1) .. +31
+// (one per lane) and output rows 4*(w>>1) .. +3 of the 64 x TY tile (the z
+// ring of those 4 points lives in its registers); for the x-pass and the CG
+// p-formation it owns whole haloed rows w, w+NW, w+2NW.  p <= 3: 16 warps
+// (512 threads, 128 registers), 64x32 tiles.  p >= 4: the ring of 2p+p
+// doubles per point needs more registers: 12 warps (384 threads, 168
+// registers), 64x24 tiles.
 constexpr int TX = 64;               // tile width (x)
-constexpr int TY = 32;               // tile height (y)
-constexpr int RPT = BSPDE_RPT;       // output rows per thread
-constexpr int NW = 2 * TY / RPT;     // warps (2 x-groups)
-constexpr int NT = 32 * NW;          // threads
+constexpr int RPT = 4;               // output rows per thread
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
-static_assert(TY == RPT * NW / 2, "mapping");
+
+#ifndef BSPDE_P5_WARPS
+#define BSPDE_P5_WARPS 12
+#endif
+__host__ __device__ constexpr int warps_of(int p) { return p <= 3 ? 16 : (p == 4 ? 12 : BSPDE_P5_WARPS); }
+__host__ __device__ constexpr int tile_h_of(int p) { return RPT * warps_of(p) / 2; }
+
+template <int P>
+struct Geo {
+  static constexpr int NW = warps_of(P);   // warps (2 x-groups)
+  static constexpr int NT = 32 * NW;       // threads
+  static constexpr int TY = tile_h_of(P);  // tile height (y)
+};
 
 enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
 
@@ -68,6 +77,7 @@ __host__ __device__ constexpr int edge_width_of(int p) {
 
 template <int P, int MODE>
 struct Cfg {
+  static constexpr int NW = Geo<P>::NW, NT = Geo<P>::NT, TY = Geo<P>::TY;
   static constexpr int R = 2 * P + 1;
   // TMA needs the box's inner start (x0 - PX) * 8 bytes to be 16-byte aligned:
   // the x halo is padded to an even width PX (odd p: one extra column per side)
@@ -78,7 +88,7 @@ struct Cfg {
   static constexpr int EW = edge_width_of(P);
   static constexpr int NC = 2 * EW + 1;          // max classes per axis
   static constexpr int NA = (MODE == M_CGA) ? 2 : 1;   // staged arrays per plane
-  static constexpr int NS = (MODE == M_CGA) ? (P <= 3 ? 3 : 2) : (P <= 3 ? 4 : 3);
+  static constexpr int NS = (MODE == M_CGA) ? 3 : 4;  // TMA stages (fits 227 KB for p = 1..5)
   static constexpr bool STIFF = (MODE != M_MASS);
   static constexpr bool INVD = (MODE == M_CGA || MODE == M_RESID);
   static constexpr int ARR = HX * HY;                        // doubles
@@ -404,8 +414,9 @@ struct ItemGeom {
 };
 
 // valid output rows of a tile (< TY only in a ragged last tile row)
+template <int P>
 __device__ __forceinline__ int tile_rows(const SepParams& prm, const ItemGeom& g) {
-  return min(TY, prm.ny - g.y0);
+  return min(Geo<P>::TY, prm.ny - g.y0);
 }
 
 // Items: (tile, z-chunk) in tile-fastest order, dealt round-robin so all
@@ -413,7 +424,9 @@ __device__ __forceinline__ int tile_rows(const SepParams& prm, const ItemGeom& g
 // are then L2 hits).  The first main_items form whole waves; each remaining
 // chunk (the ragged last wave) is split tail_split ways so it is spread over
 // all SMs instead of extending the makespan by a full chunk.
+template <int P>
 __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
+  constexpr int TY = Geo<P>::TY;
   const int tiles_xy = prm.tiles_x * prm.tiles_y;
   // branch-free: for main items jt < 0 maps to (it = item, sub = 0) via max()
   const int jt = max(item - prm.main_items, 0);
@@ -436,6 +449,7 @@ __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
 template <int P, int MODE>
 __device__ __forceinline__ bool tile_interior(const SepParams& prm, const ItemGeom& g) {
   using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   if (BSPDE_ALL_EDGE) return false;  // tuning: measure the edge-tile path everywhere
   return (g.x0 - C::PX >= prm.ew[2]) && (g.x0 + TX + C::PX <= prm.nx - prm.ew[2]) &&
          (g.y0 - P >= prm.ew[1]) && (g.y0 + TY + P <= prm.ny - prm.ew[1]);
@@ -450,8 +464,9 @@ struct Producer {
                                         const CUtensorMap* tm1, double* s_stage,
                                         uint64_t* s_full) {
     using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
     if (item >= prm.nitems) return;
-    const ItemGeom g = item_geom(prm, item);
+    const ItemGeom g = item_geom<P>(prm, item);
     const int nin = g.zc1 - g.zc0 + 2 * P;
     const int s = flat % C::NS;
     const int zb = g.zc0 - P + j + prm.ghost;
@@ -483,6 +498,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
                                             const ItemGeom& g, int jj, uint32_t f, double beta) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
@@ -509,7 +525,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
     // a ragged last tile row only needs its valid rows + 2p halo rows
     const int nrow = !RAGGED
                          ? ((warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1)
-                         : max(0, (tile_rows(prm, g) + 2 * P - warp + NW - 1) / NW);
+                         : max(0, (tile_rows<P>(prm, g) + 2 * P - warp + NW - 1) / NW);
     const int npair = nrow * PPR;
     const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
     if (INTERIOR && cz == ewz) {
@@ -559,7 +575,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
 #pragma unroll
   for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
     const int row = warp + NW * m;
-    if (row < HY && (!RAGGED || row < tile_rows(prm, g) + 2 * P)) {
+    if (row < HY && (!RAGGED || row < tile_rows<P>(prm, g) + 2 * P)) {
       const double* w = stP + row * HX + 2 * lane;
       double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
@@ -623,6 +639,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
                                            double (&dsum)[3], double beta) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   const TapSrc<P> T{prm};
   constexpr int R = C::R, HX = C::HX, NA = C::NA, NS = C::NS, NC = C::NC, S = 2 * P;
   constexpr int PX = C::PX;
@@ -857,10 +874,11 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(Geo<P>::NT, 1)
     sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
                const __grid_constant__ CUtensorMap tm1) {
   using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   constexpr int NS = C::NS;
 
   if (MODE == M_CGA) {
@@ -899,10 +917,10 @@ __global__ void __launch_bounds__(NT, 1)
   }
   uint32_t flat = 0;
   for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
-    const ItemGeom g = item_geom(prm, item);
+    const ItemGeom g = item_geom<P>(prm, item);
     if (tile_interior<P, MODE>(prm, g))
       run_item<P, MODE, TILE_INTERIOR>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
-    else if (tile_rows(prm, g) == TY)
+    else if (tile_rows<P>(prm, g) == TY)
       run_item<P, MODE, TILE_EDGE>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
     else
       run_item<P, MODE, TILE_RAGGED>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
@@ -1092,6 +1110,7 @@ struct KernelInfo {
   const void* fn;
   size_t smem;
   int ctas_per_sm;
+  int nt;  // threads per CTA
 };
 
 struct Launch {
@@ -1134,14 +1153,16 @@ namespace {
 template <int P, int MODE>
 KernelInfo kernel_info() {
   using C = Cfg<P, MODE>;
+  [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   KernelInfo ki;
   ki.fn = reinterpret_cast<const void*>(&sep_kernel<P, MODE>);
   ki.smem = C::smem_bytes();
+  ki.nt = NT;
   static int ctas = -1;
   if (ctas < 0) {
     cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ki.smem);
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ki.fn, NT, ki.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ki.fn, ki.nt, ki.smem);
     ctas = std::max(n, 1);
   }
   ki.ctas_per_sm = ctas;
@@ -1177,6 +1198,7 @@ KernelInfo kernel_for(int p, int mode) {
 constexpr double kEdgeTileWeight = 1.08;  // edge-tile plane cost / interior (B200, p=3, measured)
 
 Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
+  const int TY = tile_h_of(pl->p);
   const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
   const int tiles = tx * ty;
   const int slots = std::max(1, pl->num_sms * ki.ctas_per_sm);
@@ -1258,7 +1280,7 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
                         (cuuint64_t)(pl->d.nz + 2 * p)};
   cuuint64_t strides[2] = {(cuuint64_t)(pl->d.pitch_y * 8), (cuuint64_t)(pl->pitch_z * 8)};
   const int px = p + (p & 1);
-  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(TY + 2 * p), 1u};
+  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(tile_h_of(p) + 2 * p), 1u};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1281,7 +1303,7 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
   sp.pitch_z = pl->pitch_z;
   for (int a = 0; a < 3; ++a) sp.ew[a] = d.ew[a];
   sp.tiles_x = (d.nx + TX - 1) / TX;
-  sp.tiles_y = (d.ny + TY - 1) / TY;
+  sp.tiles_y = (d.ny + tile_h_of(pl->p) - 1) / tile_h_of(pl->p);
   for (int k = 0; k < MAXTAP; ++k) {
     sp.tzm[k] = sp.tzk[k] = sp.tym[k] = sp.tyk[k] = sp.txm[k] = sp.txk[k] = 0.0;
   }
@@ -1369,7 +1391,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
     m1 = m0;
   }
   void* args[3] = {&sp, &m0, &m1};
-  CUDA_TRY(cudaLaunchKernel(ki.fn, dim3(ln.grid), dim3(NT), args, ki.smem, st));
+  CUDA_TRY(cudaLaunchKernel(ki.fn, dim3(ln.grid), dim3(ki.nt), args, ki.smem, st));
   pl->launches++;
   return BSPDE_OK;
 }
