@@ -29,8 +29,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALG_BYTES_PASS_A = 24  # read r, p_old; write Ap              (per DoF)
-ALG_BYTES_PASS_B = 56  # read x, r, p_old, Ap; write x, r, p  (per DoF)
-ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B
+# pass B reads r, p_old, Ap and writes r, p (40 B); every other pass it also
+# reads and writes x (56 B): x moves once per two iterations
+ALG_BYTES_PASS_B = 48  # average over the pair
+ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B  # 72
+SURVEY_BYTES_ITER = 80  # x, r, p, Ap streams of the textbook fused CG
 # ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
 # filled from the committed profile summary when present
 TRAFFIC = {}
@@ -259,7 +262,9 @@ def run_ours(args, rank, world, local_rank):
     b_gbs = ALG_BYTES_PASS_B * local_dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
     dom = "pass_b" if kt["pass_b_ms"] >= kt["pass_a_ms"] else "pass_a"
     ach = b_gbs if dom == "pass_b" else a_gbs
-    it_gbs = ALG_BYTES_ITER * local_dofs / ((kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3) / 1e9
+    it_s = (kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3
+    it_gbs = ALG_BYTES_ITER * local_dofs / it_s / 1e9
+    it_gbs80 = SURVEY_BYTES_ITER * local_dofs / it_s / 1e9  # DoF-it rate vs the 80 B roofline
 
     # -- end to end through the public API: u from/to pinned host memory each step --
     e2e = e2e_rate(step, u, u0, lay, dofs, min(args.steps, 3), stream, barrier, max_over_ranks)
@@ -283,7 +288,8 @@ def run_ours(args, rank, world, local_rank):
                      "alg_bytes_per_dof": ALG_BYTES_PASS_B if dom == "pass_b" else ALG_BYTES_PASS_A,
                      "pass_a_ms": kt["pass_a_ms"], "pass_b_ms": kt["pass_b_ms"],
                      "pass_a_gbs": a_gbs, "pass_b_gbs": b_gbs,
-                     "cg_iteration_gbs": it_gbs, "cg_iteration_frac": it_gbs / peak},
+                     "cg_iteration_gbs": it_gbs, "cg_iteration_frac": it_gbs / peak,
+                     "cg_iteration_frac_80B": it_gbs80 / peak},
         "clocks": clocks,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -296,7 +302,7 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def kernel_times(op, u, F, dt, stream, world, reps=5):
+def kernel_times(op, u, F, dt, stream, world, reps=9):
     """Average device duration of CG pass A and pass B (same stream, events),
     on a copy of the current state (the timed solve is already over)."""
     import torch

@@ -948,6 +948,22 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 
 constexpr int NTB = 256;
 
+#ifndef BSPDE_PB_UNROLL
+#define BSPDE_PB_UNROLL 1
+#endif
+#ifndef BSPDE_PB_HINTS
+#define BSPDE_PB_HINTS 0
+#endif
+// streaming loads/stores of the CG vectors (6.4 GB each at C3: no L2 reuse)
+__device__ __forceinline__ double2 ld2(const double* p) {
+  if (BSPDE_PB_HINTS) return __ldcs(reinterpret_cast<const double2*>(p));
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void st2(double* p, double2 v) {
+  if (BSPDE_PB_HINTS) __stcs(reinterpret_cast<double2*>(p), v);
+  else *reinterpret_cast<double2*>(p) = v;
+}
+
 __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->active)) return;
   __shared__ double s_red[(NTB / 32) * 4];
@@ -981,13 +997,16 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     const double* apr = prm.ap + base;
     if (even) {
       const int npair = nx >> 1;
+#if BSPDE_PB_UNROLL > 1
+#pragma unroll 2
+#endif
       for (int q = lane; q < npair; q += 32) {
         const int xx = 2 * q;
         double2 xv = make_double2(0.0, 0.0);
-        if (xup) xv = *reinterpret_cast<const double2*>(xr + xx);  // issued with the others
-        const double2 rv = *reinterpret_cast<const double2*>(rrw + xx);
-        const double2 pv = *reinterpret_cast<const double2*>(pr + xx);
-        const double2 av = *reinterpret_cast<const double2*>(apr + xx);
+        if (xup) xv = ld2(xr + xx);  // issued with the others
+        const double2 rv = ld2(rrw + xx);
+        const double2 pv = ld2(pr + xx);
+        const double2 av = ld2(apr + xx);
         const double i0 = (xx >= ewx && xx < nx - ewx) ? inv_int : trow[cls_of(xx, nx, ewx)];
         const double i1 =
             (xx + 1 >= ewx && xx + 1 < nx - ewx) ? inv_int : trow[cls_of(xx + 1, nx, ewx)];
@@ -997,7 +1016,7 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
         if (xup) {
           xn.x = __dadd_rn(__dadd_rn(xv.x, __dmul_rn(apend, pv.x)), __dmul_rn(alpha, pn.x));
           xn.y = __dadd_rn(__dadd_rn(xv.y, __dmul_rn(apend, pv.y)), __dmul_rn(alpha, pn.y));
-          *reinterpret_cast<double2*>(xr + xx) = xn;
+          st2(xr + xx, xn);
         }
         rn.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
         rn.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
@@ -1005,8 +1024,8 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
         rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
         rr = fma(rn.x, rn.x, rr);
         rr = fma(rn.y, rn.y, rr);
-        *reinterpret_cast<double2*>(rrw + xx) = rn;
-        *reinterpret_cast<double2*>(pr + xx) = pn;
+        st2(rrw + xx, rn);
+        st2(pr + xx, pn);
       }
       if ((nx & 1) && lane == 0) {
         const int xx = nx - 1;
@@ -1038,18 +1057,30 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
 }
 
 // Completes a deferred x update: x += alpha_pend * p (p = the last p_k).
+// Same row partition and double2 accesses as pass B.
 __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->x_pending)) return;
   const double a = ld_vol(&prm.state->alpha_pend);
-  const long long nrows = (long long)prm.nz * prm.ny;
-  const int lane = threadIdx.x & 31;
-  for (long long row = blockIdx.x * (long long)(NTB / 32) + (threadIdx.x >> 5); row < nrows;
-       row += (long long)gridDim.x * (NTB / 32)) {
-    const int zl = (int)(row / prm.ny), y = (int)(row - (long long)zl * prm.ny);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nx = prm.nx, ny = prm.ny;
+  const int nrows = prm.nz * ny;
+  const int r0 = blockIdx.x * prm.rows_per_cta;
+  const int r1 = min(r0 + prm.rows_per_cta, nrows);
+  for (int row = r0 + warp; row < r1; row += NTB / 32) {
+    const int zl = row / ny, y = row - zl * ny;
     const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
     double* xr = prm.x + base;
     const double* pr = prm.p + base;
-    for (int xx = lane; xx < prm.nx; xx += 32) xr[xx] = __dadd_rn(xr[xx], __dmul_rn(a, pr[xx]));
+    const int npair = nx >> 1;
+#pragma unroll 2
+    for (int q = lane; q < npair; q += 32) {
+      double2 xv = *reinterpret_cast<const double2*>(xr + 2 * q);
+      const double2 pv = *reinterpret_cast<const double2*>(pr + 2 * q);
+      xv.x = __dadd_rn(xv.x, __dmul_rn(a, pv.x));
+      xv.y = __dadd_rn(xv.y, __dmul_rn(a, pv.y));
+      *reinterpret_cast<double2*>(xr + 2 * q) = xv;
+    }
+    if ((nx & 1) && lane == 0) xr[nx - 1] = __dadd_rn(xr[nx - 1], __dmul_rn(a, pr[nx - 1]));
   }
 }
 
@@ -1426,8 +1457,8 @@ int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double*
   const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
   void* args[1] = {&bp};
   if (flush) {
-    CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&x_flush_kernel),
-                              dim3(pl->num_sms * 8), dim3(NTB), args, 0, st));
+    CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&x_flush_kernel), dim3(grid),
+                              dim3(NTB), args, 0, st));
     finalize_kernel<<<1, 32, 0, st>>>(bp.state, 3);
     pl->launches += 2;
     CUDA_TRY(cudaGetLastError());
