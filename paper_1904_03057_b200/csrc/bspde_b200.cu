@@ -948,6 +948,10 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 
 constexpr int NTB = 256;
 
+// TMA L2 promotion of the plane boxes: 0 none, 1 64B, 2 128B, 3 256B
+#ifndef BSPDE_L2PROMO
+#define BSPDE_L2PROMO 1
+#endif
 #ifndef BSPDE_PB_UNROLL
 #define BSPDE_PB_UNROLL 1
 #endif
@@ -1315,7 +1319,7 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    (CUtensorMapL2promotion)BSPDE_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" +
                                                           std::to_string((int)rc) + ")");
   return BSPDE_OK;
