@@ -9,6 +9,7 @@ hand-written sm_100a CUDA kernels (``csrc/bspde_b200.cu``) behind a C ABI
 multi-GPU sharding.  There is no CPU fallback.
 """
 
+from .boundary import FACE_NAMES, DirichletPenalty, Neumann, Robin, realize_bc
 from .domain import BoxDomain, Grid
 from .errors import (ConditioningWarning, ConfigurationError, DegreeError, DeterminismError,
                      DivergenceError, IndefiniteOperatorError, NativeLibraryError,
@@ -21,7 +22,8 @@ from .system import SystemData, build_system, heat_system, mass_system
 from .transform import direct_transform, sample_solution, transform_field
 
 __all__ = [
-    "BoxDomain", "Grid", "basis_extension", "edge_width", "gram_factor", "min_axis_length",
+    "BoxDomain", "Grid", "FACE_NAMES", "Robin", "Neumann", "DirichletPenalty", "realize_bc",
+    "basis_extension", "edge_width", "gram_factor", "min_axis_length",
     "GramFactor", "SystemData", "build_system", "heat_system", "mass_system",
     "B200Operator", "OpStats", "make_operator", "assembled_rhs",
     "SolveConfig", "SolveReport", "pcg", "pcg_device",

@@ -187,6 +187,12 @@ class GramFactor:
     def diagonal_by_class(self) -> np.ndarray:
         return self.table[:, self.degree].copy()
 
+    def plus(self, add: np.ndarray) -> "GramFactor":
+        """Factor with ``add`` (same class layout) added to its table."""
+        table = self.table + add
+        table.setflags(write=False)
+        return GramFactor(degree=self.degree, n=self.n, ew=self.ew, table=table)
+
 
 @lru_cache(maxsize=None)
 def _exact_rows(p: int, deriv: int):
@@ -247,6 +253,93 @@ def degenerate_factor(p: int, kind: str) -> GramFactor:
         table[0, p] = 1.0
     table.setflags(write=False)
     return GramFactor(degree=p, n=1, ew=0, table=table)
+
+
+# ---------------------------------------------------------------------------
+# box-face (Robin / penalty) terms (reference: assembly.py:138-232)
+
+
+def bspline_value(p: int, x) -> Fraction:
+    """Exact ``beta^p(x)``."""
+    x = Fraction(x)
+    for lo, hi, coeffs in bspline_pieces(p, 0):
+        if lo <= x < hi:
+            return sum((c * x ** k for k, c in enumerate(coeffs)), Fraction(0))
+    return Fraction(0)
+
+
+def single_integral(p: int, s, lo=None, hi=None) -> Fraction:
+    """Exact ``int_lo^hi beta^p(x - s) dx``."""
+    s = Fraction(s)
+    tot = Fraction(0)
+    for a, b, coeffs in bspline_pieces(p, 0):
+        a, b = a + s, b + s
+        if lo is not None:
+            a = max(a, Fraction(lo))
+        if hi is not None:
+            b = min(b, Fraction(hi))
+        if b > a:
+            tot += _pint(_pshift(list(coeffs), s), a, b)
+    return tot
+
+
+@lru_cache(maxsize=None)
+def face_values(p: int) -> tuple:
+    """``beta(u_face - pos_i)`` for the first ``ew`` extended positions of the
+    low face (``face_point_values``, assembly.py:173-180); all later entries
+    are zero and the high face is the mirror image."""
+    _check_degree(p)
+    ext = basis_extension(p)
+    vals = tuple(bspline_value(p, ext - i) for i in range(edge_width(p)))
+    assert bspline_value(p, ext - edge_width(p)) == 0
+    return vals
+
+
+def face_vector(p: int, num_nodes: int, side: int) -> np.ndarray:
+    """Full-length face value vector (length ``num_nodes + 2*ext``)."""
+    n = num_nodes + 2 * basis_extension(p)
+    v = np.zeros(n)
+    f = [float(x) for x in face_values(p)]
+    if side == 0:
+        v[: len(f)] = f
+    else:
+        v[n - len(f):] = f[::-1]
+    return v
+
+
+def face_table(p: int, side: int) -> np.ndarray:
+    """Class-table addition (shape ``(2ew+1, 2p+1)``) of the rank-1 normal
+    factor ``v v^T`` of one face (``make_face_term`` pair factors): rows of
+    classes ``0..ew-1`` for the low face, ``ew+1..2ew`` for the high face."""
+    ew = edge_width(p)
+    v = face_values(p)
+    add = np.zeros((2 * ew + 1, 2 * p + 1))
+    for m in range(ew):
+        for mm in range(ew):
+            k = mm - m  # column offset of row m (low face)
+            if abs(k) <= p:
+                if side == 0:
+                    add[m, k + p] = float(v[m] * v[mm])
+                else:  # row n-1-m, column n-1-mm: offset m - mm
+                    add[2 * ew - m, -k + p] = float(v[m] * v[mm])
+    return add
+
+
+@lru_cache(maxsize=None)
+def surface_single_rows(p: int) -> tuple:
+    """``int_0^inf beta(u - pos_i) du`` for the first ``ew`` positions
+    (``surface_single_positions``, assembly.py:158-170); interior rows are 1."""
+    ext = basis_extension(p)
+    return tuple(single_integral(p, i - ext, lo=0) for i in range(edge_width(p)))
+
+
+def surface_single_vector(p: int, num_nodes: int) -> np.ndarray:
+    n = num_nodes + 2 * basis_extension(p)
+    s = np.ones(n)
+    rows = [float(x) for x in surface_single_rows(p)]
+    s[: len(rows)] = rows
+    s[n - len(rows):] = rows[::-1]
+    return s
 
 
 def taps_header() -> str:

@@ -4,10 +4,12 @@ The reference solves steady problems only.  One implicit
 Euler step of ``u_t = kappa * Laplace(u) + f`` in the Galerkin B-spline space
 is exactly a reference system solve:
 
-    b = M u_prev + dt F                  M: mass system (D=0, mu=1)
-    (M + dt*kappa*K) u = b, x0 = u_prev  Jacobi-PCG
+    b = M u_prev + dt (F + G)            M: mass system (D=0, mu=1)
+    (M + dt*(kappa*K + W)) u = b, x0 = u_prev  Jacobi-PCG
 
-with ``F = assembled_rhs(mass system, p, q)`` the Galerkin source.  Here both
+with ``F = assembled_rhs(mass system, p, q)`` the Galerkin source and
+``W``/``G`` the box-face surface terms of the boundary conditions (Robin /
+DirichletPenalty; ``G`` the penalty right-hand side, cf. ``face_rhs``).  Here both
 the RHS (``sep_kernel<P, M_MASS>``: fused mass apply + axpy) and the CG run
 on the GPU with every field resident in HBM between steps.
 """
@@ -22,13 +24,17 @@ from .domain import BoxDomain, Grid
 from .errors import ValidationError
 from .operator import B200Operator
 from .solver import SolveConfig, SolveReport, pcg_device
+from .boundary import realize_bc
 from .system import heat_system
 from .transform import transform_field
 
 
 @dataclass
 class HeatProblem:
-    """Constant-conductivity heat problem on a box with natural (Neumann) faces.
+    """Constant-conductivity heat problem on a box.
+
+    ``bc``: a condition or ``{face: condition}`` dict (:mod:`.boundary`;
+    default: natural Neumann faces everywhere).
 
     ``initial`` and ``source`` accept a scalar, node samples or a callable of
     the node coordinates (like the reference's ProblemSpec fields); pass
@@ -44,6 +50,7 @@ class HeatProblem:
     source: object = 0.0
     initial_coeffs: np.ndarray = None
     source_coeffs: np.ndarray = None
+    bc: object = None
 
     def __post_init__(self):
         if not self.dt > 0:
@@ -67,7 +74,9 @@ class HeatSolver:
     def __init__(self, problem: HeatProblem, config: SolveConfig = None, device=None):
         self.problem = problem
         self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
-        data = heat_system(problem.grid, problem.degree, problem.dt, problem.conductivity)
+        specs = realize_bc(problem.bc, problem.grid) if problem.bc is not None else ()
+        data = heat_system(problem.grid, problem.degree, problem.dt, problem.conductivity,
+                           face_specs=specs)
         self.data = data
         self.dt = float(problem.dt)
         self.op = B200Operator(data, device=device)
@@ -88,6 +97,14 @@ class HeatSolver:
             self.F = lay.alloc(dev)
             self.op.mass_apply_device(qb, self.F)  # F = vol * (M(x)M(x)M) q
             del qb
+        if any(ft.rhs_weight != 0.0 for ft in data.faces):
+            # penalty values: heat_system scaled the face terms by dt, so the
+            # per-unit-time surface source is face_rhs / dt (added once)
+            g = lay.upload((data.face_rhs() / self.dt).reshape(lay.owned_shape), dev)
+            if self.F is None:
+                self.F = g
+            else:
+                self.F.add_(g)
         self.reports = []
 
     @classmethod

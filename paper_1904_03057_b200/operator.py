@@ -137,10 +137,11 @@ def make_operator(data, strategy="b200", workers=1, memory_budget=None, device=N
 
 
 def assembled_rhs(data: SystemData, n_s, qcoef_ext, workers=1, device=None):
-    """``t = vol * (R(x)R(x)R) q`` (cf. operator.py:417-441) on the GPU.
+    """``t = vol * (R(x)R(x)R) q + face_rhs`` (cf. operator.py:417-441).
 
-    For a box with natural faces and ``n_s == n_b`` the source band R equals
-    the mass Gram factor (edge rows included), so this is the mass apply.
+    For a box and ``n_s == n_b`` the source band R equals the mass Gram
+    factor (edge rows included), so the volume part is the mass apply (GPU);
+    penalty faces add their rank-1 surface terms (``SystemData.face_rhs``).
     """
     if int(n_s) != int(data.n_b):
         raise ConfigurationError("the b200 RHS realizes n_s == n_b (source degree = basis degree)")
@@ -149,4 +150,7 @@ def assembled_rhs(data: SystemData, n_s, qcoef_ext, workers=1, device=None):
     cb, ob = op._io_buffers()
     op.layout.upload(q.reshape(op.layout.owned_shape), op.device, cb)
     op.mass_apply_device(cb, ob)
-    return op.layout.download(ob).reshape(data.cext).astype(data.dtype, copy=False)
+    t = op.layout.download(ob).reshape(data.cext)
+    if any(ft.rhs_weight != 0.0 for ft in data.faces):
+        t = t + data.face_rhs()
+    return t.astype(data.dtype, copy=False)

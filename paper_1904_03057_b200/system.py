@@ -21,8 +21,8 @@ import numpy as np
 
 from .domain import BoxDomain, Grid
 from .errors import ConfigurationError, ValidationError
-from .gram import (GramFactor, basis_extension, degenerate_factor, edge_width,
-                   gram_factor, min_axis_length)
+from .gram import (GramFactor, basis_extension, degenerate_factor, edge_width, face_table,
+                   face_vector, gram_factor, min_axis_length, surface_single_vector)
 
 
 def _constant_value(f, what):
@@ -37,6 +37,21 @@ def _constant_value(f, what):
             f"the b200 strategy realizes constant {what}; variable-coefficient "
             "operators are a later milestone (DESIGN.md 'next')")
     return v
+
+
+@dataclass(frozen=True)
+class FaceTerm:
+    """One box-face surface term (reference ``FaceTerm``, assembly.py:183-198).
+
+    ``axis``/``side`` use reference axis order; the operator term is
+    ``weight * (v v^T)_axis (x) (h M)_other axes`` with ``v`` the face point
+    values, the right-hand side ``rhs_weight * v (x) (h s)_other axes``.
+    """
+
+    axis: int
+    side: int
+    weight: float
+    rhs_weight: float
 
 
 @dataclass
@@ -75,6 +90,27 @@ class SystemData:
     @property
     def ew3(self):
         return tuple(f.ew for f in self.mass)
+
+    def face_rhs(self) -> np.ndarray:
+        """Penalty right-hand-side surface additions (reference ``face_rhs``,
+        assembly.py:488-501): a rank-1 tensor per face with a value."""
+        grid = self.domain.grid
+        out = np.zeros(self.cext)
+        for ft in self.faces:
+            if ft.rhs_weight == 0.0:
+                continue
+            vecs = []
+            for ax in range(self.dim):
+                n = grid.extents[ax]
+                if ax == ft.axis:
+                    vecs.append(face_vector(self.n_b, n, ft.side))
+                else:
+                    vecs.append(surface_single_vector(self.n_b, n) * grid.step[ax])
+            t = vecs[0]
+            for v in vecs[1:]:
+                t = np.multiply.outer(t, v)
+            out += ft.rhs_weight * t
+        return out
 
     # -- Jacobi diagonal by class (operator.py:190-209 for constant fields) --
     def diag_table(self) -> np.ndarray:
@@ -117,23 +153,38 @@ def build_system(domain, n_b, n_p, dcoef_ext, mcoef_ext, face_specs=(), dtype=np
 
     ``dcoef_ext``/``mcoef_ext`` are the (constant) diffusion and absorption
     coefficient fields on the extended parameter grid, or scalars.
-    ``face_specs`` must be empty: Robin / penalty faces are the next milestone.
+    ``face_specs``: ``(axis, side, weight, rhs_value_or_None)`` box-face
+    surface terms (Robin / DirichletPenalty, see :func:`.boundary.realize_bc`).
     """
     if not isinstance(domain, BoxDomain):
         raise ConfigurationError("the b200 strategy supports box domains (mask domains: out of scope)")
-    if face_specs:
-        raise ConfigurationError(
-            "the b200 strategy realizes natural (Neumann) faces; Robin / penalty "
-            "face terms are the next milestone")
     if not 1 <= int(n_b) <= 5:
         raise ValidationError(f"basis degree {n_b} not in 1..5")
-    grid = domain.grid
     D = _constant_value(dcoef_ext, "diffusion")
     mu = _constant_value(mcoef_ext, "absorption")
-    return _make(domain, int(n_b), int(n_p), D, mu, np.dtype(dtype))
+    return _make(domain, int(n_b), int(n_p), D, mu, np.dtype(dtype), face_specs)
 
 
-def _make(domain, p, n_p, D, mu, dtype) -> SystemData:
+def _face_terms(face_specs, dim):
+    out = []
+    for spec in face_specs or ():
+        try:
+            axis, side, weight, rhs_value = spec
+        except (TypeError, ValueError):
+            raise ValidationError(f"face spec {spec!r} is not (axis, side, weight, rhs_value)")
+        if not (isinstance(axis, (int, np.integer)) and 0 <= axis < dim):
+            raise ValidationError(f"face axis {axis!r} not in 0..{dim - 1}")
+        if side not in (0, 1):
+            raise ValidationError(f"face side {side!r} not 0 or 1")
+        weight = float(weight)
+        if not np.isfinite(weight):
+            raise ValidationError(f"face weight {weight} is not finite")
+        rhs_w = 0.0 if rhs_value is None else float(rhs_value) * weight
+        out.append(FaceTerm(int(axis), int(side), weight, rhs_w))
+    return out
+
+
+def _make(domain, p, n_p, D, mu, dtype, face_specs=()) -> SystemData:
     grid = domain.grid
     ext = basis_extension(p)
     for n in grid.extents:
@@ -145,22 +196,39 @@ def _make(domain, p, n_p, D, mu, dtype) -> SystemData:
     mass = [gram_factor(p, n, "mass") for n in grid.extents]
     stiff = [gram_factor(p, n, "stiff") for n in grid.extents]
     cst = [vol * D / h ** 2 for h in grid.step]
+    faces = _face_terms(face_specs, grid.dim)
+    # A face on axis a adds weight * (v v^T)_a (x) (h M)_others =
+    # c_a * [(weight * h_a / D) * (v v^T)]_a (x) M_others to the c_a K_a term
+    # (c_a = vol * D / h_a^2): the normal factor folds into the edge-row
+    # classes of K_a; interior taps are unchanged.
+    for ft in faces:
+        if not D > 0.0:
+            raise ConfigurationError(
+                "the b200 strategy realizes face terms inside the diffusion factors; "
+                "they need a positive diffusion coefficient")
+        h = grid.step[ft.axis]
+        stiff[ft.axis] = stiff[ft.axis].plus((ft.weight * h / D) * face_table(p, ft.side))
     pad = 3 - grid.dim
     mass3 = tuple([degenerate_factor(p, "mass")] * pad + mass)
     stiff3 = tuple([degenerate_factor(p, "stiff")] * pad + stiff)
     c_stiff3 = tuple([0.0] * pad + cst)
     return SystemData(
         domain=domain, n_b=p, n_p=n_p, step=grid.step, cext=cext, ext=ext, dtype=dtype,
-        diffusion=D, absorption=mu, faces=[], dims3=_as3(cext, 1), mass=mass3,
+        diffusion=D, absorption=mu, faces=faces, dims3=_as3(cext, 1), mass=mass3,
         stiff=stiff3, c_mass=vol * mu, c_stiff=c_stiff3, vol=vol)
 
 
-def heat_system(grid: Grid, degree: int, dt: float, conductivity: float = 1.0) -> SystemData:
-    """``A = M + dt*kappa*K`` of one implicit-Euler step (D = dt*kappa, mu = 1)."""
+def heat_system(grid: Grid, degree: int, dt: float, conductivity: float = 1.0,
+                face_specs=()) -> SystemData:
+    """``A = M + dt*(kappa*K + W)`` of one implicit-Euler step (D = dt*kappa,
+    mu = 1).  ``face_specs`` are the steady surface terms ``W`` (e.g. from
+    :func:`.boundary.realize_bc`); their weights are scaled by ``dt`` here,
+    so ``face_rhs()`` is ``dt`` times the steady penalty right-hand side."""
     if not dt > 0:
         raise ValidationError(f"dt must be positive, got {dt}")
+    scaled = [(a, s, float(w) * float(dt), v) for a, s, w, v in (face_specs or ())]
     return _make(BoxDomain(grid), int(degree), int(degree), float(dt) * float(conductivity),
-                 1.0, np.dtype(np.float64))
+                 1.0, np.dtype(np.float64), scaled)
 
 
 def mass_system(grid: Grid, degree: int) -> SystemData:
@@ -168,5 +236,5 @@ def mass_system(grid: Grid, degree: int) -> SystemData:
     return _make(BoxDomain(grid), int(degree), int(degree), 0.0, 1.0, np.dtype(np.float64))
 
 
-__all__ = ["SystemData", "build_system", "heat_system", "mass_system", "edge_width",
-           "GramFactor"]
+__all__ = ["SystemData", "FaceTerm", "build_system", "heat_system", "mass_system",
+           "edge_width", "GramFactor"]

@@ -15,6 +15,9 @@ Fixtures:
                   lambda=4, Jacobi-PCG tol 1e-10 (+ tol 1e-12 solution)
   heat64.npz   -- C1: 64^3, p=3, lambda=4: 10-step CG counts at tol 1e-10,
                   inputs, and the step-1 solution at tol 1e-12
+  faces.npz    -- box-face Robin / penalty terms (build_system face_specs):
+                  OnTheFlyOperator.apply, jacobi_diagonal and assembled_rhs
+                  (volume + face_rhs) for p=1..5 (3-D) and 2-D / 1-D cases
 """
 
 import os
@@ -99,6 +102,47 @@ def rhs_cases():
     np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
 
 
+# (axis, side, weight, rhs_value) in reference axis order: Robin (1/(2 gamma)),
+# penalties with values, one Neumann face left out
+FACES_3D = [(0, 0, 1 / 1.4, None), (0, 1, 100.0, 2.0), (1, 0, 50.0, -1.0),
+            (2, 0, 0.8, None), (2, 1, 1e3, 0.5)]
+FACE_CASES = [
+    # (tag, extents, step, p, D, mu, face_specs)
+    ("p1", (9, 10, 11), (0.5, 1.0, 0.25), 1, 0.37, 1.3, FACES_3D),
+    ("p2", (9, 10, 11), (0.5, 1.0, 0.25), 2, 0.37, 1.3, FACES_3D),
+    ("p3", (9, 10, 11), (0.5, 1.0, 0.25), 3, 0.37, 1.3, FACES_3D),
+    ("p4", (10, 11, 12), (0.5, 1.0, 0.25), 4, 0.37, 1.3, FACES_3D),
+    ("p5", (10, 11, 12), (0.5, 1.0, 0.25), 5, 0.37, 1.3, FACES_3D),
+    ("p3_all", (8, 8, 8), (0.125, 0.125, 0.125), 3, 0.02, 1.0,
+     [(a, s, 1e4, 20.0) for a in range(3) for s in (0, 1)]),
+    ("p2_2d", (13, 9), (0.5, 0.25), 2, 0.8, 0.2, [(0, 1, 3.0, 1.5), (1, 0, 0.25, None)]),
+    ("p3_1d", (15,), (0.3,), 3, 0.7, 1.1, [(0, 0, 5.0, 1.0), (0, 1, 2.0, None)]),
+]
+
+
+def face_cases():
+    out = {}
+    rng = np.random.default_rng(4321)
+    for tag, ext_, step, p, D, mu, specs in FACE_CASES:
+        g = Grid(ext_, step)
+        ext = basis_extension(p)
+        shp = tuple(n + 2 * ext for n in g.extents)
+        data = build_system(BoxDomain(g), p, p, np.full(shp, D), np.full(shp, mu), specs)
+        op = make_operator(data, "onthefly")
+        c = rng.normal(size=data.cext)
+        q = rng.normal(size=data.cext)
+        out[f"{tag}_c"] = c
+        out[f"{tag}_t"] = op.apply(c)
+        out[f"{tag}_diag"] = op.jacobi_diagonal()
+        out[f"{tag}_q"] = q
+        out[f"{tag}_rhs"] = assembled_rhs(data, p, q)
+        out[f"{tag}_facerhs"] = assembled_rhs(data, p, np.zeros(data.cext))
+        out[f"{tag}_meta"] = np.array([p, D, mu] + list(step) + list(ext_), dtype=float)
+        out[f"{tag}_faces"] = np.array([[a, s, w, np.nan if v is None else v]
+                                        for a, s, w, v in specs], dtype=float)
+    np.savez_compressed(os.path.join(OUT, "faces.npz"), **out)
+
+
 def heat_inputs(ncoef, p=3, lam=4.0):
     ext = basis_extension(p)
     N = ncoef - 2 * ext
@@ -166,13 +210,15 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "heat16", "heat64"]
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "heat16", "heat64"]
     if "gram" in which:
         gram()
     if "apply" in which:
         apply_cases()
     if "rhs" in which:
         rhs_cases()
+    if "faces" in which:
+        face_cases()
     if "heat16" in which:
         heat(16, 10, "heat16.npz")
     if "heat64" in which:

@@ -50,8 +50,8 @@ def test_constant_field_detection():
     f[3, 3, 3] = 0.6
     with pytest.raises(ConfigurationError):
         build_system(dom, 3, 3, f, np.full(shp, 2.0), [])
-    with pytest.raises(ConfigurationError):
-        build_system(dom, 3, 3, 1.0, 1.0, [(0, 0, 1.0, None)])
+    # box-face terms are realized (tests/test_faces.py)
+    assert len(build_system(dom, 3, 3, 1.0, 1.0, [(0, 0, 1.0, None)]).faces) == 1
     with pytest.raises(ValidationError):
         build_system(dom, 6, 3, 1.0, 1.0, [])
 
