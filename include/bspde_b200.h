@@ -57,6 +57,9 @@ typedef struct bspde_plan bspde_plan; /* opaque */
  * 0..ew-1 = first rows, ew = interior (Toeplitz), ew+1..2ew = last rows.
  * inv_diag_table[(cz*NCy + cy)*NCx + cx] (NCa = 2*ew[a]+1) is the Jacobi
  * preconditioner 1/diag (1 where diag == 0, solver.py:69-73) per class triple.
+ * Box-face Robin / penalty terms (assembly.py:201-232) arrive folded into
+ * the edge-row classes of stiff_table (the interior row must stay the
+ * Toeplitz taps: the kernels use compile-time interior taps).
  */
 typedef struct {
   int32_t device;       /* CUDA device ordinal the plan (and its launches) use */
