@@ -1574,6 +1574,19 @@ int bspde_plan_create(const bspde_plan_desc* desc, bspde_plan** out) {
     if (!d.mass_table[a] || !d.stiff_table[a]) return fail(BSPDE_ERR_ARG, "missing tables");
   }
   if (!d.inv_diag_table) return fail(BSPDE_ERR_ARG, "missing inverse diagonal table");
+  // the fast paths use compile-time interior taps: a non-degenerate axis'
+  // interior class row must be the unit Gram taps (faces live in edge rows)
+  for (int a = 0; a < 3; ++a) {
+    if (d.ew[a] == 0) continue;  // degenerate (padded) axis: tables only
+    const int Rr = 2 * d.degree + 1;
+    for (int k = 0; k < Rr; ++k) {
+      const double m = d.mass_table[a][d.ew[a] * Rr + k], kk = d.stiff_table[a][d.ew[a] * Rr + k];
+      const double gm = kHostGramM[d.degree - 1][k], gk = kHostGramK[d.degree - 1][k];
+      if (std::fabs(m - gm) > 1e-15 * std::fabs(gm) || std::fabs(kk - gk) > 1e-15 * std::fabs(gk) + 1e-300)
+        return fail(BSPDE_ERR_ARG, "interior table rows must be the unit B-spline Gram taps "
+                                   "(scale with c_mass / c_stiff; faces go in the edge rows)");
+    }
+  }
   if (d.z_offset < 0 || d.z_offset + d.nz > d.nz_global) return fail(BSPDE_ERR_ARG, "bad z slab");
   if (d.device < 0) return fail(BSPDE_ERR_ARG, "bad device ordinal");
   {
