@@ -164,6 +164,28 @@ int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
 int bspde_cg_read_report(bspde_plan* plan, const void* scratch,
                          bspde_cg_report* report, int32_t* active, void* stream);
 
+/* ---- B-spline field transforms (setup / I/O; plan-free) ------------------
+ * Direct transform (node samples -> coefficients) of lines of a strided
+ * 3-D array, in place: line (a, b) starts at data + a*sa + b*sb and has n
+ * elements at the given stride; a varies fastest across threads.  Replaces
+ * _prefilter_lines (bspline.py:168-211) with its rounding order.  poles /
+ * gain as compute_poles(degree) (bspline.py:140-155, np.roots values);
+ * extension 0 = mirror, 1 = replicate, 2 = zero (direct_transform's
+ * policies).  npoles = 0 (degree <= 1) is a no-op. */
+int bspde_prefilter_lines(double* data, int32_t n, int64_t stride, int32_t na,
+                          int32_t nb, int64_t sa, int64_t sb, const double* poles,
+                          int32_t npoles, double gain, int32_t extension,
+                          void* stream);
+/* np.pad(..., ext, mode="reflect") along one axis of a 3-D array whose inner
+ * region [ext, dims[axis]-ext) is filled (transform_field, problem.py:178-194). */
+int bspde_reflect_pad(double* data, const int32_t* dims, const int64_t* strides,
+                      int32_t axis, int32_t ext, void* stream);
+/* out[i] = sum_t taps[t] * in[i + offset + t] along one axis (sample_solution,
+ * problem.py:330-348; accumulated in the reference's order), ntaps <= 11. */
+int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
+                   const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
+                   int32_t offset, const double* taps, int32_t ntaps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

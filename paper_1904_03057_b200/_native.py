@@ -86,6 +86,12 @@ SIGNATURES = [
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                        C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,
+                                        C.c_int32, _VP]),
+    ("bspde_reflect_pad", C.c_int, [_VP, _VP, _VP, C.c_int32, C.c_int32, _VP]),
+    ("bspde_fir_axis", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
+                                 C.c_int32, _VP]),
     ("bspde_cg_finalize", C.c_int, [_VP, _VP, C.c_int, _VP]),
     ("bspde_cg_read_report", C.c_int, [_VP, _VP, C.POINTER(CgReport),
                                        C.POINTER(C.c_int32), _VP]),

@@ -1088,6 +1088,147 @@ __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ Pa
   }
 }
 
+// ---------------------------------------------------------------------------
+// B-spline field transforms (setup / I/O)
+//
+// Direct transform (node samples -> coefficients): the reference's separable
+// causal/anticausal recursive prefilter (bspline.py:168-242), one thread per
+// line, every operation in the reference's rounding order (gain, truncated
+// series causal init at 1e-12, closed-form anticausal init).  Lines along y
+// or z are coalesced across threads; lines along x (stride 1 per thread) reuse
+// each 32-byte sector from L1 over four consecutive steps.
+
+__device__ __forceinline__ int mirror_index(int i, int n) {
+  if (n == 1) return 0;
+  const int period = 2 * n - 2;
+  i %= period;
+  return i >= n ? period - i : i;
+}
+
+struct Lines {
+  double* data;
+  int n;               // line length
+  long long stride;    // element stride along a line
+  int na, nb;          // line grid (a varies fastest across threads)
+  long long sa, sb;
+};
+
+__global__ void __launch_bounds__(128) prefilter_kernel(const Lines L, const int npoles,
+                                                        const double z0, const double z1,
+                                                        const int h0, const int h1,
+                                                        const double gain, const int mode) {
+  const long long line = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (line >= (long long)L.na * L.nb) return;
+  const int ia = (int)(line % L.na), ib = (int)(line / L.na);
+  double* c = L.data + ia * L.sa + ib * L.sb;
+  const long long s = L.stride;
+  const int n = L.n;
+  for (int ip = 0; ip < npoles; ++ip) {
+    const double z = ip ? z1 : z0;
+    const int H = ip ? h1 : h0;
+    // the first cascade reads the raw samples times the gain (c = lines * gain)
+    auto rd = [&](int k) -> double { return ip == 0 ? __dmul_rn(c[k * s], gain) : c[k * s]; };
+    double init = rd(0), zk = 1.0;
+    if (mode == 0) {  // mirror
+      for (int k = 1; k < H; ++k) {
+        zk = __dmul_rn(zk, z);
+        init = __dadd_rn(init, __dmul_rn(zk, rd(mirror_index(k, n))));
+      }
+    } else {  // replicate (1) / zero (2)
+      const int kmax = min(H, n);
+      for (int k = 1; k < kmax; ++k) {
+        zk = __dmul_rn(zk, z);
+        init = __dadd_rn(init, __dmul_rn(zk, rd(k)));
+      }
+      if (mode == 1 && H > n)  // geometric tail of the replicated edge sample
+        init = __dadd_rn(init, __ddiv_rn(__dmul_rn(rd(n - 1), pow(z, (double)n)), __dsub_rn(1.0, z)));
+    }
+    const double last = rd(n - 1);  // stage input at the right edge, pre-causal
+    double prev = init, prev2 = 0.0;
+    c[0] = init;
+    for (int k = 1; k < n; ++k) {
+      prev2 = prev;
+      prev = __dadd_rn(rd(k), __dmul_rn(z, prev));
+      c[k * s] = prev;
+    }
+    double cn;
+    if (mode == 0) {
+      cn = __dmul_rn(__ddiv_rn(z, __dsub_rn(__dmul_rn(z, z), 1.0)),
+                     __dadd_rn(prev, __dmul_rn(z, n >= 2 ? prev2 : prev)));
+    } else if (mode == 1) {
+      const double s_inf = __ddiv_rn(last, __dsub_rn(1.0, z));
+      cn = __dmul_rn(-z, __dadd_rn(__ddiv_rn(s_inf, __dsub_rn(1.0, z)),
+                                   __ddiv_rn(__dsub_rn(prev, s_inf), __dsub_rn(1.0, __dmul_rn(z, z)))));
+    } else {
+      cn = __ddiv_rn(__dmul_rn(z, prev), __dsub_rn(__dmul_rn(z, z), 1.0));
+    }
+    c[(n - 1) * s] = cn;
+    double nxt = cn;
+    for (int k = n - 2; k >= 0; --k) {
+      nxt = __dmul_rn(z, __dsub_rn(nxt, c[k * s]));
+      c[k * s] = nxt;
+    }
+  }
+}
+
+// whole-sample reflection of the ext pad planes of one axis (np.pad "reflect")
+__global__ void reflect_pad_kernel(double* data, const int d0, const int d1, const int d2,
+                                   const long long s0, const long long s1, const long long s2,
+                                   const int axis, const int ext) {
+  // thread grid: the two other axes x (2*ext pad positions)
+  const int da = axis == 0 ? d1 : d0, db = axis == 2 ? d1 : d2;
+  const long long sa = axis == 0 ? s1 : s0, sb = axis == 2 ? s1 : s2;
+  const int dn = axis == 0 ? d0 : (axis == 1 ? d1 : d2);
+  const long long sn = axis == 0 ? s0 : (axis == 1 ? s1 : s2);
+  const long long total = (long long)da * db * 2 * ext;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int ib = (int)(t % db);
+    long long r = t / db;
+    const int ia = (int)(r % da);
+    const int q = (int)(r / da);  // 0..2*ext-1
+    double* base = data + ia * sa + ib * sb;
+    int dst, src;
+    if (q < ext) {  // low side: index ext-1-i <- ext+1+i
+      dst = ext - 1 - q;
+      src = ext + 1 + q;
+    } else {        // high side: index dn-ext+i <- dn-ext-2-i
+      const int i = q - ext;
+      dst = dn - ext + i;
+      src = dn - ext - 2 - i;
+    }
+    base[dst * sn] = base[src * sn];
+  }
+}
+
+// out[i] = sum_t taps[t] * in[i + offset + t] along one axis (separable FIR;
+// sample_solution, problem.py:330-348), accumulated in the reference's order
+constexpr int MAXFIR = 11;
+struct Fir {
+  const double* in;
+  long long is0, is1, is2;
+  double* out;
+  int d0, d1, d2;  // output extents
+  long long os0, os1, os2;
+  int axis, offset, ntaps;
+  double taps[MAXFIR];
+};
+
+__global__ void __launch_bounds__(256) fir_axis_kernel(const __grid_constant__ Fir f) {
+  const long long total = (long long)f.d0 * f.d1 * f.d2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i2 = (int)(t % f.d2);
+    const long long r = t / f.d2;
+    const int i1 = (int)(r % f.d1), i0 = (int)(r / f.d1);
+    const long long sa = f.axis == 0 ? f.is0 : (f.axis == 1 ? f.is1 : f.is2);
+    const double* src = f.in + i0 * f.is0 + i1 * f.is1 + i2 * f.is2 + (long long)f.offset * sa;
+    double acc = __dmul_rn(f.taps[0], src[0]);
+    for (int k = 1; k < f.ntaps; ++k) acc = __dadd_rn(acc, __dmul_rn(f.taps[k], src[k * sa]));
+    f.out[i0 * f.os0 + i1 * f.os1 + i2 * f.os2] = acc;
+  }
+}
+
 // out = diag(A) expanded from the class table
 __global__ void diag_kernel(const double* __restrict__ tab, int nx, int ny, int nz, int nz_glob,
                             int z_off, int ghost, long long pitch_y, long long pitch_z, int ewz,
@@ -1680,6 +1821,81 @@ int bspde_mass_apply(bspde_plan* pl, const double* c, const double* f, double cm
   if (!c || !out) return fail(BSPDE_ERR_ARG, "null field");
   return launch_sep(pl, M_MASS, c, nullptr, out, f, a, cm, true, nullptr, 1,
                     (cudaStream_t)stream);
+}
+
+int bspde_prefilter_lines(double* data, int32_t n, int64_t stride, int32_t na, int32_t nb,
+                          int64_t sa, int64_t sb, const double* poles, int32_t npoles,
+                          double gain, int32_t extension, void* stream) {
+  if (!data || (npoles > 0 && !poles)) return fail(BSPDE_ERR_ARG, "null argument");
+  if (n < 1 || na < 0 || nb < 0) return fail(BSPDE_ERR_ARG, "bad line geometry");
+  if (npoles < 0 || npoles > 2) return fail(BSPDE_ERR_ARG, "npoles must be 0..2 (degree <= 5)");
+  if (extension < 0 || extension > 2) return fail(BSPDE_ERR_ARG, "extension must be 0 (mirror), 1 (replicate) or 2 (zero)");
+  if (npoles > 0 && n < 2) return fail(BSPDE_ERR_ARG, "lines of length < 2 cannot be prefiltered");
+  const long long lines = (long long)na * nb;
+  if (lines == 0 || npoles == 0) {
+    if (lines > 0 && gain != 1.0) return fail(BSPDE_ERR_ARG, "gain without poles");
+    return BSPDE_OK;
+  }
+  int h[2] = {0, 0};
+  for (int i = 0; i < npoles; ++i) {
+    if (!(std::fabs(poles[i]) < 1.0) || poles[i] == 0.0) return fail(BSPDE_ERR_ARG, "poles must be in (-1, 1) \\ {0}");
+    // horizon of the truncated causal-init series at relative tolerance 1e-12
+    h[i] = (int)std::ceil(std::log(1e-12) / std::log(std::fabs(poles[i]))) + 1;
+  }
+  Lines L{data, n, stride, na, nb, sa, sb};
+  const int threads = 128;
+  prefilter_kernel<<<(unsigned)((lines + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+      L, npoles, poles[0], npoles > 1 ? poles[1] : 0.0, h[0], h[1], gain, extension);
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_reflect_pad(double* data, const int32_t* dims, const int64_t* strides, int32_t axis,
+                      int32_t ext, void* stream) {
+  if (!data || !dims || !strides) return fail(BSPDE_ERR_ARG, "null argument");
+  if (axis < 0 || axis > 2 || ext < 0) return fail(BSPDE_ERR_ARG, "bad axis / ext");
+  if (ext == 0) return BSPDE_OK;
+  if (dims[axis] < 2 * ext + ext + 2) return fail(BSPDE_ERR_ARG, "axis too short to reflect");
+  const long long other = (long long)dims[0] * dims[1] * dims[2] / dims[axis];
+  const long long total = other * 2 * ext;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)std::min<long long>((total + threads - 1) / threads, 1 << 20);
+  reflect_pad_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+      data, dims[0], dims[1], dims[2], strides[0], strides[1], strides[2], axis, ext);
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
+                   const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
+                   int32_t offset, const double* taps, int32_t ntaps, void* stream) {
+  if (!in || !in_strides || !out || !out_dims || !out_strides || !taps)
+    return fail(BSPDE_ERR_ARG, "null argument");
+  if (axis < 0 || axis > 2 || ntaps < 1 || ntaps > MAXFIR) return fail(BSPDE_ERR_ARG, "bad axis / taps");
+  Fir f;
+  f.in = in;
+  f.is0 = in_strides[0];
+  f.is1 = in_strides[1];
+  f.is2 = in_strides[2];
+  f.out = out;
+  f.d0 = out_dims[0];
+  f.d1 = out_dims[1];
+  f.d2 = out_dims[2];
+  f.os0 = out_strides[0];
+  f.os1 = out_strides[1];
+  f.os2 = out_strides[2];
+  f.axis = axis;
+  f.offset = offset;
+  f.ntaps = ntaps;
+  for (int k = 0; k < MAXFIR; ++k) f.taps[k] = k < ntaps ? taps[k] : 0.0;
+  const long long total = (long long)f.d0 * f.d1 * f.d2;
+  if (total == 0) return BSPDE_OK;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)std::min<long long>((total + threads - 1) / threads, 1 << 20);
+  void* args[1] = {&f};
+  CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&fir_axis_kernel), dim3(blocks),
+                            dim3(threads), args, 0, (cudaStream_t)stream));
+  return BSPDE_OK;
 }
 
 int bspde_jacobi_diagonal(bspde_plan* pl, const double* diag_table, double* out, void* stream) {

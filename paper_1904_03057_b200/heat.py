@@ -26,7 +26,7 @@ from .operator import B200Operator
 from .solver import SolveConfig, SolveReport, pcg_device
 from .boundary import realize_bc
 from .system import heat_system
-from .transform import transform_field
+from .transform import sample_solution_device, transform_field_device
 
 
 @dataclass
@@ -83,17 +83,21 @@ class HeatSolver:
         lay = self.op.layout
         dev = self.op.device
         u0 = problem.initial_coeffs
-        if u0 is None:
-            u0 = transform_field(problem.initial, problem.grid, problem.degree)
-        self.u = lay.upload(np.asarray(u0).reshape(lay.owned_shape), dev)
+        if u0 is None:  # GPU direct transform straight into the slab layout
+            self.u = transform_field_device(problem.initial, problem.grid, problem.degree, lay, dev)
+        else:
+            self.u = lay.upload(np.asarray(u0).reshape(lay.owned_shape), dev)
         self.b = lay.alloc(dev)
         q = problem.source_coeffs
-        if q is None and not (np.ndim(problem.source) == 0 and not callable(problem.source)
-                              and float(problem.source) == 0.0):
-            q = transform_field(problem.source, problem.grid, problem.degree)
+        has_source = q is not None or not (np.ndim(problem.source) == 0
+                                           and not callable(problem.source)
+                                           and float(problem.source) == 0.0)
         self.F = None
-        if q is not None:
-            qb = lay.upload(np.asarray(q).reshape(lay.owned_shape), dev)
+        if has_source:
+            if q is None:
+                qb = transform_field_device(problem.source, problem.grid, problem.degree, lay, dev)
+            else:
+                qb = lay.upload(np.asarray(q).reshape(lay.owned_shape), dev)
             self.F = lay.alloc(dev)
             self.op.mass_apply_device(qb, self.F)  # F = vol * (M(x)M(x)M) q
             del qb
@@ -141,6 +145,11 @@ class HeatSolver:
 
     def coefficients(self) -> np.ndarray:
         return self.op.layout.download(self.u).reshape(self.data.cext)
+
+    def node_values(self) -> np.ndarray:
+        """The solution at the grid nodes (GPU sample_solution)."""
+        grid = self.data.domain.grid
+        return sample_solution_device(self.u, grid, self.data.n_b, self.op.layout).cpu().numpy()
 
 
 def heat_solve(problem: HeatProblem, steps: int, config: SolveConfig = None, device=None):

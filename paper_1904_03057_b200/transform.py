@@ -1,25 +1,37 @@
-"""Host-side field transforms (setup only; not on the solve hot path).
+"""B-spline field transforms on the GPU (setup and I/O).
 
-* ``direct_transform``: node samples -> B-spline coefficients by the
-  separable causal/anticausal recursive prefilter with whole-sample mirror
-  boundary, as in the reference (``/root/reference/pkg/src/bspde/bspline.py:
-  140-242``; truncated-series causal init at 1e-12, closed-form anticausal
-  init).
-* ``transform_field``: constants stay exact, arrays/callables are sampled,
-  prefiltered and reflect-padded by ``ext`` (``problem.py:178-194``).
-* ``sample_solution``: coefficients -> node values, the b^n correlation
-  (``problem.py:330-348``).
+* ``direct_transform`` / ``prefilter_device``: node samples -> B-spline
+  coefficients by the separable causal/anticausal recursive prefilter of the
+  reference (``/root/reference/pkg/src/bspde/bspline.py:140-242``): gain,
+  truncated-series causal init at relative tolerance 1e-12, closed-form
+  anticausal init, ``mirror`` / ``replicate`` / ``zero`` extensions.  Runs in
+  ``prefilter_kernel`` (one thread per line, every axis in place) through
+  ``bspde_prefilter_lines``.
+* ``transform_field`` / ``transform_field_device``: constants stay exact,
+  arrays / callables are sampled, prefiltered and reflect-padded by ``ext``
+  (``problem.py:178-194``) straight into the ghosted-slab layout.
+* ``sample_solution`` / ``sample_solution_device``: coefficients -> node
+  values, the separable b^n correlation (``problem.py:330-348``), three
+  ``fir_axis_kernel`` passes.
+
+Pole and sampled-spline values are computed on the host exactly as the
+reference does (``np.roots``), so results agree to rounding.  There is no CPU
+implementation here: without the native library and a B200 these raise
+``NativeLibraryError`` (the oracle keeps its own numpy restatement for tests).
 """
 
 from __future__ import annotations
 
-import math
+import ctypes as C
 from functools import lru_cache
 
 import numpy as np
 
+from . import _native as N
 from .errors import ValidationError
 from .gram import basis_extension, bspline_pieces
+
+EXTENSIONS = ("mirror", "replicate", "zero")
 
 
 @lru_cache(maxsize=None)
@@ -39,7 +51,8 @@ def sampled_bspline(n: int) -> np.ndarray:
 
 @lru_cache(maxsize=None)
 def compute_poles(n: int):
-    """Poles in (-1, 0) and gain of the inverse sampled-B-spline filter."""
+    """Poles in (-1, 0) and gain of the inverse sampled-B-spline filter
+    (bspline.py:140-155)."""
     b = sampled_bspline(n)
     if len(b) == 1:
         return (), 1.0
@@ -51,48 +64,124 @@ def compute_poles(n: int):
     return tuple(inside), gain
 
 
-def _mirror_index(i, n):
-    if n == 1:
-        return 0
-    period = 2 * n - 2
-    i = i % period
-    return period - i if i >= n else i
+def _degree_of(basis_or_degree) -> int:
+    return int(getattr(basis_or_degree, "degree", basis_or_degree))
 
 
-def _prefilter_last_axis(c, poles, gain, tol=1e-12):
-    n = c.shape[-1]
-    c = c * gain
-    for z in poles:
-        horizon = int(math.ceil(math.log(tol) / math.log(abs(z)))) + 1
-        init = c[..., 0].copy()
-        zk = 1.0
-        for k in range(1, horizon):
-            zk *= z
-            init += zk * c[..., _mirror_index(k, n)]
-        c[..., 0] = init
-        for k in range(1, n):
-            c[..., k] += z * c[..., k - 1]
-        c[..., n - 1] = (z / (z * z - 1.0)) * (c[..., n - 1] + z * c[..., n - 2])
-        for k in range(n - 2, -1, -1):
-            c[..., k] = z * (c[..., k + 1] - c[..., k])
-    return c
+def _torch():
+    import torch
+
+    return torch
 
 
-def direct_transform(samples, degree: int) -> np.ndarray:
-    arr = np.asarray(samples, dtype=np.float64)
-    if not np.all(np.isfinite(arr)):
+def _as3(t):
+    while t.dim() < 3:
+        t = t.unsqueeze(0)
+    return t
+
+
+def _i32(vals):
+    return (C.c_int32 * 3)(*[int(v) for v in vals])
+
+
+def _i64(vals):
+    return (C.c_int64 * 3)(*[int(v) for v in vals])
+
+
+# ---------------------------------------------------------------------------
+# device-resident API (torch float64 CUDA tensors, any strides, d <= 3)
+
+
+def prefilter_device(t, degree, extension="mirror", ndim=None, stream=None):
+    """In place: direct B-spline transform along the last ``ndim`` (default
+    all) axes of ``t``, in the reference's order (first real axis first)."""
+    if extension not in EXTENSIONS:
+        raise ValidationError(f"unknown extension {extension!r}; pick from {EXTENSIONS}")
+    poles, gain = compute_poles(int(degree))
+    if not poles:
+        return t
+    lib = N.load()
+    t3 = _as3(t)
+    ndim = t.dim() if ndim is None else int(ndim)
+    parr = (C.c_double * 2)(*(list(poles) + [0.0] * (2 - len(poles))))
+    code = EXTENSIONS.index(extension)
+    for ax in range(3 - ndim, 3):
+        n = t3.shape[ax]
+        if n < 2:
+            raise ValidationError(f"extent {n} too small for degree {degree} (need >= 2)")
+        a, b = sorted((q for q in range(3) if q != ax), key=lambda q: t3.stride(q))
+        N.check(lib.bspde_prefilter_lines(
+            N.ptr(t3), n, t3.stride(ax), t3.shape[a], t3.shape[b], t3.stride(a), t3.stride(b),
+            parr, len(poles), float(gain), code, N.stream_handle(stream)))
+    return t
+
+
+def reflect_pad_device(t, ext, ndim=None, stream=None):
+    """In place: ``np.pad(inner, ext, mode='reflect')`` on the real axes of
+    ``t`` whose inner region ``[ext, n - ext)`` holds the values."""
+    if ext == 0:
+        return t
+    lib = N.load()
+    t3 = _as3(t)
+    ndim = t.dim() if ndim is None else ndim
+    for ax in range(3 - ndim, 3):
+        N.check(lib.bspde_reflect_pad(N.ptr(t3), _i32(t3.shape), _i64(t3.stride()), ax, int(ext),
+                                      N.stream_handle(stream)))
+    return t
+
+
+def fir_axis_device(src, out, axis, offset, taps, stream=None):
+    lib = N.load()
+    s3, o3 = _as3(src), _as3(out)
+    tp = (C.c_double * len(taps))(*[float(v) for v in taps])
+    N.check(lib.bspde_fir_axis(N.ptr(s3), _i64(s3.stride()), N.ptr(o3), _i32(o3.shape),
+                               _i64(o3.stride()), int(axis), int(offset), tp, len(taps),
+                               N.stream_handle(stream)))
+    return out
+
+
+def transform_field_device(value, grid, degree: int, layout, device, out=None, stream=None):
+    """Scalar, node samples or callable -> extended-grid coefficients in the
+    ghosted-slab buffer ``out`` (allocated if None).  Constants stay exact."""
+    torch = _torch()
+    ext = basis_extension(degree)
+    buf = layout.alloc(device) if out is None else out
+    own = layout.owned(buf)
+    samples = sample_field(value, grid)
+    if samples is None:
+        own.fill_(float(value))
+        return buf
+    if not np.all(np.isfinite(samples)):
         raise ValidationError("samples contain non-finite values")
-    if degree <= 1:
-        return arr.copy()
-    if any(e < 2 for e in arr.shape):
-        raise ValidationError(f"extents {arr.shape} too small for degree {degree}")
-    poles, gain = compute_poles(degree)
-    out = arr.copy()
-    for axis in range(arr.ndim):
-        moved = np.ascontiguousarray(np.moveaxis(out, axis, -1))
-        moved = _prefilter_last_axis(moved, poles, gain)
-        out = np.moveaxis(moved, -1, axis)
-    return np.ascontiguousarray(out)
+    d = grid.dim
+    own3 = own.reshape(own.shape)  # (cz, cy, cx) view
+    inner = own3[tuple(slice(ext, own3.shape[a] - ext) if a >= 3 - d else slice(None)
+                       for a in range(3))]
+    inner.copy_(torch.from_numpy(np.ascontiguousarray(samples).reshape(inner.shape)))
+    prefilter_device(inner, degree, ndim=d, stream=stream)
+    reflect_pad_device(own3, ext, ndim=d, stream=stream)
+    return buf
+
+
+def sample_solution_device(buf, grid, degree: int, layout, stream=None):
+    """Ghosted-slab coefficients -> node values (torch, grid extents)."""
+    torch = _torch()
+    b = sampled_bspline(int(degree))
+    m = len(b) // 2
+    ext = basis_extension(degree)
+    cur = layout.owned(buf)  # (cz, cy, cx)
+    d = grid.dim
+    for ax in range(3 - d, 3):
+        shp = list(cur.shape)
+        shp[ax] = grid.extents[ax - (3 - d)]
+        nxt = torch.empty(shp, dtype=torch.float64, device=cur.device)
+        fir_axis_device(cur, nxt, ax, ext - m, b, stream)
+        cur = nxt
+    return cur.reshape(tuple(grid.extents))
+
+
+# ---------------------------------------------------------------------------
+# host-array API (reference signatures; the work runs on the GPU)
 
 
 def sample_field(value, grid):
@@ -108,29 +197,58 @@ def sample_field(value, grid):
     return arr
 
 
-def transform_field(value, grid, degree: int) -> np.ndarray:
-    """Scalar, node samples or callable -> extended-grid coefficients."""
-    ext = basis_extension(degree)
-    samples = sample_field(value, grid)
-    if samples is None:
-        return np.full(tuple(n + 2 * ext for n in grid.extents), float(value))
-    coeffs = direct_transform(samples, degree)
-    if ext > 0:
-        coeffs = np.pad(coeffs, ext, mode="reflect")
-    return coeffs
+def direct_transform(samples, basis, extension="mirror", device=None):
+    """Node samples -> spline coefficients (reference ``direct_transform``,
+    bspline.py:214-242; ``basis`` may be a degree or an object with ``degree``)."""
+    from .device import require_cuda
+
+    torch = _torch()
+    n = _degree_of(basis)
+    if extension not in EXTENSIONS:
+        raise ValidationError(f"unknown extension {extension!r}; pick from {EXTENSIONS}")
+    arr = np.asarray(samples, dtype=np.float64)
+    if hasattr(basis, "dim") and arr.ndim != basis.dim:
+        raise ValidationError(f"samples are {arr.ndim}-d but basis is {basis.dim}-d")
+    if arr.ndim > 3:
+        raise ValidationError("at most 3-d samples")
+    if not np.all(np.isfinite(arr)):
+        raise ValidationError("samples contain non-finite values")
+    if n >= 2 and any(e < 2 for e in arr.shape):
+        raise ValidationError(f"extents {arr.shape} too small for degree {n} (need >= 2)")
+    if n <= 1:
+        return arr.copy()
+    dev = require_cuda(device)
+    t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+    prefilter_device(t, n, extension)
+    return t.cpu().numpy()
 
 
-def sample_solution(coeffs_ext, grid, degree: int) -> np.ndarray:
-    b = sampled_bspline(degree)
-    m = len(b) // 2
+def transform_field(value, grid, degree: int, device=None) -> np.ndarray:
+    """Scalar, node samples or callable -> extended-grid coefficients (host)."""
+    from .device import SlabLayout, require_cuda
+
     ext = basis_extension(degree)
-    out = np.asarray(coeffs_ext, dtype=np.float64)
-    for ax in range(grid.dim):
-        acc = None
-        for t, w in enumerate(b):
-            sl = [slice(None)] * grid.dim
-            sl[ax] = slice(ext - m + t, ext - m + t + grid.extents[ax])
-            term = w * out[tuple(sl)]
-            acc = term if acc is None else acc + term
-        out = acc
-    return out
+    cext = tuple(n + 2 * ext for n in grid.extents)
+    if sample_field(value, grid) is None:
+        return np.full(cext, float(value))
+    dev = require_cuda(device)
+    c3 = (1,) * (3 - len(cext)) + cext
+    lay = SlabLayout(c3[0], c3[1], c3[2], ghost=0)
+    buf = transform_field_device(value, grid, degree, lay, dev)
+    return lay.download(buf).reshape(cext)
+
+
+def sample_solution(coeffs_ext, grid, degree: int, device=None) -> np.ndarray:
+    """Coefficients on the extended grid -> node values (host)."""
+    from .device import SlabLayout, require_cuda
+
+    dev = require_cuda(device)
+    ext = basis_extension(degree)
+    cext = tuple(n + 2 * ext for n in grid.extents)
+    c = np.asarray(coeffs_ext, dtype=np.float64)
+    if c.shape != cext:
+        raise ValidationError(f"coefficients {c.shape} != extended extents {cext}")
+    c3 = (1,) * (3 - len(cext)) + cext
+    lay = SlabLayout(c3[0], c3[1], c3[2], ghost=0)
+    buf = lay.upload(c.reshape(c3), dev)
+    return sample_solution_device(buf, grid, degree, lay).cpu().numpy()

@@ -15,6 +15,9 @@ Fixtures:
                   lambda=4, Jacobi-PCG tol 1e-10 (+ tol 1e-12 solution)
   heat64.npz   -- C1: 64^3, p=3, lambda=4: 10-step CG counts at tol 1e-10,
                   inputs, and the step-1 solution at tol 1e-12
+  transform.npz -- direct_transform (mirror / replicate / zero) of random
+                  1-D / 2-D / 3-D samples, p=2..5; transform_field and
+                  sample_solution on small grids
   faces.npz    -- box-face Robin / penalty terms (build_system face_specs):
                   OnTheFlyOperator.apply, jacobi_diagonal and assembled_rhs
                   (volume + face_rhs) for p=1..5 (3-D) and 2-D / 1-D cases
@@ -143,6 +146,41 @@ def face_cases():
     np.savez_compressed(os.path.join(OUT, "faces.npz"), **out)
 
 
+TRANSFORM_CASES = [
+    # (tag, shape, p, extension)
+    ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
+    ("1d_p5_zero", (19,), 5, "zero"), ("1d_p5_mirror_short", (5,), 5, "mirror"),
+    ("2d_p3_mirror", (13, 9), 3, "mirror"), ("2d_p4_replicate", (12, 10), 4, "replicate"),
+    ("3d_p3_mirror", (9, 10, 11), 3, "mirror"), ("3d_p5_mirror", (8, 9, 10), 5, "mirror"),
+    ("3d_p4_zero", (8, 7, 9), 4, "zero"), ("3d_p2_replicate", (6, 7, 8), 2, "replicate"),
+    ("3d_p3_long", (40, 3, 5), 3, "mirror"),
+]
+
+
+def transform_cases():
+    from bspde.problem import sample_solution, transform_field
+
+    out = {}
+    rng = np.random.default_rng(777)
+    for tag, shape, p, ext_mode in TRANSFORM_CASES:
+        x = rng.normal(size=shape)
+        out[f"{tag}_x"] = x
+        out[f"{tag}_c"] = direct_transform(x, BSplineBasis(p, (1.0,) * len(shape)), ext_mode)
+    for p in range(1, 6):
+        g = Grid((9, 10, 11), (0.1, 0.2, 0.15))
+        f = rng.normal(size=g.extents)
+        ce = transform_field(f, g, p, basis_extension(p))
+        out[f"field_p{p}_f"] = f
+        out[f"field_p{p}_c"] = ce
+        out[f"field_p{p}_s"] = sample_solution(ce, g, p)
+    g2 = Grid((12, 9), (0.5, 0.25))
+    f2 = rng.normal(size=g2.extents)
+    ce2 = transform_field(f2, g2, 3, basis_extension(3))
+    out["field2d_p3_f"], out["field2d_p3_c"] = f2, ce2
+    out["field2d_p3_s"] = sample_solution(ce2, g2, 3)
+    np.savez_compressed(os.path.join(OUT, "transform.npz"), **out)
+
+
 def heat_inputs(ncoef, p=3, lam=4.0):
     ext = basis_extension(p)
     N = ncoef - 2 * ext
@@ -210,7 +248,7 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "heat16", "heat64"]
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "transform", "heat16", "heat64"]
     if "gram" in which:
         gram()
     if "apply" in which:
@@ -219,6 +257,8 @@ if __name__ == "__main__":
         rhs_cases()
     if "faces" in which:
         face_cases()
+    if "transform" in which:
+        transform_cases()
     if "heat16" in which:
         heat(16, 10, "heat16.npz")
     if "heat64" in which:

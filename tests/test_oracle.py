@@ -95,3 +95,16 @@ def test_oracle_c1_step1_vs_reference(golden):
     ref = h["u1_tol1e-13"]
     assert np.linalg.norm(u1 - ref) / np.linalg.norm(ref) < 1e-10
     assert abs(rep["iterations"] - int(h["iters1_tol1e-13"][0])) <= 1
+
+
+def test_oracle_direct_transform_vs_reference_fixtures(golden):
+    """The oracle's mirror prefilter against the reference's direct_transform
+    (tests/golden/transform.npz; replicate / zero are GPU-tested only)."""
+    g = golden("transform.npz")
+    for key in list(g.keys()):
+        if key.endswith("_x") and "_mirror" in key:
+            tag = key[:-2]
+            p = int(tag.split("_")[1][1:])
+            c = O.direct_transform(g[key], p)
+            ref = g[f"{tag}_c"]
+            assert float(np.abs(c - ref).max()) <= 1e-13 * float(np.abs(ref).max()), tag

