@@ -28,10 +28,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ALG_BYTES_PASS_A = 24  # read r, p_old; write Ap              (per DoF)
-# pass B reads r, p_old, Ap and writes r, p (40 B); every other pass it also
-# reads and writes x (56 B): x moves once per two iterations
-ALG_BYTES_PASS_B = 48  # average over the pair
+# pass A: read r, p_{k-1}; write Ap, p_k.  Pass B: read r, Ap; write r
+# (24 B), and every other iteration also read x, p_{k-1}, p_k and write x
+# (56 B): x moves once per two iterations
+ALG_BYTES_PASS_A = 32
+ALG_BYTES_PASS_B = 40  # average over the pair
 ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B  # 72
 SURVEY_BYTES_ITER = 80  # x, r, p, Ap streams of the textbook fused CG
 # ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
@@ -313,19 +314,19 @@ def kernel_times(op, u, F, dt, stream, world, reps=9):
     x = u.clone()
     b = lay.alloc(dev)
     r = lay.alloc(dev)
-    pp = lay.alloc(dev)
+    pp = (lay.alloc(dev), lay.alloc(dev))
     ap = lay.alloc(dev)
     scratch = plan.scratch()
     op.mass_apply_device(x, b, F, a=dt)
     plan.cg_setup(scratch, None, 1e-300, 10 ** 6, False, True)
     plan.cg_residual(b, x, r, scratch, 1)
     ta, tb = [], []
-    for _ in range(reps):
+    for k in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        plan.cg_pass_a(r, pp, ap, scratch, 1)
+        plan.cg_pass_a(r, pp[k & 1], pp[(k + 1) & 1], ap, scratch, 1)
         e[1].record(stream)
-        plan.cg_pass_b(x, r, pp, ap, scratch, 1)
+        plan.cg_pass_b(x, r, pp[0], pp[1], ap, scratch, 1)
         e[2].record(stream)
         torch.cuda.synchronize()
         ta.append(e[0].elapsed_time(e[1]))

@@ -125,13 +125,14 @@ int bspde_jacobi_diagonal(bspde_plan* plan, const double* diag_table,
 /* Full Jacobi-PCG on one device.  Replaces pcg(operator, rhs, config, x0)
  * (solver.py:51-117): identical recurrence, stopping rule (recursive
  * ||r||/||b|| <= tol or max_iter), indefinite and divergence guards.
- * b, x, r, p, ap are ghosted-slab fields; x holds x0 on entry when
+ * b, x, r, p, p2, ap are ghosted-slab fields (p, p2: the ping-pong search
+ * directions); x holds x0 on entry when
  * cfg->has_x0, the solution on exit.  scratch: bspde_scratch_bytes bytes.
  * history: device array of max_iter+1 doubles or NULL. */
 int bspde_pcg_solve(bspde_plan* plan, const double* b, double* x, double* r,
-                    double* p, double* ap, void* scratch, double* history,
-                    const bspde_cg_config* cfg, bspde_cg_report* report,
-                    void* stream);
+                    double* p, double* p2, double* ap, void* scratch,
+                    double* history, const bspde_cg_config* cfg,
+                    bspde_cg_report* report, void* stream);
 
 /* ---- step-wise CG for the multi-GPU driver (z-slabs, one rank per GPU).
  * fuse = 1: the kernel's last CTA reduces the per-CTA partials and runs the
@@ -143,20 +144,23 @@ int bspde_cg_setup(bspde_plan* plan, void* scratch, double* history,
 /* r = b - A x (x = x0 or zero), sums = {<b,b>, <r,D^-1 r>, <r,r>}   kind 0 */
 int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
                       double* r, void* scratch, int fuse, void* stream);
-/* p = D^-1 r + beta p_old on the fly; ap = A p; sums = {<p,Ap>}      kind 1 */
-int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p,
-                    double* ap, void* scratch, int fuse, void* stream);
-/* p = D^-1 r + beta p_old; x += alpha p; r -= alpha Ap;
- * sums = {<r,D^-1 r>, <r,r>}                                          kind 2
- * (solver.py:94-101).  The x update is applied every other call, both
- * updates in the reference's rounding order; call bspde_cg_flush_x before
- * reading x. */
-int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, double* p,
-                    const double* ap, void* scratch, int fuse, void* stream);
-/* Apply a pending x update (x += alpha_k p_k), if any.  bspde_pcg_solve does
- * this itself; step-wise drivers call it once after their loop. */
-int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p, void* scratch,
-                     void* stream);
+/* p_k = D^-1 r + beta p_{k-1} on the fly (written to p_out at owned
+ * points); ap = A p_k; sums = {<p,Ap>}                                kind 1
+ * p_in / p_out ping-pong between iterations (they must differ). */
+int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
+                    double* p_out, double* ap, void* scratch, int fuse,
+                    void* stream);
+/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p applied every
+ * other call for two iterations at once, in the reference's rounding order
+ * (solver.py:94-101).  p0 / p1: the two ping-pong p buffers.         kind 2 */
+int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, const double* p0,
+                    const double* p1, const double* ap, void* scratch, int fuse,
+                    void* stream);
+/* Apply the last iteration's x update (x += alpha_k p_k, p_k in p0 or p1 by
+ * the iteration parity).  bspde_pcg_solve does this itself; step-wise
+ * drivers call it once after their loop. */
+int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p0,
+                     const double* p1, void* scratch, void* stream);
 /* kind 0/1/2: scalar update after residual / pass A / pass B (skipped when
  * inactive); kind 3 is used internally by bspde_cg_flush_x. */
 int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);

@@ -79,13 +79,13 @@ SIGNATURES = [
     ("bspde_apply", C.c_int, [_VP, _VP, _VP, _VP]),
     ("bspde_mass_apply", C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP]),
     ("bspde_jacobi_diagonal", C.c_int, [_VP, _dptr, _VP, _VP]),
-    ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+    ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                   C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
     ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,
                                         C.c_int32, _VP]),

@@ -126,8 +126,9 @@ struct SepParams {
   double* out;
   const double* aux;
   double aux_scale;
-  const double* cg_r;  // CG pass A: r and p_old (the Z role recomputes p for <p, Ap>)
+  const double* cg_r;  // CG pass A: r and p_old (TMA-staged with their halos)
   const double* cg_p;
+  double* cg_pout;     // CG pass A: p_k at owned points (ping-pong partner of cg_p)
   double* partials;
   unsigned* counter;
   CgState* state;
@@ -173,6 +174,7 @@ struct PassBParams {
   double* x;
   double* r;
   double* p;
+  double* p1;  // flush: second ping-pong p buffer
   const double* ap;
   double* partials;
   unsigned* counter;
@@ -787,6 +789,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           __stcs(prm.out + off, v);
         } else if (MODE == M_CGA) {
           __stcs(prm.out + off, v);
+          prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
           dsum[0] = fma(pr[0][i], v, dsum[0]);
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
@@ -936,15 +939,16 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 }
 
 // ---------------------------------------------------------------------------
-// CG pass B: streaming x/r/p update + <r, D^-1 r>, <r, r>
+// CG pass B: r -= alpha Ap, <r, D^-1 r>, <r, r> and x += alpha p
+// (solver.py:94-101)
 //
-// x is only read by the caller after the solve, so its update is applied
-// every other iteration: iteration k (x_pending = 0) leaves x alone and
-// records alpha_k; iteration k+1 already reads p_k (as p_old) and forms
-// p_{k+1}, so it computes fl(fl(x + fl(alpha_k p_k)) + fl(alpha_{k+1} p_{k+1}))
-// -- bitwise the reference's two stored updates (solver.py:94) -- in
-// registers.  Saves 16 of 56 bytes/DoF on every other pass.  A solve that
-// ends with an update pending is completed by x_flush_kernel.
+// Pass A stores p_k into the ping-pong partner of p_{k-1}, so pass B never
+// recomputes p.  x is only read by the caller after the solve: iteration k
+// (x_pending = 0) leaves it and records alpha_k; iteration k+1 reads p_k and
+// p_{k+1} and computes fl(fl(x + fl(alpha_k p_k)) + fl(alpha_{k+1} p_{k+1}))
+// -- bitwise the reference's two stored updates.  So the pass streams 24
+// B/DoF (r, Ap in; r out) and 56 every other time; x_flush_kernel applies a
+// pending update at the end of a solve.
 
 constexpr int NTB = 256;
 
@@ -978,16 +982,18 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
   for (int i = threadIdx.x; i < ncz * ncy * ncx; i += NTB) s_inv[i] = prm.invd[i];
   __syncthreads();
   const double alpha = ld_vol(&prm.state->alpha);
-  const double beta = ld_vol(&prm.state->beta);
   const bool xup = ld_vol(&prm.state->x_pending) != 0;
   const double apend = ld_vol(&prm.state->alpha_pend);
+  // iteration k = it: p_k in p[(k + 1) & 1], p_{k-1} in p[k & 1]
+  const bool odd = (ld_vol(&prm.state->it) & 1) != 0;
+  const double* pcur = odd ? prm.p : prm.p1;
+  const double* pprev = odd ? prm.p1 : prm.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int nrows = prm.nz * ny;
   const int r0 = blockIdx.x * prm.rows_per_cta;
   const int r1 = min(r0 + prm.rows_per_cta, nrows);
   double rz = 0.0, rr = 0.0;
-  const bool even = ((prm.pitch_y & 1) == 0);
   for (int row = r0 + warp; row < r1; row += NTB / 32) {
     const int zl = row / ny, y = row - zl * ny;
     const int cz = cls_of(prm.z_off + zl, prm.nz_glob, ewz);
@@ -995,64 +1001,50 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     const double* trow = s_inv + (cz * ncy + cy) * ncx;
     const double inv_int = trow[ewx];
     const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
-    double* xr = prm.x + base;
     double* rrw = prm.r + base;
-    double* pr = prm.p + base;
     const double* apr = prm.ap + base;
-    if (even) {
-      const int npair = nx >> 1;
+    double* xr = prm.x + base;
+    const double* pc = pcur + base;
+    const double* pv_ = pprev + base;
+    const int npair = nx >> 1;  // pitch is even: double2 rows
 #if BSPDE_PB_UNROLL > 1
 #pragma unroll 2
 #endif
-      for (int q = lane; q < npair; q += 32) {
-        const int xx = 2 * q;
-        double2 xv = make_double2(0.0, 0.0);
-        if (xup) xv = ld2(xr + xx);  // issued with the others
-        const double2 rv = ld2(rrw + xx);
-        const double2 pv = ld2(pr + xx);
-        const double2 av = ld2(apr + xx);
-        const double i0 = (xx >= ewx && xx < nx - ewx) ? inv_int : trow[cls_of(xx, nx, ewx)];
-        const double i1 =
-            (xx + 1 >= ewx && xx + 1 < nx - ewx) ? inv_int : trow[cls_of(xx + 1, nx, ewx)];
-        double2 pn, xn, rn;
-        pn.x = pdir(rv.x, i0, pv.x, beta);
-        pn.y = pdir(rv.y, i1, pv.y, beta);
-        if (xup) {
-          xn.x = __dadd_rn(__dadd_rn(xv.x, __dmul_rn(apend, pv.x)), __dmul_rn(alpha, pn.x));
-          xn.y = __dadd_rn(__dadd_rn(xv.y, __dmul_rn(apend, pv.y)), __dmul_rn(alpha, pn.y));
-          st2(xr + xx, xn);
-        }
-        rn.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
-        rn.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
-        rz = fma(rn.x, __dmul_rn(i0, rn.x), rz);
-        rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
-        rr = fma(rn.x, rn.x, rr);
-        rr = fma(rn.y, rn.y, rr);
-        st2(rrw + xx, rn);
-        st2(pr + xx, pn);
+    for (int q = lane; q < npair; q += 32) {
+      const int xx = 2 * q;
+      double2 xv = make_double2(0.0, 0.0), p1v = xv, p0v = xv;
+      if (xup) {  // issued with the others
+        xv = ld2(xr + xx);
+        p0v = ld2(pv_ + xx);
+        p1v = ld2(pc + xx);
       }
-      if ((nx & 1) && lane == 0) {
-        const int xx = nx - 1;
-        const double i0 = trow[cls_of(xx, nx, ewx)];
-        const double pn = pdir(rrw[xx], i0, pr[xx], beta);
-        const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
-        if (xup) xr[xx] = __dadd_rn(__dadd_rn(xr[xx], __dmul_rn(apend, pr[xx])), __dmul_rn(alpha, pn));
-        rrw[xx] = rn;
-        pr[xx] = pn;
-        rz = fma(rn, __dmul_rn(i0, rn), rz);
-        rr = fma(rn, rn, rr);
+      const double2 rv = ld2(rrw + xx);
+      const double2 av = ld2(apr + xx);
+      const double i0 = (xx >= ewx && xx < nx - ewx) ? inv_int : trow[cls_of(xx, nx, ewx)];
+      const double i1 =
+          (xx + 1 >= ewx && xx + 1 < nx - ewx) ? inv_int : trow[cls_of(xx + 1, nx, ewx)];
+      double2 rn;
+      rn.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
+      rn.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
+      rz = fma(rn.x, __dmul_rn(i0, rn.x), rz);
+      rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
+      rr = fma(rn.x, rn.x, rr);
+      rr = fma(rn.y, rn.y, rr);
+      st2(rrw + xx, rn);
+      if (xup) {
+        xv.x = __dadd_rn(__dadd_rn(xv.x, __dmul_rn(apend, p0v.x)), __dmul_rn(alpha, p1v.x));
+        xv.y = __dadd_rn(__dadd_rn(xv.y, __dmul_rn(apend, p0v.y)), __dmul_rn(alpha, p1v.y));
+        st2(xr + xx, xv);
       }
-    } else {
-      for (int xx = lane; xx < nx; xx += 32) {
-        const double i0 = trow[cls_of(xx, nx, ewx)];
-        const double pn = pdir(rrw[xx], i0, pr[xx], beta);
-        const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
-        if (xup) xr[xx] = __dadd_rn(__dadd_rn(xr[xx], __dmul_rn(apend, pr[xx])), __dmul_rn(alpha, pn));
-        rrw[xx] = rn;
-        pr[xx] = pn;
-        rz = fma(rn, __dmul_rn(i0, rn), rz);
-        rr = fma(rn, rn, rr);
-      }
+    }
+    if ((nx & 1) && lane == 0) {
+      const int xx = nx - 1;
+      const double i0 = trow[cls_of(xx, nx, ewx)];
+      const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
+      rrw[xx] = rn;
+      rz = fma(rn, __dmul_rn(i0, rn), rz);
+      rr = fma(rn, rn, rr);
+      if (xup) xr[xx] = __dadd_rn(__dadd_rn(xr[xx], __dmul_rn(apend, pv_[xx])), __dmul_rn(alpha, pc[xx]));
     }
   }
   double v[2] = {rz, rr};
@@ -1060,11 +1052,14 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
                                    prm.fuse, 2);
 }
 
-// Completes a deferred x update: x += alpha_pend * p (p = the last p_k).
-// Same row partition and double2 accesses as pass B.
+// Applies the pending x update of the last iteration of a solve:
+// x += alpha_pend * p_k, p_k = the ping-pong buffer of parity it (pass A of
+// iteration k writes p_k into p[(k+1) & 1]).  Same row partition and double2
+// accesses as pass B.
 __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->x_pending)) return;
   const double a = ld_vol(&prm.state->alpha_pend);
+  const double* pk = (ld_vol(&prm.state->it) & 1) ? prm.p1 : prm.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int nrows = prm.nz * ny;
@@ -1074,7 +1069,7 @@ __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ Pa
     const int zl = row / ny, y = row - zl * ny;
     const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
     double* xr = prm.x + base;
-    const double* pr = prm.p + base;
+    const double* pr = pk + base;
     const int npair = nx >> 1;
 #pragma unroll 2
     for (int q = lane; q < npair; q += 32) {
@@ -1309,10 +1304,11 @@ struct bspde_plan {
   int64_t launches = 0;
   // CUDA graph cache for the CG loop
   struct GraphKey {
-    const void *x, *r, *p, *ap, *scratch;
+    const void *x, *r, *p, *p2, *ap, *scratch;
     int k;
     bool operator<(const GraphKey& o) const {
-      return std::tie(x, r, p, ap, scratch, k) < std::tie(o.x, o.r, o.p, o.ap, o.scratch, o.k);
+      return std::tie(x, r, p, p2, ap, scratch, k) <
+             std::tie(o.x, o.r, o.p, o.p2, o.ap, o.scratch, o.k);
     }
   };
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -1525,7 +1521,7 @@ unsigned* scratch_counter(void* s) {
 
 int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, double* out,
                const double* aux, double aux_scale, double c_mass_override, bool use_override,
-               void* scratch, int fuse, cudaStream_t st) {
+               void* scratch, int fuse, cudaStream_t st, double* cg_pout = nullptr) {
   KernelInfo ki = kernel_for(pl->p, mode);
   auto lit = pl->launch_cache.find(mode);
   if (lit == pl->launch_cache.end()) {
@@ -1549,6 +1545,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.aux_scale = aux_scale;
   sp.cg_r = (mode == M_CGA) ? in0 : nullptr;
   sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
+  sp.cg_pout = cg_pout;
   if (use_override) sp.c_mass = c_mass_override;
   if (scratch) {
     sp.state = scratch_state(scratch);
@@ -1572,7 +1569,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   return BSPDE_OK;
 }
 
-int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double* ap,
+int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, double* p1, const double* ap,
                   void* scratch, int fuse, cudaStream_t st, bool flush = false) {
   PassBParams bp;
   const auto& d = pl->d;
@@ -1594,6 +1591,7 @@ int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double*
   bp.x = x;
   bp.r = r;
   bp.p = p;
+  bp.p1 = p1;
   bp.ap = ap;
   bp.partials = scratch_partials(scratch);
   bp.counter = scratch_counter(scratch);
@@ -1632,8 +1630,8 @@ int bspde_cg_read_report(bspde_plan*, const void*, bspde_cg_report*, int32_t*, v
 }
 namespace {
 
-int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* ap,
-                 void* scratch, double* history, const bspde_cg_config* cfg,
+int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* p2,
+                 double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
                  bspde_cg_report* report, cudaStream_t st) {
   void* stream = (void*)st;
   const size_t bytes = (size_t)(pl->d.nz + 2 * pl->p) * pl->pitch_z * sizeof(double);
@@ -1646,9 +1644,13 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   int32_t active = 0;
   rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
   if (rc) return rc;
-  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  // even chunks: iteration k reads p[k & 1] and writes p[(k + 1) & 1], so every
+  // replay of the captured chunk starts from the same buffer
+  int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  K += K & 1;
+  double* pp[2] = {p, p2};
   while (active) {
-    bspde_plan::GraphKey key{x, r, p, ap, scratch, K};
+    bspde_plan::GraphKey key{x, r, p, p2, ap, scratch, K};
     auto itg = pl->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (itg == pl->graphs.end()) {
@@ -1656,8 +1658,9 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
       CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       int crc = BSPDE_OK;
       for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
-        crc = launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, 1, st);
-        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, ap, scratch, 1, st);
+        crc = launch_sep(pl, M_CGA, r, pp[k & 1], ap, nullptr, 0.0, 0.0, false, scratch, 1, st,
+                         pp[(k + 1) & 1]);
+        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, p2, ap, scratch, 1, st);
       }
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       if (crc) {
@@ -1680,7 +1683,7 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
     rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
     if (rc) return rc;
   }
-  return launch_pass_b(pl, x, r, p, ap, scratch, 1, st, /*flush=*/true);
+  return launch_pass_b(pl, x, r, p, p2, ap, scratch, 1, st, /*flush=*/true);
 }
 
 }  // namespace
@@ -1948,26 +1951,29 @@ int bspde_cg_residual(bspde_plan* pl, const double* b, const double* x, double* 
                     (cudaStream_t)stream);
 }
 
-int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p, double* ap, void* scratch,
-                    int fuse, void* stream) {
+int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p_in, double* p_out,
+                    double* ap, void* scratch, int fuse, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!r || !p || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_sep(pl, M_CGA, r, p, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
-                    (cudaStream_t)stream);
+  if (!r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  if (p_in == p_out) return fail(BSPDE_ERR_ARG, "p_in and p_out must be different buffers");
+  return launch_sep(pl, M_CGA, r, p_in, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
+                    (cudaStream_t)stream, p_out);
 }
 
-int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, double* p, const double* ap,
-                    void* scratch, int fuse, void* stream) {
+int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, const double* p0, const double* p1,
+                    const double* ap, void* scratch, int fuse, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!x || !r || !p || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_pass_b(pl, x, r, p, ap, scratch, fuse, (cudaStream_t)stream);
+  if (!x || !r || !p0 || !p1 || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, x, r, const_cast<double*>(p0), const_cast<double*>(p1), ap, scratch,
+                       fuse, (cudaStream_t)stream);
 }
 
-int bspde_cg_flush_x(bspde_plan* pl, double* x, const double* p, void* scratch, void* stream) {
+int bspde_cg_flush_x(bspde_plan* pl, double* x, const double* p0, const double* p1, void* scratch,
+                     void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!x || !p || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_pass_b(pl, x, nullptr, const_cast<double*>(p), nullptr, scratch, 1,
-                       (cudaStream_t)stream, /*flush=*/true);
+  if (!x || !p0 || !p1 || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, x, nullptr, const_cast<double*>(p0), const_cast<double*>(p1), nullptr,
+                       scratch, 1, (cudaStream_t)stream, /*flush=*/true);
 }
 
 int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
@@ -2000,19 +2006,20 @@ int bspde_cg_read_report(bspde_plan* pl, const void* scratch, bspde_cg_report* r
   return BSPDE_OK;
 }
 
-int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* ap,
-                    void* scratch, double* history, const bspde_cg_config* cfg,
+int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* p2,
+                    double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
                     bspde_cg_report* report, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!b || !x || !r || !p || !ap || !scratch || !cfg)
+  if (!b || !x || !r || !p || !p2 || !ap || !scratch || !cfg)
     return fail(BSPDE_ERR_ARG, "null argument");
+  if (p == p2) return fail(BSPDE_ERR_ARG, "p and p2 must be different buffers");
   // everything runs on the plan's private stream, ordered after the caller's
   // stream on entry and before it on exit
   cudaStream_t caller = (cudaStream_t)stream;
   cudaStream_t st = pl->work;
   CUDA_TRY(cudaEventRecord(pl->ev_in, caller));
   CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_in, 0));
-  int rc = pcg_solve_on(pl, b, x, r, p, ap, scratch, history, cfg, report, st);
+  int rc = pcg_solve_on(pl, b, x, r, p, p2, ap, scratch, history, cfg, report, st);
   cudaEventRecord(pl->ev_out, st);
   cudaStreamWaitEvent(caller, pl->ev_out, 0);
   return rc;

@@ -158,13 +158,13 @@ class NativePlan:
         N.check(self.lib.bspde_jacobi_diagonal(self.handle, tab.ctypes.data_as(N._dptr),
                                                N.ptr(out), N.stream_handle(stream)))
 
-    def pcg(self, b, x, r, p, ap, scratch, history, tol, max_iter, record_history, has_x0,
+    def pcg(self, b, x, r, p, p2, ap, scratch, history, tol, max_iter, record_history, has_x0,
             poll_every=8, stream=None):
         cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
                          int(bool(has_x0)), int(poll_every))
         rep = N.CgReport()
         N.check(self.lib.bspde_pcg_solve(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(p),
-                                         N.ptr(ap), N.ptr(scratch), N.ptr(history),
+                                         N.ptr(p2), N.ptr(ap), N.ptr(scratch), N.ptr(history),
                                          C.byref(cfg), C.byref(rep), N.stream_handle(stream)))
         return rep
 
@@ -179,17 +179,19 @@ class NativePlan:
         N.check(self.lib.bspde_cg_residual(self.handle, N.ptr(b), N.ptr(x), N.ptr(r),
                                            N.ptr(scratch), int(fuse), N.stream_handle(stream)))
 
-    def cg_pass_a(self, r, p, ap, scratch, fuse, stream=None):
-        N.check(self.lib.bspde_cg_pass_a(self.handle, N.ptr(r), N.ptr(p), N.ptr(ap),
-                                         N.ptr(scratch), int(fuse), N.stream_handle(stream)))
+    def cg_pass_a(self, r, p_in, p_out, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_a(self.handle, N.ptr(r), N.ptr(p_in), N.ptr(p_out),
+                                         N.ptr(ap), N.ptr(scratch), int(fuse),
+                                         N.stream_handle(stream)))
 
-    def cg_pass_b(self, x, r, p, ap, scratch, fuse, stream=None):
-        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(p), N.ptr(ap),
-                                         N.ptr(scratch), int(fuse), N.stream_handle(stream)))
+    def cg_pass_b(self, x, r, p0, p1, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(p0), N.ptr(p1),
+                                         N.ptr(ap), N.ptr(scratch), int(fuse),
+                                         N.stream_handle(stream)))
 
-    def cg_flush_x(self, x, p, scratch, stream=None):
-        N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(p), N.ptr(scratch),
-                                          N.stream_handle(stream)))
+    def cg_flush_x(self, x, p0, p1, scratch, stream=None):
+        N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(p0), N.ptr(p1),
+                                          N.ptr(scratch), N.stream_handle(stream)))
 
     def cg_finalize(self, scratch, kind, stream=None):
         N.check(self.lib.bspde_cg_finalize(self.handle, N.ptr(scratch), int(kind),

@@ -7,13 +7,14 @@ per side; the kernels read ghosts and write only owned planes.
 
 Per CG iteration (``distributed_pcg``):
 
-  1. halo exchange of r and p_old: the first/last p owned planes go to the
+  1. halo exchange of r and p_{k-1}: the first/last p owned planes go to the
      lower/upper neighbour's ghost planes (contiguous memory: one send + one
      recv per side, ``torch.distributed.batch_isend_irecv`` over NCCL);
-  2. pass A (fuse=0) writes the local <p, Ap>; ``all_reduce`` of 1 double;
-     the 1-thread finalize kernel runs the scalar update on every rank;
-  3. pass B (fuse=0) writes local <r, D^-1 r>, <r, r>; ``all_reduce`` of 2
-     doubles; finalize.
+  2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
+     and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
+     finalize kernel runs the scalar update on every rank;
+  3. pass B (fuse=0): r -= alpha Ap (x every other iteration), local
+     <r, D^-1 r>, <r, r>; ``all_reduce`` of 2 doubles; finalize.
 
 Every rank holds identical scalar state, so the device-side ``active`` flag
 (stop rule, guards) agrees everywhere; the host polls it every
@@ -135,25 +136,26 @@ class NativeSlabOps:
     def residual(self, b, x, r, scratch):
         self.plan.cg_residual(b, x, r, scratch, 0)
 
-    def pass_a(self, r, p, ap, scratch):
-        self.plan.cg_pass_a(r, p, ap, scratch, 0)
+    def pass_a(self, r, p_in, p_out, ap, scratch):
+        self.plan.cg_pass_a(r, p_in, p_out, ap, scratch, 0)
 
-    def pass_b(self, x, r, p, ap, scratch):
-        self.plan.cg_pass_b(x, r, p, ap, scratch, 0)
+    def pass_b(self, x, r, p0, p1, ap, scratch):
+        self.plan.cg_pass_b(x, r, p0, p1, ap, scratch, 0)
 
     def finalize(self, scratch, kind):
         self.plan.cg_finalize(scratch, kind)
 
-    def flush_x(self, x, p, scratch):
-        self.plan.cg_flush_x(x, p, scratch)
+    def flush_x(self, x, p0, p1, scratch):
+        self.plan.cg_flush_x(x, p0, p1, scratch)
 
     def read(self, scratch):
         return self.plan.cg_read(scratch)
 
 
-def distributed_pcg(ops, halo, allreduce, b, x, r, p, ap, scratch, config: SolveConfig,
+def distributed_pcg(ops, halo, allreduce, b, x, r, p, p2, ap, scratch, config: SolveConfig,
                     has_x0=True, history=None):
-    """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg)."""
+    """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
+    ``p``/``p2`` are the ping-pong search-direction buffers."""
     t0 = time.perf_counter()
     if not has_x0:
         x.zero_()
@@ -165,18 +167,22 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, p, ap, scratch, config: Solve
     ops.finalize(scratch, 0)
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
+    pp = (p, p2)
+    k = 0
     while active:
         for _ in range(K):
+            p_in, p_out = pp[k & 1], pp[(k + 1) & 1]
             halo(r)
-            halo(p)
-            ops.pass_a(r, p, ap, scratch)
+            halo(p_in)
+            ops.pass_a(r, p_in, p_out, ap, scratch)
             allreduce(ops.sums(scratch, 1))
             ops.finalize(scratch, 1)
-            ops.pass_b(x, r, p, ap, scratch)
+            ops.pass_b(x, r, p, p2, ap, scratch)
             allreduce(ops.sums(scratch, 2))
             ops.finalize(scratch, 2)
+            k += 1
         rep, active = ops.read(scratch)
-    ops.flush_x(x, p, scratch)  # pass B moves x every other iteration
+    ops.flush_x(x, p, p2, scratch)  # a pending x update of the last iteration
     return rep, time.perf_counter() - t0
 
 
@@ -260,6 +266,7 @@ class DistributedOperator:
         if self._work is None:
             lay = self.layout
             self._work = dict(r=lay.alloc(self.device), p=lay.alloc(self.device),
+                              p2=lay.alloc(self.device),
                               ap=lay.alloc(self.device), scratch=self.plan().scratch(),
                               history=None)
         w = self._work
@@ -272,7 +279,7 @@ class DistributedOperator:
         w = self._work_buffers(config.max_iter)
         ops = NativeSlabOps(self.plan(config.precond))
         rep, wall = distributed_pcg(ops, self.halo, self.allreduce, b_buf, x_buf, w["r"], w["p"],
-                                    w["ap"], w["scratch"], config, has_x0,
+                                    w["p2"], w["ap"], w["scratch"], config, has_x0,
                                     w["history"] if config.record_history else None)
         return report_from(rep, config, wall, w["history"])
 

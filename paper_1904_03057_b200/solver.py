@@ -7,10 +7,10 @@ pAp <= 0 -> IndefiniteOperatorError, alpha, x, r, z, beta, p, residual,
 history, 1e3 divergence guard; stop on recursive ||r||/||b|| <= tol or
 max_iter), executed as two fused sm_100a kernels per iteration:
 
-* pass A (``sep_kernel<P, M_CGA>``): p = D^-1 r + beta p_old formed on the
-  fly in shared memory, Ap, and <p, Ap>;
-* pass B (``cg_pass_b_kernel``): the same p, x += alpha p, r -= alpha Ap,
-  <r, D^-1 r>, <r, r>;
+* pass A (``sep_kernel<P, M_CGA>``): p_k = D^-1 r + beta p_{k-1} formed on
+  the fly in shared memory (and stored to the ping-pong partner buffer),
+  Ap_k, <p_k, Ap_k>, and the previous iteration's x += alpha_{k-1} p_{k-1};
+* pass B (``cg_pass_b_kernel``): r -= alpha Ap, <r, D^-1 r>, <r, r>;
 
 each finishing with a deterministic fixed-order reduction whose last CTA
 runs the scalar update on the device.  Chunks of iterations are replayed as
@@ -64,7 +64,8 @@ class SolveReport:
 
 
 class CgWork:
-    """Device work vectors for one operator: r, p, Ap, scalar scratch, history.
+    """Device work vectors for one operator: r, p / p2 (ping-pong search
+    directions), Ap, scalar scratch, history.
 
     Allocated once and reused; nothing is allocated inside the CG loop."""
 
@@ -72,6 +73,7 @@ class CgWork:
         lay = op.layout
         self.r = lay.alloc(op.device)
         self.p = lay.alloc(op.device)
+        self.p2 = lay.alloc(op.device)
         self.ap = lay.alloc(op.device)
         self.scratch = op.plan().scratch()
         self.history = None
@@ -124,7 +126,7 @@ def pcg_device(op, b_buf, x_buf, config: SolveConfig = None, has_x0=True, stream
     w = _work(op, config.max_iter)
     w.ensure_history(op, config.max_iter)
     plan = op.plan(config.precond)
-    rep = plan.pcg(b_buf, x_buf, w.r, w.p, w.ap, w.scratch,
+    rep = plan.pcg(b_buf, x_buf, w.r, w.p, w.p2, w.ap, w.scratch,
                    w.history if config.record_history else None, config.tol, config.max_iter,
                    config.record_history, has_x0, config.poll_every, stream)
     return report_from(rep, config, time.perf_counter() - t0, w.history)

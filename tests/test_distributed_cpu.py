@@ -64,29 +64,27 @@ class CpuSlabOps:
         scratch[1] = float((rv * (own_inv * rv)).sum())
         scratch[2] = float((rv ** 2).sum())
 
-    def pass_a(self, r, p, ap, scratch):
-        s = self.state
-        if not s["active"]:
-            return
-        nx = self.lay.nx
-        pn = r[:, :, :nx] * self.inv + s["beta"] * p[:, :, :nx]
-        self._pn = pn
-        apv = self._apply(torch.nn.functional.pad(pn, (0, p.shape[2] - nx)))
-        self._own(ap).copy_(apv)
-        g = self.lay.ghost
-        scratch[0] = float((pn[g:g + self.lay.nz] * apv).sum())
-
-    def pass_b(self, x, r, p, ap, scratch):
+    def pass_a(self, r, p_in, p_out, ap, scratch):
         s = self.state
         if not s["active"]:
             return
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
-        pn = self._pn[g:g + nz]
+        pn = r[:, :, :nx] * self.inv + s["beta"] * p_in[:, :, :nx]
+        self._own(p_out).copy_(pn[g:g + nz])
+        apv = self._apply(torch.nn.functional.pad(pn, (0, p_in.shape[2] - nx)))
+        self._own(ap).copy_(apv)
+        scratch[0] = float((pn[g:g + nz] * apv).sum())
+
+    def pass_b(self, x, r, p0, p1, ap, scratch):
+        s = self.state
+        if not s["active"]:
+            return
+        g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         own_inv = self.inv[g:g + nz, :, :nx]
-        if s.get("x_pending"):  # deferred update, same order as cg_pass_b_kernel
-            self._own(x).add_(s["alpha_pend"] * self._own(p)).add_(s["alpha"] * pn)
+        if s.get("x_pending"):  # two updates at once, as cg_pass_b_kernel
+            pcur, pprev = (p0, p1) if s["it"] & 1 else (p1, p0)
+            self._own(x).add_(s["alpha_pend"] * self._own(pprev)).add_(s["alpha"] * self._own(pcur))
         self._own(r).sub_(s["alpha"] * self._own(ap))
-        self._own(p).copy_(pn)
         rv = self._own(r)
         scratch[0] = float((rv * (own_inv * rv)).sum())
         scratch[1] = float((rv ** 2).sum())
@@ -122,9 +120,10 @@ class CpuSlabOps:
             s["it"] += 1
         s["active"] = int(s["res"] / s["scale"] > s["tol"] and s["it"] < s["max_iter"])
 
-    def flush_x(self, x, p, scratch):
+    def flush_x(self, x, p0, p1, scratch):
         if self.state.get("x_pending"):
-            self._own(x).add_(self.state["alpha_pend"] * self._own(p))
+            pk = p1 if self.state["it"] & 1 else p0
+            self._own(x).add_(self.state["alpha_pend"] * self._own(pk))
             self.state["x_pending"] = 0
 
     def read(self, scratch):
@@ -155,7 +154,7 @@ def _worker(rank, world, port, ext, p, out_q):
         lo, hi = part.bounds()
         b = lay.upload(b_full[lo:hi], "cpu")
         x = lay.upload(x0_full[lo:hi], "cpu")
-        r, pp, ap = lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu")
+        r, pp, pp2, ap = lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu")
         scratch = torch.zeros(8, dtype=torch.float64)
         ops = CpuSlabOps(ora, lay)
         halo = HaloExchanger(lay, rank, world)
@@ -164,7 +163,8 @@ def _worker(rank, world, port, ext, p, out_q):
             dist.all_reduce(t)
 
         cfg = SolveConfig(tol=1e-13, max_iter=1000, poll_every=3)
-        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pp, ap, scratch, cfg, has_x0=True)
+        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pp, pp2, ap, scratch, cfg,
+                                 has_x0=True)
         own = lay.owned(x).contiguous()
         parts = [torch.zeros((part.bounds(q)[1] - part.bounds(q)[0],) + tuple(own.shape[1:]),
                              dtype=own.dtype) for q in range(world)]
