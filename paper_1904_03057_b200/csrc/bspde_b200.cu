@@ -1007,10 +1007,42 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     const double* pc = pcur + base;
     const double* pv_ = pprev + base;
     const int npair = nx >> 1;  // pitch is even: double2 rows
-#if BSPDE_PB_UNROLL > 1
+#if BSPDE_PB_UNROLL == 2
 #pragma unroll 2
+#elif BSPDE_PB_UNROLL == 4
+#pragma unroll 4
 #endif
-    for (int q = lane; q < npair; q += 32) {
+    int q = lane;
+    if (!xup) {
+      // lean pass (r, Ap only): two pairs per step with every load issued
+      // before any store, for memory-level parallelism
+      for (; q + 32 < npair; q += 64) {
+        const int xa = 2 * q, xb = 2 * (q + 32);
+        const double2 ra = ld2(rrw + xa), aa = ld2(apr + xa);
+        const double2 rb = ld2(rrw + xb), ab = ld2(apr + xb);
+        const double ia0 = (xa >= ewx && xa < nx - ewx) ? inv_int : trow[cls_of(xa, nx, ewx)];
+        const double ia1 = (xa + 1 >= ewx && xa + 1 < nx - ewx) ? inv_int : trow[cls_of(xa + 1, nx, ewx)];
+        const double ib0 = (xb >= ewx && xb < nx - ewx) ? inv_int : trow[cls_of(xb, nx, ewx)];
+        const double ib1 = (xb + 1 >= ewx && xb + 1 < nx - ewx) ? inv_int : trow[cls_of(xb + 1, nx, ewx)];
+        double2 na, nb;
+        na.x = __dsub_rn(ra.x, __dmul_rn(alpha, aa.x));
+        na.y = __dsub_rn(ra.y, __dmul_rn(alpha, aa.y));
+        nb.x = __dsub_rn(rb.x, __dmul_rn(alpha, ab.x));
+        nb.y = __dsub_rn(rb.y, __dmul_rn(alpha, ab.y));
+        // same summation order as the one-pair loop: pair q, then pair q+32
+        rz = fma(na.x, __dmul_rn(ia0, na.x), rz);
+        rz = fma(na.y, __dmul_rn(ia1, na.y), rz);
+        rr = fma(na.x, na.x, rr);
+        rr = fma(na.y, na.y, rr);
+        rz = fma(nb.x, __dmul_rn(ib0, nb.x), rz);
+        rz = fma(nb.y, __dmul_rn(ib1, nb.y), rz);
+        rr = fma(nb.x, nb.x, rr);
+        rr = fma(nb.y, nb.y, rr);
+        st2(rrw + xa, na);
+        st2(rrw + xb, nb);
+      }
+    }
+    for (; q < npair; q += 32) {
       const int xx = 2 * q;
       double2 xv = make_double2(0.0, 0.0), p1v = xv, p0v = xv;
       if (xup) {  // issued with the others
