@@ -143,6 +143,12 @@ class HeatSolver:
             self.step()
         return self.reports
 
+    def run_host(self, host_u, steps: int, chunks: int = 16):
+        """Steps with the state in (pinned) host memory: every step uploads
+        ``host_u`` and downloads the result into it (run_steps_host)."""
+        own = self.op.layout.owned(self.u)
+        return run_steps_host(self.step, own, host_u, steps, chunks)
+
     def coefficients(self) -> np.ndarray:
         return self.op.layout.download(self.u).reshape(self.data.cext)
 
@@ -150,6 +156,61 @@ class HeatSolver:
         """The solution at the grid nodes (GPU sample_solution)."""
         grid = self.data.domain.grid
         return sample_solution_device(self.u, grid, self.data.n_b, self.op.layout).cpu().numpy()
+
+
+def run_steps_host(step, dev, host, steps: int, chunks: int = 16, stream=None):
+    """Step a device-resident state whose input and result live in host memory.
+
+    ``dev``: the device view of the state (owned region, leading axis = z);
+    ``host``: a pinned CPU tensor of the same shape holding the input.  Every
+    step copies ``host -> dev``, runs ``step()`` on ``stream`` (default: the
+    current stream) and copies ``dev -> host``.  The result copy of step k and
+    the input copy of step k+1 move the same bytes through host memory, so
+    they are split into ``chunks`` z-ranges and chunk i goes back up as soon as
+    it is down (PCIe is full duplex; copies run on two side streams).  Returns
+    the step reports.
+    """
+    import torch
+
+    comp = stream if stream is not None else torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    nz = dev.shape[0]
+    cuts = np.linspace(0, nz, max(1, min(int(chunks), nz)) + 1).astype(int)
+    bounds = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    start = torch.cuda.Event()
+    start.record(comp)
+    s_in.wait_event(start)
+    with torch.cuda.stream(s_in):
+        for a, b in bounds:
+            dev[a:b].copy_(host[a:b], non_blocking=True)
+    ready = torch.cuda.Event()
+    ready.record(s_in)
+    reports = []
+    for k in range(int(steps)):
+        comp.wait_event(ready)
+        with torch.cuda.stream(comp):
+            reports.append(step())
+        done = torch.cuda.Event()
+        done.record(comp)
+        s_out.wait_event(done)
+        down = []
+        with torch.cuda.stream(s_out):
+            for a, b in bounds:
+                host[a:b].copy_(dev[a:b], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_out)
+                down.append(e)
+        if k + 1 < steps:
+            for (a, b), e in zip(bounds, down):
+                s_in.wait_event(e)
+                with torch.cuda.stream(s_in):
+                    dev[a:b].copy_(host[a:b], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(s_in)
+    end = torch.cuda.Event()
+    end.record(s_out)
+    comp.wait_event(end)
+    return reports
 
 
 def heat_solve(problem: HeatProblem, steps: int, config: SolveConfig = None, device=None):

@@ -524,3 +524,23 @@ def test_transform_2d_and_heat_ic(golden, cuda_device):
     X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
     ref = np.exp(-40 * ((X - .5) ** 2 + (Y - .4) ** 2 + (Z - .6) ** 2))
     assert float(np.abs(hs.node_values() - ref).max()) < 1e-10
+
+
+def test_run_host_matches_device_stepping(golden, cuda_device):
+    """HeatSolver.run_host (state in pinned host memory, overlapped chunked
+    copies) gives bit-identical coefficients and counts to device stepping."""
+    import torch
+
+    h = golden("heat16.npz")
+    p, N, hh, dt = _heat_op(h)
+    grid = Grid((N,) * 3, (hh,) * 3)
+    a = HeatSolver(HeatProblem(grid, p, dt, initial_coeffs=h["u0"], source_coeffs=h["q"]))
+    its_a = [a.step().iterations for _ in range(3)]
+    b = HeatSolver(HeatProblem(grid, p, dt, initial_coeffs=h["u0"], source_coeffs=h["q"]))
+    host = torch.from_numpy(np.ascontiguousarray(h["u0"])).pin_memory()
+    b.u.zero_()  # the input must come from host memory
+    reps = b.run_host(host, 3, chunks=5)
+    torch.cuda.synchronize()
+    assert [r.iterations for r in reps] == its_a
+    assert np.array_equal(host.numpy(), a.coefficients())
+    assert np.array_equal(b.coefficients(), a.coefficients())
