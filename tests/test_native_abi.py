@@ -83,3 +83,96 @@ def test_product_fails_loudly_without_gpu():
     data = build_system(BoxDomain(Grid((8, 8, 8), (1.0,) * 3)), 3, 3, 1.0, 1.0, [])
     with pytest.raises(NativeLibraryError):
         make_operator(data, "b200")
+
+
+def _desc(p=3, ext=(12, 11, 10)):
+    """A plan descriptor built like NativePlan does, but with no device."""
+    import numpy as np
+
+    from paper_1904_03057_b200 import BoxDomain, Grid, build_system
+
+    data = build_system(BoxDomain(Grid(ext, (0.1,) * 3)), p, p, 0.5, 1.0, [])
+    keep = []
+
+    def arr(a):
+        a = np.ascontiguousarray(a, dtype=np.float64).ravel()
+        keep.append(a)
+        return a.ctypes.data_as(N._dptr)
+
+    d = N.PlanDesc()
+    d.device = 0
+    d.degree = p
+    d.nz, d.ny, d.nx = data.dims3
+    d.nz_global, d.z_offset = data.dims3[0], 0
+    for a in range(3):
+        d.ew[a] = data.mass[a].ew
+        d.mass_table[a] = arr(data.mass[a].table)
+        d.stiff_table[a] = arr(data.stiff[a].table)
+    d.inv_diag_table = arr(data.inv_diag_table())
+    d.pitch_y = data.dims3[2] + (data.dims3[2] & 1)
+    d.c_mass = data.c_mass
+    for a in range(3):
+        d.c_stiff[a] = data.c_stiff[a]
+    return d, keep, data
+
+
+@pytest.mark.parametrize("field,value,msg", [
+    ("degree", 6, b"degree"), ("degree", 0, b"degree"), ("nx", 0, b"extents"),
+    ("pitch_y", 13, b"pitch_y"), ("z_offset", 5, b"z slab"), ("device", -1, b"device"),
+])
+def test_plan_create_validates_before_touching_cuda(field, value, msg):
+    lib = N.load()
+    d, keep, _ = _desc()
+    setattr(d, field, value)
+    h = C.c_void_p()
+    assert lib.bspde_plan_create(C.byref(d), C.byref(h)) == 1  # BSPDE_ERR_ARG
+    assert msg in lib.bspde_last_error()
+
+
+def test_plan_create_rejects_non_tap_interior_rows():
+    """The kernels use compile-time interior taps; tables whose interior class
+    row differs (e.g. pre-scaled) must be refused, not silently misapplied."""
+    import numpy as np
+
+    lib = N.load()
+    d, keep, data = _desc()
+    bad = np.array(data.stiff[1].table) * 2.0
+    keep.append(bad)
+    d.stiff_table[1] = bad.ctypes.data_as(N._dptr)
+    h = C.c_void_p()
+    assert lib.bspde_plan_create(C.byref(d), C.byref(h)) == 1
+    assert b"interior" in lib.bspde_last_error()
+    # face terms live in edge rows only: accepted by the same check
+    from paper_1904_03057_b200 import BoxDomain, Grid, build_system
+
+    faced = build_system(BoxDomain(Grid((12, 11, 10), (0.1,) * 3)), 3, 3, 0.5, 1.0,
+                         [(1, 0, 5.0, None)])
+    good = np.ascontiguousarray(faced.stiff[1].table)
+    keep.append(good)
+    d.stiff_table[1] = good.ctypes.data_as(N._dptr)
+    rc = lib.bspde_plan_create(C.byref(d), C.byref(h))
+    assert rc != 1 or b"interior" not in lib.bspde_last_error()
+    if rc == 0:
+        lib.bspde_plan_destroy(h)
+
+
+def test_transform_entry_points_validate_arguments():
+    lib = N.load()
+    buf = (C.c_double * 8)()
+    poles = (C.c_double * 3)(-0.3, -0.1, -0.05)
+    vp = C.cast(buf, C.c_void_p)
+    pp = C.cast(poles, C.c_void_p)
+    assert lib.bspde_prefilter_lines(vp, 8, 1, 1, 1, 8, 8, pp, 3, 1.0, 0, None) == 1
+    assert b"npoles" in lib.bspde_last_error()
+    assert lib.bspde_prefilter_lines(vp, 8, 1, 1, 1, 8, 8, pp, 1, 1.0, 7, None) == 1
+    assert b"extension" in lib.bspde_last_error()
+    assert lib.bspde_prefilter_lines(vp, 1, 1, 1, 1, 8, 8, pp, 1, 1.0, 0, None) == 1
+    bigpole = (C.c_double * 1)(-1.5)
+    assert lib.bspde_prefilter_lines(vp, 8, 1, 1, 1, 8, 8, C.cast(bigpole, C.c_void_p), 1, 1.0,
+                                     0, None) == 1
+    assert lib.bspde_prefilter_lines(vp, 8, 1, 1, 1, 8, 8, None, 0, 1.0, 0, None) == 0  # no-op
+    dims = (C.c_int32 * 3)(1, 1, 8)
+    strides = (C.c_int64 * 3)(8, 8, 1)
+    assert lib.bspde_reflect_pad(vp, dims, strides, 3, 1, None) == 1
+    taps = (C.c_double * 12)()
+    assert lib.bspde_fir_axis(vp, strides, vp, dims, strides, 2, 0, taps, 12, None) == 1
