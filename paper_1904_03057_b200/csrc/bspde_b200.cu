@@ -56,10 +56,7 @@ constexpr int RPT = 4;               // output rows per thread
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
 
-#ifndef BSPDE_P5_WARPS
-#define BSPDE_P5_WARPS 12
-#endif
-__host__ __device__ constexpr int warps_of(int p) { return p <= 3 ? 16 : (p == 4 ? 12 : BSPDE_P5_WARPS); }
+__host__ __device__ constexpr int warps_of(int p) { return p <= 3 ? 16 : 12; }
 __host__ __device__ constexpr int tile_h_of(int p) { return RPT * warps_of(p) / 2; }
 
 template <int P>
@@ -120,7 +117,6 @@ struct SepParams {
   int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
   double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
-  double gm[MAXTAP], gk[MAXTAP];  // unit interior taps (BSPDE_TAP_SRC == 1)
   const double* tab;             // device: [axis][kind][NC*R] (NC = class stride)
   const double* invd;            // device: NCz*NCy*NCx
   double* out;
@@ -135,34 +131,18 @@ struct SepParams {
   int fuse;
 };
 
-// Interior taps for the fast paths: compile-time immediates (0) or kernel
-// parameters, i.e. constant-bank operands of the FMAs (1).
-#ifndef BSPDE_UNROLL_PLANES
-#define BSPDE_UNROLL_PLANES 1
-#endif
-#ifndef BSPDE_YSKIP
-#define BSPDE_YSKIP 1
-#endif
+// BSPDE_ALL_EDGE=1 (measurement build): every tile takes the edge-tile
+// path, to weigh edge against interior tiles in the launch planner.
 #ifndef BSPDE_ALL_EDGE
 #define BSPDE_ALL_EDGE 0
 #endif
-#ifndef BSPDE_SPLIT_WA
-#define BSPDE_SPLIT_WA 0
-#endif
-#ifndef BSPDE_TAP_SRC
-#define BSPDE_TAP_SRC 0
-#endif
+// Interior taps of the fast paths: compile-time immediates (measured faster
+// than __constant__ or kernel-parameter operands; profiles/r01_ncu_summary.md).
 template <int P>
 struct TapSrc {
   const SepParams& prm;
-  __device__ __forceinline__ double M(int k) const {
-    if constexpr (BSPDE_TAP_SRC == 1) return prm.gm[k];
-    else return GramTaps<P>::M(k);
-  }
-  __device__ __forceinline__ double K(int k) const {
-    if constexpr (BSPDE_TAP_SRC == 1) return prm.gk[k];
-    else return GramTaps<P>::K(k);
-  }
+  __device__ __forceinline__ double M(int k) const { return GramTaps<P>::M(k); }
+  __device__ __forceinline__ double K(int k) const { return GramTaps<P>::K(k); }
 };
 
 struct PassBParams {
@@ -662,17 +642,16 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   double out[RPT];
   if (in_grid) {
     // ---- y-pass: wm = My u1, wa = My t + cy Ky u1 for rows gy0 .. gy0+3 ----
-    double wm[RPT], wa[RPT], wb[RPT];
+    double wm[RPT], wa[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       wm[i] = 0.0;
       wa[i] = 0.0;
-      wb[i] = 0.0;
     }
     const double* x1c = X1 + (rg * RPT) * TX + cxl;
     const double* x2c = X2 + (rg * RPT) * TX + cxl;
     const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
-    if (BSPDE_YSKIP && RAGGED && gy0 >= ny) {
+    if (RAGGED && gy0 >= ny) {
       // row group below the grid (ragged last tile row): nothing to filter
     } else if (fast_y) {
 #pragma unroll
@@ -687,15 +666,10 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
             wm[i] = fma(T.M(k), a1, wm[i]);
             if (STIFF) {
               wa[i] = fma(T.M(k), t, wa[i]);
-              if (BSPDE_SPLIT_WA) wb[i] = fma(T.K(k), u1c, wb[i]);
-              else wa[i] = fma(T.K(k), u1c, wa[i]);
+              wa[i] = fma(T.K(k), u1c, wa[i]);
             }
           }
         }
-      }
-      if (BSPDE_SPLIT_WA && STIFF) {
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) wa[i] += wb[i];
       }
     } else {
       int cyr[RPT];
@@ -846,9 +820,6 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 
   plane_front<P, MODE, TK>(prm, sm, g, 0, flat, beta);
   __syncthreads();
-#if BSPDE_UNROLL_PLANES > 1
-#pragma unroll 2
-#endif
   for (int j = 0; j < nin; ++j) {
     // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
     double auxv[RPT];
@@ -952,25 +923,16 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 
 constexpr int NTB = 256;
 
-// TMA L2 promotion of the plane boxes: 0 none, 1 64B, 2 128B, 3 256B
-#ifndef BSPDE_L2PROMO
-#define BSPDE_L2PROMO 1
-#endif
-#ifndef BSPDE_PB_UNROLL
-#define BSPDE_PB_UNROLL 1
-#endif
-#ifndef BSPDE_PB_HINTS
-#define BSPDE_PB_HINTS 0
-#endif
-// streaming loads/stores of the CG vectors (6.4 GB each at C3: no L2 reuse)
+// TMA L2 promotion of the plane boxes: 64 B (256 B over-fetches the 32-byte
+// misaligned haloed rows: pass A DRAM reads 19.7 -> 17.1 GB at 930^3)
+constexpr CUtensorMapL2promotion kL2Promotion = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+
+// plain 16-byte loads/stores of the CG vectors (streaming cache hints were
+// measured much slower)
 __device__ __forceinline__ double2 ld2(const double* p) {
-  if (BSPDE_PB_HINTS) return __ldcs(reinterpret_cast<const double2*>(p));
   return *reinterpret_cast<const double2*>(p);
 }
-__device__ __forceinline__ void st2(double* p, double2 v) {
-  if (BSPDE_PB_HINTS) __stcs(reinterpret_cast<double2*>(p), v);
-  else *reinterpret_cast<double2*>(p) = v;
-}
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
 __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->active)) return;
@@ -1007,11 +969,6 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     const double* pc = pcur + base;
     const double* pv_ = pprev + base;
     const int npair = nx >> 1;  // pitch is even: double2 rows
-#if BSPDE_PB_UNROLL == 2
-#pragma unroll 2
-#elif BSPDE_PB_UNROLL == 4
-#pragma unroll 4
-#endif
     int q = lane;
     if (!xup) {
       // lean pass (r, Ap only): two pairs per step with every load issued
@@ -1488,7 +1445,7 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    (CUtensorMapL2promotion)BSPDE_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    kL2Promotion, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" +
                                                           std::to_string((int)rc) + ")");
   return BSPDE_OK;
@@ -1518,8 +1475,6 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
     sp.tyk[k] = d.c_stiff[1] * d.stiff_table[1][d.ew[1] * R + k];
     sp.txm[k] = d.mass_table[2][d.ew[2] * R + k];
     sp.txk[k] = d.stiff_table[2][d.ew[2] * R + k];
-    sp.gm[k] = k < R ? kHostGramM[pl->p - 1][k] : 0.0;
-    sp.gk[k] = k < R ? kHostGramK[pl->p - 1][k] : 0.0;
   }
   sp.zfast = (d.nz_global > 1 && d.ew[0] > 0) ? 1 : 0;
   sp.c_mass = d.c_mass;

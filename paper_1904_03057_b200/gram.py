@@ -345,12 +345,11 @@ def surface_single_vector(p: int, num_nodes: int) -> np.ndarray:
 def taps_header() -> str:
     """C++ header with the exact interior taps (mass, stiffness) for p=1..5.
 
-    Generated into ``csrc/gram_taps.cuh``.  Two equivalent forms: constexpr
-    functions (immediates folded by ptxas) and, with ``BSPDE_CONST_TAPS``,
-    ``__constant__`` tables read with compile-time indices (constant-bank
-    operands).  Which one is faster depends on register pressure; the build
-    picks one.  ``tests/test_gram.py`` checks the committed header against
-    ``gram_factor`` so the two cannot drift.
+    Generated into ``csrc/gram_taps.cuh``: constexpr functions (immediates the
+    kernels' fast paths fold in; measured faster than ``__constant__`` or
+    kernel-parameter taps) and a host copy that ``bspde_plan_create`` checks
+    the callers' interior table rows against.  ``tests/test_gram.py`` checks
+    the committed header against ``gram_factor`` so the two cannot drift.
     """
     def fn(name, vals):
         body = " : ".join(f"k == {i} ? {repr(float(v))}" for i, v in enumerate(vals[:-1]))
@@ -369,21 +368,11 @@ def taps_header() -> str:
              "// exact interior taps G[i, i+k-p], k=0..2p, of the unit-step 1-D Gram",
              "// factors (mass: int b(x)b(x-k); stiffness: int b'(x)b'(x-k)), p = 1..5",
              "#pragma once", "",
-             "// host copy (kernel-parameter taps are filled from it)",
+             "// host copy (bspde_plan_create validates the interior table rows)",
              f"static const double kHostGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
     lines += [f"    {{{r}}}," for r in rows_m]
     lines += ["};", f"static const double kHostGramK[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
     lines += [f"    {{{r}}}," for r in rows_k]
-    lines += ["};", "", "#ifdef BSPDE_CONST_TAPS",
-              f"__constant__ double kGramM[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
-    lines += [f"    {{{r}}}," for r in rows_m]
-    lines += ["};", f"__constant__ double kGramK[{MAX_DEGREE}][{2 * MAX_DEGREE + 1}] = {{"]
-    lines += [f"    {{{r}}}," for r in rows_k]
-    lines += ["};", "",
-              "template <int P>",
-              "struct GramTaps {",
-              "  __device__ __forceinline__ static double M(int k) { return kGramM[P - 1][k]; }",
-              "  __device__ __forceinline__ static double K(int k) { return kGramK[P - 1][k]; }",
-              "};", "#else", "template <int P> struct GramTaps;"]
-    lines += spec + ["#endif"]
+    lines += ["};", "", "template <int P> struct GramTaps;"]
+    lines += spec
     return "\n".join(lines) + "\n"

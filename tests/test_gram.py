@@ -83,6 +83,6 @@ def test_taps_header_matches_factors():
                         "paper_1904_03057_b200", "csrc", "gram_taps.cuh")
     assert open(path).read() == taps_header()
     for p in range(1, 6):
-        assert "kGramM" in taps_header()
+        assert "kHostGramM" in taps_header() and f"struct GramTaps<{p}>" in taps_header()
         interior = gram_factor(p, 20, "mass").interior
         assert repr(float(interior[p])) in taps_header()
