@@ -112,14 +112,17 @@ class ClockSampler:
 # does not exist on the GPU box)
 
 
-def cpu_port_rate(ncoef=64, iters=20, repeats=3):
+def cpu_port_rate(ncoef=64, iters=20, repeats=3, p=3):
     """Oracle port of the reference CG path (numpy/scipy Kronecker apply +
-    the reference pcg recurrence) on the C1 heat problem: CG DoF-it/s."""
+    the reference pcg recurrence) on the C1 heat problem: CG DoF-it/s.
+    Single-threaded: scipy's sparse matvec holds the GIL (a thread pool over
+    slabs measured 7.7x slower); the port is still ~6x faster than the
+    reference's fastest strategy (sparse 1.78 MDoF-it/s)."""
     from oracle import bspde_oracle as O
 
-    inp = O.heat_inputs(ncoef)
+    inp = O.heat_inputs(ncoef, p)
     N, h, dt = inp["N"], inp["h"], inp["dt"]
-    A = O.KronOperator((N,) * 3, (h,) * 3, 3, dt, 1.0)
+    A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
     b = A.mass_apply(inp["u0"]) + dt * A.mass_apply(inp["q"])
     O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=2, x0=inp["u0"])  # warm
     times = []
@@ -139,11 +142,12 @@ def run_reference(args, rank, world):
     vals = []
     info = None
     for i in range(warm + steps):
-        v, info = cpu_port_rate(64, iters=10, repeats=1)
+        v, info = cpu_port_rate(64, iters=10, repeats=1, p=args.degree)
         if i >= warm:
             vals.append(v)
     val = float(np.median(vals)) / 1e9
-    sample = (f"C1 sample: 64^3 coefficients, p=3, lambda=4, {info['iterations']} Jacobi-PCG "
+    sample = (f"C1 sample: 64^3 coefficients, p={args.degree}, lambda=4, "
+              f"{info['iterations']} Jacobi-PCG "
               f"iterations per step (oracle port: scipy CSR 1-D factors, separable Kronecker "
               f"apply, reference pcg recurrence); full config {args.ncoef}^3 infeasible on CPU")
     line = {
@@ -162,11 +166,17 @@ METRIC = "CG iteration DoF/s (GDoF/s) and % HBM roofline at 0.8B nodes, 1/2/4/8 
 
 
 def config_of(args, world):
-    ncoef = args.ncoef
-    return {"workload": f"C3 heat: {ncoef}^3 coefficients ({ncoef - 2}^3 nodes), p=3, "
+    from paper_1904_03057_b200.gram import basis_extension
+
+    ncoef, p = args.ncoef, args.degree
+    tag = "C3" if (ncoef, p) == (930, 3) else ("C4" if ncoef == 512 else "custom")
+    nodes = ncoef - 2 * basis_extension(p)
+    gb = ncoef ** 3 * 8 / 1e9
+    return {"workload": f"{tag} heat: {ncoef}^3 coefficients ({nodes}^3 nodes), p={p}, "
                         f"implicit Euler lambda=4, Jacobi-PCG tol 1e-10, z-slabs x{world}",
-            "ncoef": ncoef, "degree": 3, "dofs": ncoef ** 3, "precision": "fp64",
-            "parallelism": f"zslab{world}", "l2": "inputs (6.4 GB/vector) >> 126 MB L2"}
+            "ncoef": ncoef, "degree": p, "dofs": ncoef ** 3, "precision": "fp64",
+            "parallelism": f"zslab{world}",
+            "l2": f"inputs ({gb:.1f} GB/vector) vs 126 MB L2"}
 
 
 # ---------------------------------------------------------------------------
@@ -187,7 +197,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    p = 3
+    p = args.degree
     N, h, dt = heat_c_inputs(args.ncoef, p)
     data = heat_system(Grid((N,) * 3, (h,) * 3), p, dt)
     dofs = int(np.prod(data.cext))
@@ -272,9 +282,9 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        rate, info = cpu_port_rate(64, iters=20, repeats=3)
+        rate, info = cpu_port_rate(64, iters=20, repeats=3, p=args.degree)
         cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
-               "sample": f"C1 64^3 p=3 heat system, {info['iterations']} Jacobi-PCG iterations, "
+               "sample": f"C1 64^3 p={args.degree} heat system, {info['iterations']} Jacobi-PCG iterations, "
                          "median of 3 (oracle port, scipy/numpy single thread)"}
 
     line = {
@@ -284,7 +294,10 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic", "config": config_of(args, world),
         "cg_iterations_per_step": its,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "traffic": TRAFFIC.get(dom), "kernel": dom,
+                     "frac": ach / peak,
+                     # ncu traffic is captured for the C3 workload (profiles/traffic.json)
+                     "traffic": TRAFFIC.get(dom) if (args.ncoef, args.degree) == (930, 3) else None,
+                     "kernel": dom,
                      "peak_source": peak_kind,
                      "alg_bytes_per_dof": ALG_BYTES_PASS_B if dom == "pass_b" else ALG_BYTES_PASS_A,
                      "pass_a_ms": kt["pass_a_ms"], "pass_b_ms": kt["pass_b_ms"],
@@ -377,6 +390,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--ncoef", type=int, default=930)
+    ap.add_argument("--degree", type=int, default=3, help="B-spline degree (C4 sweep: 1..5)")
     ap.add_argument("--poll", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
