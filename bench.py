@@ -29,11 +29,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # pass A: read r, p_{k-1}; write Ap, p_k.  Pass B: read r, Ap; write r
-# (24 B), and every other iteration also read x, p_{k-1}, p_k and write x
-# (56 B): x moves once per two iterations
+# (24 B), and every P_RING-th iteration also read x and the last P_RING p's
+# and write x (24 + 16 + 8 * P_RING B): x moves once per P_RING iterations
+#
 ALG_BYTES_PASS_A = 32
-ALG_BYTES_PASS_B = 40  # average over the pair
-ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B  # 72
+ALG_BYTES_PASS_B = 24 + (16 + 8 * 4) / 4  # 36: average over the ring period (P_RING = 4)
+ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B  # 68
 SURVEY_BYTES_ITER = 80  # x, r, p, Ap streams of the textbook fused CG
 # ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
 # filled from the committed profile summary when present
@@ -327,7 +328,7 @@ def kernel_times(op, u, F, dt, stream, world, reps=9):
     x = u.clone()
     b = lay.alloc(dev)
     r = lay.alloc(dev)
-    pp = (lay.alloc(dev), lay.alloc(dev))
+    pring = lay.alloc_ring(dev)
     ap = lay.alloc(dev)
     scratch = plan.scratch()
     op.mass_apply_device(x, b, F, a=dt)
@@ -337,14 +338,15 @@ def kernel_times(op, u, F, dt, stream, world, reps=9):
     for k in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        plan.cg_pass_a(r, pp[k & 1], pp[(k + 1) & 1], ap, scratch, 1)
+        R = pring.shape[0]
+        plan.cg_pass_a(r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
         e[1].record(stream)
-        plan.cg_pass_b(x, r, pp[0], pp[1], ap, scratch, 1)
+        plan.cg_pass_b(x, r, pring, ap, scratch, 1)
         e[2].record(stream)
         torch.cuda.synchronize()
         ta.append(e[0].elapsed_time(e[1]))
         tb.append(e[1].elapsed_time(e[2]))
-    del x, b, r, pp, ap
+    del x, b, r, pring, ap
     torch.cuda.empty_cache()
     return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:]))}
 

@@ -30,6 +30,12 @@
 extern "C" {
 #endif
 
+/* CG search directions live in a ring of BSPDE_P_RING ghosted-slab fields
+ * (one contiguous allocation, field after field): iteration k writes p_k to
+ * field k % BSPDE_P_RING; x += alpha p is applied every BSPDE_P_RING
+ * iterations from the ring, in the reference's rounding order. */
+#define BSPDE_P_RING 4
+
 #define BSPDE_OK 0
 #define BSPDE_ERR_ARG 1      /* invalid argument (ValidationError) */
 #define BSPDE_ERR_CUDA 2     /* CUDA runtime / driver failure */
@@ -125,14 +131,14 @@ int bspde_jacobi_diagonal(bspde_plan* plan, const double* diag_table,
 /* Full Jacobi-PCG on one device.  Replaces pcg(operator, rhs, config, x0)
  * (solver.py:51-117): identical recurrence, stopping rule (recursive
  * ||r||/||b|| <= tol or max_iter), indefinite and divergence guards.
- * b, x, r, p, p2, ap are ghosted-slab fields (p, p2: the ping-pong search
- * directions); x holds x0 on entry when
+ * b, x, r, ap are ghosted-slab fields, p_ring BSPDE_P_RING of them back to
+ * back (the search directions); x holds x0 on entry when
  * cfg->has_x0, the solution on exit.  scratch: bspde_scratch_bytes bytes.
  * history: device array of max_iter+1 doubles or NULL. */
 int bspde_pcg_solve(bspde_plan* plan, const double* b, double* x, double* r,
-                    double* p, double* p2, double* ap, void* scratch,
-                    double* history, const bspde_cg_config* cfg,
-                    bspde_cg_report* report, void* stream);
+                    double* p_ring, double* ap, void* scratch, double* history,
+                    const bspde_cg_config* cfg, bspde_cg_report* report,
+                    void* stream);
 
 /* ---- step-wise CG for the multi-GPU driver (z-slabs, one rank per GPU).
  * fuse = 1: the kernel's last CTA reduces the per-CTA partials and runs the
@@ -150,17 +156,17 @@ int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
 int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
                     double* p_out, double* ap, void* scratch, int fuse,
                     void* stream);
-/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p applied every
- * other call for two iterations at once, in the reference's rounding order
- * (solver.py:94-101).  p0 / p1: the two ping-pong p buffers.         kind 2 */
-int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, const double* p0,
-                    const double* p1, const double* ap, void* scratch, int fuse,
-                    void* stream);
-/* Apply the last iteration's x update (x += alpha_k p_k, p_k in p0 or p1 by
- * the iteration parity).  bspde_pcg_solve does this itself; step-wise
- * drivers call it once after their loop. */
-int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p0,
-                     const double* p1, void* scratch, void* stream);
+/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p for the last
+ * BSPDE_P_RING iterations at once every BSPDE_P_RING-th call, in the
+ * reference's rounding order (solver.py:94-101).  Iteration k's pass A must
+ * read ring field (k-1) % BSPDE_P_RING and write field k % BSPDE_P_RING. kind 2 */
+int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, const double* p_ring,
+                    const double* ap, void* scratch, int fuse, void* stream);
+/* Apply the pending x updates (x += alpha_j p_j for the iterations since the
+ * last application).  bspde_pcg_solve does this itself; step-wise drivers
+ * call it once after their loop (idempotent). */
+int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p_ring,
+                     void* scratch, void* stream);
 /* kind 0/1/2: scalar update after residual / pass A / pass B (skipped when
  * inactive); kind 3 is used internally by bspde_cg_flush_x. */
 int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);

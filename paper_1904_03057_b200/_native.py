@@ -17,6 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # only; the variant is the same source with different -D constants).
 LIB_PATH = os.environ.get("BSPDE_LIB") or os.path.join(HERE, "libbspde_b200.so")
 
+P_RING = 4  # BSPDE_P_RING: CG search directions in the ring (include/bspde_b200.h)
+
 BSPDE_CG_RUNNING = 0
 BSPDE_CG_CONVERGED = 1
 BSPDE_CG_MAXITER = 2
@@ -79,13 +81,13 @@ SIGNATURES = [
     ("bspde_apply", C.c_int, [_VP, _VP, _VP, _VP]),
     ("bspde_mass_apply", C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP]),
     ("bspde_jacobi_diagonal", C.c_int, [_VP, _dptr, _VP, _VP]),
-    ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+    ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                   C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
     ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,
                                         C.c_int32, _VP]),

@@ -98,14 +98,19 @@ struct Cfg {
   }
 };
 
+// x += alpha p is applied every kPRing iterations (and by the flush at the end
+// of a solve) from a ring of kPRing search directions; see cg_pass_b_kernel
+constexpr int kPRing = BSPDE_P_RING;
+
 struct CgState {
   double sums[4];        // local partial sums (all-reduced across ranks for N>1)
   double rz, alpha, beta, pAp;
   double res, res0, scale, tol;
-  double rhs_norm, alpha_pend;  // alpha of the x update deferred by the last pass B
+  double rhs_norm, pad_d;
   int it, max_iter, active, status;
-  int record_history, has_x0, x_pending, pad_i1;
+  int record_history, has_x0, x_done, pad_i1;  // x_done: iterations applied to x
   double* history;
+  double alpha_ring[kPRing];  // alpha_j at j % kPRing for the pending x updates
 };
 
 struct SepParams {
@@ -153,8 +158,8 @@ struct PassBParams {
   const double* invd;
   double* x;
   double* r;
-  double* p;
-  double* p1;  // flush: second ping-pong p buffer
+  const double* pring;    // kPRing fields, pstride doubles apart
+  long long pstride;
   const double* ap;
   double* partials;
   unsigned* counter;
@@ -259,7 +264,7 @@ __device__ void finalize_state(CgState* s, int kind) {
     s->rhs_norm = sqrt(bb);
     s->it = 0;
     s->beta = 0.0;
-    s->x_pending = 0;
+    s->x_done = 0;
     if (s->rhs_norm == 0.0 && !s->has_x0) {
       s->status = BSPDE_CG_ZERO_RHS;
       s->active = 0;
@@ -287,13 +292,9 @@ __device__ void finalize_state(CgState* s, int kind) {
     s->alpha = s->rz / pAp;
   } else {
     const double rz_new = s->sums[0], rr = s->sums[1];
-    // x moves every other pass B (see cg_pass_b_kernel)
-    if (s->x_pending) {
-      s->x_pending = 0;
-    } else {
-      s->x_pending = 1;
-      s->alpha_pend = s->alpha;
-    }
+    // pass B of iteration k = it applied x up to k when k % kPRing == kPRing-1
+    s->alpha_ring[s->it % kPRing] = s->alpha;
+    if (s->it % kPRing == kPRing - 1) s->x_done = s->it + 1;
     s->beta = rz_new / s->rz;
     s->rz = rz_new;
     s->res = sqrt(rr);
@@ -308,11 +309,11 @@ __device__ void finalize_state(CgState* s, int kind) {
   }
 }
 
-// kind 3: the deferred x update has been applied (after x_flush_kernel)
+// kind 3: the pending x updates have been applied (after x_flush_kernel)
 __global__ void finalize_kernel(CgState* s, int kind) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     if (kind == 3) {
-      s->x_pending = 0;
+      s->x_done = s->it;
       return;
     }
     if (kind != 0 && !s->active) return;
@@ -913,13 +914,13 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 // CG pass B: r -= alpha Ap, <r, D^-1 r>, <r, r> and x += alpha p
 // (solver.py:94-101)
 //
-// Pass A stores p_k into the ping-pong partner of p_{k-1}, so pass B never
-// recomputes p.  x is only read by the caller after the solve: iteration k
-// (x_pending = 0) leaves it and records alpha_k; iteration k+1 reads p_k and
-// p_{k+1} and computes fl(fl(x + fl(alpha_k p_k)) + fl(alpha_{k+1} p_{k+1}))
-// -- bitwise the reference's two stored updates.  So the pass streams 24
-// B/DoF (r, Ap in; r out) and 56 every other time; x_flush_kernel applies a
-// pending update at the end of a solve.
+// Pass A stores p_k into ring field k % kPRing, so pass B never recomputes p.
+// x is only read by the caller after the solve: iterations leave it alone and
+// record alpha_k, and every kPRing-th iteration applies the pending updates
+// x = fl(...fl(fl(x + fl(alpha_j p_j)) + fl(alpha_{j+1} p_{j+1}))...) in
+// order -- bitwise the reference's stored updates (solver.py:94).  So the pass
+// streams 24 B/DoF (r, Ap in; r out), and 40 + 8*kPRing every kPRing-th time;
+// x_flush_kernel applies the pending updates at the end of a solve.
 
 constexpr int NTB = 256;
 
@@ -944,12 +945,19 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
   for (int i = threadIdx.x; i < ncz * ncy * ncx; i += NTB) s_inv[i] = prm.invd[i];
   __syncthreads();
   const double alpha = ld_vol(&prm.state->alpha);
-  const bool xup = ld_vol(&prm.state->x_pending) != 0;
-  const double apend = ld_vol(&prm.state->alpha_pend);
-  // iteration k = it: p_k in p[(k + 1) & 1], p_{k-1} in p[k & 1]
-  const bool odd = (ld_vol(&prm.state->it) & 1) != 0;
-  const double* pcur = odd ? prm.p : prm.p1;
-  const double* pprev = odd ? prm.p1 : prm.p;
+  const int k = ld_vol(&prm.state->it);
+  const int j0 = ld_vol(&prm.state->x_done);
+  // x updates j0..k at the end of each ring period (alpha_k is still in alpha)
+  const bool xup = (k % kPRing == kPRing - 1) && j0 <= k;
+  double aj[kPRing];
+  const double* pj[kPRing];
+#pragma unroll
+  for (int t = 0; t < kPRing; ++t) {
+    const int j = k - (kPRing - 1) + t;
+    const bool on = xup && j >= j0;
+    aj[t] = on ? (j == k ? alpha : ld_vol(&prm.state->alpha_ring[j % kPRing])) : 0.0;
+    pj[t] = on ? prm.pring + (long long)(j % kPRing) * prm.pstride : nullptr;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int nrows = prm.nz * ny;
@@ -966,8 +974,6 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     double* rrw = prm.r + base;
     const double* apr = prm.ap + base;
     double* xr = prm.x + base;
-    const double* pc = pcur + base;
-    const double* pv_ = pprev + base;
     const int npair = nx >> 1;  // pitch is even: double2 rows
     int q = lane;
     if (!xup) {
@@ -1001,11 +1007,11 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     }
     for (; q < npair; q += 32) {
       const int xx = 2 * q;
-      double2 xv = make_double2(0.0, 0.0), p1v = xv, p0v = xv;
+      double2 xv = make_double2(0.0, 0.0), pv[kPRing];
       if (xup) {  // issued with the others
         xv = ld2(xr + xx);
-        p0v = ld2(pv_ + xx);
-        p1v = ld2(pc + xx);
+#pragma unroll
+        for (int t = 0; t < kPRing; ++t) pv[t] = pj[t] ? ld2(pj[t] + base + xx) : xv;
       }
       const double2 rv = ld2(rrw + xx);
       const double2 av = ld2(apr + xx);
@@ -1021,8 +1027,13 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       rr = fma(rn.y, rn.y, rr);
       st2(rrw + xx, rn);
       if (xup) {
-        xv.x = __dadd_rn(__dadd_rn(xv.x, __dmul_rn(apend, p0v.x)), __dmul_rn(alpha, p1v.x));
-        xv.y = __dadd_rn(__dadd_rn(xv.y, __dmul_rn(apend, p0v.y)), __dmul_rn(alpha, p1v.y));
+#pragma unroll
+        for (int t = 0; t < kPRing; ++t) {
+          if (pj[t]) {
+            xv.x = __dadd_rn(xv.x, __dmul_rn(aj[t], pv[t].x));
+            xv.y = __dadd_rn(xv.y, __dmul_rn(aj[t], pv[t].y));
+          }
+        }
         st2(xr + xx, xv);
       }
     }
@@ -1033,7 +1044,13 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       rrw[xx] = rn;
       rz = fma(rn, __dmul_rn(i0, rn), rz);
       rr = fma(rn, rn, rr);
-      if (xup) xr[xx] = __dadd_rn(__dadd_rn(xr[xx], __dmul_rn(apend, pv_[xx])), __dmul_rn(alpha, pc[xx]));
+      if (xup) {
+        double xs = xr[xx];
+#pragma unroll
+        for (int t = 0; t < kPRing; ++t)
+          if (pj[t]) xs = __dadd_rn(xs, __dmul_rn(aj[t], pj[t][base + xx]));
+        xr[xx] = xs;
+      }
     }
   }
   double v[2] = {rz, rr};
@@ -1041,14 +1058,21 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
                                    prm.fuse, 2);
 }
 
-// Applies the pending x update of the last iteration of a solve:
-// x += alpha_pend * p_k, p_k = the ping-pong buffer of parity it (pass A of
-// iteration k writes p_k into p[(k+1) & 1]).  Same row partition and double2
+// Applies the pending x updates of a solve (iterations x_done .. it-1, in
+// order, p_j in ring field j % kPRing).  Same row partition and double2
 // accesses as pass B.
 __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ PassBParams prm) {
-  if (!ld_vol(&prm.state->x_pending)) return;
-  const double a = ld_vol(&prm.state->alpha_pend);
-  const double* pk = (ld_vol(&prm.state->it) & 1) ? prm.p1 : prm.p;
+  const int it = ld_vol(&prm.state->it), j0 = ld_vol(&prm.state->x_done);
+  if (j0 >= it) return;
+  double aj[kPRing];
+  const double* pj[kPRing];
+#pragma unroll
+  for (int t = 0; t < kPRing; ++t) {
+    const int j = j0 + t;
+    const bool on = j < it;
+    aj[t] = on ? ld_vol(&prm.state->alpha_ring[j % kPRing]) : 0.0;
+    pj[t] = on ? prm.pring + (long long)(j % kPRing) * prm.pstride : nullptr;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int nrows = prm.nz * ny;
@@ -1058,17 +1082,26 @@ __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ Pa
     const int zl = row / ny, y = row - zl * ny;
     const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
     double* xr = prm.x + base;
-    const double* pr = pk + base;
     const int npair = nx >> 1;
-#pragma unroll 2
     for (int q = lane; q < npair; q += 32) {
       double2 xv = *reinterpret_cast<const double2*>(xr + 2 * q);
-      const double2 pv = *reinterpret_cast<const double2*>(pr + 2 * q);
-      xv.x = __dadd_rn(xv.x, __dmul_rn(a, pv.x));
-      xv.y = __dadd_rn(xv.y, __dmul_rn(a, pv.y));
+#pragma unroll
+      for (int t = 0; t < kPRing; ++t) {
+        if (pj[t]) {
+          const double2 pv = *reinterpret_cast<const double2*>(pj[t] + base + 2 * q);
+          xv.x = __dadd_rn(xv.x, __dmul_rn(aj[t], pv.x));
+          xv.y = __dadd_rn(xv.y, __dmul_rn(aj[t], pv.y));
+        }
+      }
       *reinterpret_cast<double2*>(xr + 2 * q) = xv;
     }
-    if ((nx & 1) && lane == 0) xr[nx - 1] = __dadd_rn(xr[nx - 1], __dmul_rn(a, pr[nx - 1]));
+    if ((nx & 1) && lane == 0) {
+      double xs = xr[nx - 1];
+#pragma unroll
+      for (int t = 0; t < kPRing; ++t)
+        if (pj[t]) xs = __dadd_rn(xs, __dmul_rn(aj[t], pj[t][base + nx - 1]));
+      xr[nx - 1] = xs;
+    }
   }
 }
 
@@ -1556,7 +1589,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   return BSPDE_OK;
 }
 
-int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, double* p1, const double* ap,
+int launch_pass_b(bspde_plan* pl, double* x, double* r, const double* pring, const double* ap,
                   void* scratch, int fuse, cudaStream_t st, bool flush = false) {
   PassBParams bp;
   const auto& d = pl->d;
@@ -1577,8 +1610,8 @@ int launch_pass_b(bspde_plan* pl, double* x, double* r, double* p, double* p1, c
   bp.invd = pl->d_invd;
   bp.x = x;
   bp.r = r;
-  bp.p = p;
-  bp.p1 = p1;
+  bp.pring = pring;
+  bp.pstride = (long long)(d.nz + 2 * pl->p) * pl->pitch_z;
   bp.ap = ap;
   bp.partials = scratch_partials(scratch);
   bp.counter = scratch_counter(scratch);
@@ -1617,7 +1650,7 @@ int bspde_cg_read_report(bspde_plan*, const void*, bspde_cg_report*, int32_t*, v
 }
 namespace {
 
-int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* p2,
+int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* pring,
                  double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
                  bspde_cg_report* report, cudaStream_t st) {
   void* stream = (void*)st;
@@ -1625,19 +1658,21 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
   if (rc) return rc;
   if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
-  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  // p_{-1} = 0 lives in ring field kPRing - 1 (read by iteration 0)
+  const long long fs = (long long)(pl->d.nz + 2 * pl->p) * pl->pitch_z;
+  CUDA_TRY(cudaMemsetAsync(pring + (kPRing - 1) * fs, 0, bytes, st));
   rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
   if (rc) return rc;
   int32_t active = 0;
   rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
   if (rc) return rc;
-  // even chunks: iteration k reads p[k & 1] and writes p[(k + 1) & 1], so every
-  // replay of the captured chunk starts from the same buffer
+  // iteration k reads ring field (k-1) % R and writes k % R: chunks of a
+  // multiple of R iterations make every replay of the captured graph start
+  // from the same field
   int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
-  K += K & 1;
-  double* pp[2] = {p, p2};
+  K = ((K + kPRing - 1) / kPRing) * kPRing;
   while (active) {
-    bspde_plan::GraphKey key{x, r, p, p2, ap, scratch, K};
+    bspde_plan::GraphKey key{x, r, pring, nullptr, ap, scratch, K};
     auto itg = pl->graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (itg == pl->graphs.end()) {
@@ -1645,9 +1680,9 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
       CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       int crc = BSPDE_OK;
       for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
-        crc = launch_sep(pl, M_CGA, r, pp[k & 1], ap, nullptr, 0.0, 0.0, false, scratch, 1, st,
-                         pp[(k + 1) & 1]);
-        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, p, p2, ap, scratch, 1, st);
+        crc = launch_sep(pl, M_CGA, r, pring + ((k + kPRing - 1) % kPRing) * fs, ap, nullptr, 0.0,
+                         0.0, false, scratch, 1, st, pring + (k % kPRing) * fs);
+        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, pring, ap, scratch, 1, st);
       }
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       if (crc) {
@@ -1670,7 +1705,7 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
     rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
     if (rc) return rc;
   }
-  return launch_pass_b(pl, x, r, p, p2, ap, scratch, 1, st, /*flush=*/true);
+  return launch_pass_b(pl, x, r, pring, ap, scratch, 1, st, /*flush=*/true);
 }
 
 }  // namespace
@@ -1947,20 +1982,19 @@ int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p_in, double*
                     (cudaStream_t)stream, p_out);
 }
 
-int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, const double* p0, const double* p1,
+int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, const double* p_ring,
                     const double* ap, void* scratch, int fuse, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!x || !r || !p0 || !p1 || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_pass_b(pl, x, r, const_cast<double*>(p0), const_cast<double*>(p1), ap, scratch,
-                       fuse, (cudaStream_t)stream);
+  if (!x || !r || !p_ring || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, x, r, p_ring, ap, scratch, fuse, (cudaStream_t)stream);
 }
 
-int bspde_cg_flush_x(bspde_plan* pl, double* x, const double* p0, const double* p1, void* scratch,
+int bspde_cg_flush_x(bspde_plan* pl, double* x, const double* p_ring, void* scratch,
                      void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!x || !p0 || !p1 || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_pass_b(pl, x, nullptr, const_cast<double*>(p0), const_cast<double*>(p1), nullptr,
-                       scratch, 1, (cudaStream_t)stream, /*flush=*/true);
+  if (!x || !p_ring || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, x, nullptr, p_ring, nullptr, scratch, 1, (cudaStream_t)stream,
+                       /*flush=*/true);
 }
 
 int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
@@ -1993,20 +2027,19 @@ int bspde_cg_read_report(bspde_plan* pl, const void* scratch, bspde_cg_report* r
   return BSPDE_OK;
 }
 
-int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p, double* p2,
+int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p_ring,
                     double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
                     bspde_cg_report* report, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!b || !x || !r || !p || !p2 || !ap || !scratch || !cfg)
+  if (!b || !x || !r || !p_ring || !ap || !scratch || !cfg)
     return fail(BSPDE_ERR_ARG, "null argument");
-  if (p == p2) return fail(BSPDE_ERR_ARG, "p and p2 must be different buffers");
   // everything runs on the plan's private stream, ordered after the caller's
   // stream on entry and before it on exit
   cudaStream_t caller = (cudaStream_t)stream;
   cudaStream_t st = pl->work;
   CUDA_TRY(cudaEventRecord(pl->ev_in, caller));
   CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_in, 0));
-  int rc = pcg_solve_on(pl, b, x, r, p, p2, ap, scratch, history, cfg, report, st);
+  int rc = pcg_solve_on(pl, b, x, r, p_ring, ap, scratch, history, cfg, report, st);
   cudaEventRecord(pl->ev_out, st);
   cudaStreamWaitEvent(caller, pl->ev_out, 0);
   return rc;

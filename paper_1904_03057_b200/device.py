@@ -69,6 +69,12 @@ class SlabLayout:
         torch = _torch()
         return torch.zeros(self.buf_shape, dtype=torch.float64, device=device)
 
+    def alloc_ring(self, device, n=None):
+        """``n`` (default BSPDE_P_RING) fields back to back: the CG p ring."""
+        torch = _torch()
+        n = N.P_RING if n is None else n
+        return torch.zeros((n,) + self.buf_shape, dtype=torch.float64, device=device)
+
     def owned(self, buf):
         return buf[self.ghost:self.ghost + self.nz, :, :self.nx]
 
@@ -158,13 +164,13 @@ class NativePlan:
         N.check(self.lib.bspde_jacobi_diagonal(self.handle, tab.ctypes.data_as(N._dptr),
                                                N.ptr(out), N.stream_handle(stream)))
 
-    def pcg(self, b, x, r, p, p2, ap, scratch, history, tol, max_iter, record_history, has_x0,
+    def pcg(self, b, x, r, pring, ap, scratch, history, tol, max_iter, record_history, has_x0,
             poll_every=8, stream=None):
         cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
                          int(bool(has_x0)), int(poll_every))
         rep = N.CgReport()
-        N.check(self.lib.bspde_pcg_solve(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(p),
-                                         N.ptr(p2), N.ptr(ap), N.ptr(scratch), N.ptr(history),
+        N.check(self.lib.bspde_pcg_solve(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(pring),
+                                         N.ptr(ap), N.ptr(scratch), N.ptr(history),
                                          C.byref(cfg), C.byref(rep), N.stream_handle(stream)))
         return rep
 
@@ -184,14 +190,14 @@ class NativePlan:
                                          N.ptr(ap), N.ptr(scratch), int(fuse),
                                          N.stream_handle(stream)))
 
-    def cg_pass_b(self, x, r, p0, p1, ap, scratch, fuse, stream=None):
-        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(p0), N.ptr(p1),
+    def cg_pass_b(self, x, r, pring, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(pring),
                                          N.ptr(ap), N.ptr(scratch), int(fuse),
                                          N.stream_handle(stream)))
 
-    def cg_flush_x(self, x, p0, p1, scratch, stream=None):
-        N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(p0), N.ptr(p1),
-                                          N.ptr(scratch), N.stream_handle(stream)))
+    def cg_flush_x(self, x, pring, scratch, stream=None):
+        N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(pring), N.ptr(scratch),
+                                          N.stream_handle(stream)))
 
     def cg_finalize(self, scratch, kind, stream=None):
         N.check(self.lib.bspde_cg_finalize(self.handle, N.ptr(scratch), int(kind),

@@ -139,27 +139,28 @@ class NativeSlabOps:
     def pass_a(self, r, p_in, p_out, ap, scratch):
         self.plan.cg_pass_a(r, p_in, p_out, ap, scratch, 0)
 
-    def pass_b(self, x, r, p0, p1, ap, scratch):
-        self.plan.cg_pass_b(x, r, p0, p1, ap, scratch, 0)
+    def pass_b(self, x, r, pring, ap, scratch):
+        self.plan.cg_pass_b(x, r, pring, ap, scratch, 0)
 
     def finalize(self, scratch, kind):
         self.plan.cg_finalize(scratch, kind)
 
-    def flush_x(self, x, p0, p1, scratch):
-        self.plan.cg_flush_x(x, p0, p1, scratch)
+    def flush_x(self, x, pring, scratch):
+        self.plan.cg_flush_x(x, pring, scratch)
 
     def read(self, scratch):
         return self.plan.cg_read(scratch)
 
 
-def distributed_pcg(ops, halo, allreduce, b, x, r, p, p2, ap, scratch, config: SolveConfig,
+def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: SolveConfig,
                     has_x0=True, history=None):
     """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
-    ``p``/``p2`` are the ping-pong search-direction buffers."""
+    ``pring`` holds the ring of search directions (leading axis)."""
     t0 = time.perf_counter()
     if not has_x0:
         x.zero_()
-    p.zero_()
+    R = pring.shape[0]
+    pring[R - 1].zero_()  # p_{-1} = 0
     ops.setup(scratch, history, config, has_x0)
     halo(x)
     ops.residual(b, x, r, scratch)
@@ -167,22 +168,21 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, p, p2, ap, scratch, config: S
     ops.finalize(scratch, 0)
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
-    pp = (p, p2)
     k = 0
     while active:
         for _ in range(K):
-            p_in, p_out = pp[k & 1], pp[(k + 1) & 1]
+            p_in, p_out = pring[(k - 1) % R], pring[k % R]
             halo(r)
             halo(p_in)
             ops.pass_a(r, p_in, p_out, ap, scratch)
             allreduce(ops.sums(scratch, 1))
             ops.finalize(scratch, 1)
-            ops.pass_b(x, r, p, p2, ap, scratch)
+            ops.pass_b(x, r, pring, ap, scratch)
             allreduce(ops.sums(scratch, 2))
             ops.finalize(scratch, 2)
             k += 1
         rep, active = ops.read(scratch)
-    ops.flush_x(x, p, p2, scratch)  # a pending x update of the last iteration
+    ops.flush_x(x, pring, scratch)  # the pending x updates
     return rep, time.perf_counter() - t0
 
 
@@ -265,8 +265,7 @@ class DistributedOperator:
 
         if self._work is None:
             lay = self.layout
-            self._work = dict(r=lay.alloc(self.device), p=lay.alloc(self.device),
-                              p2=lay.alloc(self.device),
+            self._work = dict(r=lay.alloc(self.device), pring=lay.alloc_ring(self.device),
                               ap=lay.alloc(self.device), scratch=self.plan().scratch(),
                               history=None)
         w = self._work
@@ -278,8 +277,8 @@ class DistributedOperator:
         config = config or SolveConfig()
         w = self._work_buffers(config.max_iter)
         ops = NativeSlabOps(self.plan(config.precond))
-        rep, wall = distributed_pcg(ops, self.halo, self.allreduce, b_buf, x_buf, w["r"], w["p"],
-                                    w["p2"], w["ap"], w["scratch"], config, has_x0,
+        rep, wall = distributed_pcg(ops, self.halo, self.allreduce, b_buf, x_buf, w["r"],
+                                    w["pring"], w["ap"], w["scratch"], config, has_x0,
                                     w["history"] if config.record_history else None)
         return report_from(rep, config, wall, w["history"])
 

@@ -8,9 +8,10 @@ history, 1e3 divergence guard; stop on recursive ||r||/||b|| <= tol or
 max_iter), executed as two fused sm_100a kernels per iteration:
 
 * pass A (``sep_kernel<P, M_CGA>``): p_k = D^-1 r + beta p_{k-1} formed on
-  the fly in shared memory (and stored to the ping-pong partner buffer),
-  Ap_k, <p_k, Ap_k>, and the previous iteration's x += alpha_{k-1} p_{k-1};
-* pass B (``cg_pass_b_kernel``): r -= alpha Ap, <r, D^-1 r>, <r, r>;
+  the fly in shared memory (and stored to ring field k % P_RING), Ap_k,
+  <p_k, Ap_k>;
+* pass B (``cg_pass_b_kernel``): r -= alpha Ap, <r, D^-1 r>, <r, r>; every
+  P_RING-th iteration also x += alpha_j p_j for the last P_RING iterations;
 
 each finishing with a deterministic fixed-order reduction whose last CTA
 runs the scalar update on the device.  Chunks of iterations are replayed as
@@ -64,16 +65,15 @@ class SolveReport:
 
 
 class CgWork:
-    """Device work vectors for one operator: r, p / p2 (ping-pong search
-    directions), Ap, scalar scratch, history.
+    """Device work vectors for one operator: r, the ring of P_RING search
+    directions, Ap, scalar scratch, history.
 
     Allocated once and reused; nothing is allocated inside the CG loop."""
 
     def __init__(self, op, max_iter):
         lay = op.layout
         self.r = lay.alloc(op.device)
-        self.p = lay.alloc(op.device)
-        self.p2 = lay.alloc(op.device)
+        self.pring = lay.alloc_ring(op.device)
         self.ap = lay.alloc(op.device)
         self.scratch = op.plan().scratch()
         self.history = None
@@ -126,7 +126,7 @@ def pcg_device(op, b_buf, x_buf, config: SolveConfig = None, has_x0=True, stream
     w = _work(op, config.max_iter)
     w.ensure_history(op, config.max_iter)
     plan = op.plan(config.precond)
-    rep = plan.pcg(b_buf, x_buf, w.r, w.p, w.p2, w.ap, w.scratch,
+    rep = plan.pcg(b_buf, x_buf, w.r, w.pring, w.ap, w.scratch,
                    w.history if config.record_history else None, config.tol, config.max_iter,
                    config.record_history, has_x0, config.poll_every, stream)
     return report_from(rep, config, time.perf_counter() - t0, w.history)

@@ -75,15 +75,23 @@ class CpuSlabOps:
         self._own(ap).copy_(apv)
         scratch[0] = float((pn[g:g + nz] * apv).sum())
 
-    def pass_b(self, x, r, p0, p1, ap, scratch):
+    def _apply_x(self, x, pring, upto, alphas):
+        s = self.state
+        R = pring.shape[0]
+        for j in range(s.get("x_done", 0), upto):  # in order, as the kernels
+            self._own(x).add_(alphas[j % R] * self._own(pring[j % R]))
+
+    def pass_b(self, x, r, pring, ap, scratch):
         s = self.state
         if not s["active"]:
             return
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         own_inv = self.inv[g:g + nz, :, :nx]
-        if s.get("x_pending"):  # two updates at once, as cg_pass_b_kernel
-            pcur, pprev = (p0, p1) if s["it"] & 1 else (p1, p0)
-            self._own(x).add_(s["alpha_pend"] * self._own(pprev)).add_(s["alpha"] * self._own(pcur))
+        R, k = pring.shape[0], s["it"]
+        if k % R == R - 1:  # every R-th iteration: the last R updates, as cg_pass_b_kernel
+            ring = list(s.setdefault("alpha_ring", [0.0] * R))
+            ring[k % R] = s["alpha"]
+            self._apply_x(x, pring, k + 1, ring)
         self._own(r).sub_(s["alpha"] * self._own(ap))
         rv = self._own(r)
         scratch[0] = float((rv * (own_inv * rv)).sum())
@@ -110,21 +118,21 @@ class CpuSlabOps:
             return
         else:
             rz_new, rr = float(scratch[0]), float(scratch[1])
-            if s.get("x_pending"):
-                s["x_pending"] = 0
-            else:
-                s["x_pending"], s["alpha_pend"] = 1, s["alpha"]
+            ring = s.setdefault("alpha_ring", [0.0] * 4)
+            R = len(ring)
+            ring[s["it"] % R] = s["alpha"]
+            if s["it"] % R == R - 1:
+                s["x_done"] = s["it"] + 1
             s["beta"] = rz_new / s["rz"]
             s["rz"] = rz_new
             s["res"] = np.sqrt(rr)
             s["it"] += 1
         s["active"] = int(s["res"] / s["scale"] > s["tol"] and s["it"] < s["max_iter"])
 
-    def flush_x(self, x, p0, p1, scratch):
-        if self.state.get("x_pending"):
-            pk = p1 if self.state["it"] & 1 else p0
-            self._own(x).add_(self.state["alpha_pend"] * self._own(pk))
-            self.state["x_pending"] = 0
+    def flush_x(self, x, pring, scratch):
+        s = self.state
+        self._apply_x(x, pring, s["it"], s.get("alpha_ring", [0.0] * pring.shape[0]))
+        s["x_done"] = s["it"]
 
     def read(self, scratch):
         class Rep:
@@ -154,7 +162,8 @@ def _worker(rank, world, port, ext, p, out_q):
         lo, hi = part.bounds()
         b = lay.upload(b_full[lo:hi], "cpu")
         x = lay.upload(x0_full[lo:hi], "cpu")
-        r, pp, pp2, ap = lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu"), lay.alloc("cpu")
+        r, ap = lay.alloc("cpu"), lay.alloc("cpu")
+        pring = torch.zeros((4,) + tuple(lay.buf_shape), dtype=torch.float64)
         scratch = torch.zeros(8, dtype=torch.float64)
         ops = CpuSlabOps(ora, lay)
         halo = HaloExchanger(lay, rank, world)
@@ -163,7 +172,7 @@ def _worker(rank, world, port, ext, p, out_q):
             dist.all_reduce(t)
 
         cfg = SolveConfig(tol=1e-13, max_iter=1000, poll_every=3)
-        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pp, pp2, ap, scratch, cfg,
+        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, cfg,
                                  has_x0=True)
         own = lay.owned(x).contiguous()
         parts = [torch.zeros((part.bounds(q)[1] - part.bounds(q)[0],) + tuple(own.shape[1:]),

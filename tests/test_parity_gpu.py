@@ -310,8 +310,9 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     w = _work(op, 10)
     bb = lay.upload(b, op.device)
     xb = lay.upload(x0, op.device)
-    w.p.zero_()
-    w.p2.fill_(np.nan)  # pass A must write every owned point of p_out
+    R = w.pring.shape[0]
+    w.pring[R - 1].zero_()  # p_{-1}
+    w.pring[0].fill_(np.nan)  # pass A must write every owned point of p_out
     plan.cg_setup(w.scratch, None, 1e-300, 100, False, has_x0)
     plan.cg_residual(bb, xb, w.r, w.scratch, 1)
     torch.cuda.synchronize()
@@ -321,10 +322,10 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     st = w.scratch[:160].cpu().numpy().view(np.float64)
     rz0 = float(np.vdot(r0, inv * r0))
     assert abs(st[4] - rz0) / rz0 < 1e-12  # state.rz
-    plan.cg_pass_a(w.r, w.p, w.p2, w.ap, w.scratch, 1)
+    plan.cg_pass_a(w.r, w.pring[R - 1], w.pring[0], w.ap, w.scratch, 1)
     torch.cuda.synchronize()
     p0 = inv * r0
-    assert float(relmax(lay.download(w.p2), p0)) < 1e-13  # p_k written by pass A
+    assert float(relmax(lay.download(w.pring[0]), p0)) < 1e-13  # p_k written by pass A
     assert np.array_equal(lay.download(xb), x0)  # nothing pending before iteration 0
     Ap = ora.apply(p0)
     assert relmax(lay.download(w.ap), Ap) < 1e-13
@@ -333,28 +334,28 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     assert abs(st[7] - pAp) / pAp < 1e-12  # state.pAp
     alpha = rz0 / pAp
     assert abs(st[5] - alpha) / alpha < 1e-12  # state.alpha
-    plan.cg_pass_b(xb, w.r, w.p, w.p2, w.ap, w.scratch, 1)
+    plan.cg_pass_b(xb, w.r, w.pring, w.ap, w.scratch, 1)
     torch.cuda.synchronize()
     x1 = x0 + alpha * p0
     r1 = r0 - alpha * Ap
-    # the x update of an odd pass B is deferred until the next one / a flush
+    # x moves every P_RING-th pass B (or on a flush)
     assert np.array_equal(lay.download(xb), x0)
     assert relmax(lay.download(w.r), r1) < 1e-12
     rep, active = plan.cg_read(w.scratch)
     assert rep.iterations == 1
     assert abs(rep.residual - np.linalg.norm(r1)) / np.linalg.norm(r1) < 1e-12
     xe = xb.clone()
-    plan.cg_flush_x(xe, w.p, w.p2, w.scratch)
+    plan.cg_flush_x(xe, w.pring, w.scratch)
     torch.cuda.synchronize()
     assert relmax(lay.download(xe), x1) < 1e-13
-    plan.cg_flush_x(xe, w.p, w.p2, w.scratch)  # idempotent: nothing pending any more
+    plan.cg_flush_x(xe, w.pring, w.scratch)  # idempotent: nothing pending any more
     assert relmax(lay.download(xe), x1) < 1e-13
 
 
-@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5, 7, 8, 9])
 def test_deferred_x_update_is_bitwise_eager(cuda_device, iters):
-    """Pass B moves x every other iteration; flushing after every iteration
-    instead must give bit-identical x (the same two stored roundings)."""
+    """Pass B moves x every P_RING-th iteration; flushing after every
+    iteration instead must give bit-identical x (the same stored roundings)."""
     import torch
 
     ext, p = (13, 12, 11), 3
@@ -369,16 +370,17 @@ def test_deferred_x_update_is_bitwise_eager(cuda_device, iters):
         lay, plan = op.layout, op.plan()
         bb, xb = lay.upload(b, op.device), lay.upload(x0, op.device)
         r, ap = lay.alloc(op.device), lay.alloc(op.device)
-        pp = (lay.alloc(op.device), lay.alloc(op.device))
+        pring = lay.alloc_ring(op.device)
+        R = pring.shape[0]
         scratch = plan.scratch()
         plan.cg_setup(scratch, None, 1e-300, 100, False, True)
         plan.cg_residual(bb, xb, r, scratch, 1)
         for k in range(iters):
-            plan.cg_pass_a(r, pp[k & 1], pp[(k + 1) & 1], ap, scratch, 1)
-            plan.cg_pass_b(xb, r, pp[0], pp[1], ap, scratch, 1)
+            plan.cg_pass_a(r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
+            plan.cg_pass_b(xb, r, pring, ap, scratch, 1)
             if eager:
-                plan.cg_flush_x(xb, pp[0], pp[1], scratch)
-        plan.cg_flush_x(xb, pp[0], pp[1], scratch)
+                plan.cg_flush_x(xb, pring, scratch)
+        plan.cg_flush_x(xb, pring, scratch)
         torch.cuda.synchronize()
         outs.append(lay.download(xb))
     assert np.array_equal(outs[0], outs[1])
