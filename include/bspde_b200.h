@@ -196,6 +196,54 @@ int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
                    const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
                    int32_t offset, const double* taps, int32_t ntaps, void* stream);
 
+/* ---- variable-coefficient operator ---------------
+ * The reference's on-the-fly operator for spline-valued diffusion D(x) and
+ * absorption mu(x) fields (operator.py:217-229, stencil_block
+ * assembly.py:460-472): per node l the (2p+1)^3 stencil
+ *   P[a, l] = sum_b [ D[l+b] (sz Tz'Ty Tx + sy Tz Ty' Tx + sx Tz Ty Tx')[a, b]
+ *                   + mu[l+b] sm (Tz Ty Tx)[a, b] ]
+ * from per-axis trilinear tables (kernels.py:158-173, edge rows
+ * assembly.py:83-108), assembled once into HBM and applied as
+ * t_l = sum_a P[a, l] c[l + a].  Box domains, natural faces, 3-D.
+ * Fields are dense (z, y, x) arrays (x fastest) on the device. */
+typedef struct bspde_stencil bspde_stencil;
+
+typedef struct {
+  int32_t device;
+  int32_t degree;        /* n_b in 1..5 */
+  int32_t param_degree;  /* n_p in 1..5 (degree of the D / mu fields) */
+  int32_t nz, ny, nx;    /* coefficient (extended) extents */
+  int32_t pz, py, px;    /* parameter-field (extended) extents */
+  int32_t ext, ext_p;    /* basis_extension(n_b), basis_extension(n_p) */
+  int32_t ew[3];         /* edge rows per axis end */
+  /* host: per axis, [0] = value/value, [1] = derivative/derivative trilinear
+   * class tables, (2ew+1) x (2n_b+1) x (2mw+1), mw = (n_b+n_p+1)/2 */
+  const double* tables[3][2];
+  double scale_stiff[3]; /* vol / h_a^2 */
+  double scale_mass;     /* vol */
+} bspde_stencil_desc;
+
+int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** plan);
+int bspde_stencil_destroy(bspde_stencil* plan);
+/* number of doubles of the stencil array P ((2p+1)^3 * nz*ny*nx) */
+int64_t bspde_stencil_entries(const bspde_stencil* plan);
+int64_t bspde_stencil_launch_count(const bspde_stencil* plan);
+/* P <- stencils of all nodes from the parameter fields (device, dense) */
+int bspde_stencil_assemble(bspde_stencil* plan, const double* dfield,
+                           const double* mfield, double* P, void* stream);
+/* out = A c (OnTheFlyOperator.apply) */
+int bspde_stencil_apply(bspde_stencil* plan, const double* P, const double* c,
+                        double* out, void* stream);
+/* out = diag(A) (_diagonal_from_bands) */
+int bspde_stencil_diagonal(bspde_stencil* plan, const double* P, double* out,
+                           void* stream);
+/* Jacobi-PCG (solver.py:51-117; precond 1 = jacobi, 0 = none) on dense
+ * fields; scratch: bspde_scratch_bytes-sized (any plan). */
+int bspde_stencil_pcg(bspde_stencil* plan, const double* P, const double* b,
+                      double* x, double* r, double* p, double* ap, void* scratch,
+                      double* history, const bspde_cg_config* cfg,
+                      bspde_cg_report* report, int32_t precond, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

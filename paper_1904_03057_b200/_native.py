@@ -56,6 +56,21 @@ class CgConfig(C.Structure):
     ]
 
 
+class StencilDesc(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("degree", C.c_int32),
+        ("param_degree", C.c_int32),
+        ("nz", C.c_int32), ("ny", C.c_int32), ("nx", C.c_int32),
+        ("pz", C.c_int32), ("py", C.c_int32), ("px", C.c_int32),
+        ("ext", C.c_int32), ("ext_p", C.c_int32),
+        ("ew", C.c_int32 * 3),
+        ("tables", (_dptr * 2) * 3),
+        ("scale_stiff", C.c_double * 3),
+        ("scale_mass", C.c_double),
+    ]
+
+
 class CgReport(C.Structure):
     _fields_ = [
         ("iterations", C.c_int32),
@@ -88,6 +103,15 @@ SIGNATURES = [
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_stencil_create", C.c_int, [C.POINTER(StencilDesc), C.POINTER(C.c_void_p)]),
+    ("bspde_stencil_destroy", C.c_int, [_VP]),
+    ("bspde_stencil_entries", C.c_int64, [_VP]),
+    ("bspde_stencil_launch_count", C.c_int64, [_VP]),
+    ("bspde_stencil_assemble", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_stencil_apply", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_stencil_diagonal", C.c_int, [_VP, _VP, _VP, _VP]),
+    ("bspde_stencil_pcg", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                    C.POINTER(CgConfig), C.POINTER(CgReport), C.c_int32, _VP]),
     ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,
                                         C.c_int32, _VP]),

@@ -30,7 +30,8 @@ def needs_rebuild():
     if not os.path.exists(LIB):
         return True
     mt = os.path.getmtime(LIB)
-    deps = [SRC, os.path.join(ROOT, "include", "bspde_b200.h")]
+    deps = [SRC, os.path.join(ROOT, "include", "bspde_b200.h"),
+            os.path.join(HERE, "csrc", "stencil.cuh"), os.path.join(HERE, "csrc", "gram_taps.cuh")]
     return any(os.path.getmtime(d) > mt for d in deps if os.path.exists(d))
 
 

@@ -2046,3 +2046,5 @@ int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, doubl
 }
 
 }  // extern "C"
+
+#include "stencil.cuh"

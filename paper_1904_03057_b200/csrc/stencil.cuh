@@ -1,0 +1,445 @@
+// stencil.cuh -- variable-coefficient operator, included
+// at the end of bspde_b200.cu (shares the CG state machine and reductions).
+//
+// The reference's on-the-fly operator (operator.py:217-229 over
+// stencil_block, assembly.py:460-472) builds, per node l, the (2p+1)^3
+// stencil
+//
+//   P[a, l] = sum_terms s_term sum_b f_term[l + b] Tz[az, bz] Ty[ay, by] Tx[ax, bx]
+//
+// from per-axis trilinear tables (kernels.py:158-173, positional edge rows
+// assembly.py:83-108) and the parameter fields (diffusion for the three
+// stiffness terms, absorption for the mass term), then applies
+// t_l = sum_a P[a, l] c[l + a].  Here the stencil is assembled once into HBM
+// (structure of arrays: P[a * N + l], coalesced in l) by stencil_assemble_kernel
+// and applied by a streaming gather (stencil_apply_kernel) -- the B200
+// counterpart of the reference's "sparse" strategy, sized for up to ~300^3
+// per GPU (2.7 KB per DoF at p = 3).  Jacobi-PCG runs the reference
+// recurrence with three kernels per iteration (p formation, apply + <p,Ap>,
+// x/r update + dots) and the same device-side scalar state as the
+// constant-coefficient solver.
+
+namespace {
+
+constexpr int ST_NT = 256;
+
+struct StencilDev {
+  int nb, np, A, B, mw;     // A = 2nb+1 trial offsets, B = 2mw+1 parameter offsets
+  int nz, ny, nx;           // coefficient extents (dense arrays)
+  int pz, py, px;           // parameter-field extents
+  int ext, ext_p;
+  int ew[3];
+  long long N;              // nz*ny*nx
+  double s_stiff[3], s_mass;
+  const double* tab;        // [axis][d][class][A][B] (class stride 2*EWMAX+1)
+  int ncls;                 // class stride
+};
+
+__device__ __forceinline__ int st_cls(int i, int n, int ew) {
+  return i < ew ? i : (i >= n - ew ? 2 * ew - (n - 1 - i) : ew);
+}
+
+__device__ __forceinline__ const double* st_tab(const StencilDev& S, const double* tab, int axis,
+                                                int d, int cls) {
+  return tab + ((((long long)axis * 2 + d) * S.ncls + cls) * S.A) * S.B;
+}
+
+// one thread per (entry a, node l): consecutive threads = consecutive l
+__global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDev S,
+                                                                 const double* __restrict__ dfield,
+                                                                 const double* __restrict__ mfield,
+                                                                 double* __restrict__ P) {
+  extern __shared__ double s_tab[];
+  const int ntab = 3 * 2 * S.ncls * S.A * S.B;
+  for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_tab[i] = S.tab[i];
+  __syncthreads();
+  const long long A3 = (long long)S.A * S.A * S.A;
+  const long long total = A3 * S.N;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long l = t % S.N;
+    const int a = (int)(t / S.N);
+    const int ax = a % S.A, ay = (a / S.A) % S.A, az = a / (S.A * S.A);
+    const int lx = (int)(l % S.nx), ly = (int)((l / S.nx) % S.ny), lz = (int)(l / ((long long)S.nx * S.ny));
+    const int cz = st_cls(lz, S.nz, S.ew[0]), cy = st_cls(ly, S.ny, S.ew[1]),
+              cx = st_cls(lx, S.nx, S.ew[2]);
+    const double* tz0 = st_tab(S, s_tab, 0, 0, cz) + az * S.B;
+    const double* tz1 = st_tab(S, s_tab, 0, 1, cz) + az * S.B;
+    const double* ty0 = st_tab(S, s_tab, 1, 0, cy) + ay * S.B;
+    const double* ty1 = st_tab(S, s_tab, 1, 1, cy) + ay * S.B;
+    const double* tx0 = st_tab(S, s_tab, 2, 0, cx) + ax * S.B;
+    const double* tx1 = st_tab(S, s_tab, 2, 1, cx) + ax * S.B;
+    // parameter window of node l: field index (l - ext) + ext_p + (b - mw)
+    const int fz0 = lz - S.ext + S.ext_p - S.mw, fy0 = ly - S.ext + S.ext_p - S.mw,
+              fx0 = lx - S.ext + S.ext_p - S.mw;
+    double acc = 0.0;
+    for (int bz = 0; bz < S.B; ++bz) {
+      const int fz = fz0 + bz;
+      if (fz < 0 || fz >= S.pz) continue;
+      for (int by = 0; by < S.B; ++by) {
+        const int fy = fy0 + by;
+        if (fy < 0 || fy >= S.py) continue;
+        const double zy00 = tz0[bz] * ty0[by];
+        const double k_z = S.s_stiff[0] * tz1[bz] * ty0[by];
+        const double k_y = S.s_stiff[1] * tz0[bz] * ty1[by];
+        const double k_x = S.s_stiff[2] * zy00;
+        const double m_zy = S.s_mass * zy00;
+        const long long row = ((long long)fz * S.py + fy) * S.px;
+        for (int bx = 0; bx < S.B; ++bx) {
+          const int fx = fx0 + bx;
+          if (fx < 0 || fx >= S.px) continue;
+          const double dv = dfield[row + fx], mv = mfield[row + fx];
+          const double kd = (k_z + k_y) * tx0[bx] + k_x * tx1[bx];
+          acc = fma(dv, kd, fma(mv, m_zy * tx0[bx], acc));
+        }
+      }
+    }
+    P[(long long)a * S.N + l] = acc;
+  }
+}
+
+// t_l = sum_a P[a, l] c[l + a] with three epilogues:
+//   0 apply:  out = t
+//   1 resid:  out = r = b - t;  sums {<b,b>, <r,D^-1 r>, <r,r>}   (kind 0)
+//   2 cg:     out = Ap;         sums {<p,Ap>}                    (kind 1)
+template <int MODE>
+__global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S,
+                                                              const double* __restrict__ P,
+                                                              const double* __restrict__ c,
+                                                              double* __restrict__ out,
+                                                              const double* __restrict__ aux,
+                                                              double* partials, unsigned* counter,
+                                                              CgState* st, int precond) {
+  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ unsigned s_last;
+  if (MODE == 2 && !ld_vol(&st->active)) return;
+  const int A = S.A, hb = S.nb;
+  const int center = (hb * A + hb) * A + hb;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int lx = (int)(l % S.nx), ly = (int)((l / S.nx) % S.ny), lz = (int)(l / ((long long)S.nx * S.ny));
+    double t = 0.0;
+    int a = 0;
+    for (int az = -hb; az <= hb; ++az) {
+      const int z = lz + az;
+      const bool zok = z >= 0 && z < S.nz;
+      for (int ay = -hb; ay <= hb; ++ay) {
+        const int y = ly + ay;
+        const bool yok = zok && y >= 0 && y < S.ny;
+        const long long row = ((long long)z * S.ny + y) * S.nx;
+        for (int ax = -hb; ax <= hb; ++ax, ++a) {
+          const int x = lx + ax;
+          if (yok && x >= 0 && x < S.nx) t = fma(P[(long long)a * S.N + l], c[row + x], t);
+        }
+      }
+    }
+    if (MODE == 0) {
+      out[l] = t;
+    } else if (MODE == 1) {
+      const double bb = aux[l];
+      const double r = bb - t;
+      out[l] = r;
+      const double dg = P[(long long)center * S.N + l];
+      const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+      s0 = fma(bb, bb, s0);
+      s1 = fma(r, __dmul_rn(inv, r), s1);
+      s2 = fma(r, r, s2);
+    } else {
+      out[l] = t;
+      s0 = fma(c[l], t, s0);
+    }
+  }
+  if (MODE == 1) {
+    double v[3] = {s0, s1, s2};
+    reduce_and_finalize<3, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 0);
+  } else if (MODE == 2) {
+    double v[1] = {s0};
+    reduce_and_finalize<1, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 1);
+  }
+}
+
+// p = D^-1 r + beta p (reference rounding order, solver.py:96-100)
+__global__ void __launch_bounds__(ST_NT) stencil_pform_kernel(const StencilDev S, const double* P,
+                                                              const double* __restrict__ r,
+                                                              double* __restrict__ p,
+                                                              CgState* st, int precond) {
+  if (!ld_vol(&st->active)) return;
+  const double beta = ld_vol(&st->beta);
+  const int A = S.A, hb = S.nb;
+  const int center = (hb * A + hb) * A + hb;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
+       l += (long long)gridDim.x * blockDim.x) {
+    const double dg = P[(long long)center * S.N + l];
+    const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+    p[l] = pdir(r[l], inv, p[l], beta);
+  }
+}
+
+// x += alpha p; r -= alpha Ap; sums {<r, D^-1 r>, <r, r>}  (kind 2)
+__global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev S, const double* P,
+                                                               double* __restrict__ x,
+                                                               double* __restrict__ r,
+                                                               const double* __restrict__ p,
+                                                               const double* __restrict__ ap,
+                                                               double* partials, unsigned* counter,
+                                                               CgState* st, int precond) {
+  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ unsigned s_last;
+  if (!ld_vol(&st->active)) return;
+  const double alpha = ld_vol(&st->alpha);
+  const int A = S.A, hb = S.nb;
+  const int center = (hb * A + hb) * A + hb;
+  double rz = 0.0, rr = 0.0;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
+       l += (long long)gridDim.x * blockDim.x) {
+    x[l] = __dadd_rn(x[l], __dmul_rn(alpha, p[l]));
+    const double rn = __dsub_rn(r[l], __dmul_rn(alpha, ap[l]));
+    r[l] = rn;
+    const double dg = P[(long long)center * S.N + l];
+    const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+    rz = fma(rn, __dmul_rn(inv, rn), rz);
+    rr = fma(rn, rn, rr);
+  }
+  double v[2] = {rz, rr};
+  reduce_and_finalize<2, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 2);
+}
+
+__global__ void stencil_diag_kernel(const StencilDev S, const double* P, double* out) {
+  const int A = S.A, hb = S.nb;
+  const int center = (hb * A + hb) * A + hb;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
+       l += (long long)gridDim.x * blockDim.x)
+    out[l] = P[(long long)center * S.N + l];
+}
+
+}  // namespace
+
+struct bspde_stencil {
+  bspde_stencil_desc d;
+  StencilDev S;
+  int device = 0;
+  int num_sms = 148;
+  double* d_tab = nullptr;
+  size_t tab_bytes = 0;
+  void* host_state = nullptr;
+  cudaStream_t work = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int64_t launches = 0;
+};
+
+namespace {
+
+int st_check(bspde_stencil* s) {
+  if (!s) return fail(BSPDE_ERR_ARG, "null stencil plan");
+  cudaError_t e = cudaSetDevice(s->device);
+  if (e != cudaSuccess) return fail(BSPDE_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return BSPDE_OK;
+}
+
+unsigned st_grid(const bspde_stencil* s, long long n) {
+  const long long want = (n + ST_NT - 1) / ST_NT;
+  return (unsigned)std::max<long long>(1, std::min<long long>(want, std::min(MAXGRID, s->num_sms * 8)));
+}
+
+int st_read(bspde_stencil* s, void* scratch, bspde_cg_report* rep, int32_t* active, cudaStream_t st) {
+  CgState* hs = reinterpret_cast<CgState*>(s->host_state);
+  CUDA_TRY(cudaMemcpyAsync(hs, scratch_state(scratch), sizeof(CgState), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (rep) {
+    rep->iterations = hs->it;
+    rep->status = hs->status;
+    rep->residual = hs->res;
+    rep->residual0 = hs->res0;
+    rep->rhs_norm = hs->rhs_norm;
+    rep->relative_residual = hs->res / hs->scale;
+    rep->last_pAp = hs->pAp;
+  }
+  if (active) *active = hs->active;
+  return BSPDE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
+  if (!desc || !out) return fail(BSPDE_ERR_ARG, "null argument");
+  const auto& d = *desc;
+  if (d.degree < 1 || d.degree > MAXP || d.param_degree < 1 || d.param_degree > MAXP)
+    return fail(BSPDE_ERR_ARG, "degrees must be in 1..5");
+  if (d.nz < 1 || d.ny < 1 || d.nx < 1 || d.pz < 1 || d.py < 1 || d.px < 1)
+    return fail(BSPDE_ERR_ARG, "empty extents");
+  const int EW = edge_width_of(d.degree);
+  for (int a = 0; a < 3; ++a) {
+    if (d.ew[a] < 0 || d.ew[a] > EW) return fail(BSPDE_ERR_ARG, "edge width out of range");
+    for (int k = 0; k < 2; ++k)
+      if (!d.tables[a][k]) return fail(BSPDE_ERR_ARG, "missing trilinear tables");
+  }
+  if (d.device < 0) return fail(BSPDE_ERR_ARG, "bad device ordinal");
+  CUDA_TRY(cudaSetDevice(d.device));
+  auto* s = new bspde_stencil();
+  s->d = d;
+  s->device = d.device;
+  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, d.device);
+  StencilDev& S = s->S;
+  S.nb = d.degree;
+  S.np = d.param_degree;
+  S.mw = (d.degree + d.param_degree + 1) / 2;
+  S.A = 2 * S.nb + 1;
+  S.B = 2 * S.mw + 1;
+  S.nz = d.nz;
+  S.ny = d.ny;
+  S.nx = d.nx;
+  S.pz = d.pz;
+  S.py = d.py;
+  S.px = d.px;
+  S.ext = d.ext;
+  S.ext_p = d.ext_p;
+  for (int a = 0; a < 3; ++a) {
+    S.ew[a] = d.ew[a];
+    S.s_stiff[a] = d.scale_stiff[a];
+  }
+  S.s_mass = d.scale_mass;
+  S.N = (long long)d.nz * d.ny * d.nx;
+  S.ncls = 2 * EW + 1;
+  const size_t per = (size_t)S.A * S.B;
+  std::vector<double> tab((size_t)3 * 2 * S.ncls * per, 0.0);
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < 2; ++k)
+      for (int c = 0; c < 2 * d.ew[a] + 1; ++c)
+        for (size_t e = 0; e < per; ++e)
+          tab[(((size_t)a * 2 + k) * S.ncls + c) * per + e] = d.tables[a][k][c * per + e];
+  s->tab_bytes = tab.size() * sizeof(double);
+  cudaError_t e1 = cudaMalloc(&s->d_tab, s->tab_bytes);
+  cudaError_t e2 = cudaMallocHost(&s->host_state, sizeof(CgState));
+  cudaError_t e3 = cudaStreamCreateWithFlags(&s->work, cudaStreamNonBlocking);
+  cudaError_t e4 = cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming);
+  cudaError_t e5 = cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
+      e5 != cudaSuccess) {
+    bspde_stencil_destroy(s);
+    return fail(BSPDE_ERR_CUDA, "stencil plan allocation failed");
+  }
+  cudaError_t e6 = cudaMemcpy(s->d_tab, tab.data(), s->tab_bytes, cudaMemcpyHostToDevice);
+  if (e6 != cudaSuccess) {
+    bspde_stencil_destroy(s);
+    return fail(BSPDE_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e6));
+  }
+  S.tab = s->d_tab;
+  *out = s;
+  return BSPDE_OK;
+}
+
+int bspde_stencil_destroy(bspde_stencil* s) {
+  if (!s) return BSPDE_OK;
+  cudaSetDevice(s->device);
+  if (s->d_tab) cudaFree(s->d_tab);
+  if (s->host_state) cudaFreeHost(s->host_state);
+  if (s->work) cudaStreamDestroy(s->work);
+  if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->ev_out) cudaEventDestroy(s->ev_out);
+  delete s;
+  return BSPDE_OK;
+}
+
+int64_t bspde_stencil_entries(const bspde_stencil* s) {
+  if (!s) return -1;
+  return (int64_t)s->S.A * s->S.A * s->S.A * s->S.N;
+}
+
+int64_t bspde_stencil_launch_count(const bspde_stencil* s) { return s ? s->launches : -1; }
+
+int bspde_stencil_assemble(bspde_stencil* s, const double* dfield, const double* mfield,
+                           double* P, void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (!dfield || !mfield || !P) return fail(BSPDE_ERR_ARG, "null argument");
+  const long long total = (long long)s->S.A * s->S.A * s->S.A * s->S.N;
+  const unsigned grid = (unsigned)std::min<long long>((total + ST_NT - 1) / ST_NT, 1 << 20);
+  const size_t smem = s->tab_bytes;
+  if (smem > 48 * 1024)
+    CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(&stencil_assemble_kernel),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  stencil_assemble_kernel<<<grid, ST_NT, smem, (cudaStream_t)stream>>>(s->S, dfield, mfield, P);
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_stencil_apply(bspde_stencil* s, const double* P, const double* c, double* out,
+                        void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (!P || !c || !out) return fail(BSPDE_ERR_ARG, "null argument");
+  stencil_apply_kernel<0><<<st_grid(s, s->S.N), ST_NT, 0, (cudaStream_t)stream>>>(
+      s->S, P, c, out, nullptr, nullptr, nullptr, nullptr, 0);
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_stencil_diagonal(bspde_stencil* s, const double* P, double* out, void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (!P || !out) return fail(BSPDE_ERR_ARG, "null argument");
+  stencil_diag_kernel<<<st_grid(s, s->S.N), ST_NT, 0, (cudaStream_t)stream>>>(s->S, P, out);
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double* x, double* r,
+                      double* p, double* ap, void* scratch, double* history,
+                      const bspde_cg_config* cfg, bspde_cg_report* report, int32_t precond,
+                      void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (!P || !b || !x || !r || !p || !ap || !scratch || !cfg)
+    return fail(BSPDE_ERR_ARG, "null argument");
+  if (!(cfg->tol > 0.0)) return fail(BSPDE_ERR_ARG, "tol must be positive");
+  if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
+  if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
+  cudaStream_t caller = (cudaStream_t)stream, st = s->work;
+  CUDA_TRY(cudaEventRecord(s->ev_in, caller));
+  CUDA_TRY(cudaStreamWaitEvent(st, s->ev_in, 0));
+  // scalar state (same layout and state machine as bspde_cg_setup)
+  CgState* hs = reinterpret_cast<CgState*>(s->host_state);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::memset(hs, 0, sizeof(CgState));
+  hs->tol = cfg->tol;
+  hs->max_iter = cfg->max_iter;
+  hs->record_history = cfg->record_history ? 1 : 0;
+  hs->has_x0 = cfg->has_x0 ? 1 : 0;
+  hs->history = history;
+  hs->scale = 1.0;
+  CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(scratch_counter(scratch), 0, 64, st));
+  const size_t bytes = (size_t)s->S.N * sizeof(double);
+  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
+  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  const unsigned grid = st_grid(s, s->S.N);
+  double* partials = scratch_partials(scratch);
+  unsigned* counter = scratch_counter(scratch);
+  CgState* state = scratch_state(scratch);
+  stencil_apply_kernel<1><<<grid, ST_NT, 0, st>>>(s->S, P, x, r, b, partials, counter, state,
+                                                  precond);
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  int32_t active = 0;
+  int rc = st_read(s, scratch, report, &active, st);
+  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  while (rc == BSPDE_OK && active) {
+    for (int k = 0; k < K; ++k) {
+      stencil_pform_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, r, p, state, precond);
+      stencil_apply_kernel<2><<<grid, ST_NT, 0, st>>>(s->S, P, p, ap, nullptr, partials, counter,
+                                                      state, precond);
+      stencil_update_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, x, r, p, ap, partials, counter,
+                                                    state, precond);
+      s->launches += 3;
+    }
+    CUDA_TRY(cudaGetLastError());
+    rc = st_read(s, scratch, report, &active, st);
+  }
+  cudaEventRecord(s->ev_out, st);
+  cudaStreamWaitEvent(caller, s->ev_out, 0);
+  return rc;
+}
+
+}  // extern "C"

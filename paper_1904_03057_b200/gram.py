@@ -256,6 +256,78 @@ def degenerate_factor(p: int, kind: str) -> GramFactor:
 
 
 # ---------------------------------------------------------------------------
+# trilinear factors for variable coefficients (reference: kernels.py:96-173,
+# assembly.py:83-108)
+
+
+def multi_product_integral(factors, lo=None, hi=None) -> Fraction:
+    """Exact ``int prod_f D^d_f beta^{p_f}(x - s_f) dx`` over ``[lo, hi]``."""
+    pieces = []
+    for deg, shift, deriv in factors:
+        sh = Fraction(shift)
+        pieces.append([(a + sh, b + sh, _pshift(list(c), sh))
+                       for a, b, c in bspline_pieces(deg, deriv)])
+    tot = Fraction(0)
+
+    def rec(k, a, b, poly):
+        nonlocal tot
+        if k == len(pieces):
+            if b > a:
+                tot += _pint(poly, a, b)
+            return
+        for pa, pb, pc in pieces[k]:
+            na, nb = max(a, pa), min(b, pb)
+            if nb > na:
+                rec(k + 1, na, nb, _pmul(poly, pc))
+
+    lo_f = Fraction(lo) if lo is not None else Fraction(-10 ** 9)
+    hi_f = Fraction(hi) if hi is not None else Fraction(10 ** 9)
+    rec(0, lo_f, hi_f, [Fraction(1)])
+    return tot
+
+
+def param_reach(n_b: int, n_p: int) -> int:
+    return (n_b + n_p + 1) // 2
+
+
+@lru_cache(maxsize=None)
+def _trilinear_exact(n_b: int, n_p: int, deriv: int):
+    """Interior table and left edge tables (exact) of
+    ``int D^d beta(x - a) D^d beta(x) beta_np(x - b)`` (a trial, b parameter
+    offsets), edge rows integrated over ``[0, inf)`` at test position i - ext."""
+    mw = param_reach(n_b, n_p)
+    offs_a = range(-n_b, n_b + 1)
+    offs_b = range(-mw, mw + 1)
+    interior = tuple(tuple(multi_product_integral([(n_b, a, deriv), (n_b, 0, deriv), (n_p, b, 0)])
+                           for b in offs_b) for a in offs_a)
+    ext = basis_extension(n_b)
+    edge = []
+    for i in range(edge_width(n_b)):
+        pos = i - ext
+        edge.append(tuple(tuple(multi_product_integral(
+            [(n_b, pos + a, deriv), (n_b, pos, deriv), (n_p, pos + b, 0)], lo=0)
+            for b in offs_b) for a in offs_a))
+    return interior, tuple(edge)
+
+
+def trilinear_tables(n_b: int, n_p: int, deriv: int) -> np.ndarray:
+    """Class tables ``(2ew+1, 2n_b+1, 2mw+1)``: classes 0..ew-1 = first rows,
+    ew = interior, ew+1..2ew = last rows (the mirror image, sign +1 since
+    both factors carry the same derivative)."""
+    _check_degree(n_b)
+    _check_degree(n_p)
+    interior, edge = _trilinear_exact(n_b, n_p, deriv)
+    ew = edge_width(n_b)
+    A, B = 2 * n_b + 1, 2 * param_reach(n_b, n_p) + 1
+    t = np.zeros((2 * ew + 1, A, B))
+    for c in range(ew):
+        t[c] = [[float(v) for v in row] for row in edge[c]]
+        t[2 * ew - c] = t[c][::-1, ::-1]
+    t[ew] = [[float(v) for v in row] for row in interior]
+    return t
+
+
+# ---------------------------------------------------------------------------
 # box-face (Robin / penalty) terms (reference: assembly.py:138-232)
 
 

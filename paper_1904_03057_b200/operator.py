@@ -132,6 +132,10 @@ def make_operator(data, strategy="b200", workers=1, memory_budget=None, device=N
     """Strategy dispatch (cf. operator.py:407-414).  Only ``"b200"`` lives here;
     the reference's host strategies stay in the reference package."""
     if strategy == "b200":
+        from .varcoef import B200StencilOperator, VarSystemData
+
+        if isinstance(data, VarSystemData):
+            return B200StencilOperator(data, workers, device)
         return B200Operator(data, workers, device)
     raise ValidationError(f"unknown strategy {strategy!r} (this package provides 'b200')")
 

@@ -140,8 +140,14 @@ def pcg(operator, rhs, config: SolveConfig = None, x0=None):
     :class:`DivergenceError` when the residual grows a thousandfold.
     """
     from .operator import B200Operator
+    from .varcoef import B200StencilOperator
 
     config = config or SolveConfig()
+    if isinstance(operator, B200StencilOperator):
+        rhs = np.asarray(rhs, dtype=np.float64)
+        if not np.all(np.isfinite(rhs)):
+            raise ValidationError("right-hand side contains non-finite values")
+        return operator.pcg(rhs.reshape(operator.data.cext), config, x0)
     if not isinstance(operator, B200Operator) and not hasattr(operator, "pcg_device"):
         raise ConfigurationError(
             "pcg here runs the B200 device solver; pass an operator from "

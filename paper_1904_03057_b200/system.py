@@ -26,6 +26,7 @@ from .gram import (GramFactor, basis_extension, degenerate_factor, edge_width, f
 
 
 def _constant_value(f, what):
+    """The field's constant value, or None for a variable field."""
     arr = np.asarray(f, dtype=np.float64)
     if arr.size == 0:
         raise ValidationError(f"{what} field is empty")
@@ -33,9 +34,7 @@ def _constant_value(f, what):
         raise ValidationError(f"{what} field contains non-finite values")
     v = float(arr.flat[0])
     if arr.size > 1 and not np.all(arr == v):
-        raise ConfigurationError(
-            f"the b200 strategy realizes constant {what}; variable-coefficient "
-            "operators are a later milestone (DESIGN.md 'next')")
+        return None
     return v
 
 
@@ -162,6 +161,12 @@ def build_system(domain, n_b, n_p, dcoef_ext, mcoef_ext, face_specs=(), dtype=np
         raise ValidationError(f"basis degree {n_b} not in 1..5")
     D = _constant_value(dcoef_ext, "diffusion")
     mu = _constant_value(mcoef_ext, "absorption")
+    if D is None or mu is None:
+        # spline-valued fields: the assembled-stencil operator (varcoef.py)
+        from .varcoef import build_var_system
+
+        return build_var_system(domain, int(n_b), int(n_p), dcoef_ext, mcoef_ext, face_specs,
+                                dtype)
     return _make(domain, int(n_b), int(n_p), D, mu, np.dtype(dtype), face_specs)
 
 

@@ -1,0 +1,241 @@
+"""Variable-coefficient operator on the B200.
+
+For spline-valued diffusion D(x) and absorption mu(x) fields the reference
+operator (``OnTheFlyOperator`` over ``build_system``,
+``/root/reference/pkg/src/bspde/assembly.py:396-472``) is no longer a
+Kronecker product: the stencil of node l is
+
+    P[a, l] = sum_b D[l+b] (vol/hz^2 Tz'Ty Tx + vol/hy^2 Tz Ty' Tx + vol/hx^2 Tz Ty Tx')[a, b]
+            + sum_b mu[l+b] vol (Tz Ty Tx)[a, b]
+
+with per-axis trilinear tables T[a, b] = int D^d beta(x-a) D^d beta(x)
+beta_np(x-b) (``kernels.py:158-173``; positional edge rows
+``assembly.py:83-108``), computed exactly here (:func:`.gram.trilinear_tables`).
+The sm_100a kernels (``csrc/stencil.cuh``) assemble all stencils once into HBM
+and apply them as a streaming gather; Jacobi-PCG reuses the device-side
+scalar state of the constant-coefficient solver.  3-D box domains with
+natural faces; the stencil array costs (2p+1)^3 doubles per DoF (2.7 KB at
+p = 3), so one B200 holds problems up to ~300^3.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConditioningWarning, ConfigurationError, ResourceError, ValidationError
+from .gram import basis_extension, edge_width, min_axis_length, param_reach, trilinear_tables
+
+
+@dataclass
+class VarSystemData:
+    """Variable-coefficient system (cf. the reference SystemData)."""
+
+    domain: object
+    n_b: int
+    n_p: int
+    step: tuple
+    cext: tuple
+    ext: int
+    ext_p: int
+    dtype: np.dtype
+    dfield: np.ndarray  # on the extended parameter grid
+    mfield: np.ndarray
+    tables: tuple  # (value, derivative) trilinear class tables
+    scale_stiff: tuple
+    scale_mass: float
+    faces: tuple = ()
+
+    @property
+    def dim(self):
+        return len(self.cext)
+
+    @property
+    def a_flat_size(self):
+        return (2 * self.n_b + 1) ** self.dim
+
+    def num_unknowns(self):
+        return int(np.prod(self.cext))
+
+    @property
+    def vol(self):
+        return self.scale_mass
+
+
+def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> VarSystemData:
+    grid = domain.grid
+    if grid.dim != 3:
+        raise ConfigurationError("the b200 variable-coefficient operator is 3-D")
+    if face_specs:
+        raise ConfigurationError(
+            "the b200 variable-coefficient operator realizes natural (Neumann) faces")
+    if not 1 <= int(n_p) <= 5:
+        raise ValidationError(f"parameter degree {n_p} not in 1..5")
+    for n in grid.extents:
+        if n - 1 < min_axis_length(n_b):
+            raise ValidationError(f"axis with {n} nodes too short for degree {n_b} edge tables")
+    ext, ext_p = basis_extension(n_b), basis_extension(n_p)
+    pext = tuple(n + 2 * ext_p for n in grid.extents)
+    fields = []
+    for f, what in ((dfield, "diffusion"), (mfield, "absorption")):
+        a = np.asarray(f, dtype=np.float64)
+        if a.ndim == 0:
+            a = np.full(pext, float(a))
+        if a.shape != pext:
+            raise ValidationError(f"{what} field {a.shape} != extended parameter grid {pext}")
+        if not np.all(np.isfinite(a)):
+            raise ValidationError(f"{what} field contains non-finite values")
+        fields.append(np.ascontiguousarray(a))
+    vol = float(np.prod(grid.step))
+    tabs = (trilinear_tables(int(n_b), int(n_p), 0), trilinear_tables(int(n_b), int(n_p), 1))
+    return VarSystemData(
+        domain=domain, n_b=int(n_b), n_p=int(n_p), step=grid.step,
+        cext=tuple(n + 2 * ext for n in grid.extents), ext=ext, ext_p=ext_p,
+        dtype=np.dtype(dtype), dfield=fields[0], mfield=fields[1], tables=tabs,
+        scale_stiff=tuple(vol / h ** 2 for h in grid.step), scale_mass=vol)
+
+
+class B200StencilOperator:
+    """Assembled-stencil operator on one B200 (strategy ``"b200"`` for
+    variable coefficients); same protocol as the reference operators."""
+
+    strategy = "b200"
+
+    def __init__(self, data: VarSystemData, workers=1, device=None):
+        import torch
+
+        from .device import require_cuda
+
+        self.data = data
+        self.workers = int(workers)
+        self.device = require_cuda(device)
+        self.lib = N.load()
+        d = N.StencilDesc()
+        d.device = int(self.device.index)
+        d.degree, d.param_degree = data.n_b, data.n_p
+        d.nz, d.ny, d.nx = data.cext
+        d.pz, d.py, d.px = data.dfield.shape
+        d.ext, d.ext_p = data.ext, data.ext_p
+        self._keep = [np.ascontiguousarray(t, dtype=np.float64) for t in data.tables]
+        for a in range(3):
+            d.ew[a] = edge_width(data.n_b)
+            for k in range(2):
+                d.tables[a][k] = self._keep[k].ctypes.data_as(N._dptr)
+            d.scale_stiff[a] = data.scale_stiff[a]
+        d.scale_mass = data.scale_mass
+        h = C.c_void_p()
+        N.check(self.lib.bspde_stencil_create(C.byref(d), C.byref(h)))
+        self.handle = h
+        n_entries = int(self.lib.bspde_stencil_entries(h))
+        free, _ = torch.cuda.mem_get_info(self.device)
+        if n_entries * 8 > 0.9 * free:
+            raise ResourceError(f"stencil array needs {n_entries * 8 / 1e9:.1f} GB "
+                                f"(free {free / 1e9:.1f} GB)")
+        self.P = torch.empty(n_entries, dtype=torch.float64, device=self.device)
+        df = torch.from_numpy(data.dfield).to(self.device)
+        mf = torch.from_numpy(data.mfield).to(self.device)
+        N.check(self.lib.bspde_stencil_assemble(h, N.ptr(df), N.ptr(mf), N.ptr(self.P),
+                                                N.stream_handle()))
+        self._scratch = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and self.handle.value:
+                self.lib.bspde_stencil_destroy(self.handle)
+                self.handle = C.c_void_p()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+    @property
+    def shape(self):
+        return self.data.cext
+
+    @property
+    def dtype(self):
+        return self.data.dtype
+
+    def launches(self) -> int:
+        return int(self.lib.bspde_stencil_launch_count(self.handle))
+
+    def _dev(self, arr, what):
+        import torch
+
+        a = np.asarray(arr, dtype=np.float64)
+        if a.shape != self.data.cext:
+            raise ValidationError(f"{what} {a.shape} != extended extents {self.data.cext}")
+        if not np.all(np.isfinite(a)):
+            raise ValidationError(f"{what} contains non-finite values")
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def apply_device(self, c, out, stream=None):
+        N.check(self.lib.bspde_stencil_apply(self.handle, N.ptr(self.P), N.ptr(c), N.ptr(out),
+                                             N.stream_handle(stream)))
+        return out
+
+    def apply(self, c, out=None):
+        import torch
+
+        cd = self._dev(c, "input coefficients")
+        od = torch.empty_like(cd)
+        self.apply_device(cd, od)
+        t = od.cpu().numpy().astype(self.data.dtype, copy=False)
+        if out is not None:
+            out[...] = t
+            return out
+        return t
+
+    def jacobi_diagonal(self):
+        import torch
+
+        od = torch.empty(self.data.cext, dtype=torch.float64, device=self.device)
+        N.check(self.lib.bspde_stencil_diagonal(self.handle, N.ptr(self.P), N.ptr(od),
+                                                N.stream_handle()))
+        diag = od.cpu().numpy()
+        bad = diag <= 0
+        if np.any(bad):
+            idx = np.argwhere(bad)[0]
+            warnings.warn(
+                f"non-positive operator diagonal at node {tuple(int(i) for i in idx)}",
+                ConditioningWarning)
+        return diag.astype(self.data.dtype, copy=False)
+
+    def flop_byte_report(self, seconds=0.0):
+        from .operator import OpStats
+
+        n = self.data.num_unknowns()
+        a3 = (2 * self.data.n_b + 1) ** 3
+        return OpStats(flops=int(2 * a3 * n), bytes_read=int(n * 8 * (a3 + 1)),
+                       bytes_written=int(n * 8), seconds=seconds)
+
+    def pcg(self, rhs, config, x0=None):
+        """Jacobi-PCG (reference recurrence) on the device: (x, SolveReport)."""
+        import torch
+
+        from .solver import report_from
+
+        t0 = time.perf_counter()
+        b = self._dev(rhs, "rhs")
+        x = self._dev(x0, "x0") if x0 is not None else torch.zeros_like(b)
+        r, p, ap = torch.empty_like(b), torch.empty_like(b), torch.empty_like(b)
+        if self._scratch is None:
+            n = int(self.lib.bspde_scratch_bytes(None))
+            self._scratch = torch.zeros(n, dtype=torch.uint8, device=self.device)
+        hist = torch.zeros(config.max_iter + 1, dtype=torch.float64, device=self.device)
+        cfg = N.CgConfig(float(config.tol), int(config.max_iter), int(bool(config.record_history)),
+                         int(x0 is not None), int(config.poll_every))
+        rep = N.CgReport()
+        precond = 1 if config.precond == "jacobi" else 0
+        N.check(self.lib.bspde_stencil_pcg(self.handle, N.ptr(self.P), N.ptr(b), N.ptr(x), N.ptr(r),
+                                           N.ptr(p), N.ptr(ap), N.ptr(self._scratch), N.ptr(hist),
+                                           C.byref(cfg), C.byref(rep), precond,
+                                           N.stream_handle()))
+        report = report_from(rep, config, time.perf_counter() - t0, hist)
+        return x.cpu().numpy(), report
+
+
+__all__ = ["VarSystemData", "build_var_system", "B200StencilOperator", "param_reach"]

@@ -18,6 +18,9 @@ Fixtures:
   transform.npz -- direct_transform (mirror / replicate / zero) of random
                   1-D / 2-D / 3-D samples, p=2..5; transform_field and
                   sample_solution on small grids
+  varcoef.npz  -- variable (spline-valued) D and mu fields: OnTheFlyOperator
+                  apply / jacobi_diagonal and a pcg solve (tol 1e-12) for
+                  n_b, n_p in 1..5 on small 3-D boxes
   faces.npz    -- box-face Robin / penalty terms (build_system face_specs):
                   OnTheFlyOperator.apply, jacobi_diagonal and assembled_rhs
                   (volume + face_rhs) for p=1..5 (3-D) and 2-D / 1-D cases
@@ -146,6 +149,49 @@ def face_cases():
     np.savez_compressed(os.path.join(OUT, "faces.npz"), **out)
 
 
+VAR_CASES = [
+    # (tag, extents, step, n_b, n_p)
+    ("v1", (9, 10, 11), (0.5, 1.0, 0.25), 1, 1),
+    ("v2", (9, 10, 11), (0.5, 1.0, 0.25), 2, 2),
+    ("v3", (9, 10, 11), (0.5, 1.0, 0.25), 3, 3),
+    ("v4", (10, 11, 12), (0.5, 1.0, 0.25), 4, 4),
+    ("v5", (10, 11, 12), (0.5, 1.0, 0.25), 5, 5),
+    ("v3p2", (9, 10, 11), (0.5, 1.0, 0.25), 3, 2),
+    ("v2p5", (9, 10, 11), (0.5, 1.0, 0.25), 2, 5),
+]
+
+
+def var_cases():
+    out = {}
+    rng = np.random.default_rng(2468)
+    for tag, ext_, step, nb, npar in VAR_CASES:
+        g = Grid(ext_, step)
+        pext = tuple(n + 2 * basis_extension(npar) for n in g.extents)
+        D = 0.2 + rng.random(pext)          # positive, variable
+        mu = 0.5 + rng.random(pext)
+        data = build_system(BoxDomain(g), nb, npar, D, mu, [])
+        op = make_operator(data, "onthefly")
+        sop = make_operator(data, "sparse")  # same operator (test_operator.py:73-98), faster
+        c = rng.normal(size=data.cext)
+        # smooth exact solution (white-noise rhs trips the 1e3 divergence guard)
+        zz, yy, xx = np.meshgrid(*[np.linspace(0, 1, n) for n in data.cext], indexing="ij")
+        xs = np.sin(2.0 * zz + 0.5) * np.cos(1.5 * yy) * (1.0 + xx ** 2)
+        b = op.apply(xs)
+        t0 = time.time()
+        x, rep = pcg(sop, b, SolveConfig(tol=1e-12, max_iter=5000))
+        for dd in (0, 1):  # the reference's trilinear band of axis 2 (interior + edge rows)
+            band = data.stiff_bands[2][2] if dd else data.mass_bands[2]
+            out[f"{tag}_band{dd}_interior"] = np.asarray(band.interior)
+            out[f"{tag}_band{dd}_edges"] = np.stack([np.asarray(t) for _, t in band.edge_rows])
+            out[f"{tag}_band{dd}_pos"] = np.array([p_ for p_, _ in band.edge_rows])
+        out.update({f"{tag}_D": D, f"{tag}_mu": mu, f"{tag}_c": c, f"{tag}_t": op.apply(c),
+                    f"{tag}_diag": op.jacobi_diagonal(), f"{tag}_b": b, f"{tag}_x": x,
+                    f"{tag}_its": np.array([rep.iterations]),
+                    f"{tag}_meta": np.array([nb, npar] + list(step) + list(ext_), dtype=float)})
+        print(tag, rep.iterations, f"{time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(OUT, "varcoef.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -248,7 +294,8 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "transform", "heat16", "heat64"]
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "heat16",
+                             "heat64"]
     if "gram" in which:
         gram()
     if "apply" in which:
@@ -259,6 +306,8 @@ if __name__ == "__main__":
         face_cases()
     if "transform" in which:
         transform_cases()
+    if "varcoef" in which:
+        var_cases()
     if "heat16" in which:
         heat(16, 10, "heat16.npz")
     if "heat64" in which:

@@ -48,8 +48,12 @@ def test_constant_field_detection():
     assert data.diffusion == 0.5 and data.absorption == 2.0
     f = np.full(shp, 0.5)
     f[3, 3, 3] = 0.6
-    with pytest.raises(ConfigurationError):
-        build_system(dom, 3, 3, f, np.full(shp, 2.0), [])
+    # a variable field selects the assembled-stencil operator (varcoef.py)
+    from paper_1904_03057_b200.varcoef import VarSystemData
+
+    assert isinstance(build_system(dom, 3, 3, f, np.full(shp, 2.0), []), VarSystemData)
+    with pytest.raises(ConfigurationError):  # its faces are natural only
+        build_system(dom, 3, 3, f, np.full(shp, 2.0), [(0, 0, 1.0, None)])
     # box-face terms are realized (tests/test_faces.py)
     assert len(build_system(dom, 3, 3, 1.0, 1.0, [(0, 0, 1.0, None)]).faces) == 1
     with pytest.raises(ValidationError):

@@ -1,0 +1,80 @@
+"""Variable-coefficient operator: host setup (CPU) and GPU parity vs the
+reference (tests/golden/varcoef.npz from make_golden.py: var_cases)."""
+
+import numpy as np
+import pytest
+
+from paper_1904_03057_b200 import BoxDomain, Grid, SolveConfig, build_system, make_operator, pcg
+from paper_1904_03057_b200.errors import ConfigurationError
+from paper_1904_03057_b200.gram import basis_extension, edge_width, trilinear_tables
+from paper_1904_03057_b200.varcoef import VarSystemData
+
+TAGS = ["v1", "v2", "v3", "v4", "v5", "v3p2", "v2p5"]
+CONVERGED = ["v1", "v2", "v3", "v3p2", "v2p5"]  # v4, v5 stop at max_iter in the reference
+
+
+def case(golden, tag):
+    g = golden("varcoef.npz")
+    meta = g[f"{tag}_meta"]
+    nb, npar = int(meta[0]), int(meta[1])
+    step = tuple(float(v) for v in meta[2:5])
+    ext = tuple(int(v) for v in meta[5:8])
+    return g, nb, npar, step, ext
+
+
+def relmax(a, b):
+    return float(np.abs(np.asarray(a) - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_trilinear_tables_vs_reference_bands(golden, tag):
+    g, nb, npar, step, ext = case(golden, tag)
+    ew = edge_width(nb)
+    n = ext[2] + 2 * basis_extension(nb)
+    for d in (0, 1):
+        T = trilinear_tables(nb, npar, d)
+        assert np.abs(T[ew] - g[f"{tag}_band{d}_interior"]).max() < 1e-15
+        for pos, tab in zip(g[f"{tag}_band{d}_pos"], g[f"{tag}_band{d}_edges"]):
+            c = pos if pos < ew else 2 * ew - (n - 1 - pos)
+            assert np.abs(T[c] - tab).max() < 1e-15, (d, pos)
+
+
+def test_variable_fields_build_var_system():
+    dom = BoxDomain(Grid((9, 10, 11), (0.5, 1.0, 0.25)))
+    shp = (11, 12, 13)
+    d = build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0, [])
+    assert isinstance(d, VarSystemData) and d.cext == (11, 12, 13)
+    assert d.mfield.shape == shp and np.all(d.mfield == 1.0)
+    with pytest.raises(ConfigurationError):
+        build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0,
+                     [(0, 0, 1.0, None)])
+    with pytest.raises(ConfigurationError):
+        build_system(BoxDomain(Grid((9, 10), (0.5, 1.0))), 3, 3,
+                     1.0 + np.random.default_rng(0).random((11, 12)), 1.0, [])
+
+
+def _op(golden, tag):
+    g, nb, npar, step, ext = case(golden, tag)
+    data = build_system(BoxDomain(Grid(ext, step)), nb, npar, g[f"{tag}_D"], g[f"{tag}_mu"], [])
+    return g, make_operator(data, "b200")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", TAGS)
+def test_varcoef_apply_and_diagonal_vs_reference(golden, cuda_device, tag):
+    g, op = _op(golden, tag)
+    assert relmax(op.apply(g[f"{tag}_c"]), g[f"{tag}_t"]) < 1e-13
+    assert relmax(op.jacobi_diagonal(), g[f"{tag}_diag"]) < 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", CONVERGED)
+def test_varcoef_pcg_vs_reference(golden, cuda_device, tag):
+    g, op = _op(golden, tag)
+    x, rep = pcg(op, g[f"{tag}_b"], SolveConfig(tol=1e-12, max_iter=5000))
+    ref_its = int(g[f"{tag}_its"][0])
+    assert rep.converged
+    # +-1 at ~100 iterations; these take 84-644: +-max(1, 0.5%)
+    assert abs(rep.iterations - ref_its) <= max(1, round(0.005 * ref_its)), (rep.iterations, ref_its)
+    ref = g[f"{tag}_x"]
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-9
