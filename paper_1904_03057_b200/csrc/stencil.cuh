@@ -102,7 +102,12 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
 //   0 apply:  out = t
 //   1 resid:  out = r = b - t;  sums {<b,b>, <r,D^-1 r>, <r,r>}   (kind 0)
 //   2 cg:     out = Ap;         sums {<p,Ap>}                    (kind 1)
-template <int MODE>
+// Each thread computes XB consecutive x outputs: one c row segment of
+// XB + 2p values serves XB * (2p+1) taps (the gather is load-instruction
+// bound), and the P loads of neighbouring threads stay coalesced.
+constexpr int XB = 4;
+
+template <int MODE, int NB>
 __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S,
                                                               const double* __restrict__ P,
                                                               const double* __restrict__ c,
@@ -113,41 +118,64 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S
   __shared__ double s_red[(ST_NT / 32) * 4];
   __shared__ unsigned s_last;
   if (MODE == 2 && !ld_vol(&st->active)) return;
-  const int A = S.A, hb = S.nb;
-  const int center = (hb * A + hb) * A + hb;
+  constexpr int A = 2 * NB + 1, hb = NB;
+  constexpr int center = (hb * A + hb) * A + hb;
+  const int nxb = (S.nx + XB - 1) / XB;
+  const long long groups = (long long)S.nz * S.ny * nxb;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += (long long)gridDim.x * blockDim.x) {
-    const int lx = (int)(l % S.nx), ly = (int)((l / S.nx) % S.ny), lz = (int)(l / ((long long)S.nx * S.ny));
-    double t = 0.0;
+  for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
+       gi += (long long)gridDim.x * blockDim.x) {
+    const int xb = (int)(gi % nxb);
+    const long long zy = gi / nxb;
+    const int ly = (int)(zy % S.ny), lz = (int)(zy / S.ny);
+    const int lx0 = xb * XB;
+    const long long l0 = (zy * S.nx) + lx0;
+    const int nv = min(XB, S.nx - lx0);
+    double t[XB];
+#pragma unroll
+    for (int v = 0; v < XB; ++v) t[v] = 0.0;
     int a = 0;
     for (int az = -hb; az <= hb; ++az) {
       const int z = lz + az;
       const bool zok = z >= 0 && z < S.nz;
-      for (int ay = -hb; ay <= hb; ++ay) {
+      for (int ay = -hb; ay <= hb; ++ay, a += A) {
         const int y = ly + ay;
-        const bool yok = zok && y >= 0 && y < S.ny;
-        const long long row = ((long long)z * S.ny + y) * S.nx;
-        for (int ax = -hb; ax <= hb; ++ax, ++a) {
-          const int x = lx + ax;
-          if (yok && x >= 0 && x < S.nx) t = fma(P[(long long)a * S.N + l], c[row + x], t);
+        if (!(zok && y >= 0 && y < S.ny)) continue;
+        const double* crow = c + ((long long)z * S.ny + y) * S.nx;
+        double seg[XB + 2 * NB];
+#pragma unroll
+        for (int k = 0; k < XB + 2 * NB; ++k) {
+          const int x = lx0 - hb + k;
+          seg[k] = (x >= 0 && x < S.nx) ? crow[x] : 0.0;
+        }
+#pragma unroll
+        for (int ax = 0; ax < A; ++ax) {
+          const double* pa = P + (long long)(a + ax) * S.N + l0;
+#pragma unroll
+          for (int v = 0; v < XB; ++v)
+            if (v < nv) t[v] = fma(pa[v], seg[v + ax], t[v]);
         }
       }
     }
-    if (MODE == 0) {
-      out[l] = t;
-    } else if (MODE == 1) {
-      const double bb = aux[l];
-      const double r = bb - t;
-      out[l] = r;
-      const double dg = P[(long long)center * S.N + l];
-      const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
-      s0 = fma(bb, bb, s0);
-      s1 = fma(r, __dmul_rn(inv, r), s1);
-      s2 = fma(r, r, s2);
-    } else {
-      out[l] = t;
-      s0 = fma(c[l], t, s0);
+#pragma unroll
+    for (int v = 0; v < XB; ++v) {
+      if (v >= nv) break;
+      const long long l = l0 + v;
+      if (MODE == 0) {
+        out[l] = t[v];
+      } else if (MODE == 1) {
+        const double bb = aux[l];
+        const double r = bb - t[v];
+        out[l] = r;
+        const double dg = P[(long long)center * S.N + l];
+        const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+        s0 = fma(bb, bb, s0);
+        s1 = fma(r, __dmul_rn(inv, r), s1);
+        s2 = fma(r, r, s2);
+      } else {
+        out[l] = t[v];
+        s0 = fma(c[l], t[v], s0);
+      }
     }
   }
   if (MODE == 1) {
@@ -238,8 +266,23 @@ int st_check(bspde_stencil* s) {
 }
 
 unsigned st_grid(const bspde_stencil* s, long long n) {
+  // (the apply kernel covers XB outputs per thread; over-provisioned grids
+  // just stride less)
   const long long want = (n + ST_NT - 1) / ST_NT;
   return (unsigned)std::max<long long>(1, std::min<long long>(want, std::min(MAXGRID, s->num_sms * 8)));
+}
+
+template <int MODE>
+void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const double* P,
+              const double* c, double* out, const double* aux, double* partials,
+              unsigned* counter, CgState* state, int precond) {
+  switch (s->S.nb) {
+    case 1: stencil_apply_kernel<MODE, 1><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    case 2: stencil_apply_kernel<MODE, 2><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    case 3: stencil_apply_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    case 4: stencil_apply_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    default: stencil_apply_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+  }
 }
 
 int st_read(bspde_stencil* s, void* scratch, bspde_cg_report* rep, int32_t* active, cudaStream_t st) {
@@ -370,8 +413,8 @@ int bspde_stencil_apply(bspde_stencil* s, const double* P, const double* c, doub
                         void* stream) {
   if (int rc = st_check(s)) return rc;
   if (!P || !c || !out) return fail(BSPDE_ERR_ARG, "null argument");
-  stencil_apply_kernel<0><<<st_grid(s, s->S.N), ST_NT, 0, (cudaStream_t)stream>>>(
-      s->S, P, c, out, nullptr, nullptr, nullptr, nullptr, 0);
+  st_apply<0>(s, st_grid(s, s->S.N / XB + 1), (cudaStream_t)stream, P, c, out, nullptr, nullptr,
+              nullptr, nullptr, 0);
   s->launches++;
   CUDA_TRY(cudaGetLastError());
   return BSPDE_OK;
@@ -418,8 +461,8 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
   double* partials = scratch_partials(scratch);
   unsigned* counter = scratch_counter(scratch);
   CgState* state = scratch_state(scratch);
-  stencil_apply_kernel<1><<<grid, ST_NT, 0, st>>>(s->S, P, x, r, b, partials, counter, state,
-                                                  precond);
+  const unsigned agrid = st_grid(s, s->S.N / XB + 1);
+  st_apply<1>(s, agrid, st, P, x, r, b, partials, counter, state, precond);
   s->launches++;
   CUDA_TRY(cudaGetLastError());
   int32_t active = 0;
@@ -428,8 +471,7 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
   while (rc == BSPDE_OK && active) {
     for (int k = 0; k < K; ++k) {
       stencil_pform_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, r, p, state, precond);
-      stencil_apply_kernel<2><<<grid, ST_NT, 0, st>>>(s->S, P, p, ap, nullptr, partials, counter,
-                                                      state, precond);
+      st_apply<2>(s, agrid, st, P, p, ap, nullptr, partials, counter, state, precond);
       stencil_update_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, x, r, p, ap, partials, counter,
                                                     state, precond);
       s->launches += 3;
