@@ -204,7 +204,8 @@ int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
  *                   + mu[l+b] sm (Tz Ty Tx)[a, b] ]
  * from per-axis trilinear tables (kernels.py:158-173, edge rows
  * assembly.py:83-108), assembled once into HBM and applied as
- * t_l = sum_a P[a, l] c[l + a].  Box domains, natural faces, 3-D.
+ * t_l = sum_a P[a, l] c[l + a].  3-D box domains, optional Robin /
+ * penalty face terms.
  * Fields are dense (z, y, x) arrays (x fastest) on the device. */
 typedef struct bspde_stencil bspde_stencil;
 
@@ -221,6 +222,14 @@ typedef struct {
   const double* tables[3][2];
   double scale_stiff[3]; /* vol / h_a^2 */
   double scale_mass;     /* vol */
+  /* box-face Robin / penalty terms (make_face_term, assembly.py:201-232):
+   * P += weight * (v v^T)_axis (x) (h M)_other axes */
+  int32_t nfaces;        /* 0..6 */
+  int32_t face_axis[6], face_side[6];
+  double face_weight[6];
+  const double* face_values;  /* host, ew values of the low face (high face mirrored) */
+  const double* mass_gram;    /* host, unit mass Gram class table (2ew+1) x (2n_b+1) */
+  double step[3];
 } bspde_stencil_desc;
 
 int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** plan);

@@ -68,6 +68,13 @@ class StencilDesc(C.Structure):
         ("tables", (_dptr * 2) * 3),
         ("scale_stiff", C.c_double * 3),
         ("scale_mass", C.c_double),
+        ("nfaces", C.c_int32),
+        ("face_axis", C.c_int32 * 6),
+        ("face_side", C.c_int32 * 6),
+        ("face_weight", C.c_double * 6),
+        ("face_values", _dptr),
+        ("mass_gram", _dptr),
+        ("step", C.c_double * 3),
     ]
 
 

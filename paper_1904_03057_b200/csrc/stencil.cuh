@@ -33,7 +33,21 @@ struct StencilDev {
   double s_stiff[3], s_mass;
   const double* tab;        // [axis][d][class][A][B] (class stride 2*EWMAX+1)
   int ncls;                 // class stride
+  // box faces: P += w (v v^T)_axis (x) (h M)_others
+  int nfaces;
+  int face_axis[6], face_side[6];
+  double face_weight[6];
+  double fv[MAXP + 1];          // low-face values (ew entries)
+  double gram[11 * 11];         // unit mass Gram class table (2ew+1) x (2nb+1)
+  double step[3];
 };
+
+__device__ __forceinline__ double st_face_value(const StencilDev& S, int i, int n, int side) {
+  const int ew = (S.ncls - 1) / 2;  // == edge_width(n_b) for face tables
+  if (side == 0) return i >= 0 && i < ew ? S.fv[i] : 0.0;
+  const int m = n - 1 - i;
+  return m >= 0 && m < ew ? S.fv[m] : 0.0;
+}
 
 __device__ __forceinline__ int st_cls(int i, int n, int ew) {
   return i < ew ? i : (i >= n - ew ? 2 * ew - (n - 1 - i) : ew);
@@ -93,6 +107,22 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
           acc = fma(dv, kd, fma(mv, m_zy * tx0[bx], acc));
         }
       }
+    }
+    for (int f = 0; f < S.nfaces; ++f) {
+      double prod = S.face_weight[f];
+      const int li[3] = {lz, ly, lx}, ai[3] = {az - S.nb, ay - S.nb, ax - S.nb};
+      const int ni[3] = {S.nz, S.ny, S.nx}, ci[3] = {cz, cy, cx};
+#pragma unroll
+      for (int ax3 = 0; ax3 < 3; ++ax3) {
+        if (ax3 == S.face_axis[f]) {
+          prod *= st_face_value(S, li[ax3], ni[ax3], S.face_side[f]) *
+                  st_face_value(S, li[ax3] + ai[ax3], ni[ax3], S.face_side[f]);
+        } else {
+          const int j = li[ax3] + ai[ax3];
+          prod *= (j >= 0 && j < ni[ax3]) ? S.step[ax3] * S.gram[ci[ax3] * S.A + ai[ax3] + S.nb] : 0.0;
+        }
+      }
+      acc += prod;
     }
     P[(long long)a * S.N + l] = acc;
   }
@@ -346,6 +376,32 @@ int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
   S.s_mass = d.scale_mass;
   S.N = (long long)d.nz * d.ny * d.nx;
   S.ncls = 2 * EW + 1;
+  if (d.nfaces < 0 || d.nfaces > 6) {
+    delete s;
+    return fail(BSPDE_ERR_ARG, "nfaces must be 0..6");
+  }
+  S.nfaces = d.nfaces;
+  for (int f = 0; f < 6; ++f) {
+    S.face_axis[f] = f < d.nfaces ? d.face_axis[f] : 0;
+    S.face_side[f] = f < d.nfaces ? d.face_side[f] : 0;
+    S.face_weight[f] = f < d.nfaces ? d.face_weight[f] : 0.0;
+    if (f < d.nfaces && (S.face_axis[f] < 0 || S.face_axis[f] > 2 || S.face_side[f] < 0 ||
+                         S.face_side[f] > 1)) {
+      delete s;
+      return fail(BSPDE_ERR_ARG, "bad face axis / side");
+    }
+  }
+  for (int k = 0; k < MAXP + 1; ++k) S.fv[k] = 0.0;
+  for (int k = 0; k < 121; ++k) S.gram[k] = 0.0;
+  if (d.nfaces > 0) {
+    if (!d.face_values || !d.mass_gram) {
+      delete s;
+      return fail(BSPDE_ERR_ARG, "face terms need face_values and mass_gram");
+    }
+    for (int k = 0; k < EW; ++k) S.fv[k] = d.face_values[k];
+    for (int k = 0; k < (2 * EW + 1) * S.A; ++k) S.gram[k] = d.mass_gram[k];
+  }
+  for (int a = 0; a < 3; ++a) S.step[a] = d.step[a];
   const size_t per = (size_t)S.A * S.B;
   std::vector<double> tab((size_t)3 * 2 * S.ncls * per, 0.0);
   for (int a = 0; a < 3; ++a)

@@ -149,6 +149,16 @@ def assembled_rhs(data: SystemData, n_s, qcoef_ext, workers=1, device=None):
     """
     if int(n_s) != int(data.n_b):
         raise ConfigurationError("the b200 RHS realizes n_s == n_b (source degree = basis degree)")
+    from .varcoef import VarSystemData
+
+    if isinstance(data, VarSystemData):
+        # the source term does not involve D or mu: the box mass operator
+        from .system import mass_system
+
+        t = assembled_rhs(mass_system(data.domain.grid, data.n_b), n_s, qcoef_ext, workers, device)
+        if any(ft.rhs_weight != 0.0 for ft in data.faces):
+            t = t + data.face_rhs()
+        return t.astype(data.dtype, copy=False)
     q = check_host_field(qcoef_ext, data.cext, "source coefficients")
     op = B200Operator(data, workers, device)
     cb, ob = op._io_buffers()

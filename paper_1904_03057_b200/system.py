@@ -91,25 +91,7 @@ class SystemData:
         return tuple(f.ew for f in self.mass)
 
     def face_rhs(self) -> np.ndarray:
-        """Penalty right-hand-side surface additions (reference ``face_rhs``,
-        assembly.py:488-501): a rank-1 tensor per face with a value."""
-        grid = self.domain.grid
-        out = np.zeros(self.cext)
-        for ft in self.faces:
-            if ft.rhs_weight == 0.0:
-                continue
-            vecs = []
-            for ax in range(self.dim):
-                n = grid.extents[ax]
-                if ax == ft.axis:
-                    vecs.append(face_vector(self.n_b, n, ft.side))
-                else:
-                    vecs.append(surface_single_vector(self.n_b, n) * grid.step[ax])
-            t = vecs[0]
-            for v in vecs[1:]:
-                t = np.multiply.outer(t, v)
-            out += ft.rhs_weight * t
-        return out
+        return face_rhs(self)
 
     # -- Jacobi diagonal by class (operator.py:190-209 for constant fields) --
     def diag_table(self) -> np.ndarray:
@@ -139,6 +121,28 @@ class SystemData:
         cz, cy, cx = (self.class_index(a) for a in range(3))
         full = table[np.ix_(cz, cy, cx)]
         return full.reshape(self.cext)
+
+
+def face_rhs(data) -> np.ndarray:
+    """Penalty right-hand-side surface additions (reference ``face_rhs``,
+    assembly.py:488-501): a rank-1 tensor per face with a value."""
+    grid = data.domain.grid
+    out = np.zeros(data.cext)
+    for ft in data.faces:
+        if ft.rhs_weight == 0.0:
+            continue
+        vecs = []
+        for ax in range(grid.dim):
+            n = grid.extents[ax]
+            if ax == ft.axis:
+                vecs.append(face_vector(data.n_b, n, ft.side))
+            else:
+                vecs.append(surface_single_vector(data.n_b, n) * grid.step[ax])
+        t = vecs[0]
+        for v in vecs[1:]:
+            t = np.multiply.outer(t, v)
+        out += ft.rhs_weight * t
+    return out
 
 
 def _as3(seq, pad):

@@ -29,7 +29,8 @@ import numpy as np
 
 from . import _native as N
 from .errors import ConditioningWarning, ConfigurationError, ResourceError, ValidationError
-from .gram import basis_extension, edge_width, min_axis_length, param_reach, trilinear_tables
+from .gram import (basis_extension, edge_width, face_values, gram_factor, min_axis_length,
+                   param_reach, trilinear_tables)
 
 
 @dataclass
@@ -51,6 +52,11 @@ class VarSystemData:
     scale_mass: float
     faces: tuple = ()
 
+    def face_rhs(self) -> np.ndarray:
+        from .system import face_rhs
+
+        return face_rhs(self)
+
     @property
     def dim(self):
         return len(self.cext)
@@ -71,9 +77,9 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
     grid = domain.grid
     if grid.dim != 3:
         raise ConfigurationError("the b200 variable-coefficient operator is 3-D")
-    if face_specs:
-        raise ConfigurationError(
-            "the b200 variable-coefficient operator realizes natural (Neumann) faces")
+    from .system import _face_terms
+
+    faces = tuple(_face_terms(face_specs, grid.dim))
     if not 1 <= int(n_p) <= 5:
         raise ValidationError(f"parameter degree {n_p} not in 1..5")
     for n in grid.extents:
@@ -97,7 +103,7 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
         domain=domain, n_b=int(n_b), n_p=int(n_p), step=grid.step,
         cext=tuple(n + 2 * ext for n in grid.extents), ext=ext, ext_p=ext_p,
         dtype=np.dtype(dtype), dfield=fields[0], mfield=fields[1], tables=tabs,
-        scale_stiff=tuple(vol / h ** 2 for h in grid.step), scale_mass=vol)
+        scale_stiff=tuple(vol / h ** 2 for h in grid.step), scale_mass=vol, faces=faces)
 
 
 class B200StencilOperator:
@@ -128,6 +134,18 @@ class B200StencilOperator:
                 d.tables[a][k] = self._keep[k].ctypes.data_as(N._dptr)
             d.scale_stiff[a] = data.scale_stiff[a]
         d.scale_mass = data.scale_mass
+        d.nfaces = len(data.faces)
+        for f, ft in enumerate(data.faces):
+            d.face_axis[f], d.face_side[f], d.face_weight[f] = ft.axis, ft.side, ft.weight
+        if data.faces:
+            fv = np.array([float(v) for v in face_values(data.n_b)])
+            gram = np.ascontiguousarray(gram_factor(data.n_b, data.domain.grid.extents[0],
+                                                    "mass").table)
+            self._keep += [fv, gram]
+            d.face_values = fv.ctypes.data_as(N._dptr)
+            d.mass_gram = gram.ctypes.data_as(N._dptr)
+        for a in range(3):
+            d.step[a] = data.step[a]
         h = C.c_void_p()
         N.check(self.lib.bspde_stencil_create(C.byref(d), C.byref(h)))
         self.handle = h

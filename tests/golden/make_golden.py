@@ -158,7 +158,10 @@ VAR_CASES = [
     ("v5", (10, 11, 12), (0.5, 1.0, 0.25), 5, 5),
     ("v3p2", (9, 10, 11), (0.5, 1.0, 0.25), 3, 2),
     ("v2p5", (9, 10, 11), (0.5, 1.0, 0.25), 2, 5),
+    ("v3f", (9, 10, 11), (0.5, 1.0, 0.25), 3, 3),   # + Robin / penalty faces
+    ("v2f", (9, 10, 11), (0.5, 1.0, 0.25), 2, 3),
 ]
+VAR_FACES = [(0, 0, 0.7, None), (1, 1, 20.0, 1.5), (2, 0, 5.0, -0.5), (2, 1, 0.3, None)]
 
 
 def var_cases():
@@ -169,7 +172,12 @@ def var_cases():
         pext = tuple(n + 2 * basis_extension(npar) for n in g.extents)
         D = 0.2 + rng.random(pext)          # positive, variable
         mu = 0.5 + rng.random(pext)
-        data = build_system(BoxDomain(g), nb, npar, D, mu, [])
+        specs = VAR_FACES if tag.endswith("f") else []
+        data = build_system(BoxDomain(g), nb, npar, D, mu, specs)
+        if specs:
+            out[f"{tag}_faces"] = np.array([[a, s, w, np.nan if v is None else v]
+                                            for a, s, w, v in specs], dtype=float)
+            out[f"{tag}_facerhs"] = assembled_rhs(data, nb, np.zeros(data.cext))
         op = make_operator(data, "onthefly")
         sop = make_operator(data, "sparse")  # same operator (test_operator.py:73-98), faster
         c = rng.normal(size=data.cext)

@@ -52,8 +52,7 @@ def test_constant_field_detection():
     from paper_1904_03057_b200.varcoef import VarSystemData
 
     assert isinstance(build_system(dom, 3, 3, f, np.full(shp, 2.0), []), VarSystemData)
-    with pytest.raises(ConfigurationError):  # its faces are natural only
-        build_system(dom, 3, 3, f, np.full(shp, 2.0), [(0, 0, 1.0, None)])
+    assert len(build_system(dom, 3, 3, f, np.full(shp, 2.0), [(0, 0, 1.0, None)]).faces) == 1
     # box-face terms are realized (tests/test_faces.py)
     assert len(build_system(dom, 3, 3, 1.0, 1.0, [(0, 0, 1.0, None)]).faces) == 1
     with pytest.raises(ValidationError):

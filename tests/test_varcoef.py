@@ -9,8 +9,9 @@ from paper_1904_03057_b200.errors import ConfigurationError
 from paper_1904_03057_b200.gram import basis_extension, edge_width, trilinear_tables
 from paper_1904_03057_b200.varcoef import VarSystemData
 
-TAGS = ["v1", "v2", "v3", "v4", "v5", "v3p2", "v2p5"]
-CONVERGED = ["v1", "v2", "v3", "v3p2", "v2p5"]  # v4, v5 stop at max_iter in the reference
+TAGS = ["v1", "v2", "v3", "v4", "v5", "v3p2", "v2p5", "v3f", "v2f"]
+# v4, v5 stop at max_iter in the reference
+CONVERGED = ["v1", "v2", "v3", "v3p2", "v2p5", "v3f", "v2f"]
 
 
 def case(golden, tag):
@@ -45,9 +46,9 @@ def test_variable_fields_build_var_system():
     d = build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0, [])
     assert isinstance(d, VarSystemData) and d.cext == (11, 12, 13)
     assert d.mfield.shape == shp and np.all(d.mfield == 1.0)
-    with pytest.raises(ConfigurationError):
-        build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0,
-                     [(0, 0, 1.0, None)])
+    df = build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0,
+                      [(0, 0, 1.0, 2.0)])
+    assert len(df.faces) == 1 and df.face_rhs().shape == d.cext
     with pytest.raises(ConfigurationError):
         build_system(BoxDomain(Grid((9, 10), (0.5, 1.0))), 3, 3,
                      1.0 + np.random.default_rng(0).random((11, 12)), 1.0, [])
@@ -55,7 +56,9 @@ def test_variable_fields_build_var_system():
 
 def _op(golden, tag):
     g, nb, npar, step, ext = case(golden, tag)
-    data = build_system(BoxDomain(Grid(ext, step)), nb, npar, g[f"{tag}_D"], g[f"{tag}_mu"], [])
+    specs = [(int(a), int(s), float(w), None if np.isnan(v) else float(v))
+             for a, s, w, v in g.get(f"{tag}_faces", np.zeros((0, 4)))]
+    data = build_system(BoxDomain(Grid(ext, step)), nb, npar, g[f"{tag}_D"], g[f"{tag}_mu"], specs)
     return g, make_operator(data, "b200")
 
 
@@ -78,3 +81,13 @@ def test_varcoef_pcg_vs_reference(golden, cuda_device, tag):
     assert abs(rep.iterations - ref_its) <= max(1, round(0.005 * ref_its)), (rep.iterations, ref_its)
     ref = g[f"{tag}_x"]
     assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["v3f", "v2f"])
+def test_varcoef_face_rhs_vs_reference(golden, cuda_device, tag):
+    from paper_1904_03057_b200 import assembled_rhs
+
+    g, op = _op(golden, tag)
+    t = assembled_rhs(op.data, op.data.n_b, np.zeros(op.data.cext))
+    assert relmax(t, g[f"{tag}_facerhs"]) < 1e-13
