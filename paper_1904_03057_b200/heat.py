@@ -31,7 +31,11 @@ from .transform import sample_solution_device, transform_field_device
 
 @dataclass
 class HeatProblem:
-    """Constant-conductivity heat problem on a box.
+    """Heat problem on a box.
+
+    ``conductivity``: a constant, or a field on the extended parameter grid
+    (degree = ``degree``), which selects the
+    assembled-stencil operator.
 
     ``bc``: a condition or ``{face: condition}`` dict (:mod:`.boundary`;
     default: natural Neumann faces everywhere).
@@ -45,7 +49,7 @@ class HeatProblem:
     grid: Grid
     degree: int
     dt: float
-    conductivity: float = 1.0
+    conductivity: object = 1.0
     initial: object = 0.0
     source: object = 0.0
     initial_coeffs: np.ndarray = None
@@ -75,11 +79,26 @@ class HeatSolver:
         self.problem = problem
         self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
         specs = realize_bc(problem.bc, problem.grid) if problem.bc is not None else ()
-        data = heat_system(problem.grid, problem.degree, problem.dt, problem.conductivity,
-                           face_specs=specs)
+        kappa = np.asarray(problem.conductivity, dtype=np.float64)
+        self.sop = None
+        if kappa.ndim > 0 and not np.all(kappa == kappa.flat[0]):
+            # variable conductivity: A = M + dt (K(kappa) + W) as an assembled
+            # stencil; the RHS mass operator keeps the slab layout of the state
+            from .system import build_system, mass_system
+            from .varcoef import B200StencilOperator
+
+            grid, p, dt = problem.grid, int(problem.degree), float(problem.dt)
+            data = build_system(BoxDomain(grid), p, p, dt * kappa, 1.0,
+                                [(a, s, w * dt, v) for a, s, w, v in specs])
+            self.sop = B200StencilOperator(data, device=device)
+            self.op = B200Operator(mass_system(grid, p), device=device)
+        else:
+            data = heat_system(problem.grid, problem.degree, problem.dt,
+                               float(kappa.flat[0]) if kappa.ndim else float(kappa),
+                               face_specs=specs)
+            self.op = B200Operator(data, device=device)
         self.data = data
         self.dt = float(problem.dt)
-        self.op = B200Operator(data, device=device)
         lay = self.op.layout
         dev = self.op.device
         u0 = problem.initial_coeffs
@@ -116,6 +135,7 @@ class HeatSolver:
         """Wrap already-resident fields (bench / multi-step pipelines)."""
         self = cls.__new__(cls)
         self.problem = None
+        self.sop = None
         self.dt = float(dt)
         self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
         self.data = op.data
@@ -134,6 +154,13 @@ class HeatSolver:
 
     def step(self, stream=None) -> SolveReport:
         self.rhs(stream)
+        if self.sop is not None:  # variable conductivity: dense buffers for the stencil solve
+            lay = self.op.layout
+            b, x = lay.owned(self.b).contiguous(), lay.owned(self.u).contiguous()
+            rep = self.sop.pcg_device(b, x, self.config, has_x0=True, stream=stream)
+            lay.owned(self.u).copy_(x)
+            self.reports.append(rep)
+            return rep
         rep = pcg_device(self.op, self.b, self.u, self.config, has_x0=True, stream=stream)
         self.reports.append(rep)
         return rep

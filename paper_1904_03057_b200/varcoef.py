@@ -234,26 +234,33 @@ class B200StencilOperator:
         """Jacobi-PCG (reference recurrence) on the device: (x, SolveReport)."""
         import torch
 
+        b = self._dev(rhs, "rhs")
+        x = self._dev(x0, "x0") if x0 is not None else torch.zeros_like(b)
+        report = self.pcg_device(b, x, config, has_x0=x0 is not None)
+        return x.cpu().numpy(), report
+
+    def pcg_device(self, b, x, config, has_x0=True, stream=None):
+        """Solve on dense device tensors (cext shape); x holds x0 on entry
+        (if ``has_x0``) and the solution on return.  Returns SolveReport."""
+        import torch
+
         from .solver import report_from
 
         t0 = time.perf_counter()
-        b = self._dev(rhs, "rhs")
-        x = self._dev(x0, "x0") if x0 is not None else torch.zeros_like(b)
         r, p, ap = torch.empty_like(b), torch.empty_like(b), torch.empty_like(b)
         if self._scratch is None:
             n = int(self.lib.bspde_scratch_bytes(None))
             self._scratch = torch.zeros(n, dtype=torch.uint8, device=self.device)
         hist = torch.zeros(config.max_iter + 1, dtype=torch.float64, device=self.device)
         cfg = N.CgConfig(float(config.tol), int(config.max_iter), int(bool(config.record_history)),
-                         int(x0 is not None), int(config.poll_every))
+                         int(bool(has_x0)), int(config.poll_every))
         rep = N.CgReport()
         precond = 1 if config.precond == "jacobi" else 0
         N.check(self.lib.bspde_stencil_pcg(self.handle, N.ptr(self.P), N.ptr(b), N.ptr(x), N.ptr(r),
                                            N.ptr(p), N.ptr(ap), N.ptr(self._scratch), N.ptr(hist),
                                            C.byref(cfg), C.byref(rep), precond,
-                                           N.stream_handle()))
-        report = report_from(rep, config, time.perf_counter() - t0, hist)
-        return x.cpu().numpy(), report
+                                           N.stream_handle(stream)))
+        return report_from(rep, config, time.perf_counter() - t0, hist)
 
 
 __all__ = ["VarSystemData", "build_var_system", "B200StencilOperator", "param_reach"]

@@ -197,6 +197,35 @@ def var_cases():
                     f"{tag}_its": np.array([rep.iterations]),
                     f"{tag}_meta": np.array([nb, npar] + list(step) + list(ext_), dtype=float)})
         print(tag, rep.iterations, f"{time.time() - t0:.1f}s", flush=True)
+    # heat stepping with a variable conductivity (SURVEY.md Appendix A
+    # composition with D = dt * kappa(x)), with and without penalty faces
+    for tag, specs in (("heatvar", []), ("heatvarf", [(0, 0, 50.0, 1.0), (2, 1, 0.5, None)])):
+        p, n = 3, 12
+        g = Grid((n,) * 3, (1.0 / (n - 1),) * 3)
+        ext = basis_extension(p)
+        shp = tuple(k + 2 * ext for k in g.extents)
+        dt = 4.0 / (n - 1) ** 2
+        kappa = 0.5 + rng.random(shp)
+        A = make_operator(build_system(BoxDomain(g), p, p, dt * kappa, np.ones(shp),
+                                       [(a_, s_, w * dt, v) for a_, s_, w, v in specs]), "sparse")
+        Md = build_system(BoxDomain(g), p, p, np.zeros(shp), np.ones(shp), [])
+        M = make_operator(Md, "sparse")
+        zz, yy, xx = np.meshgrid(*[np.linspace(0, 1, k) for k in shp], indexing="ij")
+        u0 = np.exp(-10 * ((zz - .5) ** 2 + (yy - .4) ** 2 + (xx - .6) ** 2))
+        q = np.cos(3 * zz) * np.sin(2 * yy + xx)
+        F = assembled_rhs(Md, p, q)
+        G = assembled_rhs(A.data, p, np.zeros(shp)) if specs else 0.0
+        u, its, sols = u0.copy(), [], []
+        for _ in range(2):
+            u, rep = pcg(A, M.apply(u) + dt * F + G, SolveConfig(tol=1e-12, max_iter=5000), x0=u)
+            its.append(rep.iterations)
+            sols.append(u.copy())
+        out.update({f"{tag}_kappa": kappa, f"{tag}_u0": u0, f"{tag}_q": q,
+                    f"{tag}_its": np.array(its), f"{tag}_u": np.stack(sols),
+                    f"{tag}_meta": np.array([p, n, dt]),
+                    f"{tag}_faces": np.array([[a_, s_, w, np.nan if v is None else v]
+                                              for a_, s_, w, v in specs], dtype=float).reshape(-1, 4)})
+        print(tag, its, flush=True)
     np.savez_compressed(os.path.join(OUT, "varcoef.npz"), **out)
 
 
