@@ -641,14 +641,16 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   const double* X1 = sm.X + (f & 1) * 2 * C::XARR;
   const double* X2 = X1 + C::XARR;
   double out[RPT];
+  // ghost planes (outside the global grid) enter the z ring as zeros through
+  // the same FMA path: one writer of acc keeps the ring registers coalesced
+  double wm[RPT], wa[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    wm[i] = 0.0;
+    wa[i] = 0.0;
+  }
   if (in_grid) {
     // ---- y-pass: wm = My u1, wa = My t + cy Ky u1 for rows gy0 .. gy0+3 ----
-    double wm[RPT], wa[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      wm[i] = 0.0;
-      wa[i] = 0.0;
-    }
     const double* x1c = X1 + (rg * RPT) * TX + cxl;
     const double* x2c = X2 + (rg * RPT) * TX + cxl;
     const bool fast_y = INTERIOR || ((gy0 >= ewy) && (gy0 + RPT - 1 < ny - ewy));
@@ -698,9 +700,11 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         }
       }
     }
+  }
+  {
     // ---- z: shift-register scatter (row z' of the symmetric Mz, Kz) ----
-    const int cz = cls_of(zg, prm.nz_glob, ewz);
-    if (cz == ewz && prm.zfast) {
+    const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
+    if (false) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const double a = STIFF ? wa[i] : wm[i];
@@ -738,14 +742,6 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         if (STIFF) v = fma(tzk[S], w2, v);
         acc[S - 1][i] = v;
       }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      out[i] = acc[0][i];
-#pragma unroll
-      for (int k = 0; k < S - 1; ++k) acc[k][i] = acc[k + 1][i];
-      acc[S - 1][i] = 0.0;
     }
   }
 
