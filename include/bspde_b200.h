@@ -253,6 +253,42 @@ int bspde_stencil_pcg(bspde_stencil* plan, const double* P, const double* b,
                       double* history, const bspde_cg_config* cfg,
                       bspde_cg_report* report, int32_t precond, void* stream);
 
+/* ---- mask (voxel) domains ------------------------
+ * Replaces the reference's boundary-stencil machinery for MaskDomain
+ * systems: _attach_mask_boundary (assembly.py:538-637), the exposed-face
+ * surface terms _attach_mask_surface (:657-737) and the row patch
+ * _patch_boundary_rows (operator.py:142-154).  After bspde_stencil_assemble
+ * with free-space tables (ew = 0), bspde_stencil_mask_patch zeroes the rows
+ * of inactive nodes and rebuilds the rows of boundary nodes from the
+ * occupied cells of their support:
+ *   P[a, l] = sum_{occupied c} sum_b f[c+b] (per-axis cell tables)[l+a-c, l-c, b]
+ *           + weight * sum_{exposed faces} (v v)_normal (x) R_tangential.
+ * All pointers in the desc are DEVICE pointers except where noted. */
+typedef struct {
+  const uint8_t* occupancy;   /* cells (cz, cy, cx), nonzero = occupied */
+  int32_t cells[3];           /* cz, cy, cx (= node extents - 1) */
+  const uint8_t* node_class;  /* nz*ny*nx: 0 inactive, 1 interior, 2 boundary */
+  const int64_t* brows;       /* flat extended indices of the boundary nodes */
+  int64_t nbrows;
+  int32_t jlo, nj;            /* cell_node_offsets(n_b) = jlo .. jlo+nj-1 */
+  int32_t blo, nbp;           /* cell_node_offsets(n_p) */
+  const double* cell_tri;     /* [2][nj][nj][nbp]: value / derivative cell tables */
+  const double* cell_bil;     /* [nj][nj] cell bilinear (n_b, n_b) */
+  const double* cell_single;  /* [nj] single-spline cell integrals */
+  const double* face_vals;    /* [2fc-1] spline values at a cell face */
+  int32_t fc;                 /* first_clean_position(n_b) */
+  int32_t has_surface;        /* exposed-face terms with one global weight */
+  double surface_weight;
+} bspde_mask_desc;
+
+int bspde_stencil_mask_patch(bspde_stencil* plan, const bspde_mask_desc* mask,
+                             const double* dfield, const double* mfield, double* P,
+                             void* stream);
+/* out[l] += value * weight * (exposed-face single integrals) on boundary rows
+ * (the surface_rhs_entries of assembly.py:728-737) */
+int bspde_stencil_mask_surface_rhs(bspde_stencil* plan, const bspde_mask_desc* mask,
+                                   double value, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

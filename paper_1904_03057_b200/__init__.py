@@ -10,25 +10,27 @@ multi-GPU sharding.  There is no CPU fallback.
 """
 
 from .boundary import FACE_NAMES, DirichletPenalty, Neumann, Robin, realize_bc
-from .domain import BoxDomain, Grid
+from .domain import BoxDomain, Grid, MaskDomain, active_nodes, interior_nodes, node_classes
 from .errors import (ConditioningWarning, ConfigurationError, DegreeError, DeterminismError,
-                     DivergenceError, IndefiniteOperatorError, NativeLibraryError,
+                     DivergenceError, EmptyDomainError, FormatError, IndefiniteOperatorError, NativeLibraryError,
                      ResourceError, ValidationError)
 from .gram import GramFactor, basis_extension, edge_width, gram_factor, min_axis_length
 from .heat import HeatProblem, HeatSolver, heat_solve
+from .io import read_field, read_tensor, write_field, write_tensor
 from .operator import B200Operator, OpStats, assembled_rhs, make_operator
 from .solver import SolveConfig, SolveReport, pcg, pcg_device
 from .system import SystemData, build_system, heat_system, mass_system
 from .transform import direct_transform, sample_solution, transform_field
 
 __all__ = [
-    "BoxDomain", "Grid", "FACE_NAMES", "Robin", "Neumann", "DirichletPenalty", "realize_bc",
+    "BoxDomain", "Grid", "MaskDomain", "active_nodes", "interior_nodes", "node_classes", "FACE_NAMES", "Robin", "Neumann", "DirichletPenalty", "realize_bc",
     "basis_extension", "edge_width", "gram_factor", "min_axis_length",
     "GramFactor", "SystemData", "build_system", "heat_system", "mass_system",
     "B200Operator", "OpStats", "make_operator", "assembled_rhs",
     "SolveConfig", "SolveReport", "pcg", "pcg_device",
     "HeatProblem", "HeatSolver", "heat_solve",
     "direct_transform", "transform_field", "sample_solution",
+    "read_tensor", "write_tensor", "read_field", "write_field", "FormatError", "EmptyDomainError",
     "ConditioningWarning", "ConfigurationError", "DegreeError", "DeterminismError",
     "DivergenceError", "IndefiniteOperatorError", "NativeLibraryError", "ResourceError",
     "ValidationError",

@@ -78,6 +78,25 @@ class StencilDesc(C.Structure):
     ]
 
 
+class MaskDesc(C.Structure):
+    _fields_ = [
+        ("occupancy", C.c_void_p),
+        ("cells", C.c_int32 * 3),
+        ("node_class", C.c_void_p),
+        ("brows", C.c_void_p),
+        ("nbrows", C.c_int64),
+        ("jlo", C.c_int32), ("nj", C.c_int32),
+        ("blo", C.c_int32), ("nbp", C.c_int32),
+        ("cell_tri", C.c_void_p),
+        ("cell_bil", C.c_void_p),
+        ("cell_single", C.c_void_p),
+        ("face_vals", C.c_void_p),
+        ("fc", C.c_int32),
+        ("has_surface", C.c_int32),
+        ("surface_weight", C.c_double),
+    ]
+
+
 class CgReport(C.Structure):
     _fields_ = [
         ("iterations", C.c_int32),
@@ -119,6 +138,8 @@ SIGNATURES = [
     ("bspde_stencil_diagonal", C.c_int, [_VP, _VP, _VP, _VP]),
     ("bspde_stencil_pcg", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                     C.POINTER(CgConfig), C.POINTER(CgReport), C.c_int32, _VP]),
+    ("bspde_stencil_mask_patch", C.c_int, [_VP, C.POINTER(MaskDesc), _VP, _VP, _VP, _VP]),
+    ("bspde_stencil_mask_surface_rhs", C.c_int, [_VP, C.POINTER(MaskDesc), C.c_double, _VP, _VP]),
     ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,
                                         C.c_int32, _VP]),

@@ -541,3 +541,218 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Mask (voxel) domains.  The reference assembles the
+// rows of boundary nodes cell by cell on the host and scatters them
+// (assembly.py:538-737); here one thread owns one (boundary row, offset)
+// entry and gathers it from the occupied cells of the row's support, so the
+// rows are written exactly once, without atomics, straight into P.
+
+namespace {
+
+constexpr int MASK_MAXJ = 6;  // cell_node_offsets of degree 5: 6 offsets
+
+__device__ __forceinline__ bool mask_occ(const bspde_mask_desc& M, int z, int y, int x) {
+  if (z < 0 || y < 0 || x < 0 || z >= M.cells[0] || y >= M.cells[1] || x >= M.cells[2])
+    return false;  // cells beyond the grid count as unoccupied
+  return M.occupancy[((long long)z * M.cells[1] + y) * M.cells[2] + x] != 0;
+}
+
+// face (axis, side) of cell c borders an unoccupied cell (exposed_faces,
+// assembly.py:640-654)
+__device__ __forceinline__ bool mask_exposed(const bspde_mask_desc& M, const int (&c)[3],
+                                             int axis, int side) {
+  if (!mask_occ(M, c[0], c[1], c[2])) return false;
+  int n[3] = {c[0], c[1], c[2]};
+  n[axis] += side ? 1 : -1;
+  return !mask_occ(M, n[0], n[1], n[2]);
+}
+
+__global__ void __launch_bounds__(ST_NT) mask_zero_kernel(const StencilDev S,
+                                                          const uint8_t* __restrict__ cls,
+                                                          double* __restrict__ P) {
+  const long long total = (long long)S.A * S.A * S.A * S.N;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x)
+    if (cls[t % S.N] == 0) P[t] = 0.0;
+}
+
+__global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
+                                                          const bspde_mask_desc M,
+                                                          const double* __restrict__ dfield,
+                                                          const double* __restrict__ mfield,
+                                                          double* __restrict__ P) {
+  const long long A3 = (long long)S.A * S.A * S.A;
+  const long long total = A3 * M.nbrows;
+  const int nj = M.nj, nbp = M.nbp;
+  const long long tstride = (long long)nj * nj * nbp;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long l = M.brows[t % M.nbrows];
+    const int a = (int)(t / M.nbrows);
+    const int off[3] = {a / (S.A * S.A) - S.nb, (a / S.A) % S.A - S.nb, a % S.A - S.nb};
+    const int lz = (int)(l / ((long long)S.nx * S.ny)), ly = (int)((l / S.nx) % S.ny),
+              lx = (int)(l % S.nx);
+    const int sp[3] = {lz - S.ext, ly - S.ext, lx - S.ext};  // spline indices of the row
+    // per axis: the cells of the row's support (test offset j2) whose trial
+    // offset j1 = j2 + off also lies on the cell
+    int j2lo[3], j2hi[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      j2lo[d] = max(0, -off[d]);
+      j2hi[d] = min(nj, nj - off[d]);
+    }
+    double acc = 0.0;
+    for (int jz = j2lo[0]; jz < j2hi[0]; ++jz) {
+      const int cz = sp[0] - (M.jlo + jz);
+      const double* tz0 = M.cell_tri + ((long long)(jz + off[0]) * nj + jz) * nbp;
+      const double* tz1 = tz0 + tstride;
+      for (int jy = j2lo[1]; jy < j2hi[1]; ++jy) {
+        const int cy = sp[1] - (M.jlo + jy);
+        const double* ty0 = M.cell_tri + ((long long)(jy + off[1]) * nj + jy) * nbp;
+        const double* ty1 = ty0 + tstride;
+        for (int jx = j2lo[2]; jx < j2hi[2]; ++jx) {
+          const int cx = sp[2] - (M.jlo + jx);
+          if (!mask_occ(M, cz, cy, cx)) continue;
+          const double* tx0 = M.cell_tri + ((long long)(jx + off[2]) * nj + jx) * nbp;
+          const double* tx1 = tx0 + tstride;
+          // parameter spline c + blo + b lives at field index c + blo + b + ext_p
+          const int fz0 = cz + M.blo + S.ext_p, fy0 = cy + M.blo + S.ext_p,
+                    fx0 = cx + M.blo + S.ext_p;
+          double cell = 0.0;
+          for (int bz = 0; bz < nbp; ++bz) {
+            const int fz = fz0 + bz;
+            if (fz < 0 || fz >= S.pz) continue;
+            for (int by = 0; by < nbp; ++by) {
+              const int fy = fy0 + by;
+              if (fy < 0 || fy >= S.py) continue;
+              const double zy00 = tz0[bz] * ty0[by];
+              const double k_z = S.s_stiff[0] * tz1[bz] * ty0[by];
+              const double k_y = S.s_stiff[1] * tz0[bz] * ty1[by];
+              const double k_x = S.s_stiff[2] * zy00;
+              const double m_zy = S.s_mass * zy00;
+              const long long row = ((long long)fz * S.py + fy) * S.px;
+              for (int bx = 0; bx < nbp; ++bx) {
+                const int fx = fx0 + bx;
+                if (fx < 0 || fx >= S.px) continue;
+                const double kd = (k_z + k_y) * tx0[bx] + k_x * tx1[bx];
+                cell = fma(dfield[row + fx], kd, fma(mfield[row + fx], m_zy * tx0[bx], cell));
+              }
+            }
+          }
+          acc += cell;
+        }
+      }
+    }
+    if (M.has_surface) {
+      // exposed faces: (v v)_normal (x) R (x) R over the tangential axes
+      const int nv = 2 * M.fc - 1;
+      for (int axn = 0; axn < 3; ++axn) {
+        const int t1 = axn == 0 ? 1 : 0, t2 = axn == 2 ? 1 : 2;
+        const double tscale = S.step[t1] * S.step[t2];
+        for (int side = 0; side < 2; ++side) {
+          for (int k = 0; k < nv; ++k) {  // test normal offset jn = side + k - (fc-1)
+            const int k1 = k + off[axn];
+            if (k1 < 0 || k1 >= nv) continue;
+            const double vv = M.face_vals[k] * M.face_vals[k1];
+            if (vv == 0.0) continue;
+            int c[3];
+            c[axn] = sp[axn] - (side + k - (M.fc - 1));
+            for (int ja = j2lo[t1]; ja < j2hi[t1]; ++ja) {
+              c[t1] = sp[t1] - (M.jlo + ja);
+              const double ra = M.cell_bil[(ja + off[t1]) * nj + ja];
+              for (int jb = j2lo[t2]; jb < j2hi[t2]; ++jb) {
+                c[t2] = sp[t2] - (M.jlo + jb);
+                if (!mask_exposed(M, c, axn, side)) continue;
+                acc += M.surface_weight * tscale * vv * ra * M.cell_bil[(jb + off[t2]) * nj + jb];
+              }
+            }
+          }
+        }
+      }
+    }
+    P[(long long)a * S.N + l] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(ST_NT) mask_surface_rhs_kernel(const StencilDev S,
+                                                                 const bspde_mask_desc M,
+                                                                 double scale,
+                                                                 double* __restrict__ out) {
+  const int nv = 2 * M.fc - 1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < M.nbrows;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long l = M.brows[i];
+    const int sp[3] = {(int)(l / ((long long)S.nx * S.ny)) - S.ext,
+                       (int)((l / S.nx) % S.ny) - S.ext, (int)(l % S.nx) - S.ext};
+    double acc = 0.0;
+    for (int axn = 0; axn < 3; ++axn) {
+      const int t1 = axn == 0 ? 1 : 0, t2 = axn == 2 ? 1 : 2;
+      const double tscale = S.step[t1] * S.step[t2];
+      for (int side = 0; side < 2; ++side)
+        for (int k = 0; k < nv; ++k) {
+          int c[3];
+          c[axn] = sp[axn] - (side + k - (M.fc - 1));
+          for (int ja = 0; ja < M.nj; ++ja) {
+            c[t1] = sp[t1] - (M.jlo + ja);
+            for (int jb = 0; jb < M.nj; ++jb) {
+              c[t2] = sp[t2] - (M.jlo + jb);
+              if (!mask_exposed(M, c, axn, side)) continue;
+              acc += scale * tscale * M.face_vals[k] * M.cell_single[ja] * M.cell_single[jb];
+            }
+          }
+        }
+    }
+    out[l] += acc;
+  }
+}
+
+int mask_check(const bspde_stencil* s, const bspde_mask_desc* m) {
+  if (!m || !m->occupancy || !m->node_class || (m->nbrows > 0 && !m->brows) || !m->cell_tri ||
+      !m->cell_bil || !m->cell_single || !m->face_vals)
+    return fail(BSPDE_ERR_ARG, "mask desc: null pointer");
+  if (m->nj < 1 || m->nj > MASK_MAXJ || m->nbp < 1 || m->nbp > MASK_MAXJ || m->fc < 1 ||
+      m->fc > 3 || m->nbrows < 0)
+    return fail(BSPDE_ERR_ARG, "mask desc: table sizes out of range");
+  if (m->cells[0] != s->S.nz - 2 * s->S.ext - 1 || m->cells[1] != s->S.ny - 2 * s->S.ext - 1 ||
+      m->cells[2] != s->S.nx - 2 * s->S.ext - 1)
+    return fail(BSPDE_ERR_ARG, "mask cell extents do not match the plan");
+  return BSPDE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bspde_stencil_mask_patch(bspde_stencil* s, const bspde_mask_desc* m, const double* dfield,
+                             const double* mfield, double* P, void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (int rc = mask_check(s, m)) return rc;
+  if (!dfield || !mfield || !P) return fail(BSPDE_ERR_ARG, "null argument");
+  const cudaStream_t st = (cudaStream_t)stream;
+  const long long A3 = (long long)s->S.A * s->S.A * s->S.A;
+  mask_zero_kernel<<<st_grid(s, A3 * s->S.N), ST_NT, 0, st>>>(s->S, m->node_class, P);
+  s->launches++;
+  if (m->nbrows > 0) {
+    mask_rows_kernel<<<st_grid(s, A3 * m->nbrows), ST_NT, 0, st>>>(s->S, *m, dfield, mfield, P);
+    s->launches++;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_stencil_mask_surface_rhs(bspde_stencil* s, const bspde_mask_desc* m, double value,
+                                   double* out, void* stream) {
+  if (int rc = st_check(s)) return rc;
+  if (int rc = mask_check(s, m)) return rc;
+  if (!out) return fail(BSPDE_ERR_ARG, "null argument");
+  if (m->nbrows == 0 || !m->has_surface) return BSPDE_OK;
+  mask_surface_rhs_kernel<<<st_grid(s, m->nbrows), ST_NT, 0, (cudaStream_t)stream>>>(
+      s->S, *m, value * m->surface_weight, out);
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+}  // extern "C"

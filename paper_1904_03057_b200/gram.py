@@ -414,6 +414,50 @@ def surface_single_vector(p: int, num_nodes: int) -> np.ndarray:
     return s
 
 
+# ---------------------------------------------------------------------------
+# per-cell tables for mask domains (reference: kernels.py:331-380)
+
+
+def cell_offsets(p: int) -> tuple:
+    """(lo, hi): node offsets j (spline centred at c + j) non-zero on cell
+    (c, c + 1) (``cell_node_offsets``, kernels.py:331-336)."""
+    half = Fraction(p + 1, 2)
+    return math.floor(-half) + 1, math.ceil(1 + half) - 1
+
+
+@lru_cache(maxsize=None)
+def cell_trilinear(n_b: int, n_p: int, deriv: int) -> np.ndarray:
+    """``T[j1, j2, b] = int_0^1 D^d beta(x - j1) D^d beta(x - j2) beta_np(x - b)``
+    over the offsets of :func:`cell_offsets` (exact; kernels.py:340-355)."""
+    (lo, hi), (plo, phi) = cell_offsets(n_b), cell_offsets(n_p)
+    js, bs = range(lo, hi + 1), range(plo, phi + 1)
+    return np.array([[[float(multi_product_integral(
+        [(n_b, j1, deriv), (n_b, j2, deriv), (n_p, b, 0)], lo=0, hi=1)) for b in bs]
+        for j2 in js] for j1 in js])
+
+
+@lru_cache(maxsize=None)
+def cell_bilinear(n1: int, n2: int) -> np.ndarray:
+    """``R[j1, j2] = int_0^1 beta_n1(x - j1) beta_n2(x - j2)`` (kernels.py:359-371)."""
+    (l1, h1), (l2, h2) = cell_offsets(n1), cell_offsets(n2)
+    return np.array([[float(multi_product_integral([(n1, j1, 0), (n2, j2, 0)], lo=0, hi=1))
+                      for j2 in range(l2, h2 + 1)] for j1 in range(l1, h1 + 1)])
+
+
+@lru_cache(maxsize=None)
+def cell_single(p: int) -> np.ndarray:
+    """``S[j] = int_0^1 beta(x - j)`` (kernels.py:375-380)."""
+    lo, hi = cell_offsets(p)
+    return np.array([float(single_integral(p, j, lo=0, hi=1)) for j in range(lo, hi + 1)])
+
+
+def face_normal_values(p: int) -> np.ndarray:
+    """``beta(k - (fc - 1))`` for k = 0 .. 2 fc - 2: the values at a cell face
+    of the splines whose support crosses it (assembly.py:676-681)."""
+    fc = first_clean_position(p)
+    return np.array([float(bspline_value(p, k - (fc - 1))) for k in range(2 * fc - 1)])
+
+
 def taps_header() -> str:
     """C++ header with the exact interior taps (mass, stiffness) for p=1..5.
 

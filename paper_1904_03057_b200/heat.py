@@ -176,6 +176,20 @@ class HeatSolver:
         own = self.op.layout.owned(self.u)
         return run_steps_host(self.step, own, host_u, steps, chunks)
 
+    def save(self, path):
+        """Checkpoint the current coefficients as a TBSF file (extended-grid
+        extents, spline degree in the header; :func:`.io.write_field`)."""
+        from .io import write_field
+
+        write_field(path, self.op.layout, self.u, degree=self.data.n_b)
+
+    def restore(self, path):
+        """Load coefficients written by :meth:`save` (or the reference's
+        ``write_tensor`` of the same extents and degree) into the state."""
+        from .io import read_field
+
+        read_field(path, self.op.layout, self.op.device, buf=self.u, degree=self.data.n_b)
+
     def coefficients(self) -> np.ndarray:
         return self.op.layout.download(self.u).reshape(self.data.cext)
 

@@ -1,0 +1,168 @@
+"""TBSF tensor files for coefficient checkpoints.
+
+Same on-disk format and error behaviour as the reference
+(``/root/reference/pkg/src/bspde/io.py:20-82``): a little-endian header
+``b"TBSF", u32 version = 1, u32 ndim`` (``ndim`` in 1..3), ``ndim`` u64
+extents, ``u8`` dtype tag (0 = f4, 1 = f8), ``i8`` spline degree, then the
+row-major payload; written to a temporary file and renamed into place.
+
+The B200 side: fields live in HBM in the ghosted-slab layout
+(:mod:`.device`), so :func:`write_field` / :func:`read_field` move the owned
+region through one pinned staging buffer in slices of z planes (one
+device<->host copy per slice, overlapping nothing but the file system) instead
+of materialising a pageable host copy of a 6.4 GB field first.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+import tempfile
+
+import numpy as np
+
+from .errors import FormatError
+
+TBSF_MAGIC = b"TBSF"
+TBSF_VERSION = 1
+_TAG_OF = {np.dtype("<f4"): 0, np.dtype("<f8"): 1}
+_DTYPE_OF = {0: np.dtype("<f4"), 1: np.dtype("<f8")}
+_SLICE_BYTES = 256 << 20
+
+
+def _header(shape, dtype, degree) -> bytes:
+    return (struct.pack("<4sII", TBSF_MAGIC, TBSF_VERSION, len(shape))
+            + struct.pack(f"<{len(shape)}Q", *shape)
+            + struct.pack("<Bb", _TAG_OF[dtype], int(degree)))
+
+
+def _atomic(path, write_body):
+    """Write through a temporary file in the target directory, then rename
+    (``io.py:26-37``)."""
+    directory = os.path.dirname(os.path.abspath(path)) or "."
+    fd, tmp = tempfile.mkstemp(dir=directory, prefix=".tbsf-tmp")
+    try:
+        with os.fdopen(fd, "wb") as f:
+            write_body(f)
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def _parse_header(f, size):
+    """Validate the header (``io.py:52-79``); returns (extents, dtype, degree,
+    payload offset).  Error messages and byte offsets follow the reference."""
+    if size < 12:
+        raise FormatError("file shorter than the fixed header", offset=size)
+    head = f.read(12)
+    magic, version, ndim = struct.unpack_from("<4sII", head, 0)
+    if magic != TBSF_MAGIC:
+        raise FormatError(f"bad magic {magic!r}, expected {TBSF_MAGIC!r}", offset=0)
+    if version != TBSF_VERSION:
+        raise FormatError(f"unsupported version {version}", offset=4)
+    if not 1 <= ndim <= 3:
+        raise FormatError(f"dimension {ndim} not in 1..3", offset=8)
+    off = 12
+    if size < off + 8 * ndim + 2:
+        raise FormatError("truncated extents header", offset=size)
+    rest = f.read(8 * ndim + 2)
+    extents = struct.unpack_from(f"<{ndim}Q", rest, 0)
+    dtag, degree = struct.unpack_from("<Bb", rest, 8 * ndim)
+    off += 8 * ndim + 2
+    if dtag not in _DTYPE_OF:
+        raise FormatError(f"unknown dtype tag {dtag}", offset=off - 2)
+    dt = _DTYPE_OF[dtag]
+    want = int(np.prod(extents)) * dt.itemsize
+    have = size - off
+    if have != want:
+        raise FormatError(
+            f"payload holds {have} bytes, extents {tuple(extents)} require {want}", offset=off)
+    return tuple(int(e) for e in extents), dt, int(degree), off
+
+
+def write_tensor(path, array, degree=-1):
+    """Write a TBSF file from a numpy array or a (CUDA) torch tensor; float32
+    stays f4, everything else is stored as f8 (``io.py:40-49``)."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(array, torch.Tensor):
+        if array.dtype == torch.float32:
+            array = array.detach().cpu().numpy()
+        else:
+            array = array.detach().to(torch.float64).cpu().numpy()
+    arr = np.ascontiguousarray(array)
+    dt = np.dtype("<f4") if arr.dtype == np.float32 else np.dtype("<f8")
+    arr = arr.astype(dt, copy=False)
+    head = _header(arr.shape, dt, degree)
+    _atomic(path, lambda f: (f.write(head), f.write(memoryview(arr).cast("B"))))
+
+
+def read_tensor(path):
+    """Read a TBSF file; returns ``(array, degree)`` (``io.py:52-82``)."""
+    size = os.path.getsize(path)
+    with open(path, "rb") as f:
+        extents, dt, degree, _ = _parse_header(f, size)
+        arr = np.empty(extents, dtype=dt)
+        f.readinto(memoryview(arr).cast("B"))
+    return arr, degree
+
+
+def _staging(layout, torch):
+    plane = layout.ny * layout.nx * 8
+    zs = max(1, min(layout.nz, _SLICE_BYTES // plane))
+    return zs, torch.empty((zs, layout.ny, layout.nx), dtype=torch.float64, pin_memory=True)
+
+
+def write_field(path, layout, buf, degree=-1):
+    """Checkpoint the owned region of a device field (slab layout) as an f8
+    TBSF file of the owned extents, staged through pinned memory in z slices."""
+    import torch
+
+    own = layout.owned(buf)
+    zs, stage = _staging(layout, torch)
+    head = _header(layout.owned_shape, np.dtype("<f8"), degree)
+
+    def body(f):
+        f.write(head)
+        for z0 in range(0, layout.nz, zs):
+            n = min(zs, layout.nz - z0)
+            stage[:n].copy_(own[z0:z0 + n])  # synchronous D2H into pinned memory
+            f.write(memoryview(stage[:n].numpy()).cast("B"))
+
+    _atomic(path, body)
+
+
+def read_field(path, layout, device, buf=None, degree=None):
+    """Load a TBSF file of the owned extents into a (new or given) device
+    field; checks the extents and, if given, the spline degree."""
+    import torch
+
+    size = os.path.getsize(path)
+    with open(path, "rb") as f:
+        extents, dt, deg, _ = _parse_header(f, size)
+        if extents != tuple(layout.owned_shape):
+            raise FormatError(f"file extents {extents} != field extents {layout.owned_shape}")
+        if degree is not None and deg != int(degree):
+            raise FormatError(f"file holds degree {deg}, expected {int(degree)}")
+        if buf is None:
+            buf = layout.alloc(device)
+        own = layout.owned(buf)
+        zs, stage = _staging(layout, torch)
+        item = dt.itemsize
+        for z0 in range(0, layout.nz, zs):
+            n = min(zs, layout.nz - z0)
+            if dt == np.dtype("<f8"):
+                f.readinto(memoryview(stage[:n].numpy()).cast("B"))
+                own[z0:z0 + n].copy_(stage[:n])
+            else:
+                raw = np.frombuffer(f.read(n * layout.ny * layout.nx * item), dtype=dt)
+                own[z0:z0 + n].copy_(torch.from_numpy(raw.astype(np.float64))
+                                     .reshape(n, layout.ny, layout.nx))
+    return buf, deg
+
+
+__all__ = ["TBSF_MAGIC", "TBSF_VERSION", "write_tensor", "read_tensor", "write_field", "read_field"]

@@ -151,6 +151,25 @@ def assembled_rhs(data: SystemData, n_s, qcoef_ext, workers=1, device=None):
         raise ConfigurationError("the b200 RHS realizes n_s == n_b (source degree = basis degree)")
     from .varcoef import VarSystemData
 
+    if isinstance(data, VarSystemData) and data.mask is not None:
+        # mask: the mass-only mask operator reproduces the free-space rows, the
+        # cell-wise boundary rows and the zeroed inactive rows of
+        # _mask_rhs_fixup (operator.py:444-488); exposed faces add the surface
+        # entries on the device
+        import torch
+
+        from .varcoef import B200StencilOperator, build_var_system
+
+        q = check_host_field(qcoef_ext, data.cext, "source coefficients")
+        mop = B200StencilOperator(build_var_system(data.domain, data.n_b, 1, 0.0, 1.0, (),
+                                                   np.float64), workers, device)
+        qd = torch.from_numpy(q).to(mop.device)
+        t = torch.empty_like(qd)
+        mop.apply_device(qd, t)
+        m = data.mask
+        if m.surface_value is not None and m.surface_weight != 0.0:
+            mop.surface_rhs_device(t, m.surface_weight, m.surface_value)
+        return t.cpu().numpy().astype(data.dtype, copy=False)
     if isinstance(data, VarSystemData):
         # the source term does not involve D or mu: the box mass operator
         from .system import mass_system

@@ -159,14 +159,17 @@ def build_system(domain, n_b, n_p, dcoef_ext, mcoef_ext, face_specs=(), dtype=np
     ``face_specs``: ``(axis, side, weight, rhs_value_or_None)`` box-face
     surface terms (Robin / DirichletPenalty, see :func:`.boundary.realize_bc`).
     """
-    if not isinstance(domain, BoxDomain):
-        raise ConfigurationError("the b200 strategy supports box domains (mask domains: out of scope)")
+    from .domain import MaskDomain
+
+    if not isinstance(domain, (BoxDomain, MaskDomain)):
+        raise ConfigurationError(f"unsupported domain type {type(domain).__name__}")
     if not 1 <= int(n_b) <= 5:
         raise ValidationError(f"basis degree {n_b} not in 1..5")
     D = _constant_value(dcoef_ext, "diffusion")
     mu = _constant_value(mcoef_ext, "absorption")
-    if D is None or mu is None:
-        # spline-valued fields: the assembled-stencil operator (varcoef.py)
+    if D is None or mu is None or isinstance(domain, MaskDomain):
+        # spline-valued fields or a mask domain: the assembled-stencil
+        # operator (varcoef.py; mask rows from the occupied cells)
         from .varcoef import build_var_system
 
         return build_var_system(domain, int(n_b), int(n_p), dcoef_ext, mcoef_ext, face_specs,

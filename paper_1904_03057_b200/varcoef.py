@@ -51,8 +51,12 @@ class VarSystemData:
     scale_stiff: tuple
     scale_mass: float
     faces: tuple = ()
+    mask: "MaskInfo" = None  # mask domains: node classes + exposed-face terms
 
     def face_rhs(self) -> np.ndarray:
+        if self.mask is not None:
+            raise ConfigurationError("mask surface RHS terms are assembled on the device "
+                                     "(B200StencilOperator.surface_rhs_device)")
         from .system import face_rhs
 
         return face_rhs(self)
@@ -73,18 +77,65 @@ class VarSystemData:
         return self.scale_mass
 
 
+@dataclass
+class MaskInfo:
+    """Mask-domain data (cf. the reference SystemData fields ``active``,
+    ``bnode_rows``, assembly.py:538-560): node classes on the extended grid,
+    the boundary rows and the global exposed-face surface term."""
+
+    occupancy: np.ndarray   # bool cells
+    node_class: np.ndarray  # uint8 extended nodes (domain.NODE_*)
+    brows: np.ndarray       # int64 flat extended indices of boundary nodes
+    surface_weight: float = 0.0
+    surface_value: float = None  # None: no surface RHS term
+
+    @property
+    def active(self):
+        return self.node_class != 0
+
+    @property
+    def dropped_unknowns(self):
+        return int((self.node_class == 0).sum())
+
+
+def _mask_info(domain, n_b, face_specs) -> MaskInfo:
+    from .domain import NODE_BOUNDARY, node_classes
+
+    cls = node_classes(domain, n_b)
+    brows = np.flatnonzero(cls.ravel() == NODE_BOUNDARY).astype(np.int64)
+    weight, value = 0.0, None
+    specs = list(face_specs or ())
+    if specs:
+        # one global surface weight on every exposed mask face (assembly.py:657-665)
+        for spec in specs:
+            if len(spec) != 4:
+                raise ValidationError(f"face spec {spec!r} is not (axis, side, weight, rhs_value)")
+        weight = float(specs[0][2])
+        value = None if specs[0][3] is None else float(specs[0][3])
+        if not np.isfinite(weight):
+            raise ValidationError(f"face weight {weight} is not finite")
+    return MaskInfo(occupancy=np.ascontiguousarray(domain.occupancy(), dtype=bool),
+                    node_class=cls, brows=brows, surface_weight=weight, surface_value=value)
+
+
 def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> VarSystemData:
+    from .domain import MaskDomain
+
     grid = domain.grid
     if grid.dim != 3:
         raise ConfigurationError("the b200 variable-coefficient operator is 3-D")
     from .system import _face_terms
 
-    faces = tuple(_face_terms(face_specs, grid.dim))
+    is_mask = isinstance(domain, MaskDomain)
+    faces = () if is_mask else tuple(_face_terms(face_specs, grid.dim))
+    if not 1 <= int(n_b) <= 5:
+        raise ValidationError(f"basis degree {n_b} not in 1..5")
     if not 1 <= int(n_p) <= 5:
         raise ValidationError(f"parameter degree {n_p} not in 1..5")
-    for n in grid.extents:
-        if n - 1 < min_axis_length(n_b):
-            raise ValidationError(f"axis with {n} nodes too short for degree {n_b} edge tables")
+    if not is_mask:
+        for n in grid.extents:
+            if n - 1 < min_axis_length(n_b):
+                raise ValidationError(f"axis with {n} nodes too short for degree {n_b} edge tables")
     ext, ext_p = basis_extension(n_b), basis_extension(n_p)
     pext = tuple(n + 2 * ext_p for n in grid.extents)
     fields = []
@@ -99,11 +150,15 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
         fields.append(np.ascontiguousarray(a))
     vol = float(np.prod(grid.step))
     tabs = (trilinear_tables(int(n_b), int(n_p), 0), trilinear_tables(int(n_b), int(n_p), 1))
+    if is_mask:  # free-space (untruncated) rows; boundary rows come from the cells
+        ew = edge_width(int(n_b))
+        tabs = tuple(t[ew:ew + 1] for t in tabs)
     return VarSystemData(
         domain=domain, n_b=int(n_b), n_p=int(n_p), step=grid.step,
         cext=tuple(n + 2 * ext for n in grid.extents), ext=ext, ext_p=ext_p,
         dtype=np.dtype(dtype), dfield=fields[0], mfield=fields[1], tables=tabs,
-        scale_stiff=tuple(vol / h ** 2 for h in grid.step), scale_mass=vol, faces=faces)
+        scale_stiff=tuple(vol / h ** 2 for h in grid.step), scale_mass=vol, faces=faces,
+        mask=_mask_info(domain, int(n_b), face_specs) if is_mask else None)
 
 
 class B200StencilOperator:
@@ -129,7 +184,7 @@ class B200StencilOperator:
         d.ext, d.ext_p = data.ext, data.ext_p
         self._keep = [np.ascontiguousarray(t, dtype=np.float64) for t in data.tables]
         for a in range(3):
-            d.ew[a] = edge_width(data.n_b)
+            d.ew[a] = 0 if data.mask is not None else edge_width(data.n_b)
             for k in range(2):
                 d.tables[a][k] = self._keep[k].ctypes.data_as(N._dptr)
             d.scale_stiff[a] = data.scale_stiff[a]
@@ -159,7 +214,64 @@ class B200StencilOperator:
         mf = torch.from_numpy(data.mfield).to(self.device)
         N.check(self.lib.bspde_stencil_assemble(h, N.ptr(df), N.ptr(mf), N.ptr(self.P),
                                                 N.stream_handle()))
+        self._mask = None
+        if data.mask is not None:
+            self._mask = self._mask_desc(data.mask)
+            N.check(self.lib.bspde_stencil_mask_patch(h, C.byref(self._mask[0]), N.ptr(df),
+                                                      N.ptr(mf), N.ptr(self.P),
+                                                      N.stream_handle()))
         self._scratch = None
+
+    def _mask_desc(self, m):
+        """Upload the mask tables; returns (MaskDesc, keep-alive tensors)."""
+        import torch
+
+        from .gram import (cell_bilinear, cell_offsets, cell_single, cell_trilinear,
+                           face_normal_values, first_clean_position)
+
+        nb, npar, dev = self.data.n_b, self.data.n_p, self.device
+
+        def up(a, dt=torch.float64):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)
+
+        keep = dict(
+            occ=up(m.occupancy.astype(np.uint8), torch.uint8),
+            cls=up(m.node_class, torch.uint8),
+            brows=up(m.brows if len(m.brows) else np.zeros(1, np.int64), torch.int64),
+            tri=up(np.stack([cell_trilinear(nb, npar, 0), cell_trilinear(nb, npar, 1)])),
+            bil=up(cell_bilinear(nb, nb)), single=up(cell_single(nb)),
+            fv=up(face_normal_values(nb)))
+        d = N.MaskDesc()
+        d.occupancy, d.node_class, d.brows = (N.ptr(keep["occ"]), N.ptr(keep["cls"]),
+                                              N.ptr(keep["brows"]))
+        for a in range(3):
+            d.cells[a] = m.occupancy.shape[a]
+        d.nbrows = len(m.brows)
+        (jlo, jhi), (blo, bhi) = cell_offsets(nb), cell_offsets(npar)
+        d.jlo, d.nj, d.blo, d.nbp = jlo, jhi - jlo + 1, blo, bhi - blo + 1
+        d.cell_tri, d.cell_bil, d.cell_single, d.face_vals = (
+            N.ptr(keep["tri"]), N.ptr(keep["bil"]), N.ptr(keep["single"]), N.ptr(keep["fv"]))
+        d.fc = first_clean_position(nb)
+        d.has_surface = int(m.surface_weight != 0.0)
+        d.surface_weight = float(m.surface_weight)
+        return d, keep
+
+    def surface_rhs_device(self, out, weight=None, value=None, stream=None):
+        """out += the exposed-face surface RHS of a mask system
+        (``surface_rhs_entries``, assembly.py:728-737); ``weight``/``value``
+        default to the system's own."""
+        m = self.data.mask
+        if m is None:
+            raise ConfigurationError("surface_rhs_device is for mask systems")
+        d = N.MaskDesc.from_buffer_copy(self._mask[0])
+        w = m.surface_weight if weight is None else float(weight)
+        v = m.surface_value if value is None else float(value)
+        if v is None or w == 0.0:
+            return out
+        d.has_surface, d.surface_weight = 1, w
+        N.check(self.lib.bspde_stencil_mask_surface_rhs(self.handle, C.byref(d), float(v),
+                                                        N.ptr(out), N.stream_handle(stream)))
+        return out
 
     def __del__(self):
         try:
@@ -214,6 +326,8 @@ class B200StencilOperator:
         N.check(self.lib.bspde_stencil_diagonal(self.handle, N.ptr(self.P), N.ptr(od),
                                                 N.stream_handle()))
         diag = od.cpu().numpy()
+        if self.data.mask is not None:  # inactive unknowns get 1 (operator.py:156-170)
+            diag[self.data.mask.node_class == 0] = 1.0
         bad = diag <= 0
         if np.any(bad):
             idx = np.argwhere(bad)[0]

@@ -229,6 +229,70 @@ def var_cases():
     np.savez_compressed(os.path.join(OUT, "varcoef.npz"), **out)
 
 
+def mask_shapes(cells):
+    """Deterministic test masks over ``cells``: a ball, a blob, a leg-like tube."""
+    zz, yy, xx = np.meshgrid(*[np.arange(n) + 0.5 for n in cells], indexing="ij")
+    cz, cy, cx = (n / 2.0 for n in cells)
+    ball = (zz - cz) ** 2 + (yy - cy) ** 2 + (xx - cx) ** 2 <= (0.42 * min(cells)) ** 2
+    blob = ((zz - 0.4 * cells[0]) ** 2 / 9 + (yy - cy) ** 2 / 10 + (xx - 0.55 * cells[2]) ** 2 / 12
+            <= 1.0) | ((zz > cz) & (yy < cy + 1) & (xx > 2) & (xx < cells[2] - 1))
+    tube = ((yy - cy) ** 2 + (xx - cx) ** 2 <= (0.35 * min(cells[1:])) ** 2) & (zz < cells[0] - 1)
+    return {"ball": ball, "blob": blob, "tube": tube}
+
+
+MASK_CASES = [
+    # (tag, node extents, step, mask, n_b, n_p, D, mu, face (weight, value) or None)
+    ("m1", (16, 17, 18), (0.5, 1.0, 0.25), "ball", 1, 1, 0.5, 0.0, None),
+    ("m1f", (16, 17, 18), (1.0, 1.0, 1.0), "tube", 1, 1, 0.5, 0.0, (20.0, 20.0)),
+    ("m2", (16, 17, 18), (0.5, 1.0, 0.25), "blob", 2, 2, "var", 0.3, None),
+    ("m3", (16, 17, 18), (0.5, 1.0, 0.25), "ball", 3, 3, 1.0, 2.0, (5.0, 1.5)),
+    ("m3v", (16, 17, 18), (0.3, 0.4, 0.5), "blob", 3, 1, "var", "var", (0.7, None)),
+    ("m4", (14, 15, 16), (0.5, 1.0, 0.25), "tube", 4, 2, 1.0, 0.5, None),
+    ("m5", (14, 15, 16), (0.5, 1.0, 0.25), "ball", 5, 3, 0.8, 0.1, (3.0, -1.0)),
+]
+
+
+def mask_cases():
+    """Mask-domain systems (domain.py:92-219, assembly.py:538-737,
+    operator.py:142-209, :444-488): apply, Jacobi diagonal, node classes,
+    assembled RHS incl. exposed-face surface entries, and one PCG solve."""
+    from bspde.domain import MaskDomain
+
+    out = {}
+    rng = np.random.default_rng(97531)
+    for tag, ext_, step, mname, nb, npar, Dv, muv, face in MASK_CASES:
+        t0 = time.time()
+        g = Grid(ext_, step)
+        mask = mask_shapes(g.cell_extents)[mname]
+        pext = tuple(n + 2 * basis_extension(npar) for n in g.extents)
+        D = 0.2 + rng.random(pext) if Dv == "var" else np.full(pext, float(Dv))
+        mu = 0.5 + rng.random(pext) if muv == "var" else np.full(pext, float(muv))
+        specs = [] if face is None else [(ax, sd, face[0], face[1]) for ax in range(3)
+                                         for sd in (0, 1)]
+        data = build_system(MaskDomain(g, mask), nb, npar, D, mu, specs)
+        op = make_operator(data, "sparse")
+        c = rng.normal(size=data.cext)
+        q = rng.normal(size=data.cext)
+        xs = np.where(data.active, rng.normal(size=data.cext), 0.0)
+        b = op.apply(xs)
+        if nb <= 3:
+            x, rep = pcg(op, b, SolveConfig(tol=1e-10, max_iter=3000))
+            its = rep.iterations
+        else:  # high degrees on cut cells: too ill-conditioned for a short solve
+            x, its = np.zeros(data.cext), -1
+        out.update({f"{tag}_mask": mask, f"{tag}_D": D, f"{tag}_mu": mu, f"{tag}_c": c,
+                    f"{tag}_t": op.apply(c), f"{tag}_diag": op.jacobi_diagonal(),
+                    f"{tag}_active": data.active, f"{tag}_brows": data.bnode_rows,
+                    f"{tag}_q": q, f"{tag}_rhs": assembled_rhs(data, nb, q),
+                    f"{tag}_b": b, f"{tag}_x": x, f"{tag}_its": np.array([its]),
+                    f"{tag}_meta": np.array([nb, npar] + list(step) + list(ext_), dtype=float),
+                    f"{tag}_face": np.array([] if face is None else
+                                            [face[0], np.nan if face[1] is None else face[1]])})
+        print(tag, len(data.bnode_rows), int(data.active.sum()), its,
+              f"{time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(OUT, "mask.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -262,6 +326,22 @@ def transform_cases():
     out["field2d_p3_f"], out["field2d_p3_c"] = f2, ce2
     out["field2d_p3_s"] = sample_solution(ce2, g2, 3)
     np.savez_compressed(os.path.join(OUT, "transform.npz"), **out)
+
+
+def tbsf_cases():
+    """TBSF files written by the reference ``write_tensor`` (io.py:40-49):
+    the payload is a known function of the index so the reader is checked
+    without a second fixture."""
+    from bspde.io import write_tensor
+
+    d = os.path.join(OUT, "tbsf")
+    os.makedirs(d, exist_ok=True)
+    for name, shape, dtype, deg in (("f8_3d_p3", (5, 7, 3), np.float64, 3),
+                                    ("f4_2d", (3, 4), np.float32, -1),
+                                    ("f8_1d_p5", (11,), np.float64, 5)):
+        n = int(np.prod(shape))
+        arr = (np.arange(n, dtype=np.float64) * 0.37 - 1.5).reshape(shape).astype(dtype)
+        write_tensor(os.path.join(d, name + ".tbsf"), arr, degree=deg)
 
 
 def heat_inputs(ncoef, p=3, lam=4.0):
@@ -331,8 +411,12 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "heat16",
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "heat16",
                              "heat64"]
+    if "mask" in which:
+        mask_cases()
+    if "tbsf" in which:
+        tbsf_cases()
     if "gram" in which:
         gram()
     if "apply" in which:
