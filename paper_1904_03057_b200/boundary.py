@@ -45,21 +45,30 @@ def _face_key(axis, side):
     return FACE_NAMES[2 * axis + side]
 
 
-def realize_bc(spec_or_bc, grid=None):
-    """BC -> ``[(axis, side, weight, rhs_value)]`` for a box.
+def realize_bc(spec_or_bc, grid=None, mask=None):
+    """BC -> ``[(axis, side, weight, rhs_value)]`` (``problem.py:237-300``).
 
     Accepts the reference's ``ProblemSpec``-like object (attributes ``bc`` and
     ``grid``) or a condition / ``{face: condition}`` dict plus ``grid``.
     Same rules as the reference: a dict may use ``"all"`` and must cover every
     face of the box; unknown face names and non-positive gamma / epsilon raise
-    ``ConfigurationError``.
+    ``ConfigurationError``.  Mask domains (``mask=True``, or a spec whose
+    ``domain`` is a :class:`.domain.MaskDomain`) take one global Neumann or
+    DirichletPenalty condition and return at most one spec, whose weight
+    applies to every exposed mask face.
     """
+    from .domain import MaskDomain
+
     if grid is None:
         grid = spec_or_bc.grid
         bc = spec_or_bc.bc
+        if mask is None:
+            mask = isinstance(getattr(spec_or_bc, "domain", None), MaskDomain)
     else:
         bc = spec_or_bc
     d = grid.dim
+    if isinstance(bc, dict) and mask:
+        raise ConfigurationError("mask domains take a single global BC")
     if isinstance(bc, dict):
         per_face = {}
         for key, val in bc.items():
@@ -91,6 +100,12 @@ def realize_bc(spec_or_bc, grid=None):
             return (1.0 / eps, cond.value)
         raise ConfigurationError(
             f"{type(cond).__name__} boundary conditions are not realized by this solver")
+
+    if mask:
+        if isinstance(bc, Robin):
+            raise ConfigurationError("mask domains support Neumann or DirichletPenalty conditions only")
+        w = weight_of(bc)
+        return [] if w is None else [(0, 0, w[0], w[1])]
 
     specs = []
     for ax in range(d):

@@ -31,7 +31,8 @@ from .transform import sample_solution_device, transform_field_device
 
 @dataclass
 class HeatProblem:
-    """Heat problem on a box.
+    """Heat problem on a box, or on a voxel mask (``mask``: bool cells,
+    SURVEY.md §8(f) item 4; one global Neumann / DirichletPenalty ``bc``).
 
     ``conductivity``: a constant, or a field on the extended parameter grid
     (degree = ``degree``), which selects the
@@ -55,6 +56,7 @@ class HeatProblem:
     initial_coeffs: np.ndarray = None
     source_coeffs: np.ndarray = None
     bc: object = None
+    mask: np.ndarray = None
 
     def __post_init__(self):
         if not self.dt > 0:
@@ -78,10 +80,28 @@ class HeatSolver:
     def __init__(self, problem: HeatProblem, config: SolveConfig = None, device=None):
         self.problem = problem
         self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
-        specs = realize_bc(problem.bc, problem.grid) if problem.bc is not None else ()
+        is_mask = problem.mask is not None
+        specs = (realize_bc(problem.bc, problem.grid, mask=is_mask)
+                 if problem.bc is not None else ())
         kappa = np.asarray(problem.conductivity, dtype=np.float64)
-        self.sop = None
-        if kappa.ndim > 0 and not np.all(kappa == kappa.flat[0]):
+        self.sop = self.mop = None
+        if is_mask:
+            # mask: A = M + dt (K(kappa) + W) and the mass M as mask stencils
+            # (boundary rows from the occupied cells, inactive rows zero);
+            # the box mass plan only provides the state layout and transforms
+            from .domain import MaskDomain
+            from .system import build_system, mass_system
+            from .varcoef import B200StencilOperator, build_var_system
+
+            grid, p, dt = problem.grid, int(problem.degree), float(problem.dt)
+            dom = MaskDomain(grid, problem.mask)
+            data = build_system(dom, p, p, dt * kappa if kappa.ndim else dt * float(kappa), 1.0,
+                                [(a, s_, w * dt, v) for a, s_, w, v in specs])
+            self.sop = B200StencilOperator(data, device=device)
+            self.mop = B200StencilOperator(build_var_system(dom, p, 1, 0.0, 1.0, (), np.float64),
+                                           device=device)
+            self.op = B200Operator(mass_system(grid, p), device=device)
+        elif kappa.ndim > 0 and not np.all(kappa == kappa.flat[0]):
             # variable conductivity: A = M + dt (K(kappa) + W) as an assembled
             # stencil; the RHS mass operator keeps the slab layout of the state
             from .system import build_system, mass_system
@@ -112,6 +132,23 @@ class HeatSolver:
                                            and not callable(problem.source)
                                            and float(problem.source) == 0.0)
         self.F = None
+        if is_mask:
+            # dense F = M_mask q + (surface source per unit time)
+            import torch
+
+            self.F = torch.zeros(data.cext, dtype=torch.float64, device=dev)
+            if has_source:
+                if q is None:
+                    qb = transform_field_device(problem.source, problem.grid, problem.degree, lay,
+                                                dev)
+                else:
+                    qb = lay.upload(np.asarray(q).reshape(lay.owned_shape), dev)
+                self.mop.apply_device(lay.owned(qb).contiguous(), self.F)
+                del qb
+            if specs and specs[0][3] is not None:
+                self.mop.surface_rhs_device(self.F, specs[0][2], specs[0][3])
+            self.reports = []
+            return
         if has_source:
             if q is None:
                 qb = transform_field_device(problem.source, problem.grid, problem.degree, lay, dev)
@@ -135,7 +172,7 @@ class HeatSolver:
         """Wrap already-resident fields (bench / multi-step pipelines)."""
         self = cls.__new__(cls)
         self.problem = None
-        self.sop = None
+        self.sop = self.mop = None
         self.dt = float(dt)
         self.config = config or SolveConfig(tol=1e-10, max_iter=5000)
         self.data = op.data
@@ -147,12 +184,25 @@ class HeatSolver:
         return self
 
     def rhs(self, stream=None):
-        """b = M u + dt F (one fused kernel)."""
+        """b = M u + dt F (one fused kernel; mask: dense mask-mass apply + axpy)."""
+        if self.mop is not None:
+            x = self.op.layout.owned(self.u).contiguous()
+            b = self.mop.apply_device(x, torch_empty_like(x), stream=stream)
+            return b.add_(self.F, alpha=self.dt)
         self.op.mass_apply_device(self.u, self.b, self.F,
                                   a=self.dt if self.F is not None else 0.0, stream=stream)
         return self.b
 
     def step(self, stream=None) -> SolveReport:
+        if self.mop is not None:  # mask: b = M_mask u + dt F on dense buffers
+            lay = self.op.layout
+            x = lay.owned(self.u).contiguous()
+            b = self.mop.apply_device(x, torch_empty_like(x), stream=stream)
+            b.add_(self.F, alpha=self.dt)
+            rep = self.sop.pcg_device(b, x, self.config, has_x0=True, stream=stream)
+            lay.owned(self.u).copy_(x)
+            self.reports.append(rep)
+            return rep
         self.rhs(stream)
         if self.sop is not None:  # variable conductivity: dense buffers for the stencil solve
             lay = self.op.layout
@@ -197,6 +247,12 @@ class HeatSolver:
         """The solution at the grid nodes (GPU sample_solution)."""
         grid = self.data.domain.grid
         return sample_solution_device(self.u, grid, self.data.n_b, self.op.layout).cpu().numpy()
+
+
+def torch_empty_like(t):
+    import torch
+
+    return torch.empty_like(t)
 
 
 def run_steps_host(step, dev, host, steps: int, chunks: int = 16, stream=None):

@@ -52,3 +52,20 @@ def heat_c_inputs(ncoef, p=3, lam=4.0):
 
 IC = dict(center=(0.5, 0.4, 0.6), width=40.0, amp=1.0)
 SOURCE = dict(center=(0.3, 0.6, 0.5), width=60.0, amp=10.0)
+
+
+def leg_mask(extents=(60, 60, 240)):
+    """The reference's synthetic leg (``make_leg_mask``, domain.py:275-293):
+    cells of a tube along axis 2 whose centre wanders (sin / cos in the
+    axial coordinate) and whose radius tapers from 0.30 to 0.20 of the
+    axis-0 cell count, with an 'arteria' of 0.22 x that radius inside.
+    Returns ``(mask, arteria)`` bool cell arrays."""
+    n0, n1, n2 = (e - 1 for e in extents)
+    t = (np.arange(n2) + 0.5) / n2
+    c0 = n0 / 2.0 + 0.08 * n0 * np.sin(2 * np.pi * t)
+    c1 = n1 / 2.0 + 0.06 * n1 * np.cos(np.pi * t)
+    rad = n0 * (0.30 - 0.10 * t)
+    a0 = (np.arange(n0) + 0.5)[:, None, None]
+    a1 = (np.arange(n1) + 0.5)[None, :, None]
+    d2 = (a0 - c0[None, None, :]) ** 2 + (a1 - c1[None, None, :]) ** 2
+    return d2 <= rad[None, None, :] ** 2, d2 <= (0.22 * rad[None, None, :]) ** 2

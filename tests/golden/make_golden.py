@@ -290,6 +290,33 @@ def mask_cases():
                                             [face[0], np.nan if face[1] is None else face[1]])})
         print(tag, len(data.bnode_rows), int(data.active.sum()), its,
               f"{time.time() - t0:.1f}s", flush=True)
+    # heat stepping on a mask (SURVEY.md Appendix A composition on a
+    # MaskDomain): A = M + dt (K + W) with a global penalty, M the mask mass
+    p, ext_ = 2, (14, 15, 16)
+    g = Grid(ext_, (1.0 / 13,) * 3)
+    mask = mask_shapes(g.cell_extents)["tube"]
+    dom = MaskDomain(g, mask)
+    dt, w, val = 4.0 / 13 ** 2, 50.0, 1.0
+    shp = tuple(n + 2 * basis_extension(p) for n in g.extents)
+    kappa = 0.5 + rng.random(shp)
+    A = make_operator(build_system(dom, p, p, dt * kappa, np.ones(shp), [(0, 0, w * dt, val)]),
+                      "sparse")
+    Md = build_system(dom, p, p, np.zeros(shp), np.ones(shp), [])
+    M = make_operator(Md, "sparse")
+    zz, yy, xx = np.meshgrid(*[np.linspace(0, 1, k) for k in shp], indexing="ij")
+    u0 = np.exp(-10 * ((zz - .5) ** 2 + (yy - .4) ** 2 + (xx - .6) ** 2))
+    q = np.cos(3 * zz) * np.sin(2 * yy + xx)
+    F = assembled_rhs(Md, p, q)
+    G = assembled_rhs(A.data, p, np.zeros(shp))
+    u, its, sols = u0.copy(), [], []
+    for _ in range(3):
+        u, rep = pcg(A, M.apply(u) + dt * F + G, SolveConfig(tol=1e-12, max_iter=5000), x0=u)
+        its.append(rep.iterations)
+        sols.append(u.copy())
+    out.update({"heat_mask": mask, "heat_kappa": kappa, "heat_u0": u0, "heat_q": q,
+                "heat_its": np.array(its), "heat_u": np.stack(sols),
+                "heat_meta": np.array([p, dt, w, val] + list(ext_), dtype=float)})
+    print("heat", its, flush=True)
     np.savez_compressed(os.path.join(OUT, "mask.npz"), **out)
 
 

@@ -12,7 +12,7 @@ from paper_1904_03057_b200.domain import Grid, MaskDomain, active_nodes, node_cl
 from paper_1904_03057_b200.errors import EmptyDomainError, ValidationError
 
 GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "mask.npz"))
-TAGS = sorted({k.split("_")[0] for k in GOLD.keys()})
+TAGS = sorted({k.split("_")[0] for k in GOLD.keys() if k.startswith("m")})
 
 
 def case(tag):
@@ -88,3 +88,21 @@ def test_pcg_matches_reference(tag):
     assert abs(rep.iterations - its) <= max(1, its // 100)
     assert rel(x, GOLD[f"{tag}_x"]) <= 1e-7
     assert np.all(x[~GOLD[f"{tag}_active"]] == 0.0)
+
+
+@pytest.mark.gpu
+def test_heat_steps_on_mask_match_reference():
+    from paper_1904_03057_b200 import DirichletPenalty, HeatProblem, HeatSolver
+    from paper_1904_03057_b200.solver import SolveConfig
+
+    p, dt, w, val = (float(v) for v in GOLD["heat_meta"][:4])
+    ext = tuple(int(v) for v in GOLD["heat_meta"][4:7])
+    prob = HeatProblem(grid=Grid(ext, (1.0 / 13,) * 3), degree=int(p), dt=dt,
+                       conductivity=GOLD["heat_kappa"], initial_coeffs=GOLD["heat_u0"],
+                       source_coeffs=GOLD["heat_q"], bc=DirichletPenalty(val, 1.0 / w),
+                       mask=GOLD["heat_mask"])
+    hs = HeatSolver(prob, SolveConfig(tol=1e-12, max_iter=5000))
+    for k, its in enumerate(GOLD["heat_its"]):
+        rep = hs.step()
+        assert rep.converged and abs(rep.iterations - int(its)) <= max(1, int(its) // 100)
+        assert rel(hs.coefficients(), GOLD["heat_u"][k]) <= 1e-9
