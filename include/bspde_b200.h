@@ -190,6 +190,13 @@ int bspde_prefilter_lines(double* data, int32_t n, int64_t stride, int32_t na,
  * region [ext, dims[axis]-ext) is filled (transform_field, problem.py:178-194). */
 int bspde_reflect_pad(double* data, const int32_t* dims, const int64_t* strides,
                       int32_t axis, int32_t ext, void* stream);
+/* out[.., i, ..] = sum_t w[i*ntaps + t] * in[.., idx[i*ntaps + t], ..] along
+ * one axis (idx, w: DEVICE arrays, extension policy folded into idx): the
+ * spline evaluation of indirect_transform (bspline.py:245-310) on a lattice of
+ * points, one axis per call; ntaps <= 11. */
+int bspde_resample_axis(const double* in, const int64_t* in_strides, double* out,
+                        const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
+                        const int32_t* idx, const double* w, int32_t ntaps, void* stream);
 /* out[i] = sum_t taps[t] * in[i + offset + t] along one axis (sample_solution,
  * problem.py:330-348; accumulated in the reference's order), ntaps <= 11. */
 int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,

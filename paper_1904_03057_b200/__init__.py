@@ -12,11 +12,12 @@ multi-GPU sharding.  There is no CPU fallback.
 from .boundary import FACE_NAMES, DirichletPenalty, Neumann, Robin, realize_bc
 from .domain import BoxDomain, Grid, MaskDomain, active_nodes, interior_nodes, node_classes
 from .errors import (ConditioningWarning, ConfigurationError, DegreeError, DeterminismError,
-                     DivergenceError, EmptyDomainError, FormatError, IndefiniteOperatorError, NativeLibraryError,
+                     DivergenceError, EmptyDomainError, FormatError, OutOfDomainError, IndefiniteOperatorError, NativeLibraryError,
                      ResourceError, ValidationError)
 from .gram import GramFactor, basis_extension, edge_width, gram_factor, min_axis_length
 from .heat import HeatProblem, HeatSolver, heat_solve
 from .io import read_field, read_tensor, write_field, write_tensor
+from .problem import ProblemSpec, Solution, assemble_system, coarse_initialize, solve_problem
 from .operator import B200Operator, OpStats, assembled_rhs, make_operator
 from .solver import SolveConfig, SolveReport, pcg, pcg_device
 from .system import SystemData, build_system, heat_system, mass_system
@@ -30,7 +31,8 @@ __all__ = [
     "SolveConfig", "SolveReport", "pcg", "pcg_device",
     "HeatProblem", "HeatSolver", "heat_solve",
     "direct_transform", "transform_field", "sample_solution",
-    "read_tensor", "write_tensor", "read_field", "write_field", "FormatError", "EmptyDomainError",
+    "ProblemSpec", "Solution", "assemble_system", "coarse_initialize", "solve_problem",
+    "read_tensor", "write_tensor", "read_field", "write_field", "FormatError", "EmptyDomainError", "OutOfDomainError",
     "ConditioningWarning", "ConfigurationError", "DegreeError", "DeterminismError",
     "DivergenceError", "IndefiniteOperatorError", "NativeLibraryError", "ResourceError",
     "ValidationError",

@@ -1242,6 +1242,40 @@ __global__ void __launch_bounds__(256) fir_axis_kernel(const __grid_constant__ F
   }
 }
 
+// out[.., i, ..] = sum_t w[i, t] * in[.., idx[i, t], ..] along one axis:
+// spline evaluation on a lattice of points (indirect_transform,
+// bspline.py:245-310, separably per axis), per-output taps and gather
+// indices with the extension policy already folded into idx
+struct Resample {
+  const double* in;
+  long long is0, is1, is2;
+  double* out;
+  int d0, d1, d2;  // output extents
+  long long os0, os1, os2;
+  int axis, ntaps;
+  const int* idx;
+  const double* w;
+};
+
+__global__ void __launch_bounds__(256) resample_axis_kernel(const __grid_constant__ Resample f) {
+  const long long total = (long long)f.d0 * f.d1 * f.d2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i2 = (int)(t % f.d2);
+    const long long r = t / f.d2;
+    const int i1 = (int)(r % f.d1), i0 = (int)(r / f.d1);
+    const int io = f.axis == 0 ? i0 : (f.axis == 1 ? i1 : i2);
+    const long long sa = f.axis == 0 ? f.is0 : (f.axis == 1 ? f.is1 : f.is2);
+    const double* src = f.in + (f.axis == 0 ? 0 : i0 * f.is0) + (f.axis == 1 ? 0 : i1 * f.is1) +
+                        (f.axis == 2 ? 0 : i2 * f.is2);
+    const int* ix = f.idx + (long long)io * f.ntaps;
+    const double* wt = f.w + (long long)io * f.ntaps;
+    double acc = 0.0;
+    for (int k = 0; k < f.ntaps; ++k) acc = fma(wt[k], src[ix[k] * sa], acc);
+    f.out[i0 * f.os0 + i1 * f.os1 + i2 * f.os2] = acc;
+  }
+}
+
 // out = diag(A) expanded from the class table
 __global__ void diag_kernel(const double* __restrict__ tab, int nx, int ny, int nz, int nz_glob,
                             int z_off, int ghost, long long pitch_y, long long pitch_z, int ewz,
@@ -1915,6 +1949,38 @@ int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
   const unsigned blocks = (unsigned)std::min<long long>((total + threads - 1) / threads, 1 << 20);
   void* args[1] = {&f};
   CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&fir_axis_kernel), dim3(blocks),
+                            dim3(threads), args, 0, (cudaStream_t)stream));
+  return BSPDE_OK;
+}
+
+int bspde_resample_axis(const double* in, const int64_t* in_strides, double* out,
+                        const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
+                        const int32_t* idx, const double* w, int32_t ntaps, void* stream) {
+  if (!in || !in_strides || !out || !out_dims || !out_strides || !idx || !w)
+    return fail(BSPDE_ERR_ARG, "null argument");
+  if (axis < 0 || axis > 2 || ntaps < 1 || ntaps > MAXFIR) return fail(BSPDE_ERR_ARG, "bad axis / taps");
+  Resample f;
+  f.in = in;
+  f.is0 = in_strides[0];
+  f.is1 = in_strides[1];
+  f.is2 = in_strides[2];
+  f.out = out;
+  f.d0 = out_dims[0];
+  f.d1 = out_dims[1];
+  f.d2 = out_dims[2];
+  f.os0 = out_strides[0];
+  f.os1 = out_strides[1];
+  f.os2 = out_strides[2];
+  f.axis = axis;
+  f.ntaps = ntaps;
+  f.idx = idx;
+  f.w = w;
+  const long long total = (long long)f.d0 * f.d1 * f.d2;
+  if (total == 0) return BSPDE_OK;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)std::min<long long>((total + threads - 1) / threads, 1 << 20);
+  void* args[1] = {&f};
+  CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&resample_axis_kernel), dim3(blocks),
                             dim3(threads), args, 0, (cudaStream_t)stream));
   return BSPDE_OK;
 }

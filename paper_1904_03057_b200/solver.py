@@ -37,7 +37,7 @@ class SolveConfig:
     tol: float = 1e-8
     max_iter: int = 1000
     precond: str = "jacobi"  # "none" or "jacobi"
-    coarse_init_factor: int = 0  # accepted for API parity; coarse init is out of scope
+    coarse_init_factor: int = 0  # 0 disables coarse-grid initialization (problem.solve_problem)
     record_history: bool = False
     poll_every: int = 8  # CG iterations per CUDA-graph chunk between host polls
 

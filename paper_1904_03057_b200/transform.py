@@ -28,7 +28,7 @@ from functools import lru_cache
 import numpy as np
 
 from . import _native as N
-from .errors import ValidationError
+from .errors import OutOfDomainError, ValidationError
 from .gram import basis_extension, bspline_pieces
 
 EXTENSIONS = ("mirror", "replicate", "zero")
@@ -252,3 +252,103 @@ def sample_solution(coeffs_ext, grid, degree: int, device=None) -> np.ndarray:
     lay = SlabLayout(c3[0], c3[1], c3[2], ghost=0)
     buf = lay.upload(c.reshape(c3), dev)
     return sample_solution_device(buf, grid, degree, lay).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# spline evaluation on point lattices (indirect_transform, bspline.py:245-310)
+
+_PAD_FOLD = {"mirror", "replicate", "zero"}
+
+
+@lru_cache(maxsize=None)
+def _float_pieces(n: int):
+    return tuple((float(lo), tuple(float(c) for c in poly)) for lo, _, poly in bspline_pieces(n))
+
+
+def bspline_eval(n: int, x) -> np.ndarray:
+    """``beta^n(x)`` in float64 (piecewise polynomial, Horner), vectorized."""
+    x = np.asarray(x, dtype=np.float64)
+    pieces = _float_pieces(n)
+    a0 = pieces[0][0]
+    m = np.floor(x - a0).astype(np.int64)
+    out = np.zeros_like(x)
+    for k, (_, poly) in enumerate(pieces):
+        sel = m == k
+        if not sel.any():
+            continue
+        xs = x[sel]
+        v = np.zeros_like(xs)
+        for c in reversed(poly):
+            v = v * xs + c
+        out[sel] = v
+    return out
+
+
+def lattice_taps(n: int, step: float, points, size: int, first: int = 0, extension="mirror"):
+    """Gather indices (extension folded in) and weights of the ``n+1`` taps of
+    each point: ``k0 = floor(u - (n-1)/2)``, ``w_t = beta(u - k0 - t)`` with
+    ``u = x / h`` (``_tap_matrix``, bspline.py:245-250); coefficient ``k`` is
+    array index ``k - first``."""
+    if extension not in _PAD_FOLD:
+        raise ValidationError(f"unknown extension {extension!r}")
+    u = np.asarray(points, dtype=np.float64) / float(step)
+    lo, hi = first, first + size - 1
+    bad = (u < lo - 1e-12) | (u > hi + 1e-12)
+    if np.any(bad):
+        raise OutOfDomainError(f"grid coordinate {u[bad][0]} outside node span [{lo}, {hi}]")
+    k0 = np.floor(u - (n - 1) / 2.0).astype(np.int64)
+    taps = np.arange(n + 1)
+    w = bspline_eval(n, u[:, None] - (k0[:, None] + taps[None, :]))
+    idx = k0[:, None] + taps[None, :] - first
+    if size == 1:
+        idx = np.zeros_like(idx)
+    elif extension == "mirror":  # np.pad "reflect"
+        period = 2 * (size - 1)
+        idx = np.abs(idx) % period
+        idx = np.where(idx >= size, period - idx, idx)
+    elif extension == "replicate":
+        idx = np.clip(idx, 0, size - 1)
+    else:
+        w = np.where((idx < 0) | (idx >= size), 0.0, w)
+        idx = np.clip(idx, 0, size - 1)
+    return idx.astype(np.int32), w
+
+
+def evaluate_lattice_device(coeffs, degree: int, steps, axis_points, first_index=None,
+                            extension="mirror", stream=None):
+    """Evaluate the expansion with coefficients ``coeffs`` (dense torch CUDA
+    tensor, 1-3 d) at the tensor lattice ``axis_points`` (one 1-d array of
+    physical coordinates relative to the origin per axis): one
+    ``bspde_resample_axis`` launch per axis.  Returns a dense tensor."""
+    torch = _torch()
+    lib = N.load()
+    d = coeffs.dim()
+    first = tuple(first_index) if first_index is not None else (0,) * d
+    cur = coeffs.reshape((1,) * (3 - d) + tuple(coeffs.shape))
+    for ax in range(d):
+        a3 = ax + 3 - d
+        idx, w = lattice_taps(int(degree), steps[ax], axis_points[ax], cur.shape[a3], first[ax],
+                              extension)
+        shape = list(cur.shape)
+        shape[a3] = len(axis_points[ax])
+        out = torch.empty(shape, dtype=torch.float64, device=cur.device)
+        it = torch.from_numpy(np.ascontiguousarray(idx)).to(cur.device)
+        wt = torch.from_numpy(np.ascontiguousarray(w)).to(cur.device)
+        N.check(lib.bspde_resample_axis(N.ptr(cur), _i64(cur.stride()), N.ptr(out),
+                                        _i32(out.shape), _i64(out.stride()), a3, N.ptr(it),
+                                        N.ptr(wt), int(idx.shape[1]), N.stream_handle(stream)))
+        cur = out
+    return cur.reshape(tuple(len(p) for p in axis_points))
+
+
+def indirect_transform_lattice(coeffs, degree: int, steps, axis_points, first_index=None,
+                               extension="mirror", device=None) -> np.ndarray:
+    """Host wrapper of :func:`evaluate_lattice_device` (reference
+    ``indirect_transform`` at the points of a tensor lattice)."""
+    from .device import require_cuda
+
+    torch = _torch()
+    dev = require_cuda(device)
+    c = torch.from_numpy(np.ascontiguousarray(coeffs, dtype=np.float64)).to(dev)
+    return evaluate_lattice_device(c, degree, steps, axis_points, first_index,
+                                   extension).cpu().numpy()

@@ -320,6 +320,44 @@ def mask_cases():
     np.savez_compressed(os.path.join(OUT, "mask.npz"), **out)
 
 
+def coarse_cases():
+    """coarse_initialize + solve_problem with coarse_init_factor
+    (problem.py:374-482): a masked leg-like tube (p = 1, penalty) and a box
+    with sampled fields (p = 3, Robin faces)."""
+    from bspde.domain import MaskDomain
+    from bspde.problem import (DirichletPenalty, ProblemSpec, Robin, coarse_initialize,
+                               solve_problem)
+
+    out = {}
+    rng = np.random.default_rng(8642)
+    g1 = Grid((13, 14, 31), (1.0, 1.0, 1.0))
+    mask = mask_shapes(g1.cell_extents)["tube"]
+    src = np.zeros(g1.extents)
+    src[4:9, 5:9, 3:25] = 1.0
+    g2 = Grid((11, 12, 13), (0.1, 0.08, 0.12))
+    zz, yy, xx = np.meshgrid(*[g2.node_coordinates(a) for a in range(3)], indexing="ij")
+    cases = [
+        ("c1", ProblemSpec(domain=MaskDomain(g1, mask), basis_degree=1, diffusion=0.5,
+                           absorption=0.0, source=src, bc=DirichletPenalty(20.0, 1e-3)), 3),
+        ("c3", ProblemSpec(domain=BoxDomain(g2), basis_degree=3,
+                           diffusion=1.0 + 0.3 * np.sin(4 * xx) * np.cos(3 * yy),
+                           absorption=0.5 + zz, source=np.exp(-(xx - .5) ** 2 - yy),
+                           bc=Robin(0.7)), 2),
+    ]
+    for tag, spec, factor in cases:
+        x0, info = coarse_initialize(spec, factor)
+        sol = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000, coarse_init_factor=factor),
+                            strategy="sparse")
+        sol0 = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000), strategy="sparse")
+        out.update({f"{tag}_x0": x0, f"{tag}_coarse_its": np.array([info["coarse_iterations"]]),
+                    f"{tag}_coarse_ext": np.array(info["coarse_extents"]),
+                    f"{tag}_its": np.array([sol.report.iterations, sol0.report.iterations]),
+                    f"{tag}_coeffs": sol.coeffs, f"{tag}_samples": sol.samples})
+        print(tag, info, sol.report.iterations, sol0.report.iterations, flush=True)
+    out.update({"c1_mask": mask, "c1_src": src})
+    np.savez_compressed(os.path.join(OUT, "coarse.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -438,8 +476,10 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "heat16",
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "heat16",
                              "heat64"]
+    if "coarse" in which:
+        coarse_cases()
     if "mask" in which:
         mask_cases()
     if "tbsf" in which:

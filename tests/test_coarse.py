@@ -1,0 +1,78 @@
+"""Steady pipeline with coarse-grid initialisation against reference fixtures
+(tests/golden/coarse.npz, make_golden.py ``coarse``; problem.py:374-482)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1904_03057_b200.domain import BoxDomain, Grid, MaskDomain
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "coarse.npz"))
+
+
+def specs():
+    from paper_1904_03057_b200.boundary import DirichletPenalty, Robin
+    from paper_1904_03057_b200.problem import ProblemSpec
+
+    g1 = Grid((13, 14, 31), (1.0, 1.0, 1.0))
+    g2 = Grid((11, 12, 13), (0.1, 0.08, 0.12))
+    zz, yy, xx = np.meshgrid(*[g2.node_coordinates(a) for a in range(3)], indexing="ij")
+    return {
+        "c1": (ProblemSpec(domain=MaskDomain(g1, GOLD["c1_mask"]), basis_degree=1, diffusion=0.5,
+                           absorption=0.0, source=GOLD["c1_src"],
+                           bc=DirichletPenalty(20.0, 1e-3)), 3),
+        "c3": (ProblemSpec(domain=BoxDomain(g2), basis_degree=3,
+                           diffusion=1.0 + 0.3 * np.sin(4 * xx) * np.cos(3 * yy),
+                           absorption=0.5 + zz, source=np.exp(-(xx - .5) ** 2 - yy),
+                           bc=Robin(0.7)), 2),
+    }
+
+
+def rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def test_spec_validation():
+    from paper_1904_03057_b200.errors import ConfigurationError, ValidationError
+    from paper_1904_03057_b200.problem import ProblemSpec
+
+    g = Grid((6, 6, 6), (1.0, 1.0, 1.0))
+    with pytest.raises(ValidationError):
+        ProblemSpec(domain=BoxDomain(Grid((3, 3, 3), (1.0, 1.0, 1.0))), basis_degree=5)
+    with pytest.raises(ValidationError):
+        ProblemSpec(domain=BoxDomain(g), basis_degree=3, precision="f16")
+    with pytest.raises(ConfigurationError):
+        ProblemSpec(domain=BoxDomain(g), basis_degree=3, prefilter="l2")
+    s = ProblemSpec(domain=BoxDomain(g), basis_degree=3)
+    assert s.param_degree == 3 and s.source_degree == 3 and s.default_epsilon() == 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["c1", "c3"])
+def test_coarse_initialize_matches_reference(tag):
+    from paper_1904_03057_b200.problem import coarse_initialize
+
+    spec, factor = specs()[tag]
+    x0, info = coarse_initialize(spec, factor)
+    assert tuple(info["coarse_extents"]) == tuple(GOLD[f"{tag}_coarse_ext"])
+    assert abs(info["coarse_iterations"] - int(GOLD[f"{tag}_coarse_its"][0])) <= 1
+    # coarse solve to tol 1e-8: rounding differences scale with kappa * tol
+    assert rel(x0, GOLD[f"{tag}_x0"]) <= 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["c1", "c3"])
+def test_solve_problem_with_coarse_init(tag):
+    from paper_1904_03057_b200.problem import solve_problem
+    from paper_1904_03057_b200.solver import SolveConfig
+
+    spec, factor = specs()[tag]
+    its_ref, its_ref0 = (int(v) for v in GOLD[f"{tag}_its"])
+    sol = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000, coarse_init_factor=factor))
+    assert sol.report.converged
+    assert abs(sol.report.iterations - its_ref) <= max(1, its_ref // 100)
+    assert rel(sol.coeffs, GOLD[f"{tag}_coeffs"]) <= 1e-6
+    assert rel(sol.samples, GOLD[f"{tag}_samples"]) <= 1e-6
+    sol0 = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000))
+    assert abs(sol0.report.iterations - its_ref0) <= max(1, its_ref0 // 100)
