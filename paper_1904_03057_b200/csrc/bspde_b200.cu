@@ -704,7 +704,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   {
     // ---- z: shift-register scatter (row z' of the symmetric Mz, Kz) ----
     const int cz = in_grid ? cls_of(zg, prm.nz_glob, ewz) : ewz;
-    if (false) {
+    if (cz == ewz && prm.zfast) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const double a = STIFF ? wa[i] : wm[i];
