@@ -55,6 +55,11 @@ int main(void) {{
   F(bspde_plan_desc, c_mass) F(bspde_plan_desc, c_stiff) F(bspde_plan_desc, ew)
   F(bspde_cg_config, poll_every) F(bspde_cg_report, relative_residual)
   F(bspde_cg_report, last_pAp)
+  printf("bspde_stencil_desc %zu\\n", sizeof(bspde_stencil_desc));
+  printf("bspde_mask_desc %zu\\n", sizeof(bspde_mask_desc));
+  F(bspde_stencil_desc, tables) F(bspde_stencil_desc, face_weight) F(bspde_stencil_desc, step)
+  F(bspde_mask_desc, nbrows) F(bspde_mask_desc, cell_tri) F(bspde_mask_desc, fc)
+  F(bspde_mask_desc, surface_weight)
   return 0;
 }}
 """)
@@ -63,7 +68,8 @@ int main(void) {{
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
     vals = dict(line.split() for line in out if line.strip())
     structs = {"bspde_plan_desc": N.PlanDesc, "bspde_cg_config": N.CgConfig,
-               "bspde_cg_report": N.CgReport}
+               "bspde_cg_report": N.CgReport, "bspde_stencil_desc": N.StencilDesc,
+               "bspde_mask_desc": N.MaskDesc}
     for key, v in vals.items():
         if "." in key:
             sname, field = key.split(".")
@@ -176,3 +182,17 @@ def test_transform_entry_points_validate_arguments():
     assert lib.bspde_reflect_pad(vp, dims, strides, 3, 1, None) == 1
     taps = (C.c_double * 12)()
     assert lib.bspde_fir_axis(vp, strides, vp, dims, strides, 2, 0, taps, 12, None) == 1
+    idx = (C.c_int32 * 8)()
+    assert lib.bspde_resample_axis(vp, strides, vp, dims, strides, 2, None, vp, 2, None) == 1
+    assert lib.bspde_resample_axis(vp, strides, vp, dims, strides, 3, C.cast(idx, C.c_void_p),
+                                   vp, 2, None) == 1
+    assert lib.bspde_resample_axis(vp, strides, vp, dims, strides, 2, C.cast(idx, C.c_void_p),
+                                   vp, 12, None) == 1
+
+
+def test_mask_entry_points_validate_arguments():
+    lib = N.load()
+    m = N.MaskDesc()
+    assert lib.bspde_stencil_mask_patch(None, C.byref(m), None, None, None, None) == 1
+    assert b"null" in lib.bspde_last_error()
+    assert lib.bspde_stencil_mask_surface_rhs(None, C.byref(m), 1.0, None, None) == 1
