@@ -302,10 +302,119 @@ unsigned st_grid(const bspde_stencil* s, long long n) {
   return (unsigned)std::max<long long>(1, std::min<long long>(want, std::min(MAXGRID, s->num_sms * 8)));
 }
 
+// Same operator, outputs mapped along y: a thread owns XB consecutive y
+// outputs at one x, consecutive lanes take consecutive x.  Every P load of a
+// warp is then one contiguous 256-byte access (the x-mapped kernel's lanes
+// sit 4 doubles apart), and each output still sums its stencil entries in
+// ascending a = (az, ay, ax), so t is bitwise the x-mapped result.
+template <int MODE, int NB>
+__global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev S,
+                                                                const double* __restrict__ P,
+                                                                const double* __restrict__ c,
+                                                                double* __restrict__ out,
+                                                                const double* __restrict__ aux,
+                                                                double* partials, unsigned* counter,
+                                                                CgState* st, int precond) {
+  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ unsigned s_last;
+  if (MODE == 2 && !ld_vol(&st->active)) return;
+  constexpr int A = 2 * NB + 1, hb = NB, NR = XB + 2 * NB;
+  constexpr int center = (hb * A + hb) * A + hb;
+  const int nyb = (S.ny + XB - 1) / XB;
+  const long long groups = (long long)S.nz * nyb * S.nx;
+  const long long sy = S.nx;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
+       gi += (long long)gridDim.x * blockDim.x) {
+    const int lx = (int)(gi % S.nx);
+    const long long r = gi / S.nx;
+    const int yb = (int)(r % nyb), lz = (int)(r / nyb);
+    const int ly0 = yb * XB;
+    const long long l0 = ((long long)lz * S.ny + ly0) * S.nx + lx;
+    const int nv = min(XB, S.ny - ly0);
+    double t[XB];
+#pragma unroll
+    for (int v = 0; v < XB; ++v) t[v] = 0.0;
+#pragma unroll 1
+    for (int az = -hb; az <= hb; ++az) {
+      const int z = lz + az;
+      if (z < 0 || z >= S.nz) continue;
+      const long long abase = (long long)(az + hb) * A * A;
+#pragma unroll
+      for (int yr = 0; yr < NR; ++yr) {  // c row y' = ly0 - hb + yr
+        const int y = ly0 - hb + yr;
+        if (y < 0 || y >= S.ny) continue;
+        const double* crow = c + ((long long)z * S.ny + y) * S.nx;
+        double seg[A];
+#pragma unroll
+        for (int ax = 0; ax < A; ++ax) {
+          const int x = lx - hb + ax;
+          seg[ax] = (x >= 0 && x < S.nx) ? crow[x] : 0.0;
+        }
+#pragma unroll
+        for (int v = 0; v < XB; ++v) {
+          const int ay = yr - v;  // + hb offset: row index of the stencil
+          if (ay < 0 || ay >= A) continue;
+          if (v >= nv) continue;
+          const double* pa = P + (abase + (long long)ay * A) * S.N + l0 + v * sy;
+#pragma unroll
+          for (int ax = 0; ax < A; ++ax) t[v] = fma(pa[(long long)ax * S.N], seg[ax], t[v]);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < XB; ++v) {
+      if (v >= nv) break;
+      const long long l = l0 + v * sy;
+      if (MODE == 0) {
+        out[l] = t[v];
+      } else if (MODE == 1) {
+        const double bb = aux[l];
+        const double rr = bb - t[v];
+        out[l] = rr;
+        const double dg = P[(long long)center * S.N + l];
+        const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+        s0 = fma(bb, bb, s0);
+        s1 = fma(rr, __dmul_rn(inv, rr), s1);
+        s2 = fma(rr, rr, s2);
+      } else {
+        out[l] = t[v];
+        s0 = fma(c[l], t[v], s0);
+      }
+    }
+  }
+  if (MODE == 1) {
+    double v[3] = {s0, s1, s2};
+    reduce_and_finalize<3, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 0);
+  } else if (MODE == 2) {
+    double v[1] = {s0};
+    reduce_and_finalize<1, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 1);
+  }
+}
+
+inline bool st_ymap() {
+  static const int v = [] {
+    const char* e = getenv("BSPDE_ST_XMAP");
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 template <int MODE>
 void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const double* P,
               const double* c, double* out, const double* aux, double* partials,
               unsigned* counter, CgState* state, int precond) {
+  // y mapping for p >= 3 (measured +5-30% apply, +25% PCG at p = 3); at
+  // p = 1, 2 the compiler batches every load of the short stencil into
+  // registers (128-255) and the x mapping is faster
+  if (st_ymap() && s->S.nb >= 3) {
+    switch (s->S.nb) {
+      case 3: stencil_apply_y_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      case 4: stencil_apply_y_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      default: stencil_apply_y_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    }
+    return;
+  }
   switch (s->S.nb) {
     case 1: stencil_apply_kernel<MODE, 1><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
     case 2: stencil_apply_kernel<MODE, 2><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
