@@ -197,6 +197,12 @@ int bspde_reflect_pad(double* data, const int32_t* dims, const int64_t* strides,
 int bspde_resample_axis(const double* in, const int64_t* in_strides, double* out,
                         const int32_t* out_dims, const int64_t* out_strides, int32_t axis,
                         const int32_t* idx, const double* w, int32_t ntaps, void* stream);
+/* out[q] = sum_{a,b,k} wz[q,a] wy[q,b] wx[q,k] c[iz[q,a], iy[q,b], ix[q,k]] for
+ * npts scattered points (indirect_transform, bspline.py:253-310): idx / w are
+ * DEVICE arrays [3][npts][ntaps] (axis 0, 1, 2; extension folded into idx),
+ * c a 3-D array with the given element strides; ntaps <= 11. */
+int bspde_eval_points(const double* c, const int64_t* strides, int64_t npts, int32_t ntaps,
+                      const int32_t* idx, const double* w, double* out, void* stream);
 /* out[i] = sum_t taps[t] * in[i + offset + t] along one axis (sample_solution,
  * problem.py:330-348; accumulated in the reference's order), ntaps <= 11. */
 int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,

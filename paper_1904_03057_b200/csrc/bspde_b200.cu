@@ -1276,6 +1276,35 @@ __global__ void __launch_bounds__(256) resample_axis_kernel(const __grid_constan
   }
 }
 
+// out[q] = sum_{i,j,k} wz[q,i] wy[q,j] wx[q,k] c[iz[q,i], iy[q,j], ix[q,k]]:
+// the expansion at scattered points (indirect_transform, bspline.py:253-310),
+// taps / folded indices per point and axis precomputed, one thread per point
+__global__ void __launch_bounds__(256) eval_points_kernel(
+    const double* __restrict__ c, long long sz, long long sy, long long sx, long long npts,
+    int nt, const int* __restrict__ idx, const double* __restrict__ w, double* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < npts;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int* iz = idx + q * nt;
+    const int* iy = iz + npts * nt;
+    const int* ix = iy + npts * nt;
+    const double* wz = w + q * nt;
+    const double* wy = wz + npts * nt;
+    const double* wx = wy + npts * nt;
+    double acc = 0.0;
+    for (int a = 0; a < nt; ++a) {
+      double ya = 0.0;
+      for (int b = 0; b < nt; ++b) {
+        const double* row = c + iz[a] * sz + iy[b] * sy;
+        double xa = 0.0;
+        for (int k = 0; k < nt; ++k) xa = fma(wx[k], row[ix[k] * sx], xa);
+        ya = fma(wy[b], xa, ya);
+      }
+      acc = fma(wz[a], ya, acc);
+    }
+    out[q] = acc;
+  }
+}
+
 // out = diag(A) expanded from the class table
 __global__ void diag_kernel(const double* __restrict__ tab, int nx, int ny, int nz, int nz_glob,
                             int z_off, int ghost, long long pitch_y, long long pitch_z, int ewz,
@@ -1982,6 +2011,18 @@ int bspde_resample_axis(const double* in, const int64_t* in_strides, double* out
   void* args[1] = {&f};
   CUDA_TRY(cudaLaunchKernel(reinterpret_cast<const void*>(&resample_axis_kernel), dim3(blocks),
                             dim3(threads), args, 0, (cudaStream_t)stream));
+  return BSPDE_OK;
+}
+
+int bspde_eval_points(const double* c, const int64_t* strides, int64_t npts, int32_t ntaps,
+                      const int32_t* idx, const double* w, double* out, void* stream) {
+  if (!c || !strides || !idx || !w || !out) return fail(BSPDE_ERR_ARG, "null argument");
+  if (ntaps < 1 || ntaps > MAXFIR || npts < 0) return fail(BSPDE_ERR_ARG, "bad taps / point count");
+  if (npts == 0) return BSPDE_OK;
+  const unsigned blocks = (unsigned)std::min<long long>((npts + 255) / 256, 1 << 20);
+  eval_points_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(c, strides[0], strides[1],
+                                                              strides[2], npts, ntaps, idx, w, out);
+  CUDA_TRY(cudaGetLastError());
   return BSPDE_OK;
 }
 

@@ -352,3 +352,45 @@ def indirect_transform_lattice(coeffs, degree: int, steps, axis_points, first_in
     c = torch.from_numpy(np.ascontiguousarray(coeffs, dtype=np.float64)).to(dev)
     return evaluate_lattice_device(c, degree, steps, axis_points, first_index,
                                    extension).cpu().numpy()
+
+
+def indirect_transform(coeffs, basis, points, extension="mirror", first_index=None, step=None,
+                       device=None) -> np.ndarray:
+    """The expansion at arbitrary points (reference ``indirect_transform``,
+    bspline.py:253-310): ``points`` (npts, dim) physical coordinates with node
+    ``k`` at ``k*h``; ``basis`` a degree (then ``step`` gives h per axis) or an
+    object with ``degree`` and ``step``.  One thread per point on the GPU."""
+    from .device import require_cuda
+
+    torch = _torch()
+    n = _degree_of(basis)
+    arr = np.asarray(coeffs, dtype=np.float64)
+    d = arr.ndim
+    steps = tuple(getattr(basis, "step", None) or step or (1.0,) * d)
+    if hasattr(basis, "dim") and basis.dim != d:
+        raise ValidationError(f"coefficients are {d}-d but basis is {basis.dim}-d")
+    if extension not in EXTENSIONS:
+        raise ValidationError(f"unknown extension {extension!r}; pick from {EXTENSIONS}")
+    pts = np.asarray(points, dtype=np.float64)
+    if d == 1 and pts.ndim == 1:
+        pts = pts[:, None]
+    if pts.ndim == 1:
+        pts = pts[None, :]
+    if pts.shape[-1] != d:
+        raise ValidationError(f"points have {pts.shape[-1]} components, basis is {d}-d")
+    first = tuple(first_index) if first_index is not None else (0,) * d
+    npts, nt = pts.shape[0], n + 1
+    idx = np.zeros((3, npts, nt), dtype=np.int32)
+    w = np.zeros((3, npts, nt))
+    w[: 3 - d, :, 0] = 1.0  # leading singleton axes
+    for ax in range(d):
+        i, wt = lattice_taps(n, steps[ax], pts[:, ax], arr.shape[ax], first[ax], extension)
+        idx[3 - d + ax], w[3 - d + ax] = i, wt
+    dev = require_cuda(device)
+    c3 = torch.from_numpy(np.ascontiguousarray(arr.reshape((1,) * (3 - d) + arr.shape))).to(dev)
+    it = torch.from_numpy(idx).to(dev)
+    wt_ = torch.from_numpy(w).to(dev)
+    out = torch.empty(npts, dtype=torch.float64, device=dev)
+    N.check(N.load().bspde_eval_points(N.ptr(c3), _i64(c3.stride()), npts, nt, N.ptr(it),
+                                       N.ptr(wt_), N.ptr(out), N.stream_handle()))
+    return out.cpu().numpy()

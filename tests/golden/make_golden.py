@@ -358,6 +358,33 @@ def coarse_cases():
     np.savez_compressed(os.path.join(OUT, "coarse.npz"), **out)
 
 
+def indirect_cases():
+    """indirect_transform at scattered points (bspline.py:253-310), 1-3 d,
+    degrees 1..5, all extensions, with and without first_index."""
+    from bspde.bspline import BSplineBasis, indirect_transform
+
+    out = {}
+    rng = np.random.default_rng(1357)
+    cases = [("1d_p1", (9,), 1, "mirror", None), ("1d_p4_zero", (12,), 4, "zero", None),
+             ("2d_p2_rep", (7, 9), 2, "replicate", None), ("2d_p3", (8, 6), 3, "mirror", (-1, -1)),
+             ("3d_p3", (7, 8, 9), 3, "mirror", None), ("3d_p5_zero", (9, 8, 7), 5, "zero", (-2, -2, -2)),
+             ("3d_p2_rep", (6, 7, 5), 2, "replicate", None)]
+    for tag, shape, n, ext_, first in cases:
+        step = tuple(0.1 + 0.05 * i for i in range(len(shape)))
+        c = rng.normal(size=shape)
+        f = first or (0,) * len(shape)
+        pts = np.stack([(f[a] + rng.random(40) * (shape[a] - 1)) * step[a]
+                        for a in range(len(shape))], axis=1)
+        pts[:3] = [[(f[a] + (shape[a] - 1) * (k / 2)) * step[a] for a in range(len(shape))]
+                   for k in range(3)]  # span ends and middle
+        vals = indirect_transform(c, BSplineBasis(n, step), pts, ext_, first)
+        out.update({f"{tag}_c": c, f"{tag}_pts": pts, f"{tag}_vals": vals,
+                    f"{tag}_meta": np.array([n] + list(step)),
+                    f"{tag}_first": np.array(first if first else []),
+                    f"{tag}_ext": np.array([ext_])})
+    np.savez_compressed(os.path.join(OUT, "indirect.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -476,8 +503,10 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "heat16",
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "indirect", "heat16",
                              "heat64"]
+    if "indirect" in which:
+        indirect_cases()
     if "coarse" in which:
         coarse_cases()
     if "mask" in which:

@@ -76,3 +76,28 @@ def test_solve_problem_with_coarse_init(tag):
     assert rel(sol.samples, GOLD[f"{tag}_samples"]) <= 1e-6
     sol0 = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000))
     assert abs(sol0.report.iterations - its_ref0) <= max(1, its_ref0 // 100)
+
+
+IND = np.load(os.path.join(os.path.dirname(__file__), "golden", "indirect.npz"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", sorted({k.rsplit("_", 1)[0] for k in IND.keys()}))
+def test_indirect_transform_matches_reference(tag):
+    from paper_1904_03057_b200.transform import indirect_transform
+
+    meta = IND[f"{tag}_meta"]
+    first = IND[f"{tag}_first"]
+    vals = indirect_transform(IND[f"{tag}_c"], int(meta[0]), IND[f"{tag}_pts"],
+                              str(IND[f"{tag}_ext"][0]),
+                              tuple(int(v) for v in first) if first.size else None,
+                              step=tuple(meta[1:]))
+    assert np.abs(vals - IND[f"{tag}_vals"]).max() <= 1e-13 * max(1.0, np.abs(IND[f"{tag}_vals"]).max())
+
+
+def test_indirect_transform_rejects_points_outside_the_span():
+    from paper_1904_03057_b200.errors import OutOfDomainError
+    from paper_1904_03057_b200.transform import lattice_taps
+
+    with pytest.raises(OutOfDomainError):
+        lattice_taps(3, 0.5, np.array([0.0, 4.6]), 10)
