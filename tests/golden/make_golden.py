@@ -344,6 +344,11 @@ def coarse_cases():
                            absorption=0.5 + zz, source=np.exp(-(xx - .5) ** 2 - yy),
                            bc=Robin(0.7)), 2),
     ]
+    g3 = Grid((21, 17), (0.05, 0.06))
+    yy2, xx2 = np.meshgrid(*[g3.node_coordinates(a) for a in range(2)], indexing="ij")
+    cases.append(("c2d", ProblemSpec(domain=BoxDomain(g3), basis_degree=2, diffusion=0.8,
+                                     absorption=1.0, source=np.cos(3 * xx2) + yy2,
+                                     bc={"all": DirichletPenalty(1.0, 1e-3)}), 3))
     for tag, spec, factor in cases:
         x0, info = coarse_initialize(spec, factor)
         sol = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000, coarse_init_factor=factor),

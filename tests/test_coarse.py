@@ -18,7 +18,12 @@ def specs():
     g1 = Grid((13, 14, 31), (1.0, 1.0, 1.0))
     g2 = Grid((11, 12, 13), (0.1, 0.08, 0.12))
     zz, yy, xx = np.meshgrid(*[g2.node_coordinates(a) for a in range(3)], indexing="ij")
+    g3 = Grid((21, 17), (0.05, 0.06))
+    yy2, xx2 = np.meshgrid(*[g3.node_coordinates(a) for a in range(2)], indexing="ij")
     return {
+        "c2d": (ProblemSpec(domain=BoxDomain(g3), basis_degree=2, diffusion=0.8, absorption=1.0,
+                            source=np.cos(3 * xx2) + yy2, bc={"all": DirichletPenalty(1.0, 1e-3)}),
+                3),
         "c1": (ProblemSpec(domain=MaskDomain(g1, GOLD["c1_mask"]), basis_degree=1, diffusion=0.5,
                            absorption=0.0, source=GOLD["c1_src"],
                            bc=DirichletPenalty(20.0, 1e-3)), 3),
@@ -49,7 +54,7 @@ def test_spec_validation():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tag", ["c1", "c3"])
+@pytest.mark.parametrize("tag", ["c1", "c3", "c2d"])
 def test_coarse_initialize_matches_reference(tag):
     from paper_1904_03057_b200.problem import coarse_initialize
 
@@ -62,7 +67,7 @@ def test_coarse_initialize_matches_reference(tag):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tag", ["c1", "c3"])
+@pytest.mark.parametrize("tag", ["c1", "c3", "c2d"])
 def test_solve_problem_with_coarse_init(tag):
     from paper_1904_03057_b200.problem import solve_problem
     from paper_1904_03057_b200.solver import SolveConfig
