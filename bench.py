@@ -359,8 +359,13 @@ def e2e_rate(step, u, u0, lay, dofs, steps, stream, barrier, max_over_ranks):
     import torch
 
     host = torch.empty(lay.owned_shape, dtype=torch.float64).pin_memory()
-    host.copy_(lay.owned(u0).cpu())
     own = lay.owned(u)
+    # untimed warm-up of the same pipeline (first DMA through the freshly
+    # pinned buffer and the side streams), then reset the input
+    host.copy_(lay.owned(u0).cpu())
+    run_steps_host(step, own, host, 1, chunks=16, stream=stream)
+    torch.cuda.synchronize()
+    host.copy_(lay.owned(u0).cpu())
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
