@@ -360,6 +360,12 @@ def coarse_cases():
                     f"{tag}_coeffs": sol.coeffs, f"{tag}_samples": sol.samples})
         print(tag, info, sol.report.iterations, sol0.report.iterations, flush=True)
     out.update({"c1_mask": mask, "c1_src": src})
+    from bspde.problem import _coarsen_mask
+    for k, (shape, cn) in enumerate([((12, 13, 30), (4, 5, 11)), ((9, 9), (4, 3)),
+                                     ((17,), (6,)), ((6, 6, 6), (2, 2, 2))]):
+        m = rng.random(shape) < (0.5 if k < 3 else 0.02)
+        out[f"cm{k}_fine"] = m
+        out[f"cm{k}_coarse"] = _coarsen_mask(m, Grid(tuple(c + 1 for c in cn), (1.0,) * len(cn)))
     np.savez_compressed(os.path.join(OUT, "coarse.npz"), **out)
 
 

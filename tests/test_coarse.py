@@ -106,3 +106,13 @@ def test_indirect_transform_rejects_points_outside_the_span():
 
     with pytest.raises(OutOfDomainError):
         lattice_taps(3, 0.5, np.array([0.0, 4.6]), 10)
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_coarsen_mask_matches_reference(k):
+    from paper_1904_03057_b200.problem import _coarsen_mask
+
+    want = GOLD[f"cm{k}_coarse"]
+    got = _coarsen_mask(GOLD[f"cm{k}_fine"], Grid(tuple(c + 1 for c in want.shape),
+                                                  (1.0,) * want.ndim))
+    assert np.array_equal(got, want)
