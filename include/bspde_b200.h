@@ -225,7 +225,7 @@ typedef struct bspde_stencil bspde_stencil;
 typedef struct {
   int32_t device;
   int32_t degree;        /* n_b in 1..5 */
-  int32_t param_degree;  /* n_p in 1..5 (degree of the D / mu fields) */
+  int32_t param_degree;  /* n_p in 0..5 (degree of the D / mu fields) */
   int32_t nz, ny, nx;    /* coefficient (extended) extents */
   int32_t pz, py, px;    /* parameter-field (extended) extents */
   int32_t ext, ext_p;    /* basis_extension(n_b), basis_extension(n_p) */

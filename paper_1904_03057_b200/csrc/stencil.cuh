@@ -448,8 +448,8 @@ extern "C" {
 int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
   if (!desc || !out) return fail(BSPDE_ERR_ARG, "null argument");
   const auto& d = *desc;
-  if (d.degree < 1 || d.degree > MAXP || d.param_degree < 1 || d.param_degree > MAXP)
-    return fail(BSPDE_ERR_ARG, "degrees must be in 1..5");
+  if (d.degree < 1 || d.degree > MAXP || d.param_degree < 0 || d.param_degree > MAXP)
+    return fail(BSPDE_ERR_ARG, "degrees must be n_b in 1..5, n_p in 0..5");
   if (d.nz < 1 || d.ny < 1 || d.nx < 1 || d.pz < 1 || d.py < 1 || d.px < 1)
     return fail(BSPDE_ERR_ARG, "empty extents");
   const int EW = edge_width_of(d.degree);

@@ -315,7 +315,8 @@ def trilinear_tables(n_b: int, n_p: int, deriv: int) -> np.ndarray:
     ew = interior, ew+1..2ew = last rows (the mirror image, sign +1 since
     both factors carry the same derivative)."""
     _check_degree(n_b)
-    _check_degree(n_p)
+    if not isinstance(n_p, (int, np.integer)) or not 0 <= n_p <= MAX_DEGREE:
+        raise DegreeError(f"parameter degree {n_p} not in 0..{MAX_DEGREE}")
     interior, edge = _trilinear_exact(n_b, n_p, deriv)
     ew = edge_width(n_b)
     A, B = 2 * n_b + 1, 2 * param_reach(n_b, n_p) + 1

@@ -130,8 +130,8 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
     faces = () if is_mask else tuple(_face_terms(face_specs, grid.dim))
     if not 1 <= int(n_b) <= 5:
         raise ValidationError(f"basis degree {n_b} not in 1..5")
-    if not 1 <= int(n_p) <= 5:
-        raise ValidationError(f"parameter degree {n_p} not in 1..5")
+    if not 0 <= int(n_p) <= 5:
+        raise ValidationError(f"parameter degree {n_p} not in 0..5")
     if not is_mask:
         for n in grid.extents:
             if n - 1 < min_axis_length(n_b):

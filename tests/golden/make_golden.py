@@ -160,6 +160,8 @@ VAR_CASES = [
     ("v2p5", (9, 10, 11), (0.5, 1.0, 0.25), 2, 5),
     ("v3f", (9, 10, 11), (0.5, 1.0, 0.25), 3, 3),   # + Robin / penalty faces
     ("v2f", (9, 10, 11), (0.5, 1.0, 0.25), 2, 3),
+    ("v3p0", (9, 10, 11), (0.5, 1.0, 0.25), 3, 0),  # piecewise-constant fields
+    ("v1p0", (9, 10, 11), (0.5, 1.0, 0.25), 1, 0),
 ]
 VAR_FACES = [(0, 0, 0.7, None), (1, 1, 20.0, 1.5), (2, 0, 5.0, -0.5), (2, 1, 0.3, None)]
 
@@ -249,6 +251,7 @@ MASK_CASES = [
     ("m3v", (16, 17, 18), (0.3, 0.4, 0.5), "blob", 3, 1, "var", "var", (0.7, None)),
     ("m4", (14, 15, 16), (0.5, 1.0, 0.25), "tube", 4, 2, 1.0, 0.5, None),
     ("m5", (14, 15, 16), (0.5, 1.0, 0.25), "ball", 5, 3, 0.8, 0.1, (3.0, -1.0)),
+    ("m3p0", (16, 17, 18), (0.5, 1.0, 0.25), "blob", 3, 0, "var", "var", (0.7, None)),
 ]
 
 

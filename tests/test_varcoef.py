@@ -9,9 +9,9 @@ from paper_1904_03057_b200.errors import ConfigurationError
 from paper_1904_03057_b200.gram import basis_extension, edge_width, trilinear_tables
 from paper_1904_03057_b200.varcoef import VarSystemData
 
-TAGS = ["v1", "v2", "v3", "v4", "v5", "v3p2", "v2p5", "v3f", "v2f"]
+TAGS = ["v1", "v2", "v3", "v4", "v5", "v3p2", "v2p5", "v3f", "v2f", "v3p0", "v1p0"]
 # v4, v5 stop at max_iter in the reference
-CONVERGED = ["v1", "v2", "v3", "v3p2", "v2p5", "v3f", "v2f"]
+CONVERGED = ["v1", "v2", "v3", "v3p2", "v2p5", "v3f", "v2f", "v3p0", "v1p0"]
 
 
 def case(golden, tag):
