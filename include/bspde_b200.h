@@ -243,6 +243,10 @@ typedef struct {
   const double* face_values;  /* host, ew values of the low face (high face mirrored) */
   const double* mass_gram;    /* host, unit mass Gram class table (2ew+1) x (2n_b+1) */
   double step[3];
+  /* 1-D / 2-D problems ride as 3-D with unit leading axes: degenerate[a] = 1
+   * marks such an axis (extent 1, no extension, tables the identity factor:
+   * value class table 1 at (a = 0, b = 0), derivative table 0, step 1) */
+  int32_t degenerate[3];
 } bspde_stencil_desc;
 
 int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** plan);
@@ -292,6 +296,7 @@ typedef struct {
   int32_t fc;                 /* first_clean_position(n_b) */
   int32_t has_surface;        /* exposed-face terms with one global weight */
   double surface_weight;
+  int32_t degenerate[3];      /* unit axes of a 1-D / 2-D mask (one cell layer) */
 } bspde_mask_desc;
 
 int bspde_stencil_mask_patch(bspde_stencil* plan, const bspde_mask_desc* mask,

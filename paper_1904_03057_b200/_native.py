@@ -75,6 +75,7 @@ class StencilDesc(C.Structure):
         ("face_values", _dptr),
         ("mass_gram", _dptr),
         ("step", C.c_double * 3),
+        ("degenerate", C.c_int32 * 3),
     ]
 
 
@@ -94,6 +95,7 @@ class MaskDesc(C.Structure):
         ("fc", C.c_int32),
         ("has_surface", C.c_int32),
         ("surface_weight", C.c_double),
+        ("degenerate", C.c_int32 * 3),
     ]
 
 

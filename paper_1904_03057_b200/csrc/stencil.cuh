@@ -40,6 +40,8 @@ struct StencilDev {
   double fv[MAXP + 1];          // low-face values (ew entries)
   double gram[11 * 11];         // unit mass Gram class table (2ew+1) x (2nb+1)
   double step[3];
+  int degen[3];             // unit axes of 1-D / 2-D problems (no extension)
+  int ex[3], exp_[3];       // per-axis ext / ext_p (0 on unit axes)
 };
 
 __device__ __forceinline__ double st_face_value(const StencilDev& S, int i, int n, int side) {
@@ -84,8 +86,8 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
     const double* tx0 = st_tab(S, s_tab, 2, 0, cx) + ax * S.B;
     const double* tx1 = st_tab(S, s_tab, 2, 1, cx) + ax * S.B;
     // parameter window of node l: field index (l - ext) + ext_p + (b - mw)
-    const int fz0 = lz - S.ext + S.ext_p - S.mw, fy0 = ly - S.ext + S.ext_p - S.mw,
-              fx0 = lx - S.ext + S.ext_p - S.mw;
+    const int fz0 = lz - S.ex[0] + S.exp_[0] - S.mw, fy0 = ly - S.ex[1] + S.exp_[1] - S.mw,
+              fx0 = lx - S.ex[2] + S.exp_[2] - S.mw;
     double acc = 0.0;
     for (int bz = 0; bz < S.B; ++bz) {
       const int fz = fz0 + bz;
@@ -119,7 +121,11 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
                   st_face_value(S, li[ax3] + ai[ax3], ni[ax3], S.face_side[f]);
         } else {
           const int j = li[ax3] + ai[ax3];
-          prod *= (j >= 0 && j < ni[ax3]) ? S.step[ax3] * S.gram[ci[ax3] * S.A + ai[ax3] + S.nb] : 0.0;
+          if (S.degen[ax3])
+            prod *= ai[ax3] == 0 ? 1.0 : 0.0;
+          else
+            prod *= (j >= 0 && j < ni[ax3]) ? S.step[ax3] * S.gram[ci[ax3] * S.A + ai[ax3] + S.nb]
+                                            : 0.0;
         }
       }
       acc += prod;
@@ -510,7 +516,17 @@ int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
     for (int k = 0; k < EW; ++k) S.fv[k] = d.face_values[k];
     for (int k = 0; k < (2 * EW + 1) * S.A; ++k) S.gram[k] = d.mass_gram[k];
   }
-  for (int a = 0; a < 3; ++a) S.step[a] = d.step[a];
+  for (int a = 0; a < 3; ++a) {
+    S.step[a] = d.step[a];
+    S.degen[a] = d.degenerate[a] ? 1 : 0;
+    S.ex[a] = S.degen[a] ? 0 : d.ext;
+    S.exp_[a] = S.degen[a] ? 0 : d.ext_p;
+    if (S.degen[a] && ((a == 0 ? d.nz : a == 1 ? d.ny : d.nx) != 1 ||
+                       (a == 0 ? d.pz : a == 1 ? d.py : d.px) != 1)) {
+      delete s;
+      return fail(BSPDE_ERR_ARG, "a degenerate axis must have extent 1");
+    }
+  }
   const size_t per = (size_t)S.A * S.B;
   std::vector<double> tab((size_t)3 * 2 * S.ncls * per, 0.0);
   for (int a = 0; a < 3; ++a)
@@ -703,37 +719,47 @@ __global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
     const int off[3] = {a / (S.A * S.A) - S.nb, (a / S.A) % S.A - S.nb, a % S.A - S.nb};
     const int lz = (int)(l / ((long long)S.nx * S.ny)), ly = (int)((l / S.nx) % S.ny),
               lx = (int)(l % S.nx);
-    const int sp[3] = {lz - S.ext, ly - S.ext, lx - S.ext};  // spline indices of the row
+    const int sp[3] = {lz - S.ex[0], ly - S.ex[1], lx - S.ex[2]};  // spline indices of the row
     // per axis: the cells of the row's support (test offset j2) whose trial
-    // offset j1 = j2 + off also lies on the cell
-    int j2lo[3], j2hi[3];
+    // offset j1 = j2 + off also lies on the cell.  A unit axis has one cell
+    // layer, one offset and the identity factor (value 1, derivative 0).
+    const double unit[2] = {1.0, 0.0};
+    int j2lo[3], j2hi[3], jl[3], nbx[3], bl[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
+      const int n = M.degenerate[d] ? 1 : nj;
       j2lo[d] = max(0, -off[d]);
-      j2hi[d] = min(nj, nj - off[d]);
+      j2hi[d] = min(n, n - off[d]);
+      jl[d] = M.degenerate[d] ? 0 : M.jlo;
+      nbx[d] = M.degenerate[d] ? 1 : nbp;
+      bl[d] = M.degenerate[d] ? 0 : M.blo;
     }
+    auto tri = [&](int d, int j2, int k) -> const double* {  // k: 0 value, 1 derivative
+      if (M.degenerate[d]) return unit + k;
+      return M.cell_tri + ((long long)(j2 + off[d]) * nj + j2) * nbp + k * tstride;
+    };
     double acc = 0.0;
     for (int jz = j2lo[0]; jz < j2hi[0]; ++jz) {
-      const int cz = sp[0] - (M.jlo + jz);
-      const double* tz0 = M.cell_tri + ((long long)(jz + off[0]) * nj + jz) * nbp;
-      const double* tz1 = tz0 + tstride;
+      const int cz = sp[0] - (jl[0] + jz);
+      const double* tz0 = tri(0, jz, 0);
+      const double* tz1 = tri(0, jz, 1);
       for (int jy = j2lo[1]; jy < j2hi[1]; ++jy) {
-        const int cy = sp[1] - (M.jlo + jy);
-        const double* ty0 = M.cell_tri + ((long long)(jy + off[1]) * nj + jy) * nbp;
-        const double* ty1 = ty0 + tstride;
+        const int cy = sp[1] - (jl[1] + jy);
+        const double* ty0 = tri(1, jy, 0);
+        const double* ty1 = tri(1, jy, 1);
         for (int jx = j2lo[2]; jx < j2hi[2]; ++jx) {
-          const int cx = sp[2] - (M.jlo + jx);
+          const int cx = sp[2] - (jl[2] + jx);
           if (!mask_occ(M, cz, cy, cx)) continue;
-          const double* tx0 = M.cell_tri + ((long long)(jx + off[2]) * nj + jx) * nbp;
-          const double* tx1 = tx0 + tstride;
+          const double* tx0 = tri(2, jx, 0);
+          const double* tx1 = tri(2, jx, 1);
           // parameter spline c + blo + b lives at field index c + blo + b + ext_p
-          const int fz0 = cz + M.blo + S.ext_p, fy0 = cy + M.blo + S.ext_p,
-                    fx0 = cx + M.blo + S.ext_p;
+          const int fz0 = cz + bl[0] + S.exp_[0], fy0 = cy + bl[1] + S.exp_[1],
+                    fx0 = cx + bl[2] + S.exp_[2];
           double cell = 0.0;
-          for (int bz = 0; bz < nbp; ++bz) {
+          for (int bz = 0; bz < nbx[0]; ++bz) {
             const int fz = fz0 + bz;
             if (fz < 0 || fz >= S.pz) continue;
-            for (int by = 0; by < nbp; ++by) {
+            for (int by = 0; by < nbx[1]; ++by) {
               const int fy = fy0 + by;
               if (fy < 0 || fy >= S.py) continue;
               const double zy00 = tz0[bz] * ty0[by];
@@ -742,7 +768,7 @@ __global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
               const double k_x = S.s_stiff[2] * zy00;
               const double m_zy = S.s_mass * zy00;
               const long long row = ((long long)fz * S.py + fy) * S.px;
-              for (int bx = 0; bx < nbp; ++bx) {
+              for (int bx = 0; bx < nbx[2]; ++bx) {
                 const int fx = fx0 + bx;
                 if (fx < 0 || fx >= S.px) continue;
                 const double kd = (k_z + k_y) * tx0[bx] + k_x * tx1[bx];
@@ -756,8 +782,10 @@ __global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
     }
     if (M.has_surface) {
       // exposed faces: (v v)_normal (x) R (x) R over the tangential axes
+      // (a unit axis is never a face normal and contributes the factor 1)
       const int nv = 2 * M.fc - 1;
       for (int axn = 0; axn < 3; ++axn) {
+        if (M.degenerate[axn]) continue;
         const int t1 = axn == 0 ? 1 : 0, t2 = axn == 2 ? 1 : 2;
         const double tscale = S.step[t1] * S.step[t2];
         for (int side = 0; side < 2; ++side) {
@@ -769,12 +797,13 @@ __global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
             int c[3];
             c[axn] = sp[axn] - (side + k - (M.fc - 1));
             for (int ja = j2lo[t1]; ja < j2hi[t1]; ++ja) {
-              c[t1] = sp[t1] - (M.jlo + ja);
-              const double ra = M.cell_bil[(ja + off[t1]) * nj + ja];
+              c[t1] = sp[t1] - (jl[t1] + ja);
+              const double ra = M.degenerate[t1] ? 1.0 : M.cell_bil[(ja + off[t1]) * nj + ja];
               for (int jb = j2lo[t2]; jb < j2hi[t2]; ++jb) {
-                c[t2] = sp[t2] - (M.jlo + jb);
+                c[t2] = sp[t2] - (jl[t2] + jb);
                 if (!mask_exposed(M, c, axn, side)) continue;
-                acc += M.surface_weight * tscale * vv * ra * M.cell_bil[(jb + off[t2]) * nj + jb];
+                const double rb = M.degenerate[t2] ? 1.0 : M.cell_bil[(jb + off[t2]) * nj + jb];
+                acc += M.surface_weight * tscale * vv * ra * rb;
               }
             }
           }
@@ -793,22 +822,27 @@ __global__ void __launch_bounds__(ST_NT) mask_surface_rhs_kernel(const StencilDe
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < M.nbrows;
        i += (long long)gridDim.x * blockDim.x) {
     const long long l = M.brows[i];
-    const int sp[3] = {(int)(l / ((long long)S.nx * S.ny)) - S.ext,
-                       (int)((l / S.nx) % S.ny) - S.ext, (int)(l % S.nx) - S.ext};
+    const int sp[3] = {(int)(l / ((long long)S.nx * S.ny)) - S.ex[0],
+                       (int)((l / S.nx) % S.ny) - S.ex[1], (int)(l % S.nx) - S.ex[2]};
     double acc = 0.0;
     for (int axn = 0; axn < 3; ++axn) {
+      if (M.degenerate[axn]) continue;
       const int t1 = axn == 0 ? 1 : 0, t2 = axn == 2 ? 1 : 2;
+      const int n1 = M.degenerate[t1] ? 1 : M.nj, n2 = M.degenerate[t2] ? 1 : M.nj;
+      const int l1 = M.degenerate[t1] ? 0 : M.jlo, l2 = M.degenerate[t2] ? 0 : M.jlo;
       const double tscale = S.step[t1] * S.step[t2];
       for (int side = 0; side < 2; ++side)
         for (int k = 0; k < nv; ++k) {
           int c[3];
           c[axn] = sp[axn] - (side + k - (M.fc - 1));
-          for (int ja = 0; ja < M.nj; ++ja) {
-            c[t1] = sp[t1] - (M.jlo + ja);
-            for (int jb = 0; jb < M.nj; ++jb) {
-              c[t2] = sp[t2] - (M.jlo + jb);
+          for (int ja = 0; ja < n1; ++ja) {
+            c[t1] = sp[t1] - (l1 + ja);
+            const double sa = M.degenerate[t1] ? 1.0 : M.cell_single[ja];
+            for (int jb = 0; jb < n2; ++jb) {
+              c[t2] = sp[t2] - (l2 + jb);
               if (!mask_exposed(M, c, axn, side)) continue;
-              acc += scale * tscale * M.face_vals[k] * M.cell_single[ja] * M.cell_single[jb];
+              const double sb = M.degenerate[t2] ? 1.0 : M.cell_single[jb];
+              acc += scale * tscale * M.face_vals[k] * sa * sb;
             }
           }
         }
@@ -824,9 +858,13 @@ int mask_check(const bspde_stencil* s, const bspde_mask_desc* m) {
   if (m->nj < 1 || m->nj > MASK_MAXJ || m->nbp < 1 || m->nbp > MASK_MAXJ || m->fc < 1 ||
       m->fc > 3 || m->nbrows < 0)
     return fail(BSPDE_ERR_ARG, "mask desc: table sizes out of range");
-  if (m->cells[0] != s->S.nz - 2 * s->S.ext - 1 || m->cells[1] != s->S.ny - 2 * s->S.ext - 1 ||
-      m->cells[2] != s->S.nx - 2 * s->S.ext - 1)
-    return fail(BSPDE_ERR_ARG, "mask cell extents do not match the plan");
+  const int n3[3] = {s->S.nz, s->S.ny, s->S.nx};
+  for (int a = 0; a < 3; ++a) {
+    if ((m->degenerate[a] != 0) != (s->S.degen[a] != 0))
+      return fail(BSPDE_ERR_ARG, "mask and plan disagree on unit axes");
+    const int want = s->S.degen[a] ? 1 : n3[a] - 2 * s->S.ext - 1;
+    if (m->cells[a] != want) return fail(BSPDE_ERR_ARG, "mask cell extents do not match the plan");
+  }
   return BSPDE_OK;
 }
 

@@ -122,8 +122,6 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
     from .domain import MaskDomain
 
     grid = domain.grid
-    if grid.dim != 3:
-        raise ConfigurationError("the b200 variable-coefficient operator is 3-D")
     from .system import _face_terms
 
     is_mask = isinstance(domain, MaskDomain)
@@ -176,22 +174,31 @@ class B200StencilOperator:
         self.workers = int(workers)
         self.device = require_cuda(device)
         self.lib = N.load()
+        # 1-D / 2-D systems run as 3-D with unit leading axes (identity factor)
+        self.lead = lead = 3 - data.dim
         d = N.StencilDesc()
         d.device = int(self.device.index)
         d.degree, d.param_degree = data.n_b, data.n_p
-        d.nz, d.ny, d.nx = data.cext
-        d.pz, d.py, d.px = data.dfield.shape
+        d.nz, d.ny, d.nx = (1,) * lead + tuple(data.cext)
+        d.pz, d.py, d.px = (1,) * lead + tuple(data.dfield.shape)
         d.ext, d.ext_p = data.ext, data.ext_p
         self._keep = [np.ascontiguousarray(t, dtype=np.float64) for t in data.tables]
+        A, B = 2 * data.n_b + 1, 2 * param_reach(data.n_b, data.n_p) + 1
+        unit_v = np.zeros((1, A, B))
+        unit_v[0, data.n_b, B // 2] = 1.0
+        unit = [unit_v, np.zeros((1, A, B))]
+        self._keep += unit
         for a in range(3):
-            d.ew[a] = 0 if data.mask is not None else edge_width(data.n_b)
+            real = a >= lead
+            d.degenerate[a] = 0 if real else 1
+            d.ew[a] = edge_width(data.n_b) if (real and data.mask is None) else 0
             for k in range(2):
-                d.tables[a][k] = self._keep[k].ctypes.data_as(N._dptr)
-            d.scale_stiff[a] = data.scale_stiff[a]
+                d.tables[a][k] = (self._keep[k] if real else unit[k]).ctypes.data_as(N._dptr)
+            d.scale_stiff[a] = data.scale_stiff[a - lead] if real else 0.0
         d.scale_mass = data.scale_mass
         d.nfaces = len(data.faces)
         for f, ft in enumerate(data.faces):
-            d.face_axis[f], d.face_side[f], d.face_weight[f] = ft.axis, ft.side, ft.weight
+            d.face_axis[f], d.face_side[f], d.face_weight[f] = ft.axis + lead, ft.side, ft.weight
         if data.faces:
             fv = np.array([float(v) for v in face_values(data.n_b)])
             gram = np.ascontiguousarray(gram_factor(data.n_b, data.domain.grid.extents[0],
@@ -200,7 +207,7 @@ class B200StencilOperator:
             d.face_values = fv.ctypes.data_as(N._dptr)
             d.mass_gram = gram.ctypes.data_as(N._dptr)
         for a in range(3):
-            d.step[a] = data.step[a]
+            d.step[a] = data.step[a - lead] if a >= lead else 1.0
         h = C.c_void_p()
         N.check(self.lib.bspde_stencil_create(C.byref(d), C.byref(h)))
         self.handle = h
@@ -210,8 +217,8 @@ class B200StencilOperator:
             raise ResourceError(f"stencil array needs {n_entries * 8 / 1e9:.1f} GB "
                                 f"(free {free / 1e9:.1f} GB)")
         self.P = torch.empty(n_entries, dtype=torch.float64, device=self.device)
-        df = torch.from_numpy(data.dfield).to(self.device)
-        mf = torch.from_numpy(data.mfield).to(self.device)
+        df = torch.from_numpy(np.ascontiguousarray(data.dfield)).to(self.device)
+        mf = torch.from_numpy(np.ascontiguousarray(data.mfield)).to(self.device)
         N.check(self.lib.bspde_stencil_assemble(h, N.ptr(df), N.ptr(mf), N.ptr(self.P),
                                                 N.stream_handle()))
         self._mask = None
@@ -244,8 +251,10 @@ class B200StencilOperator:
         d = N.MaskDesc()
         d.occupancy, d.node_class, d.brows = (N.ptr(keep["occ"]), N.ptr(keep["cls"]),
                                               N.ptr(keep["brows"]))
+        cells = (1,) * self.lead + tuple(m.occupancy.shape)
         for a in range(3):
-            d.cells[a] = m.occupancy.shape[a]
+            d.cells[a] = cells[a]
+            d.degenerate[a] = 1 if a < self.lead else 0
         d.nbrows = len(m.brows)
         (jlo, jhi), (blo, bhi) = cell_offsets(nb), cell_offsets(npar)
         d.jlo, d.nj, d.blo, d.nbp = jlo, jhi - jlo + 1, blo, bhi - blo + 1

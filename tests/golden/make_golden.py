@@ -399,6 +399,50 @@ def indirect_cases():
     np.savez_compressed(os.path.join(OUT, "indirect.npz"), **out)
 
 
+def lowdim_cases():
+    """1-D / 2-D variable-coefficient boxes (with faces) and masks
+    (test_acceptance.py:95-125 mixes d = 2, 3): apply, diagonal, assembled
+    RHS, PCG."""
+    from bspde.domain import MaskDomain
+
+    out = {}
+    rng = np.random.default_rng(4242)
+    g2 = Grid((14, 15), (0.5, 0.25))
+    zz, yy = np.meshgrid(np.arange(13) + 0.5, np.arange(14) + 0.5, indexing="ij")
+    disk = (zz - 6.5) ** 2 + (yy - 7.0) ** 2 <= 30.0
+    ring = disk & ((zz - 6.5) ** 2 + (yy - 7.0) ** 2 >= 4.0)
+    line = np.array([False, True, True, True, True, True, True, True, False, False, True, True,
+                     True, True, False, False])
+    cases = [
+        ("b2v", BoxDomain(Grid((13, 11), (0.3, 0.5))), 3, 2, "var", "var",
+         [(0, 0, 0.7, None), (1, 1, 5.0, 1.5)]),
+        ("b1v", BoxDomain(Grid((17,), (0.2,))), 2, 1, "var", "var", [(0, 1, 2.0, 0.5)]),
+        ("m2d", MaskDomain(g2, disk), 2, 1, "var", 0.3, [(0, 0, 3.0, 1.0)]),
+        ("m2d3", MaskDomain(g2, ring), 3, 0, "var", "var", []),
+        ("m1d", MaskDomain(Grid((17,), (0.25,)), line), 1, 1, "var", "var", [(0, 0, 2.0, 0.5)]),
+    ]
+    for tag, dom, nb, npar, Dv, muv, specs in cases:
+        pext = tuple(n + 2 * basis_extension(npar) for n in dom.grid.extents)
+        D = 0.3 + rng.random(pext) if Dv == "var" else np.full(pext, float(Dv))
+        mu = 0.2 + rng.random(pext) if muv == "var" else np.full(pext, float(muv))
+        data = build_system(dom, nb, npar, D, mu, specs)
+        op = make_operator(data, "sparse")
+        c = rng.normal(size=data.cext)
+        q = rng.normal(size=data.cext)
+        xs = rng.normal(size=data.cext)
+        if data.active is not None:
+            xs = np.where(data.active, xs, 0.0)
+        b = op.apply(xs)
+        x, rep = pcg(op, b, SolveConfig(tol=1e-10, max_iter=4000))
+        out.update({f"{tag}_D": D, f"{tag}_mu": mu, f"{tag}_c": c, f"{tag}_t": op.apply(c),
+                    f"{tag}_diag": op.jacobi_diagonal(), f"{tag}_q": q,
+                    f"{tag}_rhs": assembled_rhs(data, nb, q), f"{tag}_b": b, f"{tag}_x": x,
+                    f"{tag}_its": np.array([rep.iterations])})
+        print(tag, rep.iterations, flush=True)
+    out.update({"m2d_mask": disk, "m2d3_mask": ring, "m1d_mask": line})
+    np.savez_compressed(os.path.join(OUT, "lowdim.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -517,8 +561,10 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "indirect", "heat16",
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "indirect", "lowdim", "heat16",
                              "heat64"]
+    if "lowdim" in which:
+        lowdim_cases()
     if "indirect" in which:
         indirect_cases()
     if "coarse" in which:

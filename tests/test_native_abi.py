@@ -58,6 +58,7 @@ int main(void) {{
   printf("bspde_stencil_desc %zu\\n", sizeof(bspde_stencil_desc));
   printf("bspde_mask_desc %zu\\n", sizeof(bspde_mask_desc));
   F(bspde_stencil_desc, tables) F(bspde_stencil_desc, face_weight) F(bspde_stencil_desc, step)
+  F(bspde_stencil_desc, degenerate) F(bspde_mask_desc, degenerate)
   F(bspde_mask_desc, nbrows) F(bspde_mask_desc, cell_tri) F(bspde_mask_desc, fc)
   F(bspde_mask_desc, surface_weight)
   return 0;
