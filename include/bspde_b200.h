@@ -217,7 +217,8 @@ int bspde_fir_axis(const double* in, const int64_t* in_strides, double* out,
  *                   + mu[l+b] sm (Tz Ty Tx)[a, b] ]
  * from per-axis trilinear tables (kernels.py:158-173, edge rows
  * assembly.py:83-108), assembled once into HBM and applied as
- * t_l = sum_a P[a, l] c[l + a].  3-D box domains, optional Robin /
+ * t_l = sum_a P[a, l] c[l + a].  Box domains in 1-3 D (unit axes, see
+ * `degenerate`), optional Robin /
  * penalty face terms.
  * Fields are dense (z, y, x) arrays (x fastest) on the device. */
 typedef struct bspde_stencil bspde_stencil;
