@@ -190,6 +190,13 @@ int bspde_prefilter_lines(double* data, int32_t n, int64_t stride, int32_t na,
  * region [ext, dims[axis]-ext) is filled (transform_field, problem.py:178-194). */
 int bspde_reflect_pad(double* data, const int32_t* dims, const int64_t* strides,
                       int32_t axis, int32_t ext, void* stream);
+/* In place along lines (same addressing as bspde_prefilter_lines): solve the
+ * banded system L U x = x with DEVICE factors lb[n][m] (L[i, i-k], unit
+ * diagonal) and ub[n][m+1] (U[i, i+k]) -- the mirror-folded Gram system of the
+ * "l2" prefilter (_l2_project_axis, problem.py:142-175); m <= 8. */
+int bspde_banded_solve_lines(double* data, int32_t n, int64_t stride, int32_t na, int32_t nb,
+                             int64_t sa, int64_t sb, const double* lb, const double* ub,
+                             int32_t m, void* stream);
 /* out[.., i, ..] = sum_t w[i*ntaps + t] * in[.., idx[i*ntaps + t], ..] along
  * one axis (idx, w: DEVICE arrays, extension policy folded into idx): the
  * spline evaluation of indirect_transform (bspline.py:245-310) on a lattice of

@@ -144,6 +144,8 @@ SIGNATURES = [
     ("bspde_stencil_mask_surface_rhs", C.c_int, [_VP, C.POINTER(MaskDesc), C.c_double, _VP, _VP]),
     ("bspde_resample_axis", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int32, _VP, _VP, C.c_int32,
                                       _VP]),
+    ("bspde_banded_solve_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                           C.c_int64, C.c_int64, _VP, _VP, C.c_int32, _VP]),
     ("bspde_eval_points", C.c_int, [_VP, _VP, C.c_int64, C.c_int32, _VP, _VP, _VP, _VP]),
     ("bspde_prefilter_lines", C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_int64, C.c_int64, _VP, C.c_int32, C.c_double,

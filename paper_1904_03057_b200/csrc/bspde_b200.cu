@@ -1242,6 +1242,32 @@ __global__ void __launch_bounds__(256) fir_axis_kernel(const __grid_constant__ F
   }
 }
 
+// x = U^-1 L^-1 x in place along lines: the banded LU (no pivoting; same
+// factors for every line) of the mirror-folded Gram system of the "l2"
+// prefilter (_l2_project_axis, problem.py:142-175).  lb[i*m + k-1] = L[i, i-k],
+// ub[i*(m+1) + k] = U[i, i+k].
+__global__ void __launch_bounds__(128) banded_solve_kernel(const Lines L,
+                                                           const double* __restrict__ lb,
+                                                           const double* __restrict__ ub,
+                                                           const int m) {
+  const long long line = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (line >= (long long)L.na * L.nb) return;
+  const int ia = (int)(line % L.na), ib = (int)(line / L.na);
+  double* c = L.data + ia * L.sa + ib * L.sb;
+  const long long s = L.stride;
+  const int n = L.n;
+  for (int i = 1; i < n; ++i) {  // forward: unit lower band
+    double v = c[i * s];
+    for (int k = 1; k <= m && k <= i; ++k) v = fma(-lb[(long long)i * m + k - 1], c[(i - k) * s], v);
+    c[i * s] = v;
+  }
+  for (int i = n - 1; i >= 0; --i) {  // backward: upper band
+    double v = c[i * s];
+    for (int k = 1; k <= m && i + k < n; ++k) v = fma(-ub[(long long)i * (m + 1) + k], c[(i + k) * s], v);
+    c[i * s] = v / ub[(long long)i * (m + 1)];
+  }
+}
+
 // out[.., i, ..] = sum_t w[i, t] * in[.., idx[i, t], ..] along one axis:
 // spline evaluation on a lattice of points (indirect_transform,
 // bspline.py:245-310, separably per axis), per-output taps and gather
@@ -1930,6 +1956,21 @@ int bspde_prefilter_lines(double* data, int32_t n, int64_t stride, int32_t na, i
   const int threads = 128;
   prefilter_kernel<<<(unsigned)((lines + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
       L, npoles, poles[0], npoles > 1 ? poles[1] : 0.0, h[0], h[1], gain, extension);
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_banded_solve_lines(double* data, int32_t n, int64_t stride, int32_t na, int32_t nb,
+                             int64_t sa, int64_t sb, const double* lb, const double* ub,
+                             int32_t m, void* stream) {
+  if (!data || !lb || !ub) return fail(BSPDE_ERR_ARG, "null argument");
+  if (n < 1 || na < 0 || nb < 0 || m < 1 || m > 8) return fail(BSPDE_ERR_ARG, "bad line geometry / band");
+  const long long lines = (long long)na * nb;
+  if (lines == 0) return BSPDE_OK;
+  Lines L{data, n, stride, na, nb, sa, sb};
+  const int threads = 128;
+  banded_solve_kernel<<<(unsigned)((lines + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+      L, lb, ub, m);
   CUDA_TRY(cudaGetLastError());
   return BSPDE_OK;
 }

@@ -30,8 +30,8 @@ from .transform import (direct_transform, indirect_transform_lattice, sample_fie
 @dataclass
 class ProblemSpec:
     """Domain, fields (scalar, node samples or callable), degrees, BCs
-    (``problem.py:66-116``).  The B200 path computes in float64 with the
-    interpolating prefilter and ``source_degree == basis_degree``."""
+    (``problem.py:66-116``).  The B200 path computes in float64 with
+    ``source_degree == basis_degree``; both prefilters are realized."""
 
     domain: object
     basis_degree: int
@@ -64,9 +64,8 @@ class ProblemSpec:
             raise ValidationError(
                 f"extents {self.grid.extents} too small for degree {self.basis_degree} "
                 f"(need >= {need})")
-        if self.precision != "f64" or self.prefilter != "interpolation":
-            raise ConfigurationError("the b200 path realizes precision='f64' with the "
-                                     "interpolating prefilter")
+        if self.precision != "f64":
+            raise ConfigurationError("the b200 path computes in float64 (precision='f64')")
 
     @property
     def dtype(self):
@@ -112,9 +111,10 @@ def transform_inputs(spec: ProblemSpec) -> FieldSet:
     """D, mu (degree n_p) and q (degree n_s) to coefficients on the GPU;
     negative D / mu overshoots are clamped with a warning (``problem.py:197-217``)."""
     grid = spec.grid
-    d = transform_field(spec.diffusion, grid, spec.param_degree)
-    m = transform_field(spec.absorption, grid, spec.param_degree)
-    q = transform_field(spec.source, grid, spec.source_degree)
+    pf = spec.prefilter
+    d = transform_field(spec.diffusion, grid, spec.param_degree, prefilter=pf)
+    m = transform_field(spec.absorption, grid, spec.param_degree, prefilter=pf)
+    q = transform_field(spec.source, grid, spec.source_degree, prefilter=pf)
     cd, cm = int(np.sum(d < 0)), int(np.sum(m < 0))
     if cd:
         warnings.warn(f"clamped {cd} negative diffusion coefficients after prefiltering")

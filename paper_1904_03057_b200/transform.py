@@ -140,9 +140,12 @@ def fir_axis_device(src, out, axis, offset, taps, stream=None):
     return out
 
 
-def transform_field_device(value, grid, degree: int, layout, device, out=None, stream=None):
+def transform_field_device(value, grid, degree: int, layout, device, out=None, stream=None,
+                           prefilter="interpolation"):
     """Scalar, node samples or callable -> extended-grid coefficients in the
-    ghosted-slab buffer ``out`` (allocated if None).  Constants stay exact."""
+    ghosted-slab buffer ``out`` (allocated if None).  Constants stay exact.
+    ``prefilter``: "interpolation" (direct transform) or "l2" (projection,
+    degree >= 2; problem.py:178-194)."""
     torch = _torch()
     ext = basis_extension(degree)
     buf = layout.alloc(device) if out is None else out
@@ -158,7 +161,14 @@ def transform_field_device(value, grid, degree: int, layout, device, out=None, s
     inner = own3[tuple(slice(ext, own3.shape[a] - ext) if a >= 3 - d else slice(None)
                        for a in range(3))]
     inner.copy_(torch.from_numpy(np.ascontiguousarray(samples).reshape(inner.shape)))
-    prefilter_device(inner, degree, ndim=d, stream=stream)
+    if prefilter == "l2" and degree >= 2:
+        dense = inner.contiguous()
+        l2_project_device(dense, degree, ndim=d)
+        inner.copy_(dense)
+    elif prefilter in ("interpolation", "l2"):
+        prefilter_device(inner, degree, ndim=d, stream=stream)
+    else:
+        raise ValidationError(f"prefilter must be interpolation/l2, got {prefilter!r}")
     reflect_pad_device(own3, ext, ndim=d, stream=stream)
     return buf
 
@@ -223,7 +233,7 @@ def direct_transform(samples, basis, extension="mirror", device=None):
     return t.cpu().numpy()
 
 
-def transform_field(value, grid, degree: int, device=None) -> np.ndarray:
+def transform_field(value, grid, degree: int, device=None, prefilter="interpolation") -> np.ndarray:
     """Scalar, node samples or callable -> extended-grid coefficients (host)."""
     from .device import SlabLayout, require_cuda
 
@@ -234,7 +244,7 @@ def transform_field(value, grid, degree: int, device=None) -> np.ndarray:
     dev = require_cuda(device)
     c3 = (1,) * (3 - len(cext)) + cext
     lay = SlabLayout(c3[0], c3[1], c3[2], ghost=0)
-    buf = transform_field_device(value, grid, degree, lay, dev)
+    buf = transform_field_device(value, grid, degree, lay, dev, prefilter=prefilter)
     return lay.download(buf).reshape(cext)
 
 
@@ -394,3 +404,89 @@ def indirect_transform(coeffs, basis, points, extension="mirror", first_index=No
     N.check(N.load().bspde_eval_points(N.ptr(c3), _i64(c3.stride()), npts, nt, N.ptr(it),
                                        N.ptr(wt_), N.ptr(out), N.stream_handle()))
     return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# "l2" prefilter (ProblemSpec(prefilter="l2"); _l2_project_axis,
+# problem.py:142-175): per axis, the projection of the piecewise-linear
+# interpolant onto the degree-n spline space -- rhs through the (1, n) cross
+# table (terms falling off the line are dropped), then the Gram system of the
+# sampled beta^(2n+1) with mirror folding.  On the GPU: the FIR is one
+# bspde_resample_axis launch, the solve one bspde_banded_solve_lines launch
+# with banded LU factors (no pivoting; shared by every line) from the host.
+
+
+@lru_cache(maxsize=None)
+def l2_cross(degree: int) -> np.ndarray:
+    """``r[o] = int beta^1(x - o) beta^n(x) dx`` for o = -R..R (exact)."""
+    from .gram import multi_product_integral
+
+    R = (degree + 3) // 2
+    taps = [float(multi_product_integral([(1, o, 0), (int(degree), 0, 0)]))
+            for o in range(-R, R + 1)]
+    while taps and taps[0] == 0.0 and taps[-1] == 0.0:
+        taps = taps[1:-1]
+    return np.array(taps)
+
+
+@lru_cache(maxsize=None)
+def l2_factors(n: int, degree: int):
+    """(lb, ub, m): banded LU of the mirror-folded Gram matrix of the sampled
+    beta^(2 degree + 1) on a line of n samples."""
+    gd = 2 * int(degree) + 1
+    m = gd // 2
+    if n < m + 1:
+        raise ValidationError(f"line of {n} samples too short for the l2 prefilter of degree "
+                              f"{degree} (need >= {m + 1})")
+    g = bspline_eval(gd, np.arange(-m, m + 1).astype(float))
+    A = np.zeros((n, n))
+    for t in range(-m, m + 1):
+        j = np.arange(n) + t
+        j = np.where(j < 0, -j, np.where(j >= n, 2 * n - 2 - j, j))
+        np.add.at(A, (np.arange(n), j), g[t + m])
+    U, lb = A.copy(), np.zeros((n, m))
+    for k in range(n):
+        hi = min(n, k + m + 1)
+        for i in range(k + 1, hi):
+            f = U[i, k] / U[k, k]
+            lb[i, i - k - 1] = f
+            U[i, k:hi] -= f * U[k, k:hi]
+    ub = np.zeros((n, m + 1))
+    for k in range(m + 1):
+        ub[: n - k, k] = np.diagonal(U, k)
+    return lb, ub, m
+
+
+def l2_project_device(t, degree, ndim=None, stream=None):
+    """In place: the "l2" prefilter along the last ``ndim`` axes of the dense
+    CUDA tensor ``t`` (first real axis first, like the reference).  Runs on
+    the current stream (``stream`` must be None or the current stream: the
+    per-axis tables are uploaded there)."""
+    torch = _torch()
+    lib = N.load()
+    ndim = t.dim() if ndim is None else int(ndim)
+    cross = l2_cross(int(degree))
+    rw = (len(cross) - 1) // 2
+    cur = _as3(t)
+    for ax in range(3 - ndim, 3):
+        n = cur.shape[ax]
+        lb, ub, m = l2_factors(n, int(degree))
+        i = np.arange(n)[:, None] + (np.arange(len(cross)) - rw)[None, :]
+        w = np.where((i >= 0) & (i < n), cross[None, :], 0.0)
+        idx = np.clip(i, 0, n - 1).astype(np.int32)
+        it = torch.from_numpy(np.ascontiguousarray(idx)).to(cur.device)
+        wt = torch.from_numpy(np.ascontiguousarray(w)).to(cur.device)
+        out = torch.empty_like(cur)
+        N.check(lib.bspde_resample_axis(N.ptr(cur), _i64(cur.stride()), N.ptr(out),
+                                        _i32(out.shape), _i64(out.stride()), ax, N.ptr(it),
+                                        N.ptr(wt), len(cross), N.stream_handle(stream)))
+        lbt = torch.from_numpy(np.ascontiguousarray(lb)).to(cur.device)
+        ubt = torch.from_numpy(np.ascontiguousarray(ub)).to(cur.device)
+        a, b = sorted((q for q in range(3) if q != ax), key=lambda q: out.stride(q))
+        N.check(lib.bspde_banded_solve_lines(N.ptr(out), n, out.stride(ax), out.shape[a],
+                                             out.shape[b], out.stride(a), out.stride(b),
+                                             N.ptr(lbt), N.ptr(ubt), m,
+                                             N.stream_handle(stream)))
+        cur = out
+    _as3(t).copy_(cur)
+    return t

@@ -443,6 +443,23 @@ def lowdim_cases():
     np.savez_compressed(os.path.join(OUT, "lowdim.npz"), **out)
 
 
+def l2_cases():
+    """transform_field(prefilter="l2") (problem.py:142-194): 1-3 d, degrees 2..5."""
+    from bspde.problem import transform_field as ref_transform_field
+
+    out = {}
+    rng = np.random.default_rng(2020)
+    for tag, shape, deg in (("l2_1d_p2", (19,), 2), ("l2_2d_p3", (11, 9), 3),
+                            ("l2_3d_p3", (8, 9, 10), 3), ("l2_2d_p5", (12, 13), 5),
+                            ("l2_3d_p4", (9, 8, 10), 4), ("l2_1d_p5", (6,), 5)):
+        grid = Grid(shape, tuple(0.1 * (a + 1) for a in range(len(shape))))
+        samples = rng.normal(size=shape)
+        coeffs = ref_transform_field(samples, grid, deg, basis_extension(deg), prefilter="l2")
+        out.update({f"{tag}_samples": samples, f"{tag}_coeffs": coeffs,
+                    f"{tag}_meta": np.array([deg, len(shape)] + list(shape))})
+    np.savez_compressed(os.path.join(OUT, "l2.npz"), **out)
+
+
 TRANSFORM_CASES = [
     # (tag, shape, p, extension)
     ("1d_p2_mirror", (17,), 2, "mirror"), ("1d_p3_replicate", (17,), 3, "replicate"),
@@ -561,8 +578,10 @@ def heat(ncoef, steps, fname, strategy="sparse", keep_all=True):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "indirect", "lowdim", "heat16",
+    which = sys.argv[1:] or ["gram", "apply", "rhs", "faces", "varcoef", "transform", "tbsf", "mask", "coarse", "indirect", "lowdim", "l2", "heat16",
                              "heat64"]
+    if "l2" in which:
+        l2_cases()
     if "lowdim" in which:
         lowdim_cases()
     if "indirect" in which:

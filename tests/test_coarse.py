@@ -48,7 +48,7 @@ def test_spec_validation():
     with pytest.raises(ValidationError):
         ProblemSpec(domain=BoxDomain(g), basis_degree=3, precision="f16")
     with pytest.raises(ConfigurationError):
-        ProblemSpec(domain=BoxDomain(g), basis_degree=3, prefilter="l2")
+        ProblemSpec(domain=BoxDomain(g), basis_degree=3, precision="f32")
     s = ProblemSpec(domain=BoxDomain(g), basis_degree=3)
     assert s.param_degree == 3 and s.source_degree == 3 and s.default_epsilon() == 1e-4
 
@@ -116,3 +116,30 @@ def test_coarsen_mask_matches_reference(k):
     got = _coarsen_mask(GOLD[f"cm{k}_fine"], Grid(tuple(c + 1 for c in want.shape),
                                                   (1.0,) * want.ndim))
     assert np.array_equal(got, want)
+
+
+L2 = np.load(os.path.join(os.path.dirname(__file__), "golden", "l2.npz"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", sorted({k.rsplit("_", 1)[0] for k in L2.keys()}))
+def test_l2_prefilter_matches_reference(tag):
+    from paper_1904_03057_b200.transform import transform_field
+
+    meta = L2[f"{tag}_meta"]
+    deg, dim = int(meta[0]), int(meta[1])
+    shape = tuple(int(v) for v in meta[2:2 + dim])
+    grid = Grid(shape, tuple(0.1 * (a + 1) for a in range(dim)))
+    got = transform_field(L2[f"{tag}_samples"], grid, deg, prefilter="l2")
+    # the folded Gram of the sampled beta^(2n+1) has condition 47 (n = 4) and
+    # 116 (n = 5) per axis: pivoted LAPACK (reference) and the banded LU differ
+    # by ~eps * cond^dim there
+    assert rel(got, L2[f"{tag}_coeffs"]) <= (1e-13 if deg <= 3 else 1e-10)
+
+
+def test_l2_factors_reject_short_lines():
+    from paper_1904_03057_b200.errors import ValidationError
+    from paper_1904_03057_b200.transform import l2_factors
+
+    with pytest.raises(ValidationError):
+        l2_factors(5, 5)
