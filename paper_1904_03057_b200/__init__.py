@@ -16,7 +16,8 @@ from .errors import (ConditioningWarning, ConfigurationError, DegreeError, Deter
                      ResourceError, ValidationError)
 from .gram import GramFactor, basis_extension, edge_width, gram_factor, min_axis_length
 from .heat import HeatProblem, HeatSolver, heat_solve
-from .io import read_field, read_tensor, write_field, write_tensor
+from .io import (export_vtk, read_field, read_mask, read_tensor, write_field, write_mask,
+                 write_tensor)
 from .problem import ProblemSpec, Solution, assemble_system, coarse_initialize, solve_problem
 from .operator import B200Operator, OpStats, assembled_rhs, make_operator
 from .solver import SolveConfig, SolveReport, pcg, pcg_device
@@ -32,7 +33,8 @@ __all__ = [
     "HeatProblem", "HeatSolver", "heat_solve",
     "direct_transform", "transform_field", "sample_solution",
     "ProblemSpec", "Solution", "assemble_system", "coarse_initialize", "solve_problem",
-    "read_tensor", "write_tensor", "read_field", "write_field", "FormatError", "EmptyDomainError", "OutOfDomainError",
+    "read_tensor", "write_tensor", "read_field", "write_field", "read_mask", "write_mask",
+    "export_vtk", "FormatError", "EmptyDomainError", "OutOfDomainError",
     "ConditioningWarning", "ConfigurationError", "DegreeError", "DeterminismError",
     "DivergenceError", "IndefiniteOperatorError", "NativeLibraryError", "ResourceError",
     "ValidationError",

@@ -165,4 +165,64 @@ def read_field(path, layout, device, buf=None, degree=None):
     return buf, deg
 
 
-__all__ = ["TBSF_MAGIC", "TBSF_VERSION", "write_tensor", "read_tensor", "write_field", "read_field"]
+# ---------------------------------------------------------------------------
+# mask volumes and VTK export (io.py:85-144): the input and output formats of
+# the masked (CT-leg) runs
+
+MASK_MAGIC = "TBSM"
+
+
+def write_mask(path, volume, threshold=128):
+    """Mask file: ``TBSM v1`` / ``extents ...`` / ``threshold t`` text lines,
+    then the raw uint8 volume (C order)."""
+    vol = np.ascontiguousarray(volume, dtype=np.uint8)
+    head = (f"{MASK_MAGIC} v1\nextents {' '.join(str(e) for e in vol.shape)}\n"
+            f"threshold {int(threshold)}\n").encode()
+    _atomic(path, lambda f: (f.write(head), f.write(memoryview(vol).cast("B"))))
+
+
+def read_mask(path):
+    """``(occupancy, threshold)``: the volume thresholded at ``>= threshold``."""
+    with open(path, "rb") as f:
+        blob = f.read()
+    k = blob.find(b"threshold")
+    end = blob.find(b"\n", k) + 1 if k >= 0 else 0
+    if k < 0 or end == 0:
+        raise FormatError("missing mask header lines", offset=0)
+    lines = blob[:end].decode(errors="replace").splitlines()
+    if not lines[0].startswith(MASK_MAGIC):
+        raise FormatError(f"bad mask magic {lines[0][:8]!r}", offset=0)
+    extents = tuple(int(t) for t in lines[1].split()[1:])
+    threshold = int(lines[2].split()[1])
+    want = int(np.prod(extents))
+    if len(blob) - end != want:
+        raise FormatError(f"mask payload holds {len(blob) - end} bytes, extents {extents} "
+                          f"require {want}", offset=end)
+    vol = np.frombuffer(blob, dtype=np.uint8, count=want, offset=end).reshape(extents)
+    return vol >= threshold, threshold
+
+
+def export_vtk(path, samples, grid, name="field"):
+    """Legacy ASCII VTK STRUCTURED_POINTS of a 2-D / 3-D node field (array
+    axis 0 is VTK's x, so values go out in Fortran order)."""
+    from .errors import ValidationError
+
+    arr = np.asarray(samples, dtype=float)
+    if arr.ndim not in (2, 3):
+        raise ValidationError(f"VTK export needs a 2-D or 3-D field, got {arr.ndim}-D")
+    pad = 3 - arr.ndim
+    dims = arr.shape + (1,) * pad
+    spacing = tuple(grid.step) + (1.0,) * pad
+    origin = tuple(grid.origin) + (0.0,) * pad
+    head = ["# vtk DataFile Version 3.0", name, "ASCII", "DATASET STRUCTURED_POINTS",
+            "DIMENSIONS {} {} {}".format(*dims),
+            "ORIGIN {:.10g} {:.10g} {:.10g}".format(*origin),
+            "SPACING {:.10g} {:.10g} {:.10g}".format(*spacing),
+            f"POINT_DATA {arr.size}", f"SCALARS {name} double 1", "LOOKUP_TABLE default"]
+    body = "\n".join(f"{v:.10e}" for v in arr.ravel(order="F"))
+    text = "\n".join(head) + "\n" + body + ("\n" if arr.size else "")
+    _atomic(path, lambda f: f.write(text.encode()))
+
+
+__all__ = ["TBSF_MAGIC", "TBSF_VERSION", "write_tensor", "read_tensor", "write_field", "read_field",
+           "MASK_MAGIC", "write_mask", "read_mask", "export_vtk"]

@@ -509,6 +509,16 @@ def tbsf_cases():
         n = int(np.prod(shape))
         arr = (np.arange(n, dtype=np.float64) * 0.37 - 1.5).reshape(shape).astype(dtype)
         write_tensor(os.path.join(d, name + ".tbsf"), arr, degree=deg)
+    # mask volume and VTK export files (io.py:85-144)
+    from bspde.io import export_vtk, write_mask
+
+    vol = (np.arange(4 * 5 * 6) * 7 % 256).astype(np.uint8).reshape(4, 5, 6)
+    write_mask(os.path.join(d, "vol_4x5x6.tbsm"), vol, threshold=100)
+    f3 = (np.arange(24, dtype=np.float64).reshape(3, 4, 2) - 7.5) / 3.0
+    export_vtk(os.path.join(d, "field3.vtk"), f3, Grid((3, 4, 2), (0.5, 1.0, 2.0), (1.0, -2.0, 0.25)),
+               name="temp")
+    f2 = np.cos(np.arange(12, dtype=np.float64)).reshape(3, 4)
+    export_vtk(os.path.join(d, "field2.vtk"), f2, Grid((3, 4), (0.5, 1.0)))
 
 
 def heat_inputs(ncoef, p=3, lam=4.0):

@@ -147,3 +147,50 @@ def test_heat_solver_save_restore_continues_bitwise(tmp_path):
     s2.restore(p)
     s2.run(2)
     assert np.array_equal(s2.coefficients(), ref.coefficients())
+
+
+# ---------------------------------------------------------------- mask / VTK
+def test_mask_file_roundtrip_and_reference_bytes(tmp_path):
+    from paper_1904_03057_b200.io import read_mask, write_mask
+
+    vol = (np.arange(4 * 5 * 6) * 7 % 256).astype(np.uint8).reshape(4, 5, 6)
+    occ, thr = read_mask(os.path.join(GOLD, "vol_4x5x6.tbsm"))
+    assert thr == 100 and np.array_equal(occ, vol >= 100)
+    p = tmp_path / "m.tbsm"
+    write_mask(p, vol, threshold=100)
+    with open(os.path.join(GOLD, "vol_4x5x6.tbsm"), "rb") as f:
+        assert p.read_bytes() == f.read()
+
+
+def test_mask_file_errors(tmp_path):
+    from paper_1904_03057_b200.io import read_mask, write_mask
+
+    p = tmp_path / "m.tbsm"
+    write_mask(p, np.ones((3, 3), dtype=np.uint8))
+    p.write_bytes(p.read_bytes() + b"\1")
+    with pytest.raises(FormatError):
+        read_mask(p)
+    p.write_bytes(b"TBSM v1\nextents 2 2\n")
+    with pytest.raises(FormatError) as exc:
+        read_mask(p)
+    assert exc.value.offset == 0
+    p.write_bytes(b"NOPE v1\nextents 1\nthreshold 1\n\1")
+    with pytest.raises(FormatError):
+        read_mask(p)
+
+
+def test_vtk_export_matches_reference_text(tmp_path):
+    from paper_1904_03057_b200.domain import Grid
+    from paper_1904_03057_b200.errors import ValidationError
+    from paper_1904_03057_b200.io import export_vtk
+
+    f3 = (np.arange(24, dtype=np.float64).reshape(3, 4, 2) - 7.5) / 3.0
+    export_vtk(tmp_path / "a.vtk", f3, Grid((3, 4, 2), (0.5, 1.0, 2.0), (1.0, -2.0, 0.25)),
+               name="temp")
+    f2 = np.cos(np.arange(12, dtype=np.float64)).reshape(3, 4)
+    export_vtk(tmp_path / "b.vtk", f2, Grid((3, 4), (0.5, 1.0)))
+    for mine, ref in (("a.vtk", "field3.vtk"), ("b.vtk", "field2.vtk")):
+        with open(os.path.join(GOLD, ref)) as f:
+            assert (tmp_path / mine).read_text() == f.read()
+    with pytest.raises(ValidationError):
+        export_vtk(tmp_path / "c.vtk", np.zeros(4), Grid((4,), (1.0,)))
