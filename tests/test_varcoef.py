@@ -5,7 +5,6 @@ import numpy as np
 import pytest
 
 from paper_1904_03057_b200 import BoxDomain, Grid, SolveConfig, build_system, make_operator, pcg
-from paper_1904_03057_b200.errors import ConfigurationError
 from paper_1904_03057_b200.gram import basis_extension, edge_width, trilinear_tables
 from paper_1904_03057_b200.varcoef import VarSystemData
 
@@ -49,9 +48,9 @@ def test_variable_fields_build_var_system():
     df = build_system(dom, 3, 3, 1.0 + np.random.default_rng(0).random(shp), 1.0,
                       [(0, 0, 1.0, 2.0)])
     assert len(df.faces) == 1 and df.face_rhs().shape == d.cext
-    with pytest.raises(ConfigurationError):
-        build_system(BoxDomain(Grid((9, 10), (0.5, 1.0))), 3, 3,
-                     1.0 + np.random.default_rng(0).random((11, 12)), 1.0, [])
+    d2 = build_system(BoxDomain(Grid((9, 10), (0.5, 1.0))), 3, 3,
+                      1.0 + np.random.default_rng(0).random((11, 12)), 1.0, [])
+    assert isinstance(d2, VarSystemData) and d2.cext == (11, 12)  # 2-D: unit leading axis
 
 
 def _op(golden, tag):
