@@ -440,6 +440,27 @@ def lowdim_cases():
                     f"{tag}_its": np.array([rep.iterations])})
         print(tag, rep.iterations, flush=True)
     out.update({"m2d_mask": disk, "m2d3_mask": ring, "m1d_mask": line})
+    # 2-D mask heat steps (reference composition, penalty on the exposed faces)
+    p, dt, w, val = 2, 0.02, 40.0, 1.0
+    dom = MaskDomain(g2, disk)
+    shp = tuple(n + 2 * basis_extension(p) for n in g2.extents)
+    kappa = 0.5 + rng.random(shp)
+    A = make_operator(build_system(dom, p, p, dt * kappa, np.ones(shp), [(0, 0, w * dt, val)]),
+                      "sparse")
+    Md = build_system(dom, p, p, np.zeros(shp), np.ones(shp), [])
+    M = make_operator(Md, "sparse")
+    u0 = rng.normal(size=shp)
+    q = rng.normal(size=shp)
+    F = assembled_rhs(Md, p, q)
+    G = assembled_rhs(A.data, p, np.zeros(shp))
+    u, its, sols = u0.copy(), [], []
+    for _ in range(3):
+        u, rep = pcg(A, M.apply(u) + dt * F + G, SolveConfig(tol=1e-12, max_iter=5000), x0=u)
+        its.append(rep.iterations)
+        sols.append(u.copy())
+    out.update({"heat2d_kappa": kappa, "heat2d_u0": u0, "heat2d_q": q,
+                "heat2d_its": np.array(its), "heat2d_u": np.stack(sols)})
+    print("heat2d", its, flush=True)
     np.savez_compressed(os.path.join(OUT, "lowdim.npz"), **out)
 
 

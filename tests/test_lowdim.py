@@ -54,3 +54,18 @@ def test_apply_diag_rhs_pcg(tag):
     its = int(GOLD[f"{tag}_its"][0])
     assert rep.converged and abs(rep.iterations - its) <= max(1, its // 100)
     assert rel(x, GOLD[f"{tag}_x"]) <= 1e-7
+
+
+@pytest.mark.gpu
+def test_heat_steps_on_2d_mask():
+    from paper_1904_03057_b200 import DirichletPenalty, HeatProblem, HeatSolver
+    from paper_1904_03057_b200.solver import SolveConfig
+
+    prob = HeatProblem(grid=G2, degree=2, dt=0.02, conductivity=GOLD["heat2d_kappa"],
+                       initial_coeffs=GOLD["heat2d_u0"], source_coeffs=GOLD["heat2d_q"],
+                       bc=DirichletPenalty(1.0, 1.0 / 40.0), mask=GOLD["m2d_mask"])
+    hs = HeatSolver(prob, SolveConfig(tol=1e-12, max_iter=5000))
+    for k, its in enumerate(GOLD["heat2d_its"]):
+        rep = hs.step()
+        assert rep.converged and abs(rep.iterations - int(its)) <= max(1, int(its) // 100)
+        assert rel(hs.coefficients(), GOLD["heat2d_u"][k]) <= 1e-9
