@@ -9,7 +9,8 @@ Per CG iteration (``distributed_pcg``):
 
   1. halo exchange of r and p_{k-1}: the first/last p owned planes go to the
      lower/upper neighbour's ghost planes (contiguous memory: one send + one
-     recv per side, ``torch.distributed.batch_isend_irecv`` over NCCL);
+     recv per side and buffer, both buffers in one
+     ``torch.distributed.batch_isend_irecv`` group over NCCL);
   2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
      and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
      finalize kernel runs the scalar update on every rank;
@@ -92,19 +93,24 @@ class HaloExchanger:
         self.world = world
         self.group = group
 
-    def __call__(self, buf):
+    def __call__(self, *bufs):
+        """Exchange the ghost planes of every buffer in ``bufs`` in ONE
+        batched P2P group (the CG loop passes r and p_{k-1} together, so an
+        iteration pays one group launch / NVLink round trip, not two)."""
         if self.world == 1:
             return
         import torch.distributed as dist
 
         g, nz = self.layout.ghost, self.layout.nz
         ops = []
-        if self.rank > 0:  # lower neighbour: my first g planes <-> its top ghosts
-            ops.append(dist.P2POp(dist.isend, buf[g:2 * g], self.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, buf[0:g], self.rank - 1, self.group))
-        if self.rank < self.world - 1:  # upper neighbour
-            ops.append(dist.P2POp(dist.isend, buf[nz:nz + g], self.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, buf[nz + g:nz + 2 * g], self.rank + 1, self.group))
+        for buf in bufs:
+            if self.rank > 0:  # lower neighbour: my first g planes <-> its top ghosts
+                ops.append(dist.P2POp(dist.isend, buf[g:2 * g], self.rank - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, buf[0:g], self.rank - 1, self.group))
+            if self.rank < self.world - 1:  # upper neighbour
+                ops.append(dist.P2POp(dist.isend, buf[nz:nz + g], self.rank + 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, buf[nz + g:nz + 2 * g], self.rank + 1,
+                                      self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
@@ -172,8 +178,7 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
     while active:
         for _ in range(K):
             p_in, p_out = pring[(k - 1) % R], pring[k % R]
-            halo(r)
-            halo(p_in)
+            halo(r, p_in)
             ops.pass_a(r, p_in, p_out, ap, scratch)
             allreduce(ops.sums(scratch, 1))
             ops.finalize(scratch, 1)
