@@ -156,6 +156,16 @@ int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
 int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
                     double* p_out, double* ap, void* scratch, int fuse,
                     void* stream);
+/* Pass A restricted to the owned output planes [z_begin, z_begin + z_count)
+ * (local indices; it streams the p planes either side).  accumulate = 1 adds
+ * the range's <p,Ap> to the sums instead of overwriting them.  The z-slab
+ * driver runs the interior range [p, nz - p) -- which reads no ghost plane --
+ * while the NCCL halo exchange is in flight, then the two boundary ranges
+ * (overlap the halo with the interior apply).  The reference
+ * analogue is a worker's window of blocks (operator.py:61-74). */
+int bspde_cg_pass_a_range(bspde_plan* plan, const double* r, const double* p_in,
+                          double* p_out, double* ap, void* scratch, int z_begin,
+                          int z_count, int accumulate, int fuse, void* stream);
 /* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p for the last
  * BSPDE_P_RING iterations at once every BSPDE_P_RING-th call, in the
  * reference's rounding order (solver.py:94-101).  Iteration k's pass A must

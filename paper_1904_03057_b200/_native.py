@@ -129,6 +129,8 @@ SIGNATURES = [
     ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_a_range", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, _VP]),
     ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_stencil_create", C.c_int, [C.POINTER(StencilDesc), C.POINTER(C.c_void_p)]),

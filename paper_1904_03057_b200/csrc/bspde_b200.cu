@@ -118,6 +118,7 @@ struct SepParams {
   long long pitch_y, pitch_z;
   int ew[3];
   int tiles_x, tiles_y, nchunks, chunk_len, nitems;
+  int z_begin, z_end;  // owned output planes [z_begin, z_end) this launch produces
   int main_items, tail_split, sub_len;  // items >= main_items: tail chunks split tail_split ways
   int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
@@ -134,6 +135,7 @@ struct SepParams {
   unsigned* counter;
   CgState* state;
   int fuse;
+  int accumulate;  // 1: add this launch's sums to the state's (a z-ranged piece)
 };
 
 // BSPDE_ALL_EDGE=1 (measurement build): every tile takes the edge-tile
@@ -327,7 +329,7 @@ __global__ void finalize_kernel(CgState* s, int kind) {
 template <int NV, int NWARP>
 __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_last_p,
                                     double* partials, unsigned* counter, CgState* st, int fuse,
-                                    int kind) {
+                                    int kind, int accumulate = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -368,7 +370,7 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
     }
     if (lane == 0) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i) st->sums[i] = tot[i];
+      for (int i = 0; i < NV; ++i) st->sums[i] = accumulate ? st->sums[i] + tot[i] : tot[i];
       if (fuse) finalize_state(st, kind);
       *counter = 0u;
       __threadfence();
@@ -421,8 +423,8 @@ __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
   ItemGeom g;
   g.x0 = (t % prm.tiles_x) * TX;
   g.y0 = (t / prm.tiles_x) * TY;
-  const int c0 = ch * prm.chunk_len;
-  const int c1 = min(c0 + prm.chunk_len, prm.nz);
+  const int c0 = prm.z_begin + ch * prm.chunk_len;
+  const int c1 = min(c0 + prm.chunk_len, prm.z_end);
   const bool tail = item >= prm.main_items;
   g.zc0 = tail ? min(c0 + sub * len, c1) : c0;   // an empty sub-chunk streams only its
   g.zc1 = tail ? min(g.zc0 + len, c1) : c1;      // 2p warm-up planes
@@ -899,7 +901,8 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 
   if (MODE == M_CGA) {
     double v[1] = {dsum[0]};
-    reduce_and_finalize<1, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 1);
+    reduce_and_finalize<1, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 1,
+                               prm.accumulate);
   } else if (MODE == M_RESID) {
     double v[3] = {dsum[0], dsum[1], dsum[2]};
     reduce_and_finalize<3, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 0);
@@ -1424,7 +1427,8 @@ struct bspde_plan {
   cudaStream_t work = nullptr;    // private stream: CUDA graphs cannot be captured on
   cudaEvent_t ev_in = nullptr;    // the legacy default stream the caller may use
   cudaEvent_t ev_out = nullptr;
-  std::map<int, Launch> launch_cache;  // per kernel mode (plan_launch is a simulation)
+  // per (kernel mode, planes streamed): plan_launch is a simulation
+  std::map<std::pair<int, int>, Launch> launch_cache;
 };
 
 namespace {
@@ -1476,12 +1480,11 @@ KernelInfo kernel_for(int p, int mode) {
 // without splitting the ragged last wave.  The plan is simulated exactly.
 constexpr double kEdgeTileWeight = 1.08;  // edge-tile plane cost / interior (B200, p=3, measured)
 
-Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki) {
+Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki, int nz) {
   const int TY = tile_h_of(pl->p);
   const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
   const int tiles = tx * ty;
   const int slots = std::max(1, pl->num_sms * ki.ctas_per_sm);
-  const int nz = pl->d.nz;
   const int p = pl->p, px = p + (p & 1);
   if (const char* fc = getenv("BSPDE_FORCE_CHUNKS")) {  // debug / tuning override
     const int nc = std::max(1, std::min(nz, atoi(fc)));
@@ -1575,6 +1578,9 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
   sp.nx = d.nx;
   sp.ny = d.ny;
   sp.nz = d.nz;
+  sp.z_begin = 0;
+  sp.z_end = d.nz;
+  sp.accumulate = 0;
   sp.nz_glob = d.nz_global;
   sp.z_off = d.z_offset;
   sp.ghost = p;
@@ -1626,11 +1632,14 @@ unsigned* scratch_counter(void* s) {
 
 int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, double* out,
                const double* aux, double aux_scale, double c_mass_override, bool use_override,
-               void* scratch, int fuse, cudaStream_t st, double* cg_pout = nullptr) {
+               void* scratch, int fuse, cudaStream_t st, double* cg_pout = nullptr,
+               int z_begin = 0, int z_count = -1, int accumulate = 0) {
   KernelInfo ki = kernel_for(pl->p, mode);
-  auto lit = pl->launch_cache.find(mode);
+  if (z_count < 0) z_count = pl->d.nz - z_begin;
+  const auto key = std::make_pair(mode, z_count);
+  auto lit = pl->launch_cache.find(key);
   if (lit == pl->launch_cache.end()) {
-    lit = pl->launch_cache.emplace(mode, plan_launch(pl, ki)).first;
+    lit = pl->launch_cache.emplace(key, plan_launch(pl, ki, z_count)).first;
     if (getenv("BSPDE_PLAN_DEBUG"))
       fprintf(stderr, "bspde plan: mode %d grid %d chunks %d len %d items %d main %d split %d\n", mode,
               lit->second.grid, lit->second.nchunks, lit->second.chunk_len, lit->second.nitems,
@@ -1658,6 +1667,9 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
     sp.counter = scratch_counter(scratch);
   }
   sp.fuse = fuse;
+  sp.z_begin = z_begin;
+  sp.z_end = z_begin + z_count;
+  sp.accumulate = accumulate;
   if (ln.grid > MAXGRID) return fail(BSPDE_ERR_STATE, "grid exceeds MAXGRID");
   CUtensorMap m0, m1;
   int rc = make_map(&m0, pl, in0);
@@ -2124,6 +2136,18 @@ int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p_in, double*
   if (p_in == p_out) return fail(BSPDE_ERR_ARG, "p_in and p_out must be different buffers");
   return launch_sep(pl, M_CGA, r, p_in, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
                     (cudaStream_t)stream, p_out);
+}
+
+int bspde_cg_pass_a_range(bspde_plan* pl, const double* r, const double* p_in, double* p_out,
+                          double* ap, void* scratch, int z_begin, int z_count, int accumulate,
+                          int fuse, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  if (p_in == p_out) return fail(BSPDE_ERR_ARG, "p_in and p_out must be different buffers");
+  if (z_begin < 0 || z_count < 1 || z_begin + z_count > pl->d.nz)
+    return fail(BSPDE_ERR_ARG, "z range outside the owned planes");
+  return launch_sep(pl, M_CGA, r, p_in, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
+                    (cudaStream_t)stream, p_out, z_begin, z_count, accumulate ? 1 : 0);
 }
 
 int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, const double* p_ring,

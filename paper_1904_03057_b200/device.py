@@ -190,6 +190,14 @@ class NativePlan:
                                          N.ptr(ap), N.ptr(scratch), int(fuse),
                                          N.stream_handle(stream)))
 
+    def cg_pass_a_range(self, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate, fuse=0,
+                        stream=None):
+        """Pass A on the owned output planes [z_begin, z_begin + z_count)."""
+        N.check(self.lib.bspde_cg_pass_a_range(self.handle, N.ptr(r), N.ptr(p_in), N.ptr(p_out),
+                                               N.ptr(ap), N.ptr(scratch), int(z_begin),
+                                               int(z_count), int(bool(accumulate)), int(fuse),
+                                               N.stream_handle(stream)))
+
     def cg_pass_b(self, x, r, pring, ap, scratch, fuse, stream=None):
         N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(pring),
                                          N.ptr(ap), N.ptr(scratch), int(fuse),

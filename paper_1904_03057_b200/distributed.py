@@ -11,6 +11,9 @@ Per CG iteration (``distributed_pcg``):
      lower/upper neighbour's ghost planes (contiguous memory: one send + one
      recv per side and buffer, both buffers in one
      ``torch.distributed.batch_isend_irecv`` group over NCCL);
+     The exchange is posted first and pass A's interior output planes
+     [p, nz - p), which read no ghost plane, run while it is in flight
+     (``bspde_cg_pass_a_range``); the 2 x p boundary planes follow;
   2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
      and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
      finalize kernel runs the scalar update on every rank;
@@ -30,6 +33,7 @@ product implementation is ``NativeSlabOps`` (the sm_100a kernels).
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -97,8 +101,20 @@ class HaloExchanger:
         """Exchange the ghost planes of every buffer in ``bufs`` in ONE
         batched P2P group (the CG loop passes r and p_{k-1} together, so an
         iteration pays one group launch / NVLink round trip, not two)."""
+        self.wait(self.start(*bufs))
+
+    @staticmethod
+    def wait(works):
+        """Complete a started exchange (NCCL: the current stream waits on the
+        transfer; gloo: the host blocks)."""
+        for req in works:
+            req.wait()
+
+    def start(self, *bufs):
+        """Post the exchange and return its work handles without waiting, so
+        kernels that read no ghost plane can run while it is in flight."""
         if self.world == 1:
-            return
+            return []
         import torch.distributed as dist
 
         g, nz = self.layout.ghost, self.layout.nz
@@ -111,9 +127,7 @@ class HaloExchanger:
                 ops.append(dist.P2POp(dist.isend, buf[nz:nz + g], self.rank + 1, self.group))
                 ops.append(dist.P2POp(dist.irecv, buf[nz + g:nz + 2 * g], self.rank + 1,
                                       self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
 
 
 def _allreduce_fn(world, group=None):
@@ -145,6 +159,9 @@ class NativeSlabOps:
     def pass_a(self, r, p_in, p_out, ap, scratch):
         self.plan.cg_pass_a(r, p_in, p_out, ap, scratch, 0)
 
+    def pass_a_range(self, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate):
+        self.plan.cg_pass_a_range(r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate, 0)
+
     def pass_b(self, x, r, pring, ap, scratch):
         self.plan.cg_pass_b(x, r, pring, ap, scratch, 0)
 
@@ -158,11 +175,28 @@ class NativeSlabOps:
         return self.plan.cg_read(scratch)
 
 
+def _overlap_enabled(ops, halo):
+    """Interior/boundary split of pass A around the halo exchange: needs more
+    than one rank, an ops object with ranged pass A, and an interior range."""
+    if os.environ.get("BSPDE_HALO_OVERLAP", "1") == "0" or halo.world == 1:
+        return False
+    lay = halo.layout
+    return hasattr(ops, "pass_a_range") and lay.nz > 2 * lay.ghost
+
+
 def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: SolveConfig,
                     has_x0=True, history=None):
     """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
-    ``pring`` holds the ring of search directions (leading axis)."""
+    ``pring`` holds the ring of search directions (leading axis).
+
+    With more than one rank, pass A of every iteration is split around the
+    halo exchange of r and p_{k-1}: the exchange is posted, the interior
+    output planes [g, nz - g) (which read no ghost plane) are computed while it
+    is in flight, then the two g-plane boundary ranges after it lands, their
+    <p,Ap> added to the interior's."""
     t0 = time.perf_counter()
+    overlap = _overlap_enabled(ops, halo)
+    g, nz = halo.layout.ghost, halo.layout.nz
     if not has_x0:
         x.zero_()
     R = pring.shape[0]
@@ -178,8 +212,15 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
     while active:
         for _ in range(K):
             p_in, p_out = pring[(k - 1) % R], pring[k % R]
-            halo(r, p_in)
-            ops.pass_a(r, p_in, p_out, ap, scratch)
+            if overlap:
+                works = halo.start(r, p_in)
+                ops.pass_a_range(r, p_in, p_out, ap, scratch, g, nz - 2 * g, False)
+                halo.wait(works)
+                ops.pass_a_range(r, p_in, p_out, ap, scratch, 0, g, True)
+                ops.pass_a_range(r, p_in, p_out, ap, scratch, nz - g, g, True)
+            else:
+                halo(r, p_in)
+                ops.pass_a(r, p_in, p_out, ap, scratch)
             allreduce(ops.sums(scratch, 1))
             ops.finalize(scratch, 1)
             ops.pass_b(x, r, pring, ap, scratch)

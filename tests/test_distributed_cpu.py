@@ -75,6 +75,23 @@ class CpuSlabOps:
         self._own(ap).copy_(apv)
         scratch[0] = float((pn[g:g + nz] * apv).sum())
 
+    def pass_a_range(self, r, p_in, p_out, ap, scratch, z0, cnt, accumulate):
+        """bspde_cg_pass_a_range: only owned planes [z0, z0 + cnt) are
+        produced; the interior range is called while the ghosts are still in
+        flight, so outputs there must not depend on them (banded in z)."""
+        s = self.state
+        if not s["active"]:
+            return
+        g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
+        self.range_calls = getattr(self, "range_calls", 0) + 1
+        pn = r[:, :, :nx] * self.inv + s["beta"] * p_in[:, :, :nx]
+        apv = self._apply(torch.nn.functional.pad(pn, (0, p_in.shape[2] - nx)))
+        sl = slice(z0, z0 + cnt)
+        self._own(p_out)[sl] = pn[g:g + nz][sl]
+        self._own(ap)[sl] = apv[sl]
+        part = float((pn[g:g + nz][sl] * apv[sl]).sum())
+        scratch[0] = (float(scratch[0]) if accumulate else 0.0) + part
+
     def _apply_x(self, x, pring, upto, alphas):
         s = self.state
         R = pring.shape[0]
@@ -144,8 +161,8 @@ class CpuSlabOps:
         return rep, bool(self.state["active"])
 
 
-def _worker(rank, world, port, ext, p, out_q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, port, ext, p, out_q, overlap="1"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BSPDE_HALO_OVERLAP=overlap)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         step = tuple(1.0 / (n - 1) for n in ext)
@@ -185,7 +202,8 @@ def _worker(rank, world, port, ext, p, out_q):
             xo, ro = O.pcg(ora.apply, ora.jacobi_diagonal, b_full, tol=1e-13, max_iter=1000,
                            x0=x0_full)
             out_q.put((rep.iterations, ro["iterations"],
-                       float(np.linalg.norm(xs - xo) / np.linalg.norm(xo))))
+                       float(np.linalg.norm(xs - xo) / np.linalg.norm(xo)),
+                       getattr(ops, "range_calls", 0), lay.nz))
     finally:
         dist.destroy_process_group()
 
@@ -196,20 +214,28 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,ext", [(2, (13, 10, 11)), (3, (17, 9, 10))])
-def test_zslab_cg_matches_single_process(world, ext):
+@pytest.mark.parametrize("world,ext,overlap", [
+    (2, (13, 10, 11), "1"),   # 15 coefficient planes: slabs of 8 / 7, both split pass A
+    (3, (17, 9, 10), "1"),    # 19: 7 / 6 / 6, only rank 0 has an interior range (> 2p)
+    (3, (13, 9, 10), "1"),    # 15: 5 / 5 / 5, no interior range: whole-slab pass A
+    (2, (21, 9, 10), "0"),    # overlap disabled
+])
+def test_zslab_cg_matches_single_process(world, ext, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, 3, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, 3, q, overlap))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
         pr.join(timeout=240)
         assert pr.exitcode == 0
-    its, its_o, rel = q.get(timeout=10)
+    its, its_o, rel, range_calls, nz0 = q.get(timeout=10)
     assert abs(its - its_o) <= 1, (its, its_o)
     assert rel < 1e-10, rel
+    split = overlap == "1" and nz0 > 2 * 3  # rank 0's slab has an interior range
+    assert (range_calls > 0) == split, range_calls
 
 
 def test_partition_bounds():

@@ -546,3 +546,88 @@ def test_run_host_matches_device_stepping(golden, cuda_device):
     assert [r.iterations for r in reps] == its_a
     assert np.array_equal(host.numpy(), a.coefficients())
     assert np.array_equal(b.coefficients(), a.coefficients())
+
+
+@pytest.mark.parametrize("p,ext,world", [(3, (30, 19, 33), 2), (3, (31, 20, 21), 3),
+                                         (5, (32, 17, 19), 2), (1, (14, 12, 13), 2)])
+def test_pass_a_ranges_on_emulated_slabs(cuda_device, p, ext, world):
+    """Pass A split as the overlapped z-slab driver runs it (interior planes
+    [p, nz-p) first, then the two p-plane boundary ranges, sums accumulated)
+    on every slab of an emulated `world`-rank partition on ONE device, ghost
+    planes filled from the neighbours by plain copies: Ap and p_k must equal
+    the unsplit pass A bit for bit and match the global oracle; the summed
+    <p,Ap> the global one."""
+    import torch
+
+    from paper_1904_03057_b200.device import NativePlan, SlabLayout
+    from paper_1904_03057_b200.distributed import SlabPartition
+
+    step = tuple(1.0 / (n - 1) for n in ext)
+    data = build_system(BoxDomain(Grid(ext, step)), p, p, 0.01, 1.0, [])
+    ora = O.KronOperator(ext, step, p, 0.01, 1.0)
+    rng = np.random.default_rng(3)
+    r_full = rng.normal(size=data.cext)
+    q_full = rng.normal(size=data.cext)
+    inv = 1.0 / ora.jacobi_diagonal()
+    beta = 0.37
+    p_full = inv * r_full + beta * q_full
+    want_ap = ora.apply(p_full)
+    nzg, ny, nx = data.dims3
+    dots = []
+    for rank in range(world):
+        part = SlabPartition(nzg, world, rank)
+        lo, hi = part.bounds()
+        lay = SlabLayout(part.nz, ny, nx, ghost=p, z_offset=part.z_offset, nz_global=nzg)
+        assert lay.nz > 2 * p
+        plan = NativePlan(data, lay, cuda_device)
+
+        def slab(full):
+            buf = lay.alloc(cuda_device)
+            glo, ghi = max(lo - p, 0), min(hi + p, nzg)
+            src = torch.from_numpy(np.ascontiguousarray(full.reshape(nzg, ny, nx)[glo:ghi]))
+            buf[glo - (lo - p):ghi - (lo - p), :, :nx] = src.to(cuda_device)
+            return buf
+
+        rb, qb = slab(r_full), slab(q_full)
+        outs = []
+        for split in (False, True):
+            scratch = plan.scratch()
+            plan.cg_setup(scratch, None, 1e-300, 100, False, False)
+            scratch[48:56].view(torch.float64)[0] = beta  # CgState.beta
+            scratch[120:124].view(torch.int32)[0] = 1     # CgState.active (14 doubles, it, max_iter)
+            ap, pout = lay.alloc(cuda_device), lay.alloc(cuda_device)
+            pout.fill_(float("nan"))
+            if split:
+                nz = lay.nz
+                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, p, nz - 2 * p, False)
+                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, 0, p, True)
+                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, nz - p, p, True)
+            else:
+                plan.cg_pass_a(rb, qb, pout, ap, scratch, 0)
+            torch.cuda.synchronize()
+            outs.append((lay.download(ap), lay.download(pout),
+                         float(scratch[:8].view(torch.float64)[0])))
+        (a0, p0, d0), (a1, p1, d1) = outs
+        assert np.array_equal(a0, a1) and np.array_equal(p0, p1)
+        assert abs(d0 - d1) <= 1e-12 * abs(d0)
+        sl = (slice(lo, hi),)
+        assert relmax(a1, want_ap.reshape(nzg, ny, nx)[sl].reshape(a1.shape)) < 1e-13
+        assert relmax(p1, p_full.reshape(nzg, ny, nx)[sl].reshape(p1.shape)) < 1e-14
+        dots.append(d1)
+    want = float(np.vdot(p_full, want_ap))
+    assert abs(sum(dots) - want) <= 1e-11 * abs(want)
+
+
+def test_pass_a_range_rejects_bad_ranges(cuda_device):
+    from paper_1904_03057_b200.errors import NativeLibraryError  # noqa: F401
+
+    ext, p = (12, 12, 12), 3
+    step = tuple(1.0 / (n - 1) for n in ext)
+    data = build_system(BoxDomain(Grid(ext, step)), p, p, 0.01, 1.0, [])
+    op = make_operator(data, "b200")
+    lay, plan = op.layout, op.plan()
+    r, q, o, ap = (lay.alloc(op.device) for _ in range(4))
+    scratch = plan.scratch()
+    for z0, cnt in [(-1, 2), (0, 0), (lay.nz - 1, 2)]:
+        with pytest.raises(Exception, match="z range"):
+            plan.cg_pass_a_range(r, q, o, ap, scratch, z0, cnt, False)
