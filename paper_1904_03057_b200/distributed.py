@@ -11,9 +11,11 @@ Per CG iteration (``distributed_pcg``):
      lower/upper neighbour's ghost planes (contiguous memory: one send + one
      recv per side and buffer, both buffers in one
      ``torch.distributed.batch_isend_irecv`` group over NCCL);
-     The exchange is posted first and pass A's interior output planes
-     [p, nz - p), which read no ghost plane, run while it is in flight
-     (``bspde_cg_pass_a_range``); the 2 x p boundary planes follow;
+     p_k's exchange is posted right after the pass A that writes it and
+     runs (on the halo communicator's own NCCL stream) under the all-reduce,
+     finalize and pass B; r's follows pass B ("pipeline", the default; see
+     ``_halo_mode`` for "split", which also runs pass A's interior planes
+     under r's exchange through ``bspde_cg_pass_a_range``);
   2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
      and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
      finalize kernel runs the scalar update on every rank;
@@ -175,32 +177,47 @@ class NativeSlabOps:
         return self.plan.cg_read(scratch)
 
 
-def _overlap_enabled(ops, halo):
-    """Interior/boundary split of pass A around the halo exchange: needs more
-    than one rank, an ops object with ranged pass A, and an interior range."""
-    if os.environ.get("BSPDE_HALO_OVERLAP", "1") == "0" or halo.world == 1:
-        return False
+HALO_MODES = ("pipeline", "split", "off")
+
+
+def _halo_mode(ops, halo):
+    """``BSPDE_HALO_OVERLAP``: "pipeline" (default), "split" or "off" ("0").
+
+    * pipeline -- p_k's ghost planes travel while the <p,Ap> all-reduce,
+      finalize and pass B of the same iteration run (the exchange is posted
+      right after pass A on the halo communicator, a separate NCCL stream);
+      only r's exchange sits between pass B and the next pass A;
+    * split -- pipeline, plus pass A split around r's exchange: the interior
+      output planes [g, nz - g), which read no ghost plane, run while it is in
+      flight, the two g-plane boundary ranges after it lands (costs 2 x 2p
+      warm-up planes per tile; tools/time_slab_split.py);
+    * off -- both exchanges before pass A.
+    """
+    if halo.world == 1:
+        return "off"
+    mode = os.environ.get("BSPDE_HALO_OVERLAP", "pipeline")
+    mode = "off" if mode == "0" else mode
+    if mode not in HALO_MODES:
+        raise ConfigurationError(f"BSPDE_HALO_OVERLAP must be one of {HALO_MODES}, got {mode!r}")
     lay = halo.layout
-    return hasattr(ops, "pass_a_range") and lay.nz > 2 * lay.ghost
+    if mode == "split" and not (hasattr(ops, "pass_a_range") and lay.nz > 2 * lay.ghost):
+        mode = "pipeline"  # no interior range on this slab
+    return mode
 
 
 def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: SolveConfig,
                     has_x0=True, history=None):
     """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
-    ``pring`` holds the ring of search directions (leading axis).
-
-    With more than one rank, pass A of every iteration is split around the
-    halo exchange of r and p_{k-1}: the exchange is posted, the interior
-    output planes [g, nz - g) (which read no ghost plane) are computed while it
-    is in flight, then the two g-plane boundary ranges after it lands, their
-    <p,Ap> added to the interior's."""
+    ``pring`` holds the ring of search directions (leading axis).  Iteration
+    k needs the ghost planes of r_k and p_{k-1}; how their exchange overlaps
+    the kernels is ``_halo_mode``."""
     t0 = time.perf_counter()
-    overlap = _overlap_enabled(ops, halo)
+    mode = _halo_mode(ops, halo)
     g, nz = halo.layout.ghost, halo.layout.nz
     if not has_x0:
         x.zero_()
     R = pring.shape[0]
-    pring[R - 1].zero_()  # p_{-1} = 0
+    pring[R - 1].zero_()  # p_{-1} = 0, ghost planes included: nothing to exchange at k = 0
     ops.setup(scratch, history, config, has_x0)
     halo(x)
     ops.residual(b, x, r, scratch)
@@ -209,25 +226,33 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
     k = 0
-    while active:
-        for _ in range(K):
-            p_in, p_out = pring[(k - 1) % R], pring[k % R]
-            if overlap:
-                works = halo.start(r, p_in)
-                ops.pass_a_range(r, p_in, p_out, ap, scratch, g, nz - 2 * g, False)
-                halo.wait(works)
-                ops.pass_a_range(r, p_in, p_out, ap, scratch, 0, g, True)
-                ops.pass_a_range(r, p_in, p_out, ap, scratch, nz - g, g, True)
-            else:
-                halo(r, p_in)
-                ops.pass_a(r, p_in, p_out, ap, scratch)
-            allreduce(ops.sums(scratch, 1))
-            ops.finalize(scratch, 1)
-            ops.pass_b(x, r, pring, ap, scratch)
-            allreduce(ops.sums(scratch, 2))
-            ops.finalize(scratch, 2)
-            k += 1
-        rep, active = ops.read(scratch)
+    pending_p = []  # the in-flight exchange of p_{k-1} (pipeline / split)
+    try:
+        while active:
+            for _ in range(K):
+                p_in, p_out = pring[(k - 1) % R], pring[k % R]
+                if mode == "off":
+                    halo(r, p_in)
+                    ops.pass_a(r, p_in, p_out, ap, scratch)
+                elif mode == "pipeline":
+                    halo.wait(halo.start(r) + pending_p)
+                    ops.pass_a(r, p_in, p_out, ap, scratch)
+                else:  # split
+                    works = halo.start(r)
+                    ops.pass_a_range(r, p_in, p_out, ap, scratch, g, nz - 2 * g, False)
+                    halo.wait(works + pending_p)
+                    ops.pass_a_range(r, p_in, p_out, ap, scratch, 0, g, True)
+                    ops.pass_a_range(r, p_in, p_out, ap, scratch, nz - g, g, True)
+                pending_p = halo.start(p_out) if mode != "off" else []
+                allreduce(ops.sums(scratch, 1))
+                ops.finalize(scratch, 1)
+                ops.pass_b(x, r, pring, ap, scratch)
+                allreduce(ops.sums(scratch, 2))
+                ops.finalize(scratch, 2)
+                k += 1
+            rep, active = ops.read(scratch)
+    finally:
+        halo.wait(pending_p)
     ops.flush_x(x, pring, scratch)  # the pending x updates
     return rep, time.perf_counter() - t0
 
@@ -258,10 +283,16 @@ class DistributedOperator:
         self.layout = SlabLayout(self.part.nz, ny, nx, ghost=data.n_b,
                                  z_offset=self.part.z_offset, nz_global=nzg)
         self._plans = {}
-        self.halo = HaloExchanger(self.layout, self.rank, self.world, group)
+        torch.cuda.set_device(self.device)
+        # halos get their own communicator (own NCCL stream), so p_k's
+        # exchange overlaps the scalar all-reduce and pass B ("pipeline")
+        self.halo_group = group
+        if self.world > 1:
+            ranks = dist.get_process_group_ranks(group) if group is not None else None
+            self.halo_group = dist.new_group(ranks=ranks)
+        self.halo = HaloExchanger(self.layout, self.rank, self.world, self.halo_group)
         self.allreduce = _allreduce_fn(self.world, group)
         self._work = None
-        torch.cuda.set_device(self.device)
 
     def plan(self, precond="jacobi"):
         from .device import NativePlan

@@ -161,7 +161,7 @@ class CpuSlabOps:
         return rep, bool(self.state["active"])
 
 
-def _worker(rank, world, port, ext, p, out_q, overlap="1"):
+def _worker(rank, world, port, ext, p, out_q, overlap="pipeline"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BSPDE_HALO_OVERLAP=overlap)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -183,7 +183,7 @@ def _worker(rank, world, port, ext, p, out_q, overlap="1"):
         pring = torch.zeros((4,) + tuple(lay.buf_shape), dtype=torch.float64)
         scratch = torch.zeros(8, dtype=torch.float64)
         ops = CpuSlabOps(ora, lay)
-        halo = HaloExchanger(lay, rank, world)
+        halo = HaloExchanger(lay, rank, world, dist.new_group())  # own communicator, as the product
 
         def allreduce(t):
             dist.all_reduce(t)
@@ -215,10 +215,12 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,ext,overlap", [
-    (2, (13, 10, 11), "1"),   # 15 coefficient planes: slabs of 8 / 7, both split pass A
-    (3, (17, 9, 10), "1"),    # 19: 7 / 6 / 6, only rank 0 has an interior range (> 2p)
-    (3, (13, 9, 10), "1"),    # 15: 5 / 5 / 5, no interior range: whole-slab pass A
-    (2, (21, 9, 10), "0"),    # overlap disabled
+    (2, (13, 10, 11), "split"),     # 15 coefficient planes: slabs of 8 / 7, both split pass A
+    (3, (17, 9, 10), "split"),      # 19: 7 / 6 / 6, only rank 0 has an interior range (> 2p)
+    (3, (13, 9, 10), "split"),      # 15: 5 / 5 / 5, no interior range: pipeline instead
+    (2, (13, 10, 11), "pipeline"),  # p_k's exchange in flight under the all-reduce + pass B
+    (3, (17, 9, 10), "pipeline"),
+    (2, (21, 9, 10), "off"),        # both exchanges before pass A
 ])
 def test_zslab_cg_matches_single_process(world, ext, overlap):
     ctx = mp.get_context("spawn")
@@ -234,7 +236,7 @@ def test_zslab_cg_matches_single_process(world, ext, overlap):
     its, its_o, rel, range_calls, nz0 = q.get(timeout=10)
     assert abs(its - its_o) <= 1, (its, its_o)
     assert rel < 1e-10, rel
-    split = overlap == "1" and nz0 > 2 * 3  # rank 0's slab has an interior range
+    split = overlap == "split" and nz0 > 2 * 3  # rank 0's slab has an interior range
     assert (range_calls > 0) == split, range_calls
 
 
