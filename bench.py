@@ -177,6 +177,8 @@ def config_of(args, world):
                         f"implicit Euler lambda=4, Jacobi-PCG tol 1e-10, z-slabs x{world}",
             "ncoef": ncoef, "degree": p, "dofs": ncoef ** 3, "precision": "fp64",
             "parallelism": f"zslab{world}",
+            "halo_overlap": (os.environ.get("BSPDE_HALO_OVERLAP", "pipeline") if world > 1
+                             else "none (single slab)"),
             "l2": f"inputs ({gb:.1f} GB/vector) vs 126 MB L2"}
 
 
