@@ -108,3 +108,18 @@ def test_oracle_direct_transform_vs_reference_fixtures(golden):
             c = O.direct_transform(g[key], p)
             ref = g[f"{tag}_c"]
             assert float(np.abs(c - ref).max()) <= 1e-13 * float(np.abs(ref).max()), tag
+
+
+def test_apply_plane_matches_full_apply():
+    """The plane-window oracle used by the C3 (930^3) GPU check equals rows
+    of the full oracle apply."""
+    N = 20
+    h = 1.0 / (N - 1)
+    ora = O.KronOperator((N,) * 3, (h,) * 3, 3, 4 * h * h, 1.0)
+    u = np.random.default_rng(0).normal(size=ora.cext)
+    A = ora.apply(u)
+    n0 = ora.cext[0]
+    for z0 in (0, 1, 5, n0 - 2, n0 - 1):
+        lo, hi = max(0, z0 - 3), min(n0, z0 + 4)
+        w = ora.apply_plane(u[lo:hi], lo, z0)
+        assert np.abs(w - A[z0]).max() <= 1e-14 * np.abs(A[z0]).max()

@@ -631,3 +631,63 @@ def test_pass_a_range_rejects_bad_ranges(cuda_device):
     for z0, cnt in [(-1, 2), (0, 0), (lay.nz - 1, 2)]:
         with pytest.raises(Exception, match="z range"):
             plan.cg_pass_a_range(r, q, o, ap, scratch, z0, cnt, False)
+
+
+@pytest.mark.slow
+def test_c3_930_windows_symmetry_and_true_residual(cuda_device):
+    """C3 at full size (930^3 coefficients, p = 3, lambda = 4): the device
+    apply of a random field against the oracle on output planes at both z
+    ends, both y/x edges and the middle (<= 1e-13); <u,Av> = <Au,v>; and a
+    heat step's PCG (tol 1e-10) checked through its true residual
+    |b - A x| / |b| computed with the (window-verified) device apply."""
+    import torch
+
+    from paper_1904_03057_b200.solver import pcg_device
+    from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
+
+    ncoef, p = 930, 3
+    N, hh, dt = heat_c_inputs(ncoef, p)
+    op = make_operator(heat_system(Grid((N,) * 3, (hh,) * 3), p, dt), "b200")
+    ora = O.KronOperator((N,) * 3, (hh,) * 3, p, dt, 1.0)
+    lay, dev = op.layout, op.device
+    assert ora.cext == op.data.cext == (ncoef,) * 3
+    gen = torch.Generator(device=dev).manual_seed(930)
+    u = lay.alloc(dev)
+    lay.owned(u).copy_(torch.randn(lay.owned_shape, generator=gen, device=dev,
+                                   dtype=torch.float64).reshape(lay.owned(u).shape))
+    Au = lay.alloc(dev)
+    op.apply_device(u, Au)
+    torch.cuda.synchronize()
+    own_u, own_Au = lay.owned(u), lay.owned(Au)
+    for z0 in (0, 1, 2, 5, 464, 927, 929):
+        lo, hi = max(0, z0 - p), min(ncoef, z0 + p + 1)
+        want = ora.apply_plane(own_u[lo:hi].cpu().numpy(), lo, z0)
+        got = own_Au[z0].cpu().numpy()
+        assert relmax(got, want) < 1e-13, z0
+    v = lay.alloc(dev)
+    lay.owned(v).copy_(1.0 + 0.1 * torch.randn(lay.owned_shape, generator=gen, device=dev,
+                                               dtype=torch.float64).reshape(own_u.shape))
+    Av = lay.alloc(dev)
+    op.apply_device(v, Av)
+    s1 = float((own_u * lay.owned(Av)).sum())
+    s2 = float((own_Au * lay.owned(v)).sum())
+    assert abs(s1 - s2) <= 1e-11 * max(abs(s1), 1.0), (s1, s2)
+    del v, Av
+    # one heat step: b = M u0 + dt M q, x0 = u0
+    gaussian_coeffs(N, hh, p, device=dev, out=u, layout=lay, **IC)
+    q = lay.alloc(dev)
+    gaussian_coeffs(N, hh, p, device=dev, out=q, layout=lay, **SOURCE)
+    F = lay.alloc(dev)
+    op.mass_apply_device(q, F)
+    b = lay.alloc(dev)
+    op.mass_apply_device(u, b, F, a=dt)
+    del q, F
+    x = u.clone()
+    rep = pcg_device(op, b, x, SolveConfig(tol=1e-10, max_iter=500), has_x0=True)
+    assert rep.converged and 10 <= rep.iterations <= 20, rep
+    op.apply_device(x, Au)
+    torch.cuda.synchronize()
+    rt = torch.linalg.vector_norm(lay.owned(b) - own_Au) / torch.linalg.vector_norm(lay.owned(b))
+    assert float(rt) < 2e-10, float(rt)
+    del u, Au, b, x
+    torch.cuda.empty_cache()
