@@ -634,24 +634,25 @@ def test_pass_a_range_rejects_bad_ranges(cuda_device):
 
 
 @pytest.mark.slow
-def test_c3_930_windows_symmetry_and_true_residual(cuda_device):
-    """C3 at full size (930^3 coefficients, p = 3, lambda = 4): the device
-    apply of a random field against the oracle on output planes at both z
-    ends, both y/x edges and the middle (<= 1e-13); <u,Av> = <Au,v>; and a
-    heat step's PCG (tol 1e-10) checked through its true residual
-    |b - A x| / |b| computed with the (window-verified) device apply."""
+@pytest.mark.parametrize("ncoef,p", [(930, 3), (512, 1), (512, 2), (512, 3), (512, 4), (512, 5)])
+def test_full_size_windows_symmetry_and_true_residual(cuda_device, ncoef, p):
+    """C3 at full size (930^3 coefficients, p = 3, lambda = 4) and the C4
+    degree sweep (512^3, p = 1..5): the device apply of a random field
+    against the oracle on output planes at both z ends and the middle (each
+    plane spans the y/x edges) (<= 1e-13); <u,Av> = <Au,v>; and a heat
+    step's PCG (tol 1e-10) checked through its true residual |b - A x| / |b|
+    computed with the (window-verified) device apply."""
     import torch
 
     from paper_1904_03057_b200.solver import pcg_device
     from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
 
-    ncoef, p = 930, 3
     N, hh, dt = heat_c_inputs(ncoef, p)
     op = make_operator(heat_system(Grid((N,) * 3, (hh,) * 3), p, dt), "b200")
     ora = O.KronOperator((N,) * 3, (hh,) * 3, p, dt, 1.0)
     lay, dev = op.layout, op.device
     assert ora.cext == op.data.cext == (ncoef,) * 3
-    gen = torch.Generator(device=dev).manual_seed(930)
+    gen = torch.Generator(device=dev).manual_seed(ncoef + p)
     u = lay.alloc(dev)
     lay.owned(u).copy_(torch.randn(lay.owned_shape, generator=gen, device=dev,
                                    dtype=torch.float64).reshape(lay.owned(u).shape))
@@ -659,7 +660,7 @@ def test_c3_930_windows_symmetry_and_true_residual(cuda_device):
     op.apply_device(u, Au)
     torch.cuda.synchronize()
     own_u, own_Au = lay.owned(u), lay.owned(Au)
-    for z0 in (0, 1, 2, 5, 464, 927, 929):
+    for z0 in sorted({0, 1, 2, 5, ncoef // 2, ncoef - 3, ncoef - 1}):
         lo, hi = max(0, z0 - p), min(ncoef, z0 + p + 1)
         want = ora.apply_plane(own_u[lo:hi].cpu().numpy(), lo, z0)
         got = own_Au[z0].cpu().numpy()
@@ -684,7 +685,9 @@ def test_c3_930_windows_symmetry_and_true_residual(cuda_device):
     del q, F
     x = u.clone()
     rep = pcg_device(op, b, x, SolveConfig(tol=1e-10, max_iter=500), has_x0=True)
-    assert rep.converged and 10 <= rep.iterations <= 20, rep
+    assert rep.converged and rep.iterations <= 200, rep
+    if (ncoef, p) == (930, 3):
+        assert 10 <= rep.iterations <= 20, rep  # the bench's 14-15
     op.apply_device(x, Au)
     torch.cuda.synchronize()
     rt = torch.linalg.vector_norm(lay.owned(b) - own_Au) / torch.linalg.vector_norm(lay.owned(b))
