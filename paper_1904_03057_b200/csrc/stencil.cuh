@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S
                                                               double* __restrict__ out,
                                                               const double* __restrict__ aux,
                                                               double* partials, unsigned* counter,
-                                                              CgState* st, int precond) {
+                                                              CgState* st, int precond,
+                                                              const uint8_t* __restrict__ live = nullptr) {
   __shared__ double s_red[(ST_NT / 32) * 4];
   __shared__ unsigned s_last;
   if (MODE == 2 && !ld_vol(&st->active)) return;
@@ -167,6 +168,14 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S
     const int lx0 = xb * XB;
     const long long l0 = (zy * S.nx) + lx0;
     const int nv = min(XB, S.nx - lx0);
+    if (MODE != 1 && live && !live[gi]) {
+      // every stencil entry of these rows is zero (inactive mask nodes): the
+      // gather would produce +0 exactly, and add nothing to <c, out>
+#pragma unroll
+      for (int v = 0; v < XB; ++v)
+        if (v < nv) out[l0 + v] = 0.0;
+      continue;
+    }
     double t[XB];
 #pragma unroll
     for (int v = 0; v < XB; ++v) t[v] = 0.0;
@@ -290,6 +299,8 @@ struct bspde_stencil {
   cudaStream_t work = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int64_t launches = 0;
+  uint8_t* d_live = nullptr;  // per apply group: any nonzero stencil entry (PCG skip list)
+  size_t live_bytes = 0;
 };
 
 namespace {
@@ -398,6 +409,35 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
   }
 }
 
+// live[g] = 1 iff output group g (XB consecutive x of one (z, y) row, the
+// x-mapped apply's unit) has a nonzero stencil entry.  Mask systems keep
+// their inactive nodes as all-zero rows (79% of the leg's 864k rows); the
+// CG apply skips those groups' 27..125 stencil loads.
+template <int NB>
+__global__ void __launch_bounds__(ST_NT) stencil_live_kernel(const StencilDev S,
+                                                             const double* __restrict__ P,
+                                                             uint8_t* __restrict__ live) {
+  constexpr int A = 2 * NB + 1, A3 = A * A * A;
+  const int nxb = (S.nx + XB - 1) / XB;
+  const long long groups = (long long)S.nz * S.ny * nxb;
+  for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
+       gi += (long long)gridDim.x * blockDim.x) {
+    const int xb = (int)(gi % nxb);
+    const long long zy = gi / nxb;
+    const int lx0 = xb * XB;
+    const long long l0 = zy * S.nx + lx0;
+    const int nv = min(XB, S.nx - lx0);
+    bool nz = false;
+    for (int e = 0; e < A3 && !nz; ++e) {
+      const double* pe = P + (long long)e * S.N + l0;
+#pragma unroll
+      for (int v = 0; v < XB; ++v)
+        if (v < nv && pe[v] != 0.0) nz = true;
+    }
+    live[gi] = nz ? 1 : 0;
+  }
+}
+
 inline bool st_ymap() {
   static const int v = [] {
     const char* e = getenv("BSPDE_ST_XMAP");
@@ -409,7 +449,7 @@ inline bool st_ymap() {
 template <int MODE>
 void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const double* P,
               const double* c, double* out, const double* aux, double* partials,
-              unsigned* counter, CgState* state, int precond) {
+              unsigned* counter, CgState* state, int precond, const uint8_t* live = nullptr) {
   // y mapping for p >= 3 (measured +5-30% apply, +25% PCG at p = 3); at
   // p = 1, 2 the compiler batches every load of the short stencil into
   // registers (128-255) and the x mapping is faster
@@ -422,12 +462,38 @@ void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const doub
     return;
   }
   switch (s->S.nb) {
-    case 1: stencil_apply_kernel<MODE, 1><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-    case 2: stencil_apply_kernel<MODE, 2><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-    case 3: stencil_apply_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-    case 4: stencil_apply_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-    default: stencil_apply_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    case 1: stencil_apply_kernel<MODE, 1><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+    case 2: stencil_apply_kernel<MODE, 2><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+    case 3: stencil_apply_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+    case 4: stencil_apply_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+    default: stencil_apply_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
   }
+}
+
+// live flags for the x-mapped apply (nullptr when the y-mapped kernel runs)
+int st_live(bspde_stencil* s, const double* P, cudaStream_t st, uint8_t** live) {
+  *live = nullptr;
+  if ((st_ymap() && s->S.nb >= 3) || getenv("BSPDE_ST_NOSKIP")) return BSPDE_OK;
+  const long long groups = (long long)s->S.nz * s->S.ny * ((s->S.nx + XB - 1) / XB);
+  if ((size_t)groups > s->live_bytes) {
+    if (s->d_live) CUDA_TRY(cudaFree(s->d_live));
+    s->d_live = nullptr;
+    s->live_bytes = 0;
+    CUDA_TRY(cudaMalloc(&s->d_live, (size_t)groups));
+    s->live_bytes = (size_t)groups;
+  }
+  const unsigned grid = st_grid(s, groups);
+  switch (s->S.nb) {
+    case 1: stencil_live_kernel<1><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 2: stencil_live_kernel<2><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 3: stencil_live_kernel<3><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 4: stencil_live_kernel<4><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    default: stencil_live_kernel<5><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+  }
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  *live = s->d_live;
+  return BSPDE_OK;
 }
 
 int st_read(bspde_stencil* s, void* scratch, bspde_cg_report* rep, int32_t* active, cudaStream_t st) {
@@ -559,6 +625,7 @@ int bspde_stencil_destroy(bspde_stencil* s) {
   if (!s) return BSPDE_OK;
   cudaSetDevice(s->device);
   if (s->d_tab) cudaFree(s->d_tab);
+  if (s->d_live) cudaFree(s->d_live);
   if (s->host_state) cudaFreeHost(s->host_state);
   if (s->work) cudaStreamDestroy(s->work);
   if (s->ev_in) cudaEventDestroy(s->ev_in);
@@ -643,6 +710,8 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
   unsigned* counter = scratch_counter(scratch);
   CgState* state = scratch_state(scratch);
   const unsigned agrid = st_grid(s, s->S.N / XB + 1);
+  uint8_t* live = nullptr;
+  if (int lrc = st_live(s, P, st, &live)) return lrc;
   st_apply<1>(s, agrid, st, P, x, r, b, partials, counter, state, precond);
   s->launches++;
   CUDA_TRY(cudaGetLastError());
@@ -652,7 +721,7 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
   while (rc == BSPDE_OK && active) {
     for (int k = 0; k < K; ++k) {
       stencil_pform_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, r, p, state, precond);
-      st_apply<2>(s, agrid, st, P, p, ap, nullptr, partials, counter, state, precond);
+      st_apply<2>(s, agrid, st, P, p, ap, nullptr, partials, counter, state, precond, live);
       stencil_update_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, x, r, p, ap, partials, counter,
                                                     state, precond);
       s->launches += 3;
