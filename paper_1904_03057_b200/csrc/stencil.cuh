@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
                                                                 double* __restrict__ out,
                                                                 const double* __restrict__ aux,
                                                                 double* partials, unsigned* counter,
-                                                                CgState* st, int precond) {
+                                                                CgState* st, int precond,
+                                                                const uint8_t* __restrict__ live = nullptr) {
   __shared__ double s_red[(ST_NT / 32) * 4];
   __shared__ unsigned s_last;
   if (MODE == 2 && !ld_vol(&st->active)) return;
@@ -349,6 +350,12 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
     const int ly0 = yb * XB;
     const long long l0 = ((long long)lz * S.ny + ly0) * S.nx + lx;
     const int nv = min(XB, S.ny - ly0);
+    if (MODE != 1 && live && !live[gi]) {  // all-zero rows: +0 exactly (see stencil_live_kernel)
+#pragma unroll
+      for (int v = 0; v < XB; ++v)
+        if (v < nv) out[l0 + v * sy] = 0.0;
+      continue;
+    }
     double t[XB];
 #pragma unroll
     for (int v = 0; v < XB; ++v) t[v] = 0.0;
@@ -413,26 +420,37 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
 // x-mapped apply's unit) has a nonzero stencil entry.  Mask systems keep
 // their inactive nodes as all-zero rows (79% of the leg's 864k rows); the
 // CG apply skips those groups' 27..125 stencil loads.
-template <int NB>
+// YMAP: the y-mapped apply's groups (XB consecutive y at one x).
+template <int NB, bool YMAP>
 __global__ void __launch_bounds__(ST_NT) stencil_live_kernel(const StencilDev S,
                                                              const double* __restrict__ P,
                                                              uint8_t* __restrict__ live) {
   constexpr int A = 2 * NB + 1, A3 = A * A * A;
-  const int nxb = (S.nx + XB - 1) / XB;
-  const long long groups = (long long)S.nz * S.ny * nxb;
+  const int nxb = (S.nx + XB - 1) / XB, nyb = (S.ny + XB - 1) / XB;
+  const long long groups = YMAP ? (long long)S.nz * nyb * S.nx : (long long)S.nz * S.ny * nxb;
   for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
        gi += (long long)gridDim.x * blockDim.x) {
-    const int xb = (int)(gi % nxb);
-    const long long zy = gi / nxb;
-    const int lx0 = xb * XB;
-    const long long l0 = zy * S.nx + lx0;
-    const int nv = min(XB, S.nx - lx0);
+    long long l0, step;
+    int nv;
+    if (YMAP) {
+      const int lx = (int)(gi % S.nx);
+      const long long r = gi / S.nx;
+      const int yb = (int)(r % nyb), lz = (int)(r / nyb);
+      l0 = ((long long)lz * S.ny + yb * XB) * S.nx + lx;
+      nv = min(XB, S.ny - yb * XB);
+      step = S.nx;
+    } else {
+      const int xb = (int)(gi % nxb);
+      l0 = (gi / nxb) * S.nx + xb * XB;
+      nv = min(XB, S.nx - xb * XB);
+      step = 1;
+    }
     bool nz = false;
     for (int e = 0; e < A3 && !nz; ++e) {
       const double* pe = P + (long long)e * S.N + l0;
 #pragma unroll
       for (int v = 0; v < XB; ++v)
-        if (v < nv && pe[v] != 0.0) nz = true;
+        if (v < nv && pe[v * step] != 0.0) nz = true;
     }
     live[gi] = nz ? 1 : 0;
   }
@@ -455,9 +473,9 @@ void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const doub
   // registers (128-255) and the x mapping is faster
   if (st_ymap() && s->S.nb >= 3) {
     switch (s->S.nb) {
-      case 3: stencil_apply_y_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-      case 4: stencil_apply_y_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
-      default: stencil_apply_y_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      case 3: stencil_apply_y_kernel<MODE, 3><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+      case 4: stencil_apply_y_kernel<MODE, 4><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
+      default: stencil_apply_y_kernel<MODE, 5><<<grid, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond, live); break;
     }
     return;
   }
@@ -470,11 +488,14 @@ void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const doub
   }
 }
 
-// live flags for the x-mapped apply (nullptr when the y-mapped kernel runs)
+// live flags in the group order of the apply kernel st_apply launches
 int st_live(bspde_stencil* s, const double* P, cudaStream_t st, uint8_t** live) {
   *live = nullptr;
-  if ((st_ymap() && s->S.nb >= 3) || getenv("BSPDE_ST_NOSKIP")) return BSPDE_OK;
-  const long long groups = (long long)s->S.nz * s->S.ny * ((s->S.nx + XB - 1) / XB);
+  if (getenv("BSPDE_ST_NOSKIP")) return BSPDE_OK;
+  const bool ymap = st_ymap() && s->S.nb >= 3;
+  const long long groups =
+      ymap ? (long long)s->S.nz * ((s->S.ny + XB - 1) / XB) * s->S.nx
+           : (long long)s->S.nz * s->S.ny * ((s->S.nx + XB - 1) / XB);
   if ((size_t)groups > s->live_bytes) {
     if (s->d_live) CUDA_TRY(cudaFree(s->d_live));
     s->d_live = nullptr;
@@ -483,12 +504,15 @@ int st_live(bspde_stencil* s, const double* P, cudaStream_t st, uint8_t** live) 
     s->live_bytes = (size_t)groups;
   }
   const unsigned grid = st_grid(s, groups);
-  switch (s->S.nb) {
-    case 1: stencil_live_kernel<1><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
-    case 2: stencil_live_kernel<2><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
-    case 3: stencil_live_kernel<3><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
-    case 4: stencil_live_kernel<4><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
-    default: stencil_live_kernel<5><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+  switch (s->S.nb * 2 + (ymap ? 1 : 0)) {
+    case 2: stencil_live_kernel<1, false><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 4: stencil_live_kernel<2, false><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 6: stencil_live_kernel<3, false><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 7: stencil_live_kernel<3, true><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 8: stencil_live_kernel<4, false><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 9: stencil_live_kernel<4, true><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    case 10: stencil_live_kernel<5, false><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
+    default: stencil_live_kernel<5, true><<<grid, ST_NT, 0, st>>>(s->S, P, s->d_live); break;
   }
   s->launches++;
   CUDA_TRY(cudaGetLastError());

@@ -106,3 +106,26 @@ def test_heat_steps_on_mask_match_reference():
         rep = hs.step()
         assert rep.converged and abs(rep.iterations - int(its)) <= max(1, int(its) // 100)
         assert rel(hs.coefficients(), GOLD["heat_u"][k]) <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", [t for t in TAGS if GOLD[f"{t}_its"][0] > 0])
+def test_pcg_inactive_skip_is_bitwise(tag, monkeypatch):
+    """The CG apply skips row groups whose stencil entries are all zero
+    (stencil_live_kernel, x- and y-mapped applies): iterates, residual
+    history and solution must be bit-identical to the dense apply
+    (BSPDE_ST_NOSKIP=1)."""
+    from paper_1904_03057_b200 import make_operator, pcg
+    from paper_1904_03057_b200.solver import SolveConfig
+
+    cfg = SolveConfig(tol=1e-10, max_iter=3000, record_history=True)
+    outs = []
+    for noskip in (False, True):
+        if noskip:
+            monkeypatch.setenv("BSPDE_ST_NOSKIP", "1")
+        op = make_operator(_system(tag), "b200")
+        outs.append(pcg(op, GOLD[f"{tag}_b"], cfg))
+    (x0, r0), (x1, r1) = outs
+    assert r0.iterations == r1.iterations
+    assert r0.history == r1.history
+    assert np.array_equal(x0, x1)
