@@ -241,11 +241,22 @@ __global__ void __launch_bounds__(ST_NT) stencil_pform_kernel(const StencilDev S
   const double beta = ld_vol(&st->beta);
   const int A = S.A, hb = S.nb;
   const int center = (hb * A + hb) * A + hb;
+  // two grid-stride elements per trip (loads of both issued together; the
+  // per-element arithmetic is unchanged)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const double* diag = P + (long long)center * S.N;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += (long long)gridDim.x * blockDim.x) {
-    const double dg = P[(long long)center * S.N + l];
+       l += 2 * stride) {
+    const long long l2 = l + stride;
+    const bool two = l2 < S.N;
+    const double dg = diag[l], rv = r[l], pv = p[l];
+    const double dg2 = two ? diag[l2] : 1.0, rv2 = two ? r[l2] : 0.0, pv2 = two ? p[l2] : 0.0;
     const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
-    p[l] = pdir(r[l], inv, p[l], beta);
+    p[l] = pdir(rv, inv, pv, beta);
+    if (two) {
+      const double inv2 = (precond && dg2 != 0.0) ? 1.0 / dg2 : 1.0;
+      p[l2] = pdir(rv2, inv2, pv2, beta);
+    }
   }
 }
 
@@ -264,15 +275,37 @@ __global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev 
   const int A = S.A, hb = S.nb;
   const int center = (hb * A + hb) * A + hb;
   double rz = 0.0, rr = 0.0;
+  // two grid-stride elements per trip, accumulated in the same order as a
+  // one-element loop (bitwise the same sums)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const double* diag = P + (long long)center * S.N;
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += (long long)gridDim.x * blockDim.x) {
-    x[l] = __dadd_rn(x[l], __dmul_rn(alpha, p[l]));
-    const double rn = __dsub_rn(r[l], __dmul_rn(alpha, ap[l]));
+       l += 2 * stride) {
+    const long long l2 = l + stride;
+    const bool two = l2 < S.N;
+    const double xv = x[l], pv = p[l], rv = r[l], av = ap[l], dg = diag[l];
+    double xv2 = 0.0, pv2 = 0.0, rv2 = 0.0, av2 = 0.0, dg2 = 1.0;
+    if (two) {
+      xv2 = x[l2];
+      pv2 = p[l2];
+      rv2 = r[l2];
+      av2 = ap[l2];
+      dg2 = diag[l2];
+    }
+    x[l] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+    const double rn = __dsub_rn(rv, __dmul_rn(alpha, av));
     r[l] = rn;
-    const double dg = P[(long long)center * S.N + l];
     const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
     rz = fma(rn, __dmul_rn(inv, rn), rz);
     rr = fma(rn, rn, rr);
+    if (two) {
+      x[l2] = __dadd_rn(xv2, __dmul_rn(alpha, pv2));
+      const double rn2 = __dsub_rn(rv2, __dmul_rn(alpha, av2));
+      r[l2] = rn2;
+      const double inv2 = (precond && dg2 != 0.0) ? 1.0 / dg2 : 1.0;
+      rz = fma(rn2, __dmul_rn(inv2, rn2), rz);
+      rr = fma(rn2, rn2, rr);
+    }
   }
   double v[2] = {rz, rr};
   reduce_and_finalize<2, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 2);
