@@ -250,3 +250,32 @@ def test_partition_bounds():
         SlabPartition(5, 8, 0)
     with pytest.raises(Exception):
         SlabPartition(10, 4, 0).check_min(3)
+
+
+def test_halo_mode_selection(monkeypatch):
+    """BSPDE_HALO_OVERLAP: single rank -> off; pipeline default; split needs a
+    ranged pass A and an interior range (> 2p planes), else pipeline; bad
+    values raise ConfigurationError."""
+    from paper_1904_03057_b200.distributed import _halo_mode
+    from paper_1904_03057_b200.errors import ConfigurationError
+
+    class Ops:
+        def pass_a_range(self, *a):
+            pass
+
+    def halo(nz, world=2):
+        return HaloExchanger(SlabLayout(nz, 5, 6, ghost=3, z_offset=0, nz_global=2 * nz),
+                             0, world)
+
+    monkeypatch.delenv("BSPDE_HALO_OVERLAP", raising=False)
+    assert _halo_mode(Ops(), halo(10, world=1)) == "off"
+    assert _halo_mode(Ops(), halo(10)) == "pipeline"
+    monkeypatch.setenv("BSPDE_HALO_OVERLAP", "split")
+    assert _halo_mode(Ops(), halo(10)) == "split"
+    assert _halo_mode(Ops(), halo(6)) == "pipeline"      # no interior range
+    assert _halo_mode(object(), halo(10)) == "pipeline"  # no ranged pass A
+    monkeypatch.setenv("BSPDE_HALO_OVERLAP", "0")
+    assert _halo_mode(Ops(), halo(10)) == "off"
+    monkeypatch.setenv("BSPDE_HALO_OVERLAP", "sideways")
+    with pytest.raises(ConfigurationError):
+        _halo_mode(Ops(), halo(10))
