@@ -795,6 +795,14 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   }
 }
 
+// the thread that issues the plane TMA loads (lane 0 of one warp): the last
+// warp owns one haloed row fewer in the front half than warps 0..(HY % NW)-1
+#ifndef BSPDE_PROD_WARP
+#define BSPDE_PROD_WARP -1
+#endif
+template <int P>
+constexpr int kProdThread = (BSPDE_PROD_WARP < 0 ? Geo<P>::NW + BSPDE_PROD_WARP : BSPDE_PROD_WARP) * 32;
+
 template <int P, int MODE, int TK>
 __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
                                          const CUtensorMap* tm1, const Smem& sm,
@@ -837,7 +845,7 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
     if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
     plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == kProdThread<P>) {
       // the stage of plane j is consumed (x-pass one iteration ago, own p now)
       fence_proxy_async();
       prod.issue(prm, tm0, tm1, sm.stage, sm.full);
@@ -885,7 +893,7 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
   const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
   double dsum[3] = {0.0, 0.0, 0.0};
   Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
-  if (tid == 0) {
+  if (tid == kProdThread<P>) {
     for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, sm.stage, sm.full);
   }
   uint32_t flat = 0;
