@@ -8,7 +8,8 @@ Jacobi-PCG solve with x0 = u_prev.
 
 Default workload (N=1): C3, 930^3 coefficients (928^3 = 0.80 B nodes), p=3,
 lambda = dt/h^2 = 4, fp64, synthetic Gaussian IC/source.
-N>1: the same global grid split in z-slabs, one rank per GPU (strong scaling).
+N>1: the same global grid split in z-slabs, one rank per GPU (strong scaling);
+`--gpus N` without a launcher spawns the N ranks itself (torch.distributed.run).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--ncoef 930] [--impl reference]
 """
@@ -28,13 +29,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# pass A: read r, p_{k-1}; write Ap, p_k.  Pass B: read r, Ap; write r
-# (24 B), and every P_RING-th iteration also read x and the last P_RING p's
-# and write x (24 + 16 + 8 * P_RING B): x moves once per P_RING iterations
-#
-ALG_BYTES_PASS_A = 32
-ALG_BYTES_PASS_B = 24 + (16 + 8 * 4) / 4  # 36: average over the ring period (P_RING = 4)
-ALG_BYTES_ITER = ALG_BYTES_PASS_A + ALG_BYTES_PASS_B  # 68
+# algorithmic bytes per DoF of the CG passes: alg_bytes(ring) below
 SURVEY_BYTES_ITER = 80  # x, r, p, Ap streams of the textbook fused CG
 # ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
 # filled from the committed profile summary when present
@@ -109,37 +104,84 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm (oracle port -- the reference is pure Python and
-# does not exist on the GPU box)
+# CPU baseline / reference arm.  The reference (package `bspde`, pure Python)
+# is installed into baseline/_ref; it runs on the host cores.
+# When it cannot be imported, the oracle port (oracle/bspde_oracle.py) stands
+# in and the line says kind "port".
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_SAMPLE_NCOEF = 64  # C1: the reference's own demo scale (BASELINE.json configs[0])
 
 
-def cpu_port_rate(ncoef=64, iters=20, repeats=3, p=3):
-    """Oracle port of the reference CG path (numpy/scipy Kronecker apply +
-    the reference pcg recurrence) on the C1 heat problem: CG DoF-it/s.
-    Single-threaded: scipy's sparse matvec holds the GIL (a thread pool over
-    slabs measured 7.7x slower); the port is still ~6x faster than the
-    reference's fastest strategy (sparse 1.78 MDoF-it/s)."""
-    from oracle import bspde_oracle as O
+def _reference_modules():
+    """The installed reference package, or None (then the oracle port is timed)."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from bspde.assembly import basis_extension, build_system
+        from bspde.domain import BoxDomain, Grid
+        from bspde.operator import make_operator
+        from bspde.solver import SolveConfig, pcg
+    except Exception:
+        return None
+    return dict(basis_extension=basis_extension, build_system=build_system,
+                BoxDomain=BoxDomain, Grid=Grid, make_operator=make_operator,
+                SolveConfig=SolveConfig, pcg=pcg)
 
-    inp = O.heat_inputs(ncoef, p)
-    N, h, dt = inp["N"], inp["h"], inp["dt"]
-    A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
-    b = A.mass_apply(inp["u0"]) + dt * A.mass_apply(inp["q"])
-    O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=2, x0=inp["u0"])  # warm
-    times = []
-    for _ in range(repeats):
+
+def _ref_system(R, p, ncoef=REF_SAMPLE_NCOEF):
+    """The C1 heat system A = M + dt K through the reference's own API
+     and a smooth right-hand side."""
+    ext = R["basis_extension"](p)
+    N = ncoef - 2 * ext
+    h = 1.0 / (N - 1)
+    dt = 4.0 * h * h
+    g = R["Grid"]((N,) * 3, (h,) * 3)
+    shp = tuple(n + 2 * ext for n in g.extents)
+    data = R["build_system"](R["BoxDomain"](g), p, p, np.full(shp, dt), np.full(shp, 1.0), [])
+    b = np.random.default_rng(0).normal(size=shp)
+    return data, b
+
+
+def _ref_sparse_worker(p, iters, nstep, barrier, out):
+    """One reference-arm worker process: the reference's pcg over its fastest
+    strategy (SparseMatrixOperator, scipy CSR) on its own C1 system; each step
+    is `iters` CG iterations timed between barriers shared by all workers (so
+    the timed regions overlap, memory-bandwidth contention included)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    R = _reference_modules()
+    data, b = _ref_system(R, p)
+    A = R["make_operator"](data, "sparse")
+    cfg = R["SolveConfig"](tol=1e-30, max_iter=iters)
+    R["pcg"](A, b, R["SolveConfig"](tol=1e-30, max_iter=1))  # warm
+    dofs = int(np.prod(b.shape))
+    res = []
+    for _ in range(nstep):
+        barrier.wait()
         t0 = time.perf_counter()
-        _, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=iters, x0=inp["u0"])
-        times.append(time.perf_counter() - t0)
-    dofs = int(np.prod(A.cext))
-    t = float(np.median(times))
-    return dofs * rep["iterations"] / t, dict(dofs=dofs, iterations=rep["iterations"], seconds=t)
+        _, rep = R["pcg"](A, b, cfg)
+        res.append((dofs * rep.iterations, time.perf_counter() - t0, rep.iterations))
+    out.put(res)
 
 
-def _ref_worker(p, iters, nstep, barrier, out):
-    """One reference-arm worker process: builds its own C1 system, then times
-    `nstep` PCG samples, each started at a barrier shared by all workers so the
-    timed regions overlap (memory-bandwidth contention included)."""
+def _ref_onthefly_rate(p, workers):
+    """The reference's default / paper strategy: OnTheFlyOperator with
+    `workers` threads, one CG iteration (one apply) on the C1 system."""
+    R = _reference_modules()
+    data, b = _ref_system(R, p)
+    A = R["make_operator"](data, "onthefly", workers=workers)
+    t0 = time.perf_counter()
+    _, rep = R["pcg"](A, b, R["SolveConfig"](tol=1e-30, max_iter=1))
+    t = time.perf_counter() - t0
+    return int(np.prod(b.shape)) * rep.iterations / t, t
+
+
+def _port_worker(p, iters, nstep, barrier, out):
+    """Fallback worker: the oracle port (no reference package importable)."""
     try:
         from threadpoolctl import threadpool_limits
         threadpool_limits(1)
@@ -147,7 +189,7 @@ def _ref_worker(p, iters, nstep, barrier, out):
         pass
     from oracle import bspde_oracle as O
 
-    inp = O.heat_inputs(64, p)
+    inp = O.heat_inputs(REF_SAMPLE_NCOEF, p)
     N, h, dt = inp["N"], inp["h"], inp["dt"]
     A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
     b = A.mass_apply(inp["u0"]) + dt * A.mass_apply(inp["q"])
@@ -162,30 +204,26 @@ def _ref_worker(p, iters, nstep, barrier, out):
     out.put(res)
 
 
-def host_workers():
+def host_workers(per_worker_bytes=0):
     try:
         n = len(os.sched_getaffinity(0))
     except AttributeError:
         n = os.cpu_count() or 1
+    if per_worker_bytes:
+        try:
+            import psutil
+            n = min(n, max(1, int(0.6 * psutil.virtual_memory().available // per_worker_bytes)))
+        except Exception:
+            pass
     return max(1, min(n, int(os.environ.get("BSPDE_REF_WORKERS", n)), 256))
 
 
-def run_reference(args, rank, world):
-    """Reference arm: the oracle port of the reference CG path on every host
-    core the process may use -- one single-threaded worker process per core
-    (scipy's matvec holds the GIL, so threads do not scale), each solving its
-    own C1 sample; a step's value is the summed DoF-iterations of all workers
-    over the slowest worker's time."""
-    if rank != 0:
-        return
+def _run_workers(target, p, iters, steps, warm, nw):
     import multiprocessing as mp
 
-    steps, warm = max(args.steps, 1), max(args.warmup, 0)
-    nw = host_workers()
-    iters = 10
     ctx = mp.get_context("fork")
     barrier, out = ctx.Barrier(nw), ctx.Queue()
-    procs = [ctx.Process(target=_ref_worker, args=(args.degree, iters, warm + steps, barrier, out))
+    procs = [ctx.Process(target=target, args=(p, iters, warm + steps, barrier, out))
              for _ in range(nw)]
     for pr in procs:
         pr.start()
@@ -198,19 +236,90 @@ def run_reference(args, rank, world):
         t = max(r[i][1] for r in results)
         vals.append(work / t)
         times.append(t)
-    val = float(np.median(vals)) / 1e9
-    its = results[0][0][2]
-    sample = (f"C1 sample: 64^3 coefficients, p={args.degree}, lambda=4, {its} Jacobi-PCG "
-              f"iterations per step in each of {nw} worker processes (one per host core, timed "
-              f"between barriers; oracle port: scipy CSR 1-D factors, separable Kronecker "
-              f"apply, reference pcg recurrence); full config {args.ncoef}^3 infeasible on CPU")
+    return float(np.median(vals)), float(np.median(times)), results[0][0][2]
+
+
+def cpu_reference_rate(p=3, iters=10, repeats=3):
+    """Our arm's cpu_baseline: one reference process (sparse strategy, the
+    reference's fastest) on the C1 system; oracle port if the reference is
+    absent.  Returns (DoF-it/s, kind, sample)."""
+    R = _reference_modules()
+    if R is not None:
+        data, b = _ref_system(R, p)
+        A = R["make_operator"](data, "sparse")
+        cfg = R["SolveConfig"](tol=1e-30, max_iter=iters)
+        R["pcg"](A, b, R["SolveConfig"](tol=1e-30, max_iter=1))
+        ts = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            _, rep = R["pcg"](A, b, cfg)
+            ts.append(time.perf_counter() - t0)
+        rate = int(np.prod(b.shape)) * rep.iterations / float(np.median(ts))
+        return rate, "reference", (f"C1 64^3 p={p}: the reference's pcg over SparseMatrixOperator "
+                                   f"(baseline/_ref), {rep.iterations} iterations, median of "
+                                   f"{repeats}, 1 process")
+    from oracle import bspde_oracle as O
+
+    inp = O.heat_inputs(REF_SAMPLE_NCOEF, p)
+    N, h, dt = inp["N"], inp["h"], inp["dt"]
+    A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
+    b = A.mass_apply(inp["u0"]) + dt * A.mass_apply(inp["q"])
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        _, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-30, max_iter=iters, x0=inp["u0"])
+        ts.append(time.perf_counter() - t0)
+    rate = int(np.prod(A.cext)) * rep["iterations"] / float(np.median(ts))
+    return rate, "port", (f"C1 64^3 p={p}: oracle port (reference package not importable), "
+                          f"{rep['iterations']} iterations, median of {repeats}, 1 process")
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference's own CPU path on every host core.  The
+    reference parallelises nothing but its on-the-fly apply (threads over
+    blocks), and its fastest strategy (sparse CSR SpMV) is single-threaded,
+    so the arm runs one single-threaded sparse-strategy pcg process per core,
+    each on its own C1 sample; a step's value is the summed DoF-iterations
+    over the slowest worker's time.  The on-the-fly strategy with
+    workers=cpu_count (the paper's algorithm) is timed beside it."""
+    if rank != 0:
+        return
+    steps, warm = max(args.steps, 1), max(args.warmup, 0)
+    R = _reference_modules()
+    iters = 2
+    if R is not None:
+        nw = host_workers(per_worker_bytes=1.6e9)  # the C1 CSR matrix is ~1 GB per process
+        val, t_med, its = _run_workers(_ref_sparse_worker, args.degree, iters, steps, warm, nw)
+        kind = "reference"
+        otf_rate, otf_t = _ref_onthefly_rate(args.degree, host_workers())
+        extra = {"onthefly": {"value": otf_rate / 1e9, "unit": "GDoF/s", "workers": host_workers(),
+                              "seconds_per_iteration": otf_t}}
+        sample = (f"C1 sample: 64^3 coefficients, p={args.degree}, lambda=4 heat system; the "
+                  f"reference's pcg over SparseMatrixOperator (baseline/_ref, scipy CSR, its "
+                  f"fastest strategy), {its} CG iterations per step in each of {nw} "
+                  f"single-threaded worker processes (one per host core) timed between barriers")
+    else:
+        nw = host_workers()
+        val, t_med, its = _run_workers(_port_worker, args.degree, 10, steps, warm, nw)
+        kind, extra = "port", {}
+        sample = (f"C1 sample: 64^3 coefficients, p={args.degree}, lambda=4; oracle port "
+                  f"(reference package not importable), {its} iterations per step in each of "
+                  f"{nw} worker processes")
+    val /= 1e9
+    cfg = config_of(args, world)
+    cfg.update(ncoef=REF_SAMPLE_NCOEF, dofs=REF_SAMPLE_NCOEF ** 3, parallelism="host cores",
+               target_config=f"{args.ncoef}^3 p={args.degree} (our arm's workload)")
+    cfg["workload"] = (f"C1 heat sample: {REF_SAMPLE_NCOEF}^3 coefficients, p={args.degree}, "
+                       f"implicit Euler lambda=4 (the {args.ncoef}^3 config is infeasible for the "
+                       f"reference on CPU: ~{args.ncoef ** 3 / 262144 * 0.17:.0f} s per sparse "
+                       f"iteration and ~{args.ncoef ** 3 * 3.8e3 / 1e12:.1f} TB of CSR)")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GDoF/s", "n_gpus": world,
-        "steps": steps, "warmup": warm, "ms_per_step": float(np.median(times)) * 1e3,
+        "steps": steps, "warmup": warm, "ms_per_step": t_med * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(args, world),
-        "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": nw, "kind": "port",
-                         "sample": sample},
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": nw, "kind": kind,
+                         "sample": sample, **extra},
         "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,7 +332,8 @@ def config_of(args, world):
     from paper_1904_03057_b200.gram import basis_extension
 
     ncoef, p = args.ncoef, args.degree
-    tag = "C3" if (ncoef, p) == (930, 3) else ("C4" if ncoef == 512 else "custom")
+    tag = {(930, 3): "C3", (256, 3): "C2"}.get((ncoef, p), "C4" if ncoef == 512 else (
+        "C5" if ncoef in (1024, 1536) else "custom"))
     nodes = ncoef - 2 * basis_extension(p)
     gb = ncoef ** 3 * 8 / 1e9
     return {"workload": f"{tag} heat: {ncoef}^3 coefficients ({nodes}^3 nodes), p={p}, "
@@ -238,14 +348,26 @@ def config_of(args, world):
 # ---------------------------------------------------------------------------
 
 
+def alg_bytes(ring):
+    """Algorithmic bytes per DoF of pass A / pass B / a CG iteration for a
+    search-direction ring of length R: pass A reads r, p_{k-1} and writes Ap,
+    p_k (32 B); pass B reads r, Ap and writes r (24 B), and every R-th pass
+    also reads x and the last R p's and writes x (16 + 8 R B), i.e.
+    24 + (16 + 8 R) / R on average."""
+    b = 24 + (16 + 8 * ring) / ring
+    return 32, b, 32 + b
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     from paper_1904_03057_b200 import SolveConfig, make_operator
+    from paper_1904_03057_b200.device import heat_memory_plan
     from paper_1904_03057_b200.distributed import DistributedOperator
     from paper_1904_03057_b200.domain import Grid
     from paper_1904_03057_b200.heat import HeatSolver
+    from paper_1904_03057_b200.solver import _work
     from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
     from paper_1904_03057_b200.system import heat_system
 
@@ -257,9 +379,12 @@ def run_ours(args, rank, world, local_rank):
     N, h, dt = heat_c_inputs(args.ncoef, p)
     data = heat_system(Grid((N,) * 3, (h,) * 3), p, dt)
     dofs = int(np.prod(data.cext))
+    mem = heat_memory_plan(data.cext, p, world)
     cfg = SolveConfig(tol=1e-10, max_iter=5000, poll_every=args.poll)
     stream = torch.cuda.current_stream()
 
+    # resident fields: u, F and the CG work set (r, Ap = b, ring) -- nothing
+    # else; q is staged in r, which the first solve overwrites
     if world == 1:
         op = make_operator(data, "b200", device=local_rank)
         lay = op.layout
@@ -269,18 +394,21 @@ def run_ours(args, rank, world, local_rank):
         lay = op.layout
         z_range = op.part.bounds()
     u = lay.alloc(dev)
-    q = lay.alloc(dev)
-    gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, z_range=z_range, **IC)
-    gaussian_coeffs(N, h, p, device=dev, out=q, layout=lay, z_range=z_range, **SOURCE)
     F = lay.alloc(dev)
-    op.mass_apply_device(q, F)
-    del q
-    u0 = u.clone()
+    gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, z_range=z_range, **IC)
+    if world == 1:
+        w = _work(op, cfg.max_iter)
+        r_buf, ring = w.r, w.pring.shape[0]
+    else:
+        wb = op._work_buffers(cfg.max_iter)
+        r_buf, ring = wb["r"], wb["pring"].shape[0]
+    gaussian_coeffs(N, h, p, device=dev, out=r_buf, layout=lay, z_range=z_range, **SOURCE)
+    op.mass_apply_device(r_buf, F)
     if world == 1:
         hs = HeatSolver.from_device(op, dt, u, F, cfg)
         step = hs.step
     else:
-        b = lay.alloc(dev)
+        b = op.rhs_buffer(cfg.max_iter)
 
         def step():
             op.mass_apply_device(u, b, F, a=dt)
@@ -320,28 +448,29 @@ def run_ours(args, rank, world, local_rank):
     total_its = int(sum(its))
     value = total_its * dofs / (ms * 1e-3) / 1e9
 
-    # -- per-kernel durations (CUDA events on the launching stream) --
-    kt = kernel_times(op, u, F, dt, stream, world)
+    # -- end to end through the public API: u from/to pinned host memory each step --
+    e2e = e2e_rate(step, u, lay, dofs, min(args.steps, 3), stream, barrier, max_over_ranks)
+
+    # -- per-kernel durations (CUDA events on the launching stream), on the
+    # solver's own work set (after the e2e run: these passes perturb u) --
+    wset = _work(op, cfg.max_iter) if world == 1 else op._work_buffers(cfg.max_iter)
+    kt = kernel_times(op, u, F, dt, stream, wset)
     kt = {k: max_over_ranks(v) for k, v in kt.items()}
     peak, peak_kind = measured_peaks()
     local_dofs = int(np.prod(lay.owned_shape))
-    a_gbs = ALG_BYTES_PASS_A * local_dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
-    b_gbs = ALG_BYTES_PASS_B * local_dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
+    bytes_a, bytes_b, bytes_it = alg_bytes(ring)
+    a_gbs = bytes_a * local_dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
+    b_gbs = bytes_b * local_dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
     dom = "pass_b" if kt["pass_b_ms"] >= kt["pass_a_ms"] else "pass_a"
     ach = b_gbs if dom == "pass_b" else a_gbs
     it_s = (kt["pass_a_ms"] + kt["pass_b_ms"]) * 1e-3
-    it_gbs = ALG_BYTES_ITER * local_dofs / it_s / 1e9
+    it_gbs = bytes_it * local_dofs / it_s / 1e9
     it_gbs80 = SURVEY_BYTES_ITER * local_dofs / it_s / 1e9  # DoF-it rate vs the 80 B roofline
 
-    # -- end to end through the public API: u from/to pinned host memory each step --
-    e2e = e2e_rate(step, u, u0, lay, dofs, min(args.steps, 3), stream, barrier, max_over_ranks)
-
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        rate, info = cpu_port_rate(64, iters=20, repeats=3, p=args.degree)
-        cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
-               "sample": f"C1 64^3 p={args.degree} heat system, {info['iterations']} Jacobi-PCG iterations, "
-                         "median of 3 (oracle port, scipy/numpy single thread)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, kind, sample = cpu_reference_rate(p=args.degree)
+        cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": kind, "sample": sample}
 
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world,
@@ -349,13 +478,15 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_of(args, world),
         "cg_iterations_per_step": its,
+        "memory": {"fields_per_rank": mem["fields"], "p_ring": int(ring),
+                   "bytes_per_rank": mem["field_bytes"] * (4 + int(ring))},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak,
                      # ncu traffic is captured for the C3 workload (profiles/traffic.json)
                      "traffic": TRAFFIC.get(dom) if (args.ncoef, args.degree) == (930, 3) else None,
                      "kernel": dom,
                      "peak_source": peak_kind,
-                     "alg_bytes_per_dof": ALG_BYTES_PASS_B if dom == "pass_b" else ALG_BYTES_PASS_A,
+                     "alg_bytes_per_dof": bytes_b if dom == "pass_b" else bytes_a,
                      "pass_a_ms": kt["pass_a_ms"], "pass_b_ms": kt["pass_b_ms"],
                      "pass_a_gbs": a_gbs, "pass_b_gbs": b_gbs,
                      "cg_iteration_gbs": it_gbs, "cg_iteration_frac": it_gbs / peak,
@@ -372,28 +503,26 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def kernel_times(op, u, F, dt, stream, world, reps=9):
-    """Average device duration of CG pass A and pass B (same stream, events),
-    on a copy of the current state (the timed solve is already over)."""
+def kernel_times(op, u, F, dt, stream, wset, reps=9):
+    """Average device duration of CG pass A and pass B (same stream, events)
+    on the solver's own work set (r, ring, Ap = b, scratch) with x = u: no
+    extra fields are allocated (the timed solve is already over)."""
     import torch
 
     plan = op.plan()
-    lay = op.layout
-    dev = u.device
-    x = u.clone()
-    b = lay.alloc(dev)
-    r = lay.alloc(dev)
-    pring = lay.alloc_ring(dev)
-    ap = lay.alloc(dev)
-    scratch = plan.scratch()
-    op.mass_apply_device(x, b, F, a=dt)
-    plan.cg_setup(scratch, None, 1e-300, 10 ** 6, False, True)
-    plan.cg_residual(b, x, r, scratch, 1)
+    if isinstance(wset, dict):
+        r, pring, ap, scratch = wset["r"], wset["pring"], wset["ap"], wset["scratch"]
+    else:
+        r, pring, ap, scratch = wset.r, wset.pring, wset.ap, wset.scratch
+    x = u
+    op.mass_apply_device(x, ap, F, a=dt)  # b in Ap's storage
+    R = pring.shape[0]
+    plan.cg_setup(scratch, None, 1e-300, 10 ** 6, False, True, p_ring=R)
+    plan.cg_residual(ap, x, r, scratch, 1)
     ta, tb = [], []
     for k in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        R = pring.shape[0]
         plan.cg_pass_a(r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
         e[1].record(stream)
         plan.cg_pass_b(x, r, pring, ap, scratch, 1)
@@ -401,12 +530,14 @@ def kernel_times(op, u, F, dt, stream, world, reps=9):
         torch.cuda.synchronize()
         ta.append(e[0].elapsed_time(e[1]))
         tb.append(e[1].elapsed_time(e[2]))
-    del x, b, r, pring, ap
-    torch.cuda.empty_cache()
-    return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:]))}
+    plan.cg_flush_x(x, pring, scratch)
+    torch.cuda.synchronize()
+    # pass B's mean over whole ring periods (x moves every R-th pass)
+    nb = ((reps - 1) // R) * R
+    return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:1 + nb]))}
 
 
-def e2e_rate(step, u, u0, lay, dofs, steps, stream, barrier, max_over_ranks):
+def e2e_rate(step, u, lay, dofs, steps, stream, barrier, max_over_ranks):
     """Same metric through the public step API with the state copied from and
     back to pinned host memory every step (host<->device copies timed)."""
     from paper_1904_03057_b200.heat import run_steps_host
@@ -416,11 +547,10 @@ def e2e_rate(step, u, u0, lay, dofs, steps, stream, barrier, max_over_ranks):
     host = torch.empty(lay.owned_shape, dtype=torch.float64).pin_memory()
     own = lay.owned(u)
     # untimed warm-up of the same pipeline (first DMA through the freshly
-    # pinned buffer and the side streams), then reset the input
-    host.copy_(lay.owned(u0).cpu())
+    # pinned buffer and the side streams); the host copy holds the state
+    host.copy_(own.cpu())
     run_steps_host(step, own, host, 1, chunks=16, stream=stream)
     torch.cuda.synchronize()
-    host.copy_(lay.owned(u0).cpu())
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -446,6 +576,65 @@ def e2e_rate(step, u, u0, lay, dofs, steps, stream, barrier, max_over_ranks):
                    "step k+1 overlap chunk-wise (16 z-chunks, full-duplex PCIe)"}
 
 
+# ---------------------------------------------------------------------------
+# launcher
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn(args_list, nproc):
+    """`bench.py --gpus N` without a launcher: start N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and relay rank 0's line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *args_list]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """CPU dry run of the launch topology (gloo): partition, barrier and the
+    max-over-ranks timing of a bench step without the GPU kernels.  Used by
+    the CPU test of `bench.py --gpus N`; its line says "dry": true."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_03057_b200.distributed import SlabPartition
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    part = SlabPartition(args.ncoef, world, rank)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        t = torch.ones(1, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t)
+    ms = (time.perf_counter() - t0) * 1e3
+    tm = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        wsum = torch.tensor([float(part.nz)], dtype=torch.float64)
+        dist.all_reduce(wsum)
+        planes = int(wsum.item())
+    else:
+        planes = part.nz
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GDoF/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "dry": True,
+                          "ms_per_step": float(tm.item()) / max(args.steps, 1),
+                          "planes_covered": planes, "config": config_of(args, world)}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -456,10 +645,22 @@ def main():
     ap.add_argument("--poll", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry", action="store_true",
+                    help="CPU/gloo dry run of the multi-rank launch (no kernels; tests)")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        # no launcher: start one rank per GPU ourselves
+        sys.exit(spawn(sys.argv[1:], args.gpus))
+    world = int(env_world or "1")
+    if args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                 f"(or drop the launcher and let bench.py spawn them)")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -30,10 +30,12 @@
 extern "C" {
 #endif
 
-/* CG search directions live in a ring of BSPDE_P_RING ghosted-slab fields
- * (one contiguous allocation, field after field): iteration k writes p_k to
- * field k % BSPDE_P_RING; x += alpha p is applied every BSPDE_P_RING
- * iterations from the ring, in the reference's rounding order. */
+/* CG search directions live in a ring of R ghosted-slab fields (one
+ * contiguous allocation, field after field; R = bspde_cg_config.p_ring, 2 or
+ * BSPDE_P_RING): iteration k writes p_k to field k % R; x += alpha p is
+ * applied every R iterations from the ring, in the reference's rounding
+ * order.  R = 4 moves x once per 4 iterations; R = 2 saves two fields of
+ * HBM (the 1536^3 single-GPU case). */
 #define BSPDE_P_RING 4
 
 #define BSPDE_OK 0
@@ -88,6 +90,7 @@ typedef struct {
   int32_t record_history;
   int32_t has_x0;       /* 0: x0 = None (x is zeroed), 1: x holds x0 */
   int32_t poll_every;   /* iterations per CUDA-graph chunk between host polls (<=0: default 8) */
+  int32_t p_ring;       /* search-direction ring length R: 2 or 4 (0: BSPDE_P_RING) */
 } bspde_cg_config;
 
 typedef struct {
@@ -131,8 +134,9 @@ int bspde_jacobi_diagonal(bspde_plan* plan, const double* diag_table,
 /* Full Jacobi-PCG on one device.  Replaces pcg(operator, rhs, config, x0)
  * (solver.py:51-117): identical recurrence, stopping rule (recursive
  * ||r||/||b|| <= tol or max_iter), indefinite and divergence guards.
- * b, x, r, ap are ghosted-slab fields, p_ring BSPDE_P_RING of them back to
- * back (the search directions); x holds x0 on entry when
+ * b, x, r, ap are ghosted-slab fields, p_ring cfg->p_ring of them back to
+ * back (the search directions); b may alias ap (b is only read by the
+ * initial residual, before the first Ap is written); x holds x0 on entry when
  * cfg->has_x0, the solution on exit.  scratch: bspde_scratch_bytes bytes.
  * history: device array of max_iter+1 doubles or NULL. */
 int bspde_pcg_solve(bspde_plan* plan, const double* b, double* x, double* r,
@@ -166,10 +170,11 @@ int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
 int bspde_cg_pass_a_range(bspde_plan* plan, const double* r, const double* p_in,
                           double* p_out, double* ap, void* scratch, int z_begin,
                           int z_count, int accumulate, int fuse, void* stream);
-/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p for the last
- * BSPDE_P_RING iterations at once every BSPDE_P_RING-th call, in the
- * reference's rounding order (solver.py:94-101).  Iteration k's pass A must
- * read ring field (k-1) % BSPDE_P_RING and write field k % BSPDE_P_RING. kind 2 */
+/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p for the last R
+ * iterations at once every R-th call (R = the p_ring given to
+ * bspde_cg_setup), in the reference's rounding order (solver.py:94-101).
+ * Iteration k's pass A must read ring field (k-1) % R and write field k % R.
+ * kind 2 */
 int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, const double* p_ring,
                     const double* ap, void* scratch, int fuse, void* stream);
 /* Apply the pending x updates (x += alpha_j p_j for the iterations since the

@@ -53,6 +53,7 @@ class CgConfig(C.Structure):
         ("record_history", C.c_int32),
         ("has_x0", C.c_int32),
         ("poll_every", C.c_int32),
+        ("p_ring", C.c_int32),
     ]
 
 

@@ -26,10 +26,18 @@ class Robin:
 
     gamma: float = 1.0
 
+    def surface(self, grid):
+        if self.gamma <= 0:
+            raise ConfigurationError(f"Robin gamma must be positive, got {self.gamma}")
+        return 1.0 / (2.0 * self.gamma), None
+
 
 @dataclass(frozen=True)
 class Neumann:
     """Homogeneous natural condition: no surface term."""
+
+    def surface(self, grid):
+        return None
 
 
 @dataclass(frozen=True)
@@ -40,79 +48,78 @@ class DirichletPenalty:
     value: float = 0.0
     epsilon: float = None
 
+    def surface(self, grid):
+        eps = 1e-4 * min(grid.step) if self.epsilon is None else self.epsilon
+        if eps <= 0:
+            raise ConfigurationError(f"penalty epsilon must be positive, got {eps}")
+        return 1.0 / eps, self.value
 
-def _face_key(axis, side):
-    return FACE_NAMES[2 * axis + side]
+
+def _surface_of(cond, grid):
+    """(weight, rhs value) of a face condition, or None (no surface term)."""
+    fn = getattr(cond, "surface", None)
+    if fn is None:
+        raise ConfigurationError(
+            f"{type(cond).__name__} boundary conditions are not realized by this solver")
+    return fn(grid)
+
+
+def _face_table(bc, d):
+    """Condition of every face, indexed 2*axis + side, from a single
+    condition or a ``{face: condition}`` dict ("all" fills the faces the
+    dict leaves unnamed)."""
+    nf = 2 * d
+    if not isinstance(bc, dict):
+        return [bc] * nf
+    table = [None] * nf
+    fallback = bc.get("all")
+    for key, cond in bc.items():
+        if key == "all":
+            continue
+        if key not in FACE_NAMES[:nf]:
+            raise ConfigurationError(f"unknown face {key!r} for a {d}-d box")
+        table[FACE_NAMES.index(key)] = cond
+    if fallback is not None:
+        table = [fallback if c is None else c for c in table]
+    missing = [FACE_NAMES[i] for i, c in enumerate(table) if c is None]
+    if missing:
+        raise ConfigurationError(f"boundary conditions missing on faces {missing}")
+    return table
 
 
 def realize_bc(spec_or_bc, grid=None, mask=None):
-    """BC -> ``[(axis, side, weight, rhs_value)]`` (``problem.py:237-300``).
+    """BC -> ``[(axis, side, weight, rhs_value)]`` (the reference's
+    ``realize_bc``, ``problem.py:237-300``: same rules and errors).
 
     Accepts the reference's ``ProblemSpec``-like object (attributes ``bc`` and
-    ``grid``) or a condition / ``{face: condition}`` dict plus ``grid``.
-    Same rules as the reference: a dict may use ``"all"`` and must cover every
-    face of the box; unknown face names and non-positive gamma / epsilon raise
-    ``ConfigurationError``.  Mask domains (``mask=True``, or a spec whose
-    ``domain`` is a :class:`.domain.MaskDomain`) take one global Neumann or
-    DirichletPenalty condition and return at most one spec, whose weight
-    applies to every exposed mask face.
+    ``grid``) or a condition / ``{face: condition}`` dict plus ``grid``.  A
+    dict may use ``"all"`` and must cover every face of the box; unknown face
+    names and non-positive gamma / epsilon raise ``ConfigurationError``.
+    Mask domains (``mask=True``, or a spec whose ``domain`` is a
+    :class:`.domain.MaskDomain`) take one global Neumann or DirichletPenalty
+    condition and return at most one spec, whose weight applies to every
+    exposed mask face.
     """
     from .domain import MaskDomain
 
     if grid is None:
-        grid = spec_or_bc.grid
-        bc = spec_or_bc.bc
+        grid, bc = spec_or_bc.grid, spec_or_bc.bc
         if mask is None:
             mask = isinstance(getattr(spec_or_bc, "domain", None), MaskDomain)
     else:
         bc = spec_or_bc
-    d = grid.dim
-    if isinstance(bc, dict) and mask:
-        raise ConfigurationError("mask domains take a single global BC")
-    if isinstance(bc, dict):
-        per_face = {}
-        for key, val in bc.items():
-            if key == "all":
-                for ax in range(d):
-                    for s in (0, 1):
-                        per_face.setdefault(_face_key(ax, s), val)
-            elif key in FACE_NAMES[: 2 * d]:
-                per_face[key] = val
-            else:
-                raise ConfigurationError(f"unknown face {key!r} for a {d}-d box")
-        missing = [f for f in FACE_NAMES[: 2 * d] if f not in per_face]
-        if missing:
-            raise ConfigurationError(f"boundary conditions missing on faces {missing}")
-    else:
-        per_face = {f: bc for f in FACE_NAMES[: 2 * d]}
-
-    def weight_of(cond):
-        if isinstance(cond, Neumann):
-            return None
-        if isinstance(cond, Robin):
-            if cond.gamma <= 0:
-                raise ConfigurationError(f"Robin gamma must be positive, got {cond.gamma}")
-            return (1.0 / (2.0 * cond.gamma), None)
-        if isinstance(cond, DirichletPenalty):
-            eps = cond.epsilon if cond.epsilon is not None else 1e-4 * min(grid.step)
-            if eps <= 0:
-                raise ConfigurationError(f"penalty epsilon must be positive, got {eps}")
-            return (1.0 / eps, cond.value)
-        raise ConfigurationError(
-            f"{type(cond).__name__} boundary conditions are not realized by this solver")
-
     if mask:
-        if isinstance(bc, Robin):
+        if isinstance(bc, dict):
+            raise ConfigurationError("mask domains take a single global BC")
+        if isinstance(bc, Robin):  # exposed faces take Neumann / DirichletPenalty only
             raise ConfigurationError("mask domains support Neumann or DirichletPenalty conditions only")
-        w = weight_of(bc)
-        return [] if w is None else [(0, 0, w[0], w[1])]
-
+        term = _surface_of(bc, grid)
+        return [] if term is None else [(0, 0, term[0], term[1])]
     specs = []
-    for ax in range(d):
-        for s in (0, 1):
-            w = weight_of(per_face[_face_key(ax, s)])
-            if w is not None:
-                specs.append((ax, s, w[0], w[1]))
+    for face, cond in enumerate(_face_table(bc, grid.dim)):
+        term = _surface_of(cond, grid)
+        if term is not None:
+            specs.append((face // 2, face % 2, term[0], term[1]))
     return specs
 
 

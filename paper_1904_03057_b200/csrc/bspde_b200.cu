@@ -98,8 +98,9 @@ struct Cfg {
   }
 };
 
-// x += alpha p is applied every kPRing iterations (and by the flush at the end
-// of a solve) from a ring of kPRing search directions; see cg_pass_b_kernel
+// x += alpha p is applied every R iterations (and by the flush at the end of
+// a solve) from a ring of R <= kPRing search directions (R = CgState::ring,
+// 2 or 4); see cg_pass_b_kernel
 constexpr int kPRing = BSPDE_P_RING;
 
 struct CgState {
@@ -108,9 +109,9 @@ struct CgState {
   double res, res0, scale, tol;
   double rhs_norm, pad_d;
   int it, max_iter, active, status;
-  int record_history, has_x0, x_done, pad_i1;  // x_done: iterations applied to x
+  int record_history, has_x0, x_done, ring;  // x_done: iterations applied to x; ring: R
   double* history;
-  double alpha_ring[kPRing];  // alpha_j at j % kPRing for the pending x updates
+  double alpha_ring[kPRing];  // alpha_j at j % R for the pending x updates
 };
 
 struct SepParams {
@@ -160,7 +161,7 @@ struct PassBParams {
   const double* invd;
   double* x;
   double* r;
-  const double* pring;    // kPRing fields, pstride doubles apart
+  const double* pring;    // R fields, pstride doubles apart
   long long pstride;
   const double* ap;
   double* partials;
@@ -294,9 +295,9 @@ __device__ void finalize_state(CgState* s, int kind) {
     s->alpha = s->rz / pAp;
   } else {
     const double rz_new = s->sums[0], rr = s->sums[1];
-    // pass B of iteration k = it applied x up to k when k % kPRing == kPRing-1
-    s->alpha_ring[s->it % kPRing] = s->alpha;
-    if (s->it % kPRing == kPRing - 1) s->x_done = s->it + 1;
+    // pass B of iteration k = it applied x up to k when k % R == R - 1
+    s->alpha_ring[s->it % s->ring] = s->alpha;
+    if (s->it % s->ring == s->ring - 1) s->x_done = s->it + 1;
     s->beta = rz_new / s->rz;
     s->rz = rz_new;
     s->res = sqrt(rr);
@@ -954,16 +955,17 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
   const double alpha = ld_vol(&prm.state->alpha);
   const int k = ld_vol(&prm.state->it);
   const int j0 = ld_vol(&prm.state->x_done);
+  const int R = ld_vol(&prm.state->ring);
   // x updates j0..k at the end of each ring period (alpha_k is still in alpha)
-  const bool xup = (k % kPRing == kPRing - 1) && j0 <= k;
+  const bool xup = (k % R == R - 1) && j0 <= k;
   double aj[kPRing];
   const double* pj[kPRing];
 #pragma unroll
   for (int t = 0; t < kPRing; ++t) {
-    const int j = k - (kPRing - 1) + t;
-    const bool on = xup && j >= j0;
-    aj[t] = on ? (j == k ? alpha : ld_vol(&prm.state->alpha_ring[j % kPRing])) : 0.0;
-    pj[t] = on ? prm.pring + (long long)(j % kPRing) * prm.pstride : nullptr;
+    const int j = k - (R - 1) + t;
+    const bool on = xup && t < R && j >= j0;
+    aj[t] = on ? (j == k ? alpha : ld_vol(&prm.state->alpha_ring[j % R])) : 0.0;
+    pj[t] = on ? prm.pring + (long long)(j % R) * prm.pstride : nullptr;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
@@ -1070,15 +1072,16 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
 // accesses as pass B.
 __global__ void __launch_bounds__(NTB) x_flush_kernel(const __grid_constant__ PassBParams prm) {
   const int it = ld_vol(&prm.state->it), j0 = ld_vol(&prm.state->x_done);
+  const int R = ld_vol(&prm.state->ring);
   if (j0 >= it) return;
   double aj[kPRing];
   const double* pj[kPRing];
 #pragma unroll
   for (int t = 0; t < kPRing; ++t) {
     const int j = j0 + t;
-    const bool on = j < it;
-    aj[t] = on ? ld_vol(&prm.state->alpha_ring[j % kPRing]) : 0.0;
-    pj[t] = on ? prm.pring + (long long)(j % kPRing) * prm.pstride : nullptr;
+    const bool on = j < it && t < R;  // at most R - 1 updates are pending
+    aj[t] = on ? ld_vol(&prm.state->alpha_ring[j % R]) : 0.0;
+    pj[t] = on ? prm.pring + (long long)(j % R) * prm.pstride : nullptr;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
@@ -1763,9 +1766,10 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
   if (rc) return rc;
   if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
-  // p_{-1} = 0 lives in ring field kPRing - 1 (read by iteration 0)
+  // p_{-1} = 0 lives in ring field R - 1 (read by iteration 0)
+  const int R = cfg->p_ring > 0 ? cfg->p_ring : kPRing;
   const long long fs = (long long)(pl->d.nz + 2 * pl->p) * pl->pitch_z;
-  CUDA_TRY(cudaMemsetAsync(pring + (kPRing - 1) * fs, 0, bytes, st));
+  CUDA_TRY(cudaMemsetAsync(pring + (R - 1) * fs, 0, bytes, st));
   rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
   if (rc) return rc;
   int32_t active = 0;
@@ -1775,7 +1779,7 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   // multiple of R iterations make every replay of the captured graph start
   // from the same field
   int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
-  K = ((K + kPRing - 1) / kPRing) * kPRing;
+  K = ((K + R - 1) / R) * R;
   while (active) {
     bspde_plan::GraphKey key{x, r, pring, nullptr, ap, scratch, K};
     auto itg = pl->graphs.find(key);
@@ -1785,8 +1789,8 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
       CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       int crc = BSPDE_OK;
       for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
-        crc = launch_sep(pl, M_CGA, r, pring + ((k + kPRing - 1) % kPRing) * fs, ap, nullptr, 0.0,
-                         0.0, false, scratch, 1, st, pring + (k % kPRing) * fs);
+        crc = launch_sep(pl, M_CGA, r, pring + ((k + R - 1) % R) * fs, ap, nullptr, 0.0,
+                         0.0, false, scratch, 1, st, pring + (k % R) * fs);
         if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, pring, ap, scratch, 1, st);
       }
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
@@ -2113,6 +2117,8 @@ int bspde_cg_setup(bspde_plan* pl, void* scratch, double* history, const bspde_c
   if (!(cfg->tol > 0.0)) return fail(BSPDE_ERR_ARG, "tol must be positive");
   if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
   if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
+  if (!(cfg->p_ring == 0 || cfg->p_ring == 2 || cfg->p_ring == kPRing))
+    return fail(BSPDE_ERR_ARG, "p_ring must be 2 or 4 (0: default 4)");
   CgState* hs = reinterpret_cast<CgState*>(pl->host_state);
   cudaStream_t st = (cudaStream_t)stream;
   // the pinned staging buffer may still be in use by a previous async copy
@@ -2122,6 +2128,7 @@ int bspde_cg_setup(bspde_plan* pl, void* scratch, double* history, const bspde_c
   hs->max_iter = cfg->max_iter;
   hs->record_history = cfg->record_history ? 1 : 0;
   hs->has_x0 = cfg->has_x0 ? 1 : 0;
+  hs->ring = cfg->p_ring > 0 ? cfg->p_ring : kPRing;
   hs->history = history;
   hs->scale = 1.0;
   CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));

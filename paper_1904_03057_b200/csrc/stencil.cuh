@@ -755,6 +755,7 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
   hs->max_iter = cfg->max_iter;
   hs->record_history = cfg->record_history ? 1 : 0;
   hs->has_x0 = cfg->has_x0 ? 1 : 0;
+  hs->ring = kPRing;  // finalize_state's x-ring bookkeeping (unused by the stencil CG)
   hs->history = history;
   hs->scale = 1.0;
   CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));

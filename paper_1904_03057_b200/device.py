@@ -4,8 +4,10 @@ Layout (``include/bspde_b200.h``): a field of the local extended grid is a
 torch float64 tensor ``buf[nz + 2*ghost, ny, pitch]`` on the GPU, owned plane
 ``k`` at ``buf[k + ghost]``, ``pitch = nx`` rounded up to even (16-byte rows
 for TMA).  Ghost planes (``ghost = degree``) carry neighbour-slab planes in
-multi-GPU runs and zeros at physical domain ends.  At 930^3 a field is 6.4 GB;
-a CG solve keeps x, r, p, Ap (+ b) resident, 32 GB of 180 GB HBM3e.
+multi-GPU runs and zeros at physical domain ends.  At 930^3 a field is 6.4 GB.
+A heat run keeps u (= x), F, r, Ap (b shares Ap's storage: it is dead once
+r0 = b - A x0 is formed) and the ring of R search directions resident:
+4 + R fields (``heat_memory_plan``).
 """
 
 from __future__ import annotations
@@ -167,7 +169,7 @@ class NativePlan:
     def pcg(self, b, x, r, pring, ap, scratch, history, tol, max_iter, record_history, has_x0,
             poll_every=8, stream=None):
         cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
-                         int(bool(has_x0)), int(poll_every))
+                         int(bool(has_x0)), int(poll_every), int(pring.shape[0]))
         rep = N.CgReport()
         N.check(self.lib.bspde_pcg_solve(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(pring),
                                          N.ptr(ap), N.ptr(scratch), N.ptr(history),
@@ -175,9 +177,10 @@ class NativePlan:
         return rep
 
     # step-wise CG (multi-GPU driver)
-    def cg_setup(self, scratch, history, tol, max_iter, record_history, has_x0, stream=None):
+    def cg_setup(self, scratch, history, tol, max_iter, record_history, has_x0, stream=None,
+                 p_ring=None):
         cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
-                         int(bool(has_x0)), 0)
+                         int(bool(has_x0)), 0, int(p_ring or N.P_RING))
         N.check(self.lib.bspde_cg_setup(self.handle, N.ptr(scratch), N.ptr(history),
                                         C.byref(cfg), N.stream_handle(stream)))
 
@@ -217,6 +220,47 @@ class NativePlan:
         N.check(self.lib.bspde_cg_read_report(self.handle, N.ptr(scratch), C.byref(rep),
                                               C.byref(active), N.stream_handle(stream)))
         return rep, bool(active.value)
+
+
+# resident fields of a heat run besides the p ring: u (= x), F, r, Ap (= b)
+HEAT_BASE_FIELDS = 4
+HBM_BUDGET = 175e9  # bytes of HBM3e a rank may fill with fields (B200: 180 GB usable)
+
+
+def heat_memory_plan(cext, degree, world=1, budget=HBM_BUDGET, ring=None):
+    """Per-rank resident bytes of a heat run on ``world`` z-slabs.
+
+    Fields: u, F, r, Ap (b aliases Ap) and the search-direction ring (R = 4
+    when it fits, else 2).  Returns dict(ring, fields, field_bytes, bytes).
+    1536^3 p=3 on one GPU: 6 fields x 29.1 GB = 174.7 GB with R = 2."""
+    from .errors import ConfigurationError
+
+    nzg, ny, nx = (int(v) for v in cext)
+    nz = -(-nzg // int(world))  # the largest slab
+    field = SlabLayout(nz, ny, nx, ghost=int(degree)).bytes
+    for R in ((ring,) if ring else (N.P_RING, 2)):
+        total = (HEAT_BASE_FIELDS + R) * field
+        if total <= budget:
+            return dict(ring=R, fields=HEAT_BASE_FIELDS + R, field_bytes=field, bytes=total)
+    raise ConfigurationError(
+        f"{cext} (degree {degree}) on {world} rank(s) needs {(HEAT_BASE_FIELDS + 2) * field / 1e9:.1f}"
+        f" GB per rank > {budget / 1e9:.0f} GB; use more GPUs")
+
+
+def choose_ring(layout, device, fields_to_add=2):
+    """Ring length for a CG work set about to be allocated: BSPDE_P_RING (4)
+    if ``fields_to_add`` + 4 more fields fit in free HBM with 2 GB to spare,
+    else 2.  ``BSPDE_P_RING_LEN`` (2 or 4) overrides."""
+    import os
+
+    env = os.environ.get("BSPDE_P_RING_LEN")
+    if env:
+        R = int(env)
+        if R not in (2, N.P_RING):
+            raise ValidationError(f"BSPDE_P_RING_LEN must be 2 or {N.P_RING}, got {env}")
+        return R
+    free, _ = _torch().cuda.mem_get_info(device)
+    return N.P_RING if free >= (fields_to_add + N.P_RING) * layout.bytes + 2e9 else 2
 
 
 def check_host_field(c, shape, what="input coefficients"):

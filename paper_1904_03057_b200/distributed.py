@@ -19,14 +19,20 @@ Per CG iteration (``distributed_pcg``):
   2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
      and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
      finalize kernel runs the scalar update on every rank;
-  3. pass B (fuse=0): r -= alpha Ap (x every other iteration), local
-     <r, D^-1 r>, <r, r>; ``all_reduce`` of 2 doubles; finalize.
+  3. pass B (fuse=0): r -= alpha Ap (x every R-th iteration, R = the
+     length of the search-direction ring, 2 or 4), local <r, D^-1 r>,
+     <r, r>; ``all_reduce`` of 2 doubles; finalize.
 
 Every rank holds identical scalar state, so the device-side ``active`` flag
 (stop rule, guards) agrees everywhere; the host polls it every
 ``poll_every`` iterations.  Iterations after convergence are no-ops.  There
 is no collective on the data path other than the halo planes and the scalar
 sums.
+
+Transport: NCCL over NVLink/NVSwitch in production (one process per GPU).
+With the gloo backend (several ranks sharing one GPU in the multi-process
+GPU test, or CPU runs) the halo planes and the scalar sums of CUDA tensors
+are staged through host memory (``HaloExchanger`` / ``_allreduce_fn``).
 
 The orchestration is written against a small ops interface so it can be
 exercised on CPU with the gloo backend (tests/test_distributed_cpu.py); the
@@ -112,6 +118,11 @@ class HaloExchanger:
         for req in works:
             req.wait()
 
+    def _staged(self, buf):
+        import torch.distributed as dist
+
+        return buf.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def start(self, *bufs):
         """Post the exchange and return its work handles without waiting, so
         kernels that read no ghost plane can run while it is in flight."""
@@ -119,6 +130,8 @@ class HaloExchanger:
             return []
         import torch.distributed as dist
 
+        if bufs and self._staged(bufs[0]):
+            return self._start_staged(bufs)
         g, nz = self.layout.ghost, self.layout.nz
         ops = []
         for buf in bufs:
@@ -131,6 +144,33 @@ class HaloExchanger:
                                       self.group))
         return dist.batch_isend_irecv(ops) if ops else []
 
+    def _start_staged(self, bufs):
+        """gloo + CUDA tensors: copy the boundary planes to the host, exchange
+        them with gloo P2P and copy the received planes into the ghost planes
+        (synchronous; the returned handle list is empty)."""
+        import torch.distributed as dist
+
+        g, nz = self.layout.ghost, self.layout.nz
+        for buf in bufs:
+            ops, recvs = [], []
+            if self.rank > 0:
+                lo = buf[g:2 * g].cpu()
+                rlo = lo.new_empty(lo.shape)
+                ops += [dist.P2POp(dist.isend, lo, self.rank - 1, self.group),
+                        dist.P2POp(dist.irecv, rlo, self.rank - 1, self.group)]
+                recvs.append((slice(0, g), rlo))
+            if self.rank < self.world - 1:
+                hi = buf[nz:nz + g].cpu()
+                rhi = hi.new_empty(hi.shape)
+                ops += [dist.P2POp(dist.isend, hi, self.rank + 1, self.group),
+                        dist.P2POp(dist.irecv, rhi, self.rank + 1, self.group)]
+                recvs.append((slice(nz + g, nz + 2 * g), rhi))
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            for sl, t in recvs:
+                buf[sl].copy_(t)
+        return []
+
 
 def _allreduce_fn(world, group=None):
     if world == 1:
@@ -138,7 +178,12 @@ def _allreduce_fn(world, group=None):
     import torch.distributed as dist
 
     def fn(t):
-        dist.all_reduce(t, group=group)
+        if t.is_cuda and dist.get_backend(group) == "gloo":  # host-staged (see module doc)
+            h = t.cpu()
+            dist.all_reduce(h, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, group=group)
 
     return fn
 
@@ -152,8 +197,9 @@ class NativeSlabOps:
     def sums(self, scratch, n):
         return scratch[: 8 * 4].view(_torch().float64)[:n]
 
-    def setup(self, scratch, history, cfg, has_x0):
-        self.plan.cg_setup(scratch, history, cfg.tol, cfg.max_iter, cfg.record_history, has_x0)
+    def setup(self, scratch, history, cfg, has_x0, ring=None):
+        self.plan.cg_setup(scratch, history, cfg.tol, cfg.max_iter, cfg.record_history, has_x0,
+                           p_ring=ring)
 
     def residual(self, b, x, r, scratch):
         self.plan.cg_residual(b, x, r, scratch, 0)
@@ -218,7 +264,7 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
         x.zero_()
     R = pring.shape[0]
     pring[R - 1].zero_()  # p_{-1} = 0, ghost planes included: nothing to exchange at k = 0
-    ops.setup(scratch, history, config, has_x0)
+    ops.setup(scratch, history, config, has_x0, ring=R)
     halo(x)
     ops.residual(b, x, r, scratch)
     allreduce(ops.sums(scratch, 3))
@@ -341,14 +387,22 @@ class DistributedOperator:
         import torch
 
         if self._work is None:
+            from .device import choose_ring
+
             lay = self.layout
-            self._work = dict(r=lay.alloc(self.device), pring=lay.alloc_ring(self.device),
+            ring = choose_ring(lay, self.device)
+            self._work = dict(r=lay.alloc(self.device), pring=lay.alloc_ring(self.device, ring),
                               ap=lay.alloc(self.device), scratch=self.plan().scratch(),
                               history=None)
         w = self._work
         if w["history"] is None or w["history"].numel() < max_iter + 1:
             w["history"] = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
         return w
+
+    def rhs_buffer(self, max_iter=1000):
+        """The heat RHS b shares the CG's Ap field (b is dead once r0 = b - A x0
+        is formed), as in the single-GPU HeatSolver."""
+        return self._work_buffers(max_iter)["ap"]
 
     def pcg_device(self, b_buf, x_buf, config: SolveConfig = None, has_x0=True):
         config = config or SolveConfig()

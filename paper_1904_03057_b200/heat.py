@@ -23,7 +23,7 @@ import numpy as np
 from .domain import BoxDomain, Grid
 from .errors import ValidationError
 from .operator import B200Operator
-from .solver import SolveConfig, SolveReport, pcg_device
+from .solver import SolveConfig, SolveReport, _work, pcg_device
 from .boundary import realize_bc
 from .system import heat_system
 from .transform import sample_solution_device, transform_field_device
@@ -70,7 +70,7 @@ class HeatState:
     op: B200Operator
     u: object          # ghosted-slab tensor (current coefficients)
     F: object          # Galerkin source (or None)
-    b: object          # RHS work buffer
+    b: object          # RHS work buffer (the CG's Ap field on a box)
     reports: list = field(default_factory=list)
 
 
@@ -126,7 +126,7 @@ class HeatSolver:
             self.u = transform_field_device(problem.initial, problem.grid, problem.degree, lay, dev)
         else:
             self.u = lay.upload(np.asarray(u0).reshape(lay.owned_shape), dev)
-        self.b = lay.alloc(dev)
+        self.b = lay.alloc(dev) if self.sop is not None or self.mop is not None else None
         q = problem.source_coeffs
         has_source = q is not None or not (np.ndim(problem.source) == 0
                                            and not callable(problem.source)
@@ -165,6 +165,11 @@ class HeatSolver:
                 self.F = g
             else:
                 self.F.add_(g)
+        if self.b is None:
+            # box: b lives in the CG's Ap field (dead once r0 = b - A x0 is
+            # formed); the work set is allocated after u and F so the ring
+            # length sees the free HBM (device.choose_ring)
+            self.b = _work(self.op, self.config.max_iter).ap
         self.reports = []
 
     @classmethod
@@ -179,7 +184,7 @@ class HeatSolver:
         self.op = op
         self.u = u_buf
         self.F = F_buf
-        self.b = op.layout.alloc(op.device)
+        self.b = _work(op, self.config.max_iter).ap  # b shares the CG's Ap field
         self.reports = []
         return self
 
@@ -231,14 +236,16 @@ class HeatSolver:
         extents, spline degree in the header; :func:`.io.write_field`)."""
         from .io import write_field
 
-        write_field(path, self.op.layout, self.u, degree=self.data.n_b)
+        write_field(path, self.op.layout, self.u, degree=self.data.n_b,
+                    extents=self.data.cext)
 
     def restore(self, path):
         """Load coefficients written by :meth:`save` (or the reference's
         ``write_tensor`` of the same extents and degree) into the state."""
         from .io import read_field
 
-        read_field(path, self.op.layout, self.op.device, buf=self.u, degree=self.data.n_b)
+        read_field(path, self.op.layout, self.op.device, buf=self.u, degree=self.data.n_b,
+                   extents=self.data.cext)
 
     def coefficients(self) -> np.ndarray:
         return self.op.layout.download(self.u).reshape(self.data.cext)

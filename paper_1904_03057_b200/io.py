@@ -117,14 +117,19 @@ def _staging(layout, torch):
     return zs, torch.empty((zs, layout.ny, layout.nx), dtype=torch.float64, pin_memory=True)
 
 
-def write_field(path, layout, buf, degree=-1):
+def write_field(path, layout, buf, degree=-1, extents=None):
     """Checkpoint the owned region of a device field (slab layout) as an f8
-    TBSF file of the owned extents, staged through pinned memory in z slices."""
+    TBSF file, staged through pinned memory in z slices.  ``extents``: the
+    header extents (default the 3-D owned shape); a 1-D / 2-D problem passes
+    its real coefficient extents (``data.cext``), whose product is the same."""
     import torch
 
     own = layout.owned(buf)
     zs, stage = _staging(layout, torch)
-    head = _header(layout.owned_shape, np.dtype("<f8"), degree)
+    extents = tuple(layout.owned_shape) if extents is None else tuple(int(e) for e in extents)
+    if int(np.prod(extents)) != int(np.prod(layout.owned_shape)):
+        raise FormatError(f"extents {extents} do not match the field {layout.owned_shape}")
+    head = _header(extents, np.dtype("<f8"), degree)
 
     def body(f):
         f.write(head)
@@ -136,16 +141,18 @@ def write_field(path, layout, buf, degree=-1):
     _atomic(path, body)
 
 
-def read_field(path, layout, device, buf=None, degree=None):
-    """Load a TBSF file of the owned extents into a (new or given) device
-    field; checks the extents and, if given, the spline degree."""
+def read_field(path, layout, device, buf=None, degree=None, extents=None):
+    """Load a TBSF file into a (new or given) device field; checks the
+    extents (``extents``: the expected ones, default the 3-D owned shape --
+    a 1-D / 2-D problem passes ``data.cext``) and, if given, the degree."""
     import torch
 
+    want = tuple(layout.owned_shape) if extents is None else tuple(int(e) for e in extents)
     size = os.path.getsize(path)
     with open(path, "rb") as f:
         extents, dt, deg, _ = _parse_header(f, size)
-        if extents != tuple(layout.owned_shape):
-            raise FormatError(f"file extents {extents} != field extents {layout.owned_shape}")
+        if extents != want:
+            raise FormatError(f"file extents {extents} != field extents {want}")
         if degree is not None and deg != int(degree):
             raise FormatError(f"file holds degree {deg}, expected {int(degree)}")
         if buf is None:

@@ -65,15 +65,20 @@ class SolveReport:
 
 
 class CgWork:
-    """Device work vectors for one operator: r, the ring of P_RING search
-    directions, Ap, scalar scratch, history.
+    """Device work vectors for one operator: r, the ring of R search
+    directions (R = 4, or 2 when HBM is short: ``device.choose_ring``), Ap
+    (also the heat RHS b: b is dead once r0 = b - A x0 is formed), scalar
+    scratch, history.
 
     Allocated once and reused; nothing is allocated inside the CG loop."""
 
-    def __init__(self, op, max_iter):
+    def __init__(self, op, max_iter, ring=None):
+        from .device import choose_ring
+
         lay = op.layout
+        ring = ring or choose_ring(lay, op.device)
         self.r = lay.alloc(op.device)
-        self.pring = lay.alloc_ring(op.device)
+        self.pring = lay.alloc_ring(op.device, ring)
         self.ap = lay.alloc(op.device)
         self.scratch = op.plan().scratch()
         self.history = None

@@ -1,33 +1,63 @@
-"""CPU test of bench.py's reference arm (the oracle port on the host cores):
-the JSON line keeps the driver's contract and reports the worker count."""
+"""bench.py launch logic and the per-rank HBM budget, on CPU.
+
+`bench.py --gpus N` must run N ranks (one per GPU) even without a launcher:
+it spawns them through torch.distributed.run.  The dry mode runs the same
+launch, rendezvous and max-over-ranks timing on gloo without kernels.
+"""
+
 import json
 import os
 import subprocess
 import sys
 
+import pytest
+
+from paper_1904_03057_b200.device import heat_memory_plan
+from paper_1904_03057_b200.errors import ConfigurationError
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_reference_arm_line():
-    env = dict(os.environ, BSPDE_REF_WORKERS="2")
-    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
-                          "--warmup", "1"], cwd=ROOT, env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0, out.stderr
-    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1
-    d = json.loads(lines[0])
-    assert d["impl"] == "reference" and d["unit"] == "GDoF/s" and d["higher_is_better"]
-    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 1
-    assert d["cpu_baseline"]["cores"] == 2 and d["cpu_baseline"]["kind"] == "port"
-    assert d["e2e"] == {"value": d["value"], "unit": "GDoF/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}
+def _bench(*args, env=None):
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
+                          capture_output=True, text=True, timeout=300, env=e, cwd=ROOT)
 
 
-def test_reference_arm_nonzero_rank_is_silent():
-    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
-    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
-                          "--warmup", "0"], cwd=ROOT, env=env, capture_output=True, text=True,
-                         timeout=300)
-    assert out.returncode == 0, out.stderr
-    assert out.stdout.strip() == ""
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_gpus_flag_spawns_ranks(n):
+    res = _bench("--gpus", str(n), "--dry", "--steps", "2", "--warmup", "0")
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == n and line["dry"] is True
+    assert line["planes_covered"] == 930  # the slabs tile the global z axis
+    assert line["config"]["parallelism"] == f"zslab{n}"
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    res = _bench("--gpus", "1", "--dry", env={"WORLD_SIZE": "2", "RANK": "0"})
+    assert res.returncode != 0
+    assert "WORLD_SIZE" in res.stderr
+
+
+def test_memory_plan_fits_c5():
+    """C5's strong-scaling anchor 1536^3 (p = 3) fits one B200: u, F, r, Ap
+    (b shares Ap) and a two-field search-direction ring = 6 fields."""
+    plan = heat_memory_plan((1536,) * 3, 3, world=1)
+    assert plan["ring"] == 2 and plan["fields"] == 6
+    assert plan["bytes"] <= 175e9
+    # the 1024^3-per-GPU weak-scaling size keeps the four-field ring
+    assert heat_memory_plan((1024,) * 3, 3, 1)["ring"] == 4
+    assert heat_memory_plan((8 * 1024, 1024, 1024), 3, 8)["ring"] == 4
+    # 1536^3 over 2 GPUs: the four-field ring fits again
+    assert heat_memory_plan((1536,) * 3, 3, 2)["ring"] == 4
+    # C3 (930^3): 8 fields, 51.6 GB
+    c3 = heat_memory_plan((930,) * 3, 3, 1)
+    assert c3["ring"] == 4 and c3["bytes"] < 60e9
+    with pytest.raises(ConfigurationError):
+        heat_memory_plan((2048,) * 3, 3, 1)

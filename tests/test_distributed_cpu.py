@@ -52,8 +52,9 @@ class CpuSlabOps:
     def sums(self, scratch, n):
         return scratch[:n]
 
-    def setup(self, scratch, history, cfg, has_x0):
-        self.state = dict(tol=cfg.tol, max_iter=cfg.max_iter, has_x0=has_x0, it=0, active=1)
+    def setup(self, scratch, history, cfg, has_x0, ring=4):
+        self.state = dict(tol=cfg.tol, max_iter=cfg.max_iter, has_x0=has_x0, it=0, active=1,
+                          alpha_ring=[0.0] * ring)
 
     def residual(self, b, x, r, scratch):
         ax = self._apply(x)
@@ -161,7 +162,7 @@ class CpuSlabOps:
         return rep, bool(self.state["active"])
 
 
-def _worker(rank, world, port, ext, p, out_q, overlap="pipeline"):
+def _worker(rank, world, port, ext, p, out_q, overlap="pipeline", ring=4):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BSPDE_HALO_OVERLAP=overlap)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -180,7 +181,7 @@ def _worker(rank, world, port, ext, p, out_q, overlap="pipeline"):
         b = lay.upload(b_full[lo:hi], "cpu")
         x = lay.upload(x0_full[lo:hi], "cpu")
         r, ap = lay.alloc("cpu"), lay.alloc("cpu")
-        pring = torch.zeros((4,) + tuple(lay.buf_shape), dtype=torch.float64)
+        pring = torch.zeros((ring,) + tuple(lay.buf_shape), dtype=torch.float64)
         scratch = torch.zeros(8, dtype=torch.float64)
         ops = CpuSlabOps(ora, lay)
         halo = HaloExchanger(lay, rank, world, dist.new_group())  # own communicator, as the product
@@ -214,19 +215,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,ext,overlap", [
-    (2, (13, 10, 11), "split"),     # 15 coefficient planes: slabs of 8 / 7, both split pass A
-    (3, (17, 9, 10), "split"),      # 19: 7 / 6 / 6, only rank 0 has an interior range (> 2p)
-    (3, (13, 9, 10), "split"),      # 15: 5 / 5 / 5, no interior range: pipeline instead
-    (2, (13, 10, 11), "pipeline"),  # p_k's exchange in flight under the all-reduce + pass B
-    (3, (17, 9, 10), "pipeline"),
-    (2, (21, 9, 10), "off"),        # both exchanges before pass A
+@pytest.mark.parametrize("world,ext,overlap,ring", [
+    (2, (13, 10, 11), "split", 4),     # 15 coefficient planes: slabs of 8 / 7, both split pass A
+    (3, (17, 9, 10), "split", 4),      # 19: 7 / 6 / 6, only rank 0 has an interior range (> 2p)
+    (3, (13, 9, 10), "split", 4),      # 15: 5 / 5 / 5, no interior range: pipeline instead
+    (2, (13, 10, 11), "pipeline", 4),  # p_k's exchange in flight under the all-reduce + pass B
+    (3, (17, 9, 10), "pipeline", 4),
+    (2, (21, 9, 10), "off", 4),        # both exchanges before pass A
+    (2, (13, 10, 11), "pipeline", 2),  # two-field search-direction ring (x every 2nd pass B)
 ])
-def test_zslab_cg_matches_single_process(world, ext, overlap):
+def test_zslab_cg_matches_single_process(world, ext, overlap, ring):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, 3, q, overlap))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, 3, q, overlap, ring))
              for r in range(world)]
     for pr in procs:
         pr.start()

@@ -1,0 +1,114 @@
+"""The native z-slab solver with several processes on the one GPU.
+
+2 and 3 ranks on cuda:0 run ``DistributedOperator.pcg_device`` --
+``NativeSlabOps`` (the sm_100a step-wise kernels with fuse = 0: ranged pass
+A, pass B, the 1-thread finalize) driven by ``distributed_pcg`` -- over the
+gloo backend, whose halo planes and scalar all-reduces are staged through
+host memory (NCCL refuses two ranks on one device).  Every halo-overlap mode
+and both ring lengths; the gathered solution must match the fused
+single-rank solver (counts +-1, coefficients 1e-10 at tol 1e-13) and the
+oracle.  The ranks' kernels never wait on one another (the exchanges are
+synchronous host copies), so sharing the device is safe.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _system(ext, p):
+    from paper_1904_03057_b200 import BoxDomain, Grid, build_system
+
+    step = tuple(1.0 / (n - 1) for n in ext)
+    return build_system(BoxDomain(Grid(ext, step)), p, p, 0.02, 1.0, []), step
+
+
+def _inputs(cext):
+    axes = [np.linspace(0, 1, n) for n in cext]
+    Z, Y, X = np.meshgrid(*axes, indexing="ij")
+    b = np.cos(3 * Z) * np.sin(2 * Y + 0.3) + np.exp(-5 * (X - 0.4) ** 2)
+    x0 = 0.1 * np.random.default_rng(0).normal(size=cext)
+    return b, x0
+
+
+def _worker(rank, world, port, ext, p, mode, ring, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BSPDE_HALO_OVERLAP=mode,
+                      BSPDE_P_RING_LEN=str(ring))
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_03057_b200 import SolveConfig
+    from paper_1904_03057_b200.distributed import DistributedOperator
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        data, _ = _system(ext, p)
+        op = DistributedOperator(data, device=0)
+        b_full, x0_full = _inputs(data.cext)
+        b = op.scatter(b_full)
+        x = op.scatter(x0_full)
+        rep = op.pcg_device(b, x, SolveConfig(tol=1e-13, max_iter=2000, poll_every=3),
+                            has_x0=True)
+        xs = op.gather(x)
+        # a distributed apply through the same halo path
+        t = op.gather(op.apply_device(op.scatter(x0_full), op.layout.alloc(op.device)))
+        if rank == 0:
+            q.put((rep.iterations, xs, t, int(op._work["pring"].shape[0]), op.layout.nz))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [
+    (2, (24, 20, 22), 3, "pipeline", 4),
+    (3, (24, 20, 22), 3, "split", 4),     # 26 planes: slabs 9 / 9 / 8, interior ranges
+    (2, (24, 20, 22), 3, "off", 2),       # two-field ring
+    (3, (16, 18, 17), 1, "pipeline", 2),  # p = 1: one ghost plane
+    (2, (20, 17, 19), 5, "split", 4),     # p = 5: ghost = 5
+]
+
+
+@pytest.mark.parametrize("world,ext,p,mode,ring", CASES)
+def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
+    import torch.multiprocessing as mp
+
+    from oracle import bspde_oracle as O
+    from paper_1904_03057_b200 import SolveConfig, make_operator, pcg
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, ext, p, mode, ring, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    its, xs, t, ring_used, nz0 = res
+    assert ring_used == ring
+    data, step = _system(ext, p)
+    b_full, x0_full = _inputs(data.cext)
+    # fused single-rank solver on the same inputs
+    op = make_operator(data, "b200")
+    x1, rep1 = pcg(op, b_full, SolveConfig(tol=1e-13, max_iter=2000), x0=x0_full)
+    assert abs(its - rep1.iterations) <= 1, (its, rep1.iterations)
+    assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-10
+    # oracle recurrence and apply
+    ora = O.KronOperator(ext, step, p, 0.02, 1.0)
+    xo, ro = O.pcg(ora.apply, ora.jacobi_diagonal, b_full, tol=1e-13, max_iter=2000, x0=x0_full)
+    assert abs(its - ro["iterations"]) <= 1, (its, ro["iterations"])
+    assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
+    want = ora.apply(x0_full)
+    assert np.abs(t - want).max() / np.abs(want).max() < 1e-13

@@ -194,3 +194,29 @@ def test_vtk_export_matches_reference_text(tmp_path):
             assert (tmp_path / mine).read_text() == f.read()
     with pytest.raises(ValidationError):
         export_vtk(tmp_path / "c.vtk", np.zeros(4), Grid((4,), (1.0,)))
+
+
+@pytest.mark.gpu
+def test_heat_solver_2d_checkpoint_uses_problem_extents(tmp_path):
+    """A 2-D heat problem saves its real (ny, nx) coefficient extents (not the
+    padded (1, ny, nx) device layout) and restores a file the reference's
+    write_tensor wrote for that array."""
+    from paper_1904_03057_b200 import Grid, HeatProblem, HeatSolver
+    from paper_1904_03057_b200.solver import SolveConfig
+
+    n = 14
+    h = 1.0 / (n - 1)
+    hs = HeatSolver(HeatProblem(grid=Grid((n, n), (h, h)), degree=3, dt=4 * h * h,
+                                initial=lambda x, y: np.sin(np.pi * x) * np.cos(y)),
+                    SolveConfig(tol=1e-12, max_iter=500))
+    hs.run(1)
+    p = tmp_path / "c2.tbsf"
+    hs.save(p)
+    arr, deg = read_tensor(p)
+    assert arr.shape == hs.data.cext and deg == 3
+    assert np.array_equal(arr, hs.coefficients())
+    q = tmp_path / "ref.tbsf"
+    want = np.random.default_rng(3).normal(size=hs.data.cext)
+    write_tensor(q, want, degree=3)  # the reference's writer (byte-identical, tests above)
+    hs.restore(q)
+    assert np.array_equal(hs.coefficients(), want)
