@@ -796,6 +796,14 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   }
 }
 
+// BSPDE_CORE_ITER=0 (measurement build): interior tiles use the generic
+// plane_front / plane_back for every plane
+#ifndef BSPDE_CORE_ITER
+#define BSPDE_CORE_ITER 1
+#endif
+template <int P, int MODE>
+__host__ __device__ constexpr bool C_INVD() { return Cfg<P, MODE>::INVD; }
+
 // the thread that issues the plane TMA loads (lane 0 of one warp): the last
 // warp owns one haloed row fewer in the front half than warps 0..(HY % NW)-1
 #ifndef BSPDE_PROD_WARP
@@ -803,6 +811,210 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
 #endif
 template <int P>
 constexpr int kProdThread = (BSPDE_PROD_WARP < 0 ? Geo<P>::NW + BSPDE_PROD_WARP : BSPDE_PROD_WARP) * 32;
+
+// ---------------------------------------------------------------------------
+// Core iterations of an interior tile.  Iteration j (front of plane j+1 +
+// back of plane j) is "core" when both planes are z-interior rows inside the
+// global grid (and, for the residual, the output plane j - P too): Toeplitz
+// taps on every axis, the interior inverse diagonal, no ghost planes.  The
+// body below is plane_front + plane_back specialised to that case -- the same
+// floating-point operations in the same order (bitwise-identical results),
+// but without class lookups, tile-kind / ghost-plane branches, per-pair
+// index divisions or per-plane 64-bit offset arithmetic, so the compiler sees
+// one straight-line block per plane and can overlap the front's shared-memory
+// latency with the back's FMAs.
+
+// pair offsets of this thread's CG p-formation work in a staged (haloed)
+// plane array (interior, full-height tiles; -1: no pair), fixed per kernel
+template <int P, int MODE>
+__device__ __forceinline__ void core_pform_offsets(int (&pfe)[4]) {
+  using C = Cfg<P, MODE>;
+  constexpr int NW = C::NW, HX = C::HX, HY = C::HY;
+  constexpr int PPR = HX / 2;
+  constexpr int NROW = (HY + NW - 1) / NW;
+  static_assert((NROW * PPR + 31) / 32 <= 4, "p-formation needs more than 4 rounds");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrow = (warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1;
+  const int npair = nrow * PPR;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int t = lane + 32 * h;
+    const int m = t / PPR, q = t - m * PPR;
+    pfe[h] = (t < npair) ? (warp + NW * m) * HX + 2 * q : -1;
+  }
+}
+
+template <int P, int MODE>
+__device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, int j, uint32_t f,
+                                          double (&acc)[2 * P][RPT], double (&pr)[P][RPT],
+                                          double (&dsum)[3], double beta, const int (&pfe)[4],
+                                          double inv0, double* op, double* pp, const double* xp,
+                                          long long py) {
+  using C = Cfg<P, MODE>;
+  constexpr int NW = C::NW, TY = C::TY, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS;
+  constexpr int PX = C::PX, DX = C::DX, S = 2 * P;
+  constexpr bool STIFF = C::STIFF;
+  const TapSrc<P> T{prm};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rg = warp >> 1;
+  const int cxl = (warp & 1) * 32 + lane;
+  (void)TY;
+
+  // epilogue operand prefetch (RESID: b, MASS: f) for output plane j - 2P
+  double auxv[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
+  if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) auxv[i] = __ldcs(xp + i * py);
+  }
+
+  // ---- front of plane j+1: stage wait, p = D^-1 r + beta p_old, x-pass ----
+  {
+    const uint32_t f1 = f + 1;
+    const int s1 = f1 % NS;
+    mbar_wait(&sm.full[s1], (f1 / NS) & 1);
+    const double* stC = sm.stage + (s1 * NA + 0) * C::ARR_D;
+    double* stP = sm.stage + (s1 * NA + (NA - 1)) * C::ARR_D;
+    double* X1 = sm.X + (f1 & 1) * 2 * C::XARR;
+    double* X2 = X1 + C::XARR;
+    if (MODE == M_CGA) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int e = pfe[h];
+        if (e >= 0) {
+          const double2 rv = *reinterpret_cast<const double2*>(stC + e);
+          const double2 qv = *reinterpret_cast<const double2*>(stP + e);
+          double2 pv;
+          pv.x = pdir(rv.x, inv0, qv.x, beta);
+          pv.y = pdir(rv.y, inv0, qv.y, beta);
+          *reinterpret_cast<double2*>(stP + e) = pv;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
+      const int row = warp + NW * m;
+      if (row < HY) {
+        const double* w = stP + row * HX + 2 * lane;
+        double raw[2 * P + 2 + 2 * DX];
+#pragma unroll
+        for (int k = 0; k < P + 1 + DX; ++k) {
+          const double2 t = *reinterpret_cast<const double2*>(w + 2 * k);
+          raw[2 * k] = t.x;
+          raw[2 * k + 1] = t.y;
+        }
+        double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const double s0 = raw[DX + k] + raw[DX + 2 * P - k];
+          const double s1 = raw[DX + 1 + k] + raw[DX + 1 + 2 * P - k];
+          m0 = fma(T.M(k), s0, m0);
+          m1 = fma(T.M(k), s1, m1);
+          if (STIFF) {
+            k0 = fma(T.K(k), s0, k0);
+            k1 = fma(T.K(k), s1, k1);
+          }
+        }
+        m0 = fma(T.M(P), raw[DX + P], m0);
+        m1 = fma(T.M(P), raw[DX + P + 1], m1);
+        if (STIFF) {
+          k0 = fma(T.K(P), raw[DX + P], k0);
+          k1 = fma(T.K(P), raw[DX + P + 1], k1);
+        }
+        *reinterpret_cast<double2*>(X1 + row * TX + 2 * lane) = make_double2(m0, m1);
+        if (STIFF) {
+          const double t0 = fma(prm.cx, k0, prm.c_mass * m0);
+          const double t1 = fma(prm.cx, k1, prm.c_mass * m1);
+          *reinterpret_cast<double2*>(X2 + row * TX + 2 * lane) = make_double2(t0, t1);
+        }
+      }
+    }
+  }
+
+  // ---- back of plane j: y-pass, z ring, epilogue of output plane j - 2P ----
+  const double* X1 = sm.X + (f & 1) * 2 * C::XARR;
+  const double* X2 = X1 + C::XARR;
+  double wm[RPT], wa[RPT], out[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    wm[i] = 0.0;
+    wa[i] = 0.0;
+  }
+  {
+    const double* x1c = X1 + (rg * RPT) * TX + cxl;
+    const double* x2c = X2 + (rg * RPT) * TX + cxl;
+#pragma unroll
+    for (int rr = 0; rr < RPT + 2 * P; ++rr) {
+      const double a1 = x1c[rr * TX];
+      const double t = STIFF ? x2c[rr * TX] : 0.0;
+      const double u1c = STIFF ? prm.cy * a1 : 0.0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int k = rr - i;
+        if (k >= 0 && k <= 2 * P) {
+          wm[i] = fma(T.M(k), a1, wm[i]);
+          if (STIFF) {
+            wa[i] = fma(T.M(k), t, wa[i]);
+            wa[i] = fma(T.K(k), u1c, wa[i]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const double a = STIFF ? wa[i] : wm[i];
+    const double w2 = STIFF ? wm[i] * prm.cz : 0.0;
+    double o = fma(T.M(0), a, acc[0][i]);
+    if (STIFF) o = fma(T.K(0), w2, o);
+    out[i] = o;
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) {
+      double v = fma(T.M(k + 1), a, acc[k + 1][i]);
+      if (STIFF) v = fma(T.K(k + 1), w2, v);
+      acc[k][i] = v;
+    }
+    double v = T.M(S) * a;
+    if (STIFF) v = fma(T.K(S), w2, v);
+    acc[S - 1][i] = v;
+  }
+  if (j >= 2 * P) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const double v = out[i];
+      if (MODE == M_APPLY) {
+        __stcs(op + i * py, v);
+      } else if (MODE == M_CGA) {
+        __stcs(op + i * py, v);
+        pp[i * py] = pr[0][i];
+        dsum[0] = fma(pr[0][i], v, dsum[0]);
+      } else if (MODE == M_MASS) {
+        double o = prm.c_mass * v;
+        if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
+        __stcs(op + i * py, o);
+      } else {  // M_RESID
+        const double bb = auxv[i];
+        const double r = bb - v;
+        __stcs(op + i * py, r);
+        dsum[0] = fma(bb, bb, dsum[0]);
+        dsum[1] = fma(r, __dmul_rn(inv0, r), dsum[1]);
+        dsum[2] = fma(r, r, dsum[2]);
+      }
+    }
+  }
+  if (MODE == M_CGA) {
+    const int s = f % NS;
+    const double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+      for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
+      pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
+    }
+  }
+}
 
 template <int P, int MODE, int TK>
 __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
@@ -826,25 +1038,57 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 #pragma unroll
     for (int i = 0; i < RPT; ++i) pr[k][i] = 0.0;
 
+  // core iterations [jlo, jhi) of an interior tile (see core_iter)
+  int jlo = 0, jhi = 0;
+  int pfe[4] = {-1, -1, -1, -1};
+  double inv0 = 0.0;
+  double *op = nullptr, *pp = nullptr;
+  const double* xp = nullptr;
+  const long long py = prm.pitch_y;
+  if (INTERIOR && BSPDE_CORE_ITER) {
+    const int ewz = prm.ew[0];
+    const int zbase = prm.z_off + g.zc0 - P;  // global z of streamed plane 0
+    jlo = max(0, ewz - zbase + (MODE == M_RESID ? P : 0));
+    jhi = prm.zfast ? min(nin - 1, prm.nz_glob - ewz - zbase - 1) : 0;
+    if (MODE == M_CGA) core_pform_offsets<P, MODE>(pfe);
+    if (C_INVD<P, MODE>())
+      inv0 = sm.invd[(ewz * (2 * prm.ew[1] + 1) + prm.ew[1]) * (2 * prm.ew[2] + 1) + prm.ew[2]];
+    // output plane of iteration 0 is zc0 - 2P (advanced one plane per iteration)
+    const long long o0 = (long long)(g.zc0 - 2 * P + prm.ghost) * prm.pitch_z +
+                         (long long)gy0 * py + gx;
+    op = prm.out + o0;
+    if (MODE == M_CGA) pp = prm.cg_pout + o0;
+    if (prm.aux) xp = prm.aux + o0;
+  }
+
   plane_front<P, MODE, TK>(prm, sm, g, 0, flat, beta);
   __syncthreads();
   for (int j = 0; j < nin; ++j) {
-    // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
-    double auxv[RPT];
+    if (INTERIOR && BSPDE_CORE_ITER && j >= jlo && j < jhi) {
+      core_iter<P, MODE>(prm, sm, j, flat, acc, pr, dsum, beta, pfe, inv0, op, pp, xp, py);
+    } else {
+      // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
+      double auxv[RPT];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
-    if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
-      const int zo = g.zc0 - 2 * P + j;
-      const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
+      for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
+      if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
+        const int zo = g.zc0 - 2 * P + j;
+        const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const int y = gy0 + i;
-        if (INTERIOR || (y < prm.ny && gx < prm.nx))
-          auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
+        for (int i = 0; i < RPT; ++i) {
+          const int y = gy0 + i;
+          if (INTERIOR || (y < prm.ny && gx < prm.nx))
+            auxv[i] = __ldcs(prm.aux + base + (long long)y * prm.pitch_y);
+        }
       }
+      if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
+      plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
     }
-    if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
-    plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
+    if (INTERIOR && BSPDE_CORE_ITER) {
+      op += prm.pitch_z;
+      if (MODE == M_CGA) pp += prm.pitch_z;
+      if (xp) xp += prm.pitch_z;
+    }
     __syncthreads();
     if (threadIdx.x == kProdThread<P>) {
       // the stage of plane j is consumed (x-pass one iteration ago, own p now)

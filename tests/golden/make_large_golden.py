@@ -1,0 +1,79 @@
+"""Oracle fixtures for the large heat configs (C2 256^3 p=3, C4 512^3 p=1..5).
+
+The reference itself is infeasible at these sizes (~0.2 s per
+sparse CG iteration at 64^3, 3.8 KB of CSR per DoF); the oracle restatement
+(oracle/bspde_oracle.py, pinned to the reference by the small fixtures of
+make_golden.py) runs the heat step 1 of SURVEY.md §8(d) here:
+
+    b = M u0 + dt F,  (M + dt K) x = b,  x0 = u0,  Jacobi-PCG to tol 1e-13
+
+recording the recursive residual of every iterate, so the iteration counts
+at tol 1e-10 and 1e-13 come from one run.  Stored per case (small): both
+counts, the residual history, ||u0||, ||b||, ||x||, and x at 4096 fixed
+pseudo-random coefficient positions (for the 1e-10 coefficient check; the
+full 1 GB vectors are not committed).
+
+Inputs are the separable Gaussians of SURVEY.md §8(d): the 3-D prefilter of
+a separable sample array is the outer product of the 1-D prefiltered
+vectors, so u0 and q are built from O.field_coeffs on 1-D samples.
+
+    python tests/golden/make_large_golden.py 256:3 512:1 512:2 512:3 512:4 512:5
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle import bspde_oracle as O  # noqa: E402
+
+NSAMPLE = 4096
+
+
+def separable(N, h, p, center, width, amp):
+    x = np.arange(N) * h
+    vs = [O.field_coeffs(np.exp(-width * (x - c) ** 2), p) for c in center]
+    return amp * np.multiply.outer(np.multiply.outer(vs[0], vs[1]), vs[2])
+
+
+def sample_index(cext, n=NSAMPLE, seed=1234):
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.integers(0, e, size=n) for e in cext], axis=1).astype(np.int32)
+
+
+def case(ncoef, p):
+    ext = O.basis_extension(p)
+    N = ncoef - 2 * ext
+    h = 1.0 / (N - 1)
+    dt = 4.0 * h * h
+    t0 = time.time()
+    # SURVEY.md §8(d) / synthetic.IC, SOURCE (axis order z, y, x)
+    u0 = separable(N, h, p, (0.5, 0.4, 0.6), 40.0, 1.0)
+    q = separable(N, h, p, (0.3, 0.6, 0.5), 60.0, 10.0)
+    A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
+    b = A.mass_apply(u0) + dt * A.mass_apply(q)
+    del q
+    hist = []
+    x, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-13, max_iter=5000, x0=u0,
+                   res_history=hist)
+    hist = np.asarray(hist)
+    its10 = int(np.argmax(hist <= 1e-10)) if np.any(hist <= 1e-10) else -1
+    idx = sample_index(A.cext)
+    out = dict(meta=np.array([ncoef, p, N, h, dt]), its_1e10=its10,
+               its_1e13=rep["iterations"], res_history=hist,
+               u0_norm=np.linalg.norm(u0), b_norm=np.linalg.norm(b), x_norm=np.linalg.norm(x),
+               idx=idx, x_sample=x[idx[:, 0], idx[:, 1], idx[:, 2]],
+               u0_sample=u0[idx[:, 0], idx[:, 1], idx[:, 2]])
+    path = os.path.join(HERE, f"large_{ncoef}_p{p}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{path}: its 1e-10 {its10}, 1e-13 {rep['iterations']}, {time.time() - t0:.0f} s",
+          flush=True)
+
+
+if __name__ == "__main__":
+    for arg in sys.argv[1:]:
+        n, p = (int(v) for v in arg.split(":"))
+        case(n, p)

@@ -704,3 +704,56 @@ def test_full_size_windows_symmetry_and_true_residual(cuda_device, ncoef, p):
     assert float(rt) < 2e-10, float(rt)
     del u, Au, b, x
     torch.cuda.empty_cache()
+
+
+LARGE = [(256, 3), (512, 1), (512, 2), (512, 3), (512, 4), (512, 5)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ncoef,p", LARGE)
+def test_large_heat_step_vs_oracle_fixture(golden, cuda_device, ncoef, p):
+    """C2 (256^3) and C4 (512^3, p = 1..5): heat step 1 (b = M u0 + dt F,
+    x0 = u0) against the oracle recurrence run in the build container
+    (tests/golden/make_large_golden.py): CG iteration counts within +-1 at
+    tol 1e-10 and 1e-13 (BASELINE.json configs[1] / [3]; north_star), and at
+    tol 1e-13 the coefficients within 1e-10 relative (||x|| and 4096 fixed
+    sampled coefficients)."""
+    import torch
+
+    from paper_1904_03057_b200.solver import pcg_device
+    from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs
+
+    g = golden(f"large_{ncoef}_p{p}.npz")
+    N, hh, dt = heat_c_inputs(ncoef, p)
+    assert np.allclose(g["meta"], [ncoef, p, N, hh, dt], rtol=1e-15, atol=0)
+    op = make_operator(heat_system(Grid((N,) * 3, (hh,) * 3), p, dt), "b200")
+    lay, dev = op.layout, op.device
+    idx = torch.from_numpy(g["idx"].astype(np.int64)).to(dev)
+
+    def sample(buf):
+        own = lay.owned(buf)
+        return own[idx[:, 0], idx[:, 1], idx[:, 2]].cpu().numpy()
+
+    u = lay.alloc(dev)
+    gaussian_coeffs(N, hh, p, device=dev, out=u, layout=lay, **IC)
+    assert relmax(sample(u), g["u0_sample"]) < 1e-13  # same inputs as the oracle run
+    q = lay.alloc(dev)
+    gaussian_coeffs(N, hh, p, device=dev, out=q, layout=lay, **SOURCE)
+    F = lay.alloc(dev)
+    op.mass_apply_device(q, F)
+    del q
+    b = lay.alloc(dev)
+    op.mass_apply_device(u, b, F, a=dt)
+    del F
+    bn = float(torch.linalg.vector_norm(lay.owned(b)))
+    assert abs(bn - float(g["b_norm"])) <= 1e-13 * bn
+    for tol, key in ((1e-10, "its_1e10"), (1e-13, "its_1e13")):
+        x = u.clone()
+        rep = pcg_device(op, b, x, SolveConfig(tol=tol, max_iter=5000), has_x0=True)
+        assert abs(rep.iterations - int(g[key])) <= 1, (tol, rep.iterations, int(g[key]))
+    xs, xo = sample(x), g["x_sample"]
+    assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
+    xn = float(torch.linalg.vector_norm(lay.owned(x)))
+    assert abs(xn - float(g["x_norm"])) <= 1e-10 * xn
+    del x, u, b
+    torch.cuda.empty_cache()

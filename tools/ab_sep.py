@@ -1,0 +1,85 @@
+"""A/B a sep_kernel variant (BSPDE_LIB) on the bench's heat system: times
+pass A, pass B, the residual and the RHS kernels (CUDA events, median of 15
+after 3 warm-ups) and prints sha256 digests of every output plus the CG
+scalars, so two builds can be checked bitwise-identical.
+
+    BSPDE_LIB=path python tools/ab_sep.py [ncoef] [degree]
+"""
+import hashlib
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1904_03057_b200 import make_operator  # noqa: E402
+from paper_1904_03057_b200.domain import Grid  # noqa: E402
+from paper_1904_03057_b200.solver import _work  # noqa: E402
+from paper_1904_03057_b200.synthetic import IC, SOURCE, gaussian_coeffs, heat_c_inputs  # noqa: E402
+from paper_1904_03057_b200.system import heat_system  # noqa: E402
+
+ncoef = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+p = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+N, h, dt = heat_c_inputs(ncoef, p)
+op = make_operator(heat_system(Grid((N,) * 3, (h,) * 3), p, dt), "b200")
+lay, dev = op.layout, op.device
+w = _work(op, 10)
+u, F = lay.alloc(dev), lay.alloc(dev)
+gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, **IC)
+gaussian_coeffs(N, h, p, device=dev, out=w.r, layout=lay, **SOURCE)
+op.mass_apply_device(w.r, F)
+plan = op.plan()
+R = w.pring.shape[0]
+
+
+def digest(t):
+    return hashlib.sha256(t.contiguous().cpu().numpy().tobytes()).hexdigest()[:16]
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+times = {"rhs": [], "resid": [], "pass_a": [], "pass_b": []}
+dig = {}
+x = u.clone()
+for it in range(18):
+    e = [ev() for _ in range(5)]
+    e[0].record()
+    op.mass_apply_device(u, w.ap, F, a=dt)           # b (in Ap's storage)
+    e[1].record()
+    if it == 0:
+        torch.cuda.synchronize()
+        dig["b"] = digest(lay.owned(w.ap))
+        x.copy_(u)
+        plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True, p_ring=R)
+    e1b = ev()
+    e1b.record()
+    plan.cg_residual(w.ap, x, w.r, w.scratch, 1)
+    e[2].record()
+    if it == 0:
+        torch.cuda.synchronize()
+        dig["r0"] = digest(lay.owned(w.r))
+        dig["resid_sums"] = digest(w.scratch[:64])
+    k = it
+    plan.cg_pass_a(w.r, w.pring[(k - 1) % R], w.pring[k % R], w.ap, w.scratch, 1)
+    e[3].record()
+    plan.cg_pass_b(x, w.r, w.pring, w.ap, w.scratch, 1)
+    e[4].record()
+    torch.cuda.synchronize()
+    if it == 0:
+        dig["ap"] = digest(lay.owned(w.ap))
+        dig["p0"] = digest(lay.owned(w.pring[0]))
+        dig["after_b_state"] = digest(w.scratch[:256])
+    if it >= 3:
+        times["rhs"].append(e[0].elapsed_time(e[1]))
+        times["resid"].append(e1b.elapsed_time(e[2]))
+        times["pass_a"].append(e[2].elapsed_time(e[3]))
+        times["pass_b"].append(e[3].elapsed_time(e[4]))
+dig["r_final"] = digest(lay.owned(w.r))
+out = {"lib": os.path.basename(os.environ.get("BSPDE_LIB", "product")), "ncoef": ncoef, "p": p,
+       **{k + "_ms": round(float(np.median(v)), 4) for k, v in times.items()},
+       "digests": dig}
+print(json.dumps(out), flush=True)
