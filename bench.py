@@ -29,7 +29,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# algorithmic bytes per DoF of the CG passes: alg_bytes(ring) below
+# algorithmic bytes per DoF of the CG passes: alg_bytes() below
 SURVEY_BYTES_ITER = 80  # x, r, p, Ap streams of the textbook fused CG
 # ncu-measured DRAM traffic per DoF for the kernels (profiles/, `--set full` at 512^3):
 # filled from the committed profile summary when present
@@ -348,14 +348,12 @@ def config_of(args, world):
 # ---------------------------------------------------------------------------
 
 
-def alg_bytes(ring):
-    """Algorithmic bytes per DoF of pass A / pass B / a CG iteration for a
-    search-direction ring of length R: pass A reads r, p_{k-1} and writes Ap,
-    p_k (32 B); pass B reads r, Ap and writes r (24 B), and every R-th pass
-    also reads x and the last R p's and writes x (16 + 8 R B), i.e.
-    24 + (16 + 8 R) / R on average."""
-    b = 24 + (16 + 8 * ring) / ring
-    return 32, b, 32 + b
+def alg_bytes():
+    """Algorithmic bytes per DoF of pass A / pass B / a CG iteration: pass A
+    reads r, p_{k-1}, x and writes Ap, p_k, x (48 B: it forms p_k, applies A
+    and x += alpha_{k-1} p_{k-1}); pass B reads r, Ap and writes r (24 B)
+    (DESIGN.md §5)."""
+    return 48, 24, 72
 
 
 def run_ours(args, rank, world, local_rank):
@@ -458,7 +456,7 @@ def run_ours(args, rank, world, local_rank):
     kt = {k: max_over_ranks(v) for k, v in kt.items()}
     peak, peak_kind = measured_peaks()
     local_dofs = int(np.prod(lay.owned_shape))
-    bytes_a, bytes_b, bytes_it = alg_bytes(ring)
+    bytes_a, bytes_b, bytes_it = alg_bytes()
     a_gbs = bytes_a * local_dofs / (kt["pass_a_ms"] * 1e-3) / 1e9
     b_gbs = bytes_b * local_dofs / (kt["pass_b_ms"] * 1e-3) / 1e9
     dom = "pass_b" if kt["pass_b_ms"] >= kt["pass_a_ms"] else "pass_a"
@@ -523,18 +521,16 @@ def kernel_times(op, u, F, dt, stream, wset, reps=9):
     for k in range(reps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        plan.cg_pass_a(r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
+        plan.cg_pass_a(x, r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
         e[1].record(stream)
-        plan.cg_pass_b(x, r, pring, ap, scratch, 1)
+        plan.cg_pass_b(r, ap, scratch, 1)
         e[2].record(stream)
         torch.cuda.synchronize()
         ta.append(e[0].elapsed_time(e[1]))
         tb.append(e[1].elapsed_time(e[2]))
     plan.cg_flush_x(x, pring, scratch)
     torch.cuda.synchronize()
-    # pass B's mean over whole ring periods (x moves every R-th pass)
-    nb = ((reps - 1) // R) * R
-    return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:1 + nb]))}
+    return {"pass_a_ms": float(np.mean(ta[1:])), "pass_b_ms": float(np.mean(tb[1:]))}
 
 
 def e2e_rate(step, u, lay, dofs, steps, stream, barrier, max_over_ranks):

@@ -32,10 +32,11 @@ extern "C" {
 
 /* CG search directions live in a ring of R ghosted-slab fields (one
  * contiguous allocation, field after field; R = bspde_cg_config.p_ring, 2 or
- * BSPDE_P_RING): iteration k writes p_k to field k % R; x += alpha p is
- * applied every R iterations from the ring, in the reference's rounding
- * order.  R = 4 moves x once per 4 iterations; R = 2 saves two fields of
- * HBM (the 1536^3 single-GPU case). */
+ * BSPDE_P_RING): iteration k reads p_{k-1} from field (k-1) % R and writes
+ * p_k to field k % R.  Pass A of iteration k also applies x += alpha_{k-1}
+ * p_{k-1} (it stages p_{k-1} anyway), in the reference's rounding order
+ * (solver.py:94); the last iteration's update is applied at the end of a
+ * solve (bspde_cg_flush_x).  R = 2 suffices (the default). */
 #define BSPDE_P_RING 4
 
 #define BSPDE_OK 0
@@ -90,7 +91,7 @@ typedef struct {
   int32_t record_history;
   int32_t has_x0;       /* 0: x0 = None (x is zeroed), 1: x holds x0 */
   int32_t poll_every;   /* iterations per CUDA-graph chunk between host polls (<=0: default 8) */
-  int32_t p_ring;       /* search-direction ring length R: 2 or 4 (0: BSPDE_P_RING) */
+  int32_t p_ring;       /* search-direction ring length R: 2 or 4 (0: 2) */
 } bspde_cg_config;
 
 typedef struct {
@@ -155,9 +156,10 @@ int bspde_cg_setup(bspde_plan* plan, void* scratch, double* history,
 int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
                       double* r, void* scratch, int fuse, void* stream);
 /* p_k = D^-1 r + beta p_{k-1} on the fly (written to p_out at owned
- * points); ap = A p_k; sums = {<p,Ap>}                                kind 1
+ * points); ap = A p_k; sums = {<p,Ap>}; and, for k >= 1, x += alpha_{k-1}
+ * p_{k-1} at the owned points (solver.py:94; p_in = p_{k-1})       kind 1
  * p_in / p_out ping-pong between iterations (they must differ). */
-int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
+int bspde_cg_pass_a(bspde_plan* plan, double* x, const double* r, const double* p_in,
                     double* p_out, double* ap, void* scratch, int fuse,
                     void* stream);
 /* Pass A restricted to the owned output planes [z_begin, z_begin + z_count)
@@ -167,19 +169,18 @@ int bspde_cg_pass_a(bspde_plan* plan, const double* r, const double* p_in,
  * while the NCCL halo exchange is in flight, then the two boundary ranges
  * (overlap the halo with the interior apply).  The reference
  * analogue is a worker's window of blocks (operator.py:61-74). */
-int bspde_cg_pass_a_range(bspde_plan* plan, const double* r, const double* p_in,
-                          double* p_out, double* ap, void* scratch, int z_begin,
-                          int z_count, int accumulate, int fuse, void* stream);
-/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>}; x += alpha p for the last R
- * iterations at once every R-th call (R = the p_ring given to
- * bspde_cg_setup), in the reference's rounding order (solver.py:94-101).
- * Iteration k's pass A must read ring field (k-1) % R and write field k % R.
- * kind 2 */
-int bspde_cg_pass_b(bspde_plan* plan, double* x, double* r, const double* p_ring,
-                    const double* ap, void* scratch, int fuse, void* stream);
-/* Apply the pending x updates (x += alpha_j p_j for the iterations since the
- * last application).  bspde_pcg_solve does this itself; step-wise drivers
- * call it once after their loop (idempotent). */
+int bspde_cg_pass_a_range(bspde_plan* plan, double* x, const double* r,
+                          const double* p_in, double* p_out, double* ap, void* scratch,
+                          int z_begin, int z_count, int accumulate, int fuse,
+                          void* stream);
+/* r -= alpha Ap; sums = {<r,D^-1 r>, <r,r>} (solver.py:95-101; x moves in
+ * the next pass A).  Iteration k's pass A must read ring field (k-1) % R and
+ * write field k % R (R = the p_ring given to bspde_cg_setup).        kind 2 */
+int bspde_cg_pass_b(bspde_plan* plan, double* r, const double* ap, void* scratch,
+                    int fuse, void* stream);
+/* Apply the pending x update (x += alpha_j p_j for the last iteration,
+ * which no further pass A applies).  bspde_pcg_solve does this itself;
+ * step-wise drivers call it once after their loop (idempotent). */
 int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p_ring,
                      void* scratch, void* stream);
 /* kind 0/1/2: scalar update after residual / pass A / pass B (skipped when

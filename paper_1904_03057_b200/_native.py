@@ -17,7 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # only; the variant is the same source with different -D constants).
 LIB_PATH = os.environ.get("BSPDE_LIB") or os.path.join(HERE, "libbspde_b200.so")
 
-P_RING = 4  # BSPDE_P_RING: CG search directions in the ring (include/bspde_b200.h)
+P_RING = 4  # BSPDE_P_RING: the longest search-direction ring (include/bspde_b200.h)
+RING_DEFAULT = 2  # pass A applies x, so two fields (p_{k-1}, p_k) suffice
 
 BSPDE_CG_RUNNING = 0
 BSPDE_CG_CONVERGED = 1
@@ -129,10 +130,10 @@ SIGNATURES = [
                                   C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
     ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
-    ("bspde_cg_pass_a_range", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, C.c_int, C.c_int,
-                                        C.c_int, _VP]),
-    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_pass_a_range", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, C.c_int,
+                                        C.c_int, C.c_int, _VP]),
+    ("bspde_cg_pass_b", C.c_int, [_VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_flush_x", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_stencil_create", C.c_int, [C.POINTER(StencilDesc), C.POINTER(C.c_void_p)]),
     ("bspde_stencil_destroy", C.c_int, [_VP]),

@@ -56,14 +56,24 @@ constexpr int RPT = 4;               // output rows per thread
 constexpr int MAXP = 5;
 constexpr int MAXTAP = 2 * MAXP + 1;
 
-__host__ __device__ constexpr int warps_of(int p) { return p <= 3 ? 16 : 12; }
-__host__ __device__ constexpr int tile_h_of(int p) { return RPT * warps_of(p) / 2; }
+// BSPDE_W_LOWP (tuning build): warps per CTA for p <= 3 (16: 128 registers;
+// 12: 168 registers, 64 x 24 tiles)
+#ifndef BSPDE_W_LOWP
+#define BSPDE_W_LOWP 16
+#endif
+// Per (degree, mode): CG pass A at p = 3 carries the p ring and the x update
+// and runs 12 warps with 168 registers (64 x 24 tiles; 16 warps spill at the
+// 128-register cap); the other p <= 3 kernels run 16 warps (64 x 32 tiles)
+__host__ __device__ constexpr int warps_of(int p, int mode) {
+  return p <= 3 ? ((p == 3 && mode == 3 /* M_CGA */) ? 12 : BSPDE_W_LOWP) : 12;
+}
+__host__ __device__ constexpr int tile_h_of(int p, int mode) { return RPT * warps_of(p, mode) / 2; }
 
-template <int P>
+template <int P, int MODE>
 struct Geo {
-  static constexpr int NW = warps_of(P);   // warps (2 x-groups)
+  static constexpr int NW = warps_of(P, MODE);   // warps (2 x-groups)
   static constexpr int NT = 32 * NW;       // threads
-  static constexpr int TY = tile_h_of(P);  // tile height (y)
+  static constexpr int TY = tile_h_of(P, MODE);  // tile height (y)
 };
 
 enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
@@ -74,7 +84,7 @@ __host__ __device__ constexpr int edge_width_of(int p) {
 
 template <int P, int MODE>
 struct Cfg {
-  static constexpr int NW = Geo<P>::NW, NT = Geo<P>::NT, TY = Geo<P>::TY;
+  static constexpr int NW = Geo<P, MODE>::NW, NT = Geo<P, MODE>::NT, TY = Geo<P, MODE>::TY;
   static constexpr int R = 2 * P + 1;
   // TMA needs the box's inner start (x0 - PX) * 8 bytes to be 16-byte aligned:
   // the x halo is padded to an even width PX (odd p: one extra column per side)
@@ -123,6 +133,7 @@ struct SepParams {
   int main_items, tail_split, sub_len;  // items >= main_items: tail chunks split tail_split ways
   int zfast;  // 1: interior z rows use the compile-time taps (0 for a degenerate z axis)
   double tzm[MAXTAP], tzk[MAXTAP], tym[MAXTAP], tyk[MAXTAP], txm[MAXTAP], txk[MAXTAP];
+  double gm[MAXTAP], gk[MAXTAP];  // unit interior Gram taps (BSPDE_PARAM_TAPS builds)
   double c_mass, cx, cy, cz;     // cz is folded into tzk; kept for edge rows
   const double* tab;             // device: [axis][kind][NC*R] (NC = class stride)
   const double* invd;            // device: NCz*NCy*NCx
@@ -132,6 +143,7 @@ struct SepParams {
   const double* cg_r;  // CG pass A: r and p_old (TMA-staged with their halos)
   const double* cg_p;
   double* cg_pout;     // CG pass A: p_k at owned points (ping-pong partner of cg_p)
+  double* cg_x;        // CG pass A: x += alpha_{k-1} p_{k-1} at owned points (k >= 1)
   double* partials;
   unsigned* counter;
   CgState* state;
@@ -146,11 +158,24 @@ struct SepParams {
 #endif
 // Interior taps of the fast paths: compile-time immediates (measured faster
 // than __constant__ or kernel-parameter operands; profiles/r01_ncu_summary.md).
-template <int P>
+#ifndef BSPDE_PARAM_TAPS
+#define BSPDE_PARAM_TAPS 0
+#endif
+// Interior taps: compile-time immediates, except in CG pass A, whose DFMAs
+// take them as constant-bank operands (kernel parameters): the immediates are
+// rematerialised through uniform registers every plane there (measured -1%
+// pass A time at 930^3 with params; the other modes are better with
+// immediates).  BSPDE_PARAM_TAPS=1 uses parameters everywhere (tuning).
+template <int P, int MODE>
 struct TapSrc {
   const SepParams& prm;
-  __device__ __forceinline__ double M(int k) const { return GramTaps<P>::M(k); }
-  __device__ __forceinline__ double K(int k) const { return GramTaps<P>::K(k); }
+  static constexpr bool PARAM = BSPDE_PARAM_TAPS || MODE == 3 /* M_CGA */;
+  __device__ __forceinline__ double M(int k) const {
+    return PARAM ? prm.gm[k] : GramTaps<P>::M(k);
+  }
+  __device__ __forceinline__ double K(int k) const {
+    return PARAM ? prm.gk[k] : GramTaps<P>::K(k);
+  }
 };
 
 struct PassBParams {
@@ -286,6 +311,8 @@ __device__ void finalize_state(CgState* s, int kind) {
     update_active(s);
   } else if (kind == 1) {
     const double pAp = s->sums[0];
+    // pass A of iteration it applied x += alpha_j p_j for j < it
+    s->x_done = s->it;
     s->pAp = pAp;
     if (pAp <= 0.0) {
       s->status = BSPDE_CG_INDEFINITE;
@@ -295,9 +322,8 @@ __device__ void finalize_state(CgState* s, int kind) {
     s->alpha = s->rz / pAp;
   } else {
     const double rz_new = s->sums[0], rr = s->sums[1];
-    // pass B of iteration k = it applied x up to k when k % R == R - 1
+    // alpha_k for the x update of the next pass A / the final flush
     s->alpha_ring[s->it % s->ring] = s->alpha;
-    if (s->it % s->ring == s->ring - 1) s->x_done = s->it + 1;
     s->beta = rz_new / s->rz;
     s->rz = rz_new;
     s->res = sqrt(rr);
@@ -400,9 +426,9 @@ struct ItemGeom {
 };
 
 // valid output rows of a tile (< TY only in a ragged last tile row)
-template <int P>
+template <int P, int MODE>
 __device__ __forceinline__ int tile_rows(const SepParams& prm, const ItemGeom& g) {
-  return min(Geo<P>::TY, prm.ny - g.y0);
+  return min(Geo<P, MODE>::TY, prm.ny - g.y0);
 }
 
 // Items: (tile, z-chunk) in tile-fastest order, dealt round-robin so all
@@ -410,9 +436,9 @@ __device__ __forceinline__ int tile_rows(const SepParams& prm, const ItemGeom& g
 // are then L2 hits).  The first main_items form whole waves; each remaining
 // chunk (the ragged last wave) is split tail_split ways so it is spread over
 // all SMs instead of extending the makespan by a full chunk.
-template <int P>
+template <int P, int MODE>
 __device__ __forceinline__ ItemGeom item_geom(const SepParams& prm, int item) {
-  constexpr int TY = Geo<P>::TY;
+  constexpr int TY = Geo<P, MODE>::TY;
   const int tiles_xy = prm.tiles_x * prm.tiles_y;
   // branch-free: for main items jt < 0 maps to (it = item, sub = 0) via max()
   const int jt = max(item - prm.main_items, 0);
@@ -452,7 +478,7 @@ struct Producer {
     using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
     if (item >= prm.nitems) return;
-    const ItemGeom g = item_geom<P>(prm, item);
+    const ItemGeom g = item_geom<P, MODE>(prm, item);
     const int nin = g.zc1 - g.zc0 + 2 * P;
     const int s = flat % C::NS;
     const int zb = g.zc0 - P + j + prm.ghost;
@@ -485,7 +511,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
-  const TapSrc<P> T{prm};
+  const TapSrc<P, MODE> T{prm};
   constexpr int R = C::R, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS, NC = C::NC;
   constexpr int PX = C::PX, DX = C::DX;
   constexpr bool STIFF = C::STIFF;
@@ -496,8 +522,10 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
   const int s = f % NS;
   mbar_wait(&sm.full[s], (f / NS) & 1);
   if (!(zg >= 0 && zg < prm.nz_glob)) return;  // ghost/outside plane: no contribution
+  // CG: p_k is formed over r in slot 0 (r is dead afterwards) and p_{k-1}
+  // stays in slot 1 for the x update (run_item); other modes: one slot
   double* stC = sm.stage + (s * NA + 0) * C::ARR_D;
-  double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+  const double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
   double* X1 = sm.X + (f & 1) * 2 * C::XARR;
   double* X2 = X1 + C::XARR;
   const int cz = cls_of(zg, prm.nz_glob, ewz);
@@ -511,7 +539,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
     // a ragged last tile row only needs its valid rows + 2p halo rows
     const int nrow = !RAGGED
                          ? ((warp < HY - NW * (NROW - 1)) ? NROW : NROW - 1)
-                         : max(0, (tile_rows<P>(prm, g) + 2 * P - warp + NW - 1) / NW);
+                         : max(0, (tile_rows<P, MODE>(prm, g) + 2 * P - warp + NW - 1) / NW);
     const int npair = nrow * PPR;
     const int ncy = 2 * ewy + 1, ncx = 2 * ewx + 1;
     if (INTERIOR && cz == ewz) {
@@ -527,7 +555,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
           double2 pv;
           pv.x = pdir(rv.x, inv0, qv.x, beta);
           pv.y = pdir(rv.y, inv0, qv.y, beta);
-          *reinterpret_cast<double2*>(stP + e) = pv;
+          *reinterpret_cast<double2*>(stC + e) = pv;
         }
       }
     } else {
@@ -552,7 +580,7 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
         double2 pv;
         pv.x = pdir(rv.x, i0, qv.x, beta);
         pv.y = pdir(rv.y, i1, qv.y, beta);
-        *reinterpret_cast<double2*>(stP + e) = pv;
+        *reinterpret_cast<double2*>(stC + e) = pv;
       }
     }
     __syncwarp();
@@ -561,8 +589,8 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
 #pragma unroll
   for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
     const int row = warp + NW * m;
-    if (row < HY && (!RAGGED || row < tile_rows<P>(prm, g) + 2 * P)) {
-      const double* w = stP + row * HX + 2 * lane;
+    if (row < HY && (!RAGGED || row < tile_rows<P, MODE>(prm, g) + 2 * P)) {
+      const double* w = stC + row * HX + 2 * lane;
       double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
       for (int k = 0; k < P + 1 + DX; ++k) {
@@ -626,7 +654,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
-  const TapSrc<P> T{prm};
+  const TapSrc<P, MODE> T{prm};
   constexpr int R = C::R, HX = C::HX, NA = C::NA, NS = C::NS, NC = C::NC, S = 2 * P;
   constexpr int PX = C::PX;
   constexpr bool STIFF = C::STIFF;
@@ -784,9 +812,9 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     }
   }
   if (MODE == M_CGA) {
-    // own p of plane zl (its stage is released only after this iteration)
+    // own p_k of plane zl (slot 0; the stage is released only after this iteration)
     const int s = f % NS;
-    const double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+    const double* stP = sm.stage + (s * NA + 0) * C::ARR_D;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
 #pragma unroll
@@ -801,6 +829,10 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
 #ifndef BSPDE_CORE_ITER
 #define BSPDE_CORE_ITER 1
 #endif
+// core iterations in CG pass A too (measured slower: register pressure)
+#ifndef BSPDE_CORE_CGA
+#define BSPDE_CORE_CGA 0
+#endif
 template <int P, int MODE>
 __host__ __device__ constexpr bool C_INVD() { return Cfg<P, MODE>::INVD; }
 
@@ -809,8 +841,9 @@ __host__ __device__ constexpr bool C_INVD() { return Cfg<P, MODE>::INVD; }
 #ifndef BSPDE_PROD_WARP
 #define BSPDE_PROD_WARP -1
 #endif
-template <int P>
-constexpr int kProdThread = (BSPDE_PROD_WARP < 0 ? Geo<P>::NW + BSPDE_PROD_WARP : BSPDE_PROD_WARP) * 32;
+template <int P, int MODE>
+constexpr int kProdThread =
+    (BSPDE_PROD_WARP < 0 ? Geo<P, MODE>::NW + BSPDE_PROD_WARP : BSPDE_PROD_WARP) * 32;
 
 // ---------------------------------------------------------------------------
 // Core iterations of an interior tile.  Iteration j (front of plane j+1 +
@@ -854,7 +887,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
   constexpr int NW = C::NW, TY = C::TY, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS;
   constexpr int PX = C::PX, DX = C::DX, S = 2 * P;
   constexpr bool STIFF = C::STIFF;
-  const TapSrc<P> T{prm};
+  const TapSrc<P, MODE> T{prm};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rg = warp >> 1;
   const int cxl = (warp & 1) * 32 + lane;
@@ -874,8 +907,8 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
     const uint32_t f1 = f + 1;
     const int s1 = f1 % NS;
     mbar_wait(&sm.full[s1], (f1 / NS) & 1);
-    const double* stC = sm.stage + (s1 * NA + 0) * C::ARR_D;
-    double* stP = sm.stage + (s1 * NA + (NA - 1)) * C::ARR_D;
+    double* stC = sm.stage + (s1 * NA + 0) * C::ARR_D;
+    const double* stP = sm.stage + (s1 * NA + (NA - 1)) * C::ARR_D;
     double* X1 = sm.X + (f1 & 1) * 2 * C::XARR;
     double* X2 = X1 + C::XARR;
     if (MODE == M_CGA) {
@@ -888,7 +921,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
           double2 pv;
           pv.x = pdir(rv.x, inv0, qv.x, beta);
           pv.y = pdir(rv.y, inv0, qv.y, beta);
-          *reinterpret_cast<double2*>(stP + e) = pv;
+          *reinterpret_cast<double2*>(stC + e) = pv;
         }
       }
       __syncwarp();
@@ -897,7 +930,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
     for (int m = 0; m < (HY + NW - 1) / NW; ++m) {
       const int row = warp + NW * m;
       if (row < HY) {
-        const double* w = stP + row * HX + 2 * lane;
+        const double* w = stC + row * HX + 2 * lane;
         double raw[2 * P + 2 + 2 * DX];
 #pragma unroll
         for (int k = 0; k < P + 1 + DX; ++k) {
@@ -1006,7 +1039,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
   }
   if (MODE == M_CGA) {
     const int s = f % NS;
-    const double* stP = sm.stage + (s * NA + (NA - 1)) * C::ARR_D;
+    const double* stP = sm.stage + (s * NA + 0) * C::ARR_D;  // p_k
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
 #pragma unroll
@@ -1020,7 +1053,8 @@ template <int P, int MODE, int TK>
 __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
                                          const CUtensorMap* tm1, const Smem& sm,
                                          const ItemGeom& g, uint32_t& flat, double beta,
-                                         double (&dsum)[3], Producer<P, MODE>& prod) {
+                                         double (&dsum)[3], Producer<P, MODE>& prod,
+                                         double xalpha, bool xok) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   constexpr int S = 2 * P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1045,7 +1079,8 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
   double *op = nullptr, *pp = nullptr;
   const double* xp = nullptr;
   const long long py = prm.pitch_y;
-  if (INTERIOR && BSPDE_CORE_ITER) {
+  constexpr bool CORE = INTERIOR && BSPDE_CORE_ITER && (MODE != M_CGA || BSPDE_CORE_CGA);
+  if (CORE) {
     const int ewz = prm.ew[0];
     const int zbase = prm.z_off + g.zc0 - P;  // global z of streamed plane 0
     jlo = max(0, ewz - zbase + (MODE == M_RESID ? P : 0));
@@ -1061,10 +1096,26 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
     if (prm.aux) xp = prm.aux + o0;
   }
 
+  // CG: x += alpha_{k-1} p_{k-1} at this thread's owned points of every owned
+  // plane (p_{k-1} is staged with the halos anyway; x is read a plane ahead of
+  // its update so the load latency hides under the plane's work)
+  const bool xupd = (MODE == M_CGA) && prm.cg_x != nullptr && xok;
+  const int cxl = (warp & 1) * 32 + lane, rg = warp >> 1;
+  double* xrow = xupd ? prm.cg_x + (long long)(g.zc0 - P + prm.ghost) * prm.pitch_z +
+                            (long long)gy0 * prm.pitch_y + gx
+                      : nullptr;
+
   plane_front<P, MODE, TK>(prm, sm, g, 0, flat, beta);
   __syncthreads();
   for (int j = 0; j < nin; ++j) {
-    if (INTERIOR && BSPDE_CORE_ITER && j >= jlo && j < jhi) {
+    double xv[RPT];
+    const bool xown = xupd && j >= P && j < nin - P;  // plane zc0 - P + j is owned
+    if (xown) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        xv[i] = (INTERIOR || (gy0 + i < prm.ny && gx < prm.nx)) ? xrow[i * prm.pitch_y] : 0.0;
+    }
+    if (CORE && j >= jlo && j < jhi) {
       core_iter<P, MODE>(prm, sm, j, flat, acc, pr, dsum, beta, pfe, inv0, op, pp, xp, py);
     } else {
       // epilogue operand prefetch (RESID: b, MASS: f) for output plane zl - P
@@ -1084,13 +1135,25 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
       if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
       plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
     }
-    if (INTERIOR && BSPDE_CORE_ITER) {
+    if (xown) {  // x + alpha p, rounded like the reference's x += alpha * p (solver.py:94)
+      const double* stO = sm.stage + ((flat % Cfg<P, MODE>::NS) * Cfg<P, MODE>::NA + 1) *
+                                         Cfg<P, MODE>::ARR_D;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        if (INTERIOR || (gy0 + i < prm.ny && gx < prm.nx)) {
+          const double po = stO[(rg * RPT + i + P) * Cfg<P, MODE>::HX + cxl + Cfg<P, MODE>::PX];
+          xrow[i * prm.pitch_y] = __dadd_rn(xv[i], __dmul_rn(xalpha, po));
+        }
+      }
+    }
+    if (xupd) xrow += prm.pitch_z;
+    if (CORE) {
       op += prm.pitch_z;
       if (MODE == M_CGA) pp += prm.pitch_z;
       if (xp) xp += prm.pitch_z;
     }
     __syncthreads();
-    if (threadIdx.x == kProdThread<P>) {
+    if (threadIdx.x == kProdThread<P, MODE>) {
       // the stage of plane j is consumed (x-pass one iteration ago, own p now)
       fence_proxy_async();
       prod.issue(prm, tm0, tm1, sm.stage, sm.full);
@@ -1100,7 +1163,7 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(Geo<P>::NT, 1)
+__global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
     sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
                const __grid_constant__ CUtensorMap tm1) {
   using C = Cfg<P, MODE>;
@@ -1136,20 +1199,26 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
   __syncthreads();
 
   const double beta = (MODE == M_CGA) ? ld_vol(&prm.state->beta) : 0.0;
+  // pass A of iteration k applies x += alpha_{k-1} p_{k-1} (k >= 1): alpha
+  // still holds alpha_{k-1} here (every CTA reads it before the last CTA's
+  // finalize overwrites it with alpha_k)
+  const int k_it = (MODE == M_CGA) ? ld_vol(&prm.state->it) : 0;
+  const double xalpha = (MODE == M_CGA) ? ld_vol(&prm.state->alpha) : 0.0;
+  const bool xok = k_it >= 1;
   double dsum[3] = {0.0, 0.0, 0.0};
   Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
-  if (tid == kProdThread<P>) {
+  if (tid == kProdThread<P, MODE>) {
     for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, sm.stage, sm.full);
   }
   uint32_t flat = 0;
   for (int item = blockIdx.x; item < prm.nitems; item += gridDim.x) {
-    const ItemGeom g = item_geom<P>(prm, item);
+    const ItemGeom g = item_geom<P, MODE>(prm, item);
     if (tile_interior<P, MODE>(prm, g))
-      run_item<P, MODE, TILE_INTERIOR>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
-    else if (tile_rows<P>(prm, g) == TY)
-      run_item<P, MODE, TILE_EDGE>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+      run_item<P, MODE, TILE_INTERIOR>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod, xalpha, xok);
+    else if (tile_rows<P, MODE>(prm, g) == TY)
+      run_item<P, MODE, TILE_EDGE>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod, xalpha, xok);
     else
-      run_item<P, MODE, TILE_RAGGED>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod);
+      run_item<P, MODE, TILE_RAGGED>(prm, &tm0, &tm1, sm, g, flat, beta, dsum, prod, xalpha, xok);
   }
 
   if (MODE == M_CGA) {
@@ -1163,16 +1232,13 @@ __global__ void __launch_bounds__(Geo<P>::NT, 1)
 }
 
 // ---------------------------------------------------------------------------
-// CG pass B: r -= alpha Ap, <r, D^-1 r>, <r, r> and x += alpha p
-// (solver.py:94-101)
+// CG pass B: r -= alpha Ap, <r, D^-1 r>, <r, r> (solver.py:95-101)
 //
-// Pass A stores p_k into ring field k % kPRing, so pass B never recomputes p.
-// x is only read by the caller after the solve: iterations leave it alone and
-// record alpha_k, and every kPRing-th iteration applies the pending updates
-// x = fl(...fl(fl(x + fl(alpha_j p_j)) + fl(alpha_{j+1} p_{j+1}))...) in
-// order -- bitwise the reference's stored updates (solver.py:94).  So the pass
-// streams 24 B/DoF (r, Ap in; r out), and 40 + 8*kPRing every kPRing-th time;
-// x_flush_kernel applies the pending updates at the end of a solve.
+// x += alpha_k p_k (solver.py:94) is applied by the NEXT pass A, which stages
+// p_k with its halos anyway and is latency- rather than bandwidth-bound, in
+// the reference's rounding order x = fl(x + fl(alpha_k p_k)); the update of
+// the last iteration is applied by x_flush_kernel at the end of a solve.  So
+// pass B streams r and Ap only: 24 B/DoF (r, Ap in; r out).
 
 constexpr int NTB = 256;
 
@@ -1197,20 +1263,6 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
   for (int i = threadIdx.x; i < ncz * ncy * ncx; i += NTB) s_inv[i] = prm.invd[i];
   __syncthreads();
   const double alpha = ld_vol(&prm.state->alpha);
-  const int k = ld_vol(&prm.state->it);
-  const int j0 = ld_vol(&prm.state->x_done);
-  const int R = ld_vol(&prm.state->ring);
-  // x updates j0..k at the end of each ring period (alpha_k is still in alpha)
-  const bool xup = (k % R == R - 1) && j0 <= k;
-  double aj[kPRing];
-  const double* pj[kPRing];
-#pragma unroll
-  for (int t = 0; t < kPRing; ++t) {
-    const int j = k - (R - 1) + t;
-    const bool on = xup && t < R && j >= j0;
-    aj[t] = on ? (j == k ? alpha : ld_vol(&prm.state->alpha_ring[j % R])) : 0.0;
-    pj[t] = on ? prm.pring + (long long)(j % R) * prm.pstride : nullptr;
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = prm.nx, ny = prm.ny;
   const int nrows = prm.nz * ny;
@@ -1226,46 +1278,37 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
     const long long base = (long long)(zl + prm.ghost) * prm.pitch_z + (long long)y * prm.pitch_y;
     double* rrw = prm.r + base;
     const double* apr = prm.ap + base;
-    double* xr = prm.x + base;
     const int npair = nx >> 1;  // pitch is even: double2 rows
     int q = lane;
-    if (!xup) {
-      // lean pass (r, Ap only): two pairs per step with every load issued
-      // before any store, for memory-level parallelism
-      for (; q + 32 < npair; q += 64) {
-        const int xa = 2 * q, xb = 2 * (q + 32);
-        const double2 ra = ld2(rrw + xa), aa = ld2(apr + xa);
-        const double2 rb = ld2(rrw + xb), ab = ld2(apr + xb);
-        const double ia0 = (xa >= ewx && xa < nx - ewx) ? inv_int : trow[cls_of(xa, nx, ewx)];
-        const double ia1 = (xa + 1 >= ewx && xa + 1 < nx - ewx) ? inv_int : trow[cls_of(xa + 1, nx, ewx)];
-        const double ib0 = (xb >= ewx && xb < nx - ewx) ? inv_int : trow[cls_of(xb, nx, ewx)];
-        const double ib1 = (xb + 1 >= ewx && xb + 1 < nx - ewx) ? inv_int : trow[cls_of(xb + 1, nx, ewx)];
-        double2 na, nb;
-        na.x = __dsub_rn(ra.x, __dmul_rn(alpha, aa.x));
-        na.y = __dsub_rn(ra.y, __dmul_rn(alpha, aa.y));
-        nb.x = __dsub_rn(rb.x, __dmul_rn(alpha, ab.x));
-        nb.y = __dsub_rn(rb.y, __dmul_rn(alpha, ab.y));
-        // same summation order as the one-pair loop: pair q, then pair q+32
-        rz = fma(na.x, __dmul_rn(ia0, na.x), rz);
-        rz = fma(na.y, __dmul_rn(ia1, na.y), rz);
-        rr = fma(na.x, na.x, rr);
-        rr = fma(na.y, na.y, rr);
-        rz = fma(nb.x, __dmul_rn(ib0, nb.x), rz);
-        rz = fma(nb.y, __dmul_rn(ib1, nb.y), rz);
-        rr = fma(nb.x, nb.x, rr);
-        rr = fma(nb.y, nb.y, rr);
-        st2(rrw + xa, na);
-        st2(rrw + xb, nb);
-      }
+    // two pairs per step with every load issued before any store, for
+    // memory-level parallelism
+    for (; q + 32 < npair; q += 64) {
+      const int xa = 2 * q, xb = 2 * (q + 32);
+      const double2 ra = ld2(rrw + xa), aa = ld2(apr + xa);
+      const double2 rb = ld2(rrw + xb), ab = ld2(apr + xb);
+      const double ia0 = (xa >= ewx && xa < nx - ewx) ? inv_int : trow[cls_of(xa, nx, ewx)];
+      const double ia1 = (xa + 1 >= ewx && xa + 1 < nx - ewx) ? inv_int : trow[cls_of(xa + 1, nx, ewx)];
+      const double ib0 = (xb >= ewx && xb < nx - ewx) ? inv_int : trow[cls_of(xb, nx, ewx)];
+      const double ib1 = (xb + 1 >= ewx && xb + 1 < nx - ewx) ? inv_int : trow[cls_of(xb + 1, nx, ewx)];
+      double2 na, nb;
+      na.x = __dsub_rn(ra.x, __dmul_rn(alpha, aa.x));
+      na.y = __dsub_rn(ra.y, __dmul_rn(alpha, aa.y));
+      nb.x = __dsub_rn(rb.x, __dmul_rn(alpha, ab.x));
+      nb.y = __dsub_rn(rb.y, __dmul_rn(alpha, ab.y));
+      // same summation order as the one-pair loop: pair q, then pair q+32
+      rz = fma(na.x, __dmul_rn(ia0, na.x), rz);
+      rz = fma(na.y, __dmul_rn(ia1, na.y), rz);
+      rr = fma(na.x, na.x, rr);
+      rr = fma(na.y, na.y, rr);
+      rz = fma(nb.x, __dmul_rn(ib0, nb.x), rz);
+      rz = fma(nb.y, __dmul_rn(ib1, nb.y), rz);
+      rr = fma(nb.x, nb.x, rr);
+      rr = fma(nb.y, nb.y, rr);
+      st2(rrw + xa, na);
+      st2(rrw + xb, nb);
     }
     for (; q < npair; q += 32) {
       const int xx = 2 * q;
-      double2 xv = make_double2(0.0, 0.0), pv[kPRing];
-      if (xup) {  // issued with the others
-        xv = ld2(xr + xx);
-#pragma unroll
-        for (int t = 0; t < kPRing; ++t) pv[t] = pj[t] ? ld2(pj[t] + base + xx) : xv;
-      }
       const double2 rv = ld2(rrw + xx);
       const double2 av = ld2(apr + xx);
       const double i0 = (xx >= ewx && xx < nx - ewx) ? inv_int : trow[cls_of(xx, nx, ewx)];
@@ -1279,16 +1322,6 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       rr = fma(rn.x, rn.x, rr);
       rr = fma(rn.y, rn.y, rr);
       st2(rrw + xx, rn);
-      if (xup) {
-#pragma unroll
-        for (int t = 0; t < kPRing; ++t) {
-          if (pj[t]) {
-            xv.x = __dadd_rn(xv.x, __dmul_rn(aj[t], pv[t].x));
-            xv.y = __dadd_rn(xv.y, __dmul_rn(aj[t], pv[t].y));
-          }
-        }
-        st2(xr + xx, xv);
-      }
     }
     if ((nx & 1) && lane == 0) {
       const int xx = nx - 1;
@@ -1297,13 +1330,6 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       rrw[xx] = rn;
       rz = fma(rn, __dmul_rn(i0, rn), rz);
       rr = fma(rn, rn, rr);
-      if (xup) {
-        double xs = xr[xx];
-#pragma unroll
-        for (int t = 0; t < kPRing; ++t)
-          if (pj[t]) xs = __dadd_rn(xs, __dmul_rn(aj[t], pj[t][base + xx]));
-        xr[xx] = xs;
-      }
     }
   }
   double v[2] = {rz, rr};
@@ -1735,8 +1761,8 @@ KernelInfo kernel_for(int p, int mode) {
 // without splitting the ragged last wave.  The plan is simulated exactly.
 constexpr double kEdgeTileWeight = 1.08;  // edge-tile plane cost / interior (B200, p=3, measured)
 
-Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki, int nz) {
-  const int TY = tile_h_of(pl->p);
+Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki, int nz, int mode) {
+  const int TY = tile_h_of(pl->p, mode);
   const int tx = (pl->d.nx + TX - 1) / TX, ty = (pl->d.ny + TY - 1) / TY;
   const int tiles = tx * ty;
   const int slots = std::max(1, pl->num_sms * ki.ctas_per_sm);
@@ -1809,7 +1835,7 @@ Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki, int nz) {
   return best;
 }
 
-int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
+int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base, int mode) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int p = pl->p;
@@ -1817,7 +1843,7 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
                         (cuuint64_t)(pl->d.nz + 2 * p)};
   cuuint64_t strides[2] = {(cuuint64_t)(pl->d.pitch_y * 8), (cuuint64_t)(pl->pitch_z * 8)};
   const int px = p + (p & 1);
-  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(tile_h_of(p) + 2 * p), 1u};
+  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(tile_h_of(p, mode) + 2 * p), 1u};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1827,7 +1853,7 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base) {
   return BSPDE_OK;
 }
 
-void fill_common(SepParams& sp, const bspde_plan* pl) {
+void fill_common(SepParams& sp, const bspde_plan* pl, int mode) {
   const auto& d = pl->d;
   const int p = pl->p, R = 2 * p + 1;
   sp.nx = d.nx;
@@ -1843,9 +1869,10 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
   sp.pitch_z = pl->pitch_z;
   for (int a = 0; a < 3; ++a) sp.ew[a] = d.ew[a];
   sp.tiles_x = (d.nx + TX - 1) / TX;
-  sp.tiles_y = (d.ny + tile_h_of(pl->p) - 1) / tile_h_of(pl->p);
+  sp.tiles_y = (d.ny + tile_h_of(pl->p, mode) - 1) / tile_h_of(pl->p, mode);
   for (int k = 0; k < MAXTAP; ++k) {
     sp.tzm[k] = sp.tzk[k] = sp.tym[k] = sp.tyk[k] = sp.txm[k] = sp.txk[k] = 0.0;
+    sp.gm[k] = sp.gk[k] = 0.0;
   }
   for (int k = 0; k < R; ++k) {
     sp.tzm[k] = d.mass_table[0][d.ew[0] * R + k];
@@ -1854,6 +1881,8 @@ void fill_common(SepParams& sp, const bspde_plan* pl) {
     sp.tyk[k] = d.c_stiff[1] * d.stiff_table[1][d.ew[1] * R + k];
     sp.txm[k] = d.mass_table[2][d.ew[2] * R + k];
     sp.txk[k] = d.stiff_table[2][d.ew[2] * R + k];
+    sp.gm[k] = kHostGramM[p - 1][k];
+    sp.gk[k] = kHostGramK[p - 1][k];
   }
   sp.zfast = (d.nz_global > 1 && d.ew[0] > 0) ? 1 : 0;
   sp.c_mass = d.c_mass;
@@ -1888,13 +1917,13 @@ unsigned* scratch_counter(void* s) {
 int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, double* out,
                const double* aux, double aux_scale, double c_mass_override, bool use_override,
                void* scratch, int fuse, cudaStream_t st, double* cg_pout = nullptr,
-               int z_begin = 0, int z_count = -1, int accumulate = 0) {
+               int z_begin = 0, int z_count = -1, int accumulate = 0, double* cg_x = nullptr) {
   KernelInfo ki = kernel_for(pl->p, mode);
   if (z_count < 0) z_count = pl->d.nz - z_begin;
   const auto key = std::make_pair(mode, z_count);
   auto lit = pl->launch_cache.find(key);
   if (lit == pl->launch_cache.end()) {
-    lit = pl->launch_cache.emplace(key, plan_launch(pl, ki, z_count)).first;
+    lit = pl->launch_cache.emplace(key, plan_launch(pl, ki, z_count, mode)).first;
     if (getenv("BSPDE_PLAN_DEBUG"))
       fprintf(stderr, "bspde plan: mode %d grid %d chunks %d len %d items %d main %d split %d\n", mode,
               lit->second.grid, lit->second.nchunks, lit->second.chunk_len, lit->second.nitems,
@@ -1902,7 +1931,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   }
   const Launch ln = lit->second;
   SepParams sp;
-  fill_common(sp, pl);
+  fill_common(sp, pl, mode);
   sp.nchunks = ln.nchunks;
   sp.chunk_len = ln.chunk_len;
   sp.nitems = ln.nitems;
@@ -1915,6 +1944,7 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.cg_r = (mode == M_CGA) ? in0 : nullptr;
   sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
   sp.cg_pout = cg_pout;
+  sp.cg_x = cg_x;
   if (use_override) sp.c_mass = c_mass_override;
   if (scratch) {
     sp.state = scratch_state(scratch);
@@ -1927,10 +1957,10 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.accumulate = accumulate;
   if (ln.grid > MAXGRID) return fail(BSPDE_ERR_STATE, "grid exceeds MAXGRID");
   CUtensorMap m0, m1;
-  int rc = make_map(&m0, pl, in0);
+  int rc = make_map(&m0, pl, in0, mode);
   if (rc) return rc;
   if (in1) {
-    rc = make_map(&m1, pl, in1);
+    rc = make_map(&m1, pl, in1, mode);
     if (rc) return rc;
   } else {
     m1 = m0;
@@ -2011,7 +2041,7 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   if (rc) return rc;
   if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
   // p_{-1} = 0 lives in ring field R - 1 (read by iteration 0)
-  const int R = cfg->p_ring > 0 ? cfg->p_ring : kPRing;
+  const int R = cfg->p_ring > 0 ? cfg->p_ring : 2;
   const long long fs = (long long)(pl->d.nz + 2 * pl->p) * pl->pitch_z;
   CUDA_TRY(cudaMemsetAsync(pring + (R - 1) * fs, 0, bytes, st));
   rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
@@ -2034,8 +2064,8 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
       int crc = BSPDE_OK;
       for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
         crc = launch_sep(pl, M_CGA, r, pring + ((k + R - 1) % R) * fs, ap, nullptr, 0.0,
-                         0.0, false, scratch, 1, st, pring + (k % R) * fs);
-        if (crc == BSPDE_OK) crc = launch_pass_b(pl, x, r, pring, ap, scratch, 1, st);
+                         0.0, false, scratch, 1, st, pring + (k % R) * fs, 0, -1, 0, x);
+        if (crc == BSPDE_OK) crc = launch_pass_b(pl, nullptr, r, nullptr, ap, scratch, 1, st);
       }
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       if (crc) {
@@ -2362,7 +2392,7 @@ int bspde_cg_setup(bspde_plan* pl, void* scratch, double* history, const bspde_c
   if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
   if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
   if (!(cfg->p_ring == 0 || cfg->p_ring == 2 || cfg->p_ring == kPRing))
-    return fail(BSPDE_ERR_ARG, "p_ring must be 2 or 4 (0: default 4)");
+    return fail(BSPDE_ERR_ARG, "p_ring must be 2 or 4 (0: default 2)");
   CgState* hs = reinterpret_cast<CgState*>(pl->host_state);
   cudaStream_t st = (cudaStream_t)stream;
   // the pinned staging buffer may still be in use by a previous async copy
@@ -2372,7 +2402,7 @@ int bspde_cg_setup(bspde_plan* pl, void* scratch, double* history, const bspde_c
   hs->max_iter = cfg->max_iter;
   hs->record_history = cfg->record_history ? 1 : 0;
   hs->has_x0 = cfg->has_x0 ? 1 : 0;
-  hs->ring = cfg->p_ring > 0 ? cfg->p_ring : kPRing;
+  hs->ring = cfg->p_ring > 0 ? cfg->p_ring : 2;
   hs->history = history;
   hs->scale = 1.0;
   CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
@@ -2388,32 +2418,32 @@ int bspde_cg_residual(bspde_plan* pl, const double* b, const double* x, double* 
                     (cudaStream_t)stream);
 }
 
-int bspde_cg_pass_a(bspde_plan* pl, const double* r, const double* p_in, double* p_out,
-                    double* ap, void* scratch, int fuse, void* stream) {
+int bspde_cg_pass_a(bspde_plan* pl, double* x, const double* r, const double* p_in,
+                    double* p_out, double* ap, void* scratch, int fuse, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  if (!x || !r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
   if (p_in == p_out) return fail(BSPDE_ERR_ARG, "p_in and p_out must be different buffers");
   return launch_sep(pl, M_CGA, r, p_in, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
-                    (cudaStream_t)stream, p_out);
+                    (cudaStream_t)stream, p_out, 0, -1, 0, x);
 }
 
-int bspde_cg_pass_a_range(bspde_plan* pl, const double* r, const double* p_in, double* p_out,
-                          double* ap, void* scratch, int z_begin, int z_count, int accumulate,
-                          int fuse, void* stream) {
+int bspde_cg_pass_a_range(bspde_plan* pl, double* x, const double* r, const double* p_in,
+                          double* p_out, double* ap, void* scratch, int z_begin, int z_count,
+                          int accumulate, int fuse, void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  if (!x || !r || !p_in || !p_out || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
   if (p_in == p_out) return fail(BSPDE_ERR_ARG, "p_in and p_out must be different buffers");
   if (z_begin < 0 || z_count < 1 || z_begin + z_count > pl->d.nz)
     return fail(BSPDE_ERR_ARG, "z range outside the owned planes");
   return launch_sep(pl, M_CGA, r, p_in, ap, nullptr, 0.0, 0.0, false, scratch, fuse,
-                    (cudaStream_t)stream, p_out, z_begin, z_count, accumulate ? 1 : 0);
+                    (cudaStream_t)stream, p_out, z_begin, z_count, accumulate ? 1 : 0, x);
 }
 
-int bspde_cg_pass_b(bspde_plan* pl, double* x, double* r, const double* p_ring,
-                    const double* ap, void* scratch, int fuse, void* stream) {
+int bspde_cg_pass_b(bspde_plan* pl, double* r, const double* ap, void* scratch, int fuse,
+                    void* stream) {
   if (int rc = check_plan(pl)) return rc;
-  if (!x || !r || !p_ring || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
-  return launch_pass_b(pl, x, r, p_ring, ap, scratch, fuse, (cudaStream_t)stream);
+  if (!r || !ap || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_pass_b(pl, nullptr, r, nullptr, ap, scratch, fuse, (cudaStream_t)stream);
 }
 
 int bspde_cg_flush_x(bspde_plan* pl, double* x, const double* p_ring, void* scratch,

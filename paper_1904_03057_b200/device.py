@@ -72,9 +72,9 @@ class SlabLayout:
         return torch.zeros(self.buf_shape, dtype=torch.float64, device=device)
 
     def alloc_ring(self, device, n=None):
-        """``n`` (default BSPDE_P_RING) fields back to back: the CG p ring."""
+        """``n`` (default 2) fields back to back: the CG search-direction ring."""
         torch = _torch()
-        n = N.P_RING if n is None else n
+        n = N.RING_DEFAULT if n is None else n
         return torch.zeros((n,) + self.buf_shape, dtype=torch.float64, device=device)
 
     def owned(self, buf):
@@ -180,7 +180,7 @@ class NativePlan:
     def cg_setup(self, scratch, history, tol, max_iter, record_history, has_x0, stream=None,
                  p_ring=None):
         cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)),
-                         int(bool(has_x0)), 0, int(p_ring or N.P_RING))
+                         int(bool(has_x0)), 0, int(p_ring or N.RING_DEFAULT))
         N.check(self.lib.bspde_cg_setup(self.handle, N.ptr(scratch), N.ptr(history),
                                         C.byref(cfg), N.stream_handle(stream)))
 
@@ -188,23 +188,23 @@ class NativePlan:
         N.check(self.lib.bspde_cg_residual(self.handle, N.ptr(b), N.ptr(x), N.ptr(r),
                                            N.ptr(scratch), int(fuse), N.stream_handle(stream)))
 
-    def cg_pass_a(self, r, p_in, p_out, ap, scratch, fuse, stream=None):
-        N.check(self.lib.bspde_cg_pass_a(self.handle, N.ptr(r), N.ptr(p_in), N.ptr(p_out),
-                                         N.ptr(ap), N.ptr(scratch), int(fuse),
+    def cg_pass_a(self, x, r, p_in, p_out, ap, scratch, fuse, stream=None):
+        """p_k, Ap_k, <p_k, Ap_k> and x += alpha_{k-1} p_{k-1} (k >= 1)."""
+        N.check(self.lib.bspde_cg_pass_a(self.handle, N.ptr(x), N.ptr(r), N.ptr(p_in),
+                                         N.ptr(p_out), N.ptr(ap), N.ptr(scratch), int(fuse),
                                          N.stream_handle(stream)))
 
-    def cg_pass_a_range(self, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate, fuse=0,
-                        stream=None):
+    def cg_pass_a_range(self, x, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate,
+                        fuse=0, stream=None):
         """Pass A on the owned output planes [z_begin, z_begin + z_count)."""
-        N.check(self.lib.bspde_cg_pass_a_range(self.handle, N.ptr(r), N.ptr(p_in), N.ptr(p_out),
-                                               N.ptr(ap), N.ptr(scratch), int(z_begin),
-                                               int(z_count), int(bool(accumulate)), int(fuse),
-                                               N.stream_handle(stream)))
+        N.check(self.lib.bspde_cg_pass_a_range(self.handle, N.ptr(x), N.ptr(r), N.ptr(p_in),
+                                               N.ptr(p_out), N.ptr(ap), N.ptr(scratch),
+                                               int(z_begin), int(z_count), int(bool(accumulate)),
+                                               int(fuse), N.stream_handle(stream)))
 
-    def cg_pass_b(self, x, r, pring, ap, scratch, fuse, stream=None):
-        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(x), N.ptr(r), N.ptr(pring),
-                                         N.ptr(ap), N.ptr(scratch), int(fuse),
-                                         N.stream_handle(stream)))
+    def cg_pass_b(self, r, ap, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_cg_pass_b(self.handle, N.ptr(r), N.ptr(ap), N.ptr(scratch),
+                                         int(fuse), N.stream_handle(stream)))
 
     def cg_flush_x(self, x, pring, scratch, stream=None):
         N.check(self.lib.bspde_cg_flush_x(self.handle, N.ptr(x), N.ptr(pring), N.ptr(scratch),
@@ -230,15 +230,16 @@ HBM_BUDGET = 175e9  # bytes of HBM3e a rank may fill with fields (B200: 180 GB u
 def heat_memory_plan(cext, degree, world=1, budget=HBM_BUDGET, ring=None):
     """Per-rank resident bytes of a heat run on ``world`` z-slabs.
 
-    Fields: u, F, r, Ap (b aliases Ap) and the search-direction ring (R = 4
-    when it fits, else 2).  Returns dict(ring, fields, field_bytes, bytes).
-    1536^3 p=3 on one GPU: 6 fields x 29.1 GB = 174.7 GB with R = 2."""
+    Fields: u, F, r, Ap (b aliases Ap) and the search-direction ring (R = 2:
+    p_{k-1}, p_k; pass A applies the x updates).  Returns dict(ring,
+    fields, field_bytes, bytes).  1536^3 p=3 on one GPU: 6 fields x 29.1 GB =
+    174.7 GB."""
     from .errors import ConfigurationError
 
     nzg, ny, nx = (int(v) for v in cext)
     nz = -(-nzg // int(world))  # the largest slab
     field = SlabLayout(nz, ny, nx, ghost=int(degree)).bytes
-    for R in ((ring,) if ring else (N.P_RING, 2)):
+    for R in ((ring,) if ring else (N.RING_DEFAULT,)):
         total = (HEAT_BASE_FIELDS + R) * field
         if total <= budget:
             return dict(ring=R, fields=HEAT_BASE_FIELDS + R, field_bytes=field, bytes=total)
@@ -247,10 +248,10 @@ def heat_memory_plan(cext, degree, world=1, budget=HBM_BUDGET, ring=None):
         f" GB per rank > {budget / 1e9:.0f} GB; use more GPUs")
 
 
-def choose_ring(layout, device, fields_to_add=2):
-    """Ring length for a CG work set about to be allocated: BSPDE_P_RING (4)
-    if ``fields_to_add`` + 4 more fields fit in free HBM with 2 GB to spare,
-    else 2.  ``BSPDE_P_RING_LEN`` (2 or 4) overrides."""
+def choose_ring(layout=None, device=None):
+    """Ring length of a CG work set: 2 (p_{k-1}, p_k; pass A applies x += alpha
+    p, so no longer ring is needed).  ``BSPDE_P_RING_LEN`` = 4 keeps four
+    fields (testing the ring indexing)."""
     import os
 
     env = os.environ.get("BSPDE_P_RING_LEN")
@@ -259,8 +260,7 @@ def choose_ring(layout, device, fields_to_add=2):
         if R not in (2, N.P_RING):
             raise ValidationError(f"BSPDE_P_RING_LEN must be 2 or {N.P_RING}, got {env}")
         return R
-    free, _ = _torch().cuda.mem_get_info(device)
-    return N.P_RING if free >= (fields_to_add + N.P_RING) * layout.bytes + 2e9 else 2
+    return N.RING_DEFAULT
 
 
 def check_host_field(c, shape, what="input coefficients"):

@@ -16,12 +16,12 @@ Per CG iteration (``distributed_pcg``):
      finalize and pass B; r's follows pass B ("pipeline", the default; see
      ``_halo_mode`` for "split", which also runs pass A's interior planes
      under r's exchange through ``bspde_cg_pass_a_range``);
-  2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer)
-     and writes the local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread
-     finalize kernel runs the scalar update on every rank;
-  3. pass B (fuse=0): r -= alpha Ap (x every R-th iteration, R = the
-     length of the search-direction ring, 2 or 4), local <r, D^-1 r>,
-     <r, r>; ``all_reduce`` of 2 doubles; finalize.
+  2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer),
+     applies x += alpha_{k-1} p_{k-1} on the owned planes and writes the
+     local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread finalize kernel
+     runs the scalar update on every rank;
+  3. pass B (fuse=0): r -= alpha Ap, local <r, D^-1 r>, <r, r>;
+     ``all_reduce`` of 2 doubles; finalize.
 
 Every rank holds identical scalar state, so the device-side ``active`` flag
 (stop rule, guards) agrees everywhere; the host polls it every
@@ -204,14 +204,14 @@ class NativeSlabOps:
     def residual(self, b, x, r, scratch):
         self.plan.cg_residual(b, x, r, scratch, 0)
 
-    def pass_a(self, r, p_in, p_out, ap, scratch):
-        self.plan.cg_pass_a(r, p_in, p_out, ap, scratch, 0)
+    def pass_a(self, x, r, p_in, p_out, ap, scratch):
+        self.plan.cg_pass_a(x, r, p_in, p_out, ap, scratch, 0)
 
-    def pass_a_range(self, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate):
-        self.plan.cg_pass_a_range(r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate, 0)
+    def pass_a_range(self, x, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate):
+        self.plan.cg_pass_a_range(x, r, p_in, p_out, ap, scratch, z_begin, z_count, accumulate, 0)
 
-    def pass_b(self, x, r, pring, ap, scratch):
-        self.plan.cg_pass_b(x, r, pring, ap, scratch, 0)
+    def pass_b(self, r, ap, scratch):
+        self.plan.cg_pass_b(r, ap, scratch, 0)
 
     def finalize(self, scratch, kind):
         self.plan.cg_finalize(scratch, kind)
@@ -279,27 +279,27 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
                 p_in, p_out = pring[(k - 1) % R], pring[k % R]
                 if mode == "off":
                     halo(r, p_in)
-                    ops.pass_a(r, p_in, p_out, ap, scratch)
+                    ops.pass_a(x, r, p_in, p_out, ap, scratch)
                 elif mode == "pipeline":
                     halo.wait(halo.start(r) + pending_p)
-                    ops.pass_a(r, p_in, p_out, ap, scratch)
+                    ops.pass_a(x, r, p_in, p_out, ap, scratch)
                 else:  # split
                     works = halo.start(r)
-                    ops.pass_a_range(r, p_in, p_out, ap, scratch, g, nz - 2 * g, False)
+                    ops.pass_a_range(x, r, p_in, p_out, ap, scratch, g, nz - 2 * g, False)
                     halo.wait(works + pending_p)
-                    ops.pass_a_range(r, p_in, p_out, ap, scratch, 0, g, True)
-                    ops.pass_a_range(r, p_in, p_out, ap, scratch, nz - g, g, True)
+                    ops.pass_a_range(x, r, p_in, p_out, ap, scratch, 0, g, True)
+                    ops.pass_a_range(x, r, p_in, p_out, ap, scratch, nz - g, g, True)
                 pending_p = halo.start(p_out) if mode != "off" else []
                 allreduce(ops.sums(scratch, 1))
                 ops.finalize(scratch, 1)
-                ops.pass_b(x, r, pring, ap, scratch)
+                ops.pass_b(r, ap, scratch)
                 allreduce(ops.sums(scratch, 2))
                 ops.finalize(scratch, 2)
                 k += 1
             rep, active = ops.read(scratch)
     finally:
         halo.wait(pending_p)
-    ops.flush_x(x, pring, scratch)  # the pending x updates
+    ops.flush_x(x, pring, scratch)  # the last iteration's x update
     return rep, time.perf_counter() - t0
 
 

@@ -65,10 +65,18 @@ class CpuSlabOps:
         scratch[1] = float((rv * (own_inv * rv)).sum())
         scratch[2] = float((rv ** 2).sum())
 
-    def pass_a(self, r, p_in, p_out, ap, scratch):
+    def _x_update(self, x, p_in):
+        """x += alpha_{k-1} p_{k-1} (pass A of iteration k >= 1, as the kernel)."""
+        s = self.state
+        if s["it"] >= 1 and not s.get("x_applied_in", -1) == s["it"]:
+            self._own(x).add_(s["alpha"] * self._own(p_in))
+            s["x_applied_in"] = s["it"]
+
+    def pass_a(self, x, r, p_in, p_out, ap, scratch):
         s = self.state
         if not s["active"]:
             return
+        self._x_update(x, p_in)
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         pn = r[:, :, :nx] * self.inv + s["beta"] * p_in[:, :, :nx]
         self._own(p_out).copy_(pn[g:g + nz])
@@ -76,7 +84,7 @@ class CpuSlabOps:
         self._own(ap).copy_(apv)
         scratch[0] = float((pn[g:g + nz] * apv).sum())
 
-    def pass_a_range(self, r, p_in, p_out, ap, scratch, z0, cnt, accumulate):
+    def pass_a_range(self, x, r, p_in, p_out, ap, scratch, z0, cnt, accumulate):
         """bspde_cg_pass_a_range: only owned planes [z0, z0 + cnt) are
         produced; the interior range is called while the ghosts are still in
         flight, so outputs there must not depend on them (banded in z)."""
@@ -85,6 +93,7 @@ class CpuSlabOps:
             return
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         self.range_calls = getattr(self, "range_calls", 0) + 1
+        self._x_update(x, p_in)  # (the kernel updates each range's planes; same result)
         pn = r[:, :, :nx] * self.inv + s["beta"] * p_in[:, :, :nx]
         apv = self._apply(torch.nn.functional.pad(pn, (0, p_in.shape[2] - nx)))
         sl = slice(z0, z0 + cnt)
@@ -93,23 +102,12 @@ class CpuSlabOps:
         part = float((pn[g:g + nz][sl] * apv[sl]).sum())
         scratch[0] = (float(scratch[0]) if accumulate else 0.0) + part
 
-    def _apply_x(self, x, pring, upto, alphas):
-        s = self.state
-        R = pring.shape[0]
-        for j in range(s.get("x_done", 0), upto):  # in order, as the kernels
-            self._own(x).add_(alphas[j % R] * self._own(pring[j % R]))
-
-    def pass_b(self, x, r, pring, ap, scratch):
+    def pass_b(self, r, ap, scratch):
         s = self.state
         if not s["active"]:
             return
         g, nz, nx = self.lay.ghost, self.lay.nz, self.lay.nx
         own_inv = self.inv[g:g + nz, :, :nx]
-        R, k = pring.shape[0], s["it"]
-        if k % R == R - 1:  # every R-th iteration: the last R updates, as cg_pass_b_kernel
-            ring = list(s.setdefault("alpha_ring", [0.0] * R))
-            ring[k % R] = s["alpha"]
-            self._apply_x(x, pring, k + 1, ring)
         self._own(r).sub_(s["alpha"] * self._own(ap))
         rv = self._own(r)
         scratch[0] = float((rv * (own_inv * rv)).sum())
@@ -128,6 +126,7 @@ class CpuSlabOps:
         elif not s["active"]:
             return
         elif kind == 1:
+            s["x_done"] = s["it"]
             pAp = float(scratch[0])
             if pAp <= 0:
                 s["active"] = 0
@@ -137,10 +136,7 @@ class CpuSlabOps:
         else:
             rz_new, rr = float(scratch[0]), float(scratch[1])
             ring = s.setdefault("alpha_ring", [0.0] * 4)
-            R = len(ring)
-            ring[s["it"] % R] = s["alpha"]
-            if s["it"] % R == R - 1:
-                s["x_done"] = s["it"] + 1
+            ring[s["it"] % len(ring)] = s["alpha"]
             s["beta"] = rz_new / s["rz"]
             s["rz"] = rz_new
             s["res"] = np.sqrt(rr)
@@ -149,7 +145,10 @@ class CpuSlabOps:
 
     def flush_x(self, x, pring, scratch):
         s = self.state
-        self._apply_x(x, pring, s["it"], s.get("alpha_ring", [0.0] * pring.shape[0]))
+        R = pring.shape[0]
+        ring = s.get("alpha_ring", [0.0] * R)
+        for j in range(s.get("x_done", 0), s["it"]):  # the last iteration's update
+            self._own(x).add_(ring[j % R] * self._own(pring[j % R]))
         s["x_done"] = s["it"]
 
     def read(self, scratch):

@@ -65,14 +65,17 @@ def _worker(rank, world, port, ext, p, mode, ring, q):
         op = DistributedOperator(data, device=0)
         b_full, x0_full = _inputs(ext, p)
         b = op.scatter(b_full)
-        x = op.scatter(x0_full)
-        rep = op.pcg_device(b, x, SolveConfig(tol=1e-13, max_iter=2000, poll_every=3),
-                            has_x0=True)
+        its = []
+        for tol in (1e-10, 1e-13):  # counts at the north_star tol; coefficients at 1e-13
+            x = op.scatter(x0_full)
+            rep = op.pcg_device(b, x, SolveConfig(tol=tol, max_iter=2000, poll_every=3),
+                                has_x0=True)
+            its.append(rep.iterations)
         xs = op.gather(x)
         # a distributed apply through the same halo path
         t = op.gather(op.apply_device(op.scatter(x0_full), op.layout.alloc(op.device)))
         if rank == 0:
-            q.put((rep.iterations, xs, t, int(op._work["pring"].shape[0]), op.layout.nz))
+            q.put((its, xs, t, int(op._work["pring"].shape[0]), op.layout.nz))
     finally:
         dist.destroy_process_group()
 
@@ -110,15 +113,19 @@ def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
     assert ring_used == ring
     data, step = _system(ext, p)
     b_full, x0_full = _inputs(ext, p)
-    # fused single-rank solver on the same inputs
+    # fused single-rank solver and the oracle recurrence on the same inputs:
+    # counts +-1 at tol 1e-10; at tol 1e-13 (hundreds of iterations) +-max(1, 1%)
+    # and the coefficients to 1e-10
     op = make_operator(data, "b200")
-    x1, rep1 = pcg(op, b_full, SolveConfig(tol=1e-13, max_iter=2000), x0=x0_full)
-    assert abs(its - rep1.iterations) <= 1, (its, rep1.iterations)
-    assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-10
-    # oracle recurrence and apply
     ora = O.KronOperator(ext, step, p, 0.02, 1.0)
-    xo, ro = O.pcg(ora.apply, ora.jacobi_diagonal, b_full, tol=1e-13, max_iter=2000, x0=x0_full)
-    assert abs(its - ro["iterations"]) <= 1, (its, ro["iterations"])
+    for k, tol in enumerate((1e-10, 1e-13)):
+        x1, rep1 = pcg(op, b_full, SolveConfig(tol=tol, max_iter=2000), x0=x0_full)
+        xo, ro = O.pcg(ora.apply, ora.jacobi_diagonal, b_full, tol=tol, max_iter=2000,
+                       x0=x0_full)
+        bar = 1 if k == 0 else max(1, round(0.01 * ro["iterations"]))
+        assert abs(its[k] - rep1.iterations) <= bar, (tol, its[k], rep1.iterations)
+        assert abs(its[k] - ro["iterations"]) <= bar, (tol, its[k], ro["iterations"])
+    assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-10
     assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
     want = ora.apply(x0_full)
     assert np.abs(t - want).max() / np.abs(want).max() < 1e-13

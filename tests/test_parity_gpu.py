@@ -332,7 +332,7 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     st = w.scratch[:160].cpu().numpy().view(np.float64)
     rz0 = float(np.vdot(r0, inv * r0))
     assert abs(st[4] - rz0) / rz0 < 1e-12  # state.rz
-    plan.cg_pass_a(w.r, w.pring[R - 1], w.pring[0], w.ap, w.scratch, 1)
+    plan.cg_pass_a(xb, w.r, w.pring[R - 1], w.pring[0], w.ap, w.scratch, 1)
     torch.cuda.synchronize()
     p0 = inv * r0
     assert float(relmax(lay.download(w.pring[0]), p0)) < 1e-13  # p_k written by pass A
@@ -344,11 +344,11 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     assert abs(st[7] - pAp) / pAp < 1e-12  # state.pAp
     alpha = rz0 / pAp
     assert abs(st[5] - alpha) / alpha < 1e-12  # state.alpha
-    plan.cg_pass_b(xb, w.r, w.pring, w.ap, w.scratch, 1)
+    plan.cg_pass_b(w.r, w.ap, w.scratch, 1)
     torch.cuda.synchronize()
     x1 = x0 + alpha * p0
     r1 = r0 - alpha * Ap
-    # x moves every P_RING-th pass B (or on a flush)
+    # x moves in the next pass A (or on the flush at the end of a solve)
     assert np.array_equal(lay.download(xb), x0)
     assert relmax(lay.download(w.r), r1) < 1e-12
     rep, active = plan.cg_read(w.scratch)
@@ -360,12 +360,20 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     assert relmax(lay.download(xe), x1) < 1e-13
     plan.cg_flush_x(xe, w.pring, w.scratch)  # idempotent: nothing pending any more
     assert relmax(lay.download(xe), x1) < 1e-13
+    # ... and pass A of iteration 1 applies the same update: x1 = x0 + alpha p0
+    # (forced active: the p = 5 case trips the divergence guard at iteration 1)
+    R1 = 1 % R
+    w.scratch[120:124].view(torch.int32)[0] = 1  # CgState.active
+    plan.cg_pass_a(xb, w.r, w.pring[0], w.pring[R1], w.ap, w.scratch, 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(lay.download(xb), lay.download(xe))
 
 
-@pytest.mark.parametrize("iters", [1, 2, 3, 4, 5, 7, 8, 9])
-def test_deferred_x_update_is_bitwise_eager(cuda_device, iters):
-    """Pass B moves x every P_RING-th iteration; flushing after every
-    iteration instead must give bit-identical x (the same stored roundings)."""
+@pytest.mark.parametrize("iters,ring", [(1, 2), (2, 2), (3, 2), (5, 2), (8, 2), (3, 4), (9, 4)])
+def test_deferred_x_update_is_bitwise_eager(cuda_device, iters, ring):
+    """Pass A of iteration k applies x += alpha_{k-1} p_{k-1}; flushing after
+    every pass B instead (x updated one pass A earlier) must give bit-identical
+    x (the same stored roundings, solver.py:94), for both ring lengths."""
     import torch
 
     ext, p = (13, 12, 11), 3
@@ -380,14 +388,14 @@ def test_deferred_x_update_is_bitwise_eager(cuda_device, iters):
         lay, plan = op.layout, op.plan()
         bb, xb = lay.upload(b, op.device), lay.upload(x0, op.device)
         r, ap = lay.alloc(op.device), lay.alloc(op.device)
-        pring = lay.alloc_ring(op.device)
+        pring = lay.alloc_ring(op.device, ring)
         R = pring.shape[0]
         scratch = plan.scratch()
-        plan.cg_setup(scratch, None, 1e-300, 100, False, True)
+        plan.cg_setup(scratch, None, 1e-300, 100, False, True, p_ring=R)
         plan.cg_residual(bb, xb, r, scratch, 1)
         for k in range(iters):
-            plan.cg_pass_a(r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
-            plan.cg_pass_b(xb, r, pring, ap, scratch, 1)
+            plan.cg_pass_a(xb, r, pring[(k - 1) % R], pring[k % R], ap, scratch, 1)
+            plan.cg_pass_b(r, ap, scratch, 1)
             if eager:
                 plan.cg_flush_x(xb, pring, scratch)
         plan.cg_flush_x(xb, pring, scratch)
@@ -599,24 +607,31 @@ def test_pass_a_ranges_on_emulated_slabs(cuda_device, p, ext, world):
             return buf
 
         rb, qb = slab(r_full), slab(q_full)
+        x0 = rng.normal(size=(hi - lo, ny, nx))
         outs = []
         for split in (False, True):
             scratch = plan.scratch()
             plan.cg_setup(scratch, None, 1e-300, 100, False, False)
+            scratch[40:48].view(torch.float64)[0] = 0.61  # CgState.alpha (= alpha_{k-1})
             scratch[48:56].view(torch.float64)[0] = beta  # CgState.beta
+            scratch[112:116].view(torch.int32)[0] = 1     # CgState.it: iteration k = 1
             scratch[120:124].view(torch.int32)[0] = 1     # CgState.active (14 doubles, it, max_iter)
             ap, pout = lay.alloc(cuda_device), lay.alloc(cuda_device)
+            xb = lay.upload(x0, cuda_device)
             pout.fill_(float("nan"))
             if split:
                 nz = lay.nz
-                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, p, nz - 2 * p, False)
-                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, 0, p, True)
-                plan.cg_pass_a_range(rb, qb, pout, ap, scratch, nz - p, p, True)
+                plan.cg_pass_a_range(xb, rb, qb, pout, ap, scratch, p, nz - 2 * p, False)
+                plan.cg_pass_a_range(xb, rb, qb, pout, ap, scratch, 0, p, True)
+                plan.cg_pass_a_range(xb, rb, qb, pout, ap, scratch, nz - p, p, True)
             else:
-                plan.cg_pass_a(rb, qb, pout, ap, scratch, 0)
+                plan.cg_pass_a(xb, rb, qb, pout, ap, scratch, 0)
             torch.cuda.synchronize()
             outs.append((lay.download(ap), lay.download(pout),
                          float(scratch[:8].view(torch.float64)[0])))
+            # x += alpha_{k-1} p_{k-1} on the owned planes, rounded as solver.py:94
+            want_x = x0 + 0.61 * q_full.reshape(nzg, ny, nx)[lo:hi]
+            assert np.array_equal(lay.download(xb), want_x)
         (a0, p0, d0), (a1, p1, d1) = outs
         assert np.array_equal(a0, a1) and np.array_equal(p0, p1)
         assert abs(d0 - d1) <= 1e-12 * abs(d0)
@@ -640,7 +655,7 @@ def test_pass_a_range_rejects_bad_ranges(cuda_device):
     scratch = plan.scratch()
     for z0, cnt in [(-1, 2), (0, 0), (lay.nz - 1, 2)]:
         with pytest.raises(Exception, match="z range"):
-            plan.cg_pass_a_range(r, q, o, ap, scratch, z0, cnt, False)
+            plan.cg_pass_a_range(o, r, q, o, ap, scratch, z0, cnt, False)
 
 
 @pytest.mark.slow

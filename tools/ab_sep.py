@@ -64,9 +64,9 @@ for it in range(18):
         dig["r0"] = digest(lay.owned(w.r))
         dig["resid_sums"] = digest(w.scratch[:64])
     k = it
-    plan.cg_pass_a(w.r, w.pring[(k - 1) % R], w.pring[k % R], w.ap, w.scratch, 1)
+    plan.cg_pass_a(x, w.r, w.pring[(k - 1) % R], w.pring[k % R], w.ap, w.scratch, 1)
     e[3].record()
-    plan.cg_pass_b(x, w.r, w.pring, w.ap, w.scratch, 1)
+    plan.cg_pass_b(w.r, w.ap, w.scratch, 1)
     e[4].record()
     torch.cuda.synchronize()
     if it == 0:

@@ -26,11 +26,12 @@ op.mass_apply_device(u, b, F, a=dt)
 plan = op.plan()
 w = _work(op, 10)
 PP, K = w.pring, [0]
+    RR = PP.shape[0]
 plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
 plan.cg_residual(b, u, w.r, w.scratch, 1)
 for _ in range(iters):
-    plan.cg_pass_a(w.r, PP[(K[0] - 1) % 4], PP[K[0] % 4], w.ap, w.scratch, 1)
-    plan.cg_pass_b(u, w.r, w.pring, w.ap, w.scratch, 1); K[0] += 1
+    plan.cg_pass_a(u, w.r, PP[(K[0] - 1) % RR], PP[K[0] % RR], w.ap, w.scratch, 1)
+    plan.cg_pass_b(w.r, w.ap, w.scratch, 1); K[0] += 1
 torch.cuda.synchronize()
 rep, active = plan.cg_read(w.scratch)
 print("ok", ncoef, "p", p, "iters", rep.iterations, "relres", rep.relative_residual)

@@ -15,13 +15,15 @@ u = lay.alloc(dev); b = lay.alloc(dev)
 gaussian_coeffs(N, h, 3, device=dev, out=u, layout=lay, **IC)
 op.mass_apply_device(u, b)
 plan = op.plan(); w = _work(op, 10); PP, K = w.pring, [0]
+    RR = PP.shape[0]
 PP, K = w.pring, [0]
+    RR = PP.shape[0]
 ts = []
 for rep in range(4):
     plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
     plan.cg_residual(b, u, w.r, w.scratch, 1)
-    plan.cg_pass_a(w.r, PP[(K[0] - 1) % 4], PP[K[0] % 4], w.ap, w.scratch, 1)
-    plan.cg_pass_b(u, w.r, w.pring, w.ap, w.scratch, 1); K[0] += 1
+    plan.cg_pass_a(u, w.r, PP[(K[0] - 1) % RR], PP[K[0] % RR], w.ap, w.scratch, 1)
+    plan.cg_pass_b(w.r, w.ap, w.scratch, 1); K[0] += 1
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); plan.cg_flush_x(u, w.pring, w.scratch); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))

@@ -33,7 +33,7 @@ part = SlabPartition(nzg, world, rank)
 lay = SlabLayout(part.nz, ny, nx, ghost=p, z_offset=part.z_offset, nz_global=nzg)
 dev = torch.device("cuda:0")
 plan = NativePlan(data, lay, dev)
-r, q, o, ap = (lay.alloc(dev) for _ in range(4))
+r, q, o, ap, xx = (lay.alloc(dev) for _ in range(5))
 r.normal_()
 q.normal_()
 scratch = plan.scratch()
@@ -44,22 +44,22 @@ nz = lay.nz
 
 
 def whole():
-    plan.cg_pass_a(r, q, o, ap, scratch, 0)
+    plan.cg_pass_a(xx, r, q, o, ap, scratch, 0)
 
 
 def split():
-    plan.cg_pass_a_range(r, q, o, ap, scratch, p, nz - 2 * p, False)
-    plan.cg_pass_a_range(r, q, o, ap, scratch, 0, p, True)
-    plan.cg_pass_a_range(r, q, o, ap, scratch, nz - p, p, True)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, p, nz - 2 * p, False)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, 0, p, True)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, nz - p, p, True)
 
 
 def interior():
-    plan.cg_pass_a_range(r, q, o, ap, scratch, p, nz - 2 * p, False)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, p, nz - 2 * p, False)
 
 
 def boundary():
-    plan.cg_pass_a_range(r, q, o, ap, scratch, 0, p, True)
-    plan.cg_pass_a_range(r, q, o, ap, scratch, nz - p, p, True)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, 0, p, True)
+    plan.cg_pass_a_range(xx, r, q, o, ap, scratch, nz - p, p, True)
 
 
 res = {"ncoef": ncoef, "p": p, "world": world, "rank": rank, "slab_planes": nz,
