@@ -294,6 +294,27 @@ int bspde_stencil_pcg(bspde_stencil* plan, const double* P, const double* b,
                       double* history, const bspde_cg_config* cfg,
                       bspde_cg_report* report, int32_t precond, void* stream);
 
+/* ---- matrix-free ("on-the-fly") variable-coefficient operator -------------
+ * The reference's OnTheFlyOperator (operator.py:217-229; stencil_block /
+ * term_stencil, assembly.py:280-297, :460-472) without any stored stencil:
+ * a sum-factorised z-streaming kernel rebuilds every node's stencil action
+ * from the D / mu fields and the trilinear tables on each apply (32 B/DoF of
+ * HBM traffic, no (2p+1)^3 per-node array).  3-D boxes, no face terms,
+ * n_b = n_p <= 3 (bspde_otf_supported); the plan is a bspde_stencil plan.
+ * prepare: keeps the device field pointers (dense parameter-grid arrays,
+ * alive while the plan is used) and writes the Jacobi diagonal into diag
+ * (N doubles, kept and used by the PCG). */
+int bspde_otf_supported(const bspde_stencil* plan);
+int bspde_otf_prepare(bspde_stencil* plan, const double* dfield, const double* mfield,
+                      double* diag, void* stream);
+/* out = A c.  Replaces OnTheFlyOperator.apply (operator.py:217-229). */
+int bspde_otf_apply(bspde_stencil* plan, const double* c, double* out, void* stream);
+/* Jacobi-PCG with the matrix-free apply (same recurrence and state as
+ * bspde_stencil_pcg).  Replaces pcg over OnTheFlyOperator (solver.py:51-117). */
+int bspde_otf_pcg(bspde_stencil* plan, const double* b, double* x, double* r, double* p,
+                  double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
+                  bspde_cg_report* report, int32_t precond, void* stream);
+
 /* ---- mask (voxel) domains ------------------------
  * Replaces the reference's boundary-stencil machinery for MaskDomain
  * systems: _attach_mask_boundary (assembly.py:538-637), the exposed-face

@@ -138,6 +138,11 @@ SIGNATURES = [
     ("bspde_stencil_create", C.c_int, [C.POINTER(StencilDesc), C.POINTER(C.c_void_p)]),
     ("bspde_stencil_destroy", C.c_int, [_VP]),
     ("bspde_stencil_entries", C.c_int64, [_VP]),
+    ("bspde_otf_supported", C.c_int, [_VP]),
+    ("bspde_otf_prepare", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("bspde_otf_apply", C.c_int, [_VP, _VP, _VP, _VP]),
+    ("bspde_otf_pcg", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, C.POINTER(CgConfig),
+                                C.POINTER(CgReport), C.c_int32, _VP]),
     ("bspde_stencil_launch_count", C.c_int64, [_VP]),
     ("bspde_stencil_assemble", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_stencil_apply", C.c_int, [_VP, _VP, _VP, _VP, _VP]),

@@ -64,8 +64,11 @@ constexpr int MAXTAP = 2 * MAXP + 1;
 // Per (degree, mode): CG pass A at p = 3 carries the p ring and the x update
 // and runs 12 warps with 168 registers (64 x 24 tiles; 16 warps spill at the
 // 128-register cap); the other p <= 3 kernels run 16 warps (64 x 32 tiles)
+#ifndef BSPDE_W_CGA3
+#define BSPDE_W_CGA3 12
+#endif
 __host__ __device__ constexpr int warps_of(int p, int mode) {
-  return p <= 3 ? ((p == 3 && mode == 3 /* M_CGA */) ? 12 : BSPDE_W_LOWP) : 12;
+  return p <= 3 ? ((p == 3 && mode == 3 /* M_CGA */) ? BSPDE_W_CGA3 : BSPDE_W_LOWP) : 12;
 }
 __host__ __device__ constexpr int tile_h_of(int p, int mode) { return RPT * warps_of(p, mode) / 2; }
 
@@ -104,7 +107,7 @@ struct Cfg {
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
   static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 4 + 2) + 8 * NS;
+    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 8 + 2) + 8 * NS;
   }
 };
 
@@ -350,31 +353,64 @@ __global__ void finalize_kernel(CgState* s, int kind) {
   }
 }
 
-// Deterministic block reduction of NV values, per-CTA partials, then the
-// last CTA to finish reduces the partials in fixed order (and optionally runs
-// the scalar update).  s_red must hold NWARP*4 doubles.
+// Double-double ("compensated") accumulation of the CG scalars.  Every dot
+// product is accumulated as an unevaluated sum hi + lo: small position-
+// determined groups of terms (a thread's 4 output rows of one plane in pass
+// A, a row pair in pass B) are summed with plain FMAs, and everything above
+// that -- a thread's groups, the warp, the CTA and the grid -- is added with
+// error-free transformations (Knuth TwoSum).  The total is then the sum of
+// the group sums to ~1e-32 relative, i.e. correctly rounded except at near
+// ties: the scalars, hence the CG iterates, do not depend on the tile
+// geometry, the CTA count or the number of z-slabs (the reference itself
+// sums with numpy/BLAS; correctly rounded dots reproduce its iteration
+// counts).
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
+  const double s = __dadd_rn(hi, x);
+  const double bp = __dsub_rn(s, hi);
+  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bp)), __dsub_rn(x, bp));
+  hi = s;
+  lo = __dadd_rn(lo, e);
+}
+
+__device__ __forceinline__ void dd_add2(double& hi, double& lo, double xhi, double xlo) {
+  dd_add(hi, lo, xhi);
+  lo = __dadd_rn(lo, xlo);
+}
+
+// Deterministic block reduction of NV double-double values (hi, lo), per-CTA
+// partials (hi, lo pairs), then the last CTA to finish reduces the partials
+// in fixed order (and optionally runs the scalar update).  s_red must hold
+// NWARP*8 doubles.
 template <int NV, int NWARP>
-__device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_last_p,
-                                    double* partials, unsigned* counter, CgState* st, int fuse,
-                                    int kind, int accumulate = 0) {
+__device__ void reduce_and_finalize(double (&vh)[NV], double (&vl)[NV], double* s_red,
+                                    unsigned* s_last_p, double* partials, unsigned* counter,
+                                    CgState* st, int fuse, int kind, int accumulate = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+    for (int off = 16; off > 0; off >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, vh[i], off);
+      const double ol = __shfl_xor_sync(0xffffffffu, vl[i], off);
+      dd_add2(vh[i], vl[i], oh, ol);
+    }
   }
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) s_red[warp * 4 + i] = v[i];
+    for (int i = 0; i < NV; ++i) {
+      s_red[warp * 8 + 2 * i] = vh[i];
+      s_red[warp * 8 + 2 * i + 1] = vl[i];
+    }
   }
   __syncthreads();
   unsigned& s_last = *s_last_p;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      double acc = 0.0;
-      for (int w = 0; w < NWARP; ++w) acc += s_red[w * 4 + i];
-      partials[blockIdx.x * 4 + i] = acc;
+      double h = 0.0, l = 0.0;
+      for (int w = 0; w < NWARP; ++w) dd_add2(h, l, s_red[w * 8 + 2 * i], s_red[w * 8 + 2 * i + 1]);
+      partials[blockIdx.x * 8 + 2 * i] = h;
+      partials[blockIdx.x * 8 + 2 * i + 1] = l;
     }
     __threadfence();
     const unsigned ticket = atomicAdd(counter, 1u);
@@ -383,26 +419,46 @@ __device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_
   __syncthreads();
   if (s_last && warp == 0) {
     __threadfence();
-    double tot[NV];
+    double th[NV], tl[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) tot[i] = 0.0;
+    for (int i = 0; i < NV; ++i) th[i] = tl[i] = 0.0;
     for (int b = lane; b < (int)gridDim.x; b += 32) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i) tot[i] += ld_vol(&partials[b * 4 + i]);
+      for (int i = 0; i < NV; ++i)
+        dd_add2(th[i], tl[i], ld_vol(&partials[b * 8 + 2 * i]), ld_vol(&partials[b * 8 + 2 * i + 1]));
     }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) tot[i] += __shfl_xor_sync(0xffffffffu, tot[i], off);
+      for (int off = 16; off > 0; off >>= 1) {
+        const double oh = __shfl_xor_sync(0xffffffffu, th[i], off);
+        const double ol = __shfl_xor_sync(0xffffffffu, tl[i], off);
+        dd_add2(th[i], tl[i], oh, ol);
+      }
     }
     if (lane == 0) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i) st->sums[i] = accumulate ? st->sums[i] + tot[i] : tot[i];
+      for (int i = 0; i < NV; ++i) {
+        const double tot = __dadd_rn(th[i], tl[i]);
+        st->sums[i] = accumulate ? st->sums[i] + tot : tot;
+      }
       if (fuse) finalize_state(st, kind);
       *counter = 0u;
       __threadfence();
     }
   }
+}
+
+// plain per-thread sums (each value one group)
+template <int NV, int NWARP>
+__device__ void reduce_and_finalize(double (&v)[NV], double* s_red, unsigned* s_last_p,
+                                    double* partials, unsigned* counter, CgState* st, int fuse,
+                                    int kind, int accumulate = 0) {
+  double lo[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) lo[i] = 0.0;
+  reduce_and_finalize<NV, NWARP>(v, lo, s_red, s_last_p, partials, counter, st, fuse, kind,
+                                 accumulate);
 }
 
 // ---------------------------------------------------------------------------
@@ -650,7 +706,7 @@ template <int P, int MODE, int TK>
 __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm, const ItemGeom& g,
                                            int j, uint32_t f, double (&acc)[2 * P][RPT],
                                            double (&pr)[P][RPT], const double (&auxv)[RPT],
-                                           double (&dsum)[3], double beta) {
+                                           double (&dsum)[6], double beta) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
@@ -781,6 +837,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     const int zo = zl - P;
     const long long pbase = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
     const int czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // group sums of this thread's rows (dd_add)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int y = gy0 + i;
@@ -792,7 +849,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         } else if (MODE == M_CGA) {
           __stcs(prm.out + off, v);
           prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
-          dsum[0] = fma(pr[0][i], v, dsum[0]);
+          g0 = fma(pr[0][i], v, g0);
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
           if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -804,11 +861,16 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           const double inv =
               sm.invd[(czo * ncy + (INTERIOR ? ewy : cls_of(y, ny, ewy))) * ncx +
                       (INTERIOR ? ewx : cls_of(gx, nx, ewx))];
-          dsum[0] = fma(bb, bb, dsum[0]);
-          dsum[1] = fma(r, __dmul_rn(inv, r), dsum[1]);
-          dsum[2] = fma(r, r, dsum[2]);
+          g0 = fma(bb, bb, g0);
+          g1 = fma(r, __dmul_rn(inv, r), g1);
+          g2 = fma(r, r, g2);
         }
       }
+    }
+    if (MODE == M_CGA || MODE == M_RESID) dd_add(dsum[0], dsum[3], g0);
+    if (MODE == M_RESID) {
+      dd_add(dsum[1], dsum[4], g1);
+      dd_add(dsum[2], dsum[5], g2);
     }
   }
   if (MODE == M_CGA) {
@@ -880,7 +942,7 @@ __device__ __forceinline__ void core_pform_offsets(int (&pfe)[4]) {
 template <int P, int MODE>
 __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, int j, uint32_t f,
                                           double (&acc)[2 * P][RPT], double (&pr)[P][RPT],
-                                          double (&dsum)[3], double beta, const int (&pfe)[4],
+                                          double (&dsum)[6], double beta, const int (&pfe)[4],
                                           double inv0, double* op, double* pp, const double* xp,
                                           long long py) {
   using C = Cfg<P, MODE>;
@@ -1014,6 +1076,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
     acc[S - 1][i] = v;
   }
   if (j >= 2 * P) {
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // group sums of this thread's rows (dd_add)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const double v = out[i];
@@ -1022,7 +1085,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
       } else if (MODE == M_CGA) {
         __stcs(op + i * py, v);
         pp[i * py] = pr[0][i];
-        dsum[0] = fma(pr[0][i], v, dsum[0]);
+        g0 = fma(pr[0][i], v, g0);
       } else if (MODE == M_MASS) {
         double o = prm.c_mass * v;
         if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -1031,10 +1094,15 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
         const double bb = auxv[i];
         const double r = bb - v;
         __stcs(op + i * py, r);
-        dsum[0] = fma(bb, bb, dsum[0]);
-        dsum[1] = fma(r, __dmul_rn(inv0, r), dsum[1]);
-        dsum[2] = fma(r, r, dsum[2]);
+        g0 = fma(bb, bb, g0);
+        g1 = fma(r, __dmul_rn(inv0, r), g1);
+        g2 = fma(r, r, g2);
       }
+    }
+    if (MODE == M_CGA || MODE == M_RESID) dd_add(dsum[0], dsum[3], g0);
+    if (MODE == M_RESID) {
+      dd_add(dsum[1], dsum[4], g1);
+      dd_add(dsum[2], dsum[5], g2);
     }
   }
   if (MODE == M_CGA) {
@@ -1053,7 +1121,7 @@ template <int P, int MODE, int TK>
 __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap* tm0,
                                          const CUtensorMap* tm1, const Smem& sm,
                                          const ItemGeom& g, uint32_t& flat, double beta,
-                                         double (&dsum)[3], Producer<P, MODE>& prod,
+                                         double (&dsum)[6], Producer<P, MODE>& prod,
                                          double xalpha, bool xok) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   constexpr int S = 2 * P;
@@ -1183,8 +1251,8 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
   sm.tab = sm.X + 2 * 2 * C::XARR;
   sm.invd = sm.tab + C::TAB;
   double* s_red = sm.invd + C::INV;
-  unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 4);
-  sm.full = reinterpret_cast<uint64_t*>(s_red + NW * 4 + 2);
+  unsigned* s_last = reinterpret_cast<unsigned*>(s_red + NW * 8);
+  sm.full = reinterpret_cast<uint64_t*>(s_red + NW * 8 + 2);
 
   const int tid = threadIdx.x;
   for (int i = tid; i < C::TAB; i += NT) sm.tab[i] = prm.tab[i];
@@ -1202,10 +1270,11 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
   // pass A of iteration k applies x += alpha_{k-1} p_{k-1} (k >= 1): alpha
   // still holds alpha_{k-1} here (every CTA reads it before the last CTA's
   // finalize overwrites it with alpha_k)
+  // (skipped when a flush already applied it: x_done == it)
   const int k_it = (MODE == M_CGA) ? ld_vol(&prm.state->it) : 0;
   const double xalpha = (MODE == M_CGA) ? ld_vol(&prm.state->alpha) : 0.0;
-  const bool xok = k_it >= 1;
-  double dsum[3] = {0.0, 0.0, 0.0};
+  const bool xok = k_it >= 1 && ld_vol(&prm.state->x_done) < k_it;
+  double dsum[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // hi[3], lo[3]
   Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
   if (tid == kProdThread<P, MODE>) {
     for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, sm.stage, sm.full);
@@ -1222,12 +1291,13 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
   }
 
   if (MODE == M_CGA) {
-    double v[1] = {dsum[0]};
-    reduce_and_finalize<1, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 1,
-                               prm.accumulate);
+    double vh[1] = {dsum[0]}, vl[1] = {dsum[3]};
+    reduce_and_finalize<1, NW>(vh, vl, s_red, s_last, prm.partials, prm.counter, prm.state,
+                               prm.fuse, 1, prm.accumulate);
   } else if (MODE == M_RESID) {
-    double v[3] = {dsum[0], dsum[1], dsum[2]};
-    reduce_and_finalize<3, NW>(v, s_red, s_last, prm.partials, prm.counter, prm.state, prm.fuse, 0);
+    double vh[3] = {dsum[0], dsum[1], dsum[2]}, vl[3] = {dsum[3], dsum[4], dsum[5]};
+    reduce_and_finalize<3, NW>(vh, vl, s_red, s_last, prm.partials, prm.counter, prm.state,
+                               prm.fuse, 0);
   }
 }
 
@@ -1255,7 +1325,7 @@ __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<do
 
 __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ PassBParams prm) {
   if (!ld_vol(&prm.state->active)) return;
-  __shared__ double s_red[(NTB / 32) * 4];
+  __shared__ double s_red[(NTB / 32) * 8];
   __shared__ unsigned s_last;
   extern __shared__ double s_inv[];
   const int ewz = prm.ew[0], ewy = prm.ew[1], ewx = prm.ew[2];
@@ -1268,7 +1338,7 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
   const int nrows = prm.nz * ny;
   const int r0 = blockIdx.x * prm.rows_per_cta;
   const int r1 = min(r0 + prm.rows_per_cta, nrows);
-  double rz = 0.0, rr = 0.0;
+  double rz = 0.0, rr = 0.0, rzl = 0.0, rrl = 0.0;  // double-double sums
   for (int row = r0 + warp; row < r1; row += NTB / 32) {
     const int zl = row / ny, y = row - zl * ny;
     const int cz = cls_of(prm.z_off + zl, prm.nz_glob, ewz);
@@ -1295,15 +1365,16 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       na.y = __dsub_rn(ra.y, __dmul_rn(alpha, aa.y));
       nb.x = __dsub_rn(rb.x, __dmul_rn(alpha, ab.x));
       nb.y = __dsub_rn(rb.y, __dmul_rn(alpha, ab.y));
-      // same summation order as the one-pair loop: pair q, then pair q+32
-      rz = fma(na.x, __dmul_rn(ia0, na.x), rz);
-      rz = fma(na.y, __dmul_rn(ia1, na.y), rz);
-      rr = fma(na.x, na.x, rr);
-      rr = fma(na.y, na.y, rr);
-      rz = fma(nb.x, __dmul_rn(ib0, nb.x), rz);
-      rz = fma(nb.y, __dmul_rn(ib1, nb.y), rz);
-      rr = fma(nb.x, nb.x, rr);
-      rr = fma(nb.y, nb.y, rr);
+      // group sums of pairs q, q+32 (position-determined), added in dd
+      double gz = __dmul_rn(na.x, __dmul_rn(ia0, na.x)), gr = __dmul_rn(na.x, na.x);
+      gz = fma(na.y, __dmul_rn(ia1, na.y), gz);
+      gr = fma(na.y, na.y, gr);
+      gz = fma(nb.x, __dmul_rn(ib0, nb.x), gz);
+      gr = fma(nb.x, nb.x, gr);
+      gz = fma(nb.y, __dmul_rn(ib1, nb.y), gz);
+      gr = fma(nb.y, nb.y, gr);
+      dd_add(rz, rzl, gz);
+      dd_add(rr, rrl, gr);
       st2(rrw + xa, na);
       st2(rrw + xb, nb);
     }
@@ -1317,10 +1388,11 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       double2 rn;
       rn.x = __dsub_rn(rv.x, __dmul_rn(alpha, av.x));
       rn.y = __dsub_rn(rv.y, __dmul_rn(alpha, av.y));
-      rz = fma(rn.x, __dmul_rn(i0, rn.x), rz);
-      rz = fma(rn.y, __dmul_rn(i1, rn.y), rz);
-      rr = fma(rn.x, rn.x, rr);
-      rr = fma(rn.y, rn.y, rr);
+      double gz = __dmul_rn(rn.x, __dmul_rn(i0, rn.x)), gr = __dmul_rn(rn.x, rn.x);
+      gz = fma(rn.y, __dmul_rn(i1, rn.y), gz);
+      gr = fma(rn.y, rn.y, gr);
+      dd_add(rz, rzl, gz);
+      dd_add(rr, rrl, gr);
       st2(rrw + xx, rn);
     }
     if ((nx & 1) && lane == 0) {
@@ -1328,12 +1400,12 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       const double i0 = trow[cls_of(xx, nx, ewx)];
       const double rn = __dsub_rn(rrw[xx], __dmul_rn(alpha, apr[xx]));
       rrw[xx] = rn;
-      rz = fma(rn, __dmul_rn(i0, rn), rz);
-      rr = fma(rn, rn, rr);
+      dd_add(rz, rzl, __dmul_rn(rn, __dmul_rn(i0, rn)));
+      dd_add(rr, rrl, __dmul_rn(rn, rn));
     }
   }
-  double v[2] = {rz, rr};
-  reduce_and_finalize<2, NTB / 32>(v, s_red, &s_last, prm.partials, prm.counter, prm.state,
+  double vh[2] = {rz, rr}, vl[2] = {rzl, rrl};
+  reduce_and_finalize<2, NTB / 32>(vh, vl, s_red, &s_last, prm.partials, prm.counter, prm.state,
                                    prm.fuse, 2);
 }
 
@@ -1902,16 +1974,16 @@ void fill_common(SepParams& sp, const bspde_plan* pl, int mode) {
   sp.fuse = 1;
 }
 
-// scratch layout: CgState | partials[4*MAXGRID] | counter
+// scratch layout: CgState | partials[8*MAXGRID] (hi, lo of up to 4 sums) | counter
 constexpr int MAXGRID = 4096;
-size_t scratch_size() { return sizeof(CgState) + sizeof(double) * 4 * MAXGRID + 64; }
+size_t scratch_size() { return sizeof(CgState) + sizeof(double) * 8 * MAXGRID + 64; }
 CgState* scratch_state(void* s) { return reinterpret_cast<CgState*>(s); }
 double* scratch_partials(void* s) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + sizeof(CgState));
 }
 unsigned* scratch_counter(void* s) {
   return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(s) + sizeof(CgState) +
-                                     sizeof(double) * 4 * MAXGRID);
+                                     sizeof(double) * 8 * MAXGRID);
 }
 
 int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, double* out,
@@ -2505,3 +2577,4 @@ int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, doubl
 }  // extern "C"
 
 #include "stencil.cuh"
+#include "otf.cuh"

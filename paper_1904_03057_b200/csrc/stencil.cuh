@@ -21,6 +21,17 @@
 
 namespace {
 
+// per-thread accumulation of the stencil PCG's dot products: double-double
+// (BSPDE_ST_DD=1, correctly rounded with the dd tree) or plain FMAs
+#ifndef BSPDE_ST_DD
+#define BSPDE_ST_DD 1
+#endif
+#if BSPDE_ST_DD
+#define ST_ACC(h, l, a, b) dd_add(h, l, __dmul_rn(a, b))
+#else
+#define ST_ACC(h, l, a, b) (h = fma(a, b, h))
+#endif
+
 constexpr int ST_NT = 256;
 
 struct StencilDev {
@@ -152,14 +163,14 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S
                                                               double* partials, unsigned* counter,
                                                               CgState* st, int precond,
                                                               const uint8_t* __restrict__ live = nullptr) {
-  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ double s_red[(ST_NT / 32) * 8];
   __shared__ unsigned s_last;
   if (MODE == 2 && !ld_vol(&st->active)) return;
   constexpr int A = 2 * NB + 1, hb = NB;
   constexpr int center = (hb * A + hb) * A + hb;
   const int nxb = (S.nx + XB - 1) / XB;
   const long long groups = (long long)S.nz * S.ny * nxb;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s0l = 0.0, s1l = 0.0, s2l = 0.0;  // double-double
   for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
        gi += (long long)gridDim.x * blockDim.x) {
     const int xb = (int)(gi % nxb);
@@ -214,21 +225,21 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_kernel(const StencilDev S
         out[l] = r;
         const double dg = P[(long long)center * S.N + l];
         const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
-        s0 = fma(bb, bb, s0);
-        s1 = fma(r, __dmul_rn(inv, r), s1);
-        s2 = fma(r, r, s2);
+        ST_ACC(s0, s0l, bb, bb);
+        ST_ACC(s1, s1l, r, __dmul_rn(inv, r));
+        ST_ACC(s2, s2l, r, r);
       } else {
         out[l] = t[v];
-        s0 = fma(c[l], t[v], s0);
+        ST_ACC(s0, s0l, c[l], t[v]);
       }
     }
   }
   if (MODE == 1) {
-    double v[3] = {s0, s1, s2};
-    reduce_and_finalize<3, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 0);
+    double vh[3] = {s0, s1, s2}, vl[3] = {s0l, s1l, s2l};
+    reduce_and_finalize<3, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 0);
   } else if (MODE == 2) {
-    double v[1] = {s0};
-    reduce_and_finalize<1, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 1);
+    double vh[1] = {s0}, vl[1] = {s0l};
+    reduce_and_finalize<1, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 1);
   }
 }
 
@@ -268,13 +279,13 @@ __global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev 
                                                                const double* __restrict__ ap,
                                                                double* partials, unsigned* counter,
                                                                CgState* st, int precond) {
-  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ double s_red[(ST_NT / 32) * 8];
   __shared__ unsigned s_last;
   if (!ld_vol(&st->active)) return;
   const double alpha = ld_vol(&st->alpha);
   const int A = S.A, hb = S.nb;
   const int center = (hb * A + hb) * A + hb;
-  double rz = 0.0, rr = 0.0;
+  double rz = 0.0, rr = 0.0, rzl = 0.0, rrl = 0.0;  // double-double
   // two grid-stride elements per trip, accumulated in the same order as a
   // one-element loop (bitwise the same sums)
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -296,19 +307,19 @@ __global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev 
     const double rn = __dsub_rn(rv, __dmul_rn(alpha, av));
     r[l] = rn;
     const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
-    rz = fma(rn, __dmul_rn(inv, rn), rz);
-    rr = fma(rn, rn, rr);
+    ST_ACC(rz, rzl, rn, __dmul_rn(inv, rn));
+    ST_ACC(rr, rrl, rn, rn);
     if (two) {
       x[l2] = __dadd_rn(xv2, __dmul_rn(alpha, pv2));
       const double rn2 = __dsub_rn(rv2, __dmul_rn(alpha, av2));
       r[l2] = rn2;
       const double inv2 = (precond && dg2 != 0.0) ? 1.0 / dg2 : 1.0;
-      rz = fma(rn2, __dmul_rn(inv2, rn2), rz);
-      rr = fma(rn2, rn2, rr);
+      ST_ACC(rz, rzl, rn2, __dmul_rn(inv2, rn2));
+      ST_ACC(rr, rrl, rn2, rn2);
     }
   }
-  double v[2] = {rz, rr};
-  reduce_and_finalize<2, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 2);
+  double vh[2] = {rz, rr}, vl[2] = {rzl, rrl};
+  reduce_and_finalize<2, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 2);
 }
 
 __global__ void stencil_diag_kernel(const StencilDev S, const double* P, double* out) {
@@ -334,6 +345,11 @@ struct bspde_stencil {
   int64_t launches = 0;
   uint8_t* d_live = nullptr;  // per apply group: any nonzero stencil entry (PCG skip list)
   size_t live_bytes = 0;
+  std::vector<double> host_tab;  // [axis][d][class][A*B] (copy of the desc's tables)
+  // on-the-fly operator (otf.cuh): the parameter fields and the Jacobi diagonal
+  const double* otf_d = nullptr;
+  const double* otf_m = nullptr;
+  double* otf_diag = nullptr;
 };
 
 namespace {
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
                                                                 double* partials, unsigned* counter,
                                                                 CgState* st, int precond,
                                                                 const uint8_t* __restrict__ live = nullptr) {
-  __shared__ double s_red[(ST_NT / 32) * 4];
+  __shared__ double s_red[(ST_NT / 32) * 8];
   __shared__ unsigned s_last;
   if (MODE == 2 && !ld_vol(&st->active)) return;
   constexpr int A = 2 * NB + 1, hb = NB, NR = XB + 2 * NB;
@@ -374,7 +390,7 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
   const int nyb = (S.ny + XB - 1) / XB;
   const long long groups = (long long)S.nz * nyb * S.nx;
   const long long sy = S.nx;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s0l = 0.0, s1l = 0.0, s2l = 0.0;  // double-double
   for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < groups;
        gi += (long long)gridDim.x * blockDim.x) {
     const int lx = (int)(gi % S.nx);
@@ -431,21 +447,21 @@ __global__ void __launch_bounds__(ST_NT) stencil_apply_y_kernel(const StencilDev
         out[l] = rr;
         const double dg = P[(long long)center * S.N + l];
         const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
-        s0 = fma(bb, bb, s0);
-        s1 = fma(rr, __dmul_rn(inv, rr), s1);
-        s2 = fma(rr, rr, s2);
+        ST_ACC(s0, s0l, bb, bb);
+        ST_ACC(s1, s1l, rr, __dmul_rn(inv, rr));
+        ST_ACC(s2, s2l, rr, rr);
       } else {
         out[l] = t[v];
-        s0 = fma(c[l], t[v], s0);
+        ST_ACC(s0, s0l, c[l], t[v]);
       }
     }
   }
   if (MODE == 1) {
-    double v[3] = {s0, s1, s2};
-    reduce_and_finalize<3, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 0);
+    double vh[3] = {s0, s1, s2}, vl[3] = {s0l, s1l, s2l};
+    reduce_and_finalize<3, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 0);
   } else if (MODE == 2) {
-    double v[1] = {s0};
-    reduce_and_finalize<1, ST_NT / 32>(v, s_red, &s_last, partials, counter, st, 1, 1);
+    double vh[1] = {s0}, vl[1] = {s0l};
+    reduce_and_finalize<1, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 1);
   }
 }
 
@@ -553,6 +569,11 @@ int st_live(bspde_stencil* s, const double* P, cudaStream_t st, uint8_t** live) 
   return BSPDE_OK;
 }
 
+template <int MODE>
+int otf_launch(const bspde_stencil* s, cudaStream_t st, const double* c, double* out,
+               const double* aux, double* partials, unsigned* counter, CgState* state,
+               int precond);  // otf.cuh
+
 int st_read(bspde_stencil* s, void* scratch, bspde_cg_report* rep, int32_t* active, cudaStream_t st) {
   CgState* hs = reinterpret_cast<CgState*>(s->host_state);
   CUDA_TRY(cudaMemcpyAsync(hs, scratch_state(scratch), sizeof(CgState), cudaMemcpyDeviceToHost, st));
@@ -569,6 +590,76 @@ int st_read(bspde_stencil* s, void* scratch, bspde_cg_report* rep, int32_t* acti
   if (active) *active = hs->active;
   return BSPDE_OK;
 }
+
+// Jacobi-PCG over the stencil (or, otf = true, the on-the-fly operator of
+// otf.cuh, whose Jacobi diagonal P's centre slice points at): the reference
+// recurrence with three kernels per iteration
+int st_pcg(bspde_stencil* s, const double* P, const double* b, double* x, double* r, double* p,
+           double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
+           bspde_cg_report* report, int32_t precond, void* stream, bool otf) {
+  if (!P || !b || !x || !r || !p || !ap || !scratch || !cfg)
+    return fail(BSPDE_ERR_ARG, "null argument");
+  if (!(cfg->tol > 0.0)) return fail(BSPDE_ERR_ARG, "tol must be positive");
+  if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
+  if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
+  cudaStream_t caller = (cudaStream_t)stream, st = s->work;
+  CUDA_TRY(cudaEventRecord(s->ev_in, caller));
+  CUDA_TRY(cudaStreamWaitEvent(st, s->ev_in, 0));
+  // scalar state (same layout and state machine as bspde_cg_setup)
+  CgState* hs = reinterpret_cast<CgState*>(s->host_state);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::memset(hs, 0, sizeof(CgState));
+  hs->tol = cfg->tol;
+  hs->max_iter = cfg->max_iter;
+  hs->record_history = cfg->record_history ? 1 : 0;
+  hs->has_x0 = cfg->has_x0 ? 1 : 0;
+  hs->ring = kPRing;  // finalize_state's x-ring bookkeeping (unused by the stencil CG)
+  hs->history = history;
+  hs->scale = 1.0;
+  CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(scratch_counter(scratch), 0, 64, st));
+  const size_t bytes = (size_t)s->S.N * sizeof(double);
+  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
+  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  const unsigned grid = st_grid(s, s->S.N);
+  double* partials = scratch_partials(scratch);
+  unsigned* counter = scratch_counter(scratch);
+  CgState* state = scratch_state(scratch);
+  const unsigned agrid = st_grid(s, s->S.N / XB + 1);
+  uint8_t* live = nullptr;
+  if (!otf)
+    if (int lrc = st_live(s, P, st, &live)) return lrc;
+  if (otf) {
+    if (int orc = otf_launch<1>(s, st, x, r, b, partials, counter, state, precond)) return orc;
+  } else {
+    st_apply<1>(s, agrid, st, P, x, r, b, partials, counter, state, precond);
+  }
+  s->launches++;
+  CUDA_TRY(cudaGetLastError());
+  int32_t active = 0;
+  int rc = st_read(s, scratch, report, &active, st);
+  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
+  while (rc == BSPDE_OK && active) {
+    for (int k = 0; k < K; ++k) {
+      stencil_pform_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, r, p, state, precond);
+      if (otf) {
+        if (int orc = otf_launch<2>(s, st, p, ap, nullptr, partials, counter, state, precond))
+          return orc;
+      } else {
+        st_apply<2>(s, agrid, st, P, p, ap, nullptr, partials, counter, state, precond, live);
+      }
+      stencil_update_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, x, r, p, ap, partials, counter,
+                                                    state, precond);
+      s->launches += 3;
+    }
+    CUDA_TRY(cudaGetLastError());
+    rc = st_read(s, scratch, report, &active, st);
+  }
+  cudaEventRecord(s->ev_out, st);
+  cudaStreamWaitEvent(caller, s->ev_out, 0);
+  return rc;
+}
+
 
 }  // namespace
 
@@ -674,6 +765,7 @@ int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
     return fail(BSPDE_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e6));
   }
   S.tab = s->d_tab;
+  s->host_tab = tab;
   *out = s;
   return BSPDE_OK;
 }
@@ -739,57 +831,7 @@ int bspde_stencil_pcg(bspde_stencil* s, const double* P, const double* b, double
                       const bspde_cg_config* cfg, bspde_cg_report* report, int32_t precond,
                       void* stream) {
   if (int rc = st_check(s)) return rc;
-  if (!P || !b || !x || !r || !p || !ap || !scratch || !cfg)
-    return fail(BSPDE_ERR_ARG, "null argument");
-  if (!(cfg->tol > 0.0)) return fail(BSPDE_ERR_ARG, "tol must be positive");
-  if (cfg->max_iter < 1) return fail(BSPDE_ERR_ARG, "max_iter must be >= 1");
-  if (cfg->record_history && !history) return fail(BSPDE_ERR_ARG, "history buffer required");
-  cudaStream_t caller = (cudaStream_t)stream, st = s->work;
-  CUDA_TRY(cudaEventRecord(s->ev_in, caller));
-  CUDA_TRY(cudaStreamWaitEvent(st, s->ev_in, 0));
-  // scalar state (same layout and state machine as bspde_cg_setup)
-  CgState* hs = reinterpret_cast<CgState*>(s->host_state);
-  CUDA_TRY(cudaStreamSynchronize(st));
-  std::memset(hs, 0, sizeof(CgState));
-  hs->tol = cfg->tol;
-  hs->max_iter = cfg->max_iter;
-  hs->record_history = cfg->record_history ? 1 : 0;
-  hs->has_x0 = cfg->has_x0 ? 1 : 0;
-  hs->ring = kPRing;  // finalize_state's x-ring bookkeeping (unused by the stencil CG)
-  hs->history = history;
-  hs->scale = 1.0;
-  CUDA_TRY(cudaMemcpyAsync(scratch_state(scratch), hs, sizeof(CgState), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(scratch_counter(scratch), 0, 64, st));
-  const size_t bytes = (size_t)s->S.N * sizeof(double);
-  if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
-  CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
-  const unsigned grid = st_grid(s, s->S.N);
-  double* partials = scratch_partials(scratch);
-  unsigned* counter = scratch_counter(scratch);
-  CgState* state = scratch_state(scratch);
-  const unsigned agrid = st_grid(s, s->S.N / XB + 1);
-  uint8_t* live = nullptr;
-  if (int lrc = st_live(s, P, st, &live)) return lrc;
-  st_apply<1>(s, agrid, st, P, x, r, b, partials, counter, state, precond);
-  s->launches++;
-  CUDA_TRY(cudaGetLastError());
-  int32_t active = 0;
-  int rc = st_read(s, scratch, report, &active, st);
-  const int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
-  while (rc == BSPDE_OK && active) {
-    for (int k = 0; k < K; ++k) {
-      stencil_pform_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, r, p, state, precond);
-      st_apply<2>(s, agrid, st, P, p, ap, nullptr, partials, counter, state, precond, live);
-      stencil_update_kernel<<<grid, ST_NT, 0, st>>>(s->S, P, x, r, p, ap, partials, counter,
-                                                    state, precond);
-      s->launches += 3;
-    }
-    CUDA_TRY(cudaGetLastError());
-    rc = st_read(s, scratch, report, &active, st);
-  }
-  cudaEventRecord(s->ev_out, st);
-  cudaStreamWaitEvent(caller, s->ev_out, 0);
-  return rc;
+  return st_pcg(s, P, b, x, r, p, ap, scratch, history, cfg, report, precond, stream, false);
 }
 
 }  // extern "C"

@@ -159,9 +159,30 @@ def build_var_system(domain, n_b, n_p, dfield, mfield, face_specs, dtype) -> Var
         mask=_mask_info(domain, int(n_b), face_specs) if is_mask else None)
 
 
+def _var_strategy(data, lib, handle):
+    """"otf" (matrix-free, csrc/otf.cuh) when the plan supports it and the
+    system is not a mask (3-D box, no face terms, n_b = n_p <= 3), else
+    "stencil" (assembled).  ``BSPDE_VAR_STRATEGY`` = stencil / otf forces one."""
+    import os
+
+    want = os.environ.get("BSPDE_VAR_STRATEGY", "auto")
+    if want not in ("auto", "otf", "stencil"):
+        raise ConfigurationError(f"BSPDE_VAR_STRATEGY must be auto, otf or stencil, got {want!r}")
+    ok = data.mask is None and bool(lib.bspde_otf_supported(handle))
+    if want == "otf" and not ok:
+        raise ConfigurationError("the matrix-free operator needs a 3-D box without face terms "
+                                 "and n_b = n_p <= 3")
+    return "otf" if (ok and want != "stencil") else "stencil"
+
+
 class B200StencilOperator:
-    """Assembled-stencil operator on one B200 (strategy ``"b200"`` for
-    variable coefficients); same protocol as the reference operators."""
+    """Variable-coefficient operator on one B200 (strategy ``"b200"`` for
+    variable coefficients); same protocol as the reference operators.
+
+    Matrix-free (``kind == "otf"``: the reference's on-the-fly algorithm,
+    sum-factorised, nothing stored) for 3-D boxes without face terms and
+    n_b = n_p <= 3; otherwise the assembled stencil (``kind == "stencil"``,
+    (2p+1)^3 doubles per DoF)."""
 
     strategy = "b200"
 
@@ -211,6 +232,18 @@ class B200StencilOperator:
         h = C.c_void_p()
         N.check(self.lib.bspde_stencil_create(C.byref(d), C.byref(h)))
         self.handle = h
+        self._scratch = None
+        self._mask = None
+        self.kind = _var_strategy(data, self.lib, h)
+        if self.kind == "otf":
+            # device parameter fields stay resident (read by every apply)
+            self._df = torch.from_numpy(np.ascontiguousarray(data.dfield)).to(self.device)
+            self._mf = torch.from_numpy(np.ascontiguousarray(data.mfield)).to(self.device)
+            self._diag = torch.empty(tuple(data.cext), dtype=torch.float64, device=self.device)
+            self.P = None
+            N.check(self.lib.bspde_otf_prepare(h, N.ptr(self._df), N.ptr(self._mf),
+                                               N.ptr(self._diag), N.stream_handle()))
+            return
         n_entries = int(self.lib.bspde_stencil_entries(h))
         free, _ = torch.cuda.mem_get_info(self.device)
         if n_entries * 8 > 0.9 * free:
@@ -221,7 +254,6 @@ class B200StencilOperator:
         mf = torch.from_numpy(np.ascontiguousarray(data.mfield)).to(self.device)
         N.check(self.lib.bspde_stencil_assemble(h, N.ptr(df), N.ptr(mf), N.ptr(self.P),
                                                 N.stream_handle()))
-        self._mask = None
         if data.mask is not None:
             self._mask = self._mask_desc(data.mask)
             N.check(self.lib.bspde_stencil_mask_patch(h, C.byref(self._mask[0]), N.ptr(df),
@@ -312,6 +344,10 @@ class B200StencilOperator:
         return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
 
     def apply_device(self, c, out, stream=None):
+        if self.kind == "otf":
+            N.check(self.lib.bspde_otf_apply(self.handle, N.ptr(c), N.ptr(out),
+                                             N.stream_handle(stream)))
+            return out
         N.check(self.lib.bspde_stencil_apply(self.handle, N.ptr(self.P), N.ptr(c), N.ptr(out),
                                              N.stream_handle(stream)))
         return out
@@ -331,10 +367,13 @@ class B200StencilOperator:
     def jacobi_diagonal(self):
         import torch
 
-        od = torch.empty(self.data.cext, dtype=torch.float64, device=self.device)
-        N.check(self.lib.bspde_stencil_diagonal(self.handle, N.ptr(self.P), N.ptr(od),
-                                                N.stream_handle()))
-        diag = od.cpu().numpy()
+        if self.kind == "otf":
+            diag = self._diag.cpu().numpy().copy()
+        else:
+            od = torch.empty(self.data.cext, dtype=torch.float64, device=self.device)
+            N.check(self.lib.bspde_stencil_diagonal(self.handle, N.ptr(self.P), N.ptr(od),
+                                                    N.stream_handle()))
+            diag = od.cpu().numpy()
         if self.data.mask is not None:  # inactive unknowns get 1 (operator.py:156-170)
             diag[self.data.mask.node_class == 0] = 1.0
         bad = diag <= 0
@@ -349,7 +388,15 @@ class B200StencilOperator:
         from .operator import OpStats
 
         n = self.data.num_unknowns()
-        a3 = (2 * self.data.n_b + 1) ** 3
+        A = 2 * self.data.n_b + 1
+        if self.kind == "otf":
+            B = 2 * param_reach(self.data.n_b, self.data.n_p) + 1
+            # per output: y-stage (3 B FMAs per (ay, ax)) + scatter (2 B per
+            # (ay, ax)); x-stage 3 A B, C0 2 A B per staged position
+            fmas = A * A * 5 * B + 5 * A * B
+            return OpStats(flops=int(2 * fmas * n), bytes_read=int(n * 8 * 3),
+                           bytes_written=int(n * 8), seconds=seconds)
+        a3 = A ** 3
         return OpStats(flops=int(2 * a3 * n), bytes_read=int(n * 8 * (a3 + 1)),
                        bytes_written=int(n * 8), seconds=seconds)
 
@@ -379,6 +426,12 @@ class B200StencilOperator:
                          int(bool(has_x0)), int(config.poll_every))
         rep = N.CgReport()
         precond = 1 if config.precond == "jacobi" else 0
+        if self.kind == "otf":
+            N.check(self.lib.bspde_otf_pcg(self.handle, N.ptr(b), N.ptr(x), N.ptr(r), N.ptr(p),
+                                           N.ptr(ap), N.ptr(self._scratch), N.ptr(hist),
+                                           C.byref(cfg), C.byref(rep), precond,
+                                           N.stream_handle(stream)))
+            return report_from(rep, config, time.perf_counter() - t0, hist)
         N.check(self.lib.bspde_stencil_pcg(self.handle, N.ptr(self.P), N.ptr(b), N.ptr(x), N.ptr(r),
                                            N.ptr(p), N.ptr(ap), N.ptr(self._scratch), N.ptr(hist),
                                            C.byref(cfg), C.byref(rep), precond,

@@ -76,7 +76,12 @@ def test_solve_problem_with_coarse_init(tag):
     its_ref, its_ref0 = (int(v) for v in GOLD[f"{tag}_its"])
     sol = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000, coarse_init_factor=factor))
     assert sol.report.converged
-    assert abs(sol.report.iterations - its_ref) <= max(1, its_ref // 100)
+    # c2d (penalty weight 1e3 on every face) stops in a residual plateau: the
+    # reference itself takes 94 or 96 iterations when its dot products are
+    # perturbed by one rounding unit (5 of 6 seeds give 96;
+    # tools/count_sensitivity.py c2d), so its bar is +-2
+    bar = 2 if tag == "c2d" else max(1, its_ref // 100)
+    assert abs(sol.report.iterations - its_ref) <= bar
     assert rel(sol.coeffs, GOLD[f"{tag}_coeffs"]) <= 1e-6
     assert rel(sol.samples, GOLD[f"{tag}_samples"]) <= 1e-6
     sol0 = solve_problem(spec, SolveConfig(tol=1e-9, max_iter=4000))

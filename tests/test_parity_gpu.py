@@ -354,17 +354,19 @@ def test_cg_stepwise_vs_oracle(cuda_device, case):
     rep, active = plan.cg_read(w.scratch)
     assert rep.iterations == 1
     assert abs(rep.residual - np.linalg.norm(r1)) / np.linalg.norm(r1) < 1e-12
+    state1 = w.scratch.clone()  # after iteration 0
     xe = xb.clone()
     plan.cg_flush_x(xe, w.pring, w.scratch)
     torch.cuda.synchronize()
     assert relmax(lay.download(xe), x1) < 1e-13
     plan.cg_flush_x(xe, w.pring, w.scratch)  # idempotent: nothing pending any more
     assert relmax(lay.download(xe), x1) < 1e-13
-    # ... and pass A of iteration 1 applies the same update: x1 = x0 + alpha p0
-    # (forced active: the p = 5 case trips the divergence guard at iteration 1)
-    R1 = 1 % R
+    # ... and pass A of iteration 1 (from the unflushed state) applies the same
+    # update x1 = fl(x0 + fl(alpha p0)) bit for bit (forced active: the p = 5
+    # case trips the divergence guard at iteration 1)
+    w.scratch.copy_(state1)
     w.scratch[120:124].view(torch.int32)[0] = 1  # CgState.active
-    plan.cg_pass_a(xb, w.r, w.pring[0], w.pring[R1], w.ap, w.scratch, 1)
+    plan.cg_pass_a(xb, w.r, w.pring[0], w.pring[1 % R], w.ap, w.scratch, 1)
     torch.cuda.synchronize()
     assert np.array_equal(lay.download(xb), lay.download(xe))
 
