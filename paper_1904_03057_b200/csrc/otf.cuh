@@ -39,7 +39,11 @@
 
 namespace {
 
-constexpr int OTF_TX = 32, OTF_TY = 8, OTF_RPT = 2, OTF_NT = 128;
+#ifndef BSPDE_OTF_RPT
+#define BSPDE_OTF_RPT 1
+#endif
+// a CTA: 32 x 8 outputs per plane; each thread RPT rows of one column
+constexpr int OTF_TX = 32, OTF_TY = 8, OTF_RPT = BSPDE_OTF_RPT, OTF_NT = 32 * OTF_TY / OTF_RPT;
 constexpr int OTF_MAXNB = 3;
 
 template <int NB>

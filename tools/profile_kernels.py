@@ -26,7 +26,7 @@ op.mass_apply_device(u, b, F, a=dt)
 plan = op.plan()
 w = _work(op, 10)
 PP, K = w.pring, [0]
-    RR = PP.shape[0]
+RR = PP.shape[0]
 plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
 plan.cg_residual(b, u, w.r, w.scratch, 1)
 for _ in range(iters):

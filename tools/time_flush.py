@@ -15,9 +15,9 @@ u = lay.alloc(dev); b = lay.alloc(dev)
 gaussian_coeffs(N, h, 3, device=dev, out=u, layout=lay, **IC)
 op.mass_apply_device(u, b)
 plan = op.plan(); w = _work(op, 10); PP, K = w.pring, [0]
-    RR = PP.shape[0]
+RR = PP.shape[0]
 PP, K = w.pring, [0]
-    RR = PP.shape[0]
+RR = PP.shape[0]
 ts = []
 for rep in range(4):
     plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True)
