@@ -145,6 +145,22 @@ int bspde_pcg_solve(bspde_plan* plan, const double* b, double* x, double* r,
                     const bspde_cg_config* cfg, bspde_cg_report* report,
                     void* stream);
 
+/* One implicit-Euler heat step: solves (M + dt K) u_new = cm M u + a f with
+ * x0 = u (Jacobi-PCG as bspde_pcg_solve), u updated in place.  The right-hand
+ * side is never formed: the first residual r0 = (cm M u + a f) - A u and its
+ * sums come from one fused kernel (the mass apply rides along as a second
+ * z ring; b = cm M u + a f is rounded as bspde_mass_apply rounds it).
+ * f may be NULL (no source).  cfg->has_x0 must be 1.  Replaces the
+ * composition b = M.apply(u) + dt F; pcg(A, b, cfg, x0 = u) of the heat
+ * oracle (solver.py:51-117). */
+int bspde_heat_step(bspde_plan* plan, double* u, const double* f, double cm, double a,
+                    double* r, double* p_ring, double* ap, void* scratch, double* history,
+                    const bspde_cg_config* cfg, bspde_cg_report* report, void* stream);
+/* The fused first residual alone (step-wise / tests): r = (cm M u + a f) - A u,
+ * sums = {<b,b>, <r,D^-1 r>, <r,r>} of that b (kind 0). */
+int bspde_heat_residual(bspde_plan* plan, const double* u, const double* f, double cm,
+                        double a, double* r, void* scratch, int fuse, void* stream);
+
 /* ---- step-wise CG for the multi-GPU driver (z-slabs, one rank per GPU).
  * fuse = 1: the kernel's last CTA reduces the per-CTA partials and runs the
  * scalar update (single device).  fuse = 0: it only writes the local sums

@@ -128,6 +128,10 @@ SIGNATURES = [
     ("bspde_jacobi_diagonal", C.c_int, [_VP, _dptr, _VP, _VP]),
     ("bspde_pcg_solve", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                   C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
+    ("bspde_heat_step", C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP, _VP, _VP,
+                                  _VP, C.POINTER(CgConfig), C.POINTER(CgReport), _VP]),
+    ("bspde_heat_residual", C.c_int, [_VP, _VP, _VP, C.c_double, C.c_double, _VP, _VP, C.c_int,
+                                      _VP]),
     ("bspde_cg_setup", C.c_int, [_VP, _VP, _VP, C.POINTER(CgConfig), _VP]),
     ("bspde_cg_residual", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),
     ("bspde_cg_pass_a", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _VP]),

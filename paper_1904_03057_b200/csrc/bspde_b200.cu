@@ -68,7 +68,9 @@ constexpr int MAXTAP = 2 * MAXP + 1;
 #define BSPDE_W_CGA3 12
 #endif
 __host__ __device__ constexpr int warps_of(int p, int mode) {
-  return p <= 3 ? ((p == 3 && mode == 3 /* M_CGA */) ? BSPDE_W_CGA3 : BSPDE_W_LOWP) : 12;
+  return p <= 3 ? ((p == 3 && (mode == 3 /* M_CGA */ || mode == 4 /* M_HRES */)) ? BSPDE_W_CGA3
+                                                                                 : BSPDE_W_LOWP)
+                : 12;
 }
 __host__ __device__ constexpr int tile_h_of(int p, int mode) { return RPT * warps_of(p, mode) / 2; }
 
@@ -79,7 +81,10 @@ struct Geo {
   static constexpr int TY = tile_h_of(P, MODE);  // tile height (y)
 };
 
-enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3 };
+// M_HRES: the heat step's first residual fused with its right-hand side,
+// r0 = (rhs_cm (Mz(x)My(x)Mx) u + a F) - A u with the three initial sums,
+// b never stored (a second z ring carries the pure mass apply)
+enum Mode { M_APPLY = 0, M_MASS = 1, M_RESID = 2, M_CGA = 3, M_HRES = 4 };
 
 __host__ __device__ constexpr int edge_width_of(int p) {
   return p == 1 ? 1 : (p <= 3 ? 3 : 5);
@@ -100,7 +105,7 @@ struct Cfg {
   static constexpr int NA = (MODE == M_CGA) ? 2 : 1;   // staged arrays per plane
   static constexpr int NS = (MODE == M_CGA) ? 3 : 4;  // TMA stages (fits 227 KB for p = 1..5)
   static constexpr bool STIFF = (MODE != M_MASS);
-  static constexpr bool INVD = (MODE == M_CGA || MODE == M_RESID);
+  static constexpr bool INVD = (MODE == M_CGA || MODE == M_RESID || MODE == M_HRES);
   static constexpr int ARR = HX * HY;                        // doubles
   static constexpr int ARR_D = ((ARR * 8 + 127) / 128) * 16; // doubles, 128B-rounded
   static constexpr int XARR = HY * TX;                       // doubles per X array
@@ -143,6 +148,7 @@ struct SepParams {
   double* out;
   const double* aux;
   double aux_scale;
+  double rhs_cm;       // M_HRES: mass scale of the right-hand side (vol)
   const double* cg_r;  // CG pass A: r and p_old (TMA-staged with their halos)
   const double* cg_p;
   double* cg_pout;     // CG pass A: p_k at owned points (ping-pong partner of cg_p)
@@ -706,7 +712,8 @@ template <int P, int MODE, int TK>
 __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm, const ItemGeom& g,
                                            int j, uint32_t f, double (&acc)[2 * P][RPT],
                                            double (&pr)[P][RPT], const double (&auxv)[RPT],
-                                           double (&dsum)[6], double beta) {
+                                           double (&dsum)[6], double beta,
+                                           double (&accm)[2 * P][RPT]) {
   constexpr bool INTERIOR = (TK == TILE_INTERIOR), RAGGED = (TK == TILE_RAGGED);
   using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
@@ -727,7 +734,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   const bool in_grid = (zg >= 0) && (zg < prm.nz_glob);
   const double* X1 = sm.X + (f & 1) * 2 * C::XARR;
   const double* X2 = X1 + C::XARR;
-  double out[RPT];
+  double out[RPT], om[RPT];
   // ghost planes (outside the global grid) enter the z ring as zeros through
   // the same FMA path: one writer of acc keeps the ring registers coalesced
   double wm[RPT], wa[RPT];
@@ -830,6 +837,19 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         acc[S - 1][i] = v;
       }
     }
+    if (MODE == M_HRES) {
+      // pure mass ring (Mz(x)My(x)Mx) u: the M_MASS kernel's z pass on wm
+      const double* tzm = sm.tab + ((0 * 2 + 0) * NC + cz) * R;
+      const bool fz = cz == ewz && prm.zfast;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const double a = wm[i];
+        om[i] = fma(fz ? T.M(0) : tzm[0], a, accm[0][i]);
+#pragma unroll
+        for (int k = 0; k < S - 1; ++k) accm[k][i] = fma(fz ? T.M(k + 1) : tzm[k + 1], a, accm[k + 1][i]);
+        accm[S - 1][i] = (fz ? T.M(S) : tzm[S]) * a;
+      }
+    }
   }
 
   // ---- epilogue: output plane zo = zl - P (complete once j >= 2P) ----
@@ -854,8 +874,12 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           double o = prm.c_mass * v;
           if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
           __stcs(prm.out + off, o);
-        } else {  // M_RESID
-          const double bb = auxv[i];
+        } else {  // M_RESID (b loaded) / M_HRES (b = rhs_cm M u + a F, rounded as M_MASS)
+          double bb = auxv[i];
+          if (MODE == M_HRES) {
+            bb = prm.rhs_cm * om[i];
+            if (prm.aux) bb = fma(prm.aux_scale, auxv[i], bb);
+          }
           const double r = bb - v;
           __stcs(prm.out + off, r);
           const double inv =
@@ -867,8 +891,8 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         }
       }
     }
-    if (MODE == M_CGA || MODE == M_RESID) dd_add(dsum[0], dsum[3], g0);
-    if (MODE == M_RESID) {
+    if (MODE == M_CGA || MODE == M_RESID || MODE == M_HRES) dd_add(dsum[0], dsum[3], g0);
+    if (MODE == M_RESID || MODE == M_HRES) {
       dd_add(dsum[1], dsum[4], g1);
       dd_add(dsum[2], dsum[5], g2);
     }
@@ -1131,10 +1155,11 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
   const int nin = g.zc1 - g.zc0 + 2 * P;
   double acc[S][RPT];
   double pr[P][RPT];
+  double accm[S][RPT];  // M_HRES: the pure mass ring
 #pragma unroll
   for (int k = 0; k < S; ++k)
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[k][i] = 0.0;
+    for (int i = 0; i < RPT; ++i) acc[k][i] = accm[k][i] = 0.0;
 #pragma unroll
   for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -1147,7 +1172,8 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
   double *op = nullptr, *pp = nullptr;
   const double* xp = nullptr;
   const long long py = prm.pitch_y;
-  constexpr bool CORE = INTERIOR && BSPDE_CORE_ITER && (MODE != M_CGA || BSPDE_CORE_CGA);
+  constexpr bool CORE = INTERIOR && BSPDE_CORE_ITER && MODE != M_HRES &&
+                        (MODE != M_CGA || BSPDE_CORE_CGA);
   if (CORE) {
     const int ewz = prm.ew[0];
     const int zbase = prm.z_off + g.zc0 - P;  // global z of streamed plane 0
@@ -1190,7 +1216,8 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
       double auxv[RPT];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
-      if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
+      if ((MODE == M_RESID || ((MODE == M_MASS || MODE == M_HRES) && prm.aux != nullptr)) &&
+          j >= 2 * P) {
         const int zo = g.zc0 - 2 * P + j;
         const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
 #pragma unroll
@@ -1201,7 +1228,7 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
         }
       }
       if (j + 1 < nin) plane_front<P, MODE, TK>(prm, sm, g, j + 1, flat + 1, beta);
-      plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta);
+      plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta, accm);
     }
     if (xown) {  // x + alpha p, rounded like the reference's x += alpha * p (solver.py:94)
       const double* stO = sm.stage + ((flat % Cfg<P, MODE>::NS) * Cfg<P, MODE>::NA + 1) *
@@ -1294,7 +1321,7 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
     double vh[1] = {dsum[0]}, vl[1] = {dsum[3]};
     reduce_and_finalize<1, NW>(vh, vl, s_red, s_last, prm.partials, prm.counter, prm.state,
                                prm.fuse, 1, prm.accumulate);
-  } else if (MODE == M_RESID) {
+  } else if (MODE == M_RESID || MODE == M_HRES) {
     double vh[3] = {dsum[0], dsum[1], dsum[2]}, vl[3] = {dsum[3], dsum[4], dsum[5]};
     reduce_and_finalize<3, NW>(vh, vl, s_red, s_last, prm.partials, prm.counter, prm.state,
                                prm.fuse, 0);
@@ -1821,6 +1848,7 @@ KernelInfo kernel_for(int p, int mode) {
     case M_APPLY: return kernel_info_p<M_APPLY>(p);
     case M_MASS: return kernel_info_p<M_MASS>(p);
     case M_RESID: return kernel_info_p<M_RESID>(p);
+    case M_HRES: return kernel_info_p<M_HRES>(p);
     default: return kernel_info_p<M_CGA>(p);
   }
 }
@@ -1966,6 +1994,7 @@ void fill_common(SepParams& sp, const bspde_plan* pl, int mode) {
   sp.out = nullptr;
   sp.aux = nullptr;
   sp.aux_scale = 0.0;
+  sp.rhs_cm = 0.0;
   sp.cg_r = nullptr;
   sp.cg_p = nullptr;
   sp.partials = nullptr;
@@ -2017,7 +2046,10 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
   sp.cg_pout = cg_pout;
   sp.cg_x = cg_x;
-  if (use_override) sp.c_mass = c_mass_override;
+  if (mode == M_HRES)
+    sp.rhs_cm = c_mass_override;  // the RHS mass scale (A keeps the plan's c_mass)
+  else if (use_override)
+    sp.c_mass = c_mass_override;
   if (scratch) {
     sp.state = scratch_state(scratch);
     sp.partials = scratch_partials(scratch);
@@ -2104,9 +2136,12 @@ int bspde_cg_read_report(bspde_plan*, const void*, bspde_cg_report*, int32_t*, v
 }
 namespace {
 
+// b == nullptr: heat step, r0 = (hcm M x + ha hf) - A x by the fused M_HRES
+// kernel (b is never formed)
 int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* pring,
                  double* ap, void* scratch, double* history, const bspde_cg_config* cfg,
-                 bspde_cg_report* report, cudaStream_t st) {
+                 bspde_cg_report* report, cudaStream_t st, const double* hf = nullptr,
+                 double hcm = 0.0, double ha = 0.0) {
   void* stream = (void*)st;
   const size_t bytes = (size_t)(pl->d.nz + 2 * pl->p) * pl->pitch_z * sizeof(double);
   int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
@@ -2116,7 +2151,8 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   const int R = cfg->p_ring > 0 ? cfg->p_ring : 2;
   const long long fs = (long long)(pl->d.nz + 2 * pl->p) * pl->pitch_z;
   CUDA_TRY(cudaMemsetAsync(pring + (R - 1) * fs, 0, bytes, st));
-  rc = launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st);
+  rc = b ? launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st)
+         : launch_sep(pl, M_HRES, x, nullptr, r, hf, ha, hcm, true, scratch, 1, st);
   if (rc) return rc;
   int32_t active = 0;
   rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
@@ -2258,7 +2294,7 @@ int bspde_plan_create(const bspde_plan_desc* desc, bspde_plan** out) {
     pl->d.stiff_table[a] = pl->host_tab.data() + ((a * 2 + 1) * pl->NC) * R;
   }
   // resolve kernel attributes before any stream capture
-  for (int mode = 0; mode < 4; ++mode) kernel_for(pl->p, mode);
+  for (int mode = 0; mode < 5; ++mode) kernel_for(pl->p, mode);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     bspde_plan_destroy(pl);
@@ -2554,6 +2590,31 @@ int bspde_cg_read_report(bspde_plan* pl, const void* scratch, bspde_cg_report* r
   }
   if (active) *active = hs->active;
   return BSPDE_OK;
+}
+
+int bspde_heat_residual(bspde_plan* pl, const double* u, const double* f, double cm, double a,
+                        double* r, void* scratch, int fuse, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!u || !r || !scratch) return fail(BSPDE_ERR_ARG, "null argument");
+  return launch_sep(pl, M_HRES, u, nullptr, r, f, f ? a : 0.0, cm, true, scratch, fuse,
+                    (cudaStream_t)stream);
+}
+
+int bspde_heat_step(bspde_plan* pl, double* u, const double* f, double cm, double a, double* r,
+                    double* p_ring, double* ap, void* scratch, double* history,
+                    const bspde_cg_config* cfg, bspde_cg_report* report, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!u || !r || !p_ring || !ap || !scratch || !cfg) return fail(BSPDE_ERR_ARG, "null argument");
+  if (!cfg->has_x0) return fail(BSPDE_ERR_ARG, "a heat step starts from x0 = u (has_x0 = 1)");
+  cudaStream_t caller = (cudaStream_t)stream;
+  cudaStream_t st = pl->work;
+  CUDA_TRY(cudaEventRecord(pl->ev_in, caller));
+  CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_in, 0));
+  int rc = pcg_solve_on(pl, nullptr, u, r, p_ring, ap, scratch, history, cfg, report, st, f, cm,
+                        f ? a : 0.0);
+  cudaEventRecord(pl->ev_out, st);
+  cudaStreamWaitEvent(caller, pl->ev_out, 0);
+  return rc;
 }
 
 int bspde_pcg_solve(bspde_plan* pl, const double* b, double* x, double* r, double* p_ring,

@@ -176,6 +176,24 @@ class NativePlan:
                                          C.byref(cfg), C.byref(rep), N.stream_handle(stream)))
         return rep
 
+    def heat_step(self, u, f, cm, a, r, pring, ap, scratch, history, tol, max_iter,
+                  record_history, poll_every=8, stream=None):
+        """One implicit-Euler step in place: (M + dt K) u <- cm M u + a f,
+        x0 = u; the RHS is fused into the first residual (bspde_heat_step)."""
+        cfg = N.CgConfig(float(tol), int(max_iter), int(bool(record_history)), 1,
+                         int(poll_every), int(pring.shape[0]))
+        rep = N.CgReport()
+        N.check(self.lib.bspde_heat_step(self.handle, N.ptr(u), N.ptr(f), float(cm), float(a),
+                                         N.ptr(r), N.ptr(pring), N.ptr(ap), N.ptr(scratch),
+                                         N.ptr(history), C.byref(cfg), C.byref(rep),
+                                         N.stream_handle(stream)))
+        return rep
+
+    def heat_residual(self, u, f, cm, a, r, scratch, fuse, stream=None):
+        N.check(self.lib.bspde_heat_residual(self.handle, N.ptr(u), N.ptr(f), float(cm),
+                                             float(a), N.ptr(r), N.ptr(scratch), int(fuse),
+                                             N.stream_handle(stream)))
+
     # step-wise CG (multi-GPU driver)
     def cg_setup(self, scratch, history, tol, max_iter, record_history, has_x0, stream=None,
                  p_ring=None):

@@ -199,6 +199,9 @@ class HeatSolver:
         return self.b
 
     def step(self, stream=None) -> SolveReport:
+        """Advance one dt.  Box: one fused native call (bspde_heat_step: the
+        RHS rides in the first residual kernel, b is never formed); mask /
+        variable conductivity: b = M u + dt F, then the stencil solve."""
         if self.mop is not None:  # mask: b = M_mask u + dt F on dense buffers
             lay = self.op.layout
             x = lay.owned(self.u).contiguous()
@@ -208,15 +211,15 @@ class HeatSolver:
             lay.owned(self.u).copy_(x)
             self.reports.append(rep)
             return rep
-        self.rhs(stream)
         if self.sop is not None:  # variable conductivity: dense buffers for the stencil solve
+            self.rhs(stream)
             lay = self.op.layout
             b, x = lay.owned(self.b).contiguous(), lay.owned(self.u).contiguous()
             rep = self.sop.pcg_device(b, x, self.config, has_x0=True, stream=stream)
             lay.owned(self.u).copy_(x)
             self.reports.append(rep)
             return rep
-        rep = pcg_device(self.op, self.b, self.u, self.config, has_x0=True, stream=stream)
+        rep = heat_step_device(self.op, self.u, self.F, self.dt, self.config, stream=stream)
         self.reports.append(rep)
         return rep
 
@@ -254,6 +257,23 @@ class HeatSolver:
         """The solution at the grid nodes (GPU sample_solution)."""
         grid = self.data.domain.grid
         return sample_solution_device(self.u, grid, self.data.n_b, self.op.layout).cpu().numpy()
+
+
+def heat_step_device(op, u_buf, F_buf, dt, config: SolveConfig, stream=None) -> SolveReport:
+    """(M + dt K) u <- vol M u + dt F in place on a box operator (x0 = u)."""
+    import time
+
+    from .solver import report_from
+
+    t0 = time.perf_counter()
+    w = _work(op, config.max_iter)
+    w.ensure_history(op, config.max_iter)
+    plan = op.plan(config.precond)
+    rep = plan.heat_step(u_buf, F_buf, op.data.vol, dt if F_buf is not None else 0.0, w.r,
+                         w.pring, w.ap, w.scratch,
+                         w.history if config.record_history else None, config.tol,
+                         config.max_iter, config.record_history, config.poll_every, stream)
+    return report_from(rep, config, time.perf_counter() - t0, w.history)
 
 
 def torch_empty_like(t):
