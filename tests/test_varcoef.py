@@ -121,3 +121,73 @@ def test_heat_with_variable_conductivity_vs_reference(golden, cuda_device, tag):
     # face makes heatvarf much worse conditioned (~750 iterations)
     bar = 1e-8 if tag == "heatvarf" else 1e-9
     assert np.linalg.norm(hs.coefficients() - ref) / np.linalg.norm(ref) < bar
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,ext", [(1, (40, 33, 35)), (2, (37, 41, 30)), (3, (64, 48, 72))])
+def test_otf_matches_assembled_stencil(cuda_device, monkeypatch, p, ext):
+    """The matrix-free operator (otf.cuh: the reference's on-the-fly
+    algorithm, nothing stored) against the assembled stencil (stencil.cuh):
+    two independent device implementations of the same variable-coefficient
+    operator; apply <= 1e-13, Jacobi diagonal <= 1e-14, PCG counts +-1 and
+    solutions 1e-10 at tol 1e-13.  Sizes with several x-y tiles, ragged
+    tiles and every edge class."""
+    import torch
+
+    from paper_1904_03057_b200.gram import basis_extension
+
+    step = tuple(1.0 / (n - 1) for n in ext)
+    pe = [n + 2 * basis_extension(p) for n in ext]
+    z, y, x = (np.linspace(0, 1, n) for n in pe)
+    D = 0.01 * (1.0 + 0.5 * np.sin(3 * z)[:, None, None] * np.cos(2 * y)[None, :, None]
+                * (1 + x[None, None, :]))
+    mu = 1.0 + 0.2 * np.cos(5 * z)[:, None, None] * np.sin(2 * y + 1)[None, :, None] \
+        * np.ones((1, 1, pe[2]))
+    data = build_system(BoxDomain(Grid(ext, step)), p, p, D, mu, [])
+    ops = {}
+    for kind in ("otf", "stencil"):
+        monkeypatch.setenv("BSPDE_VAR_STRATEGY", kind)
+        ops[kind] = make_operator(data, "b200")
+        assert ops[kind].kind == kind
+    c = np.random.default_rng(p).normal(size=data.cext)
+    t_o, t_s = ops["otf"].apply(c), ops["stencil"].apply(c)
+    assert relmax(t_o, t_s) < 1e-13
+    assert relmax(ops["otf"].jacobi_diagonal(), ops["stencil"].jacobi_diagonal()) < 1e-14
+    b = ops["stencil"].apply(np.cos(np.linspace(0, 3, c.size)).reshape(c.shape))
+    res = {k: pcg(op, b, SolveConfig(tol=1e-13, max_iter=3000)) for k, op in ops.items()}
+    (xo, ro), (xs, rs) = res["otf"], res["stencil"]
+    assert ro.converged and rs.converged
+    assert abs(ro.iterations - rs.iterations) <= 1, (ro.iterations, rs.iterations)
+    assert np.linalg.norm(xo - xs) / np.linalg.norm(xs) < 1e-10
+    torch.cuda.empty_cache()
+
+
+def test_otf_strategy_selection(monkeypatch):
+    """Matrix-free for 3-D boxes without faces and n_b = n_p <= 3; the
+    assembled stencil otherwise (faces, other degrees, 1-D / 2-D, masks)."""
+    import ctypes as C
+
+    from paper_1904_03057_b200 import varcoef
+
+    class Lib:
+        def __init__(self, ok):
+            self.ok = ok
+
+        def bspde_otf_supported(self, h):
+            return self.ok
+
+    class D:
+        mask = None
+
+    assert varcoef._var_strategy(D(), Lib(1), C.c_void_p()) == "otf"
+    assert varcoef._var_strategy(D(), Lib(0), C.c_void_p()) == "stencil"
+    monkeypatch.setenv("BSPDE_VAR_STRATEGY", "stencil")
+    assert varcoef._var_strategy(D(), Lib(1), C.c_void_p()) == "stencil"
+    monkeypatch.setenv("BSPDE_VAR_STRATEGY", "otf")
+    from paper_1904_03057_b200.errors import ConfigurationError
+    with pytest.raises(ConfigurationError):
+        varcoef._var_strategy(D(), Lib(0), C.c_void_p())
+    m = D()
+    m.mask = object()
+    monkeypatch.setenv("BSPDE_VAR_STRATEGY", "auto")
+    assert varcoef._var_strategy(m, Lib(1), C.c_void_p()) == "stencil"

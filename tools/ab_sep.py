@@ -42,7 +42,7 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
-times = {"rhs": [], "resid": [], "pass_a": [], "pass_b": []}
+times = {"rhs": [], "resid": [], "pass_a": [], "pass_b": [], "hres": [], "flush": []}
 dig = {}
 x = u.clone()
 for it in range(18):
@@ -79,6 +79,23 @@ for it in range(18):
         times["pass_a"].append(e[2].elapsed_time(e[3]))
         times["pass_b"].append(e[3].elapsed_time(e[4]))
 dig["r_final"] = digest(lay.owned(w.r))
+# fused heat residual (RHS + residual in one kernel) and the end-of-solve flush
+for it in range(8):
+    e = [ev() for _ in range(3)]
+    plan.cg_setup(w.scratch, None, 1e-300, 10 ** 6, False, True, p_ring=R)
+    e[0].record()
+    plan.heat_residual(x, F, op.data.vol, dt, w.r, w.scratch, 1)
+    e[1].record()
+    plan.cg_pass_a(x, w.r, w.pring[R - 1], w.pring[0], w.ap, w.scratch, 1)
+    plan.cg_pass_b(w.r, w.ap, w.scratch, 1)
+    e2 = ev()
+    e2.record()
+    plan.cg_flush_x(x, w.pring, w.scratch)
+    e[2].record()
+    torch.cuda.synchronize()
+    if it >= 2:
+        times["hres"].append(e[0].elapsed_time(e[1]))
+        times["flush"].append(e2.elapsed_time(e[2]))
 out = {"lib": os.path.basename(os.environ.get("BSPDE_LIB", "product")), "ncoef": ncoef, "p": p,
        **{k + "_ms": round(float(np.median(v)), 4) for k, v in times.items()},
        "digests": dig}
