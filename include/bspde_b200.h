@@ -291,8 +291,16 @@ typedef struct {
 
 int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** plan);
 int bspde_stencil_destroy(bspde_stencil* plan);
-/* number of doubles of the stencil array P ((2p+1)^3 * nz*ny*nx) */
+/* number of doubles of the stencil array P ((2p+1)^3 * rows) */
 int64_t bspde_stencil_entries(const bspde_stencil* plan);
+/* Compact mode (mask domains): store and iterate only the nact active rows
+ * (device array of their dense indices, ascending, kept alive by the caller)
+ * -- P[a * nact + k]; the vectors stay dense and their inactive entries are
+ * never written (inactive entries of a right-hand side must be zero, as the
+ * reference's _mask_rhs_fixup makes them, operator.py:444-459).  Call before
+ * bspde_stencil_assemble; the 600 x 600 x 2400 leg needs ~40 GB instead of
+ * 187 GB of stencil. */
+int bspde_stencil_set_rows(bspde_stencil* plan, const int64_t* rows, int64_t nact);
 int64_t bspde_stencil_launch_count(const bspde_stencil* plan);
 /* P <- stencils of all nodes from the parameter fields (device, dense) */
 int bspde_stencil_assemble(bspde_stencil* plan, const double* dfield,
@@ -348,6 +356,7 @@ typedef struct {
   const uint8_t* node_class;  /* nz*ny*nx: 0 inactive, 1 interior, 2 boundary */
   const int64_t* brows;       /* flat extended indices of the boundary nodes */
   int64_t nbrows;
+  const int64_t* brows_k;     /* compact plans: each boundary row's slot in the active-row list */
   int32_t jlo, nj;            /* cell_node_offsets(n_b) = jlo .. jlo+nj-1 */
   int32_t blo, nbp;           /* cell_node_offsets(n_p) */
   const double* cell_tri;     /* [2][nj][nj][nbp]: value / derivative cell tables */

@@ -88,6 +88,7 @@ class MaskDesc(C.Structure):
         ("node_class", C.c_void_p),
         ("brows", C.c_void_p),
         ("nbrows", C.c_int64),
+        ("brows_k", C.c_void_p),
         ("jlo", C.c_int32), ("nj", C.c_int32),
         ("blo", C.c_int32), ("nbp", C.c_int32),
         ("cell_tri", C.c_void_p),
@@ -142,6 +143,7 @@ SIGNATURES = [
     ("bspde_stencil_create", C.c_int, [C.POINTER(StencilDesc), C.POINTER(C.c_void_p)]),
     ("bspde_stencil_destroy", C.c_int, [_VP]),
     ("bspde_stencil_entries", C.c_int64, [_VP]),
+    ("bspde_stencil_set_rows", C.c_int, [_VP, _VP, C.c_int64]),
     ("bspde_otf_supported", C.c_int, [_VP]),
     ("bspde_otf_prepare", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("bspde_otf_apply", C.c_int, [_VP, _VP, _VP, _VP]),

@@ -53,7 +53,20 @@ struct StencilDev {
   double step[3];
   int degen[3];             // unit axes of 1-D / 2-D problems (no extension)
   int ex[3], exp_[3];       // per-axis ext / ext_p (0 on unit axes)
+  // compact mode (mask domains): only the active rows are stored and
+  // iterated, P[a * nact + k] for active row k = dense index rows[k]
+  // (ascending); vectors stay dense, inactive entries are never touched
+  const int64_t* rows;
+  long long nact;
 };
+
+// rows iterated by the row-wise kernels (all nodes, or the active rows)
+__device__ __forceinline__ long long st_nrows(const StencilDev& S) {
+  return S.rows ? S.nact : S.N;
+}
+__device__ __forceinline__ long long st_row(const StencilDev& S, long long k) {
+  return S.rows ? S.rows[k] : k;
+}
 
 __device__ __forceinline__ double st_face_value(const StencilDev& S, int i, int n, int side) {
   const int ew = (S.ncls - 1) / 2;  // == edge_width(n_b) for face tables
@@ -81,11 +94,13 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_tab[i] = S.tab[i];
   __syncthreads();
   const long long A3 = (long long)S.A * S.A * S.A;
-  const long long total = A3 * S.N;
+  const long long nr = st_nrows(S);
+  const long long total = A3 * nr;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long l = t % S.N;
-    const int a = (int)(t / S.N);
+    const long long kr = t % nr;
+    const long long l = st_row(S, kr);
+    const int a = (int)(t / nr);
     const int ax = a % S.A, ay = (a / S.A) % S.A, az = a / (S.A * S.A);
     const int lx = (int)(l % S.nx), ly = (int)((l / S.nx) % S.ny), lz = (int)(l / ((long long)S.nx * S.ny));
     const int cz = st_cls(lz, S.nz, S.ew[0]), cy = st_cls(ly, S.ny, S.ew[1]),
@@ -141,7 +156,7 @@ __global__ void __launch_bounds__(ST_NT) stencil_assemble_kernel(const StencilDe
       }
       acc += prod;
     }
-    P[(long long)a * S.N + l] = acc;
+    P[(long long)a * nr + kr] = acc;
   }
 }
 
@@ -255,13 +270,14 @@ __global__ void __launch_bounds__(ST_NT) stencil_pform_kernel(const StencilDev S
   // two grid-stride elements per trip (loads of both issued together; the
   // per-element arithmetic is unchanged)
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const double* diag = P + (long long)center * S.N;
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += 2 * stride) {
-    const long long l2 = l + stride;
-    const bool two = l2 < S.N;
-    const double dg = diag[l], rv = r[l], pv = p[l];
-    const double dg2 = two ? diag[l2] : 1.0, rv2 = two ? r[l2] : 0.0, pv2 = two ? p[l2] : 0.0;
+  const long long nr = st_nrows(S);
+  const double* diag = P + (long long)center * nr;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nr; k += 2 * stride) {
+    const long long k2 = k + stride;
+    const bool two = k2 < nr;
+    const long long l = st_row(S, k), l2 = two ? st_row(S, k2) : 0;
+    const double dg = diag[k], rv = r[l], pv = p[l];
+    const double dg2 = two ? diag[k2] : 1.0, rv2 = two ? r[l2] : 0.0, pv2 = two ? p[l2] : 0.0;
     const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
     p[l] = pdir(rv, inv, pv, beta);
     if (two) {
@@ -289,19 +305,20 @@ __global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev 
   // two grid-stride elements per trip, accumulated in the same order as a
   // one-element loop (bitwise the same sums)
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const double* diag = P + (long long)center * S.N;
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += 2 * stride) {
-    const long long l2 = l + stride;
-    const bool two = l2 < S.N;
-    const double xv = x[l], pv = p[l], rv = r[l], av = ap[l], dg = diag[l];
+  const long long nr = st_nrows(S);
+  const double* diag = P + (long long)center * nr;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nr; k += 2 * stride) {
+    const long long k2 = k + stride;
+    const bool two = k2 < nr;
+    const long long l = st_row(S, k), l2 = two ? st_row(S, k2) : 0;
+    const double xv = x[l], pv = p[l], rv = r[l], av = ap[l], dg = diag[k];
     double xv2 = 0.0, pv2 = 0.0, rv2 = 0.0, av2 = 0.0, dg2 = 1.0;
     if (two) {
       xv2 = x[l2];
       pv2 = p[l2];
       rv2 = r[l2];
       av2 = ap[l2];
-      dg2 = diag[l2];
+      dg2 = diag[k2];
     }
     x[l] = __dadd_rn(xv, __dmul_rn(alpha, pv));
     const double rn = __dsub_rn(rv, __dmul_rn(alpha, av));
@@ -325,9 +342,71 @@ __global__ void __launch_bounds__(ST_NT) stencil_update_kernel(const StencilDev 
 __global__ void stencil_diag_kernel(const StencilDev S, const double* P, double* out) {
   const int A = S.A, hb = S.nb;
   const int center = (hb * A + hb) * A + hb;
-  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < S.N;
-       l += (long long)gridDim.x * blockDim.x)
-    out[l] = P[(long long)center * S.N + l];
+  const long long nr = st_nrows(S);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nr;
+       k += (long long)gridDim.x * blockDim.x)
+    out[st_row(S, k)] = P[(long long)center * nr + k];
+}
+
+// Compact mode apply: one thread per active row, t = sum_a P[a, k] c[l + a]
+// (ascending a, as the dense kernels), epilogues as stencil_apply_kernel.
+template <int MODE, int NB>
+__global__ void __launch_bounds__(ST_NT) stencil_capply_kernel(
+    const StencilDev S, const double* __restrict__ P, const double* __restrict__ c,
+    double* __restrict__ out, const double* __restrict__ aux, double* partials,
+    unsigned* counter, CgState* st, int precond) {
+  __shared__ double s_red[(ST_NT / 32) * 8];
+  __shared__ unsigned s_last;
+  if (MODE == 2 && !ld_vol(&st->active)) return;
+  constexpr int A = 2 * NB + 1, hb = NB;
+  constexpr int center = (hb * A + hb) * A + hb;
+  const long long nr = S.nact;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s0l = 0.0, s1l = 0.0, s2l = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nr;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long l = S.rows[k];
+    const int lx = (int)(l % S.nx), ly = (int)((l / S.nx) % S.ny),
+              lz = (int)(l / ((long long)S.nx * S.ny));
+    double t = 0.0;
+    int a = 0;
+#pragma unroll
+    for (int az = -hb; az <= hb; ++az) {
+      const int z = lz + az;
+#pragma unroll
+      for (int ay = -hb; ay <= hb; ++ay) {
+        const int y = ly + ay;
+        const bool ok = z >= 0 && z < S.nz && y >= 0 && y < S.ny;
+        const double* crow = c + ((long long)z * S.ny + y) * S.nx;
+#pragma unroll
+        for (int ax = -hb; ax <= hb; ++ax, ++a) {
+          const int x = lx + ax;
+          if (ok && x >= 0 && x < S.nx) t = fma(P[(long long)a * nr + k], crow[x], t);
+        }
+      }
+    }
+    if (MODE == 0) {
+      out[l] = t;
+    } else if (MODE == 1) {
+      const double bb = aux[l];
+      const double r = bb - t;
+      out[l] = r;
+      const double dg = P[(long long)center * nr + k];
+      const double inv = (precond && dg != 0.0) ? 1.0 / dg : 1.0;
+      ST_ACC(s0, s0l, bb, bb);
+      ST_ACC(s1, s1l, r, __dmul_rn(inv, r));
+      ST_ACC(s2, s2l, r, r);
+    } else {
+      out[l] = t;
+      ST_ACC(s0, s0l, c[l], t);
+    }
+  }
+  if (MODE == 1) {
+    double vh[3] = {s0, s1, s2}, vl[3] = {s0l, s1l, s2l};
+    reduce_and_finalize<3, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 0);
+  } else if (MODE == 2) {
+    double vh[1] = {s0}, vl[1] = {s0l};
+    reduce_and_finalize<1, ST_NT / 32>(vh, vl, s_red, &s_last, partials, counter, st, 1, 1);
+  }
 }
 
 }  // namespace
@@ -517,6 +596,17 @@ template <int MODE>
 void st_apply(const bspde_stencil* s, unsigned grid, cudaStream_t st, const double* P,
               const double* c, double* out, const double* aux, double* partials,
               unsigned* counter, CgState* state, int precond, const uint8_t* live = nullptr) {
+  if (s->S.rows) {  // compact (active rows only)
+    const unsigned cg = st_grid(s, s->S.nact);
+    switch (s->S.nb) {
+      case 1: stencil_capply_kernel<MODE, 1><<<cg, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      case 2: stencil_capply_kernel<MODE, 2><<<cg, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      case 3: stencil_capply_kernel<MODE, 3><<<cg, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      case 4: stencil_capply_kernel<MODE, 4><<<cg, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+      default: stencil_capply_kernel<MODE, 5><<<cg, ST_NT, 0, st>>>(s->S, P, c, out, aux, partials, counter, state, precond); break;
+    }
+    return;
+  }
   // y mapping for p >= 3 (measured +5-30% apply, +25% PCG at p = 3); at
   // p = 1, 2 the compiler batches every load of the short stencil into
   // registers (128-255) and the x mapping is faster
@@ -621,6 +711,10 @@ int st_pcg(bspde_stencil* s, const double* P, const double* b, double* x, double
   const size_t bytes = (size_t)s->S.N * sizeof(double);
   if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
   CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+  if (s->S.rows) {  // compact: the inactive entries of r and Ap are never written
+    CUDA_TRY(cudaMemsetAsync(r, 0, bytes, st));
+    CUDA_TRY(cudaMemsetAsync(ap, 0, bytes, st));
+  }
   const unsigned grid = st_grid(s, s->S.N);
   double* partials = scratch_partials(scratch);
   unsigned* counter = scratch_counter(scratch);
@@ -628,7 +722,8 @@ int st_pcg(bspde_stencil* s, const double* P, const double* b, double* x, double
   const unsigned agrid = st_grid(s, s->S.N / XB + 1);
   uint8_t* live = nullptr;
   if (!otf)
-    if (int lrc = st_live(s, P, st, &live)) return lrc;
+    if (!s->S.rows)
+      if (int lrc = st_live(s, P, st, &live)) return lrc;
   if (otf) {
     if (int orc = otf_launch<1>(s, st, x, r, b, partials, counter, state, precond)) return orc;
   } else {
@@ -720,6 +815,8 @@ int bspde_stencil_create(const bspde_stencil_desc* desc, bspde_stencil** out) {
       return fail(BSPDE_ERR_ARG, "bad face axis / side");
     }
   }
+  S.rows = nullptr;
+  S.nact = 0;
   for (int k = 0; k < MAXP + 1; ++k) S.fv[k] = 0.0;
   for (int k = 0; k < 121; ++k) S.gram[k] = 0.0;
   if (d.nfaces > 0) {
@@ -785,7 +882,16 @@ int bspde_stencil_destroy(bspde_stencil* s) {
 
 int64_t bspde_stencil_entries(const bspde_stencil* s) {
   if (!s) return -1;
-  return (int64_t)s->S.A * s->S.A * s->S.A * s->S.N;
+  return (int64_t)s->S.A * s->S.A * s->S.A * (s->S.rows ? s->S.nact : s->S.N);
+}
+
+int bspde_stencil_set_rows(bspde_stencil* s, const int64_t* rows, int64_t nact) {
+  if (int rc = st_check(s)) return rc;
+  if ((rows == nullptr) != (nact == 0) || nact < 0 || nact > s->S.N)
+    return fail(BSPDE_ERR_ARG, "rows / nact: device array of 1..N ascending active rows");
+  s->S.rows = rows;
+  s->S.nact = nact;
+  return BSPDE_OK;
 }
 
 int64_t bspde_stencil_launch_count(const bspde_stencil* s) { return s ? s->launches : -1; }
@@ -979,7 +1085,8 @@ __global__ void __launch_bounds__(ST_NT) mask_rows_kernel(const StencilDev S,
         }
       }
     }
-    P[(long long)a * S.N + l] = acc;
+    // compact mode: the row's slot in the active-row list (M.brows_k)
+    P[(long long)a * st_nrows(S) + (S.rows ? M.brows_k[t % M.nbrows] : l)] = acc;
   }
 }
 
@@ -1048,8 +1155,12 @@ int bspde_stencil_mask_patch(bspde_stencil* s, const bspde_mask_desc* m, const d
   if (!dfield || !mfield || !P) return fail(BSPDE_ERR_ARG, "null argument");
   const cudaStream_t st = (cudaStream_t)stream;
   const long long A3 = (long long)s->S.A * s->S.A * s->S.A;
-  mask_zero_kernel<<<st_grid(s, A3 * s->S.N), ST_NT, 0, st>>>(s->S, m->node_class, P);
-  s->launches++;
+  if (!s->S.rows) {  // dense: zero the rows of inactive nodes (compact P has none)
+    mask_zero_kernel<<<st_grid(s, A3 * s->S.N), ST_NT, 0, st>>>(s->S, m->node_class, P);
+    s->launches++;
+  } else if (m->nbrows > 0 && !m->brows_k) {
+    return fail(BSPDE_ERR_ARG, "compact mask plan: brows_k required");
+  }
   if (m->nbrows > 0) {
     mask_rows_kernel<<<st_grid(s, A3 * m->nbrows), ST_NT, 0, st>>>(s->S, *m, dfield, mfield, P);
     s->launches++;
