@@ -915,6 +915,10 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
 #ifndef BSPDE_CORE_ITER
 #define BSPDE_CORE_ITER 1
 #endif
+// degrees whose pass A prefetches x a plane ahead (tuning)
+#ifndef BSPDE_XPF_MAXP
+#define BSPDE_XPF_MAXP 3
+#endif
 // core iterations in CG pass A too (measured slower: register pressure)
 #ifndef BSPDE_CORE_CGA
 #define BSPDE_CORE_CGA 0
@@ -1202,9 +1206,12 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
   plane_front<P, MODE, TK>(prm, sm, g, 0, flat, beta);
   __syncthreads();
   for (int j = 0; j < nin; ++j) {
+    // x is prefetched at the start of the plane for p <= 3; p >= 4 loads it
+    // at the update (the 3p-deep rings leave no registers to hold it)
+    constexpr bool XPF = P <= BSPDE_XPF_MAXP;
     double xv[RPT];
     const bool xown = xupd && j >= P && j < nin - P;  // plane zc0 - P + j is owned
-    if (xown) {
+    if (XPF && xown) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
         xv[i] = (INTERIOR || (gy0 + i < prm.ny && gx < prm.nx)) ? xrow[i * prm.pitch_y] : 0.0;
@@ -1231,6 +1238,11 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
       plane_back<P, MODE, TK>(prm, sm, g, j, flat, acc, pr, auxv, dsum, beta, accm);
     }
     if (xown) {  // x + alpha p, rounded like the reference's x += alpha * p (solver.py:94)
+      if (!XPF) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          xv[i] = (INTERIOR || (gy0 + i < prm.ny && gx < prm.nx)) ? xrow[i * prm.pitch_y] : 0.0;
+      }
       const double* stO = sm.stage + ((flat % Cfg<P, MODE>::NS) * Cfg<P, MODE>::NA + 1) *
                                          Cfg<P, MODE>::ARR_D;
 #pragma unroll
