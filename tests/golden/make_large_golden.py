@@ -60,17 +60,21 @@ def case(ncoef, p):
     # p >= 4 need many more iterations to 1e-13 (the degree-5 mass matrix):
     # capped by BSPDE_LARGE_MAXIT; its_1e13 = -1 when the cap is hit first
     cap = int(os.environ.get("BSPDE_LARGE_MAXIT", "5000"))
-    x, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=1e-13, max_iter=cap, x0=u0,
+    # the final tolerance (default 1e-13; C3 930^3 runs to 1e-10 on the GPU
+    # box, where the 64 GB of oracle vectors fit in host memory)
+    tol = float(os.environ.get("BSPDE_LARGE_TOL", "1e-13"))
+    x, rep = O.pcg(A.apply, A.jacobi_diagonal, b, tol=tol, max_iter=cap, x0=u0,
                    res_history=hist)
     hist = np.asarray(hist)
     its10 = int(np.argmax(hist <= 1e-10)) if np.any(hist <= 1e-10) else -1
     idx = sample_index(A.cext)
     out = dict(meta=np.array([ncoef, p, N, h, dt]), its_1e10=its10,
-               its_1e13=rep["iterations"] if rep["converged"] else -1, res_history=hist,
+               its_1e13=(rep["iterations"] if rep["converged"] and tol <= 1e-13 else -1),
+               final_tol=tol, res_history=hist,
                u0_norm=np.linalg.norm(u0), b_norm=np.linalg.norm(b), x_norm=np.linalg.norm(x),
                idx=idx, x_sample=x[idx[:, 0], idx[:, 1], idx[:, 2]],
                u0_sample=u0[idx[:, 0], idx[:, 1], idx[:, 2]])
-    path = os.path.join(HERE, f"large_{ncoef}_p{p}.npz")
+    path = os.path.join(os.environ.get("BSPDE_LARGE_OUT", HERE), f"large_{ncoef}_p{p}.npz")
     np.savez_compressed(path, **out)
     print(f"{path}: its 1e-10 {its10}, 1e-13 {rep['iterations']}, {time.time() - t0:.0f} s",
           flush=True)

@@ -723,7 +723,7 @@ def test_full_size_windows_symmetry_and_true_residual(cuda_device, ncoef, p):
     torch.cuda.empty_cache()
 
 
-LARGE = [(256, 3), (512, 1), (512, 2), (512, 3), (512, 4), (512, 5)]
+LARGE = [(256, 3), (512, 1), (512, 2), (512, 3), (512, 4), (512, 5), (930, 3)]
 
 
 @pytest.mark.slow
@@ -764,8 +764,11 @@ def test_large_heat_step_vs_oracle_fixture(golden, cuda_device, ncoef, p):
     del F
     bn = float(torch.linalg.vector_norm(lay.owned(b)))
     assert abs(bn - float(g["b_norm"])) <= 1e-13 * bn
-    nmax = len(g["res_history"]) - 1  # the oracle run's iteration cap
+    nmax = len(g["res_history"]) - 1  # the oracle run's last iteration
+    final_tol = float(g["final_tol"]) if "final_tol" in g else 1e-13
     for tol, key in ((1e-10, "its_1e10"), (1e-13, "its_1e13")):
+        if tol < final_tol:
+            continue  # C3: the oracle ran to 1e-10 only (host-memory / time bound)
         x = u.clone()
         want = int(g[key])
         rep = pcg_device(op, b, x, SolveConfig(tol=tol, max_iter=nmax if want < 0 else 5000),
@@ -774,11 +777,13 @@ def test_large_heat_step_vs_oracle_fixture(golden, cuda_device, ncoef, p):
             assert rep.iterations == nmax
         else:
             assert abs(rep.iterations - want) <= 1, (tol, rep.iterations, want)
-    # both runs stop at the same point: compare the final coefficients
+    # the final coefficients: 1e-10 at tol 1e-13; at tol
+    # 1e-10 two correct solvers drift ~kappa * tol apart (C3 bar 1e-7)
+    bar = 1e-10 if final_tol <= 1e-13 else 1e-7
     xs, xo = sample(x), g["x_sample"]
-    assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
+    assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < bar
     xn = float(torch.linalg.vector_norm(lay.owned(x)))
-    assert abs(xn - float(g["x_norm"])) <= 1e-10 * xn
+    assert abs(xn - float(g["x_norm"])) <= bar * xn
     del x, u, b
     torch.cuda.empty_cache()
 
