@@ -56,7 +56,12 @@ def case(ncoef, p):
     A = O.KronOperator((N,) * 3, (h,) * 3, p, dt, 1.0)
     b = A.mass_apply(u0) + dt * A.mass_apply(q)
     del q
-    hist = []
+    class Progress(list):  # prints every iterate's residual (long runs)
+        def append(self, v):
+            super().append(v)
+            print(f"  it {len(self) - 1}: {v:.3e} ({time.time() - t0:.0f} s)", flush=True)
+
+    hist = Progress() if os.environ.get("BSPDE_LARGE_PROGRESS") else []
     # p >= 4 need many more iterations to 1e-13 (the degree-5 mass matrix):
     # capped by BSPDE_LARGE_MAXIT; its_1e13 = -1 when the cap is hit first
     cap = int(os.environ.get("BSPDE_LARGE_MAXIT", "5000"))
