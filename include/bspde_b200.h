@@ -163,9 +163,11 @@ int bspde_heat_residual(bspde_plan* plan, const double* u, const double* f, doub
 
 /* ---- step-wise CG for the multi-GPU driver (z-slabs, one rank per GPU).
  * fuse = 1: the kernel's last CTA reduces the per-CTA partials and runs the
- * scalar update (single device).  fuse = 0: it only writes the local sums
- * (4 doubles at the start of scratch); the caller all-reduces them and calls
- * bspde_cg_finalize(kind). */
+ * scalar update (single device).  fuse = 0: it only writes this rank's sums
+ * as double-double pairs (the first 64 bytes of scratch: 4 hi, then 4 lo);
+ * one rank calls bspde_cg_finalize(kind), N ranks all-gather those 64 bytes
+ * and call bspde_cg_finalize_gathered(kind) -- the scalars, hence the
+ * iterates, are then bit-identical to the single-device solve. */
 int bspde_cg_setup(bspde_plan* plan, void* scratch, double* history,
                    const bspde_cg_config* cfg, void* stream);
 /* r = b - A x (x = x0 or zero), sums = {<b,b>, <r,D^-1 r>, <r,r>}   kind 0 */
@@ -202,6 +204,11 @@ int bspde_cg_flush_x(bspde_plan* plan, double* x, const double* p_ring,
 /* kind 0/1/2: scalar update after residual / pass A / pass B (skipped when
  * inactive); kind 3 is used internally by bspde_cg_flush_x. */
 int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
+/* N-rank scalar update: `gathered` = the rank-major all-gather (world x 8
+ * doubles) of every rank's first 64 scratch bytes; the pairs are summed in
+ * rank order in double-double and rounded once (kind 0..2). */
+int bspde_cg_finalize_gathered(bspde_plan* plan, void* scratch, const void* gathered,
+                               int world, int kind, void* stream);
 /* Copy the scalar state to the host (synchronizes the stream). */
 int bspde_cg_read_report(bspde_plan* plan, const void* scratch,
                          bspde_cg_report* report, int32_t* active, void* stream);

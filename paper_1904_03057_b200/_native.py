@@ -169,6 +169,7 @@ SIGNATURES = [
     ("bspde_fir_axis", C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
                                  C.c_int32, _VP]),
     ("bspde_cg_finalize", C.c_int, [_VP, _VP, C.c_int, _VP]),
+    ("bspde_cg_finalize_gathered", C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, _VP]),
     ("bspde_cg_read_report", C.c_int, [_VP, _VP, C.POINTER(CgReport),
                                        C.POINTER(C.c_int32), _VP]),
 ]

@@ -116,13 +116,15 @@ struct Cfg {
   }
 };
 
-// x += alpha p is applied every R iterations (and by the flush at the end of
-// a solve) from a ring of R <= kPRing search directions (R = CgState::ring,
-// 2 or 4); see cg_pass_b_kernel
+// Search directions live in a ring of R <= kPRing fields (R = CgState::ring,
+// 2 or 4): iteration k writes p_k to field k % R and its pass A applies
+// x += alpha_{k-1} p_{k-1} from field (k-1) % R; the flush at the end of a
+// solve applies the last update (x_flush_kernel)
 constexpr int kPRing = BSPDE_P_RING;
 
 struct CgState {
-  double sums[4];        // local partial sums (all-reduced across ranks for N>1)
+  double sums[4];        // the dot products of the last pass (fuse = 1: rounded totals;
+  double sums_lo[4];     // fuse = 0: this rank's double-double pairs sums + sums_lo)
   double rz, alpha, beta, pAp;
   double res, res0, scale, tol;
   double rhs_norm, pad_d;
@@ -355,6 +357,10 @@ __global__ void finalize_kernel(CgState* s, int kind) {
       return;
     }
     if (kind != 0 && !s->active) return;
+    for (int i = 0; i < 4; ++i) {  // round the (single-rank) double-double pairs
+      s->sums[i] = __dadd_rn(s->sums[i], s->sums_lo[i]);
+      s->sums_lo[i] = 0.0;
+    }
     finalize_state(s, kind);
   }
 }
@@ -381,6 +387,24 @@ __device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
 __device__ __forceinline__ void dd_add2(double& hi, double& lo, double xhi, double xlo) {
   dd_add(hi, lo, xhi);
   lo = __dadd_rn(lo, xlo);
+}
+
+// Multi-rank scalar update: `gathered` holds every rank's 8 doubles
+// (sums[4], sums_lo[4]; rank-major, the all-gather of the first 64 bytes of
+// each rank's scratch).  The pairs are added in rank order in double-double
+// and rounded once, so every rank computes the same scalars -- equal to the
+// single-device ones (the total is the correctly rounded dot either way).
+__global__ void finalize_gathered_kernel(CgState* s, const double* gathered, int world, int kind) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (kind != 0 && !s->active) return;
+    for (int i = 0; i < 4; ++i) {
+      double h = 0.0, l = 0.0;
+      for (int r = 0; r < world; ++r) dd_add2(h, l, gathered[r * 8 + i], gathered[r * 8 + 4 + i]);
+      s->sums[i] = __dadd_rn(h, l);
+      s->sums_lo[i] = 0.0;
+    }
+    finalize_state(s, kind);
+  }
 }
 
 // Deterministic block reduction of NV double-double values (hi, lo), per-CTA
@@ -445,8 +469,14 @@ __device__ void reduce_and_finalize(double (&vh)[NV], double (&vl)[NV], double* 
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const double tot = __dadd_rn(th[i], tl[i]);
-        st->sums[i] = accumulate ? st->sums[i] + tot : tot;
+        if (fuse) {
+          const double tot = __dadd_rn(th[i], tl[i]);
+          st->sums[i] = accumulate ? st->sums[i] + tot : tot;
+        } else {  // keep the pair: the ranks' pairs are combined before rounding
+          if (accumulate) dd_add2(th[i], tl[i], st->sums[i], st->sums_lo[i]);
+          st->sums[i] = th[i];
+          st->sums_lo[i] = tl[i];
+        }
       }
       if (fuse) finalize_state(st, kind);
       *counter = 0u;
@@ -2578,6 +2608,18 @@ int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
   if (int rc = check_plan(pl)) return rc;
   if (kind < 0 || kind > 3) return fail(BSPDE_ERR_ARG, "finalize kind must be 0..3");
   finalize_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(scratch_state(scratch), kind);
+  pl->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_cg_finalize_gathered(bspde_plan* pl, void* scratch, const void* gathered, int world,
+                               int kind, void* stream) {
+  if (int rc = check_plan(pl)) return rc;
+  if (kind < 0 || kind > 2) return fail(BSPDE_ERR_ARG, "finalize_gathered kind must be 0..2");
+  if (world < 1 || !gathered) return fail(BSPDE_ERR_ARG, "finalize_gathered: bad world/buffer");
+  finalize_gathered_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
+      scratch_state(scratch), (const double*)gathered, world, kind);
   pl->launches++;
   CUDA_TRY(cudaGetLastError());
   return BSPDE_OK;

@@ -232,6 +232,11 @@ class NativePlan:
         N.check(self.lib.bspde_cg_finalize(self.handle, N.ptr(scratch), int(kind),
                                            N.stream_handle(stream)))
 
+    def cg_finalize_gathered(self, scratch, gathered, world, kind, stream=None):
+        N.check(self.lib.bspde_cg_finalize_gathered(self.handle, N.ptr(scratch), N.ptr(gathered),
+                                                    int(world), int(kind),
+                                                    N.stream_handle(stream)))
+
     def cg_read(self, scratch, stream=None):
         rep = N.CgReport()
         active = C.c_int32()

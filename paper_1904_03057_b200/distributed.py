@@ -18,10 +18,15 @@ Per CG iteration (``distributed_pcg``):
      under r's exchange through ``bspde_cg_pass_a_range``);
   2. pass A (fuse=0) forms p_k (stored into the ping-pong partner buffer),
      applies x += alpha_{k-1} p_{k-1} on the owned planes and writes the
-     local <p, Ap>; ``all_reduce`` of 1 double; the 1-thread finalize kernel
-     runs the scalar update on every rank;
-  3. pass B (fuse=0): r -= alpha Ap, local <r, D^-1 r>, <r, r>;
-     ``all_reduce`` of 2 doubles; finalize.
+     local <p, Ap> as a double-double pair; ``all_gather`` of the ranks'
+     pairs (64 bytes each); the 1-thread finalize kernel adds them in rank
+     order, rounds once and runs the scalar update on every rank;
+  3. pass B (fuse=0): r -= alpha Ap, local <r, D^-1 r>, <r, r>; all-gather;
+     finalize.
+
+The rounded scalars equal the single-device ones (both are the correctly
+rounded dot products, bspde_b200.cu "Double-double"), so an N-rank solve
+takes the same iterations as one GPU, bit for bit.
 
 Every rank holds identical scalar state, so the device-side ``active`` flag
 (stop rule, guards) agrees everywhere; the host polls it every
@@ -32,7 +37,7 @@ sums.
 Transport: NCCL over NVLink/NVSwitch in production (one process per GPU).
 With the gloo backend (several ranks sharing one GPU in the multi-process
 GPU test, or CPU runs) the halo planes and the scalar sums of CUDA tensors
-are staged through host memory (``HaloExchanger`` / ``_allreduce_fn``).
+are staged through host memory (``HaloExchanger`` / ``_all_gather_fn``).
 
 The orchestration is written against a small ops interface so it can be
 exercised on CPU with the gloo backend (tests/test_distributed_cpu.py); the
@@ -172,30 +177,48 @@ class HaloExchanger:
         return []
 
 
-def _allreduce_fn(world, group=None):
-    if world == 1:
-        return lambda t: None
+def _all_gather_fn(world, group=None):
+    """t (k values) -> the rank-major (world x k) gather, on t's device."""
     import torch.distributed as dist
 
-    def fn(t):
+    torch = _torch()
+
+    def fn(t, out):
         if t.is_cuda and dist.get_backend(group) == "gloo":  # host-staged (see module doc)
-            h = t.cpu()
-            dist.all_reduce(h, group=group)
-            t.copy_(h)
+            parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, t.cpu(), group=group)
+            out.copy_(torch.cat(parts))
         else:
-            dist.all_reduce(t, group=group)
+            dist.all_gather_into_tensor(out, t, group=group)
 
     return fn
 
 
 class NativeSlabOps:
-    """Step-wise CG through the C ABI on one rank's slab (fuse = 0)."""
+    """Step-wise CG through the C ABI on one rank's slab (fuse = 0).
 
-    def __init__(self, plan):
+    The passes leave this rank's dot products as double-double pairs (the
+    first 64 bytes of scratch); ``reduce`` all-gathers the world's pairs (8
+    doubles per rank) and the finalize kernel adds them in rank order before
+    rounding once, so the scalars -- and the iterates -- are bit-identical on
+    every rank and to the single-device solve."""
+
+    def __init__(self, plan, world=1, group=None):
         self.plan = plan
+        self.world = world
+        self._gather = _all_gather_fn(world, group) if world > 1 else None
+        self._gathered = None
 
-    def sums(self, scratch, n):
-        return scratch[: 8 * 4].view(_torch().float64)[:n]
+    def reduce(self, scratch, n, kind):
+        """Cross-rank scalar step after a fuse = 0 pass (n sums, finalize kind)."""
+        if self.world == 1:
+            self.plan.cg_finalize(scratch, kind)
+            return
+        torch = _torch()
+        if self._gathered is None or self._gathered.device != scratch.device:
+            self._gathered = torch.empty(self.world * 8, dtype=torch.float64, device=scratch.device)
+        self._gather(scratch[:64].view(torch.float64), self._gathered)
+        self.plan.cg_finalize_gathered(scratch, self._gathered, self.world, kind)
 
     def setup(self, scratch, history, cfg, has_x0, ring=None):
         self.plan.cg_setup(scratch, history, cfg.tol, cfg.max_iter, cfg.record_history, has_x0,
@@ -212,9 +235,6 @@ class NativeSlabOps:
 
     def pass_b(self, r, ap, scratch):
         self.plan.cg_pass_b(r, ap, scratch, 0)
-
-    def finalize(self, scratch, kind):
-        self.plan.cg_finalize(scratch, kind)
 
     def flush_x(self, x, pring, scratch):
         self.plan.cg_flush_x(x, pring, scratch)
@@ -251,7 +271,7 @@ def _halo_mode(ops, halo):
     return mode
 
 
-def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: SolveConfig,
+def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
                     has_x0=True, history=None):
     """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
     ``pring`` holds the ring of search directions (leading axis).  Iteration
@@ -267,8 +287,7 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
     ops.setup(scratch, history, config, has_x0, ring=R)
     halo(x)
     ops.residual(b, x, r, scratch)
-    allreduce(ops.sums(scratch, 3))
-    ops.finalize(scratch, 0)
+    ops.reduce(scratch, 3, 0)
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
     k = 0
@@ -290,11 +309,9 @@ def distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, config: S
                     ops.pass_a_range(x, r, p_in, p_out, ap, scratch, 0, g, True)
                     ops.pass_a_range(x, r, p_in, p_out, ap, scratch, nz - g, g, True)
                 pending_p = halo.start(p_out) if mode != "off" else []
-                allreduce(ops.sums(scratch, 1))
-                ops.finalize(scratch, 1)
+                ops.reduce(scratch, 1, 1)
                 ops.pass_b(r, ap, scratch)
-                allreduce(ops.sums(scratch, 2))
-                ops.finalize(scratch, 2)
+                ops.reduce(scratch, 2, 2)
                 k += 1
             rep, active = ops.read(scratch)
     finally:
@@ -337,7 +354,6 @@ class DistributedOperator:
             ranks = dist.get_process_group_ranks(group) if group is not None else None
             self.halo_group = dist.new_group(ranks=ranks)
         self.halo = HaloExchanger(self.layout, self.rank, self.world, self.halo_group)
-        self.allreduce = _allreduce_fn(self.world, group)
         self._work = None
 
     def plan(self, precond="jacobi"):
@@ -407,8 +423,8 @@ class DistributedOperator:
     def pcg_device(self, b_buf, x_buf, config: SolveConfig = None, has_x0=True):
         config = config or SolveConfig()
         w = self._work_buffers(config.max_iter)
-        ops = NativeSlabOps(self.plan(config.precond))
-        rep, wall = distributed_pcg(ops, self.halo, self.allreduce, b_buf, x_buf, w["r"],
+        ops = NativeSlabOps(self.plan(config.precond), self.world, self.group)
+        rep, wall = distributed_pcg(ops, self.halo, b_buf, x_buf, w["r"],
                                     w["pring"], w["ap"], w["scratch"], config, has_x0,
                                     w["history"] if config.record_history else None)
         return report_from(rep, config, wall, w["history"])

@@ -49,8 +49,12 @@ class CpuSlabOps:
         out = self.ora.apply(full[g:g + nzg])
         return torch.from_numpy(out[lo:lo + nz].copy())
 
-    def sums(self, scratch, n):
-        return scratch[:n]
+    def reduce(self, scratch, n, kind):
+        """NativeSlabOps.reduce: combine the ranks' sums, then the scalar update
+        (a plain all-reduce here; the product all-gathers double-double pairs)."""
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(scratch[:n])
+        self.finalize(scratch, kind)
 
     def setup(self, scratch, history, cfg, has_x0, ring=4):
         self.state = dict(tol=cfg.tol, max_iter=cfg.max_iter, has_x0=has_x0, it=0, active=1,
@@ -185,12 +189,8 @@ def _worker(rank, world, port, ext, p, out_q, overlap="pipeline", ring=4):
         ops = CpuSlabOps(ora, lay)
         halo = HaloExchanger(lay, rank, world, dist.new_group())  # own communicator, as the product
 
-        def allreduce(t):
-            dist.all_reduce(t)
-
         cfg = SolveConfig(tol=1e-13, max_iter=1000, poll_every=3)
-        rep, _ = distributed_pcg(ops, halo, allreduce, b, x, r, pring, ap, scratch, cfg,
-                                 has_x0=True)
+        rep, _ = distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, cfg, has_x0=True)
         own = lay.owned(x).contiguous()
         parts = [torch.zeros((part.bounds(q)[1] - part.bounds(q)[0],) + tuple(own.shape[1:]),
                              dtype=own.dtype) for q in range(world)]

@@ -3,11 +3,11 @@
 2 and 3 ranks on cuda:0 run ``DistributedOperator.pcg_device`` --
 ``NativeSlabOps`` (the sm_100a step-wise kernels with fuse = 0: ranged pass
 A, pass B, the 1-thread finalize) driven by ``distributed_pcg`` -- over the
-gloo backend, whose halo planes and scalar all-reduces are staged through
+gloo backend, whose halo planes and scalar all-gathers are staged through
 host memory (NCCL refuses two ranks on one device).  Every halo-overlap mode
-and both ring lengths; the gathered solution must match the fused
-single-rank solver (counts +-1, coefficients 1e-10 at tol 1e-13) and the
-oracle.  The ranks' kernels never wait on one another (the exchanges are
+and both ring lengths; the gathered solution must equal the fused
+single-rank solver's bit for bit (same iteration count) and match the oracle
+(counts +-1, coefficients 1e-10 at tol 1e-13).  The ranks' kernels never wait on one another (the exchanges are
 synchronous host copies), so sharing the device is safe.
 """
 
@@ -125,6 +125,10 @@ def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
         bar = 1 if k == 0 else max(1, round(0.01 * ro["iterations"]))
         assert abs(its[k] - rep1.iterations) <= bar, (tol, its[k], rep1.iterations)
         assert abs(its[k] - ro["iterations"]) <= bar, (tol, its[k], ro["iterations"])
+    # the ranks' double-double pairs are combined before rounding, so the slab
+    # solve reproduces the single-device iterates bit for bit
+    assert its[1] == rep1.iterations
+    assert np.array_equal(xs, x1), np.abs(xs - x1).max()
     assert np.linalg.norm(xs - x1) / np.linalg.norm(x1) < 1e-10
     assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
     want = ora.apply(x0_full)

@@ -38,8 +38,8 @@ r.normal_()
 q.normal_()
 scratch = plan.scratch()
 plan.cg_setup(scratch, None, 1e-300, 100, False, False)
-scratch[48:56].view(torch.float64)[0] = 0.5   # CgState.beta
-scratch[120:124].view(torch.int32)[0] = 1     # CgState.active
+scratch[80:88].view(torch.float64)[0] = 0.5   # CgState.beta
+scratch[152:156].view(torch.int32)[0] = 1     # CgState.active
 nz = lay.nz
 
 
