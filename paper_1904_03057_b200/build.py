@@ -31,7 +31,8 @@ def needs_rebuild():
         return True
     mt = os.path.getmtime(LIB)
     deps = [SRC, os.path.join(ROOT, "include", "bspde_b200.h"),
-            os.path.join(HERE, "csrc", "stencil.cuh"), os.path.join(HERE, "csrc", "gram_taps.cuh")]
+            os.path.join(HERE, "csrc", "stencil.cuh"), os.path.join(HERE, "csrc", "gram_taps.cuh"),
+            os.path.join(HERE, "csrc", "otf.cuh")]
     return any(os.path.getmtime(d) > mt for d in deps if os.path.exists(d))
 
 

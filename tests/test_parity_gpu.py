@@ -763,7 +763,8 @@ def test_large_heat_step_vs_oracle_fixture(golden, cuda_device, ncoef, p):
     op.mass_apply_device(u, b, F, a=dt)
     del F
     bn = float(torch.linalg.vector_norm(lay.owned(b)))
-    assert abs(bn - float(g["b_norm"])) <= 1e-13 * bn
+    # input check (the oracle run's b): <= 1e-13 at 256^3 / 512^3, 3.4e-13 at 930^3
+    assert abs(bn - float(g["b_norm"])) <= 1e-12 * bn, (bn, float(g["b_norm"]))
     nmax = len(g["res_history"]) - 1  # the oracle run's last iteration
     final_tol = float(g["final_tol"]) if "final_tol" in g else 1e-13
     for tol, key in ((1e-10, "its_1e10"), (1e-13, "its_1e13")):
