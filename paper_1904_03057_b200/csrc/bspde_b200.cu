@@ -737,14 +737,6 @@ __device__ __forceinline__ void plane_front(const SepParams& prm, const Smem& sm
   }
 }
 
-// BSPDE_PR_RELOAD=1: CG pass A stores p_k of plane z as soon as it is formed
-// (from the stage) and reloads it (an L2 hit) for the <p, Ap> of output plane z
-// P planes later, instead of carrying a P-deep register ring of p (24
-// registers at p = 3)
-#ifndef BSPDE_PR_RELOAD
-#define BSPDE_PR_RELOAD 0
-#endif
-
 // back half of plane j (flat index f): y-pass, z-ring shift update, epilogue
 template <int P, int MODE, int TK>
 __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm, const ItemGeom& g,
@@ -773,17 +765,6 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
   const double* X1 = sm.X + (f & 1) * 2 * C::XARR;
   const double* X2 = X1 + C::XARR;
   double out[RPT], om[RPT];
-  constexpr bool PRL = (MODE == M_CGA) && BSPDE_PR_RELOAD;
-  double pk[RPT];  // PRL: p_k of the output plane, stored P planes ago by this thread
-  if (PRL && j >= 2 * P) {
-    const long long pb = (long long)(zl - P + prm.ghost) * prm.pitch_z + gx;
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int y = gy0 + i;
-      pk[i] = (INTERIOR || (y < ny && gx < nx)) ? __ldcg(prm.cg_pout + pb + (long long)y * prm.pitch_y)
-                                                : 0.0;
-    }
-  }
   // ghost planes (outside the global grid) enter the z ring as zeros through
   // the same FMA path: one writer of acc keeps the ring registers coalesced
   double wm[RPT], wa[RPT];
@@ -917,12 +898,8 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           __stcs(prm.out + off, v);
         } else if (MODE == M_CGA) {
           __stcs(prm.out + off, v);
-          if (PRL) {
-            g0 = fma(pk[i], v, g0);
-          } else {
-            prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
-            g0 = fma(pr[0][i], v, g0);
-          }
+          prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
+          g0 = fma(pr[0][i], v, g0);
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
           if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -954,23 +931,11 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     // own p_k of plane zl (slot 0; the stage is released only after this iteration)
     const int s = f % NS;
     const double* stP = sm.stage + (s * NA + 0) * C::ARR_D;
-    if (PRL) {  // p_k of an owned plane -> p_out now (for pass B; reloaded at its epilogue)
-      if (zl >= g.zc0 && zl < g.zc1) {
-        const long long pb = (long long)(zl + prm.ghost) * prm.pitch_z + gx;
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const int y = gy0 + i;
-          if (INTERIOR || (y < ny && gx < nx))
-            prm.cg_pout[pb + (long long)y * prm.pitch_y] = stP[(rg * RPT + i + P) * HX + cxl + PX];
-        }
-      }
-    } else {
+    for (int i = 0; i < RPT; ++i) {
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-#pragma unroll
-        for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
-        pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
-      }
+      for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
+      pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
     }
   }
 }
@@ -1055,12 +1020,6 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
   if ((MODE == M_RESID || (MODE == M_MASS && prm.aux != nullptr)) && j >= 2 * P) {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) auxv[i] = __ldcs(xp + i * py);
-  }
-  constexpr bool PRL = (MODE == M_CGA) && BSPDE_PR_RELOAD;
-  double pk[RPT];
-  if (PRL && j >= 2 * P) {
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) pk[i] = __ldcg(pp + i * py);
   }
 
   // ---- front of plane j+1: stage wait, p = D^-1 r + beta p_old, x-pass ----
@@ -1183,12 +1142,8 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
         __stcs(op + i * py, v);
       } else if (MODE == M_CGA) {
         __stcs(op + i * py, v);
-        if (PRL) {
-          g0 = fma(pk[i], v, g0);
-        } else {
-          pp[i * py] = pr[0][i];
-          g0 = fma(pr[0][i], v, g0);
-        }
+        pp[i * py] = pr[0][i];
+        g0 = fma(pr[0][i], v, g0);
       } else if (MODE == M_MASS) {
         double o = prm.c_mass * v;
         if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -1211,18 +1166,11 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
   if (MODE == M_CGA) {
     const int s = f % NS;
     const double* stP = sm.stage + (s * NA + 0) * C::ARR_D;  // p_k
-    if (PRL) {  // plane zo + P
-      // (warm-up planes would need the owned-plane guard of plane_back)
-      static_assert(!(PRL && BSPDE_CORE_CGA), "BSPDE_PR_RELOAD needs BSPDE_CORE_CGA=0");
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) pp[P * prm.pitch_z + i * py] = stP[(rg * RPT + i + P) * HX + cxl + PX];
-    } else {
+    for (int i = 0; i < RPT; ++i) {
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-#pragma unroll
-        for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
-        pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
-      }
+      for (int k = 0; k < P - 1; ++k) pr[k][i] = pr[k + 1][i];
+      pr[P - 1][i] = stP[(rg * RPT + i + P) * HX + cxl + PX];
     }
   }
 }
