@@ -328,7 +328,7 @@ def run_reference(args, rank, world):
 METRIC = "CG iteration DoF/s (GDoF/s) and % HBM roofline at 0.8B nodes, 1/2/4/8 B200"
 
 
-def config_of(args, world):
+def config_of(args, world, halo=None):
     from paper_1904_03057_b200.gram import basis_extension
 
     ncoef, p = args.ncoef, args.degree
@@ -340,8 +340,8 @@ def config_of(args, world):
                         f"implicit Euler lambda=4, Jacobi-PCG tol 1e-10, z-slabs x{world}",
             "ncoef": ncoef, "degree": p, "dofs": ncoef ** 3, "precision": "fp64",
             "parallelism": f"zslab{world}",
-            "halo_overlap": (os.environ.get("BSPDE_HALO_OVERLAP", "pipeline") if world > 1
-                             else "none (single slab)"),
+            "halo_overlap": (halo or os.environ.get("BSPDE_HALO_OVERLAP", "peer or pipeline")
+                             if world > 1 else "none (single slab)"),
             "l2": f"inputs ({gb:.1f} GB/vector) vs 126 MB L2"}
 
 
@@ -391,6 +391,7 @@ def run_ours(args, rank, world, local_rank):
         op = DistributedOperator(data)
         lay = op.layout
         z_range = op.part.bounds()
+    halo_mode = None
     u = lay.alloc(dev)
     F = lay.alloc(dev)
     gaussian_coeffs(N, h, p, device=dev, out=u, layout=lay, z_range=z_range, **IC)
@@ -400,6 +401,10 @@ def run_ours(args, rank, world, local_rank):
     else:
         wb = op._work_buffers(cfg.max_iter)
         r_buf, ring = wb["r"], wb["pring"].shape[0]
+        # peer: pass A / pass B store the halo planes into the neighbours'
+        # fields (CUDA IPC over NVLink); else NCCL halo transfers
+        halo_mode = os.environ.get("BSPDE_HALO_OVERLAP",
+                                   "peer" if op._peers is not None else "pipeline")
     gaussian_coeffs(N, h, p, device=dev, out=r_buf, layout=lay, z_range=z_range, **SOURCE)
     op.mass_apply_device(r_buf, F)
     if world == 1:
@@ -476,7 +481,7 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(args, world),
+        "data": "synthetic", "config": config_of(args, world, halo_mode),
         "cg_iterations_per_step": its,
         "memory": {"fields_per_rank": mem["fields"], "p_ring": int(ring),
                    "bytes_per_rank": mem["field_bytes"] * (4 + int(ring))},

@@ -209,6 +209,35 @@ int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
  * rank order in double-double and rounded once (kind 0..2). */
 int bspde_cg_finalize_gathered(bspde_plan* plan, void* scratch, const void* gathered,
                                int world, int kind, void* stream);
+/* ---- z-slab peer halos (NVLink peer memory / CUDA IPC) ------------------
+ * With peers set, the step-wise pass A also stores p_k of its first / last
+ * p owned planes into the lower / upper neighbour's ghost planes of the same
+ * ring field (k % R), and pass B stores the new r of those planes into the
+ * neighbours' r ghost planes: the compute kernels carry the halo exchange
+ * (no separate NCCL transfer per iteration).  The scalar all-gather after
+ * each pass orders the peer stores before the neighbour's next read.  The
+ * reference analogue is the worker windows' halo (operator.py:61-74). */
+typedef struct {
+  const double* ring;        /* this rank's p ring: ring_len fields, ring_stride doubles apart */
+  const double* r;           /* this rank's r */
+  long long ring_stride;
+  int ring_len;
+  int lo_nz;                 /* owned planes of the lower neighbour */
+  double* lo_ring;           /* lower neighbour (NULL: none) */
+  long long lo_ring_stride;
+  double* lo_r;
+  double* hi_ring;           /* upper neighbour (NULL: none) */
+  long long hi_ring_stride;
+  double* hi_r;
+} bspde_slab_peers;
+/* NULL clears. */
+int bspde_slab_set_peers(bspde_plan* plan, const bspde_slab_peers* peers);
+/* CUDA IPC of a device pointer inside a cudaMalloc'd block: 64-byte handle of
+ * the block + the pointer's offset; import maps it (peer access enabled
+ * lazily) and returns the pointer; close unmaps. */
+int bspde_ipc_export(const void* ptr, void* handle64, uint64_t* offset);
+int bspde_ipc_import(const void* handle64, uint64_t offset, void** ptr);
+int bspde_ipc_close(void* ptr);
 /* Copy the scalar state to the host (synchronizes the stream). */
 int bspde_cg_read_report(bspde_plan* plan, const void* scratch,
                          bspde_cg_report* report, int32_t* active, void* stream);

@@ -114,6 +114,22 @@ class CgReport(C.Structure):
     ]
 
 
+class SlabPeers(C.Structure):
+    _fields_ = [
+        ("ring", C.c_void_p),
+        ("r", C.c_void_p),
+        ("ring_stride", C.c_int64),
+        ("ring_len", C.c_int32),
+        ("lo_nz", C.c_int32),
+        ("lo_ring", C.c_void_p),
+        ("lo_ring_stride", C.c_int64),
+        ("lo_r", C.c_void_p),
+        ("hi_ring", C.c_void_p),
+        ("hi_ring_stride", C.c_int64),
+        ("hi_r", C.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) -- must cover every function in include/bspde_b200.h
 _VP = C.c_void_p
 SIGNATURES = [
@@ -170,6 +186,10 @@ SIGNATURES = [
                                  C.c_int32, _VP]),
     ("bspde_cg_finalize", C.c_int, [_VP, _VP, C.c_int, _VP]),
     ("bspde_cg_finalize_gathered", C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, _VP]),
+    ("bspde_slab_set_peers", C.c_int, [_VP, C.POINTER(SlabPeers)]),
+    ("bspde_ipc_export", C.c_int, [_VP, _VP, C.POINTER(C.c_uint64)]),
+    ("bspde_ipc_import", C.c_int, [_VP, C.c_uint64, C.POINTER(_VP)]),
+    ("bspde_ipc_close", C.c_int, [_VP]),
     ("bspde_cg_read_report", C.c_int, [_VP, _VP, C.POINTER(CgReport),
                                        C.POINTER(C.c_int32), _VP]),
 ]

@@ -155,6 +155,12 @@ struct SepParams {
   const double* cg_p;
   double* cg_pout;     // CG pass A: p_k at owned points (ping-pong partner of cg_p)
   double* cg_x;        // CG pass A: x += alpha_{k-1} p_{k-1} at owned points (k >= 1)
+  // z-slab peer halos: the neighbours' p_out fields (NVLink peer memory /
+  // CUDA IPC); p_k of the first / last `ghost` owned planes is also stored
+  // into their upper / lower ghost planes (the lower neighbour owns nz_lo planes)
+  double* peer_lo;
+  double* peer_hi;
+  int nz_lo;
   double* partials;
   unsigned* counter;
   CgState* state;
@@ -204,6 +210,9 @@ struct PassBParams {
   unsigned* counter;
   CgState* state;
   int fuse;
+  double* peer_lo;  // z-slab peer halos of r (see SepParams)
+  double* peer_hi;
+  int nz_lo;
 };
 
 // ---------------------------------------------------------------------------
@@ -888,6 +897,9 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     const long long obase =
         (long long)(zo + prm.ghost) * prm.pitch_z + (long long)gy0 * prm.pitch_y + gx;
     const int czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
+    // z-slab peer halos: this output plane is one of a neighbour's ghost planes
+    const bool peer_lo_pl = (MODE == M_CGA) && prm.peer_lo != nullptr && zo < prm.ghost;
+    const bool peer_hi_pl = (MODE == M_CGA) && prm.peer_hi != nullptr && zo >= prm.nz - prm.ghost;
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // group sums of this thread's rows (dd_add)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -901,6 +913,8 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           __stcs(prm.out + off, v);
           prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
           g0 = fma(pr[0][i], v, g0);
+          if (peer_lo_pl) prm.peer_lo[off + (long long)prm.nz_lo * prm.pitch_z] = pr[0][i];
+          if (peer_hi_pl) prm.peer_hi[off - (long long)prm.nz * prm.pitch_z] = pr[0][i];
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
           if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -922,6 +936,7 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         }
       }
     }
+    if (peer_lo_pl || peer_hi_pl) __threadfence_system();
     if (MODE == M_CGA || MODE == M_RESID || MODE == M_HRES) dd_add(dsum[0], dsum[3], g0);
     if (MODE == M_RESID || MODE == M_HRES) {
       dd_add(dsum[1], dsum[4], g1);
@@ -1005,6 +1020,7 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
                                           double inv0, double* op, double* pp, const double* xp,
                                           long long py) {
   using C = Cfg<P, MODE>;
+  static_assert(!(MODE == M_CGA && BSPDE_CORE_CGA), "core_iter: no z-slab peer halo stores");
   constexpr int NW = C::NW, TY = C::TY, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS;
   constexpr int PX = C::PX, DX = C::DX, S = 2 * P;
   constexpr bool STIFF = C::STIFF;
@@ -1473,6 +1489,20 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       dd_add(rz, rzl, __dmul_rn(rn, __dmul_rn(i0, rn)));
       dd_add(rr, rrl, __dmul_rn(rn, rn));
     }
+    // z-slab peer halos: the new r of a boundary row is also a neighbour's ghost row
+    const bool plo = prm.peer_lo != nullptr && zl < prm.ghost;
+    const bool phi = prm.peer_hi != nullptr && zl >= prm.nz - prm.ghost;
+    if (plo || phi) {
+      __syncwarp();
+      double* dst = plo ? prm.peer_lo + base + (long long)prm.nz_lo * prm.pitch_z
+                        : prm.peer_hi + base - (long long)prm.nz * prm.pitch_z;
+      for (int xx = lane; xx < nx; xx += 32) dst[xx] = rrw[xx];
+      if (plo && phi) {  // a slab of <= 2 ghost planes feeds both neighbours
+        double* d2 = prm.peer_hi + base - (long long)prm.nz * prm.pitch_z;
+        for (int xx = lane; xx < nx; xx += 32) d2[xx] = rrw[xx];
+      }
+      __threadfence_system();
+    }
   }
   double vh[2] = {rz, rr}, vl[2] = {rzl, rrl};
   reduce_and_finalize<2, NTB / 32>(vh, vl, s_red, &s_last, prm.partials, prm.counter, prm.state,
@@ -1886,6 +1916,8 @@ struct bspde_plan {
   cudaEvent_t ev_out = nullptr;
   // per (kernel mode, planes streamed): plan_launch is a simulation
   std::map<std::pair<int, int>, Launch> launch_cache;
+  bool peers = false;         // z-slab peer halos (bspde_slab_set_peers)
+  bspde_slab_peers peer{};
 };
 
 namespace {
@@ -2128,6 +2160,19 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
   sp.cg_pout = cg_pout;
   sp.cg_x = cg_x;
+  sp.peer_lo = sp.peer_hi = nullptr;
+  sp.nz_lo = 0;
+  if (mode == M_CGA && pl->peers && cg_pout) {
+    // p_out is ring field k % R of this rank: the neighbours' field k % R
+    const bspde_slab_peers& q = pl->peer;
+    const long long d = cg_pout - q.ring;
+    if (q.ring_stride > 0 && d >= 0 && d % q.ring_stride == 0 && d / q.ring_stride < q.ring_len) {
+      const long long slot = d / q.ring_stride;
+      if (q.lo_ring) sp.peer_lo = q.lo_ring + slot * q.lo_ring_stride;
+      if (q.hi_ring) sp.peer_hi = q.hi_ring + slot * q.hi_ring_stride;
+      sp.nz_lo = q.lo_nz;
+    }
+  }
   if (mode == M_HRES)
     sp.rhs_cm = c_mass_override;  // the RHS mass scale (A keeps the plan's c_mass)
   else if (use_override)
@@ -2185,6 +2230,13 @@ int launch_pass_b(bspde_plan* pl, double* x, double* r, const double* pring, con
   bp.counter = scratch_counter(scratch);
   bp.state = scratch_state(scratch);
   bp.fuse = fuse;
+  bp.peer_lo = bp.peer_hi = nullptr;
+  bp.nz_lo = 0;
+  if (!flush && pl->peers && r && r == pl->peer.r) {
+    bp.peer_lo = pl->peer.lo_r;
+    bp.peer_hi = pl->peer.hi_r;
+    bp.nz_lo = pl->peer.lo_nz;
+  }
   const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
   void* args[1] = {&bp};
   if (flush) {
@@ -2650,6 +2702,77 @@ int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
   finalize_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(scratch_state(scratch), kind);
   pl->launches++;
   CUDA_TRY(cudaGetLastError());
+  return BSPDE_OK;
+}
+
+int bspde_slab_set_peers(bspde_plan* pl, const bspde_slab_peers* peers) {
+  if (int rc = check_plan(pl)) return rc;
+  if (!peers) {
+    pl->peers = false;
+    pl->peer = bspde_slab_peers{};
+    return BSPDE_OK;
+  }
+  const bspde_slab_peers& q = *peers;
+  if (!q.ring || !q.r || q.ring_stride <= 0 || q.ring_len < 2 || q.ring_len > kPRing)
+    return fail(BSPDE_ERR_ARG, "slab peers: bad ring / r");
+  if ((q.lo_ring == nullptr) != (q.lo_r == nullptr) || (q.hi_ring == nullptr) != (q.hi_r == nullptr))
+    return fail(BSPDE_ERR_ARG, "slab peers: a neighbour needs both its ring and r");
+  if (q.lo_ring && (q.lo_ring_stride <= 0 || q.lo_nz < pl->p))
+    return fail(BSPDE_ERR_ARG, "slab peers: bad lower neighbour");
+  if (q.hi_ring && q.hi_ring_stride <= 0) return fail(BSPDE_ERR_ARG, "slab peers: bad upper neighbour");
+  if (pl->d.nz < pl->p) return fail(BSPDE_ERR_ARG, "slab peers: slab thinner than the halo");
+  pl->peer = q;
+  pl->peers = true;
+  return BSPDE_OK;
+}
+
+namespace {
+using GetRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+GetRangeFn get_range_fn() {
+  static GetRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<GetRangeFn>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+int bspde_ipc_export(const void* ptr, void* handle, uint64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(BSPDE_ERR_ARG, "null argument");
+  GetRangeFn rng = get_range_fn();
+  if (!rng) return fail(BSPDE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (rng(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return fail(BSPDE_ERR_ARG, "ipc export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((const char*)ptr - (const char*)base);
+  return BSPDE_OK;
+}
+
+int bspde_ipc_import(const void* handle, uint64_t offset, void** ptr) {
+  if (!handle || !ptr) return fail(BSPDE_ERR_ARG, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr = (char*)base + offset;
+  return BSPDE_OK;
+}
+
+int bspde_ipc_close(void* ptr) {
+  if (!ptr) return BSPDE_OK;
+  GetRangeFn rng = get_range_fn();
+  CUdeviceptr base = (CUdeviceptr)ptr;
+  size_t size = 0;
+  if (rng) rng(&base, &size, (CUdeviceptr)ptr);
+  CUDA_TRY(cudaIpcCloseMemHandle((void*)base));
   return BSPDE_OK;
 }
 

@@ -237,6 +237,11 @@ class NativePlan:
                                                     int(world), int(kind),
                                                     N.stream_handle(stream)))
 
+    def set_peers(self, peers):
+        """z-slab peer halos (``_native.SlabPeers`` or None to clear)."""
+        N.check(self.lib.bspde_slab_set_peers(self.handle,
+                                              C.byref(peers) if peers is not None else None))
+
     def cg_read(self, scratch, stream=None):
         rep = N.CgReport()
         active = C.c_int32()
@@ -248,6 +253,28 @@ class NativePlan:
 # resident fields of a heat run besides the p ring: u (= x), F, r, Ap (= b)
 HEAT_BASE_FIELDS = 4
 HBM_BUDGET = 175e9  # bytes of HBM3e a rank may fill with fields (B200: 180 GB usable)
+
+
+def ipc_export(t):
+    """CUDA IPC handle (64 bytes) and byte offset of a device tensor's data."""
+    lib = N.load()
+    h = (C.c_char * 64)()
+    off = C.c_uint64()
+    N.check(lib.bspde_ipc_export(N.ptr(t), h, C.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def ipc_import(handle, offset):
+    """Map another process's allocation (``ipc_export``): a device pointer."""
+    lib = N.load()
+    out = C.c_void_p()
+    N.check(lib.bspde_ipc_import(C.create_string_buffer(bytes(handle), 64), int(offset),
+                                 C.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(ptr):
+    N.check(N.load().bspde_ipc_close(C.c_void_p(ptr)))
 
 
 def heat_memory_plan(cext, degree, world=1, budget=HBM_BUDGET, ring=None):

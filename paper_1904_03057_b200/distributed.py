@@ -203,11 +203,18 @@ class NativeSlabOps:
     rounding once, so the scalars -- and the iterates -- are bit-identical on
     every rank and to the single-device solve."""
 
-    def __init__(self, plan, world=1, group=None):
+    def __init__(self, plan, world=1, group=None, peers=None):
         self.plan = plan
         self.world = world
         self._gather = _all_gather_fn(world, group) if world > 1 else None
         self._gathered = None
+        self.peers = peers  # _native.SlabPeers of this rank's work set, or None
+        self.peer_ready = peers is not None
+
+    def use_peers(self, on):
+        """Pass A / pass B store the boundary planes of p_k / r into the
+        neighbours' ghost planes themselves (bspde_slab_set_peers)."""
+        self.plan.set_peers(self.peers if on else None)
 
     def reduce(self, scratch, n, kind):
         """Cross-rank scalar step after a fuse = 0 pass (n sums, finalize kind)."""
@@ -243,11 +250,18 @@ class NativeSlabOps:
         return self.plan.cg_read(scratch)
 
 
-HALO_MODES = ("pipeline", "split", "off")
+HALO_MODES = ("peer", "pipeline", "split", "off")
 
 
 def _halo_mode(ops, halo):
-    """``BSPDE_HALO_OVERLAP``: "pipeline" (default), "split" or "off" ("0").
+    """``BSPDE_HALO_OVERLAP``: "peer" (default when the neighbours' fields are
+    mapped), "pipeline" (default otherwise), "split" or "off" ("0").
+
+    * peer -- the kernels store the halo planes themselves: pass A writes
+      p_k's first / last p owned planes into the neighbours' ghost planes
+      (NVLink peer memory, mapped by CUDA IPC), pass B the new r's; the
+      scalar all-gather after each pass orders those stores before the
+      neighbour's next pass, so no halo transfer is issued per iteration;
 
     * pipeline -- p_k's ghost planes travel while the <p,Ap> all-reduce,
       finalize and pass B of the same iteration run (the exchange is posted
@@ -261,10 +275,13 @@ def _halo_mode(ops, halo):
     """
     if halo.world == 1:
         return "off"
-    mode = os.environ.get("BSPDE_HALO_OVERLAP", "pipeline")
+    peer_ready = getattr(ops, "peer_ready", False)
+    mode = os.environ.get("BSPDE_HALO_OVERLAP", "peer" if peer_ready else "pipeline")
     mode = "off" if mode == "0" else mode
     if mode not in HALO_MODES:
         raise ConfigurationError(f"BSPDE_HALO_OVERLAP must be one of {HALO_MODES}, got {mode!r}")
+    if mode == "peer" and not peer_ready:
+        mode = "pipeline"  # the neighbours' fields are not mapped (BSPDE_PEER_HALO=0 / no IPC)
     lay = halo.layout
     if mode == "split" and not (hasattr(ops, "pass_a_range") and lay.nz > 2 * lay.ghost):
         mode = "pipeline"  # no interior range on this slab
@@ -285,9 +302,13 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
     R = pring.shape[0]
     pring[R - 1].zero_()  # p_{-1} = 0, ghost planes included: nothing to exchange at k = 0
     ops.setup(scratch, history, config, has_x0, ring=R)
+    if hasattr(ops, "use_peers"):
+        ops.use_peers(mode == "peer")
     halo(x)
     ops.residual(b, x, r, scratch)
     ops.reduce(scratch, 3, 0)
+    if mode == "peer":
+        halo(r)  # r_0's ghost planes; from here on pass A / pass B store the halos
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
     k = 0
@@ -296,7 +317,9 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
         while active:
             for _ in range(K):
                 p_in, p_out = pring[(k - 1) % R], pring[k % R]
-                if mode == "off":
+                if mode == "peer":
+                    ops.pass_a(x, r, p_in, p_out, ap, scratch)
+                elif mode == "off":
                     halo(r, p_in)
                     ops.pass_a(x, r, p_in, p_out, ap, scratch)
                 elif mode == "pipeline":
@@ -308,7 +331,7 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
                     halo.wait(works + pending_p)
                     ops.pass_a_range(x, r, p_in, p_out, ap, scratch, 0, g, True)
                     ops.pass_a_range(x, r, p_in, p_out, ap, scratch, nz - g, g, True)
-                pending_p = halo.start(p_out) if mode != "off" else []
+                pending_p = halo.start(p_out) if mode not in ("off", "peer") else []
                 ops.reduce(scratch, 1, 1)
                 ops.pass_b(r, ap, scratch)
                 ops.reduce(scratch, 2, 2)
@@ -316,6 +339,8 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
             rep, active = ops.read(scratch)
     finally:
         halo.wait(pending_p)
+        if hasattr(ops, "use_peers"):
+            ops.use_peers(False)
     ops.flush_x(x, pring, scratch)  # the last iteration's x update
     return rep, time.perf_counter() - t0
 
@@ -410,10 +435,57 @@ class DistributedOperator:
             self._work = dict(r=lay.alloc(self.device), pring=lay.alloc_ring(self.device, ring),
                               ap=lay.alloc(self.device), scratch=self.plan().scratch(),
                               history=None)
+            self._peers = self._map_peers(self._work)
         w = self._work
         if w["history"] is None or w["history"].numel() < max_iter + 1:
             w["history"] = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
         return w
+
+    def _map_peers(self, w):
+        """Map the neighbours' p ring and r (CUDA IPC: NVLink peer memory
+        across GPUs, the same device in the one-GPU multi-process test) for
+        the "peer" halo mode.  Every rank must succeed or none uses it."""
+        import torch.distributed as dist
+
+        from . import _native as N
+        from .device import ipc_close, ipc_export, ipc_import
+
+        if self.world == 1 or os.environ.get("BSPDE_PEER_HALO", "1") == "0":
+            return None
+        ring, r = w["pring"], w["r"]
+        try:
+            mine = dict(ring=ipc_export(ring), r=ipc_export(r), stride=int(ring.stride(0)),
+                        nz=self.layout.nz)
+        except Exception:  # noqa: BLE001 - no IPC on this platform: NCCL halos
+            mine = None
+        info = [None] * self.world
+        dist.all_gather_object(info, mine, group=self.group)
+        opened, ok = [], all(v is not None for v in info)
+        nb = {}
+        if ok:
+            try:
+                for side, q in (("lo", self.rank - 1), ("hi", self.rank + 1)):
+                    if 0 <= q < self.world:
+                        pr = ipc_import(*info[q]["ring"])
+                        opened.append(pr)
+                        rr = ipc_import(*info[q]["r"])
+                        opened.append(rr)
+                        nb[side] = (pr, info[q]["stride"], rr, info[q]["nz"])
+            except Exception:  # noqa: BLE001
+                ok = False
+        flags = [None] * self.world
+        dist.all_gather_object(flags, ok, group=self.group)
+        if not all(flags):
+            for ptr in opened:
+                ipc_close(ptr)
+            return None
+        self._peer_maps = opened
+        lo, hi = nb.get("lo"), nb.get("hi")
+        return N.SlabPeers(ring=ring.data_ptr(), r=r.data_ptr(), ring_stride=int(ring.stride(0)),
+                           ring_len=int(ring.shape[0]), lo_nz=lo[3] if lo else 0,
+                           lo_ring=lo[0] if lo else None, lo_ring_stride=lo[1] if lo else 0,
+                           lo_r=lo[2] if lo else None, hi_ring=hi[0] if hi else None,
+                           hi_ring_stride=hi[1] if hi else 0, hi_r=hi[2] if hi else None)
 
     def rhs_buffer(self, max_iter=1000):
         """The heat RHS b shares the CG's Ap field (b is dead once r0 = b - A x0
@@ -423,7 +495,8 @@ class DistributedOperator:
     def pcg_device(self, b_buf, x_buf, config: SolveConfig = None, has_x0=True):
         config = config or SolveConfig()
         w = self._work_buffers(config.max_iter)
-        ops = NativeSlabOps(self.plan(config.precond), self.world, self.group)
+        ops = NativeSlabOps(self.plan(config.precond), self.world, self.group,
+                            peers=getattr(self, "_peers", None))
         rep, wall = distributed_pcg(ops, self.halo, b_buf, x_buf, w["r"],
                                     w["pring"], w["ap"], w["scratch"], config, has_x0,
                                     w["history"] if config.record_history else None)

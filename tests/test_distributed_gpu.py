@@ -4,8 +4,10 @@
 ``NativeSlabOps`` (the sm_100a step-wise kernels with fuse = 0: ranged pass
 A, pass B, the 1-thread finalize) driven by ``distributed_pcg`` -- over the
 gloo backend, whose halo planes and scalar all-gathers are staged through
-host memory (NCCL refuses two ranks on one device).  Every halo-overlap mode
-and both ring lengths; the gathered solution must equal the fused
+host memory (NCCL refuses two ranks on one device), and the "peer" mode
+in which pass A / pass B store the halo planes into the neighbours' fields
+mapped by CUDA IPC (the same device here; NVLink peer memory across GPUs).
+Every halo mode and both ring lengths; the gathered solution must equal the fused
 single-rank solver's bit for bit (same iteration count) and match the oracle
 (counts +-1, coefficients 1e-10 at tol 1e-13).  The ranks' kernels never wait on one another (the exchanges are
 synchronous host copies), so sharing the device is safe.
@@ -74,13 +76,17 @@ def _worker(rank, world, port, ext, p, mode, ring, q):
         xs = op.gather(x)
         # a distributed apply through the same halo path
         t = op.gather(op.apply_device(op.scatter(x0_full), op.layout.alloc(op.device)))
+        peer = op._peers is not None
         if rank == 0:
-            q.put((its, xs, t, int(op._work["pring"].shape[0]), op.layout.nz))
+            q.put((its, xs, t, int(op._work["pring"].shape[0]), op.layout.nz, peer))
     finally:
         dist.destroy_process_group()
 
 
 CASES = [
+    (2, (24, 20, 22), 3, "peer", 2),      # halos stored by pass A / pass B through IPC
+    (3, (24, 20, 22), 3, "peer", 4),
+    (3, (16, 18, 17), 1, "peer", 2),      # p = 1: one ghost plane per side
     (2, (24, 20, 22), 3, "pipeline", 4),
     (3, (24, 20, 22), 3, "split", 4),     # 26 planes: slabs 9 / 9 / 8, interior ranges
     (2, (24, 20, 22), 3, "off", 2),       # two-field ring
@@ -109,8 +115,9 @@ def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
-    its, xs, t, ring_used, nz0 = res
+    its, xs, t, ring_used, nz0, peer = res
     assert ring_used == ring
+    assert peer  # the neighbours' fields were mapped (CUDA IPC on the one device)
     data, step = _system(ext, p)
     b_full, x0_full = _inputs(ext, p)
     # fused single-rank solver and the oracle recurrence on the same inputs:

@@ -61,6 +61,9 @@ int main(void) {{
   F(bspde_stencil_desc, degenerate) F(bspde_mask_desc, degenerate)
   F(bspde_mask_desc, nbrows) F(bspde_mask_desc, cell_tri) F(bspde_mask_desc, fc)
   F(bspde_mask_desc, surface_weight)
+  printf("bspde_slab_peers %zu\\n", sizeof(bspde_slab_peers));
+  F(bspde_slab_peers, ring_len) F(bspde_slab_peers, lo_nz) F(bspde_slab_peers, lo_ring)
+  F(bspde_slab_peers, hi_r)
   return 0;
 }}
 """)
@@ -70,7 +73,7 @@ int main(void) {{
     vals = dict(line.split() for line in out if line.strip())
     structs = {"bspde_plan_desc": N.PlanDesc, "bspde_cg_config": N.CgConfig,
                "bspde_cg_report": N.CgReport, "bspde_stencil_desc": N.StencilDesc,
-               "bspde_mask_desc": N.MaskDesc}
+               "bspde_mask_desc": N.MaskDesc, "bspde_slab_peers": N.SlabPeers}
     for key, v in vals.items():
         if "." in key:
             sname, field = key.split(".")
