@@ -210,12 +210,12 @@ int bspde_cg_finalize(bspde_plan* plan, void* scratch, int kind, void* stream);
 int bspde_cg_finalize_gathered(bspde_plan* plan, void* scratch, const void* gathered,
                                int world, int kind, void* stream);
 /* ---- z-slab peer halos (NVLink peer memory / CUDA IPC) ------------------
- * With peers set, the step-wise pass A also stores p_k of its first / last
- * p owned planes into the lower / upper neighbour's ghost planes of the same
- * ring field (k % R), and pass B stores the new r of those planes into the
- * neighbours' r ghost planes: the compute kernels carry the halo exchange
- * (no separate NCCL transfer per iteration).  The scalar all-gather after
- * each pass orders the peer stores before the neighbour's next read.  The
+ * With peers set, the step-wise pass B stores the new r of its first / last
+ * p owned planes into the lower / upper neighbour's r ghost planes, and the
+ * preceding pass A's p_k of those planes into the neighbours' ghost planes
+ * of the same ring field (k % R): the compute kernels carry the halo
+ * exchange (no separate transfer per iteration).  The scalar all-gather
+ * after pass B orders those stores before the neighbours' next pass A.  The
  * reference analogue is the worker windows' halo (operator.py:61-74). */
 typedef struct {
   const double* ring;        /* this rank's p ring: ring_len fields, ring_stride doubles apart */

@@ -155,12 +155,6 @@ struct SepParams {
   const double* cg_p;
   double* cg_pout;     // CG pass A: p_k at owned points (ping-pong partner of cg_p)
   double* cg_x;        // CG pass A: x += alpha_{k-1} p_{k-1} at owned points (k >= 1)
-  // z-slab peer halos: the neighbours' p_out fields (NVLink peer memory /
-  // CUDA IPC); p_k of the first / last `ghost` owned planes is also stored
-  // into their upper / lower ghost planes (the lower neighbour owns nz_lo planes)
-  double* peer_lo;
-  double* peer_hi;
-  int nz_lo;
   double* partials;
   unsigned* counter;
   CgState* state;
@@ -210,8 +204,15 @@ struct PassBParams {
   unsigned* counter;
   CgState* state;
   int fuse;
-  double* peer_lo;  // z-slab peer halos of r (see SepParams)
+  // z-slab peer halos: the new r and the preceding pass A's p_k of the first /
+  // last `ghost` owned planes are also stored into the lower / upper
+  // neighbour's ghost planes (NVLink peer memory / CUDA IPC; the lower
+  // neighbour owns nz_lo planes)
+  double* peer_lo;
   double* peer_hi;
+  const double* p_src;
+  double* p_lo;
+  double* p_hi;
   int nz_lo;
 };
 
@@ -897,9 +898,6 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     const long long obase =
         (long long)(zo + prm.ghost) * prm.pitch_z + (long long)gy0 * prm.pitch_y + gx;
     const int czo = cls_of(prm.z_off + zo, prm.nz_glob, ewz);
-    // z-slab peer halos: this output plane is one of a neighbour's ghost planes
-    const bool peer_lo_pl = (MODE == M_CGA) && prm.peer_lo != nullptr && zo < prm.ghost;
-    const bool peer_hi_pl = (MODE == M_CGA) && prm.peer_hi != nullptr && zo >= prm.nz - prm.ghost;
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // group sums of this thread's rows (dd_add)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -913,8 +911,6 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           __stcs(prm.out + off, v);
           prm.cg_pout[off] = pr[0][i];  // p_k for pass B (ping-pong partner of p_{k-1})
           g0 = fma(pr[0][i], v, g0);
-          if (peer_lo_pl) prm.peer_lo[off + (long long)prm.nz_lo * prm.pitch_z] = pr[0][i];
-          if (peer_hi_pl) prm.peer_hi[off - (long long)prm.nz * prm.pitch_z] = pr[0][i];
         } else if (MODE == M_MASS) {
           double o = prm.c_mass * v;
           if (prm.aux) o = fma(prm.aux_scale, auxv[i], o);
@@ -936,7 +932,6 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
         }
       }
     }
-    if (peer_lo_pl || peer_hi_pl) __threadfence_system();
     if (MODE == M_CGA || MODE == M_RESID || MODE == M_HRES) dd_add(dsum[0], dsum[3], g0);
     if (MODE == M_RESID || MODE == M_HRES) {
       dd_add(dsum[1], dsum[4], g1);
@@ -1020,7 +1015,6 @@ __device__ __forceinline__ void core_iter(const SepParams& prm, const Smem& sm, 
                                           double inv0, double* op, double* pp, const double* xp,
                                           long long py) {
   using C = Cfg<P, MODE>;
-  static_assert(!(MODE == M_CGA && BSPDE_CORE_CGA), "core_iter: no z-slab peer halo stores");
   constexpr int NW = C::NW, TY = C::TY, HX = C::HX, HY = C::HY, NA = C::NA, NS = C::NS;
   constexpr int PX = C::PX, DX = C::DX, S = 2 * P;
   constexpr bool STIFF = C::STIFF;
@@ -1489,17 +1483,26 @@ __global__ void __launch_bounds__(NTB) cg_pass_b_kernel(const __grid_constant__ 
       dd_add(rz, rzl, __dmul_rn(rn, __dmul_rn(i0, rn)));
       dd_add(rr, rrl, __dmul_rn(rn, rn));
     }
-    // z-slab peer halos: the new r of a boundary row is also a neighbour's ghost row
+    // z-slab peer halos: a boundary row of the new r (and of p_k) is also a
+    // neighbour's ghost row
     const bool plo = prm.peer_lo != nullptr && zl < prm.ghost;
     const bool phi = prm.peer_hi != nullptr && zl >= prm.nz - prm.ghost;
     if (plo || phi) {
       __syncwarp();
-      double* dst = plo ? prm.peer_lo + base + (long long)prm.nz_lo * prm.pitch_z
-                        : prm.peer_hi + base - (long long)prm.nz * prm.pitch_z;
-      for (int xx = lane; xx < nx; xx += 32) dst[xx] = rrw[xx];
-      if (plo && phi) {  // a slab of <= 2 ghost planes feeds both neighbours
-        double* d2 = prm.peer_hi + base - (long long)prm.nz * prm.pitch_z;
-        for (int xx = lane; xx < nx; xx += 32) d2[xx] = rrw[xx];
+      const long long olo = base + (long long)prm.nz_lo * prm.pitch_z;
+      const long long ohi = base - (long long)prm.nz * prm.pitch_z;
+      const double* ps = prm.p_src ? prm.p_src + base : nullptr;
+      for (int xx = lane; xx < nx; xx += 32) {
+        const double rv = rrw[xx];
+        const double pv = ps ? ps[xx] : 0.0;
+        if (plo) {
+          prm.peer_lo[olo + xx] = rv;
+          if (ps && prm.p_lo) prm.p_lo[olo + xx] = pv;
+        }
+        if (phi) {
+          prm.peer_hi[ohi + xx] = rv;
+          if (ps && prm.p_hi) prm.p_hi[ohi + xx] = pv;
+        }
       }
       __threadfence_system();
     }
@@ -1918,6 +1921,9 @@ struct bspde_plan {
   std::map<std::pair<int, int>, Launch> launch_cache;
   bool peers = false;         // z-slab peer halos (bspde_slab_set_peers)
   bspde_slab_peers peer{};
+  const double* peer_p_src = nullptr;  // p_k of the last pass A (its pass B copies the halo)
+  double* peer_p_lo = nullptr;
+  double* peer_p_hi = nullptr;
 };
 
 namespace {
@@ -2160,17 +2166,17 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   sp.cg_p = (mode == M_CGA) ? in1 : nullptr;
   sp.cg_pout = cg_pout;
   sp.cg_x = cg_x;
-  sp.peer_lo = sp.peer_hi = nullptr;
-  sp.nz_lo = 0;
-  if (mode == M_CGA && pl->peers && cg_pout) {
-    // p_out is ring field k % R of this rank: the neighbours' field k % R
+  if (mode == M_CGA && pl->peers) {
+    // z-slab peer halos: p_out is ring field k % R of this rank; the next
+    // pass B stores its boundary planes into the neighbours' field k % R
     const bspde_slab_peers& q = pl->peer;
-    const long long d = cg_pout - q.ring;
+    const long long d = cg_pout ? cg_pout - q.ring : -1;
+    pl->peer_p_src = nullptr;
     if (q.ring_stride > 0 && d >= 0 && d % q.ring_stride == 0 && d / q.ring_stride < q.ring_len) {
       const long long slot = d / q.ring_stride;
-      if (q.lo_ring) sp.peer_lo = q.lo_ring + slot * q.lo_ring_stride;
-      if (q.hi_ring) sp.peer_hi = q.hi_ring + slot * q.hi_ring_stride;
-      sp.nz_lo = q.lo_nz;
+      pl->peer_p_src = cg_pout;
+      pl->peer_p_lo = q.lo_ring ? q.lo_ring + slot * q.lo_ring_stride : nullptr;
+      pl->peer_p_hi = q.hi_ring ? q.hi_ring + slot * q.hi_ring_stride : nullptr;
     }
   }
   if (mode == M_HRES)
@@ -2230,12 +2236,17 @@ int launch_pass_b(bspde_plan* pl, double* x, double* r, const double* pring, con
   bp.counter = scratch_counter(scratch);
   bp.state = scratch_state(scratch);
   bp.fuse = fuse;
-  bp.peer_lo = bp.peer_hi = nullptr;
+  bp.peer_lo = bp.peer_hi = bp.p_lo = bp.p_hi = nullptr;
+  bp.p_src = nullptr;
   bp.nz_lo = 0;
   if (!flush && pl->peers && r && r == pl->peer.r) {
     bp.peer_lo = pl->peer.lo_r;
     bp.peer_hi = pl->peer.hi_r;
     bp.nz_lo = pl->peer.lo_nz;
+    bp.p_src = pl->peer_p_src;
+    bp.p_lo = pl->peer_p_lo;
+    bp.p_hi = pl->peer_p_hi;
+    pl->peer_p_src = nullptr;
   }
   const int ninv = (2 * d.ew[0] + 1) * (2 * d.ew[1] + 1) * (2 * d.ew[2] + 1);
   void* args[1] = {&bp};
@@ -2707,6 +2718,7 @@ int bspde_cg_finalize(bspde_plan* pl, void* scratch, int kind, void* stream) {
 
 int bspde_slab_set_peers(bspde_plan* pl, const bspde_slab_peers* peers) {
   if (int rc = check_plan(pl)) return rc;
+  pl->peer_p_src = nullptr;
   if (!peers) {
     pl->peers = false;
     pl->peer = bspde_slab_peers{};

@@ -212,8 +212,8 @@ class NativeSlabOps:
         self.peer_ready = peers is not None
 
     def use_peers(self, on):
-        """Pass A / pass B store the boundary planes of p_k / r into the
-        neighbours' ghost planes themselves (bspde_slab_set_peers)."""
+        """Pass B stores the boundary planes of r and p_k into the
+        neighbours' ghost planes itself (bspde_slab_set_peers)."""
         self.plan.set_peers(self.peers if on else None)
 
     def reduce(self, scratch, n, kind):
@@ -257,11 +257,12 @@ def _halo_mode(ops, halo):
     """``BSPDE_HALO_OVERLAP``: "peer" (default when the neighbours' fields are
     mapped), "pipeline" (default otherwise), "split" or "off" ("0").
 
-    * peer -- the kernels store the halo planes themselves: pass A writes
-      p_k's first / last p owned planes into the neighbours' ghost planes
-      (NVLink peer memory, mapped by CUDA IPC), pass B the new r's; the
-      scalar all-gather after each pass orders those stores before the
-      neighbour's next pass, so no halo transfer is issued per iteration;
+    * peer -- the kernels store the halo planes themselves: pass B writes
+      the new r and the preceding pass A's p_k of its first / last p owned
+      planes into the neighbours' ghost planes (NVLink peer memory, mapped
+      by CUDA IPC); the scalar all-gather after pass B orders those stores
+      before the neighbours' next pass A, so no halo transfer is issued per
+      iteration;
 
     * pipeline -- p_k's ghost planes travel while the <p,Ap> all-reduce,
       finalize and pass B of the same iteration run (the exchange is posted
@@ -308,7 +309,7 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
     ops.residual(b, x, r, scratch)
     ops.reduce(scratch, 3, 0)
     if mode == "peer":
-        halo(r)  # r_0's ghost planes; from here on pass A / pass B store the halos
+        halo(r)  # r_0's ghost planes; from here on pass B stores the halos
     rep, active = ops.read(scratch)
     K = max(1, int(config.poll_every))
     k = 0

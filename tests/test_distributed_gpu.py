@@ -5,8 +5,8 @@
 A, pass B, the 1-thread finalize) driven by ``distributed_pcg`` -- over the
 gloo backend, whose halo planes and scalar all-gathers are staged through
 host memory (NCCL refuses two ranks on one device), and the "peer" mode
-in which pass A / pass B store the halo planes into the neighbours' fields
-mapped by CUDA IPC (the same device here; NVLink peer memory across GPUs).
+in which pass B stores the halo planes of r and p_k into the neighbours'
+fields mapped by CUDA IPC (the same device here; NVLink peer memory across GPUs).
 Every halo mode and both ring lengths; the gathered solution must equal the fused
 single-rank solver's bit for bit (same iteration count) and match the oracle
 (counts +-1, coefficients 1e-10 at tol 1e-13).  The ranks' kernels never wait on one another (the exchanges are
@@ -84,7 +84,7 @@ def _worker(rank, world, port, ext, p, mode, ring, q):
 
 
 CASES = [
-    (2, (24, 20, 22), 3, "peer", 2),      # halos stored by pass A / pass B through IPC
+    (2, (24, 20, 22), 3, "peer", 2),      # halos stored by pass B through IPC
     (3, (24, 20, 22), 3, "peer", 4),
     (3, (16, 18, 17), 1, "peer", 2),      # p = 1: one ghost plane per side
     (2, (24, 20, 22), 3, "pipeline", 4),
