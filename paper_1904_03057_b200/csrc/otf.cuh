@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(OTF_NT, 1)
                      const double* __restrict__ mfield, const double* __restrict__ c,
                      double* __restrict__ out, const double* __restrict__ aux,
                      const double* __restrict__ diag, double* partials, unsigned* counter,
-                     CgState* st, int precond) {
+                     CgState* st, int precond, int zchunk) {
   using C = OtfCfg<NB>;
   constexpr int A = C::A, B = C::B, CR = C::CR, HX = C::HX, FY = C::FY, FX = C::FX;
   constexpr int TX = OTF_TX, TY = OTF_TY, RPT = OTF_RPT;
@@ -177,8 +177,13 @@ __global__ void __launch_bounds__(OTF_NT, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntab = 6 * S.ncls * C::TABD;
   for (int i = tid; i < ntab; i += OTF_NT) tab[i] = S.tab[i];
+  // item = (x-y tile, z-chunk of zchunk output planes): a chunk streams B - 1
+  // extra field planes to warm up its partial-output ring
   const int tiles_x = (S.nx + TX - 1) / TX;
-  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+  const int tiles = tiles_x * ((S.ny + TY - 1) / TY);
+  const int tile = blockIdx.x % tiles, chunk = blockIdx.x / tiles;
+  const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
+  const int lz0 = chunk * zchunk, lz1 = min(lz0 + zchunk, S.nz);
   const int dz = S.exp_[0] - S.ex[0] - C::MW, dy = S.exp_[1] - S.ex[1] - C::MW,
             dx = S.exp_[2] - S.ex[2] - C::MW;
   const int ewz = S.ew[0], ewy = S.ew[1], ewx = S.ew[2];
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(OTF_NT, 1)
     }
   };
   // ring: planes [fz - dz - (B-1) - NB, fz - dz + NB] at field plane fz
-  const int fz0 = dz, fz1 = S.nz - 1 + dz + B - 1;
+  const int fz0 = lz0 + dz, fz1 = lz1 - 1 + dz + B - 1;
   for (int i = tid; i < CR * C::CPL; i += OTF_NT) ring[i] = 0.0;
   __syncthreads();
   for (int q = fz0 - dz - (B - 1) - NB; q < fz0 - dz + NB; ++q)
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(OTF_NT, 1)
     }
     // ---- output plane lz = fz - dz - (B - 1) is complete ----
     const int lz = fz - dz - (B - 1);
-    if (lz >= 0 && lz < S.nz) {
+    if (lz >= lz0 && lz < lz1) {
       double g0 = 0.0, g1 = 0.0, g2 = 0.0;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -422,9 +427,37 @@ int otf_launch_nb(const bspde_stencil* s, cudaStream_t st, const double* c, doub
   }
   const int tiles = ((s->S.nx + OTF_TX - 1) / OTF_TX) * ((s->S.ny + OTF_TY - 1) / OTF_TY);
   if (tiles > MAXGRID && MODE != 0) return fail(BSPDE_ERR_STATE, "OTF grid exceeds MAXGRID");
-  otf_apply_kernel<NB, MODE><<<tiles, OTF_NT, smem, st>>>(s->S, s->otf_d, s->otf_m, c, out, aux,
-                                                          s->otf_diag, partials, counter, state,
-                                                          precond);
+  // z-chunks: one CTA per (tile, chunk), chosen to minimise waves x (chunk +
+  // B - 1 warm-up planes) -- a small x-y grid (240 x 240: 240 tiles on 148
+  // SMs) would otherwise run 1.6 waves
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int nz = s->S.nz;
+  int zchunk = nz;
+  if (const char* e = getenv("BSPDE_OTF_ZCHUNK")) zchunk = std::max(1, atoi(e));
+  else {
+    double best = 1e300;
+    for (int nc = 1; nc <= nz; ++nc) {
+      const int len = (nz + nc - 1) / nc;
+      const int ncr = (nz + len - 1) / len;
+      if ((long long)tiles * ncr > MAXGRID) break;
+      const long long waves = ((long long)tiles * ncr + nsm - 1) / nsm;
+      const double cost = (double)waves * (len + OtfCfg<NB>::B - 1);
+      if (cost < best * (1.0 - 1e-9)) {
+        best = cost;
+        zchunk = len;
+      }
+    }
+  }
+  const int grid = tiles * ((nz + zchunk - 1) / zchunk);
+  if (grid > MAXGRID && MODE != 0) return fail(BSPDE_ERR_STATE, "OTF grid exceeds MAXGRID");
+  otf_apply_kernel<NB, MODE><<<grid, OTF_NT, smem, st>>>(s->S, s->otf_d, s->otf_m, c, out, aux,
+                                                         s->otf_diag, partials, counter, state,
+                                                         precond, zchunk);
   return BSPDE_OK;
 }
 
