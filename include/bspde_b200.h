@@ -176,7 +176,8 @@ int bspde_cg_residual(bspde_plan* plan, const double* b, const double* x,
 /* p_k = D^-1 r + beta p_{k-1} on the fly (written to p_out at owned
  * points); ap = A p_k; sums = {<p,Ap>}; and, for k >= 1, x += alpha_{k-1}
  * p_{k-1} at the owned points (solver.py:94; p_in = p_{k-1})       kind 1
- * p_in / p_out ping-pong between iterations (they must differ). */
+ * p_in / p_out ping-pong between iterations (they must differ); at k = 0
+ * (beta = 0) p_in only needs finite values (the drivers pass r). */
 int bspde_cg_pass_a(bspde_plan* plan, double* x, const double* r, const double* p_in,
                     double* p_out, double* ap, void* scratch, int fuse,
                     void* stream);

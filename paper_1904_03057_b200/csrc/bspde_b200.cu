@@ -2292,19 +2292,26 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
   int rc = bspde_cg_setup(pl, scratch, history, cfg, stream);
   if (rc) return rc;
   if (!cfg->has_x0) CUDA_TRY(cudaMemsetAsync(x, 0, bytes, st));
-  // p_{-1} = 0 lives in ring field R - 1 (read by iteration 0)
   const int R = cfg->p_ring > 0 ? cfg->p_ring : 2;
   const long long fs = (long long)(pl->d.nz + 2 * pl->p) * pl->pitch_z;
-  CUDA_TRY(cudaMemsetAsync(pring + (R - 1) * fs, 0, bytes, st));
   rc = b ? launch_sep(pl, M_RESID, x, nullptr, r, b, 0.0, 0.0, false, scratch, 1, st)
          : launch_sep(pl, M_HRES, x, nullptr, r, hf, ha, hcm, true, scratch, 1, st);
   if (rc) return rc;
   int32_t active = 0;
   rc = bspde_cg_read_report(pl, scratch, report, &active, stream);
   if (rc) return rc;
-  // iteration k reads ring field (k-1) % R and writes k % R: chunks of a
-  // multiple of R iterations make every replay of the captured graph start
-  // from the same field
+  if (active) {
+    // iteration 0: beta = 0, so p_0 = D^-1 r + 0 * p_in for any finite p_in --
+    // r itself is staged as p_{-1} (no zeroed field, no 6.4 GB memset per
+    // solve at 930^3); it writes ring field 0
+    rc = launch_sep(pl, M_CGA, r, r, ap, nullptr, 0.0, 0.0, false, scratch, 1, st, pring, 0, -1,
+                    0, x);
+    if (rc == BSPDE_OK) rc = launch_pass_b(pl, nullptr, r, nullptr, ap, scratch, 1, st);
+    if (rc) return rc;
+  }
+  // iteration k >= 1 reads ring field (k-1) % R and writes k % R: chunks of a
+  // multiple of R iterations (k = 1 .. K, K + 1 .. 2K, ...) make every replay
+  // of the captured graph start from the same field
   int K = cfg->poll_every > 0 ? cfg->poll_every : 8;
   K = ((K + R - 1) / R) * R;
   while (active) {
@@ -2315,7 +2322,7 @@ int pcg_solve_on(bspde_plan* pl, const double* b, double* x, double* r, double* 
       cudaGraph_t graph = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       int crc = BSPDE_OK;
-      for (int k = 0; k < K && crc == BSPDE_OK; ++k) {
+      for (int k = 1; k <= K && crc == BSPDE_OK; ++k) {
         crc = launch_sep(pl, M_CGA, r, pring + ((k + R - 1) % R) * fs, ap, nullptr, 0.0,
                          0.0, false, scratch, 1, st, pring + (k % R) * fs, 0, -1, 0, x);
         if (crc == BSPDE_OK) crc = launch_pass_b(pl, nullptr, r, nullptr, ap, scratch, 1, st);

@@ -301,7 +301,6 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
     if not has_x0:
         x.zero_()
     R = pring.shape[0]
-    pring[R - 1].zero_()  # p_{-1} = 0, ghost planes included: nothing to exchange at k = 0
     ops.setup(scratch, history, config, has_x0, ring=R)
     if hasattr(ops, "use_peers"):
         ops.use_peers(mode == "peer")
@@ -317,11 +316,13 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
     try:
         while active:
             for _ in range(K):
-                p_in, p_out = pring[(k - 1) % R], pring[k % R]
+                # iteration 0 has beta = 0: r itself stands in for p_{-1}
+                # (p_0 = D^-1 r + 0 * r; no zeroed field, nothing extra to exchange)
+                p_in, p_out = (r if k == 0 else pring[(k - 1) % R]), pring[k % R]
                 if mode == "peer":
                     ops.pass_a(x, r, p_in, p_out, ap, scratch)
                 elif mode == "off":
-                    halo(r, p_in)
+                    halo(r) if k == 0 else halo(r, p_in)
                     ops.pass_a(x, r, p_in, p_out, ap, scratch)
                 elif mode == "pipeline":
                     halo.wait(halo.start(r) + pending_p)
