@@ -61,6 +61,11 @@ constexpr int MAXTAP = 2 * MAXP + 1;
 #ifndef BSPDE_W_LOWP
 #define BSPDE_W_LOWP 16
 #endif
+// fused heat residual: F's owned tile of the output plane is staged by TMA
+// with the input plane instead of prefetched into registers (Cfg::AS)
+#ifndef BSPDE_AUX_TMA
+#define BSPDE_AUX_TMA 1
+#endif
 // Per (degree, mode): CG pass A at p = 3 carries the p ring and the x update
 // and runs 12 warps with 168 registers (64 x 24 tiles; 16 warps spill at the
 // 128-register cap); the other p <= 3 kernels run 16 warps (64 x 32 tiles)
@@ -111,9 +116,13 @@ struct Cfg {
   static constexpr int XARR = HY * TX;                       // doubles per X array
   static constexpr int TAB = 6 * NC * R;                     // doubles
   static constexpr int INV = INVD ? NC * NC * NC : 0;
-  static constexpr size_t smem_bytes() {
-    return (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 8 + 2) + 8 * NS;
-  }
+  static constexpr int AST = TX * TY;  // doubles per staged aux tile
+  static constexpr size_t BASE_BYTES =
+      (size_t)8 * (NS * NA * ARR_D + 2 * 2 * XARR + TAB + INV + NW * 8 + 2) + 8 * NS;
+  static constexpr bool AS = (MODE == M_HRES) && BSPDE_AUX_TMA &&
+                             BASE_BYTES + (size_t)8 * NS * AST <= 227 * 1024;
+  static constexpr int AS_D = AS ? NS * AST : 0;
+  static constexpr size_t smem_bytes() { return BASE_BYTES + (size_t)8 * AS_D; }
 };
 
 // Search directions live in a ring of R <= kPRing fields (R = CgState::ring,
@@ -574,6 +583,7 @@ template <int P, int MODE>
 struct Producer {
   int item, j;
   uint32_t flat;
+  const CUtensorMap* tma;  // Cfg::AS: the aux (F) map, nullptr: no aux
   __device__ __forceinline__ void issue(const SepParams& prm, const CUtensorMap* tm0,
                                         const CUtensorMap* tm1, double* s_stage,
                                         uint64_t* s_full) {
@@ -584,10 +594,15 @@ struct Producer {
     const int nin = g.zc1 - g.zc0 + 2 * P;
     const int s = flat % C::NS;
     const int zb = g.zc0 - P + j + prm.ghost;
-    mbar_expect_tx(&s_full[s], C::NA * C::HX * C::HY * 8);
+    // Cfg::AS: the aux tile of output plane zc0 - 2P + j rides with input plane j
+    const bool al = C::AS && tma != nullptr && j >= 2 * P;
+    mbar_expect_tx(&s_full[s], C::NA * C::HX * C::HY * 8 + (al ? C::AST * 8 : 0));
     tma_load_3d(s_stage + (s * C::NA + 0) * C::ARR_D, tm0, g.x0 - C::PX, g.y0 - P, zb, &s_full[s]);
     if (C::NA == 2)
       tma_load_3d(s_stage + (s * C::NA + 1) * C::ARR_D, tm1, g.x0 - C::PX, g.y0 - P, zb,
+                  &s_full[s]);
+    if (al)
+      tma_load_3d(s_stage + C::NS * C::NA * C::ARR_D + s * C::AST, tma, g.x0, g.y0, zb - P,
                   &s_full[s]);
     ++flat;
     if (++j == nin) {
@@ -919,7 +934,13 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
           double bb = auxv[i];
           if (MODE == M_HRES) {
             bb = prm.rhs_cm * om[i];
-            if (prm.aux) bb = fma(prm.aux_scale, auxv[i], bb);
+            if (prm.aux) {
+              const double fv =
+                  C::AS ? sm.stage[NS * NA * C::ARR_D + (f % NS) * C::AST + (rg * RPT + i) * TX +
+                                   cxl]
+                        : auxv[i];
+              bb = fma(prm.aux_scale, fv, bb);
+            }
           }
           const double r = bb - v;
           __stcs(prm.out + off, r);
@@ -1264,7 +1285,8 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
       double auxv[RPT];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) auxv[i] = 0.0;
-      if ((MODE == M_RESID || ((MODE == M_MASS || MODE == M_HRES) && prm.aux != nullptr)) &&
+      if ((MODE == M_RESID ||
+           ((MODE == M_MASS || (MODE == M_HRES && !Cfg<P, MODE>::AS)) && prm.aux != nullptr)) &&
           j >= 2 * P) {
         const int zo = g.zc0 - 2 * P + j;
         const long long base = (long long)(zo + prm.ghost) * prm.pitch_z + gx;
@@ -1313,7 +1335,7 @@ __device__ __forceinline__ void run_item(const SepParams& prm, const CUtensorMap
 template <int P, int MODE>
 __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
     sep_kernel(const __grid_constant__ SepParams prm, const __grid_constant__ CUtensorMap tm0,
-               const __grid_constant__ CUtensorMap tm1) {
+               const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
   using C = Cfg<P, MODE>;
   [[maybe_unused]] constexpr int NW = C::NW, NT = C::NT, TY = C::TY;
   constexpr int NS = C::NS;
@@ -1327,7 +1349,7 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
   extern __shared__ __align__(1024) double smem[];
   Smem sm;
   sm.stage = smem;
-  sm.X = sm.stage + NS * C::NA * C::ARR_D;
+  sm.X = sm.stage + NS * C::NA * C::ARR_D + C::AS_D;
   sm.tab = sm.X + 2 * 2 * C::XARR;
   sm.invd = sm.tab + C::TAB;
   double* s_red = sm.invd + C::INV;
@@ -1355,7 +1377,8 @@ __global__ void __launch_bounds__(Geo<P, MODE>::NT, 1)
   const double xalpha = (MODE == M_CGA) ? ld_vol(&prm.state->alpha) : 0.0;
   const bool xok = k_it >= 1 && ld_vol(&prm.state->x_done) < k_it;
   double dsum[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // hi[3], lo[3]
-  Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u};
+  Producer<P, MODE> prod{(int)blockIdx.x, 0, 0u,
+                         (C::AS && prm.aux != nullptr) ? &tm2 : nullptr};
   if (tid == kProdThread<P, MODE>) {
     for (int s = 0; s < NS; ++s) prod.issue(prm, &tm0, &tm1, sm.stage, sm.full);
   }
@@ -1973,6 +1996,16 @@ KernelInfo kernel_for(int p, int mode) {
 }
 #endif
 
+bool kAsOf(int p) {
+  switch (p) {
+    case 1: return Cfg<1, M_HRES>::AS;
+    case 2: return Cfg<2, M_HRES>::AS;
+    case 3: return Cfg<3, M_HRES>::AS;
+    case 4: return Cfg<4, M_HRES>::AS;
+    default: return Cfg<5, M_HRES>::AS;
+  }
+}
+
 // Choose the z-chunking.  Items are dealt round-robin (item i -> CTA
 // i % grid, see item_geom), so the kernel time is the largest per-CTA sum of
 // streamed planes (chunk + 2p warm-up), with edge tiles weighted by their
@@ -2055,7 +2088,8 @@ Launch plan_launch(const bspde_plan* pl, const KernelInfo& ki, int nz, int mode)
   return best;
 }
 
-int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base, int mode) {
+int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base, int mode,
+             bool owned_box = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(BSPDE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int p = pl->p;
@@ -2064,6 +2098,10 @@ int make_map(CUtensorMap* m, const bspde_plan* pl, const double* base, int mode)
   cuuint64_t strides[2] = {(cuuint64_t)(pl->d.pitch_y * 8), (cuuint64_t)(pl->pitch_z * 8)};
   const int px = p + (p & 1);
   cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * px), (cuuint32_t)(tile_h_of(p, mode) + 2 * p), 1u};
+  if (owned_box) {  // the tile itself (Cfg::AS)
+    box[0] = TX;
+    box[1] = (cuuint32_t)tile_h_of(p, mode);
+  }
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -2202,7 +2240,12 @@ int launch_sep(bspde_plan* pl, int mode, const double* in0, const double* in1, d
   } else {
     m1 = m0;
   }
-  void* args[3] = {&sp, &m0, &m1};
+  CUtensorMap m2 = m0;
+  if (mode == M_HRES && aux && kAsOf(pl->p)) {
+    rc = make_map(&m2, pl, aux, mode, true);
+    if (rc) return rc;
+  }
+  void* args[4] = {&sp, &m0, &m1, &m2};
   CUDA_TRY(cudaLaunchKernel(ki.fn, dim3(ln.grid), dim3(ki.nt), args, ki.smem, st));
   pl->launches++;
   return BSPDE_OK;
