@@ -234,6 +234,10 @@ class NativeSlabOps:
     def residual(self, b, x, r, scratch):
         self.plan.cg_residual(b, x, r, scratch, 0)
 
+    def heat_residual(self, u, F, cm, a, r, scratch):
+        """r0 = (cm M u + a F) - A u and the three initial sums, b never formed."""
+        self.plan.heat_residual(u, F, cm, a, r, scratch, 0)
+
     def pass_a(self, x, r, p_in, p_out, ap, scratch):
         self.plan.cg_pass_a(x, r, p_in, p_out, ap, scratch, 0)
 
@@ -290,7 +294,7 @@ def _halo_mode(ops, halo):
 
 
 def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
-                    has_x0=True, history=None):
+                    has_x0=True, history=None, heat=None):
     """Jacobi-PCG over z-slabs (same recurrence and stop rule as solver.pcg);
     ``pring`` holds the ring of search directions (leading axis).  Iteration
     k needs the ghost planes of r_k and p_{k-1}; how their exchange overlaps
@@ -305,7 +309,11 @@ def distributed_pcg(ops, halo, b, x, r, pring, ap, scratch, config: SolveConfig,
     if hasattr(ops, "use_peers"):
         ops.use_peers(mode == "peer")
     halo(x)
-    ops.residual(b, x, r, scratch)
+    if heat is not None:  # heat step: b = cm M u + a F fused into the first residual
+        F, cm, a = heat
+        ops.heat_residual(x, F, cm, a, r, scratch)
+    else:
+        ops.residual(b, x, r, scratch)
     ops.reduce(scratch, 3, 0)
     if mode == "peer":
         halo(r)  # r_0's ghost planes; from here on pass B stores the halos
@@ -502,6 +510,20 @@ class DistributedOperator:
         rep, wall = distributed_pcg(ops, self.halo, b_buf, x_buf, w["r"],
                                     w["pring"], w["ap"], w["scratch"], config, has_x0,
                                     w["history"] if config.record_history else None)
+        return report_from(rep, config, wall, w["history"])
+
+    def heat_step_device(self, u_buf, F_buf, dt, config: SolveConfig = None):
+        """One implicit-Euler step in place on this rank's slab, x0 = u: the
+        right-hand side vol M u + dt F is fused into the first residual
+        (``bspde_heat_residual``), as in the single-GPU ``bspde_heat_step``."""
+        config = config or SolveConfig()
+        w = self._work_buffers(config.max_iter)
+        ops = NativeSlabOps(self.plan(config.precond), self.world, self.group,
+                            peers=getattr(self, "_peers", None))
+        rep, wall = distributed_pcg(ops, self.halo, None, u_buf, w["r"], w["pring"], w["ap"],
+                                    w["scratch"], config, True,
+                                    w["history"] if config.record_history else None,
+                                    heat=(F_buf, self.data.vol, dt))
         return report_from(rep, config, wall, w["history"])
 
     def pcg_host(self, rhs, config, x0=None):

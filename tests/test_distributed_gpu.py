@@ -76,9 +76,15 @@ def _worker(rank, world, port, ext, p, mode, ring, q):
         xs = op.gather(x)
         # a distributed apply through the same halo path
         t = op.gather(op.apply_device(op.scatter(x0_full), op.layout.alloc(op.device)))
+        # one heat step (RHS fused into the first residual), u0 = x0, F = b
+        u = op.scatter(x0_full)
+        hrep = op.heat_step_device(u, op.scatter(b_full), 0.01,
+                                   SolveConfig(tol=1e-12, max_iter=2000, poll_every=3))
+        hs = op.gather(u)
         peer = op._peers is not None
         if rank == 0:
-            q.put((its, xs, t, int(op._work["pring"].shape[0]), op.layout.nz, peer))
+            q.put((its, xs, t, int(op._work["pring"].shape[0]), op.layout.nz, peer,
+                   hrep.iterations, hs))
     finally:
         dist.destroy_process_group()
 
@@ -115,7 +121,7 @@ def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
-    its, xs, t, ring_used, nz0, peer = res
+    its, xs, t, ring_used, nz0, peer, h_its, hs = res
     assert ring_used == ring
     assert peer  # the neighbours' fields were mapped (CUDA IPC on the one device)
     data, step = _system(ext, p)
@@ -140,3 +146,16 @@ def test_native_zslab_multiprocess(cuda_device, world, ext, p, mode, ring):
     assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-10
     want = ora.apply(x0_full)
     assert np.abs(t - want).max() / np.abs(want).max() < 1e-13
+    # the distributed heat step equals the single-GPU bspde_heat_step bit for bit
+    import torch
+
+    from paper_1904_03057_b200.heat import heat_step_device
+
+    lay = op.layout
+    u1 = lay.upload(x0_full, op.device)
+    F1 = lay.upload(b_full, op.device)
+    rep1 = heat_step_device(op, u1, F1, 0.01, SolveConfig(tol=1e-12, max_iter=2000))
+    assert h_its == rep1.iterations
+    assert np.array_equal(hs, lay.download(u1))
+    del u1, F1
+    torch.cuda.empty_cache()
