@@ -895,15 +895,23 @@ __device__ __forceinline__ void plane_back(const SepParams& prm, const Smem& sm,
     if (MODE == M_HRES) {
       // pure mass ring (Mz(x)My(x)Mx) u: the M_MASS kernel's z pass on wm
       const double* tzm = sm.tab + ((0 * 2 + 0) * NC + cz) * R;
-      const bool fz = cz == ewz && prm.zfast;
+      // two plane-uniform branches (interior taps / class table), like the
+      // main ring: a per-FMA select made both operands live (LDS + SEL per
+      // tap; 16% of the kernel's instructions)
+      auto mass_ring = [&](auto tap) {
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const double a = wm[i];
-        om[i] = fma(fz ? T.M(0) : tzm[0], a, accm[0][i]);
+        for (int i = 0; i < RPT; ++i) {
+          const double a = wm[i];
+          om[i] = fma(tap(0), a, accm[0][i]);
 #pragma unroll
-        for (int k = 0; k < S - 1; ++k) accm[k][i] = fma(fz ? T.M(k + 1) : tzm[k + 1], a, accm[k + 1][i]);
-        accm[S - 1][i] = (fz ? T.M(S) : tzm[S]) * a;
-      }
+          for (int k = 0; k < S - 1; ++k) accm[k][i] = fma(tap(k + 1), a, accm[k + 1][i]);
+          accm[S - 1][i] = tap(S) * a;
+        }
+      };
+      if (cz == ewz && prm.zfast)
+        mass_ring([&](int k) { return T.M(k); });
+      else
+        mass_ring([&](int k) { return tzm[k]; });
     }
   }
 
